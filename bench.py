@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- SRM hot loop throughput on B200 (BASELINE.json metric).
+
+A step is one SRM round (engine.hpp:227-234: grid rebuild -> migrate with n_l attempts
+-> overlap-count/max-penetration reduction) over every particle of the workload, at
+fixed size in the steady-state window (SURVEY.md §8d protocol (i)).  Default workload:
+BASELINE.json configs[3] ("cfg4"), 10^7 monodisperse spheres in the periodic unit
+cube, f_target 0.30, c_m = 0.05 r_target; start = seeded RSA at f0 = 0.1 (the paper's
+protocol; host rsa_place) grown on the device by srm_generate to 0.98 f_target.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config cfg4]
+
+N > 1 runs one independent replica per GPU (replicas only: the path does not shard,
+DESIGN.md §6); value = all particles of all ranks x K / max-over-ranks device time.
+--impl reference times the reference's own CPU engine (oracle/_ref, built from the
+reference sources) on the box's host cores: one replica per hardware thread
+(srmgen --ensemble semantics), each step one round per replica on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-updates/sec per SRM iteration (1 B200) and % of HBM roofline"
+UNIT = "particle-updates/s"
+
+# BASELINE.json configs (SURVEY.md §8d synthetic inputs)
+CONFIGS = {
+    "cfg1": dict(desc="2D monodisperse disks N=1e4, unit square, f_target 0.50, c_m=0.1 r_t",
+                 dim=2, n=10_000, f_target=0.50, cm_rel=0.10, f0=0.1),
+    "cfg2": dict(desc="3D monodisperse spheres N=1e6, unit cube, f_target 0.40, c_m=0.1 r_t",
+                 dim=3, n=1_000_000, f_target=0.40, cm_rel=0.10, f0=0.1),
+    "cfg4": dict(desc="3D monodisperse spheres N=1e7, unit cube, f_target 0.30, c_m=0.05 r_t",
+                 dim=3, n=10_000_000, f_target=0.30, cm_rel=0.05, f0=0.1),
+}
+F_WINDOW = 0.98   # steady-state window at 0.98 f_target
+N_K = 10          # rounds per iteration / shake sweeps (srmgen.cpp:407-410)
+N_L = 10          # attempts per particle per round
+C_W = 0.02        # SrmParams default swelling rate (engine.hpp:23)
+SAMPLE_N = 100_000  # CPU sample size (same density, radius and c_m as the workload)
+BYTES_STEP = {2: 40, 3: 56}  # algorithmic HBM bytes per particle-update, migrate step (§8d)
+
+
+def unit_measure(dim):
+    return math.pi if dim == 2 else 4.0 / 3.0 * math.pi
+
+
+def radius_for(f, n, dim, L=1.0):
+    return (f * L ** dim / (n * unit_measure(dim))) ** (1.0 / dim)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- distributed plumbing ------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def max_over_ranks(pg, v):
+    if pg is None:
+        return v
+    import torch
+    dev = "cuda" if torch.cuda.is_available() and pg.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---- clocks ------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- reference CPU engine (oracle/_ref) ------------------------------------------------
+def ref_lib():
+    path = os.path.join(ROOT, "oracle", "_ref", "libsrm_ref.so")
+    L = C.CDLL(path)
+    vp = C.c_void_p
+    L.ref_rsa_place.restype = C.c_int
+    L.ref_rsa_place.argtypes = [C.c_int, vp, C.c_int64, vp, C.c_int64, C.c_uint64, vp, vp, vp]
+    L.ref_generate.restype = C.c_int
+    L.ref_generate.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, C.c_double, C.c_double, C.c_int,
+                               C.c_int, C.c_double, C.c_int64, C.c_uint64, C.c_int, vp, vp, vp]
+    L.ref_bench_rounds.restype = C.c_double
+    L.ref_bench_rounds.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, C.c_double, C.c_int, C.c_int,
+                                   C.c_uint64, C.c_int, vp]
+    return L
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def ref_sample_state(cfg, seed):
+    """SAMPLE_N spheres at the workload's number density, radius and c_m, prepared by
+    the reference itself: rsa_place at f0, then srm_generate to the window."""
+    L = ref_lib()
+    dim, n = cfg["dim"], SAMPLE_N
+    box = (n / cfg["n"]) ** (1.0 / dim)
+    Lb = np.full(dim, box)
+    r_t = radius_for(cfg["f_target"], cfg["n"], dim)
+    r0 = radius_for(cfg["f0"], cfg["n"], dim)
+    radii = np.full(n, r0)
+    pos = np.zeros((n, dim))
+    ids = np.zeros(n, np.int32)
+    placed = np.zeros(1, np.int64)
+    st = L.ref_rsa_place(dim, _p(Lb), n, _p(radii), 10000, seed, _p(pos), _p(ids), _p(placed))
+    assert st == 0, "reference rsa_place failed"
+    it = np.zeros(1, np.int64)
+    f = np.zeros(1)
+    acc = np.zeros(1, np.int64)
+    c_m = cfg["cm_rel"] * r_t
+    st = L.ref_generate(dim, _p(Lb), n, _p(pos), _p(radii), _p(ids), C_W, c_m, N_K, N_L,
+                        F_WINDOW * cfg["f_target"], 100000, seed + 1, 16, _p(it), _p(f), _p(acc))
+    assert st == 0, "reference srm_generate failed"
+    return L, Lb, pos, radii, ids, c_m
+
+
+def ref_rounds(L, Lb, pos, radii, ids, c_m, rounds, threads, seed):
+    acc = np.zeros(1, np.int64)
+    secs = L.ref_bench_rounds(len(Lb), _p(Lb), len(radii), _p(pos), _p(radii), _p(ids), c_m, N_L,
+                              rounds, seed, threads, _p(acc))
+    return secs
+
+
+def run_reference(args, cfg, world, rank, pg):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    seed = 20260101
+    t0 = time.time()
+    L, Lb, pos, radii, ids, c_m = ref_sample_state(cfg, seed)
+    prep = time.time() - t0
+    if args.warmup > 0:
+        ref_rounds(L, Lb, pos, radii, ids, c_m, args.warmup, threads, seed + 7)
+    secs = ref_rounds(L, Lb, pos, radii, ids, c_m, args.steps, threads, seed + 9)
+    value = threads * SAMPLE_N * args.steps / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded reference rsa_place at f0 + reference srm_generate to 0.98 f_target)",
+        "config": {"workload": args.config + ": " + cfg["desc"], "n_workload": cfg["n"],
+                   "n_sample_per_replica": SAMPLE_N, "replicas": threads, "n_l": N_L,
+                   "c_m": c_m, "step": "one SRM round (build_shape_grid -> migrate -> shape_any_collision) per replica"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{threads} replicas x {SAMPLE_N} spheres (workload density/radius/c_m), "
+                                   f"{args.steps} rounds each; state prep {prep:.1f}s untimed"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- B200 arm ------------------------------------------------------------------------------
+def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
+    dim = cfg["dim"]
+    n = n or cfg["n"]
+    Lb = [box] * dim
+    r_t = radius_for(cfg["f_target"], cfg["n"], dim)
+    r0 = radius_for(cfg["f0"], cfg["n"], dim)
+    c_m = cfg["cm_rel"] * r_t
+    t0 = time.time()
+    pos, ids = srm.rsa_place(np.full(n, r0), Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
+    t_rsa = time.time() - t0
+    ctx = srm.Context(Lb, n, device)
+    ctx.upload(pos, np.full(n, r0), ids)
+    t0 = time.time()
+    params = srm.SrmParams(c_w=C_W, c_m=c_m, n_k=N_K, n_l=N_L, f_target=F_WINDOW * cfg["f_target"],
+                           max_iterations=100000, seed=seed + 1, reorder_period=16)
+    out = ctx.generate(params)
+    t_gen = time.time() - t0
+    info = {"rsa_s": round(t_rsa, 2), "generate_s": round(t_gen, 3), "generate_iterations": out.iteration_count,
+            "generate_rounds": out.rounds, "generate_shake_rounds": out.shake_rounds,
+            "f_window": out.volume_fraction}
+    return ctx, c_m, info
+
+
+def run_b200(args, cfg, world, rank, local, pg):
+    import paper_2605_18254_b200 as srm
+    dim, n = cfg["dim"], cfg["n"]
+    seed = srm.mix_seed(20260101, rank)
+    ctx, c_m, prep = gpu_state(srm, cfg, seed, local)
+    max_r = ctx.max_bounding_radius()
+    cs = 2.5 * max_r + c_m
+    key = srm.mix_seed(seed, 99)
+
+    # warm-up rounds, then exactly K timed rounds bracketed by barrier + sync
+    if args.warmup:
+        ctx.rounds(cs, c_m, N_L, key, 0, 1, args.warmup)
+    ctx.sync()
+    barrier(pg)
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = ctx.launch_count()
+    ctx.stopwatch_start()
+    st = ctx.rounds(cs, c_m, N_L, key, 1000, 1, args.steps)
+    ms = ctx.stopwatch_stop()
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    barrier(pg)
+    ms_max = max_over_ranks(pg, ms)
+    value = world * n * args.steps / (ms_max * 1e-3)
+
+    # per-kernel-family split (separate pass: the events sit between kernels)
+    ctx.timing_enable(True)
+    ctx.rounds(cs, c_m, N_L, key, 2000, 1, args.steps)
+    fam_ms, fam_calls = ctx.timing_get()
+    ctx.timing_enable(False)
+    per_round = [v / args.steps for v in fam_ms]
+    t_mig = per_round[1] + per_round[2]
+    peak, peak_kind = peaks()
+    algo = n * BYTES_STEP[dim]
+    achieved = algo / (t_mig * 1e-3) / 1e9 if t_mig > 0 else 0.0
+
+    # e2e through the C ABI with host buffers: H2D of the state, n_k rounds (one
+    # iteration's worth, like shake()), D2H of the state + the round statistics
+    import torch
+    pos_h = torch.empty((n, dim), dtype=torch.float64, pin_memory=True).numpy()
+    r_h = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    id_h = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+    ctx.download(pos_h, r_h, id_h)
+    e2e_steps = max(2, min(args.steps, 5))
+    ctx.upload(pos_h, r_h, id_h)
+    ctx.rounds(cs, c_m, N_L, key, 3000, 1, N_K)
+    ctx.download(pos_h, r_h, id_h)
+    barrier(pg)
+    ctx.stopwatch_start()
+    for s in range(e2e_steps):
+        ctx.upload(pos_h, r_h, id_h)
+        ctx.rounds(cs, c_m, N_L, key, 4000 + s * N_K, 1, N_K)
+        ctx.download(pos_h, r_h, id_h)
+    e2e_ms = max_over_ranks(pg, ctx.stopwatch_stop()) / e2e_steps
+    bytes_io = n * (8 * dim + 8 + 4)
+    e2e_value = world * n * N_K / (e2e_ms * 1e-3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, c_m)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded rsa_place at f0=0.1, grown on device by srm_generate to 0.98 f_target)",
+            "config": {"workload": args.config + ": " + cfg["desc"], "n": n, "dim": dim,
+                       "f_window": prep["f_window"], "c_m": c_m, "n_l": N_L, "cell_size": cs,
+                       "parallelism": f"replicas x{world}", "step": "one SRM round: grid rebuild + migrate (n_l attempts) + overlap reduction",
+                       "l2": f"inputs larger than L2 (state {n * (8 * dim + 16) / 1e6:.0f} MB)",
+                       "prep": prep},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "migrate step (k_phase0 + k_phase, n_l attempts) per round",
+                         "algorithmic_bytes_per_update": BYTES_STEP[dim], "peak_kind": peak_kind},
+            "phase_ms_per_round": {"grid_rebuild": per_round[0], "migrate_phase0": per_round[1],
+                                   "migrate_phases_ge1": per_round[2], "reduction": per_round[3]},
+            "last_round": {"overlap_pairs": st.overlap_pairs, "movers": st.movers,
+                           "max_penetration": st.max_penetration},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_io,
+                    "d2h_bytes_per_step": bytes_io, "rounds_per_step": N_K,
+                    "api": "srm_b200_upload + srm_b200_rounds(n_k) + srm_b200_download"},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def cpu_baseline(cfg, c_m):
+    """oracle/_ref (the reference engine) on 1 host core, bounded sample ~10-20 s."""
+    try:
+        L, Lb, pos, radii, ids, c_m_s = ref_sample_state(cfg, 777)
+        t1 = ref_rounds(L, Lb, pos, radii, ids, c_m_s, 2, 1, 5) / 2
+        rounds = int(max(3, min(200, 12.0 / max(t1, 1e-6))))
+        secs = ref_rounds(L, Lb, pos, radii, ids, c_m_s, rounds, 1, 6)
+        return {"value": SAMPLE_N * rounds / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"{SAMPLE_N} spheres at the workload's density/radius/c_m, {rounds} rounds "
+                          f"(build_shape_grid -> migrate -> shape_any_collision), 1 thread"}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    cfg = CONFIGS[args.config]
+    world, rank, local, pg = dist_setup()
+    try:
+        if args.impl == "reference":
+            return run_reference(args, cfg, world, rank, pg)
+        return run_b200(args, cfg, world, rank, local, pg)
+    finally:
+        if pg is not None:
+            try:
+                pg.destroy_process_group()
+            except Exception:
+                pass
+
+
+if __name__ == "__main__":
+    sys.exit(main())

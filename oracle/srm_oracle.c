@@ -1,0 +1,447 @@
+/*
+ * srm_oracle.c -- CPU restatement of the SRM hot loop.  TEST INFRASTRUCTURE ONLY:
+ * the product never loads this file's library.  See srm_oracle.h for scope and
+ * DESIGN.md §3 for the parallel round semantics restated here.
+ *
+ * Compile with -ffp-contract=off -fno-fast-math: every double operation below is a
+ * single correctly rounded IEEE operation in the order written, which is the order
+ * of the reference's expressions cited next to each function.
+ */
+#include "srm_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------ */
+/* geometry.hpp:107-114  PeriodicBox::wrap -- two sequential conditional shifts.   */
+void orc_wrap(int dim, const double* L, double* p) {
+    for (int a = 0; a < dim; ++a) {
+        if (p[a] < 0.0) p[a] += L[a];
+        if (p[a] >= L[a]) p[a] -= L[a];
+    }
+}
+
+/* geometry.hpp:117-129  min_image (single conditional shift per axis) + ordered
+ * norm2 (geometry.hpp:44-49: s = 0; s += v0*v0; s += v1*v1; ...).                 */
+double orc_min_image_dist2(int dim, const double* L, const double* a, const double* b) {
+    double s = 0.0;
+    for (int k = 0; k < dim; ++k) {
+        double d = a[k] - b[k];
+        const double half = 0.5 * L[k];
+        if (d > half) d -= L[k];
+        if (d < -half) d += L[k];
+        s += d * d;
+    }
+    return s;
+}
+
+/* shape.hpp:508-511 SphereShape::overlap: contact counts as overlap. */
+static int sphere_overlap(int dim, const double* L, const double* a, double ra, const double* b,
+                          double rb) {
+    const double rr = ra + rb;
+    return orc_min_image_dist2(dim, L, a, b) <= rr * rr;
+}
+
+/* ------------------------------------------------------------------------------ */
+/* cell_grid.hpp:297-309 CellGrid(box, cell_size): n = max(3, (int)floor(L/cs)),
+ * edge = L/n.                                                                      */
+int orc_grid_dims(int dim, const double* L, double cell_size, int32_t* dims, double* edge) {
+    if (!(cell_size > 0.0)) return -1;
+    for (int a = 0; a < dim; ++a) {
+        int n = (int)floor(L[a] / cell_size);
+        if (n < 3) n = 3;
+        dims[a] = n;
+        edge[a] = L[a] / n;
+    }
+    return 0;
+}
+
+/* cell_grid.hpp:319-328: i = (int)floor(p/edge); i %= n; if (i < 0) i += n. */
+void orc_cell_coords(int dim, const int32_t* dims, const double* edge, const double* p,
+                     int32_t* c) {
+    for (int a = 0; a < dim; ++a) {
+        int i = (int)floor(p[a] / edge[a]);
+        i %= dims[a];
+        if (i < 0) i += dims[a];
+        c[a] = i;
+    }
+}
+
+/* cell_grid.hpp:331-336 row-major, x fastest. */
+uint64_t orc_cell_of(int dim, const int32_t* dims, const double* edge, const double* p) {
+    int32_t c[3];
+    orc_cell_coords(dim, dims, edge, p, c);
+    uint64_t idx = 0;
+    for (int a = dim - 1; a >= 0; --a) idx = idx * (uint64_t)dims[a] + (uint64_t)c[a];
+    return idx;
+}
+
+void orc_keys(int dim, const int32_t* dims, const double* edge, int64_t n, const double* pos,
+              uint32_t* keys) {
+    for (int64_t i = 0; i < n; ++i) keys[i] = (uint32_t)orc_cell_of(dim, dims, edge, pos + i * dim);
+}
+
+/* engine.hpp:151-163: counting sort by cell, stable in storage order.  Here the
+ * tie-break is the slot (= storage index in the reference), so the result equals
+ * reorder_by_locality's permutation whenever slot[i] == i.                          */
+void orc_sort_by_cell(int64_t n, const uint32_t* keys, const int32_t* slot, int64_t ncells,
+                      int32_t* order, int64_t* cell_start) {
+    memset(cell_start, 0, sizeof(int64_t) * (size_t)(ncells + 1));
+    for (int64_t i = 0; i < n; ++i) ++cell_start[keys[i] + 1];
+    for (int64_t c = 0; c < ncells; ++c) cell_start[c + 1] += cell_start[c];
+    /* process sources in ascending slot order so the counting sort's stability
+       yields (key, slot) order */
+    int32_t* by_slot = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int64_t* cursor = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ncells > 0 ? ncells : 1));
+    /* slots are a permutation of 0..n-1 in every use; fall back to an insertion
+       order by slot value otherwise */
+    int perm_ok = 1;
+    for (int64_t i = 0; i < n; ++i) by_slot[i] = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        if (slot[i] < 0 || slot[i] >= n || by_slot[slot[i]] != -1) { perm_ok = 0; break; }
+        by_slot[slot[i]] = (int32_t)i;
+    }
+    if (!perm_ok) {
+        for (int64_t i = 0; i < n; ++i) by_slot[i] = (int32_t)i;
+        /* stable insertion sort of indices by slot value */
+        for (int64_t i = 1; i < n; ++i) {
+            int32_t v = by_slot[i];
+            int64_t k = i - 1;
+            while (k >= 0 && slot[by_slot[k]] > slot[v]) { by_slot[k + 1] = by_slot[k]; --k; }
+            by_slot[k + 1] = v;
+        }
+    }
+    for (int64_t c = 0; c < ncells; ++c) cursor[c] = cell_start[c];
+    for (int64_t q = 0; q < n; ++q) {
+        const int32_t src = by_slot[q];
+        order[cursor[keys[src]]++] = src;
+    }
+    free(by_slot);
+    free(cursor);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as easy as
+ * 1, 2, 3", SC'11): 10 rounds of two 32x32->64 multiplies with the published
+ * multipliers and Weyl key increments.                                             */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n1 = lo1;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        const uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Counter layout:
+ *   key  = (lo32(seed), hi32(seed))
+ *   ctr  = (slot, attempt, (round_id & 0xFFFFFF) | stream << 24 | draw << 25, iteration)
+ * Unit vectors use only +,-,*,/,sqrt so CPU and GPU agree bit for bit:
+ *   3D: Marsaglia (1972) -- (x1,x2) uniform in the unit disk, s = x1^2+x2^2 < 1,
+ *       u = (2 x1 sqrt(1-s), 2 x2 sqrt(1-s), 1 - 2 s)
+ *   2D: (x1,x2) uniform in the unit disk (1e-24 < s < 1), u = (x1,x2) * (1/sqrt(s))
+ *       (the reference normalises the same way: random.hpp:238, g * (1/sqrt(n2)))
+ * A draw takes one Philox block: two 53-bit uniforms on [-1,1).  After 64 rejected
+ * draws (probability < 1e-42) the direction falls back to +x.                       */
+void orc_unit_vector(int dim, uint64_t seed, uint32_t slot, uint32_t attempt, uint32_t stream,
+                     uint32_t round_id, uint32_t iteration, double* u) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (uint32_t draw = 0; draw < 64; ++draw) {
+        const uint32_t ctr[4] = {slot, attempt,
+                                 (round_id & 0xFFFFFFu) | (stream << 24) | (draw << 25),
+                                 iteration};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        const uint64_t a = (((uint64_t)o[0] << 32) | o[1]) >> 11;
+        const uint64_t b = (((uint64_t)o[2] << 32) | o[3]) >> 11;
+        const double x1 = (double)a * 0x1p-52 - 1.0;
+        const double x2 = (double)b * 0x1p-52 - 1.0;
+        const double t1 = x1 * x1;
+        const double t2 = x2 * x2;
+        const double s = t1 + t2;
+        if (dim == 3) {
+            if (s < 1.0) {
+                const double q = 2.0 * sqrt(1.0 - s);
+                u[0] = x1 * q;
+                u[1] = x2 * q;
+                u[2] = 1.0 - 2.0 * s;
+                return;
+            }
+        } else {
+            if (s < 1.0 && s > 1e-24) {
+                const double inv = 1.0 / sqrt(s);
+                u[0] = x1 * inv;
+                u[1] = x2 * inv;
+                return;
+            }
+        }
+    }
+    u[0] = 1.0;
+    u[1] = 0.0;
+    if (dim == 3) u[2] = 0.0;
+}
+
+/* shape.hpp:513-518 SphereShape::propose_move: wrap(p + c_m * u), where
+ * Vec operator*(double, Vec) multiplies each component (geometry.hpp:29-33) and
+ * operator+ adds component-wise (geometry.hpp:21-24).                             */
+void orc_propose(int dim, const double* L, const double* x, double c_m, uint64_t seed,
+                 uint32_t slot, uint32_t attempt, uint32_t round_id, uint32_t iteration,
+                 double* out) {
+    double u[3];
+    orc_unit_vector(dim, seed, slot, attempt, 0, round_id, iteration, u);
+    for (int a = 0; a < dim; ++a) {
+        const double step = u[a] * c_m;
+        out[a] = x[a] + step;
+    }
+    orc_wrap(dim, L, out);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Independent pair search (not the reference's grid): a uniform bin grid whose bin
+ * edge is >= cutoff; emits, for every i, all j != i whose min-image distance to i is
+ * <= cut_ij (a superset filter; callers apply the exact predicate).                  */
+typedef struct {
+    int64_t* start; /* n+1 */
+    int32_t* nbr;
+} orc_csr;
+
+static void csr_free(orc_csr* c) { free(c->start); free(c->nbr); }
+
+static void build_pairs(int dim, const double* L, int64_t n, const double* x, const double* r,
+                        double extra, int brute, orc_csr* out) {
+    /* cut_ij = (r_i + r_j + extra) * (1 + 1e-9) + 1e-300 */
+    double maxr = 0.0;
+    for (int64_t i = 0; i < n; ++i) if (r[i] > maxr) maxr = r[i];
+    const double cut_max = (2.0 * maxr + extra) * (1.0 + 1e-9) + 1e-300;
+    int64_t cap = 16 * n + 16;
+    int64_t cnt = 0;
+    out->start = (int64_t*)calloc((size_t)(n + 1), sizeof(int64_t));
+    out->nbr = (int32_t*)malloc(sizeof(int32_t) * (size_t)cap);
+#define ORC_PUSH(jj)                                                                     \
+    do {                                                                                 \
+        if (cnt == cap) { cap *= 2; out->nbr = (int32_t*)realloc(out->nbr, sizeof(int32_t) * (size_t)cap); } \
+        out->nbr[cnt++] = (int32_t)(jj);                                                 \
+    } while (0)
+    if (brute || n < 64) {
+        for (int64_t i = 0; i < n; ++i) {
+            out->start[i] = cnt;
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                const double c = (r[i] + r[j] + extra) * (1.0 + 1e-9) + 1e-300;
+                if (orc_min_image_dist2(dim, L, x + i * dim, x + j * dim) <= c * c) ORC_PUSH(j);
+            }
+        }
+        out->start[n] = cnt;
+        return;
+    }
+    int32_t nb[3] = {1, 1, 1};
+    double be[3] = {1, 1, 1};
+    int64_t nbins = 1;
+    for (int a = 0; a < dim; ++a) {
+        int64_t k = (int64_t)(L[a] / cut_max);
+        if (k < 1) k = 1;
+        if (k > 4096) k = 4096;
+        nb[a] = (int32_t)k;
+        be[a] = L[a] / (double)k;
+        nbins *= k;
+    }
+    int64_t* bstart = (int64_t*)calloc((size_t)(nbins + 1), sizeof(int64_t));
+    int64_t* bin = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    int32_t* items = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)nbins);
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t idx = 0;
+        for (int a = dim - 1; a >= 0; --a) {
+            int64_t c = (int64_t)floor(x[i * dim + a] / be[a]);
+            c %= nb[a];
+            if (c < 0) c += nb[a];
+            idx = idx * nb[a] + c;
+        }
+        bin[i] = idx;
+        ++bstart[idx + 1];
+    }
+    for (int64_t b = 0; b < nbins; ++b) bstart[b + 1] += bstart[b];
+    for (int64_t b = 0; b < nbins; ++b) cur[b] = bstart[b];
+    for (int64_t i = 0; i < n; ++i) items[cur[bin[i]]++] = (int32_t)i;
+    for (int64_t i = 0; i < n; ++i) {
+        out->start[i] = cnt;
+        int64_t c[3] = {0, 0, 0};
+        int64_t rem = bin[i];
+        for (int a = 0; a < dim; ++a) { c[a] = rem % nb[a]; rem /= nb[a]; }
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            if (a >= dim) { lo[a] = 0; hi[a] = 0; continue; }
+            if (nb[a] <= 3) { lo[a] = 0; hi[a] = nb[a] - 1; }
+            else { lo[a] = -1; hi[a] = 1; }
+        }
+        for (int dz = lo[2]; dz <= hi[2]; ++dz)
+            for (int dy = lo[1]; dy <= hi[1]; ++dy)
+                for (int dx = lo[0]; dx <= hi[0]; ++dx) {
+                    int64_t m[3];
+                    const int d[3] = {dx, dy, dz};
+                    for (int a = 0; a < dim; ++a) {
+                        if (nb[a] <= 3) m[a] = d[a];
+                        else { m[a] = c[a] + d[a]; if (m[a] < 0) m[a] += nb[a]; if (m[a] >= nb[a]) m[a] -= nb[a]; }
+                    }
+                    int64_t idx = 0;
+                    for (int a = dim - 1; a >= 0; --a) idx = idx * nb[a] + m[a];
+                    for (int64_t t = bstart[idx]; t < bstart[idx + 1]; ++t) {
+                        const int32_t j = items[t];
+                        if (j == i) continue;
+                        const double cj = (r[i] + r[j] + extra) * (1.0 + 1e-9) + 1e-300;
+                        if (orc_min_image_dist2(dim, L, x + i * dim, x + (int64_t)j * dim) <= cj * cj)
+                            ORC_PUSH(j);
+                    }
+                }
+    }
+    out->start[n] = cnt;
+#undef ORC_PUSH
+    free(bstart); free(bin); free(items); free(cur);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Parallel migrate round ("J-phase").  For l = 0 .. n_l-1, every
+ * particle that has not yet accepted proposes p_i = propose(x0_i, attempt l); the
+ * proposal is accepted iff for every j with id_j != id_i:
+ *   j still active in phase l :  p_i clears x0_j  and  p_i clears p_j
+ *   j accepted in phase m < l :  p_i clears xnew_j
+ * using the reference predicate (shape.hpp:508-511, trial first as in
+ * shape.hpp:539-546).  Decisions of one phase are simultaneous.  The reference's
+ * per-particle loop structure (engine.hpp:94-104: <= n_l trials from the pre-sweep
+ * position, first clear trial kept, otherwise an exact revert) is kept.             */
+void orc_migrate_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
+                       const int32_t* id, const int32_t* slot, double c_m, int n_l,
+                       uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
+                       uint8_t* acc, int brute) {
+    orc_csr nb;
+    build_pairs(dim, L, n, x0, r, 2.0 * c_m, brute, &nb);
+    double* prop = (double*)malloc(sizeof(double) * (size_t)(n * dim + 1));
+    uint8_t* dec = (uint8_t*)malloc((size_t)(n + 1));
+    memcpy(xnew, x0, sizeof(double) * (size_t)(n * dim));
+    for (int64_t i = 0; i < n; ++i) acc[i] = ORC_NOT_ACCEPTED;
+    for (int l = 0; l < n_l; ++l) {
+        int64_t active = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            if (acc[i] != ORC_NOT_ACCEPTED) continue;
+            ++active;
+            orc_propose(dim, L, x0 + i * dim, c_m, seed, (uint32_t)slot[i], (uint32_t)l, round_id,
+                        iteration, prop + i * dim);
+        }
+        if (active == 0) break;
+        for (int64_t i = 0; i < n; ++i) {
+            dec[i] = 0;
+            if (acc[i] != ORC_NOT_ACCEPTED) continue;
+            int ok = 1;
+            for (int64_t t = nb.start[i]; t < nb.start[i + 1] && ok; ++t) {
+                const int64_t j = nb.nbr[t];
+                if (id[j] == id[i]) continue;
+                if (acc[j] == ORC_NOT_ACCEPTED) {
+                    if (sphere_overlap(dim, L, prop + i * dim, r[i], x0 + j * dim, r[j])) ok = 0;
+                    else if (sphere_overlap(dim, L, prop + i * dim, r[i], prop + j * dim, r[j])) ok = 0;
+                } else {
+                    if (sphere_overlap(dim, L, prop + i * dim, r[i], xnew + j * dim, r[j])) ok = 0;
+                }
+            }
+            dec[i] = (uint8_t)ok;
+        }
+        for (int64_t i = 0; i < n; ++i) {
+            if (acc[i] == ORC_NOT_ACCEPTED && dec[i]) {
+                acc[i] = (uint8_t)l;
+                memcpy(xnew + i * dim, prop + i * dim, sizeof(double) * (size_t)dim);
+            }
+        }
+    }
+    free(prop);
+    free(dec);
+    csr_free(&nb);
+}
+
+/* Global overlap statistics over all pairs of a state (the counting form of
+ * cell_grid.hpp:466-472 / shape.hpp:549-555: count > 0 <=> any collision).        */
+void orc_overlap_stats(int dim, const double* L, int64_t n, const double* x, const double* r,
+                       const int32_t* id, orc_round_stats* out) {
+    orc_csr nb;
+    build_pairs(dim, L, n, x, r, 0.0, 0, &nb);
+    int64_t pairs = 0;
+    double pen = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t t = nb.start[i]; t < nb.start[i + 1]; ++t) {
+            const int64_t j = nb.nbr[t];
+            if (j <= i || id[j] == id[i]) continue;
+            const double rr = r[i] + r[j];
+            const double d2 = orc_min_image_dist2(dim, L, x + i * dim, x + j * dim);
+            if (d2 <= rr * rr) {
+                ++pairs;
+                const double p = rr - sqrt(d2);
+                if (p > pen) pen = p;
+            }
+        }
+    }
+    out->overlap_pairs = pairs;
+    out->max_penetration = pen;
+    out->candidate_pairs = 0;
+    out->movers = 0;
+    csr_free(&nb);
+}
+
+/* Ordered candidate pairs visited by a 3^d neighbourhood scan (cell_grid.hpp:394-414
+ * with dims >= 3, so the offset cells are distinct), self excluded.                  */
+int64_t orc_candidate_pairs(int dim, const int32_t* dims, int64_t n, const uint32_t* keys) {
+    int64_t ncells = 1;
+    for (int a = 0; a < dim; ++a) ncells *= dims[a];
+    int64_t* cnt = (int64_t*)calloc((size_t)ncells, sizeof(int64_t));
+    for (int64_t i = 0; i < n; ++i) ++cnt[keys[i]];
+    int64_t total = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t rem = keys[i];
+        int c[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a) { c[a] = (int)(rem % dims[a]); rem /= dims[a]; }
+        const int zlo = dim == 3 ? -1 : 0, zhi = dim == 3 ? 1 : 0;
+        for (int dz = zlo; dz <= zhi; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int d[3] = {dx, dy, dz};
+                    int64_t idx = 0;
+                    for (int a = dim - 1; a >= 0; --a) {
+                        int m = c[a] + d[a];
+                        if (m < 0) m += dims[a];
+                        if (m >= dims[a]) m -= dims[a];
+                        idx = idx * dims[a] + m;
+                    }
+                    total += cnt[idx];
+                }
+        total -= 1;
+    }
+    free(cnt);
+    return total;
+}
+
+double orc_max_radius(int64_t n, const double* r) {
+    double m = 0.0; /* shape.hpp:565-570 starts from 0.0 */
+    for (int64_t i = 0; i < n; ++i) m = r[i] > m ? r[i] : m;
+    return m;
+}
+
+/* geometry.hpp:149-164: pi r^2 or (4/3) pi r^3, summed in storage order, / measure */
+double orc_volume_fraction_seq(int dim, const double* L, int64_t n, const double* r) {
+    const double pi = 3.141592653589793238462643383279502884;
+    double sum = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (dim == 2) sum += pi * r[i] * r[i];
+        else sum += (4.0 / 3.0) * pi * r[i] * r[i] * r[i];
+    }
+    double m = 1.0;
+    for (int a = 0; a < dim; ++a) m *= L[a];
+    return sum / m;
+}

@@ -1,0 +1,431 @@
+"""B200-native SRM hot loop -- Python mirror of the reference's proj/core API.
+
+Every call runs on the GPU through libsrm_b200.so's C ABI (include/srm_b200.h);
+there is no CPU fallback.  Names follow /root/reference/proj/core/include/srm/:
+
+    SrmParams, Snapshot, GenerateStatus, GenerateResult, ProgressRecord  (engine.hpp:22-82)
+    srm_generate                                                         (engine.hpp:176-260)
+    relax_sweeps, shake, swell_all, reorder_by_locality                  (engine.hpp:112-166)
+    rsa_place, mix_seed                                                  (rsa.hpp:21-69, random.hpp:84-89)
+    Error, ValidationError, PlacementFailure                            (errors.hpp:10-43)
+
+Particles are numpy arrays: ``pos`` float64 (n, dim), ``radius`` float64 (n,),
+``id`` int32 (n,), in the reference's storage order.  The functions that take an
+``Rng&`` in the reference take a 64-bit Philox ``key`` here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _native
+from ._native import GenerateOut, Params, RoundStats
+
+__all__ = [
+    "Error", "ValidationError", "PlacementFailure", "CudaError", "NoDeviceError",
+    "SrmParams", "Snapshot", "GenerateStatus", "GenerateResult", "ProgressRecord",
+    "Context", "srm_generate", "relax_sweeps", "shake", "swell_all", "reorder_by_locality",
+    "rsa_place", "mix_seed", "K_RSA_DEFAULT_ATTEMPTS",
+]
+
+K_RSA_DEFAULT_ATTEMPTS = 10000  # rsa.hpp:15 kRsaDefaultAttempts
+
+OK, ITER_LIMIT, INVALID, CUDA_ERROR, PLACEMENT_FAILURE, NO_DEVICE = range(6)
+
+
+class Error(RuntimeError):
+    """errors.hpp:10-13 srm::Error"""
+
+
+class ValidationError(Error):
+    """errors.hpp:25-28"""
+
+
+class PlacementFailure(Error):
+    """errors.hpp:15-23"""
+
+    def __init__(self, what: str, placed_count: int, attempt_limit: int):
+        super().__init__(what)
+        self.placed_count = placed_count
+        self.attempt_limit = attempt_limit
+
+
+class CudaError(Error):
+    """device failure (no reference counterpart)"""
+
+
+class NoDeviceError(CudaError):
+    """no CUDA device: the B200 path has no CPU fallback"""
+
+
+def _ptr(a: Optional[np.ndarray]):
+    # data_as keeps a reference to the array for the duration of the call
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _check(status: int, ctx_handle=None, allow_iter_limit: bool = False) -> int:
+    if status == OK or (allow_iter_limit and status == ITER_LIMIT):
+        return status
+    lib = _native.lib()
+    msg = (lib.srm_b200_last_error(ctx_handle) if ctx_handle else lib.srm_b200_create_error()) or b""
+    msg = msg.decode(errors="replace")
+    if status == INVALID:
+        raise ValidationError(msg)
+    if status == NO_DEVICE:
+        raise NoDeviceError(msg)
+    raise CudaError(f"status {status}: {msg}")
+
+
+@dataclass
+class SrmParams:
+    """engine.hpp:22-32, same defaults."""
+
+    c_w: float = 0.02
+    c_m: float = 0.01
+    c_r: float = 0.0
+    n_k: int = 8
+    n_l: int = 8
+    f_target: float = 0.5
+    max_iterations: int = 1000000
+    seed: int = 1
+    reorder_period: int = 16
+
+    def to_c(self) -> Params:
+        return Params(self.c_w, self.c_m, self.c_r, self.n_k, self.n_l, self.f_target,
+                      self.max_iterations, self.seed & 0xFFFFFFFFFFFFFFFF, self.reorder_period)
+
+
+def particle_measure(dim: int, radius: np.ndarray) -> np.ndarray:
+    if dim == 2:
+        return math.pi * radius * radius
+    return (4.0 / 3.0) * math.pi * radius * radius * radius
+
+
+@dataclass
+class Snapshot:
+    """engine.hpp:53-65 Snapshot<S> for disks/spheres."""
+
+    box: Sequence[float]
+    pos: np.ndarray
+    radius: np.ndarray
+    id: Optional[np.ndarray] = None
+    volume_fraction: float = 0.0
+    iteration_count: int = 0
+    params: SrmParams = field(default_factory=SrmParams)
+    seed: int = 0
+
+    def __post_init__(self):
+        self.box = tuple(float(v) for v in self.box)
+        self.pos = np.ascontiguousarray(self.pos, dtype=np.float64).reshape(-1, len(self.box))
+        self.radius = np.ascontiguousarray(self.radius, dtype=np.float64).reshape(-1)
+        if self.id is None:
+            self.id = np.arange(len(self.radius), dtype=np.int32)
+        self.id = np.ascontiguousarray(self.id, dtype=np.int32)
+
+    @property
+    def dim(self) -> int:
+        return len(self.box)
+
+    @property
+    def n(self) -> int:
+        return len(self.radius)
+
+    def refresh_volume_fraction(self) -> None:
+        """shape.hpp:557-563 (sequential host sum)"""
+        s = 0.0
+        for v in particle_measure(self.dim, self.radius).tolist():
+            s += v
+        m = 1.0
+        for L in self.box:
+            m *= L
+        self.volume_fraction = s / m
+
+    def copy(self) -> "Snapshot":
+        return Snapshot(self.box, self.pos.copy(), self.radius.copy(), self.id.copy(),
+                        self.volume_fraction, self.iteration_count, self.params, self.seed)
+
+
+class GenerateStatus(enum.Enum):
+    Converged = 0
+    IterationLimitExceeded = 1
+
+
+@dataclass
+class ProgressRecord:
+    """engine.hpp:75-80 (+ rounds run in the iteration)."""
+
+    iteration: int
+    volume_fraction: float
+    accepted: bool
+    elapsed_seconds: float
+    rounds: int = 0
+
+
+@dataclass
+class GenerateResult:
+    status: GenerateStatus
+    snapshot: Snapshot
+    accepted_iterations: int = 0
+    rounds: int = 0
+    shake_rounds: int = 0
+
+
+class Context:
+    """One device-resident particle state on one CUDA stream (srm_b200_ctx)."""
+
+    def __init__(self, box: Sequence[float], capacity: int, device: int = 0):
+        lib = _native.lib()
+        self.box = tuple(float(v) for v in box)
+        self.dim = len(self.box)
+        L = (C.c_double * self.dim)(*self.box)
+        h = C.c_void_p()
+        _check(lib.srm_b200_create(self.dim, 0, L, int(capacity), int(device), C.byref(h)))
+        self._h = h
+        self.capacity = int(capacity)
+        self.n = 0
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _native.lib().srm_b200_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _c(self, status, allow_iter_limit=False):
+        return _check(status, self._h, allow_iter_limit)
+
+    # ---- state --------------------------------------------------------------------
+    def upload(self, pos: np.ndarray, radius: np.ndarray, id: Optional[np.ndarray] = None) -> None:
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, self.dim)
+        radius = np.ascontiguousarray(radius, dtype=np.float64).reshape(-1)
+        if id is not None:
+            id = np.ascontiguousarray(id, dtype=np.int32)
+        n = len(radius)
+        self._c(_native.lib().srm_b200_upload(self._h, n, _ptr(pos), _ptr(radius), _ptr(id)))
+        self.n = n
+
+    def upload_records(self, records: np.ndarray, off_id: int, off_pos: int, off_radius: int) -> None:
+        n = len(records)
+        self._c(_native.lib().srm_b200_upload_records(self._h, n, _ptr(records), records.itemsize,
+                                                       off_id, off_pos, off_radius))
+        self.n = n
+
+    def download_records(self, records: np.ndarray, off_id: int, off_pos: int, off_radius: int) -> None:
+        self._c(_native.lib().srm_b200_download_records(self._h, _ptr(records), records.itemsize,
+                                                         off_id, off_pos, off_radius))
+
+    def download(self, pos=None, radius=None, id=None):
+        n = self.n
+        pos = np.empty((n, self.dim), np.float64) if pos is None else pos
+        radius = np.empty(n, np.float64) if radius is None else radius
+        id = np.empty(n, np.int32) if id is None else id
+        self._c(_native.lib().srm_b200_download(self._h, _ptr(pos), _ptr(radius), _ptr(id)))
+        return pos, radius, id
+
+    # ---- reference entry points ------------------------------------------------------
+    def generate(self, params: SrmParams, iteration_count: int = 0,
+                 progress: Optional[Callable[[ProgressRecord], None]] = None) -> GenerateOut:
+        cp = params.to_c()
+        out = GenerateOut()
+        if progress is not None:
+            def _cb(rec_p, _user):
+                r = rec_p.contents
+                progress(ProgressRecord(r.iteration, r.volume_fraction, bool(r.accepted),
+                                        r.elapsed_seconds, r.rounds))
+            cb = _native.PROGRESS_FN(_cb)
+        else:
+            cb = _native.PROGRESS_FN()
+        st = _native.lib().srm_b200_generate(self._h, C.byref(cp), int(iteration_count), cb, None, C.byref(out))
+        self._c(st, allow_iter_limit=True)
+        return out
+
+    def relax_sweeps(self, c_m: float, c_r: float, n_l: int, sweeps: int, key: int) -> None:
+        self._c(_native.lib().srm_b200_relax_sweeps(self._h, c_m, c_r, n_l, sweeps, key & 0xFFFFFFFFFFFFFFFF))
+
+    def swell_all(self, c_w: float) -> None:
+        self._c(_native.lib().srm_b200_swell_all(self._h, c_w))
+
+    def reorder_by_locality(self, cell_size: float) -> np.ndarray:
+        remap = np.empty(self.n, np.int32)
+        self._c(_native.lib().srm_b200_reorder_by_locality(self._h, cell_size, _ptr(remap)))
+        return remap
+
+    def max_bounding_radius(self) -> float:
+        v = C.c_double()
+        self._c(_native.lib().srm_b200_max_bounding_radius(self._h, C.byref(v)))
+        return v.value
+
+    def volume_fraction(self) -> float:
+        v = C.c_double()
+        self._c(_native.lib().srm_b200_volume_fraction(self._h, C.byref(v)))
+        return v.value
+
+    # ---- stages ------------------------------------------------------------------------
+    def grid_dims(self, cell_size: float, max_radius: float = -1.0, slack: float = 0.0):
+        dims = (C.c_int32 * 3)()
+        edge = (C.c_double * 3)()
+        nc = C.c_int64()
+        self._c(_native.lib().srm_b200_grid_dims(self._h, cell_size, max_radius, slack, dims, edge, C.byref(nc)))
+        return tuple(dims[: self.dim]), tuple(edge[: self.dim]), nc.value
+
+    def grid_build(self, cell_size: float):
+        _, _, ncells = self.grid_dims(cell_size)
+        keys = np.empty(self.n, np.uint32)
+        order = np.empty(self.n, np.int32)
+        cell_start = np.empty(ncells + 1, np.int64)
+        self._c(_native.lib().srm_b200_grid_build(self._h, cell_size, _ptr(keys), _ptr(order), _ptr(cell_start)))
+        return keys, order, cell_start
+
+    def overlap_stats(self, cell_size: float) -> RoundStats:
+        st = RoundStats()
+        self._c(_native.lib().srm_b200_overlap_stats(self._h, cell_size, C.byref(st)))
+        return st
+
+    def round(self, cell_size: float, c_m: float, n_l: int, key: int, round_id: int = 0,
+              iteration: int = 0, with_candidates: bool = False, want_accepted: bool = True):
+        st = RoundStats()
+        acc = np.empty(self.n, np.uint8) if want_accepted else None
+        self._c(_native.lib().srm_b200_round(self._h, cell_size, c_m, n_l, key & 0xFFFFFFFFFFFFFFFF,
+                                             round_id, iteration, int(with_candidates), _ptr(acc),
+                                             C.byref(st)))
+        return st, acc
+
+    def rounds(self, cell_size: float, c_m: float, n_l: int, key: int, first_round: int,
+               iteration: int, rounds: int) -> RoundStats:
+        st = RoundStats()
+        self._c(_native.lib().srm_b200_rounds(self._h, cell_size, c_m, n_l, key & 0xFFFFFFFFFFFFFFFF,
+                                              first_round, iteration, rounds, C.byref(st)))
+        return st
+
+    # ---- instrumentation -------------------------------------------------------------
+    def launch_count(self) -> int:
+        return _native.lib().srm_b200_launch_count(self._h)
+
+    def reset_launch_count(self) -> None:
+        _native.lib().srm_b200_reset_launch_count(self._h)
+
+    def timing_enable(self, on: bool = True) -> None:
+        self._c(_native.lib().srm_b200_timing_enable(self._h, int(on)))
+
+    def timing_get(self):
+        ms = (C.c_double * _native.NPHASE)()
+        calls = (C.c_int64 * _native.NPHASE)()
+        self._c(_native.lib().srm_b200_timing_get(self._h, ms, calls))
+        return list(ms), list(calls)
+
+    def sync(self) -> None:
+        self._c(_native.lib().srm_b200_sync(self._h))
+
+    def stopwatch_start(self) -> None:
+        """record a CUDA event on the context stream"""
+        self._c(_native.lib().srm_b200_stopwatch(self._h, 0, None))
+
+    def stopwatch_stop(self) -> float:
+        """record the stop event, wait for it; device milliseconds since start"""
+        v = C.c_double()
+        self._c(_native.lib().srm_b200_stopwatch(self._h, 1, C.byref(v)))
+        return v.value
+
+
+def _ctx_for(snap: Snapshot, device: int) -> Context:
+    ctx = Context(snap.box, max(snap.n, 1), device)
+    if snap.n:
+        ctx.upload(snap.pos, snap.radius, snap.id)
+    return ctx
+
+
+def srm_generate(initial: Snapshot, params: SrmParams,
+                 progress: Optional[Callable[[ProgressRecord], None]] = None,
+                 device: int = 0) -> GenerateResult:
+    """engine.hpp:176-260 srm_generate<S>: the initial snapshot is copied in and the
+    result returned by value; the loop runs on the GPU."""
+    with _ctx_for(initial, device) as ctx:
+        out = ctx.generate(params, initial.iteration_count, progress)
+        snap = initial.copy()
+        if initial.n:
+            snap.pos, snap.radius, snap.id = ctx.download()
+    snap.params = params
+    snap.seed = params.seed
+    snap.volume_fraction = out.volume_fraction
+    snap.iteration_count = out.iteration_count
+    status = GenerateStatus.Converged if out.status == OK else GenerateStatus.IterationLimitExceeded
+    return GenerateResult(status, snap, out.accepted_iterations, out.rounds, out.shake_rounds)
+
+
+def relax_sweeps(snap: Snapshot, c_m: float, c_r: float, n_l: int, sweeps: int, key: int,
+                 device: int = 0) -> None:
+    """engine.hpp:112-122 (in place on snap)."""
+    if snap.n == 0 or sweeps < 1:
+        return
+    with _ctx_for(snap, device) as ctx:
+        ctx.relax_sweeps(c_m, c_r, n_l, sweeps, key)
+        snap.pos, snap.radius, snap.id = ctx.download()
+
+
+def shake(snap: Snapshot, params: SrmParams, key: int, device: int = 0) -> None:
+    """engine.hpp:126-130"""
+    relax_sweeps(snap, params.c_m, params.c_r, params.n_l, params.n_k, key, device)
+
+
+def swell_all(snap: Snapshot, c_w: float, device: int = 0) -> None:
+    """engine.hpp:134-138 (device kernel; radius *= 1 + c_w)."""
+    if snap.n == 0:
+        return
+    with _ctx_for(snap, device) as ctx:
+        ctx.swell_all(c_w)
+        snap.pos, snap.radius, snap.id = ctx.download()
+
+
+def reorder_by_locality(snap: Snapshot, cell_size: float, device: int = 0) -> np.ndarray:
+    """engine.hpp:144-166: returns remap[old] = new; snap is reordered in place."""
+    if snap.n == 0:
+        return np.empty(0, np.int32)
+    with _ctx_for(snap, device) as ctx:
+        remap = ctx.reorder_by_locality(cell_size)
+        snap.pos, snap.radius, snap.id = ctx.download()
+    return remap
+
+
+def rsa_place(radii, box: Sequence[float], max_attempts: int, seed: int):
+    """rsa.hpp:21-61 with Rng(seed): returns (pos, id).  Bit-identical to the reference."""
+    radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+    dim = len(box)
+    L = (C.c_double * dim)(*[float(v) for v in box])
+    n = len(radii)
+    pos = np.empty((max(n, 1), dim), np.float64)
+    ids = np.empty(max(n, 1), np.int32)
+    placed = C.c_int64()
+    st = _native.lib().srm_b200_rsa_place(dim, L, n, _ptr(radii), int(max_attempts),
+                                          seed & 0xFFFFFFFFFFFFFFFF, _ptr(pos), _ptr(ids), C.byref(placed))
+    if st == PLACEMENT_FAILURE:
+        raise PlacementFailure(
+            f"rsa_place: exceeded {max_attempts} attempts after placing {placed.value} particles; "
+            "initial volume fraction too high", placed.value, max_attempts)
+    if st == INVALID:
+        raise ValidationError("rsa_place: invalid radii or box")
+    _check(st)
+    return pos[:n], ids[:n]
+
+
+def mix_seed(seed: int, stream: int) -> int:
+    """random.hpp:84-89"""
+    return _native.lib().srm_b200_mix_seed(seed & 0xFFFFFFFFFFFFFFFF, stream & 0xFFFFFFFFFFFFFFFF)

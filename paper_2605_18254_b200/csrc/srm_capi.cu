@@ -1,0 +1,907 @@
+// srm_capi.cu -- context, C ABI and the SRM control loop of libsrm_b200.so.
+//
+// See include/srm_b200.h for the contract of every entry point and the reference
+// interface it replaces.  Device data layout: DESIGN.md §2.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/srm_b200.h"
+#include "srm_kernels.cuh"
+
+using namespace srmb;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaError {
+    std::string msg;
+};
+struct Invalid {
+    std::string msg;
+};
+
+#define SRM_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            throw CudaError{std::string(#call) + ": " + cudaGetErrorString(e_)};           \
+    } while (0)
+
+constexpr int kMaxPhases = 254;  // acc[] encodes the phase of acceptance in a byte
+
+int blocks_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 2147483647) b = 2147483647;
+    return static_cast<int>(b);
+}
+
+template <typename T>
+T* dalloc(int64_t count) {
+    void* p = nullptr;
+    if (count < 1) count = 1;
+    SRM_CUDA(cudaMalloc(&p, sizeof(T) * static_cast<size_t>(count)));
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct srm_b200_ctx {
+    int dim = 3;
+    int shape = 0;
+    int device = 0;
+    Box box{};
+    int64_t cap = 0;
+    int64_t n = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    State P{}, Q{}, S{};
+    double* xblock[3] = {nullptr, nullptr, nullptr};  // contiguous x storage of P, Q, S
+    uint32_t* key = nullptr;
+    uint32_t* skey = nullptr;
+    int32_t* perm = nullptr;
+    uint8_t* acc = nullptr;
+    int32_t* nbr = nullptr;
+    uint8_t* nbr_cnt = nullptr;
+
+    uint32_t* count = nullptr;
+    int64_t* cell_start = nullptr;
+    uint64_t* partial = nullptr;
+    int64_t cell_cap = 0;
+    int64_t tile_cap = 0;
+
+    GridParams* gp = nullptr;
+    RoundParams* rp = nullptr;
+    StatsDev* stats = nullptr;
+    double* red_part_sum = nullptr;
+    double* red_part_max = nullptr;
+    double* red_out = nullptr;
+
+    StatsDev* h_stats = nullptr;  // pinned
+    double* h_red = nullptr;      // pinned [2]
+
+    char* rec_stage = nullptr;
+    size_t rec_stage_bytes = 0;
+
+    int64_t launches = 0;
+
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Pending {
+        int fam;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    double ms[SRM_B200_NPHASE] = {0, 0, 0, 0};
+    int64_t calls[SRM_B200_NPHASE] = {0, 0, 0, 0};
+
+    GridParams hg{};  // host copy of the grid currently in gp
+    bool hg_set = false;
+
+    cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
+
+    // ---------------------------------------------------------------------------
+    cudaEvent_t take_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            SRM_CUDA(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    struct FamScope {
+        srm_b200_ctx* c;
+        int fam;
+        cudaEvent_t a = nullptr;
+        FamScope(srm_b200_ctx* c_, int f) : c(c_), fam(f) {
+            if (c->timing) {
+                a = c->take_event();
+                SRM_CUDA(cudaEventRecord(a, c->stream));
+            }
+        }
+        ~FamScope() {
+            if (c->timing && a) {
+                try {
+                    cudaEvent_t b = c->take_event();
+                    if (cudaEventRecord(b, c->stream) == cudaSuccess) c->pending.push_back({fam, a, b});
+                } catch (...) {
+                }
+            }
+        }
+    };
+    void harvest_timing() {
+        if (pending.empty()) return;
+        for (auto& p : pending) {
+            float t = 0.f;
+            SRM_CUDA(cudaEventSynchronize(p.b));
+            SRM_CUDA(cudaEventElapsedTime(&t, p.a, p.b));
+            ms[p.fam] += t;
+            calls[p.fam] += 1;
+        }
+        pending.clear();
+        ev_used = 0;
+    }
+    void sync() {
+        SRM_CUDA(cudaStreamSynchronize(stream));
+        SRM_CUDA(cudaGetLastError());
+        if (timing && ev_used > 4096) harvest_timing();
+    }
+    void launched(int k = 1) {
+        launches += k;
+        SRM_CUDA(cudaPeekAtLastError());
+    }
+
+    // ---------------------------------------------------------------------------
+    void alloc_state(State& s, int slotx) {
+        xblock[slotx] = dalloc<double>(3 * cap);
+        for (int a = 0; a < 3; ++a) s.x[a] = xblock[slotx] + a * cap;
+        s.r = dalloc<double>(cap);
+        s.id = dalloc<int32_t>(cap);
+        s.slot = dalloc<int32_t>(cap);
+    }
+    static void free_state(State& s) {
+        cudaFree(s.r);
+        cudaFree(s.id);
+        cudaFree(s.slot);
+    }
+
+    void init() {
+        SRM_CUDA(cudaSetDevice(device));
+        SRM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        alloc_state(P, 0);
+        alloc_state(Q, 1);
+        alloc_state(S, 2);
+        key = dalloc<uint32_t>(cap);
+        skey = dalloc<uint32_t>(cap);
+        perm = dalloc<int32_t>(cap);
+        acc = dalloc<uint8_t>(cap);
+        nbr = dalloc<int32_t>(cap * kNbrCap);
+        nbr_cnt = dalloc<uint8_t>(cap);
+        gp = dalloc<GridParams>(1);
+        rp = dalloc<RoundParams>(1);
+        stats = dalloc<StatsDev>(1);
+        red_part_sum = dalloc<double>(kRedBlocks);
+        red_part_max = dalloc<double>(kRedBlocks);
+        red_out = dalloc<double>(2);
+        SRM_CUDA(cudaMallocHost(&h_stats, sizeof(StatsDev)));
+        SRM_CUDA(cudaMallocHost(&h_red, 2 * sizeof(double)));
+    }
+
+    ~srm_b200_ctx() {
+        if (device >= 0) cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (int k = 0; k < 3; ++k) cudaFree(xblock[k]);
+        free_state(P);
+        free_state(Q);
+        free_state(S);
+        cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc); cudaFree(nbr);
+        cudaFree(nbr_cnt); cudaFree(count); cudaFree(cell_start); cudaFree(partial);
+        cudaFree(gp); cudaFree(rp); cudaFree(stats); cudaFree(red_part_sum);
+        cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
+        if (h_stats) cudaFreeHost(h_stats);
+        if (h_red) cudaFreeHost(h_red);
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        if (sw_start) cudaEventDestroy(sw_start);
+        if (sw_stop) cudaEventDestroy(sw_stop);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    // ---------------------------------------------------------------------------
+    // CellGrid ctor (cell_grid.hpp:288-309) + the near-search stencil for a state
+    // whose largest radius is max_r_state and whose moves reach `extra`/2.
+    GridParams make_grid(double cell_size, double max_r_state, double extra) const {
+        if (!(cell_size > 0.0)) throw Invalid{"CellGrid: cell_size must be positive"};
+        GridParams g{};
+        g.ncells = 1;
+        for (int a = 0; a < 3; ++a) {
+            if (a >= dim) {
+                g.dims[a] = 1;
+                g.edge[a] = 1.0;
+                g.near_s[a] = -1;
+                continue;
+            }
+            const double L = box.L[a];
+            int nn = static_cast<int>(std::floor(L / cell_size));
+            if (nn < 3) nn = 3;
+            g.dims[a] = nn;
+            g.edge[a] = L / nn;
+            g.ncells *= nn;
+            if (g.ncells > 4294967295LL)
+                throw Invalid{"CellGrid: more than 2^32 cells (radius too small for the box)"};
+        }
+        g.extra = extra;
+        const double cut = ((max_r_state + max_r_state + extra) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
+        for (int a = 0; a < dim; ++a) {
+            int64_t s = 1;
+            while (static_cast<double>(s) * g.edge[a] < cut && 2 * s + 1 < g.dims[a]) ++s;
+            g.near_s[a] = (2 * s + 1 >= g.dims[a]) ? -1 : static_cast<int32_t>(s);
+        }
+        return g;
+    }
+
+    void ensure_cells(int64_t ncells) {
+        if (ncells <= cell_cap) return;
+        cudaFree(count);
+        cudaFree(cell_start);
+        cudaFree(partial);
+        count = nullptr; cell_start = nullptr; partial = nullptr;
+        const int64_t c = ncells + ncells / 8 + 1024;
+        count = dalloc<uint32_t>(c);
+        cell_start = dalloc<int64_t>(c + 1);
+        tile_cap = (c + kScanTile - 1) / kScanTile;
+        partial = dalloc<uint64_t>(tile_cap);
+        SRM_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * c, stream));
+        cell_cap = c;
+    }
+
+    void set_grid(const GridParams& g) {
+        ensure_cells(g.ncells);
+        k_set_grid<<<1, 1, 0, stream>>>(gp, g);
+        launched();
+        hg = g;
+        hg_set = true;
+    }
+
+    void set_round(double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration) {
+        RoundParams v{};
+        v.c_m = c_m;
+        v.n_l = n_l;
+        v.key.k0 = static_cast<uint32_t>(seed);
+        v.key.k1 = static_cast<uint32_t>(seed >> 32);
+        v.key.round_id = round_id & 0xFFFFFFu;
+        v.key.iteration = iteration;
+        k_set_round<<<1, 1, 0, stream>>>(rp, v);
+        launched();
+    }
+
+    // grid rebuild T -> S (sorted) + skey; gp must be set
+    void grid_build(State& T) {
+        FamScope fs(this, 0);
+        const int nb = blocks_for(n, 256);
+        const int cb = static_cast<int>(std::min<int64_t>(blocks_for(hg.ncells, 256), 148 * 64));
+        if (dim == 2) k_keys<2><<<nb, 256, 0, stream>>>(n, T, gp, key, count);
+        else k_keys<3><<<nb, 256, 0, stream>>>(n, T, gp, key, count);
+        const int tiles = static_cast<int>((hg.ncells + kScanTile - 1) / kScanTile);
+        k_scan_tiles<<<tiles, 1024, 0, stream>>>(count, gp, partial);
+        k_scan_partials<<<1, 1024, 0, stream>>>(partial, tile_cap, gp, cell_start);
+        k_scan_down<<<tiles, 1024, 0, stream>>>(count, partial, gp, cell_start);
+        k_scatter<<<nb, 256, 0, stream>>>(n, key, cell_start, count, perm);
+        k_cellsort<<<cb, 256, 0, stream>>>(gp, cell_start, T.slot, perm);
+        if (dim == 2) k_gather<2><<<nb, 256, 0, stream>>>(n, perm, key, T, S, skey);
+        else k_gather<3><<<nb, 256, 0, stream>>>(n, perm, key, T, S, skey);
+        launched(7);
+    }
+
+    void copy_state(State& A, State& B) {
+        if (dim == 2) k_copy_state<2><<<blocks_for(n, 256), 256, 0, stream>>>(n, A, B);
+        else k_copy_state<3><<<blocks_for(n, 256), 256, 0, stream>>>(n, A, B);
+        launched();
+    }
+
+    // one round on T (T is rewritten in this round's sorted order); gp must be set
+    void round(State& T, double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
+               bool with_stats, bool with_candidates) {
+        if (n_l > kMaxPhases) throw Invalid{"n_l > 254 is not supported by the B200 path"};
+        set_round(c_m, n_l, seed, round_id, iteration);
+        grid_build(T);
+        SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
+        const int nb = blocks_for(n, 256);
+        {
+            FamScope fs(this, 1);
+            if (dim == 2)
+                k_phase0<2><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+            else
+                k_phase0<3><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+            launched();
+        }
+        if (n_l > 1) {
+            FamScope fs(this, 2);
+            for (int l = 1; l < n_l; ++l) {
+                if (dim == 2)
+                    k_phase<2><<<nb, 256, 0, stream>>>(n, l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+                else
+                    k_phase<3><<<nb, 256, 0, stream>>>(n, l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+            }
+            launched(n_l - 1);
+        }
+        if (with_stats) {
+            FamScope fs(this, 3);
+            if (dim == 2)
+                k_stats<2><<<nb, 256, 0, stream>>>(n, S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, with_candidates ? 1 : 0, stats);
+            else
+                k_stats<3><<<nb, 256, 0, stream>>>(n, S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, with_candidates ? 1 : 0, stats);
+            launched();
+        }
+    }
+
+    srm_b200_round_stats read_stats(bool with_candidates) {
+        SRM_CUDA(cudaMemcpyAsync(h_stats, stats, sizeof(StatsDev), cudaMemcpyDeviceToHost, stream));
+        sync();
+        srm_b200_round_stats o{};
+        o.overlap_pairs = static_cast<int64_t>(h_stats->overlap_pairs);
+        double pen = 0.0;
+        std::memcpy(&pen, &h_stats->pen_bits, sizeof(double));
+        o.max_penetration = pen;
+        o.candidate_pairs = with_candidates ? static_cast<int64_t>(h_stats->candidate_pairs) : -1;
+        o.movers = static_cast<int64_t>(h_stats->movers);
+        return o;
+    }
+
+    // fixed-order reductions over T.r: {sum of measures, max radius}
+    void reduce(const State& T, double* sum_measure, double* max_r) {
+        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, T.r, red_part_sum, red_part_max);
+        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, T.r, red_part_sum, red_part_max);
+        k_reduce_final<<<1, 256, 0, stream>>>(red_part_sum, red_part_max, red_out);
+        launched(2);
+        SRM_CUDA(cudaMemcpyAsync(h_red, red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        sync();
+        if (sum_measure) *sum_measure = h_red[0];
+        if (max_r) *max_r = h_red[1];
+    }
+    double box_measure() const {
+        double m = 1.0;  // geometry.hpp:98-102
+        for (int a = 0; a < dim; ++a) m *= box.L[a];
+        return m;
+    }
+    double volume_fraction(const State& T) {
+        double s = 0.0;
+        reduce(T, &s, nullptr);
+        return s / box_measure();
+    }
+    double max_radius(const State& T) {
+        double m = 0.0;
+        reduce(T, nullptr, &m);
+        return m;
+    }
+
+    void scale_radius(State& T, double factor) {
+        k_scale_radius<<<blocks_for(n, 256), 256, 0, stream>>>(n, T.r, factor);
+        launched();
+    }
+};
+
+namespace {
+
+int fail(srm_b200_ctx* c, int code, const std::string& m) {
+    if (c) c->err = m;
+    return code;
+}
+
+template <typename F>
+int guarded(srm_b200_ctx* c, F&& f) {
+    if (!c) return SRM_B200_INVALID;
+    try {
+        c->err.clear();
+        if (c->device >= 0) SRM_CUDA(cudaSetDevice(c->device));
+        return f();
+    } catch (const Invalid& e) {
+        return fail(c, SRM_B200_INVALID, e.msg);
+    } catch (const CudaError& e) {
+        return fail(c, SRM_B200_CUDA_ERROR, e.msg);
+    } catch (const std::bad_alloc&) {
+        return fail(c, SRM_B200_CUDA_ERROR, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(c, SRM_B200_CUDA_ERROR, e.what());
+    }
+}
+
+// engine.hpp:38-49 validate_params, same order and messages
+void validate_params(const srm_b200_params& p) {
+    if (!(p.c_w >= 0.0)) throw Invalid{"params: c_w must be >= 0"};
+    if (!(p.c_w <= 0.25)) throw Invalid{"params: c_w must be <= 0.25 (cell safety bound)"};
+    if (!(p.c_m >= 0.0)) throw Invalid{"params: c_m must be >= 0"};
+    if (!(p.c_r >= 0.0)) throw Invalid{"params: c_r must be >= 0"};
+    if (p.n_k < 1) throw Invalid{"params: n_k must be >= 1"};
+    if (p.n_l < 1) throw Invalid{"params: n_l must be >= 1"};
+    if (!(p.f_target > 0.0 && p.f_target < 1.0)) throw Invalid{"params: f_target must lie in (0, 1)"};
+    if (p.max_iterations < 1) throw Invalid{"params: max_iterations must be >= 1"};
+    if (p.reorder_period < 0) throw Invalid{"params: reorder_period must be >= 0"};
+    if (p.n_l > kMaxPhases) throw Invalid{"params: n_l > 254 is not supported by the B200 path"};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* srm_b200_create_error(void) { return g_create_error.c_str(); }
+
+int srm_b200_create(int dim, int shape_kind, const double* box_lengths, int64_t capacity, int device,
+                    srm_b200_ctx** out) {
+    g_create_error.clear();
+    if (!out) return SRM_B200_INVALID;
+    *out = nullptr;
+    if (dim != 2 && dim != 3) { g_create_error = "dim must be 2 or 3"; return SRM_B200_INVALID; }
+    if (shape_kind != SRM_B200_SPHERE) { g_create_error = "unsupported shape kind"; return SRM_B200_INVALID; }
+    if (capacity < 1) { g_create_error = "capacity must be >= 1"; return SRM_B200_INVALID; }
+    for (int a = 0; a < dim; ++a)
+        if (!(box_lengths[a] > 0.0)) {
+            g_create_error = "PeriodicBox: axis length " + std::to_string(a) + " must be positive";
+            return SRM_B200_INVALID;
+        }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        g_create_error = "no CUDA device: the B200 SRM path has no CPU fallback";
+        return SRM_B200_NO_DEVICE;
+    }
+    if (device < 0 || device >= ndev) { g_create_error = "bad device ordinal"; return SRM_B200_INVALID; }
+    srm_b200_ctx* c = nullptr;
+    try {
+        c = new srm_b200_ctx();
+        c->dim = dim;
+        c->shape = shape_kind;
+        c->device = device;
+        c->cap = capacity;
+        for (int a = 0; a < 3; ++a) {
+            c->box.L[a] = a < dim ? box_lengths[a] : 1.0;
+            c->box.half[a] = 0.5 * c->box.L[a];
+        }
+        c->init();
+    } catch (const CudaError& e) {
+        g_create_error = e.msg;
+        delete c;
+        return SRM_B200_CUDA_ERROR;
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        delete c;
+        return SRM_B200_CUDA_ERROR;
+    }
+    *out = c;
+    return SRM_B200_OK;
+}
+
+void srm_b200_destroy(srm_b200_ctx* ctx) { delete ctx; }
+
+const char* srm_b200_last_error(const srm_b200_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t srm_b200_count(const srm_b200_ctx* ctx) { return ctx ? ctx->n : 0; }
+
+int srm_b200_upload(srm_b200_ctx* c, int64_t n, const double* pos, const double* radius, const int32_t* id) {
+    return guarded(c, [&]() -> int {
+        if (n < 0 || n > c->cap) throw Invalid{"upload: n exceeds the context capacity"};
+        if (n > 0 && (!pos || !radius)) throw Invalid{"upload: null pointer"};
+        c->n = n;
+        if (n == 0) return SRM_B200_OK;
+        // stage through Q's buffers (scratch outside a generate call)
+        double* dpos = c->xblock[1];
+        SRM_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * n * c->dim, cudaMemcpyHostToDevice, c->stream));
+        SRM_CUDA(cudaMemcpyAsync(c->Q.r, radius, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        int32_t* did = nullptr;
+        if (id) {
+            SRM_CUDA(cudaMemcpyAsync(c->Q.id, id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+            did = c->Q.id;
+        }
+        if (c->dim == 2) k_unpack_soa<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, dpos, c->Q.r, did, c->P);
+        else k_unpack_soa<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, dpos, c->Q.r, did, c->P);
+        c->launched();
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_download(srm_b200_ctx* c, double* pos, double* radius, int32_t* id) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (n == 0) return SRM_B200_OK;
+        double* dpos = c->xblock[2];
+        if (c->dim == 2) k_pack_soa<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, dpos, c->S.r, c->S.id);
+        else k_pack_soa<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, dpos, c->S.r, c->S.id);
+        c->launched();
+        if (pos) SRM_CUDA(cudaMemcpyAsync(pos, dpos, sizeof(double) * n * c->dim, cudaMemcpyDeviceToHost, c->stream));
+        if (radius) SRM_CUDA(cudaMemcpyAsync(radius, c->S.r, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        if (id) SRM_CUDA(cudaMemcpyAsync(id, c->S.id, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_upload_records(srm_b200_ctx* c, int64_t n, const void* records, int64_t stride, int64_t off_id,
+                            int64_t off_pos, int64_t off_radius) {
+    return guarded(c, [&]() -> int {
+        if (n < 0 || n > c->cap) throw Invalid{"upload: n exceeds the context capacity"};
+        if (stride < 1) throw Invalid{"upload: bad stride"};
+        c->n = n;
+        if (n == 0) return SRM_B200_OK;
+        const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(stride);
+        if (bytes > c->rec_stage_bytes) {
+            cudaFree(c->rec_stage);
+            c->rec_stage = nullptr;
+            c->rec_stage = dalloc<char>(static_cast<int64_t>(bytes));
+            c->rec_stage_bytes = bytes;
+        }
+        SRM_CUDA(cudaMemcpyAsync(c->rec_stage, records, bytes, cudaMemcpyHostToDevice, c->stream));
+        if (c->dim == 2)
+            k_unpack_records<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->rec_stage, stride, off_id, off_pos, off_radius, c->P);
+        else
+            k_unpack_records<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->rec_stage, stride, off_id, off_pos, off_radius, c->P);
+        c->launched();
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_download_records(srm_b200_ctx* c, void* records, int64_t stride, int64_t off_id, int64_t off_pos,
+                              int64_t off_radius) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (n == 0) return SRM_B200_OK;
+        const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(stride);
+        if (bytes > c->rec_stage_bytes) {
+            cudaFree(c->rec_stage);
+            c->rec_stage = nullptr;
+            c->rec_stage = dalloc<char>(static_cast<int64_t>(bytes));
+            c->rec_stage_bytes = bytes;
+        }
+        // keep any bytes of the records we do not own (padding, extra fields)
+        SRM_CUDA(cudaMemcpyAsync(c->rec_stage, records, bytes, cudaMemcpyHostToDevice, c->stream));
+        if (c->dim == 2)
+            k_pack_records<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, c->rec_stage, stride, off_id, off_pos, off_radius);
+        else
+            k_pack_records<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, c->rec_stage, stride, off_id, off_pos, off_radius);
+        c->launched();
+        SRM_CUDA(cudaMemcpyAsync(records, c->rec_stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_grid_dims(srm_b200_ctx* c, double cell_size, double max_radius, double slack, int32_t* dims_out,
+                       double* edge_out, int64_t* ncells_out) {
+    return guarded(c, [&]() -> int {
+        const GridParams g = c->make_grid(cell_size, 0.0, 0.0);
+        if (max_radius >= 0.0) {
+            const double min_safe = 2.0 * max_radius + slack;  // cell_grid.hpp:290-292
+            if (cell_size < min_safe) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
+        }
+        for (int a = 0; a < c->dim; ++a) {
+            if (dims_out) dims_out[a] = g.dims[a];
+            if (edge_out) edge_out[a] = g.edge[a];
+        }
+        if (ncells_out) *ncells_out = g.ncells;
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_grid_build(srm_b200_ctx* c, double cell_size, uint32_t* keys_out, int32_t* order_out,
+                        int64_t* cell_start_out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        const GridParams g = c->make_grid(cell_size, 0.0, 0.0);
+        c->set_grid(g);
+        if (n > 0) {
+            c->grid_build(c->P);
+            if (keys_out) {
+                k_keys_by_slot<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S.slot, c->skey, c->key);
+                c->launched();
+                SRM_CUDA(cudaMemcpyAsync(keys_out, c->key, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+            }
+            if (order_out)
+                SRM_CUDA(cudaMemcpyAsync(order_out, c->S.slot, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+            c->copy_state(c->S, c->P);  // keep the state physically sorted
+        } else {
+            SRM_CUDA(cudaMemsetAsync(c->cell_start, 0, sizeof(int64_t) * (g.ncells + 1), c->stream));
+        }
+        if (cell_start_out)
+            SRM_CUDA(cudaMemcpyAsync(cell_start_out, c->cell_start, sizeof(int64_t) * (g.ncells + 1),
+                                     cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_overlap_stats(srm_b200_ctx* c, double cell_size, srm_b200_round_stats* out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        srm_b200_round_stats o{0, 0.0, 0, 0};
+        if (n > 0) {
+            const double mr = c->max_radius(c->P);
+            const GridParams g = c->make_grid(cell_size, mr, 0.0);
+            c->set_grid(g);
+            c->grid_build(c->P);
+            c->copy_state(c->S, c->P);
+            SRM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(StatsDev), c->stream));
+            {
+                srm_b200_ctx::FamScope fs(c, 3);
+                if (c->dim == 2)
+                    k_overlap_full<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, 1, c->stats);
+                else
+                    k_overlap_full<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, 1, c->stats);
+                c->launched();
+            }
+            o = c->read_stats(true);
+            o.movers = 0;
+        }
+        if (out) *out = o;
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_round(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint64_t key, uint32_t round_id,
+                   uint32_t iteration, int with_candidates, uint8_t* accepted_out, srm_b200_round_stats* out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (n_l < 1) throw Invalid{"params: n_l must be >= 1"};
+        if (!(c_m >= 0.0)) throw Invalid{"params: c_m must be >= 0"};
+        srm_b200_round_stats o{0, 0.0, with_candidates ? 0 : -1, 0};
+        if (n > 0) {
+            const double mr = c->max_radius(c->P);
+            const GridParams g = c->make_grid(cell_size, mr, 2.0 * c_m);
+            // the reference scans the 3^d cells of the trial position, which is only
+            // complete under CellGrid's safety bound (cell_grid.hpp:288-293)
+            if (cell_size < 2.0 * mr + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
+            c->set_grid(g);
+            c->round(c->P, c_m, n_l, key, round_id, iteration, true, with_candidates != 0);
+            if (accepted_out) {
+                k_acc_by_slot<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P.slot, c->acc, reinterpret_cast<uint8_t*>(c->perm));
+                c->launched();
+                SRM_CUDA(cudaMemcpyAsync(accepted_out, c->perm, n, cudaMemcpyDeviceToHost, c->stream));
+            }
+            o = c->read_stats(with_candidates != 0);
+        }
+        if (out) *out = o;
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_rounds(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint64_t key, uint32_t first_round,
+                    uint32_t iteration, int rounds, srm_b200_round_stats* last) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (n_l < 1) throw Invalid{"params: n_l must be >= 1"};
+        srm_b200_round_stats o{0, 0.0, -1, 0};
+        if (n > 0 && rounds > 0) {
+            const double mr = c->max_radius(c->P);
+            if (cell_size < 2.0 * mr + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
+            const GridParams g = c->make_grid(cell_size, mr, 2.0 * c_m);
+            c->set_grid(g);
+            for (int k = 0; k < rounds; ++k) c->round(c->P, c_m, n_l, key, first_round + k, iteration, true, false);
+            o = c->read_stats(false);
+        }
+        if (last) *last = o;
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_relax_sweeps(srm_b200_ctx* c, double c_m, double c_r, int n_l, int sweeps, uint64_t key) {
+    (void)c_r;  // rotation rate is ignored by disks/spheres (shape.hpp:500-502)
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (n == 0 || sweeps < 1) return SRM_B200_OK;  // engine.hpp:115
+        if (n_l < 1) throw Invalid{"params: n_l must be >= 1"};
+        const double max_r = c->max_radius(c->P);
+        const double cs = 2.5 * max_r + c_m;  // engine.hpp:116-117
+        const GridParams g = c->make_grid(cs, max_r, 2.0 * c_m);
+        if (cs < 2.0 * max_r + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
+        c->set_grid(g);
+        for (int k = 0; k < sweeps; ++k) c->round(c->P, c_m, n_l, key, static_cast<uint32_t>(k), 0u, false, false);
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_swell_all(srm_b200_ctx* c, double c_w) {
+    return guarded(c, [&]() -> int {
+        if (c->n > 0) c->scale_radius(c->P, 1.0 + c_w);  // engine.hpp:136
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_reorder_by_locality(srm_b200_ctx* c, double cell_size, int32_t* remap_out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        const GridParams g = c->make_grid(cell_size, 0.0, 0.0);
+        if (n == 0) return SRM_B200_OK;
+        c->set_grid(g);
+        c->grid_build(c->P);
+        // old slots of the sorted order are S.slot; remap[old] = new
+        int32_t* remap_dev = c->perm;
+        SRM_CUDA(cudaMemcpyAsync(c->Q.slot, c->S.slot, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+        k_assign_slots<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, remap_dev, c->Q.slot);
+        c->launched();
+        c->copy_state(c->S, c->P);
+        if (remap_out) SRM_CUDA(cudaMemcpyAsync(remap_out, remap_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_max_bounding_radius(srm_b200_ctx* c, double* out) {
+    return guarded(c, [&]() -> int {
+        *out = c->n > 0 ? c->max_radius(c->P) : 0.0;
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_volume_fraction(srm_b200_ctx* c, double* out) {
+    return guarded(c, [&]() -> int {
+        *out = c->n > 0 ? c->volume_fraction(c->P) : 0.0;
+        return SRM_B200_OK;
+    });
+}
+
+// engine.hpp:176-260 srm_generate
+int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t iteration_count_in,
+                      srm_b200_progress_fn progress, void* user, srm_b200_generate_out* out) {
+    return guarded(c, [&]() -> int {
+        if (!params) throw Invalid{"params: null"};
+        const srm_b200_params p = *params;
+        validate_params(p);
+        const int N = c->dim;
+        double min_len = c->box.L[0];
+        for (int a = 1; a < N; ++a) min_len = std::min(min_len, c->box.L[a]);
+        if (!(p.c_m < 0.5 * min_len))
+            throw Invalid{"srm_generate: c_m must be below half the shortest box length"};
+        if (c->n == 0) throw Invalid{"srm_generate: initial snapshot has no particles"};
+
+        double f = c->volume_fraction(c->P);
+        const double stop = p.f_target * (1.0 - 1e-12);
+        if (f < stop && p.c_w == 0.0)
+            throw Invalid{"srm_generate: c_w must be positive to grow toward f_target"};
+
+        const auto t_start = std::chrono::steady_clock::now();
+        int64_t done = 0, accepted_iters = 0, rounds = 0, shakes = 0;
+        int accepted_since_reorder = 0;
+        int status = SRM_B200_OK;
+        while (f < stop) {
+            if (done >= p.max_iterations) {
+                status = SRM_B200_ITERATION_LIMIT;
+                break;
+            }
+            ++done;
+            const int64_t it = iteration_count_in + done;
+            double factor = 1.0 + p.c_w;
+            if (f * std::pow(factor, N) > p.f_target) factor = std::pow(p.f_target / f, 1.0 / N);
+
+            const double max_r = c->max_radius(c->P);
+            const double cs = 2.5 * max_r + p.c_m;
+            if (cs < 2.0 * (max_r * factor) + p.c_m)  // CellGrid(box, cs, max_r*factor, c_m)
+                throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
+            const GridParams gq = c->make_grid(cs, max_r * factor, 2.0 * p.c_m);
+            c->set_grid(gq);
+
+            c->copy_state(c->P, c->Q);
+            c->scale_radius(c->Q, factor);
+
+            bool success = false;
+            int rounds_this = 0;
+            for (int k = 0; k < p.n_k; ++k) {
+                c->round(c->Q, p.c_m, p.n_l, p.seed, static_cast<uint32_t>(k), static_cast<uint32_t>(it), true, false);
+                ++rounds;
+                ++rounds_this;
+                const srm_b200_round_stats st = c->read_stats(false);
+                if (st.overlap_pairs == 0) {
+                    success = true;
+                    break;
+                }
+            }
+            if (success) {
+                c->copy_state(c->Q, c->P);
+                f = c->volume_fraction(c->P);
+                ++accepted_iters;
+                if (p.reorder_period > 0 && ++accepted_since_reorder >= p.reorder_period) {
+                    accepted_since_reorder = 0;
+                    // reorder_by_locality(P, grid) (engine.hpp:239-243)
+                    c->grid_build(c->P);
+                    SRM_CUDA(cudaMemcpyAsync(c->Q.slot, c->S.slot, sizeof(int32_t) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+                    k_assign_slots<<<blocks_for(c->n, 256), 256, 0, c->stream>>>(c->n, c->S, nullptr, c->Q.slot);
+                    c->launched();
+                    c->copy_state(c->S, c->P);
+                }
+            } else {
+                // shake: n_k sweeps on the pre-swell state with the same grid (engine.hpp:244-249)
+                const GridParams gp_ = c->make_grid(cs, max_r, 2.0 * p.c_m);
+                c->set_grid(gp_);
+                for (int k = 0; k < p.n_k; ++k) {
+                    c->round(c->P, p.c_m, p.n_l, p.seed, static_cast<uint32_t>(p.n_k + k), static_cast<uint32_t>(it), false, false);
+                    ++shakes;
+                }
+                c->sync();
+                rounds_this = p.n_k;
+            }
+            if (progress) {
+                const std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t_start;
+                srm_b200_progress_record rec{it, f, success ? 1 : 0, dt.count(), rounds_this};
+                progress(&rec, user);
+            }
+        }
+        c->sync();
+        if (out) {
+            out->status = status;
+            out->volume_fraction = f;
+            out->iteration_count = iteration_count_in + done;
+            out->accepted_iterations = accepted_iters;
+            out->rounds = rounds;
+            out->shake_rounds = shakes;
+        }
+        return status;
+    });
+}
+
+int64_t srm_b200_launch_count(const srm_b200_ctx* c) { return c ? c->launches : 0; }
+void srm_b200_reset_launch_count(srm_b200_ctx* c) {
+    if (c) c->launches = 0;
+}
+
+int srm_b200_timing_enable(srm_b200_ctx* c, int enable) {
+    return guarded(c, [&]() -> int {
+        c->sync();
+        c->harvest_timing();
+        c->timing = enable != 0;
+        for (int k = 0; k < SRM_B200_NPHASE; ++k) {
+            c->ms[k] = 0.0;
+            c->calls[k] = 0;
+        }
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_timing_get(srm_b200_ctx* c, double* ms, int64_t* calls) {
+    return guarded(c, [&]() -> int {
+        c->sync();
+        c->harvest_timing();
+        for (int k = 0; k < SRM_B200_NPHASE; ++k) {
+            if (ms) ms[k] = c->ms[k];
+            if (calls) calls[k] = c->calls[k];
+        }
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_sync(srm_b200_ctx* c) {
+    return guarded(c, [&]() -> int {
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_stopwatch(srm_b200_ctx* c, int op, double* ms) {
+    return guarded(c, [&]() -> int {
+        if (!c->sw_start) {
+            SRM_CUDA(cudaEventCreate(&c->sw_start));
+            SRM_CUDA(cudaEventCreate(&c->sw_stop));
+        }
+        if (op == 0) {
+            SRM_CUDA(cudaEventRecord(c->sw_start, c->stream));
+        } else {
+            SRM_CUDA(cudaEventRecord(c->sw_stop, c->stream));
+            SRM_CUDA(cudaEventSynchronize(c->sw_stop));
+            float t = 0.f;
+            SRM_CUDA(cudaEventElapsedTime(&t, c->sw_start, c->sw_stop));
+            if (ms) *ms = t;
+        }
+        return SRM_B200_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// srm_rsa.cpp -- host-side initial-state generator: rsa_place (rsa.hpp:21-69).
+//
+// Random sequential adsorption is sequential by definition (each acceptance changes
+// the next candidate's test), so it stays on the host, as input generation whose time
+// is excluded from the metric.  It consumes std::mt19937_64 exactly as the reference's
+// Rng does (random.hpp:16-61), and its accept test is the reference predicate
+// (strictly non-touching, cell_grid.hpp:454-464), so the output is bit-identical to
+// srm::rsa_place for the same seed (pinned in tests/test_rsa.py).  The neighbour search
+// is its own flat cell list; any complete search yields the same decisions.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <random>
+#include <vector>
+
+#include "../../include/srm_b200.h"
+
+namespace {
+
+struct RsaGrid {
+    int dim;
+    int n[3] = {1, 1, 1};
+    double edge[3] = {1, 1, 1};
+    std::vector<int32_t> head, next;
+
+    int coord(int a, double p) const {
+        int i = static_cast<int>(std::floor(p / edge[a]));
+        i %= n[a];
+        if (i < 0) i += n[a];
+        return i;
+    }
+};
+
+inline double min_image_dist2(int dim, const double* L, const double* a, const double* b) {
+    double s = 0.0;
+    for (int k = 0; k < dim; ++k) {
+        double d = a[k] - b[k];
+        const double half = 0.5 * L[k];
+        if (d > half) d -= L[k];
+        if (d < -half) d += L[k];
+        s += d * d;
+    }
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t srm_b200_mix_seed(uint64_t seed, uint64_t stream) {
+    // random.hpp:84-89 splitmix64 step
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+int srm_b200_rsa_place(int dim, const double* L, int64_t count, const double* radii, int64_t max_attempts,
+                       uint64_t seed, double* pos_out, int32_t* id_out, int64_t* placed_out) {
+    if (placed_out) *placed_out = 0;
+    if (dim != 2 && dim != 3) return SRM_B200_INVALID;
+    if (count < 1) return SRM_B200_INVALID;  // rsa.hpp:22 need at least one particle
+    double max_r = radii[0];
+    for (int64_t i = 1; i < count; ++i) max_r = std::max(max_r, radii[i]);
+    double min_len = L[0];
+    for (int a = 1; a < dim; ++a) min_len = std::min(min_len, L[a]);
+    for (int64_t i = 0; i < count; ++i)
+        if (!(radii[i] > 0.0)) return SRM_B200_INVALID;      // rsa.hpp:26-27
+    if (!(max_r < min_len / 4.0)) return SRM_B200_INVALID;  // rsa.hpp:28-29
+
+    RsaGrid g;
+    g.dim = dim;
+    int64_t ncells = 1;
+    for (int a = 0; a < dim; ++a) {
+        int k = static_cast<int>(std::floor(L[a] / (2.0 * max_r)));
+        k = std::max(1, std::min(k, 1 << 12));
+        g.n[a] = k;
+        g.edge[a] = L[a] / k;
+        ncells *= k;
+    }
+    g.head.assign(static_cast<size_t>(ncells), -1);
+    g.next.assign(static_cast<size_t>(count), -1);
+
+    std::mt19937_64 gen(seed);
+    auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+
+    double cand[3];
+    for (int64_t i = 0; i < count; ++i) {
+        const double ri = radii[i];
+        bool accepted = false;
+        for (int64_t attempt = 0; attempt < max_attempts; ++attempt) {
+            for (int a = 0; a < dim; ++a) cand[a] = uniform() * L[a];  // random.hpp:56-61
+            for (int a = 0; a < dim; ++a) {                             // geometry.hpp:107-114
+                if (cand[a] < 0.0) cand[a] += L[a];
+                if (cand[a] >= L[a]) cand[a] -= L[a];
+            }
+            int c[3] = {0, 0, 0};
+            for (int a = 0; a < dim; ++a) c[a] = g.coord(a, cand[a]);
+            bool hit = false;
+            int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+            for (int a = 0; a < dim; ++a) {
+                if (g.n[a] <= 3) { lo[a] = 0; hi[a] = g.n[a] - 1; }
+                else { lo[a] = c[a] - 1; hi[a] = c[a] + 1; }
+            }
+            for (int zz = lo[2]; zz <= hi[2] && !hit; ++zz) {
+                int z = dim == 3 ? ((zz % g.n[2]) + g.n[2]) % g.n[2] : 0;
+                for (int yy = lo[1]; yy <= hi[1] && !hit; ++yy) {
+                    int y = ((yy % g.n[1]) + g.n[1]) % g.n[1];
+                    for (int xx = lo[0]; xx <= hi[0] && !hit; ++xx) {
+                        int x = ((xx % g.n[0]) + g.n[0]) % g.n[0];
+                        const int64_t cell = (static_cast<int64_t>(z) * g.n[1] + y) * g.n[0] + x;
+                        for (int32_t j = g.head[cell]; j >= 0; j = g.next[j]) {
+                            const double rr = ri + radii[j];
+                            if (min_image_dist2(dim, L, cand, pos_out + static_cast<int64_t>(j) * dim) <= rr * rr) {
+                                hit = true;
+                                break;
+                            }
+                        }
+                    }
+                }
+            }
+            if (!hit) {
+                accepted = true;
+                break;
+            }
+        }
+        if (!accepted) {
+            if (placed_out) *placed_out = i;
+            return SRM_B200_PLACEMENT_FAILURE;
+        }
+        for (int a = 0; a < dim; ++a) pos_out[i * dim + a] = cand[a];
+        if (id_out) id_out[i] = static_cast<int32_t>(i);
+        int c[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a) c[a] = g.coord(a, cand[a]);
+        const int64_t cell = (static_cast<int64_t>(c[2]) * g.n[1] + c[1]) * g.n[0] + c[0];
+        g.next[i] = g.head[cell];
+        g.head[cell] = static_cast<int32_t>(i);
+    }
+    if (placed_out) *placed_out = count;
+    return SRM_B200_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+reference, on the same seeded inputs.  Bit-exact for keys, order, offsets, counts,
+accept decisions and positions (the kernels are compiled with --fmad=false and use
+only correctly rounded operations); max penetration bit-exact too."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import orc
+import paper_2605_18254_b200 as srm
+from paper_2605_18254_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(L, pos, r, ids=None):
+    ctx = srm.Context(L, max(len(r), 1))
+    ctx.upload(pos, r, ids)
+    return ctx
+
+
+def _rsa_state(dim, n, f, seed, L=None, poly=False):
+    L = L or [1.0] * dim
+    unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
+    if poly:
+        rng = np.random.default_rng(seed)
+        rel = np.clip(rng.lognormal(-0.5 * np.log(1.04), np.sqrt(np.log(1.04)), n), 0.5, 2.0)
+        scale = (f * np.prod(L) / (unit * np.sum(rel ** dim))) ** (1.0 / dim)
+        r = rel * scale
+    else:
+        r = np.full(n, (f * np.prod(L) / (n * unit)) ** (1.0 / dim))
+    pos, ids = srm.rsa_place(r, L, 10000, seed)
+    return L, pos, r, ids
+
+
+# ---- primitives -------------------------------------------------------------------
+def test_philox_device_vs_curand_and_oracle():
+    rng = np.random.default_rng(1)
+    n = 4096
+    ctr = rng.integers(0, 2**32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 2**32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+    ctr[0] = 0; key[0] = 0
+    mine = np.zeros((n, 4), np.uint32)
+    cur = np.zeros((n, 4), np.uint32)
+    assert _native.lib().srm_b200_selftest_philox(n, orc.P(ctr), orc.P(key), orc.P(mine), orc.P(cur)) == 0
+    assert np.array_equal(mine, cur)
+    for i in range(0, n, 97):
+        assert np.array_equal(mine[i], orc.o_philox(ctr[i], key[i]))
+    assert tuple(mine[0]) == (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_unit_vectors_bitwise(dim):
+    n = 3000
+    slot = np.arange(n, dtype=np.uint32) * 7919
+    att = (np.arange(n, dtype=np.uint32) % 11)
+    out = np.zeros((n, dim))
+    seed = 0xDEADBEEF12345678
+    assert _native.lib().srm_b200_selftest_unit_vectors(dim, seed, n, orc.P(slot), orc.P(att), 0, 5, 42,
+                                                         orc.P(out)) == 0
+    exp = np.array([orc.o_unit_vector(dim, seed, int(s), int(a), 0, 5, 42) for s, a in zip(slot, att)])
+    assert np.array_equal(out, exp)
+
+
+# ---- grid rebuild -------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n,cs,L", [
+    (2, 5000, 0.013, [1.0, 1.0]), (3, 20000, 0.02, [1.0, 1.0, 1.0]), (3, 3000, 0.4, [1.0, 1.0, 1.0]),
+    (2, 777, 0.05, [2.0, 1.0]), (3, 10000, 0.05, [1.0, 1.3, 0.7]), (2, 1, 0.1, [1.0, 1.0]),
+])
+def test_grid_build_bit_exact(dim, n, cs, L):
+    pos, r = orc.random_particles(n, dim, 0.001, 0.002, L, 21)
+    if n > 3:
+        pos[0, 0] = -1e-9
+        pos[1, 0] = np.nextafter(L[0], 0)
+        pos[2, :] = 0.0
+    with _ctx(L, pos, r) as ctx:
+        keys, order, cell_start = ctx.grid_build(cs)
+    k_o, dims, _ = orc.o_keys(dim, L, cs, pos)
+    assert np.array_equal(keys, k_o)
+    k_r, _ = orc.r_keys(dim, L, cs, pos)
+    assert np.array_equal(keys.astype(np.uint64), k_r)
+    o_order, o_cs = orc.o_sort(k_o, np.arange(n, dtype=np.int32), int(np.prod(dims)))
+    assert np.array_equal(order, o_order)
+    assert np.array_equal(cell_start, o_cs)
+    # == reorder_by_locality of the reference
+    _, _, _, remap = orc.r_reorder(dim, L, cs, pos, r, np.arange(n, dtype=np.int32))
+    assert np.array_equal(remap[order], np.arange(n))
+
+
+def test_reorder_by_locality_matches_reference():
+    L = [1.0, 1.0, 1.0]
+    pos, r = orc.random_particles(4000, 3, 0.001, 0.002, L, 5)
+    snap = srm.Snapshot(L, pos, r)
+    remap = srm.reorder_by_locality(snap, 0.07)
+    pos_r, r_r, ids_r, remap_r = orc.r_reorder(3, L, 0.07, pos, r, np.arange(4000, dtype=np.int32))
+    assert np.array_equal(remap, remap_r)
+    assert np.array_equal(snap.pos, pos_r) and np.array_equal(snap.radius, r_r)
+    assert np.array_equal(snap.id, ids_r)
+
+
+# ---- overlap reduction --------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n,rmin,rmax,seed", [(2, 200, 0.005, 0.02, 11), (3, 3000, 0.005, 0.02, 12),
+                                                  (2, 20000, 0.001, 0.004, 13), (3, 500, 0.0, 0.0, 14)])
+def test_overlap_stats_bit_exact(dim, n, rmin, rmax, seed):
+    L = [1.0] * dim
+    pos, r = orc.random_particles(n, dim, rmin, rmax, L, seed)
+    if rmax == 0.0:  # coincident points (contact at distance 0), duplicate ids ignored
+        r[:] = 0.001
+        pos[1] = pos[0]
+    cs = 2.5 * r.max()
+    with _ctx(L, pos, r) as ctx:
+        st = ctx.overlap_stats(cs)
+    o = orc.o_stats(dim, L, pos, r)
+    assert st.overlap_pairs == o.overlap_pairs
+    assert st.max_penetration == o.max_penetration
+    keys, dims, _ = orc.o_keys(dim, L, cs, pos)
+    assert st.candidate_pairs == orc.o_candidates(dim, dims, keys)
+    anyc, _ = orc.r_collisions(dim, L, cs, pos, r)
+    assert (st.overlap_pairs > 0) == anyc
+
+
+# ---- one round ------------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n,f,swell,cm_rel,n_l,seed", [
+    (2, 2000, 0.45, 1.03, 0.1, 10, 1),
+    (3, 3000, 0.3, 1.02, 0.1, 10, 2),
+    (3, 2000, 0.25, 1.06, 0.5, 8, 3),
+    (2, 1500, 0.6, 1.0, 0.05, 4, 4),
+    (3, 5000, 0.3, 1.0, 0.05, 1, 5),
+])
+def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed):
+    L, pos, r, ids = _rsa_state(dim, n, min(f, 0.55 if dim == 2 else 0.3), seed)
+    r = r * (f / min(f, 0.55 if dim == 2 else 0.3)) ** (1 / dim) * swell
+    c_m = cm_rel * r.max()
+    cs = 2.5 * r.max() / swell + c_m
+    key, round_id, it = 0x0123456789ABCDEF + seed, 3, 17
+    with _ctx(L, pos, r, ids) as ctx:
+        st, acc = ctx.round(cs, c_m, n_l, key, round_id, it, with_candidates=True)
+        pos_d, r_d, id_d = ctx.download()
+    xnew, acc_o = orc.o_round(dim, L, pos, r, ids, ids, c_m, n_l, key, round_id, it)
+    assert np.array_equal(acc, acc_o)
+    assert np.array_equal(pos_d, xnew)
+    assert np.array_equal(r_d, r) and np.array_equal(id_d, ids)
+    o = orc.o_stats(dim, L, xnew, r)
+    assert st.overlap_pairs == o.overlap_pairs
+    assert st.max_penetration == o.max_penetration
+    assert st.movers == int(np.sum(acc_o != 255))
+    keys, dims, _ = orc.o_keys(dim, L, cs, pos)
+    assert st.candidate_pairs == orc.o_candidates(dim, dims, keys)
+
+
+def test_round_polydisperse_bit_exact():
+    L, pos, r, ids = _rsa_state(3, 4000, 0.3, 9, L=[1.0, 1.0, 1.0], poly=True)
+    r = r * 1.04
+    c_m = 0.1 * np.mean(r)
+    cs = 2.5 * r.max() / 1.04 + c_m
+    with _ctx(L, pos, r, ids) as ctx:
+        st, acc = ctx.round(cs, c_m, 10, 99, 0, 1)
+        pos_d, _, _ = ctx.download()
+    xnew, acc_o = orc.o_round(3, L, pos, r, ids, ids, c_m, 10, 99, 0, 1)
+    assert np.array_equal(acc, acc_o) and np.array_equal(pos_d, xnew)
+    assert st.overlap_pairs == orc.o_stats(3, L, xnew, r).overlap_pairs
+
+
+def test_rounds_are_deterministic_and_chain():
+    L, pos, r, ids = _rsa_state(3, 6000, 0.3, 7)
+    r = r * 1.02
+    c_m = 0.1 * r[0]
+    cs = 2.5 * r[0] / 1.02 + c_m
+    outs = []
+    for _ in range(2):
+        with _ctx(L, pos, r, ids) as ctx:
+            ctx.rounds(cs, c_m, 10, 5, 0, 1, 3)
+            outs.append(ctx.download()[0])
+    assert np.array_equal(outs[0], outs[1])
+    x = pos
+    for k in range(3):
+        x, _ = orc.o_round(3, L, x, r, ids, ids, c_m, 10, 5, k, 1)
+    assert np.array_equal(outs[0], x)
+
+
+def test_caged_particle_reverts():
+    pos = orc.arr([[0.5, 0.5]] + [[0.5 + 0.2000000001 * np.cos(k * np.pi / 3),
+                                     0.5 + 0.2000000001 * np.sin(k * np.pi / 3)] for k in range(6)])
+    r = np.full(7, 0.1)
+    with _ctx([1.0, 1.0], pos, r) as ctx:
+        _, acc = ctx.round(0.25, 0.05, 1, 99, 0, 0)
+        p, _, _ = ctx.download()
+    assert acc[0] == 255 and np.array_equal(p[0], pos[0])
+
+
+def test_single_particle_moves_c_m():
+    with _ctx([1.0, 1.0], orc.arr([[0.5, 0.5]]), orc.arr([0.1])) as ctx:
+        _, acc = ctx.round(0.25, 0.05, 4, 17, 0, 0)
+        p, _, _ = ctx.download()
+    assert acc[0] == 0
+    assert np.linalg.norm(p[0] - [0.5, 0.5]) == pytest.approx(0.05, rel=1e-12)
+
+
+def test_records_roundtrip():
+    # std::vector<srm::Particle<3>> layout: int id @0, double pos[3] @8, radius @32, stride 40
+    dt = np.dtype({"names": ["id", "pos", "radius"], "formats": ["<i4", ("<f8", 3), "<f8"],
+                   "offsets": [0, 8, 32], "itemsize": 40})
+    L = [1.0, 1.0, 1.0]
+    pos, r = orc.random_particles(1000, 3, 0.001, 0.002, L, 3)
+    rec = np.zeros(1000, dt)
+    rec["id"] = np.arange(1000)[::-1]
+    rec["pos"] = pos
+    rec["radius"] = r
+    ctx = srm.Context(L, 1000)
+    ctx.upload_records(rec, 0, 8, 32)
+    ctx.grid_build(0.05)  # permutes the device copy
+    out = np.zeros(1000, dt)
+    ctx.download_records(out, 0, 8, 32)
+    ctx.close()
+    assert np.array_equal(out["pos"], pos) and np.array_equal(out["radius"], r)
+    assert np.array_equal(out["id"], rec["id"])
