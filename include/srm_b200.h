@@ -194,6 +194,11 @@ int srm_b200_sync(srm_b200_ctx* ctx);
 /* CUDA-event stopwatch on the context stream: op 0 records the start event, op 1
  * records the stop event, waits for it and writes the elapsed device milliseconds. */
 int srm_b200_stopwatch(srm_b200_ctx* ctx, int op, double* ms);
+/* Diagnostics of the last round whose statistics were read: info[0] attempt-0 rejects,
+ * [1] shared-memory bricks that fell back to global memory, [2] bricks launched (0 =
+ * untiled), [3] brick capacity (particles), [4] brick shared memory bytes, [5] brick
+ * width in cells. */
+int srm_b200_last_round_info(srm_b200_ctx* ctx, int64_t* info);
 
 /* ---- self tests of the device primitives (no reference counterpart) ------------------ */
 /* the hand-written device Philox4x32-10 next to CUDA's curand_Philox4x32_10 */

@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -14,6 +15,7 @@
 
 #include "../../include/srm_b200.h"
 #include "srm_kernels.cuh"
+#include "srm_tiles.cuh"
 
 using namespace srmb;
 
@@ -69,6 +71,9 @@ struct srm_b200_ctx {
     uint32_t* key = nullptr;
     uint32_t* skey = nullptr;
     int32_t* perm = nullptr;
+    int32_t* active = nullptr;  // attempt-0 reject list
+    TileParams* tpp = nullptr;
+    TileParams ht{};
     uint8_t* acc = nullptr;
     int32_t* nbr = nullptr;
     uint8_t* nbr_cnt = nullptr;
@@ -109,6 +114,9 @@ struct srm_b200_ctx {
     bool hg_set = false;
 
     cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
+    bool force_global = false;  // SRM_B200_NO_TILES=1: phase 0 without shared-memory bricks
+    int64_t last_fallback_tiles = 0;
+    int64_t last_rejected0 = 0;
 
     // ---------------------------------------------------------------------------
     cudaEvent_t take_event() {
@@ -189,6 +197,11 @@ struct srm_b200_ctx {
         nbr_cnt = dalloc<uint8_t>(cap);
         gp = dalloc<GridParams>(1);
         rp = dalloc<RoundParams>(1);
+        tpp = dalloc<TileParams>(1);
+        if (const char* e = std::getenv("SRM_B200_NO_TILES")) force_global = e[0] == '1';
+        active = dalloc<int32_t>(cap);
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -206,7 +219,7 @@ struct srm_b200_ctx {
         free_state(S);
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc); cudaFree(nbr);
         cudaFree(nbr_cnt); cudaFree(count); cudaFree(cell_start); cudaFree(partial);
-        cudaFree(gp); cudaFree(rp); cudaFree(stats); cudaFree(red_part_sum);
+        cudaFree(gp); cudaFree(rp); cudaFree(tpp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -264,12 +277,72 @@ struct srm_b200_ctx {
         cell_cap = c;
     }
 
+    // Brick decomposition for k_phase0_tiled: bricks of ~256 particles, staged halo of
+    // near_s cells, capacity with a Poisson margin; disabled when the stencil is too wide.
+    TileParams make_tiles(const GridParams& g) const {
+        TileParams tp{};
+        tp.enabled = 0;
+        if (n == 0) return tp;
+        const double occ = static_cast<double>(n) / static_cast<double>(g.ncells);
+        int Bt = std::max(1, static_cast<int>(std::lround(std::pow(256.0 / std::max(occ, 1e-3), 1.0 / dim))));
+        for (; Bt >= 1; --Bt) {
+            int nst[3];
+            int64_t ntiles = 1;
+            int ncr = 1;
+            bool ok = true;
+            double ext = 0.0;
+            for (int a = 0; a < 3; ++a) {
+                AxisTile A{};
+                if (a >= dim) {
+                    A.full = 1; A.all = 1; A.B = 1; A.ntile = 1; A.s = 0;
+                    nst[a] = 1;
+                } else {
+                    const int s = g.near_s[a], d = g.dims[a];
+                    A.all = s < 0 ? 1 : 0;
+                    A.s = s < 0 ? 0 : s;
+                    if (A.all || Bt + 2 * s >= d) {
+                        A.full = 1; A.B = d; A.ntile = 1; nst[a] = d;
+                        ext = std::max(ext, box.L[a]);
+                    } else {
+                        A.full = 0; A.B = Bt; A.ntile = (d + Bt - 1) / Bt; nst[a] = Bt + 2 * s;
+                        ext = std::max(ext, nst[a] * g.edge[a]);
+                    }
+                    if (!A.all && 2 * A.s + 1 > 16) ok = false;
+                    if (A.all && a > 0 && d > 16) ok = false;
+                    if (a > 0) ncr *= A.B;
+                }
+                tp.ax[a] = A;
+                ntiles *= A.ntile;
+            }
+            const int rows = nst[1] * nst[2];
+            if (!ok || rows > kMaxRows || ncr > kTileThreads) continue;
+            const double mean = occ * nst[0] * nst[1] * nst[2];
+            int capv = static_cast<int>(std::ceil(mean * 1.3 + 4.0 * std::sqrt(mean) + 32.0));
+            capv = (capv + 31) / 32 * 32;
+            const int64_t smem = static_cast<int64_t>(capv) * (8 * (2 * dim + 1) + 16 + 8) +
+                                 static_cast<int64_t>(rows) * (nst[0] + 1) * 4;
+            if (smem > kTileSmemMax) continue;
+            tp.ntiles = ntiles;
+            tp.cap = capv;
+            for (int a = 0; a < 3; ++a) tp.nst_max[a] = nst[a];
+            tp.margin = static_cast<float>(16.0 * std::ldexp(1.0, -24) * ext);
+            tp.extra_f = static_cast<float>(g.extra);
+            tp.smem_bytes = static_cast<int32_t>(smem);
+            tp.enabled = 1;
+            return tp;
+        }
+        return tp;
+    }
+
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
         k_set_grid<<<1, 1, 0, stream>>>(gp, g);
         launched();
         hg = g;
         hg_set = true;
+        ht = make_tiles(g);
+        k_set_tiles<<<1, 1, 0, stream>>>(tpp, ht);
+        launched();
     }
 
     void set_round(double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration) {
@@ -318,29 +391,43 @@ struct srm_b200_ctx {
         const int nb = blocks_for(n, 256);
         {
             FamScope fs(this, 1);
-            if (dim == 2)
-                k_phase0<2><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
-            else
-                k_phase0<3><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+            if (ht.enabled && !force_global) {
+                const int grid = static_cast<int>(std::min<int64_t>(ht.ntiles, 2147483647));
+                if (dim == 2)
+                    k_phase0_tiled<2><<<grid, kTileThreads, ht.smem_bytes, stream>>>(S, T, box, gp, tpp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                else
+                    k_phase0_tiled<3><<<grid, kTileThreads, ht.smem_bytes, stream>>>(S, T, box, gp, tpp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+            } else {
+                if (dim == 2)
+                    k_phase0<2><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                else
+                    k_phase0<3><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+            }
             launched();
         }
+        const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
         if (n_l > 1) {
             FamScope fs(this, 2);
             for (int l = 1; l < n_l; ++l) {
                 if (dim == 2)
-                    k_phase<2><<<nb, 256, 0, stream>>>(n, l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+                    k_phase_list<2><<<lb, 256, 0, stream>>>(l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
                 else
-                    k_phase<3><<<nb, 256, 0, stream>>>(n, l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, stats);
+                    k_phase_list<3><<<lb, 256, 0, stream>>>(l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
             }
             launched(n_l - 1);
         }
         if (with_stats) {
             FamScope fs(this, 3);
             if (dim == 2)
-                k_stats<2><<<nb, 256, 0, stream>>>(n, S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, with_candidates ? 1 : 0, stats);
+                k_stats_list<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
             else
-                k_stats<3><<<nb, 256, 0, stream>>>(n, S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, with_candidates ? 1 : 0, stats);
+                k_stats_list<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
             launched();
+            if (with_candidates) {
+                if (dim == 2) k_candidates<2><<<nb, 256, 0, stream>>>(n, gp, cell_start, skey, stats);
+                else k_candidates<3><<<nb, 256, 0, stream>>>(n, gp, cell_start, skey, stats);
+                launched();
+            }
         }
     }
 
@@ -353,7 +440,9 @@ struct srm_b200_ctx {
         std::memcpy(&pen, &h_stats->pen_bits, sizeof(double));
         o.max_penetration = pen;
         o.candidate_pairs = with_candidates ? static_cast<int64_t>(h_stats->candidate_pairs) : -1;
-        o.movers = static_cast<int64_t>(h_stats->movers);
+        o.movers = n - static_cast<int64_t>(h_stats->nonmovers);
+        last_fallback_tiles = static_cast<int64_t>(h_stats->fallback_tiles);
+        last_rejected0 = static_cast<int64_t>(h_stats->active_count);
         return o;
     }
 
@@ -881,6 +970,18 @@ int srm_b200_timing_get(srm_b200_ctx* c, double* ms, int64_t* calls) {
 int srm_b200_sync(srm_b200_ctx* c) {
     return guarded(c, [&]() -> int {
         c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
+    return guarded(c, [&]() -> int {
+        info[0] = c->last_rejected0;
+        info[1] = c->last_fallback_tiles;
+        info[2] = c->ht.enabled && !c->force_global ? c->ht.ntiles : 0;
+        info[3] = c->ht.enabled ? c->ht.cap : 0;
+        info[4] = c->ht.enabled ? c->ht.smem_bytes : 0;
+        info[5] = c->ht.enabled ? c->ht.ax[0].B : 0;
         return SRM_B200_OK;
     });
 }

@@ -46,8 +46,10 @@ struct StatsDev {
     unsigned long long overlap_pairs;
     unsigned long long pen_bits;  // max penetration as the bits of a non-negative double
     unsigned long long candidate_pairs;
-    unsigned long long movers;
-    unsigned long long rejected[64];  // rejected after phase l (early exit of later phases)
+    unsigned long long nonmovers;     // particles that kept their round-start position
+    unsigned long long active_count;  // length of the attempt-0 reject list
+    unsigned long long fallback_tiles;  // phase-0 tiles that overflowed shared memory
+    unsigned long long rejected[256];  // rejected after phase l (early exit of later phases)
 };
 
 __device__ __forceinline__ double near_cut(double ri, double rj, double extra) {
@@ -295,8 +297,66 @@ __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
     for (int a = 0; a < D; ++a) p[a] = S.x[a][i];
 }
 
-// Migrate attempt 0 fused with the near-list build.  S = sorted round-start state
+// Rejected particles of attempt 0 are appended to the active list (warp-aggregated).
+__device__ __forceinline__ void push_active(bool rejected, int64_t i, int32_t* __restrict__ active,
+                                            StatsDev* stats) {
+    const unsigned full = __activemask();
+    const unsigned m = __ballot_sync(full, rejected);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(&stats->active_count, (unsigned long long)__popc(m));
+    base = __shfl_sync(full, base, leader);
+    if (rejected) active[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
+}
+
+// Migrate attempt 0 fused with the near-list build for one particle, straight from
+// global memory (the fallback of the tiled kernel).  S = sorted round-start state
 // (read only), T = output state (sorted order): T.x = new positions, T.r/id/slot copied.
+template <int D>
+__device__ __forceinline__ bool phase0_global(int64_t i, const State& S, const State& T, const Box& box,
+                                              const GridParams& g, const RoundParams& rp,
+                                              const int64_t* __restrict__ cs,
+                                              const uint32_t* __restrict__ skey,
+                                              uint8_t* __restrict__ acc, int32_t* __restrict__ nbr,
+                                              uint8_t* __restrict__ nbr_cnt) {
+    double xi[D], p[D];
+    load_pos<D>(S, i, xi);
+    const double ri = S.r[i];
+    const int32_t idi = S.id[i];
+    const int32_t sloti = S.slot[i];
+    propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sloti), 0u, p);
+    bool ok = true;
+    int nn = 0;
+    bool overflow = false;
+    int32_t* my = nbr + i * kNbrCap;
+    for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+        for (int64_t j = b; j < e; ++j) {
+            if (j == i) continue;
+            double xj[D];
+            load_pos<D>(S, j, xj);
+            const double rj = S.r[j];
+            if (dist2<D>(box, xi, xj) > near_cut(ri, rj, g.extra)) continue;
+            if (nn < kNbrCap) my[nn++] = static_cast<int32_t>(j);
+            else overflow = true;
+            if (!ok || S.id[j] == idi) continue;
+            if (sphere_overlap<D>(box, p, ri, xj, rj)) { ok = false; continue; }
+            double pj[D];
+            propose<D>(box, xj, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[j]), 0u, pj);
+            if (sphere_overlap<D>(box, p, ri, pj, rj)) ok = false;
+        }
+    });
+#pragma unroll
+    for (int a = 0; a < D; ++a) T.x[a][i] = ok ? p[a] : xi[a];
+    T.r[i] = ri;
+    T.id[i] = idi;
+    T.slot[i] = sloti;
+    acc[i] = ok ? 0 : kNotAccepted;
+    nbr_cnt[i] = overflow ? kOverflow : static_cast<uint8_t>(nn);
+    return !ok;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_phase0(int64_t n, State S, State T, Box box,
                                                 const GridParams* __restrict__ gp,
@@ -304,67 +364,37 @@ __global__ void __launch_bounds__(256) k_phase0(int64_t n, State S, State T, Box
                                                 const int64_t* __restrict__ cs,
                                                 const uint32_t* __restrict__ skey,
                                                 uint8_t* __restrict__ acc, int32_t* __restrict__ nbr,
-                                                uint8_t* __restrict__ nbr_cnt, StatsDev* stats) {
+                                                uint8_t* __restrict__ nbr_cnt, int32_t* __restrict__ active,
+                                                StatsDev* stats) {
     const GridParams g = *gp;
     const RoundParams rp = *rpp;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     bool rejected = false;
-    if (i < n) {
-        double xi[D], p[D];
-        load_pos<D>(S, i, xi);
-        const double ri = S.r[i];
-        const int32_t idi = S.id[i];
-        const int32_t sloti = S.slot[i];
-        propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sloti), 0u, p);
-        bool ok = true;
-        int nn = 0;
-        bool overflow = false;
-        int32_t* my = nbr + i * kNbrCap;
-        for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
-            for (int64_t j = b; j < e; ++j) {
-                if (j == i) continue;
-                double xj[D];
-                load_pos<D>(S, j, xj);
-                const double rj = S.r[j];
-                if (dist2<D>(box, xi, xj) > near_cut(ri, rj, g.extra)) continue;
-                if (nn < kNbrCap) my[nn++] = static_cast<int32_t>(j);
-                else overflow = true;
-                if (!ok || S.id[j] == idi) continue;
-                if (sphere_overlap<D>(box, p, ri, xj, rj)) { ok = false; continue; }
-                double pj[D];
-                propose<D>(box, xj, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[j]), 0u, pj);
-                if (sphere_overlap<D>(box, p, ri, pj, rj)) ok = false;
-            }
-        });
-#pragma unroll
-        for (int a = 0; a < D; ++a) T.x[a][i] = ok ? p[a] : xi[a];
-        T.r[i] = ri;
-        T.id[i] = idi;
-        T.slot[i] = sloti;
-        acc[i] = ok ? 0 : kNotAccepted;
-        nbr_cnt[i] = overflow ? kOverflow : static_cast<uint8_t>(nn);
-        rejected = !ok;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, rejected);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&stats->rejected[0], (unsigned long long)__popc(m));
+    if (i < n) rejected = phase0_global<D>(i, S, T, box, g, rp, cs, skey, acc, nbr, nbr_cnt);
+    push_active(rejected, i, active, stats);
 }
 
-// Migrate attempt l >= 1 for the still-active particles.
+
+// Migrate attempt l >= 1 for the still-active particles, over the
+// list of attempt-0 rejects (grid-stride; the list length is read on the device).
 template <int D>
-__global__ void __launch_bounds__(256) k_phase(int64_t n, int l, State S, State T, Box box,
-                                               const GridParams* __restrict__ gp,
-                                               const RoundParams* __restrict__ rpp,
-                                               const int64_t* __restrict__ cs,
-                                               const uint32_t* __restrict__ skey,
-                                               uint8_t* __restrict__ acc,
-                                               const int32_t* __restrict__ nbr,
-                                               const uint8_t* __restrict__ nbr_cnt, StatsDev* stats) {
+__global__ void __launch_bounds__(256) k_phase_list(int l, State S, State T, Box box,
+                                                    const GridParams* __restrict__ gp,
+                                                    const RoundParams* __restrict__ rpp,
+                                                    const int64_t* __restrict__ cs,
+                                                    const uint32_t* __restrict__ skey,
+                                                    uint8_t* __restrict__ acc,
+                                                    const int32_t* __restrict__ nbr,
+                                                    const uint8_t* __restrict__ nbr_cnt,
+                                                    const int32_t* __restrict__ active, StatsDev* stats) {
     if (l >= rpp->n_l || stats->rejected[l - 1] == 0) return;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool rejected = false;
-    if (i < n && acc[i] == kNotAccepted) {
-        const GridParams& g = *gp;
-        const RoundParams rp = *rpp;
+    const int64_t m = static_cast<int64_t>(stats->active_count);
+    const GridParams& g = *gp;
+    const RoundParams rp = *rpp;
+    unsigned long long rej = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = active[k];
+        if (acc[i] != kNotAccepted) continue;
         double xi[D], p[D];
         load_pos<D>(S, i, xi);
         const double ri = S.r[i];
@@ -407,80 +437,91 @@ __global__ void __launch_bounds__(256) k_phase(int64_t n, int l, State S, State 
 #pragma unroll
             for (int a = 0; a < D; ++a) T.x[a][i] = p[a];
             acc[i] = static_cast<uint8_t>(l);
+        } else {
+            ++rej;
         }
-        rejected = !ok;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, rejected);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&stats->rejected[l], (unsigned long long)__popc(m));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rej += __shfl_down_sync(0xffffffffu, rej, o);
+    if ((threadIdx.x & 31) == 0 && rej) atomicAdd(&stats->rejected[l], rej);
 }
 
 // Overlap reduction after the round.  Only pairs of non-movers can overlap (DESIGN.md
-// §3.3), so each non-mover scans its near list for later non-movers.
+// §3.3) and every non-mover is on the attempt-0 reject list, so the reduction walks
+// that list: each non-mover scans its near list for later non-movers.
 template <int D>
-__global__ void __launch_bounds__(256) k_stats(int64_t n, State S, Box box,
-                                               const GridParams* __restrict__ gp,
-                                               const int64_t* __restrict__ cs,
-                                               const uint32_t* __restrict__ skey,
-                                               const uint8_t* __restrict__ acc,
-                                               const int32_t* __restrict__ nbr,
-                                               const uint8_t* __restrict__ nbr_cnt,
-                                               int with_candidates, StatsDev* stats) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    unsigned long long pairs = 0, movers = 0, cand = 0;
+__global__ void __launch_bounds__(256) k_stats_list(State S, Box box, const GridParams* __restrict__ gp,
+                                                    const int64_t* __restrict__ cs,
+                                                    const uint32_t* __restrict__ skey,
+                                                    const uint8_t* __restrict__ acc,
+                                                    const int32_t* __restrict__ nbr,
+                                                    const uint8_t* __restrict__ nbr_cnt,
+                                                    const int32_t* __restrict__ active, StatsDev* stats) {
+    const int64_t m = static_cast<int64_t>(stats->active_count);
+    const GridParams& g = *gp;
+    unsigned long long pairs = 0, stay = 0;
     double pen = 0.0;
-    if (i < n) {
-        const GridParams& g = *gp;
-        if (acc[i] != kNotAccepted) {
-            movers = 1;
-        } else {
-            double xi[D];
-            load_pos<D>(S, i, xi);
-            const double ri = S.r[i];
-            const int32_t idi = S.id[i];
-            auto test = [&](int64_t j) {
-                if (j <= i || acc[j] != kNotAccepted || S.id[j] == idi) return;
-                double xj[D];
-                load_pos<D>(S, j, xj);
-                const double rr = ri + S.r[j];
-                const double d2 = dist2<D>(box, xi, xj);
-                if (d2 <= rr * rr) {
-                    ++pairs;
-                    const double pe = rr - sqrt(d2);
-                    pen = pe > pen ? pe : pen;
-                }
-            };
-            const uint8_t c = nbr_cnt[i];
-            if (c != kOverflow) {
-                const int32_t* my = nbr + i * kNbrCap;
-                for (int t = 0; t < c; ++t) test(my[t]);
-            } else {
-                for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
-                    for (int64_t j = b; j < e; ++j) test(j);
-                });
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = active[k];
+        if (acc[i] != kNotAccepted) continue;
+        ++stay;
+        double xi[D];
+        load_pos<D>(S, i, xi);
+        const double ri = S.r[i];
+        const int32_t idi = S.id[i];
+        auto test = [&](int64_t j) {
+            if (j <= i || acc[j] != kNotAccepted || S.id[j] == idi) return;
+            double xj[D];
+            load_pos<D>(S, j, xj);
+            const double rr = ri + S.r[j];
+            const double d2 = dist2<D>(box, xi, xj);
+            if (d2 <= rr * rr) {
+                ++pairs;
+                const double pe = rr - sqrt(d2);
+                pen = pe > pen ? pe : pen;
             }
-        }
-        if (with_candidates) {
-            const int32_t s1[3] = {g.dims[0] <= 3 ? -1 : 1, g.dims[1] <= 3 ? -1 : 1,
-                                   g.dims[2] <= 3 ? -1 : 1};
-            for_near_ranges<D>(g, cs, skey[i], s1, [&](int64_t b, int64_t e) { cand += (unsigned long long)(e - b); });
-            cand -= 1;
+        };
+        const uint8_t c = nbr_cnt[i];
+        if (c != kOverflow) {
+            const int32_t* my = nbr + i * kNbrCap;
+            for (int t = 0; t < c; ++t) test(my[t]);
+        } else {
+            for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+                for (int64_t j = b; j < e; ++j) test(j);
+            });
         }
     }
-    // warp reduce then one atomic per warp
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         pairs += __shfl_down_sync(0xffffffffu, pairs, o);
-        movers += __shfl_down_sync(0xffffffffu, movers, o);
-        cand += __shfl_down_sync(0xffffffffu, cand, o);
+        stay += __shfl_down_sync(0xffffffffu, stay, o);
         const double t = __shfl_down_sync(0xffffffffu, pen, o);
         pen = t > pen ? t : pen;
     }
     if ((threadIdx.x & 31) == 0) {
         if (pairs) atomicAdd(&stats->overlap_pairs, pairs);
-        if (movers) atomicAdd(&stats->movers, movers);
-        if (cand) atomicAdd(&stats->candidate_pairs, cand);
+        if (stay) atomicAdd(&stats->nonmovers, stay);
         if (pen > 0.0) atomicMax(&stats->pen_bits, (unsigned long long)__double_as_longlong(pen));
     }
+}
+
+// Ordered candidate pairs of the reference's 3^d scan (cell_grid.hpp:394-414), from the
+// cell offsets only (parity statistic, not on the timed path).
+template <int D>
+__global__ void __launch_bounds__(256) k_candidates(int64_t n, const GridParams* __restrict__ gp,
+                                                    const int64_t* __restrict__ cs,
+                                                    const uint32_t* __restrict__ skey, StatsDev* stats) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long cand = 0;
+    if (i < n) {
+        const GridParams& g = *gp;
+        const int32_t s1[3] = {g.dims[0] <= 3 ? -1 : 1, g.dims[1] <= 3 ? -1 : 1, g.dims[2] <= 3 ? -1 : 1};
+        for_near_ranges<D>(g, cs, skey[i], s1, [&](int64_t b, int64_t e) { cand += (unsigned long long)(e - b); });
+        cand -= 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cand += __shfl_down_sync(0xffffffffu, cand, o);
+    if ((threadIdx.x & 31) == 0 && cand) atomicAdd(&stats->candidate_pairs, cand);
 }
 
 // Overlap statistics of a state with no migration (srm_b200_overlap_stats): every pair

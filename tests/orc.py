@@ -167,6 +167,59 @@ def o_philox(ctr, key):
     return out
 
 
+def o_generate(dim, L, pos, r, ids, c_w, c_m, n_k, n_l, f_target, max_iterations, seed,
+               reorder_period=16, iteration_count=0):
+    """Oracle restatement of the device srm_generate loop (engine.hpp:176-260 with the
+    parallel round).  The volume fraction uses the sequential sum (the device uses a
+    fixed tree, equal to ~1e-15), so this is a statistical, not bitwise, oracle for the
+    whole loop.  Returns (status, pos, r, ids, iterations, f, stats dict)."""
+    pos = arr(pos).copy()
+    r = arr(r).copy()
+    ids = arr(ids, np.int32).copy()
+    slot = np.arange(len(r), dtype=np.int32)
+    Lp = P(arr(L))
+    f = orc().orc_volume_fraction_seq(dim, Lp, len(r), P(r))
+    stop = f_target * (1.0 - 1e-12)
+    done = acc_it = rounds = shakes = 0
+    status = 0
+    while f < stop:
+        if done >= max_iterations:
+            status = 1
+            break
+        done += 1
+        it = iteration_count + done
+        factor = 1.0 + c_w
+        if f * factor ** dim > f_target:
+            factor = (f_target / f) ** (1.0 / dim)
+        max_r = float(r.max())
+        q = r * factor
+        x = pos
+        ok = False
+        for k in range(n_k):
+            x, _ = o_round(dim, L, x, q, ids, slot, c_m, n_l, seed, k, it & 0xFFFFFFFF)
+            rounds += 1
+            if o_stats(dim, L, x, q, ids).overlap_pairs == 0:
+                ok = True
+                break
+        if ok:
+            pos, r = x, q
+            f = orc().orc_volume_fraction_seq(dim, Lp, len(r), P(r))
+            acc_it += 1
+            # reorder cadence changes slots/ids exactly like reorder_by_locality
+            if reorder_period > 0 and acc_it % reorder_period == 0:
+                cs = 2.5 * max_r + c_m
+                keys, dims, _ = o_keys(dim, L, cs, pos)
+                order, _ = o_sort(keys, slot, int(np.prod(dims)))
+                pos, r = pos[order], r[order]
+                slot = np.arange(len(r), dtype=np.int32)
+                ids = slot.copy()
+        else:
+            for k in range(n_k):
+                pos, _ = o_round(dim, L, pos, r, ids, slot, c_m, n_l, seed, n_k + k, it & 0xFFFFFFFF)
+                shakes += 1
+    return status, pos, r, ids, iteration_count + done, f, dict(accepted=acc_it, rounds=rounds, shakes=shakes)
+
+
 # ---- reference helpers ---------------------------------------------------------------
 def r_keys(dim, L, cs, pos):
     pos = arr(pos)

@@ -129,8 +129,8 @@ def test_overlap_stats_bit_exact(dim, n, rmin, rmax, seed):
     (3, 5000, 0.3, 1.0, 0.05, 1, 5),
 ])
 def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed):
-    L, pos, r, ids = _rsa_state(dim, n, min(f, 0.55 if dim == 2 else 0.3), seed)
-    r = r * (f / min(f, 0.55 if dim == 2 else 0.3)) ** (1 / dim) * swell
+    L, pos, r, ids = _rsa_state(dim, n, min(f, 0.45 if dim == 2 else 0.25), seed)
+    r = r * (f / min(f, 0.45 if dim == 2 else 0.25)) ** (1 / dim) * swell
     c_m = cm_rel * r.max()
     cs = 2.5 * r.max() / swell + c_m
     key, round_id, it = 0x0123456789ABCDEF + seed, 3, 17
@@ -149,8 +149,70 @@ def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed):
     assert st.candidate_pairs == orc.o_candidates(dim, dims, keys)
 
 
+@pytest.mark.parametrize("dim,n,L,cm_rel,swell", [
+    (3, 400, [1.0, 1.0, 1.0], 0.1, 1.02),      # dims 3-4: whole-axis bricks, every cell a neighbour
+    (3, 3000, [2.0, 1.0, 0.5], 0.1, 1.03),     # rectangular: brick / whole-axis mix
+    (3, 4000, [1.0, 1.0, 1.0], 0.45, 1.05),    # wide moves: near half width 2
+    (2, 6000, [1.0, 3.0], 0.2, 1.02),
+    (2, 300, [1.0, 1.0], 0.3, 1.0),
+])
+def test_round_brick_modes_bit_exact(dim, n, L, cm_rel, swell):
+    unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
+    f = 0.35 if dim == 2 else 0.2
+    r = (f * np.prod(L) / (n * unit)) ** (1.0 / dim)
+    pos, ids = srm.rsa_place(np.full(n, r), L, 10000, 31)
+    rr = np.full(n, r * swell)
+    c_m = cm_rel * r
+    cs = 2.5 * r + c_m
+    with _ctx(L, pos, rr, ids) as ctx:
+        st, acc = ctx.round(cs, c_m, 6, 4242, 1, 2, with_candidates=True)
+        pos_d, _, _ = ctx.download()
+        info = ctx.last_round_info()
+    xnew, acc_o = orc.o_round(dim, L, pos, rr, ids, ids, c_m, 6, 4242, 1, 2)
+    assert np.array_equal(acc, acc_o) and np.array_equal(pos_d, xnew)
+    o = orc.o_stats(dim, L, xnew, rr)
+    assert st.overlap_pairs == o.overlap_pairs and st.max_penetration == o.max_penetration
+    assert info["rejected_attempt0"] == int(np.sum(acc_o != 0))
+
+
+def test_clustered_start_overflows_bricks_bit_exact():
+    # dense Gaussian clusters (cfg3-like start) push bricks over their shared-memory
+    # capacity: those bricks take the global-memory path, results unchanged
+    rng = np.random.default_rng(8)
+    n, L = 6000, [1.0, 1.0, 1.0]
+    centres = rng.uniform(0, 1, (6, 3))
+    pos = np.mod(centres[np.arange(n) % 6] + rng.normal(0, 0.04, (n, 3)), 1.0)
+    r = np.full(n, 0.0035)
+    c_m = 0.1 * r[0]
+    cs = 2.5 * r[0] + c_m
+    with _ctx(L, pos, r) as ctx:
+        st, acc = ctx.round(cs, c_m, 5, 7, 0, 0)
+        pos_d, _, _ = ctx.download()
+        info = ctx.last_round_info()
+    xnew, acc_o = orc.o_round(3, L, pos, r, np.arange(n, dtype=np.int32), np.arange(n, dtype=np.int32),
+                              c_m, 5, 7, 0, 0)
+    assert info["fallback_bricks"] > 0
+    assert np.array_equal(acc, acc_o) and np.array_equal(pos_d, xnew)
+    assert st.overlap_pairs == orc.o_stats(3, L, xnew, r).overlap_pairs
+
+
+def test_bricks_equal_untiled(monkeypatch):
+    L, pos, r, ids = _rsa_state(3, 20000, 0.25, 17)
+    r = r * (0.3 / 0.25) ** (1 / 3)
+    c_m = 0.05 * r[0]
+    cs = 2.5 * r[0] / 1.02 + c_m
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SRM_B200_NO_TILES", flag)
+        with _ctx(L, pos, r, ids) as ctx:
+            st = ctx.rounds(cs, c_m, 10, 3, 0, 9, 2)
+            out.append((ctx.download()[0], st.overlap_pairs, st.movers, ctx.last_round_info()["bricks"]))
+    assert out[0][3] > 0 and out[1][3] == 0
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1:3] == out[1][1:3]
+
+
 def test_round_polydisperse_bit_exact():
-    L, pos, r, ids = _rsa_state(3, 4000, 0.3, 9, L=[1.0, 1.0, 1.0], poly=True)
+    L, pos, r, ids = _rsa_state(3, 4000, 0.22, 9, L=[1.0, 1.0, 1.0], poly=True)
     r = r * 1.04
     c_m = 0.1 * np.mean(r)
     cs = 2.5 * r.max() / 1.04 + c_m
