@@ -19,7 +19,7 @@ all: lib oracle
 
 lib: $(LIB)
 
-$(CSRC)/srm_capi.o: $(CSRC)/srm_capi.cu $(CSRC)/srm_kernels.cuh $(CSRC)/srm_device.cuh include/srm_b200.h
+$(CSRC)/srm_capi.o: $(CSRC)/srm_capi.cu $(wildcard $(CSRC)/*.cuh) include/srm_b200.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; exit 1)
 
 $(CSRC)/srm_selftest.o: $(CSRC)/srm_selftest.cu $(CSRC)/srm_device.cuh include/srm_b200.h

@@ -387,8 +387,9 @@ __global__ void __launch_bounds__(256) k_phase_list(int l, State S, State T, Box
                                                     const int32_t* __restrict__ nbr,
                                                     const uint8_t* __restrict__ nbr_cnt,
                                                     const int32_t* __restrict__ active, StatsDev* stats) {
-    if (l >= rpp->n_l || stats->rejected[l - 1] == 0) return;
+    if (l >= rpp->n_l) return;
     const int64_t m = static_cast<int64_t>(stats->active_count);
+    if ((l == 1 ? static_cast<unsigned long long>(m) : stats->rejected[l - 1]) == 0) return;
     const GridParams& g = *gp;
     const RoundParams rp = *rpp;
     unsigned long long rej = 0;

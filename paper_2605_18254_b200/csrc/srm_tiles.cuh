@@ -138,9 +138,11 @@ __global__ void __launch_bounds__(kTileThreads, 2)
             const int iy = r % nst[1], iz = r / nst[1];
             int gy = tp.ax[1].full ? iy : o[1] - tp.ax[1].s + iy;
             int gz = tp.ax[2].full ? iz : o[2] - tp.ax[2].s + iz;
+            // unwrapped cell u < 0 is global cell u + dims: its positions sit one box
+            // length above the brick, so they are shifted by -L (and u >= dims by +L)
             signed char shy = 0, shz = 0;
-            if (gy < 0) { gy += dy; shy = 1; } else if (gy >= dy) { gy -= dy; shy = -1; }
-            if (gz < 0) { gz += dimsv[2]; shz = 1; } else if (gz >= dimsv[2]) { gz -= dimsv[2]; shz = -1; }
+            if (gy < 0) { gy += dy; shy = -1; } else if (gy >= dy) { gy -= dy; shy = 1; }
+            if (gz < 0) { gz += dimsv[2]; shz = -1; } else if (gz >= dimsv[2]) { gz -= dimsv[2]; shz = 1; }
             const long long rc0 = (static_cast<long long>(gz) * dy + gy) * dx;
             int A0, A1, B1 = 0, kA;
             signed char shA = 0, shB = 0;
@@ -148,8 +150,8 @@ __global__ void __launch_bounds__(kTileThreads, 2)
                 A0 = 0; A1 = dx; kA = dx;
             } else {
                 const int u0 = o[0] - tp.ax[0].s, u1 = u0 + nst[0];
-                if (u0 < 0) { A0 = u0 + dx; A1 = dx; shA = 1; B1 = u1; }
-                else if (u1 > dx) { A0 = u0; A1 = dx; B1 = u1 - dx; shB = -1; }
+                if (u0 < 0) { A0 = u0 + dx; A1 = dx; shA = -1; B1 = u1; }
+                else if (u1 > dx) { A0 = u0; A1 = dx; B1 = u1 - dx; shB = 1; }
                 else { A0 = u0; A1 = u1; }
                 kA = A1 - A0;
             }
@@ -164,9 +166,9 @@ __global__ void __launch_bounds__(kTileThreads, 2)
         }
         const int rb = block_excl_scan_int(tot, &s_total);
         if (threadIdx.x < nrows) s_rowbase[threadIdx.x] = rb;
+        if (threadIdx.x == nrows - 1) s_rowbase[nrows] = rb + tot;
         __syncthreads();
         const int total = s_total;
-        if (threadIdx.x == 0) s_rowbase[nrows] = total;
 
         if (total > cap) {
             // ---- fallback: brick particles straight from global memory ---------------
