@@ -200,8 +200,12 @@ struct srm_b200_ctx {
         tpp = dalloc<TileParams>(1);
         if (const char* e = std::getenv("SRM_B200_NO_TILES")) force_global = e[0] == '1';
         active = dalloc<int32_t>(cap);
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_pairs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
+        SRM_CUDA(cudaFuncSetAttribute(k_phase0_pairs<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -253,6 +257,7 @@ struct srm_b200_ctx {
                 throw Invalid{"CellGrid: more than 2^32 cells (radius too small for the box)"};
         }
         g.extra = extra;
+        g.rmax = max_r_state;
         const double cut = ((max_r_state + max_r_state + extra) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
         for (int a = 0; a < dim; ++a) {
             int64_t s = 1;
@@ -277,62 +282,110 @@ struct srm_b200_ctx {
         cell_cap = c;
     }
 
-    // Brick decomposition for k_phase0_tiled: bricks of ~256 particles, staged halo of
-    // near_s cells, capacity with a Poisson margin; disabled when the stencil is too wide.
-    TileParams make_tiles(const GridParams& g) const {
+    // Brick decomposition for k_phase0_tiled.  Per-axis brick widths are searched so
+    // that a brick holds at most ~230 particles on average (one per thread of a
+    // 256-thread CTA; bigger bricks mean less halo), staged capacity = mean + 5 sigma
+    // (Poisson) + 32, shared memory <= kTileSmemMax.  Axes whose brick would cover the
+    // whole axis (or whose stencil does) are staged whole, in global order.
+    TileParams build_tiles(const GridParams& g, const int* Bw, double occ, bool& fits) const {
         TileParams tp{};
-        tp.enabled = 0;
-        if (n == 0) return tp;
-        const double occ = static_cast<double>(n) / static_cast<double>(g.ncells);
-        int Bt = std::max(1, static_cast<int>(std::lround(std::pow(256.0 / std::max(occ, 1e-3), 1.0 / dim))));
-        for (; Bt >= 1; --Bt) {
-            int nst[3];
-            int64_t ntiles = 1;
-            int ncr = 1;
-            bool ok = true;
-            double ext = 0.0;
-            for (int a = 0; a < 3; ++a) {
-                AxisTile A{};
-                if (a >= dim) {
-                    A.full = 1; A.all = 1; A.B = 1; A.ntile = 1; A.s = 0;
-                    nst[a] = 1;
+        fits = false;
+        int nst[3];
+        int64_t ntiles = 1;
+        int ncr = 1;
+        double ext = 0.0, centre = occ;
+        bool bricks_only = true;
+        for (int a = 0; a < 3; ++a) {
+            AxisTile A{};
+            if (a >= dim) {
+                A.full = 1; A.all = 1; A.B = 1; A.ntile = 1; A.s = 0;
+                nst[a] = 1;
+            } else {
+                const int s = g.near_s[a], d = g.dims[a];
+                A.all = s < 0 ? 1 : 0;
+                A.s = s < 0 ? 0 : s;
+                if (A.all || Bw[a] + 2 * s >= d) {
+                    A.full = 1; A.B = d; A.ntile = 1; nst[a] = d;
+                    ext = std::max(ext, box.L[a]);
+                    bricks_only = false;
                 } else {
-                    const int s = g.near_s[a], d = g.dims[a];
-                    A.all = s < 0 ? 1 : 0;
-                    A.s = s < 0 ? 0 : s;
-                    if (A.all || Bt + 2 * s >= d) {
-                        A.full = 1; A.B = d; A.ntile = 1; nst[a] = d;
-                        ext = std::max(ext, box.L[a]);
-                    } else {
-                        A.full = 0; A.B = Bt; A.ntile = (d + Bt - 1) / Bt; nst[a] = Bt + 2 * s;
-                        ext = std::max(ext, nst[a] * g.edge[a]);
-                    }
-                    if (!A.all && 2 * A.s + 1 > 16) ok = false;
-                    if (A.all && a > 0 && d > 16) ok = false;
-                    if (a > 0) ncr *= A.B;
+                    A.full = 0; A.B = Bw[a]; A.ntile = (d + Bw[a] - 1) / Bw[a]; nst[a] = Bw[a] + 2 * s;
+                    ext = std::max(ext, nst[a] * g.edge[a]);
                 }
-                tp.ax[a] = A;
-                ntiles *= A.ntile;
+                if (!A.all && 2 * A.s + 1 > 16) return tp;
+                if (A.all && a > 0 && d > 16) return tp;
+                if (a > 0) ncr *= A.B;
+                centre *= A.B;
             }
-            const int rows = nst[1] * nst[2];
-            if (!ok || rows > kMaxRows || ncr > kTileThreads) continue;
-            const double mean = occ * nst[0] * nst[1] * nst[2];
-            int capv = static_cast<int>(std::ceil(mean * 1.3 + 4.0 * std::sqrt(mean) + 32.0));
-            capv = (capv + 31) / 32 * 32;
-            const int64_t smem = static_cast<int64_t>(capv) * (8 * (2 * dim + 1) + 16 + 8) +
-                                 static_cast<int64_t>(rows) * (nst[0] + 1) * 4;
-            if (smem > kTileSmemMax) continue;
-            tp.ntiles = ntiles;
-            tp.cap = capv;
-            for (int a = 0; a < 3; ++a) tp.nst_max[a] = nst[a];
-            tp.margin = static_cast<float>(16.0 * std::ldexp(1.0, -24) * ext);
-            tp.extra_f = static_cast<float>(g.extra);
-            tp.smem_bytes = static_cast<int32_t>(smem);
-            tp.enabled = 1;
-            return tp;
+            tp.ax[a] = A;
+            ntiles *= A.ntile;
         }
+        const int rows = nst[1] * nst[2];
+        if (rows > kMaxRows || ncr > kTileThreads) return tp;
+        const double staged = occ * nst[0] * nst[1] * nst[2];
+        int capS = static_cast<int>(std::ceil(staged + 5.0 * std::sqrt(staged) + 32.0));
+        int capC = static_cast<int>(std::ceil(centre + 5.0 * std::sqrt(centre) + 32.0));
+        capS = (capS + 31) / 32 * 32;
+        capC = (capC + 31) / 32 * 32;
+        int maxseg = 1;
+        for (int a = 1; a < dim; ++a) maxseg *= 2 * tp.ax[a].s + 1;
+        int64_t smem;
+        if (bricks_only) {  // k_phase0_pairs layout
+            smem = static_cast<int64_t>(capS) * (16 + 16 + 4 + 4) + static_cast<int64_t>(capC) * 8 * dim +
+                   static_cast<int64_t>(rows) * (nst[0] + 1) * 4 + kTileThreads * kNbrCap * 2;
+        } else {  // k_phase0_tiled layout
+            smem = static_cast<int64_t>(capS) * (16 + 8 * dim + 8 + 12) + static_cast<int64_t>(capC) * (16 + 8 * dim) +
+                   static_cast<int64_t>(rows) * (nst[0] + 1) * 4;
+        }
+        smem = (smem + 15) / 16 * 16;
+        if (smem > kTileSmemMax) return tp;
+        tp.maxseg = maxseg;
+        tp.ntiles = ntiles;
+        tp.capS = capS;
+        tp.capC = capC;
+        for (int a = 0; a < 3; ++a) {
+            tp.nst_max[a] = nst[a];
+            tp.edge_f[a] = static_cast<float>(a < dim ? g.edge[a] : 1.0);
+        }
+        tp.margin = static_cast<float>(16.0 * std::ldexp(1.0, -24) * ext);
+        tp.extra_f = static_cast<float>(g.extra);
+        tp.rmax_f = static_cast<float>(g.rmax);
+        tp.bricks_only = bricks_only ? 1 : 0;
+        tp.smem_bytes = static_cast<int32_t>(smem);
+        tp.enabled = 1;
+        fits = true;
         return tp;
     }
+
+    TileParams make_tiles(const GridParams& g) const {
+        TileParams best{};
+        best.enabled = 0;
+        if (n == 0) return best;
+        const double occ = static_cast<double>(n) / static_cast<double>(g.ncells);
+        const double target = 230.0;
+        double best_score = -1.0;
+        const int bmax = 24;
+        for (int b0 = 1; b0 <= bmax; ++b0)
+            for (int b1 = 1; b1 <= (dim >= 2 ? b0 : 1); ++b1)
+                for (int b2 = 1; b2 <= (dim == 3 ? b1 : 1); ++b2) {
+                    const double centre = occ * b0 * b1 * (dim == 3 ? b2 : 1);
+                    if (centre > target) continue;
+                    const int Bw[3] = {b0, b1, b2};
+                    bool fits = false;
+                    const TileParams tp = build_tiles(g, Bw, occ, fits);
+                    if (!fits) continue;
+                    // prefer full bricks, then less halo per brick particle
+                    const double staged = static_cast<double>(tp.nst_max[0]) * tp.nst_max[1] * tp.nst_max[2];
+                    const double cells = static_cast<double>(b0) * b1 * (dim == 3 ? b2 : 1);
+                    const double score = centre / target - 0.25 * staged / cells;
+                    if (score > best_score) {
+                        best_score = score;
+                        best = tp;
+                    }
+                }
+        return best;
+    }
+
 
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
@@ -393,10 +446,10 @@ struct srm_b200_ctx {
             FamScope fs(this, 1);
             if (ht.enabled && !force_global) {
                 const int grid = static_cast<int>(std::min<int64_t>(ht.ntiles, 2147483647));
-                if (dim == 2)
-                    k_phase0_tiled<2><<<grid, kTileThreads, ht.smem_bytes, stream>>>(S, T, box, gp, tpp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
-                else
-                    k_phase0_tiled<3><<<grid, kTileThreads, ht.smem_bytes, stream>>>(S, T, box, gp, tpp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                auto kern = dim == 2 ? (ht.bricks_only ? k_phase0_pairs<2> : k_phase0_tiled<2, false>)
+                                     : (ht.bricks_only ? k_phase0_pairs<3> : k_phase0_tiled<3, false>);
+                kern<<<grid, kTileThreads, ht.smem_bytes, stream>>>(S, T, box, gp, tpp, rp, cell_start, skey, acc, nbr,
+                                                                    nbr_cnt, active, stats);
             } else {
                 if (dim == 2)
                     k_phase0<2><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
@@ -979,7 +1032,7 @@ int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
         info[0] = c->last_rejected0;
         info[1] = c->last_fallback_tiles;
         info[2] = c->ht.enabled && !c->force_global ? c->ht.ntiles : 0;
-        info[3] = c->ht.enabled ? c->ht.cap : 0;
+        info[3] = c->ht.enabled ? c->ht.capS : 0;
         info[4] = c->ht.enabled ? c->ht.smem_bytes : 0;
         info[5] = c->ht.enabled ? c->ht.ax[0].B : 0;
         return SRM_B200_OK;

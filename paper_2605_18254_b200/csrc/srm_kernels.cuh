@@ -26,6 +26,7 @@ struct GridParams {
     int64_t ncells;
     int32_t near_s[3];  // near-search half width per axis; -1 = every cell on the axis
     double extra;       // near cutoff: (ri + rj + extra) * (1 + 1e-9) + 1e-300
+    double rmax;        // largest radius of the state the grid indexes
 };
 
 struct RoundParams {
