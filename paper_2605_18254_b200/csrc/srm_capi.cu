@@ -332,7 +332,8 @@ struct srm_b200_ctx {
         int64_t smem;
         if (bricks_only) {  // k_phase0_pairs layout
             smem = static_cast<int64_t>(capS) * (16 + 16 + 4 + 4) + static_cast<int64_t>(capC) * 8 * dim +
-                   static_cast<int64_t>(rows) * (nst[0] + 1) * 4 + kTileThreads * kNbrCap * 2;
+                   static_cast<int64_t>(rows) * (nst[0] + 1) * 4 + kTileThreads * kNbrBuf * 2 +
+                   static_cast<int64_t>(kTileThreads) * maxseg * 4;
         } else {  // k_phase0_tiled layout
             smem = static_cast<int64_t>(capS) * (16 + 8 * dim + 8 + 12) + static_cast<int64_t>(capC) * (16 + 8 * dim) +
                    static_cast<int64_t>(rows) * (nst[0] + 1) * 4;

@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kTileThreads, 3)
 // all staged particles are computed in one uniform pass; the exact fp64 tests (close
 // calls only) reload positions from global memory and recompute the proposal.
 constexpr int kPairChunk = 8;
-constexpr int kNbrSmem = 24;  // near-list entries kept per brick particle (more -> overflow)
+constexpr int kNbrBuf = 16;  // near candidates buffered per brick particle (more -> overflow)
 
 template <int D>
 __device__ __forceinline__ void proposal_of(const State& S, int64_t gi, const Box& box, const RoundParams& rp,
@@ -513,7 +513,8 @@ __global__ void __launch_bounds__(kTileThreads, 3)
     __shared__ int s_lenA[kMaxRows];
     __shared__ int s_kA[kMaxRows];
     __shared__ int s_A0[kMaxRows];
-    __shared__ long long s_gA[kMaxRows], s_gB[kMaxRows], s_rc0[kMaxRows];
+    __shared__ int s_gA[kMaxRows], s_gB[kMaxRows];
+    __shared__ unsigned s_rc0[kMaxRows];  // row cell index (< 2^32 cells)
     __shared__ signed char s_shA[kMaxRows], s_shB[kMaxRows], s_shY[kMaxRows], s_shZ[kMaxRows];
     __shared__ int s_cpre[kMaxRows + 1];
     __shared__ int s_crow[kMaxRows];
@@ -531,7 +532,8 @@ __global__ void __launch_bounds__(kTileThreads, 3)
     int* sid = reinterpret_cast<int*>(sp + D * capC);
     int* sgi = sid + capS;
     int* coff = sgi + capS;
-    short* wbuf = reinterpret_cast<short*>(coff + rows_max * X1);  // kNbrCap per thread
+    short2* srng = reinterpret_cast<short2*>(coff + rows_max * X1);          // MS ranges per thread
+    short* wbuf = reinterpret_cast<short*>(srng + kTileThreads * MS);       // kNbrCap per thread
     (void)MS;
 
     const int dimsv[3] = {g.dims[0], g.dims[1], D == 3 ? g.dims[2] : 1};
@@ -587,7 +589,7 @@ __global__ void __launch_bounds__(kTileThreads, 3)
             const int lenB = B1 > 0 ? static_cast<int>(cs[rc0 + B1] - gB) : 0;
             tot = lenA + lenB;
             s_lenA[r] = lenA; s_kA[r] = A1 - A0; s_A0[r] = A0;
-            s_gA[r] = gA; s_gB[r] = gB; s_rc0[r] = rc0;
+            s_gA[r] = static_cast<int>(gA); s_gB[r] = static_cast<int>(gB); s_rc0[r] = static_cast<unsigned>(rc0);
             s_shA[r] = shA; s_shB[r] = shB; s_shY[r] = shy; s_shZ[r] = shz;
         }
         const int rb = block_excl_scan_int(tot, &s_total);
@@ -602,8 +604,8 @@ __global__ void __launch_bounds__(kTileThreads, 3)
                 const int r = idx / (nst[0] + 1), k = idx % (nst[0] + 1);
                 int off;
                 if (k == nst[0]) off = s_rowbase[r + 1] - s_rowbase[r];
-                else if (k < s_kA[r]) off = static_cast<int>(cs[s_rc0[r] + s_A0[r] + k] - s_gA[r]);
-                else off = s_lenA[r] + static_cast<int>(cs[s_rc0[r] + (k - s_kA[r])] - s_gB[r]);
+                else if (k < s_kA[r]) off = static_cast<int>(cs[static_cast<long long>(s_rc0[r]) + s_A0[r] + k] - s_gA[r]);
+                else off = s_lenA[r] + static_cast<int>(cs[static_cast<long long>(s_rc0[r]) + (k - s_kA[r])] - s_gB[r]);
                 coff[r * X1 + k] = s_rowbase[r] + off;
             }
         }
@@ -681,7 +683,7 @@ __global__ void __launch_bounds__(kTileThreads, 3)
         // short loop, so the near-pair work does not diverge inside the candidate loop.
         for (int cb = 0; cb < nc; cb += kTileThreads) {
             const int c = cb + threadIdx.x;
-            short* wb = wbuf + threadIdx.x * kNbrCap;
+            short* wb = wbuf + threadIdx.x * kNbrBuf;
             bool rejected = false;
             int gi = -1;
             if (c < nc) {
@@ -733,6 +735,10 @@ __global__ void __launch_bounds__(kTileThreads, 3)
                     }
                     conflict = conflict || cf;
                 };
+                // pruned stencil -> contiguous candidate ranges; each row's x range is cut to
+                // the chord of the (margin-inflated) cutoff sphere at the row's distance
+                short2* rg = srng + threadIdx.x * MS;
+                int nr = 0;
                 for (int iz2 = zlo; iz2 <= zhi; ++iz2) {
                     float dzd = 0.f;
                     if (D == 3) {
@@ -742,21 +748,38 @@ __global__ void __launch_bounds__(kTileThreads, 3)
                     for (int iy2 = ylo; iy2 <= yhi; ++iy2) {
                         const float yb = (iy2 - sw[1]) * tp.edge_f[1];
                         const float dyd = fmaxf(0.f, fmaxf(yb - me.y, me.y - (yb + tp.edge_f[1])));
-                        if (__fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd)) > cut2) continue;
+                        const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
+                        if (dyz2 > cut2) continue;
+                        const float xh = __fadd_rn(__fsqrt_rn(__fsub_rn(cut2, dyz2)), margin);
+                        const int xl = max(xlo, static_cast<int>(floorf(__fdiv_rn(__fsub_rn(me.x, xh), tp.edge_f[0]))) + sw[0]);
+                        const int xr = min(xhi, static_cast<int>(ceilf(__fdiv_rn(__fadd_rn(me.x, xh), tp.edge_f[0]))) - 1 + sw[0]);
                         const int* rowoff = coff + (iz2 * nst[1] + iy2) * X1;
-                        const int e = rowoff[xhi + 1];
-                        for (int q2 = rowoff[xlo]; q2 < e; ++q2) {
-                            const float4 cq = srel[q2];
-                            if (clear_f(d2_rel<D, true>(me, cq, nullptr, nullptr, nullptr), __fadd_rn(lim0, cq.w)))
-                                continue;
-                            if (q2 == q) continue;
-                            if (nn < kNbrCap) wb[nn] = static_cast<short>(q2);
+                        const int b = rowoff[xl], e = rowoff[xr + 1];
+                        if (e > b) rg[nr++] = make_short2(static_cast<short>(b), static_cast<short>(e));
+                    }
+                }
+                // one flat loop over every candidate of every range
+                if (nr > 0) {
+                    int k = 0;
+                    short2 cur = rg[0];
+                    int q2 = cur.x, e = cur.y;
+                    while (true) {
+                        const float4 cq = srel[q2];
+                        if (!clear_f(d2_rel<D, true>(me, cq, nullptr, nullptr, nullptr), __fadd_rn(lim0, cq.w)) &&
+                            q2 != q) {
+                            if (nn < kNbrBuf) wb[nn] = static_cast<short>(q2);
                             else test(q2);  // buffer full (rare): test inline
                             ++nn;
                         }
+                        if (++q2 == e) {
+                            if (++k == nr) break;
+                            cur = rg[k];
+                            q2 = cur.x;
+                            e = cur.y;
+                        }
                     }
                 }
-                const int nb = min(nn, kNbrCap);
+                const int nb = min(nn, kNbrBuf);
                 for (int k = 0; k < nb; ++k) test(wb[k]);
                 const bool ok = !conflict;
 #pragma unroll
@@ -765,9 +788,11 @@ __global__ void __launch_bounds__(kTileThreads, 3)
                 T.id[gi] = idq;
                 T.slot[gi] = S.slot[gi];
                 acc[gi] = ok ? 0 : kNotAccepted;
-                nbr_cnt[gi] = nn > kNbrCap ? kOverflow : static_cast<uint8_t>(nn);
+                // more near candidates than the buffer holds: the list is marked overflowed
+                // and later attempts rescan the grid for this particle
+                nbr_cnt[gi] = nn > kNbrBuf ? kOverflow : static_cast<uint8_t>(nn);
                 // only rejected particles need their near list (later attempts, reduction)
-                if (!ok && nn <= kNbrCap) {
+                if (!ok && nn <= kNbrBuf) {
                     int32_t* my = nbr + static_cast<int64_t>(gi) * kNbrCap;
                     for (int k = 0; k < nn; ++k) my[k] = sgi[wb[k]];
                 }
