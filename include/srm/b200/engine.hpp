@@ -1,0 +1,247 @@
+// srm/b200/engine.hpp -- header-only C++ drop-in for the reference's SRM engine API,
+// running on a B200 through libsrm_b200.so (C ABI: include/srm_b200.h).
+//
+// The functions keep the signatures of /root/reference/proj/core/include/srm/engine.hpp
+// and shape.hpp, on the reference's own types, so switching a caller is a namespace
+// change:  srm::srm_generate<S>(...)  ->  srm::b200::srm_generate<S>(...).
+//
+//   srm_generate        engine.hpp:176-260
+//   migrate             engine.hpp:89-107   (Rng& -> one rng.raw() draw as the Philox key)
+//   relax_sweeps/shake  engine.hpp:112-130  (idem)
+//   swell_all           engine.hpp:134-138
+//   reorder_by_locality engine.hpp:144-166
+//   shape_any_collision shape.hpp:549-555
+//   rsa_place           rsa.hpp:21-61       (seeded form; bit-identical to Rng(seed))
+//
+// Differences the caller can observe:
+//   * migrate is the parallel round: decisions depend on (key, slot), not on storage
+//     order, and trajectories differ from the sequential mt19937_64 sweep;
+//   * errors: ValidationError / PlacementFailure / std::invalid_argument as in the
+//     reference; device failures throw srm::b200::DeviceError.
+// Disks and spheres (SphereShape<2>, SphereShape<3>) are supported.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "srm/cell_grid.hpp"
+#include "srm/engine.hpp"
+#include "srm/errors.hpp"
+#include "srm/geometry.hpp"
+#include "srm/random.hpp"
+#include "srm/rsa.hpp"
+#include "srm/shape.hpp"
+#include "srm_b200.h"
+
+namespace srm::b200 {
+
+struct DeviceError : srm::Error {
+    using srm::Error::Error;
+};
+
+template <typename S>
+inline constexpr bool is_sphere_shape_v = std::is_same_v<S, SphereShape<S::dim>>;
+
+namespace detail {
+
+inline void check(int st, const srm_b200_ctx* c, bool invalid_argument = false) {
+    if (st == SRM_B200_OK || st == SRM_B200_ITERATION_LIMIT) return;
+    const std::string msg = c ? srm_b200_last_error(c) : srm_b200_create_error();
+    if (st == SRM_B200_INVALID) {
+        if (invalid_argument) throw std::invalid_argument(msg);
+        throw ValidationError(msg);
+    }
+    throw DeviceError("srm_b200 status " + std::to_string(st) + ": " + msg);
+}
+
+// RAII over one device context holding a copy of the particles
+template <int N>
+class Device {
+  public:
+    Device(const PeriodicBox<N>& box, std::size_t capacity, int device = 0) {
+        double L[3] = {1.0, 1.0, 1.0};
+        for (int a = 0; a < N; ++a) L[a] = box.length(a);
+        check(srm_b200_create(N, SRM_B200_SPHERE, L, static_cast<int64_t>(capacity < 1 ? 1 : capacity), device,
+                              &ctx_),
+              nullptr);
+    }
+    ~Device() { srm_b200_destroy(ctx_); }
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+
+    srm_b200_ctx* get() const { return ctx_; }
+
+    // Particle<N> is {int id; Vec<N> pos; double radius} (geometry.hpp:139-144)
+    void upload(std::span<const Particle<N>> ps) {
+        check(srm_b200_upload_records(ctx_, static_cast<int64_t>(ps.size()), ps.data(), sizeof(Particle<N>),
+                                      offsetof(Particle<N>, id), offsetof(Particle<N>, pos),
+                                      offsetof(Particle<N>, radius)),
+              ctx_);
+    }
+    void download(std::vector<Particle<N>>& ps) {
+        check(srm_b200_download_records(ctx_, ps.data(), sizeof(Particle<N>), offsetof(Particle<N>, id),
+                                        offsetof(Particle<N>, pos), offsetof(Particle<N>, radius)),
+              ctx_);
+    }
+
+  private:
+    srm_b200_ctx* ctx_ = nullptr;
+};
+
+inline srm_b200_params to_c(const SrmParams& p) {
+    srm_b200_params c{};
+    c.c_w = p.c_w;
+    c.c_m = p.c_m;
+    c.c_r = p.c_r;
+    c.n_k = p.n_k;
+    c.n_l = p.n_l;
+    c.f_target = p.f_target;
+    c.max_iterations = p.max_iterations;
+    c.seed = p.seed;
+    c.reorder_period = p.reorder_period;
+    return c;
+}
+
+inline void progress_trampoline(const srm_b200_progress_record* rec, void* user) {
+    const auto* sink = static_cast<const ProgressSink*>(user);
+    (*sink)(ProgressRecord{rec->iteration, rec->volume_fraction, rec->accepted != 0, rec->elapsed_seconds});
+}
+
+}  // namespace detail
+
+// engine.hpp:176-260
+template <ShapeModel S>
+GenerateResult<S> srm_generate(const Snapshot<S>& initial, const SrmParams& params,
+                               const ProgressSink& progress = {}) {
+    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    constexpr int N = S::dim;
+    GenerateResult<S> result;
+    result.snapshot = initial;
+    Snapshot<S>& snap = result.snapshot;
+    snap.params = params;
+    snap.seed = params.seed;
+    detail::Device<N> dev(initial.box, initial.particles.size());
+    dev.upload(initial.particles);
+    const srm_b200_params cp = detail::to_c(params);
+    srm_b200_generate_out out{};
+    const int st = srm_b200_generate(dev.get(), &cp, initial.iteration_count,
+                                     progress ? &detail::progress_trampoline : nullptr,
+                                     const_cast<ProgressSink*>(&progress), &out);
+    detail::check(st, dev.get());
+    dev.download(snap.particles);
+    snap.volume_fraction = out.volume_fraction;
+    snap.iteration_count = out.iteration_count;
+    result.status = st == SRM_B200_ITERATION_LIMIT ? GenerateStatus::IterationLimitExceeded
+                                                   : GenerateStatus::Converged;
+    return result;
+}
+
+// engine.hpp:89-107: one migration sweep against `grid` (its cell size), the parallel
+// round of DESIGN.md §3 keyed by one draw of rng.  Returns the accepted flags.
+template <ShapeModel S>
+std::vector<std::uint8_t> migrate(std::vector<typename S::ParticleT>& particles, const CellGrid<S::dim>& grid,
+                                  double c_m, double /*c_r*/, int n_l, Rng& rng) {
+    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    constexpr int N = S::dim;
+    std::vector<std::uint8_t> acc(particles.size(), 0);
+    if (particles.empty()) return acc;
+    const std::uint64_t key = rng.raw();
+    detail::Device<N> dev(grid.box(), particles.size());
+    dev.upload(particles);
+    srm_b200_round_stats st{};
+    detail::check(srm_b200_round(dev.get(), grid.cell_size(), c_m, n_l, key, 0, 0, 0, acc.data(), &st), dev.get(),
+                  true);
+    dev.download(particles);
+    for (auto& a : acc) a = a != 255 ? 1 : 0;
+    return acc;
+}
+
+// engine.hpp:112-122
+template <ShapeModel S>
+void relax_sweeps(std::vector<typename S::ParticleT>& particles, const PeriodicBox<S::dim>& box, double c_m,
+                  double c_r, int n_l, int sweeps, Rng& rng) {
+    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    if (particles.empty() || sweeps < 1) return;
+    const std::uint64_t key = rng.raw();
+    detail::Device<S::dim> dev(box, particles.size());
+    dev.upload(particles);
+    detail::check(srm_b200_relax_sweeps(dev.get(), c_m, c_r, n_l, sweeps, key), dev.get(), true);
+    dev.download(particles);
+}
+
+// engine.hpp:126-130
+template <ShapeModel S>
+void shake(std::vector<typename S::ParticleT>& particles, const PeriodicBox<S::dim>& box, const SrmParams& params,
+           Rng& rng) {
+    relax_sweeps<S>(particles, box, params.c_m, params.c_r, params.n_l, params.n_k, rng);
+}
+
+// engine.hpp:134-138 (on the device; radius *= 1 + c_w)
+template <ShapeModel S>
+void swell_all(std::vector<typename S::ParticleT>& particles, double c_w) {
+    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    if (particles.empty()) return;
+    detail::Device<S::dim> dev(PeriodicBox<S::dim>::unit(), particles.size());
+    dev.upload(particles);
+    detail::check(srm_b200_swell_all(dev.get(), c_w), dev.get());
+    dev.download(particles);
+}
+
+// engine.hpp:144-166
+template <ShapeModel S>
+std::vector<int> reorder_by_locality(std::vector<typename S::ParticleT>& particles, const CellGrid<S::dim>& grid) {
+    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    std::vector<int> remap(particles.size());
+    if (particles.empty()) return remap;
+    detail::Device<S::dim> dev(grid.box(), particles.size());
+    dev.upload(particles);
+    detail::check(srm_b200_reorder_by_locality(dev.get(), grid.cell_size(), remap.data()), dev.get(), true);
+    dev.download(particles);
+    return remap;
+}
+
+// shape.hpp:549-555 (the device counts overlapping pairs; any collision <=> count > 0)
+template <ShapeModel S>
+bool shape_any_collision(std::span<const typename S::ParticleT> particles, const CellGrid<S::dim>& grid) {
+    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    if (particles.empty()) return false;
+    detail::Device<S::dim> dev(grid.box(), particles.size());
+    dev.upload(particles);
+    srm_b200_round_stats st{};
+    detail::check(srm_b200_overlap_stats(dev.get(), grid.cell_size(), &st), dev.get(), true);
+    return st.overlap_pairs > 0;
+}
+
+// rsa.hpp:21-61 with Rng(seed): bit-identical to srm::rsa_place for a fresh Rng(seed)
+template <int N>
+std::vector<Particle<N>> rsa_place(std::span<const double> radii, const PeriodicBox<N>& box,
+                                   std::size_t max_attempts_per_particle, std::uint64_t seed) {
+    double L[3] = {1.0, 1.0, 1.0};
+    for (int a = 0; a < N; ++a) L[a] = box.length(a);
+    std::vector<double> pos(radii.size() * N);
+    std::vector<int32_t> ids(radii.size());
+    int64_t placed = 0;
+    const int st = srm_b200_rsa_place(N, L, static_cast<int64_t>(radii.size()), radii.data(),
+                                      static_cast<int64_t>(max_attempts_per_particle), seed, pos.data(), ids.data(),
+                                      &placed);
+    if (st == SRM_B200_PLACEMENT_FAILURE)
+        throw PlacementFailure("rsa_place: exceeded " + std::to_string(max_attempts_per_particle) +
+                                   " attempts after placing " + std::to_string(placed) +
+                                   " particles; initial volume fraction too high",
+                               static_cast<std::size_t>(placed), max_attempts_per_particle);
+    if (st == SRM_B200_INVALID) throw ValidationError("rsa_place: invalid radii or box");
+    std::vector<Particle<N>> out(radii.size());
+    for (std::size_t i = 0; i < radii.size(); ++i) {
+        out[i].id = ids[i];
+        for (int a = 0; a < N; ++a) out[i].pos[a] = pos[i * N + a];
+        out[i].radius = radii[i];
+    }
+    return out;
+}
+
+}  // namespace srm::b200
