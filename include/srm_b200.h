@@ -194,10 +194,9 @@ int srm_b200_sync(srm_b200_ctx* ctx);
 /* CUDA-event stopwatch on the context stream: op 0 records the start event, op 1
  * records the stop event, waits for it and writes the elapsed device milliseconds. */
 int srm_b200_stopwatch(srm_b200_ctx* ctx, int op, double* ms);
-/* Diagnostics of the last round whose statistics were read: info[0] attempt-0 rejects,
- * [1] shared-memory bricks that fell back to global memory, [2] bricks launched (0 =
- * untiled), [3] brick capacity (particles), [4] brick shared memory bytes, [5] brick
- * width in cells. */
+/* Diagnostics of the last round whose statistics were read: info[0] non-movers,
+ * [1] colour classes of the sweep, [2] largest cells per class, [3] near-search half
+ * width (x), [4] colouring modulus (x), [5] cells of the grid. */
 int srm_b200_last_round_info(srm_b200_ctx* ctx, int64_t* info);
 
 /* ---- self tests of the device primitives (no reference counterpart) ------------------ */

@@ -311,59 +311,92 @@ static void build_pairs(int dim, const double* L, int64_t n, const double* x, co
 }
 
 /* ------------------------------------------------------------------------------ */
-/* Parallel migrate round ("J-phase").  For l = 0 .. n_l-1, every
- * particle that has not yet accepted proposes p_i = propose(x0_i, attempt l); the
- * proposal is accepted iff for every j with id_j != id_i:
- *   j still active in phase l :  p_i clears x0_j  and  p_i clears p_j
- *   j accepted in phase m < l :  p_i clears xnew_j
- * using the reference predicate (shape.hpp:508-511, trial first as in
- * shape.hpp:539-546).  Decisions of one phase are simultaneous.  The reference's
- * per-particle loop structure (engine.hpp:94-104: <= n_l trials from the pre-sweep
- * position, first clear trial kept, otherwise an exact revert) is kept.             */
-void orc_migrate_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
-                       const int32_t* id, const int32_t* slot, double c_m, int n_l,
-                       uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
-                       uint8_t* acc, int brute) {
+/* Colouring of the round grid.  Per axis: s = smallest s >= 1 with
+ * s * edge >= cutc, cutc = (2 maxR + 3 c_m)(1+1e-9)^2 + ..., the reach of any trial
+ * against any (possibly moving) neighbour; "all" when 2s+1 >= dims (every coordinate its
+ * own colour), else modulus m = s+1 with the tail cells (dims mod m) each its own
+ * colour.  Two cells of one class are then farther apart than any interaction.      */
+void orc_colouring(int dim, const int32_t* dims, const double* edge, double maxr, double c_m,
+                   int32_t* m_out, int32_t* ncol_out) {
+    const double cutc = ((maxr + maxr + 3.0 * c_m) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
+    for (int a = 0; a < 3; ++a) {
+        if (a >= dim) { m_out[a] = 1; ncol_out[a] = 1; continue; }
+        int64_t s = 1;
+        while ((double)s * edge[a] < cutc && 2 * s + 1 < dims[a]) ++s;
+        if (2 * s + 1 >= dims[a]) { m_out[a] = dims[a]; ncol_out[a] = dims[a]; }
+        else { m_out[a] = (int32_t)(s + 1); ncol_out[a] = (int32_t)(s + 1) + dims[a] % (int32_t)(s + 1); }
+    }
+}
+
+static int colour1(int x, int m, int n) {
+    const int body = m * (n / m);
+    return x < body ? x % m : m + (x - body);
+}
+
+/* One SRM round's migrate as a coloured Gauss-Seidel sweep: the
+ * reference's migrate (engine.hpp:89-107) -- per particle <= n_l trials from its
+ * pre-sweep position, each tested against the LIVE positions of all other particles
+ * (shape.hpp:539-546, trial first), first clear trial kept, otherwise an exact revert --
+ * in the order (colour class, cell, slot) of the round grid of cell size `cell_size`
+ * instead of storage order.  Cells of one class never interact, so the GPU runs them
+ * concurrently and equals this sequential sweep bit for bit.  Trials draw Philox
+ * (orc_propose) instead of mt19937_64.  brute != 0: all-pairs candidate search.      */
+void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
+                     const int32_t* id, const int32_t* slot, double cell_size, double c_m, int n_l,
+                     uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
+                     uint8_t* acc, int brute) {
+    int32_t dims[3] = {1, 1, 1};
+    double edge[3] = {1.0, 1.0, 1.0};
+    orc_grid_dims(dim, L, cell_size, dims, edge);
+    const double maxr = orc_max_radius(n, r);
+    int32_t m[3], ncol[3];
+    orc_colouring(dim, dims, edge, maxr, c_m, m, ncol);
+    /* candidates: j whose round-start distance is within ri + rj + 2 c_m (a superset of
+       every j a trial of i can touch while j sits within c_m of its start) */
     orc_csr nb;
     build_pairs(dim, L, n, x0, r, 2.0 * c_m, brute, &nb);
-    double* prop = (double*)malloc(sizeof(double) * (size_t)(n * dim + 1));
-    uint8_t* dec = (uint8_t*)malloc((size_t)(n + 1));
+    int64_t ncells = 1;
+    for (int a = 0; a < dim; ++a) ncells *= dims[a];
+    uint32_t* keys = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(n + 1));
+    orc_keys(dim, dims, edge, n, x0, keys);
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int64_t* cstart = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ncells + 1));
+    orc_sort_by_cell(n, keys, slot, ncells, order, cstart);
+    /* class of every particle, then a stable pass per class in (cell, slot) order */
+    int32_t* cls = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int64_t nclass = (int64_t)ncol[0] * ncol[1] * ncol[2];
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t c[3];
+        orc_cell_coords(dim, dims, edge, x0 + i * dim, c);
+        int64_t k = 0;
+        for (int a = dim - 1; a >= 0; --a) k = k * ncol[a] + colour1(c[a], m[a], dims[a]);
+        cls[i] = (int32_t)k;
+    }
     memcpy(xnew, x0, sizeof(double) * (size_t)(n * dim));
     for (int64_t i = 0; i < n; ++i) acc[i] = ORC_NOT_ACCEPTED;
-    for (int l = 0; l < n_l; ++l) {
-        int64_t active = 0;
-        for (int64_t i = 0; i < n; ++i) {
-            if (acc[i] != ORC_NOT_ACCEPTED) continue;
-            ++active;
-            orc_propose(dim, L, x0 + i * dim, c_m, seed, (uint32_t)slot[i], (uint32_t)l, round_id,
-                        iteration, prop + i * dim);
-        }
-        if (active == 0) break;
-        for (int64_t i = 0; i < n; ++i) {
-            dec[i] = 0;
-            if (acc[i] != ORC_NOT_ACCEPTED) continue;
-            int ok = 1;
-            for (int64_t t = nb.start[i]; t < nb.start[i + 1] && ok; ++t) {
-                const int64_t j = nb.nbr[t];
-                if (id[j] == id[i]) continue;
-                if (acc[j] == ORC_NOT_ACCEPTED) {
-                    if (sphere_overlap(dim, L, prop + i * dim, r[i], x0 + j * dim, r[j])) ok = 0;
-                    else if (sphere_overlap(dim, L, prop + i * dim, r[i], prop + j * dim, r[j])) ok = 0;
-                } else {
-                    if (sphere_overlap(dim, L, prop + i * dim, r[i], xnew + j * dim, r[j])) ok = 0;
+    double p[3];
+    for (int64_t k = 0; k < nclass; ++k) {
+        for (int64_t q = 0; q < n; ++q) { /* q walks the (cell, slot) order */
+            const int64_t i = order[q];
+            if (cls[i] != k) continue;
+            for (int l = 0; l < n_l; ++l) {
+                orc_propose(dim, L, x0 + i * dim, c_m, seed, (uint32_t)slot[i], (uint32_t)l, round_id,
+                            iteration, p);
+                int ok = 1;
+                for (int64_t t = nb.start[i]; t < nb.start[i + 1] && ok; ++t) {
+                    const int64_t j = nb.nbr[t];
+                    if (id[j] == id[i]) continue;
+                    if (sphere_overlap(dim, L, p, r[i], xnew + j * dim, r[j])) ok = 0;
                 }
-            }
-            dec[i] = (uint8_t)ok;
-        }
-        for (int64_t i = 0; i < n; ++i) {
-            if (acc[i] == ORC_NOT_ACCEPTED && dec[i]) {
-                acc[i] = (uint8_t)l;
-                memcpy(xnew + i * dim, prop + i * dim, sizeof(double) * (size_t)dim);
+                if (ok) {
+                    memcpy(xnew + i * dim, p, sizeof(double) * (size_t)dim);
+                    acc[i] = (uint8_t)l;
+                    break;
+                }
             }
         }
     }
-    free(prop);
-    free(dec);
+    free(keys); free(order); free(cstart); free(cls);
     csr_free(&nb);
 }
 

@@ -13,15 +13,16 @@
  *   - overlap predicates       (shape.hpp:508-511, cell_grid.hpp:454-472)
  *   - Philox4x32-10            (Salmon et al. SC'11; checked against curand's
  *                               curand_Philox4x32_10 and the Random123 KAT vectors)
- *   - the parallel ("J-phase") migrate round that the GPU implements; this one has no
- *     reference counterpart bit for bit (the reference sweep is sequential
- *     Gauss-Seidel over one mt19937_64 stream, engine.hpp:89-107), see DESIGN.md §3.
+ *   - the migrate round the GPU implements: the reference's sequential Gauss-Seidel
+ *     migrate (engine.hpp:89-107) in a colour-class order with Philox trials instead of
+ *     storage order with one mt19937_64 stream, see DESIGN.md §3.
  *
  * Parity status: the grid/key/sort/overlap functions are PINNED against the reference
  * itself (oracle/_ref, built from /root/reference sources) and the reference's own
- * known-answer test cases (tests/test_oracle_pins.py).  The parallel round semantics
- * is a new algorithm; it is pinned to the reference through its primitives (same
- * propose_move arithmetic, same overlap predicate) and end to end statistically.
+ * known-answer test cases (tests/test_oracle_pins.py).  The sweep keeps the
+ * reference's per-particle algorithm; only the visiting order and the random stream
+ * differ, so it is pinned to the reference through its primitives (same propose_move
+ * arithmetic, same overlap predicate) and end to end statistically.
  */
 #ifndef SRM_ORACLE_H
 #define SRM_ORACLE_H
@@ -67,14 +68,19 @@ typedef struct {
     int64_t movers;          /* particles that accepted a trial this round          */
 } orc_round_stats;
 
-/* One parallel migrate round for disks/spheres:
- *   x0[n*dim] round-start positions, r[n], id[n], slot[n] (Philox stream id);
- *   xnew[n*dim] out, acc[n] out (phase of acceptance or 255).
- * brute != 0 forces the O(n^2) all-pairs search (no cell list). */
-void orc_migrate_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
-                       const int32_t* id, const int32_t* slot, double c_m, int n_l,
-                       uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
-                       uint8_t* acc, int brute);
+/* Colouring of the round grid: per-axis modulus m and colour count. */
+void orc_colouring(int dim, const int32_t* dims, const double* edge, double maxr, double c_m,
+                   int32_t* m_out, int32_t* ncol_out);
+
+/* One SRM round's migrate for disks/spheres as the coloured Gauss-Seidel sweep of
+ * DESIGN.md §3.1 on the round grid of cell size `cell_size`:
+ *   x0[n*dim] round-start positions, r[n], id[n], slot[n] (Philox stream and in-cell
+ *   order); xnew[n*dim] out, acc[n] out (attempt of acceptance or 255).
+ * brute != 0 forces the O(n^2) all-pairs candidate search. */
+void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
+                     const int32_t* id, const int32_t* slot, double cell_size, double c_m, int n_l,
+                     uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
+                     uint8_t* acc, int brute);
 
 /* Global overlap statistics of a state (all pairs, cell-list accelerated). */
 void orc_overlap_stats(int dim, const double* L, int64_t n, const double* x, const double* r,

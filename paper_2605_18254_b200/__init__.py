@@ -338,8 +338,8 @@ class Context:
     def last_round_info(self) -> dict:
         v = (C.c_int64 * 6)()
         self._c(_native.lib().srm_b200_last_round_info(self._h, v))
-        return {"rejected_attempt0": v[0], "fallback_bricks": v[1], "bricks": v[2], "brick_cap": v[3],
-                "brick_smem_bytes": v[4], "brick_cells_x": v[5]}
+        return {"nonmovers": v[0], "colour_classes": v[1], "cells_per_class": v[2], "near_half_width": v[3],
+                "colour_modulus": v[4], "cells": v[5]}
 
     def stopwatch_start(self) -> None:
         """record a CUDA event on the context stream"""

@@ -15,7 +15,6 @@
 
 #include "../../include/srm_b200.h"
 #include "srm_kernels.cuh"
-#include "srm_tiles.cuh"
 
 using namespace srmb;
 
@@ -71,12 +70,8 @@ struct srm_b200_ctx {
     uint32_t* key = nullptr;
     uint32_t* skey = nullptr;
     int32_t* perm = nullptr;
-    int32_t* active = nullptr;  // attempt-0 reject list
-    TileParams* tpp = nullptr;
-    TileParams ht{};
+    int32_t* active = nullptr;  // non-mover list of the current round
     uint8_t* acc = nullptr;
-    int32_t* nbr = nullptr;
-    uint8_t* nbr_cnt = nullptr;
 
     uint32_t* count = nullptr;
     int64_t* cell_start = nullptr;
@@ -114,9 +109,7 @@ struct srm_b200_ctx {
     bool hg_set = false;
 
     cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
-    bool force_global = false;  // SRM_B200_NO_TILES=1: phase 0 without shared-memory bricks
-    int64_t last_fallback_tiles = 0;
-    int64_t last_rejected0 = 0;
+    int64_t last_nonmovers = 0;
 
     // ---------------------------------------------------------------------------
     cudaEvent_t take_event() {
@@ -193,19 +186,9 @@ struct srm_b200_ctx {
         skey = dalloc<uint32_t>(cap);
         perm = dalloc<int32_t>(cap);
         acc = dalloc<uint8_t>(cap);
-        nbr = dalloc<int32_t>(cap * kNbrCap);
-        nbr_cnt = dalloc<uint8_t>(cap);
         gp = dalloc<GridParams>(1);
         rp = dalloc<RoundParams>(1);
-        tpp = dalloc<TileParams>(1);
-        if (const char* e = std::getenv("SRM_B200_NO_TILES")) force_global = e[0] == '1';
         active = dalloc<int32_t>(cap);
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_tiled<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_pairs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
-        SRM_CUDA(cudaFuncSetAttribute(k_phase0_pairs<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmemMax));
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -221,9 +204,9 @@ struct srm_b200_ctx {
         free_state(P);
         free_state(Q);
         free_state(S);
-        cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc); cudaFree(nbr);
-        cudaFree(nbr_cnt); cudaFree(count); cudaFree(cell_start); cudaFree(partial);
-        cudaFree(gp); cudaFree(rp); cudaFree(tpp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
+        cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
+        cudaFree(count); cudaFree(cell_start); cudaFree(partial);
+        cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -234,9 +217,11 @@ struct srm_b200_ctx {
     }
 
     // ---------------------------------------------------------------------------
-    // CellGrid ctor (cell_grid.hpp:288-309) + the near-search stencil for a state
-    // whose largest radius is max_r_state and whose moves reach `extra`/2.
-    GridParams make_grid(double cell_size, double max_r_state, double extra) const {
+    // CellGrid ctor (cell_grid.hpp:288-309) + the near-search stencil and the colouring
+    // for a state whose largest radius is max_r_state and whose trial
+    // moves have length c_m.  The colouring expression is the oracle's orc_colouring.
+    GridParams make_grid(double cell_size, double max_r_state, double c_m) const {
+        const double extra = 2.0 * c_m;
         if (!(cell_size > 0.0)) throw Invalid{"CellGrid: cell_size must be positive"};
         GridParams g{};
         g.ncells = 1;
@@ -264,6 +249,28 @@ struct srm_b200_ctx {
             while (static_cast<double>(s) * g.edge[a] < cut && 2 * s + 1 < g.dims[a]) ++s;
             g.near_s[a] = (2 * s + 1 >= g.dims[a]) ? -1 : static_cast<int32_t>(s);
         }
+        // colouring: two cells of one class are more than any trial's reach apart
+        const double cutc = ((max_r_state + max_r_state + 3.0 * c_m) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
+        g.ncls = 1;
+        g.cls_cells = 1;
+        for (int a = 0; a < 3; ++a) {
+            if (a >= dim) {
+                g.col_m[a] = 1;
+                g.col_n[a] = 1;
+                continue;
+            }
+            int64_t s = 1;
+            while (static_cast<double>(s) * g.edge[a] < cutc && 2 * s + 1 < g.dims[a]) ++s;
+            if (2 * s + 1 >= g.dims[a]) {
+                g.col_m[a] = g.dims[a];
+                g.col_n[a] = g.dims[a];
+            } else {
+                g.col_m[a] = static_cast<int32_t>(s + 1);
+                g.col_n[a] = g.col_m[a] + g.dims[a] % g.col_m[a];
+            }
+            g.ncls *= g.col_n[a];
+            g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
+        }
         return g;
     }
 
@@ -282,121 +289,12 @@ struct srm_b200_ctx {
         cell_cap = c;
     }
 
-    // Brick decomposition for k_phase0_tiled.  Per-axis brick widths are searched so
-    // that a brick holds at most ~230 particles on average (one per thread of a
-    // 256-thread CTA; bigger bricks mean less halo), staged capacity = mean + 5 sigma
-    // (Poisson) + 32, shared memory <= kTileSmemMax.  Axes whose brick would cover the
-    // whole axis (or whose stencil does) are staged whole, in global order.
-    TileParams build_tiles(const GridParams& g, const int* Bw, double occ, bool& fits) const {
-        TileParams tp{};
-        fits = false;
-        int nst[3];
-        int64_t ntiles = 1;
-        int ncr = 1;
-        double ext = 0.0, centre = occ;
-        bool bricks_only = true;
-        for (int a = 0; a < 3; ++a) {
-            AxisTile A{};
-            if (a >= dim) {
-                A.full = 1; A.all = 1; A.B = 1; A.ntile = 1; A.s = 0;
-                nst[a] = 1;
-            } else {
-                const int s = g.near_s[a], d = g.dims[a];
-                A.all = s < 0 ? 1 : 0;
-                A.s = s < 0 ? 0 : s;
-                if (A.all || Bw[a] + 2 * s >= d) {
-                    A.full = 1; A.B = d; A.ntile = 1; nst[a] = d;
-                    ext = std::max(ext, box.L[a]);
-                    bricks_only = false;
-                } else {
-                    A.full = 0; A.B = Bw[a]; A.ntile = (d + Bw[a] - 1) / Bw[a]; nst[a] = Bw[a] + 2 * s;
-                    ext = std::max(ext, nst[a] * g.edge[a]);
-                }
-                if (!A.all && 2 * A.s + 1 > 16) return tp;
-                if (A.all && a > 0 && d > 16) return tp;
-                if (a > 0) ncr *= A.B;
-                centre *= A.B;
-            }
-            tp.ax[a] = A;
-            ntiles *= A.ntile;
-        }
-        const int rows = nst[1] * nst[2];
-        if (rows > kMaxRows || ncr > kTileThreads) return tp;
-        const double staged = occ * nst[0] * nst[1] * nst[2];
-        int capS = static_cast<int>(std::ceil(staged + 5.0 * std::sqrt(staged) + 32.0));
-        int capC = static_cast<int>(std::ceil(centre + 5.0 * std::sqrt(centre) + 32.0));
-        capS = (capS + 31) / 32 * 32;
-        capC = (capC + 31) / 32 * 32;
-        int maxseg = 1;
-        for (int a = 1; a < dim; ++a) maxseg *= 2 * tp.ax[a].s + 1;
-        int64_t smem;
-        if (bricks_only) {  // k_phase0_pairs layout
-            smem = static_cast<int64_t>(capS) * (16 + 16 + 4 + 4) + static_cast<int64_t>(capC) * 8 * dim +
-                   static_cast<int64_t>(rows) * (nst[0] + 1) * 4 + kTileThreads * kNbrBuf * 2 +
-                   static_cast<int64_t>(kTileThreads) * maxseg * 4;
-        } else {  // k_phase0_tiled layout
-            smem = static_cast<int64_t>(capS) * (16 + 8 * dim + 8 + 12) + static_cast<int64_t>(capC) * (16 + 8 * dim) +
-                   static_cast<int64_t>(rows) * (nst[0] + 1) * 4;
-        }
-        smem = (smem + 15) / 16 * 16;
-        if (smem > kTileSmemMax) return tp;
-        tp.maxseg = maxseg;
-        tp.ntiles = ntiles;
-        tp.capS = capS;
-        tp.capC = capC;
-        for (int a = 0; a < 3; ++a) {
-            tp.nst_max[a] = nst[a];
-            tp.edge_f[a] = static_cast<float>(a < dim ? g.edge[a] : 1.0);
-        }
-        tp.margin = static_cast<float>(16.0 * std::ldexp(1.0, -24) * ext);
-        tp.extra_f = static_cast<float>(g.extra);
-        tp.rmax_f = static_cast<float>(g.rmax);
-        tp.bricks_only = bricks_only ? 1 : 0;
-        tp.smem_bytes = static_cast<int32_t>(smem);
-        tp.enabled = 1;
-        fits = true;
-        return tp;
-    }
-
-    TileParams make_tiles(const GridParams& g) const {
-        TileParams best{};
-        best.enabled = 0;
-        if (n == 0) return best;
-        const double occ = static_cast<double>(n) / static_cast<double>(g.ncells);
-        const double target = 230.0;
-        double best_score = -1.0;
-        const int bmax = 24;
-        for (int b0 = 1; b0 <= bmax; ++b0)
-            for (int b1 = 1; b1 <= (dim >= 2 ? b0 : 1); ++b1)
-                for (int b2 = 1; b2 <= (dim == 3 ? b1 : 1); ++b2) {
-                    const double centre = occ * b0 * b1 * (dim == 3 ? b2 : 1);
-                    if (centre > target) continue;
-                    const int Bw[3] = {b0, b1, b2};
-                    bool fits = false;
-                    const TileParams tp = build_tiles(g, Bw, occ, fits);
-                    if (!fits) continue;
-                    // prefer full bricks, then less halo per brick particle
-                    const double staged = static_cast<double>(tp.nst_max[0]) * tp.nst_max[1] * tp.nst_max[2];
-                    const double cells = static_cast<double>(b0) * b1 * (dim == 3 ? b2 : 1);
-                    const double score = centre / target - 0.25 * staged / cells;
-                    if (score > best_score) {
-                        best_score = score;
-                        best = tp;
-                    }
-                }
-        return best;
-    }
-
-
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
         k_set_grid<<<1, 1, 0, stream>>>(gp, g);
         launched();
         hg = g;
         hg_set = true;
-        ht = make_tiles(g);
-        k_set_tiles<<<1, 1, 0, stream>>>(tpp, ht);
-        launched();
     }
 
     void set_round(double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration) {
@@ -435,49 +333,37 @@ struct srm_b200_ctx {
         launched();
     }
 
-    // one round on T (T is rewritten in this round's sorted order); gp must be set
+    // One round on T (T is rewritten in this round's sorted order); gp must be set.
+    // grid rebuild, then the coloured Gauss-Seidel sweep (one launch per colour class),
+    // then the overlap reduction over the non-movers.
     void round(State& T, double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
                bool with_stats, bool with_candidates) {
         if (n_l > kMaxPhases) throw Invalid{"n_l > 254 is not supported by the B200 path"};
         set_round(c_m, n_l, seed, round_id, iteration);
         grid_build(T);
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
-        const int nb = blocks_for(n, 256);
+        SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
             FamScope fs(this, 1);
-            if (ht.enabled && !force_global) {
-                const int grid = static_cast<int>(std::min<int64_t>(ht.ntiles, 2147483647));
-                auto kern = dim == 2 ? (ht.bricks_only ? k_phase0_pairs<2> : k_phase0_tiled<2, false>)
-                                     : (ht.bricks_only ? k_phase0_pairs<3> : k_phase0_tiled<3, false>);
-                kern<<<grid, kTileThreads, ht.smem_bytes, stream>>>(S, T, box, gp, tpp, rp, cell_start, skey, acc, nbr,
-                                                                    nbr_cnt, active, stats);
-            } else {
+            const int sb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(hg.cls_cells, 128), 148 * 64)));
+            for (int cls = 0; cls < hg.ncls; ++cls) {
                 if (dim == 2)
-                    k_phase0<2><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                    k_sweep_class<2><<<sb, 128, 0, stream>>>(cls, S, T, box, gp, rp, cell_start, skey, acc, active, stats);
                 else
-                    k_phase0<3><<<nb, 256, 0, stream>>>(n, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                    k_sweep_class<3><<<sb, 128, 0, stream>>>(cls, S, T, box, gp, rp, cell_start, skey, acc, active, stats);
             }
-            launched();
-        }
-        const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
-        if (n_l > 1) {
-            FamScope fs(this, 2);
-            for (int l = 1; l < n_l; ++l) {
-                if (dim == 2)
-                    k_phase_list<2><<<lb, 256, 0, stream>>>(l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
-                else
-                    k_phase_list<3><<<lb, 256, 0, stream>>>(l, S, T, box, gp, rp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
-            }
-            launched(n_l - 1);
+            launched(hg.ncls);
         }
         if (with_stats) {
             FamScope fs(this, 3);
+            const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
             if (dim == 2)
-                k_stats_list<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
             else
-                k_stats_list<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, nbr, nbr_cnt, active, stats);
+                k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
             launched();
             if (with_candidates) {
+                const int nb = blocks_for(n, 256);
                 if (dim == 2) k_candidates<2><<<nb, 256, 0, stream>>>(n, gp, cell_start, skey, stats);
                 else k_candidates<3><<<nb, 256, 0, stream>>>(n, gp, cell_start, skey, stats);
                 launched();
@@ -494,9 +380,8 @@ struct srm_b200_ctx {
         std::memcpy(&pen, &h_stats->pen_bits, sizeof(double));
         o.max_penetration = pen;
         o.candidate_pairs = with_candidates ? static_cast<int64_t>(h_stats->candidate_pairs) : -1;
-        o.movers = n - static_cast<int64_t>(h_stats->nonmovers);
-        last_fallback_tiles = static_cast<int64_t>(h_stats->fallback_tiles);
-        last_rejected0 = static_cast<int64_t>(h_stats->active_count);
+        o.movers = n - static_cast<int64_t>(h_stats->active_count);
+        last_nonmovers = static_cast<int64_t>(h_stats->active_count);
         return o;
     }
 
@@ -798,7 +683,7 @@ int srm_b200_round(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint6
         srm_b200_round_stats o{0, 0.0, with_candidates ? 0 : -1, 0};
         if (n > 0) {
             const double mr = c->max_radius(c->P);
-            const GridParams g = c->make_grid(cell_size, mr, 2.0 * c_m);
+            const GridParams g = c->make_grid(cell_size, mr, c_m);
             // the reference scans the 3^d cells of the trial position, which is only
             // complete under CellGrid's safety bound (cell_grid.hpp:288-293)
             if (cell_size < 2.0 * mr + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
@@ -825,7 +710,7 @@ int srm_b200_rounds(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint
         if (n > 0 && rounds > 0) {
             const double mr = c->max_radius(c->P);
             if (cell_size < 2.0 * mr + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
-            const GridParams g = c->make_grid(cell_size, mr, 2.0 * c_m);
+            const GridParams g = c->make_grid(cell_size, mr, c_m);
             c->set_grid(g);
             for (int k = 0; k < rounds; ++k) c->round(c->P, c_m, n_l, key, first_round + k, iteration, true, false);
             o = c->read_stats(false);
@@ -843,7 +728,7 @@ int srm_b200_relax_sweeps(srm_b200_ctx* c, double c_m, double c_r, int n_l, int 
         if (n_l < 1) throw Invalid{"params: n_l must be >= 1"};
         const double max_r = c->max_radius(c->P);
         const double cs = 2.5 * max_r + c_m;  // engine.hpp:116-117
-        const GridParams g = c->make_grid(cs, max_r, 2.0 * c_m);
+        const GridParams g = c->make_grid(cs, max_r, c_m);
         if (cs < 2.0 * max_r + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
         c->set_grid(g);
         for (int k = 0; k < sweeps; ++k) c->round(c->P, c_m, n_l, key, static_cast<uint32_t>(k), 0u, false, false);
@@ -930,7 +815,7 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
             const double cs = 2.5 * max_r + p.c_m;
             if (cs < 2.0 * (max_r * factor) + p.c_m)  // CellGrid(box, cs, max_r*factor, c_m)
                 throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
-            const GridParams gq = c->make_grid(cs, max_r * factor, 2.0 * p.c_m);
+            const GridParams gq = c->make_grid(cs, max_r * factor, p.c_m);
             c->set_grid(gq);
 
             c->copy_state(c->P, c->Q);
@@ -963,7 +848,7 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
                 }
             } else {
                 // shake: n_k sweeps on the pre-swell state with the same grid (engine.hpp:244-249)
-                const GridParams gp_ = c->make_grid(cs, max_r, 2.0 * p.c_m);
+                const GridParams gp_ = c->make_grid(cs, max_r, p.c_m);
                 c->set_grid(gp_);
                 for (int k = 0; k < p.n_k; ++k) {
                     c->round(c->P, p.c_m, p.n_l, p.seed, static_cast<uint32_t>(p.n_k + k), static_cast<uint32_t>(it), false, false);
@@ -1030,12 +915,12 @@ int srm_b200_sync(srm_b200_ctx* c) {
 
 int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
     return guarded(c, [&]() -> int {
-        info[0] = c->last_rejected0;
-        info[1] = c->last_fallback_tiles;
-        info[2] = c->ht.enabled && !c->force_global ? c->ht.ntiles : 0;
-        info[3] = c->ht.enabled ? c->ht.capS : 0;
-        info[4] = c->ht.enabled ? c->ht.smem_bytes : 0;
-        info[5] = c->ht.enabled ? c->ht.ax[0].B : 0;
+        info[0] = c->last_nonmovers;
+        info[1] = c->hg.ncls;
+        info[2] = c->hg.cls_cells;
+        info[3] = c->hg.near_s[0];
+        info[4] = c->hg.col_m[0];
+        info[5] = c->hg.ncells;
         return SRM_B200_OK;
     });
 }

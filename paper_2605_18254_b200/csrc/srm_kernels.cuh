@@ -3,8 +3,8 @@
 // One SRM round (engine.hpp:227-234: build_shape_grid -> migrate -> shape_any_collision)
 // is, on the device:
 //   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
-//   migrate        k_phase0 (fused near-list build + attempt 0) -> k_phase (attempts >= 1)
-//   reduction      k_stats  (overlap pairs, max penetration, movers, candidate pairs)
+//   migrate        k_sweep_class, one launch per colour class (coloured Gauss-Seidel)
+//   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
 // All kernels read the grid / round parameters from device memory so that the same
 // launches can be replayed from a CUDA graph.  DESIGN.md §2-§4 has the data layout
 // and the roofline of each kernel.
@@ -16,8 +16,6 @@
 
 namespace srmb {
 
-constexpr int kNbrCap = 32;  // near-list capacity per particle; overflow -> full rescan
-constexpr uint8_t kOverflow = 255;
 constexpr int kScanTile = 4096;  // cells per scan tile (1024 threads x 4)
 
 struct GridParams {
@@ -27,6 +25,10 @@ struct GridParams {
     int32_t near_s[3];  // near-search half width per axis; -1 = every cell on the axis
     double extra;       // near cutoff: (ri + rj + extra) * (1 + 1e-9) + 1e-300
     double rmax;        // largest radius of the state the grid indexes
+    int32_t col_m[3];   // colouring modulus per axis
+    int32_t col_n[3];   // colours per axis
+    int32_t ncls;       // colour classes = col_n[0] * col_n[1] * col_n[2]
+    int64_t cls_cells;  // largest number of cells in one class
 };
 
 struct RoundParams {
@@ -47,10 +49,7 @@ struct StatsDev {
     unsigned long long overlap_pairs;
     unsigned long long pen_bits;  // max penetration as the bits of a non-negative double
     unsigned long long candidate_pairs;
-    unsigned long long nonmovers;     // particles that kept their round-start position
-    unsigned long long active_count;  // length of the attempt-0 reject list
-    unsigned long long fallback_tiles;  // phase-0 tiles that overflowed shared memory
-    unsigned long long rejected[256];  // rejected after phase l (early exit of later phases)
+    unsigned long long active_count;  // non-movers: particles that kept their round-start position
 };
 
 __device__ __forceinline__ double near_cut(double ri, double rj, double extra) {
@@ -298,136 +297,73 @@ __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
     for (int a = 0; a < D; ++a) p[a] = S.x[a][i];
 }
 
-// Rejected particles of attempt 0 are appended to the active list (warp-aggregated).
-__device__ __forceinline__ void push_active(bool rejected, int64_t i, int32_t* __restrict__ active,
-                                            StatsDev* stats) {
-    const unsigned full = __activemask();
-    const unsigned m = __ballot_sync(full, rejected);
-    if (!m) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(&stats->active_count, (unsigned long long)__popc(m));
-    base = __shfl_sync(full, base, leader);
-    if (rejected) active[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
+// ---------------------------------------------------------------------------------
+// Migrate: coloured Gauss-Seidel sweep.
+//
+// The reference's migrate (engine.hpp:89-107) visits particles in storage order; each
+// gets <= n_l trials from its pre-sweep position and keeps the first one that clears the
+// LIVE positions of all others.  Here the visiting order is (colour class, cell, slot):
+// cells are coloured so that two cells of one class are farther apart than any trial can
+// reach (GridParams::col_*), hence one class is swept by one launch with a thread per
+// cell, particles of a cell sequentially in slot order, and the result is identical to
+// the sequential sweep in that order (oracle/srm_oracle.c orc_sweep_round).
+//
+// Live positions: a particle that accepted in this round (acc != 255) lives at T.x, every
+// other one at its round-start position S.x.
+
+template <int D>
+__device__ __forceinline__ void live_pos(const State& S, const State& T, const uint8_t* __restrict__ acc, int64_t j,
+                                         double* p) {
+    if (acc[j] != kNotAccepted) load_pos<D>(T, j, p);
+    else load_pos<D>(S, j, p);
 }
 
-// Migrate attempt 0 fused with the near-list build for one particle, straight from
-// global memory (the fallback of the tiled kernel).  S = sorted round-start state
-// (read only), T = output state (sorted order): T.x = new positions, T.r/id/slot copied.
+constexpr int kNearLocal = 16;  // near candidates kept per particle; more -> rescan per trial
+
 template <int D>
-__device__ __forceinline__ bool phase0_global(int64_t i, const State& S, const State& T, const Box& box,
-                                              const GridParams& g, const RoundParams& rp,
-                                              const int64_t* __restrict__ cs,
-                                              const uint32_t* __restrict__ skey,
-                                              uint8_t* __restrict__ acc, int32_t* __restrict__ nbr,
-                                              uint8_t* __restrict__ nbr_cnt) {
-    double xi[D], p[D];
-    load_pos<D>(S, i, xi);
-    const double ri = S.r[i];
-    const int32_t idi = S.id[i];
-    const int32_t sloti = S.slot[i];
-    propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sloti), 0u, p);
-    bool ok = true;
+__device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const State& T, const Box& box,
+                                               const GridParams& g, const RoundParams& rp,
+                                               const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                               uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                               StatsDev* stats) {
+    double xi[D];
+    load_pos<D>(S, q, xi);
+    const double ri = S.r[q];
+    const int32_t idi = S.id[q];
+    const int32_t sl = S.slot[q];
+    // candidates: j whose round-start distance is within ri + rj + 2 c_m -- every j a
+    // trial of q can touch while j sits within c_m of its start
+    int32_t nb[kNearLocal];
     int nn = 0;
     bool overflow = false;
-    int32_t* my = nbr + i * kNbrCap;
-    for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+    const uint32_t kq = skey[q];
+    for_near_ranges<D>(g, cs, kq, g.near_s, [&](int64_t b, int64_t e) {
         for (int64_t j = b; j < e; ++j) {
-            if (j == i) continue;
+            if (j == q) continue;
             double xj[D];
             load_pos<D>(S, j, xj);
-            const double rj = S.r[j];
-            if (dist2<D>(box, xi, xj) > near_cut(ri, rj, g.extra)) continue;
-            if (nn < kNbrCap) my[nn++] = static_cast<int32_t>(j);
+            if (dist2<D>(box, xi, xj) > near_cut(ri, S.r[j], g.extra)) continue;
+            if (nn < kNearLocal) nb[nn++] = static_cast<int32_t>(j);
             else overflow = true;
-            if (!ok || S.id[j] == idi) continue;
-            if (sphere_overlap<D>(box, p, ri, xj, rj)) { ok = false; continue; }
-            double pj[D];
-            propose<D>(box, xj, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[j]), 0u, pj);
-            if (sphere_overlap<D>(box, p, ri, pj, rj)) ok = false;
         }
     });
-#pragma unroll
-    for (int a = 0; a < D; ++a) T.x[a][i] = ok ? p[a] : xi[a];
-    T.r[i] = ri;
-    T.id[i] = idi;
-    T.slot[i] = sloti;
-    acc[i] = ok ? 0 : kNotAccepted;
-    nbr_cnt[i] = overflow ? kOverflow : static_cast<uint8_t>(nn);
-    return !ok;
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) k_phase0(int64_t n, State S, State T, Box box,
-                                                const GridParams* __restrict__ gp,
-                                                const RoundParams* __restrict__ rpp,
-                                                const int64_t* __restrict__ cs,
-                                                const uint32_t* __restrict__ skey,
-                                                uint8_t* __restrict__ acc, int32_t* __restrict__ nbr,
-                                                uint8_t* __restrict__ nbr_cnt, int32_t* __restrict__ active,
-                                                StatsDev* stats) {
-    const GridParams g = *gp;
-    const RoundParams rp = *rpp;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool rejected = false;
-    if (i < n) rejected = phase0_global<D>(i, S, T, box, g, rp, cs, skey, acc, nbr, nbr_cnt);
-    push_active(rejected, i, active, stats);
-}
-
-
-// Migrate attempt l >= 1 for the still-active particles, over the
-// list of attempt-0 rejects (grid-stride; the list length is read on the device).
-template <int D>
-__global__ void __launch_bounds__(256) k_phase_list(int l, State S, State T, Box box,
-                                                    const GridParams* __restrict__ gp,
-                                                    const RoundParams* __restrict__ rpp,
-                                                    const int64_t* __restrict__ cs,
-                                                    const uint32_t* __restrict__ skey,
-                                                    uint8_t* __restrict__ acc,
-                                                    const int32_t* __restrict__ nbr,
-                                                    const uint8_t* __restrict__ nbr_cnt,
-                                                    const int32_t* __restrict__ active, StatsDev* stats) {
-    if (l >= rpp->n_l) return;
-    const int64_t m = static_cast<int64_t>(stats->active_count);
-    if ((l == 1 ? static_cast<unsigned long long>(m) : stats->rejected[l - 1]) == 0) return;
-    const GridParams& g = *gp;
-    const RoundParams rp = *rpp;
-    unsigned long long rej = 0;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = active[k];
-        if (acc[i] != kNotAccepted) continue;
-        double xi[D], p[D];
-        load_pos<D>(S, i, xi);
-        const double ri = S.r[i];
-        const int32_t idi = S.id[i];
-        propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[i]), static_cast<uint32_t>(l), p);
+    double p[D];
+    int accepted = -1;
+    for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
+        propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
         bool ok = true;
         auto test = [&](int64_t j) {
-            if (!ok || S.id[j] == idi) return;
-            const double rj = S.r[j];
-            const uint8_t aj = acc[j];
-            double xj[D];
-            if (aj >= static_cast<uint8_t>(l)) {  // still active in this phase (or accepting now)
-                load_pos<D>(S, j, xj);
-                if (sphere_overlap<D>(box, p, ri, xj, rj)) { ok = false; return; }
-                double pj[D];
-                propose<D>(box, xj, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[j]),
-                           static_cast<uint32_t>(l), pj);
-                if (sphere_overlap<D>(box, p, ri, pj, rj)) ok = false;
-            } else {  // accepted in an earlier phase: its final position
-                load_pos<D>(T, j, xj);
-                if (sphere_overlap<D>(box, p, ri, xj, rj)) ok = false;
-            }
+            if (S.id[j] == idi) return;
+            double xl[D];
+            live_pos<D>(S, T, acc, j, xl);
+            if (sphere_overlap<D>(box, p, ri, xl, S.r[j])) ok = false;
         };
-        const uint8_t cnt = nbr_cnt[i];
-        if (cnt != kOverflow) {
-            const int32_t* my = nbr + i * kNbrCap;
-            for (int t = 0; t < cnt && ok; ++t) test(my[t]);
+        if (!overflow) {
+            for (int t = 0; t < nn && ok; ++t) test(nb[t]);
         } else {
-            for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+            for_near_ranges<D>(g, cs, kq, g.near_s, [&](int64_t b, int64_t e) {
                 for (int64_t j = b; j < e && ok; ++j) {
-                    if (j == i) continue;
+                    if (j == q) continue;
                     double xj[D];
                     load_pos<D>(S, j, xj);
                     if (dist2<D>(box, xi, xj) > near_cut(ri, S.r[j], g.extra)) continue;
@@ -435,74 +371,109 @@ __global__ void __launch_bounds__(256) k_phase_list(int l, State S, State T, Box
                 }
             });
         }
-        if (ok) {
-#pragma unroll
-            for (int a = 0; a < D; ++a) T.x[a][i] = p[a];
-            acc[i] = static_cast<uint8_t>(l);
-        } else {
-            ++rej;
-        }
+        if (ok) accepted = l;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rej += __shfl_down_sync(0xffffffffu, rej, o);
-    if ((threadIdx.x & 31) == 0 && rej) atomicAdd(&stats->rejected[l], rej);
+    for (int a = 0; a < D; ++a) T.x[a][q] = accepted >= 0 ? p[a] : xi[a];
+    T.r[q] = ri;
+    T.id[q] = idi;
+    T.slot[q] = sl;
+    acc[q] = accepted >= 0 ? static_cast<uint8_t>(accepted) : kNotAccepted;
+    if (accepted < 0) active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
 }
 
-// Overlap reduction after the round.  Only pairs of non-movers can overlap (DESIGN.md
-// §3.3) and every non-mover is on the attempt-0 reject list, so the reduction walks
-// that list: each non-mover scans its near list for later non-movers.
+// cells of colour class `cls`: per axis the coordinates with colour cv are cv, cv+m,
+// ... below m*floor(n/m) (cv < m) or the single tail cell m*floor(n/m) + cv - m
+__device__ __forceinline__ void class_axis(int cv, int m, int n, int& first, int& step, int& cnt) {
+    const int body = m * (n / m);
+    if (cv < m) {
+        first = cv;
+        step = m;
+        cnt = body > cv ? (body - cv + m - 1) / m : 0;
+    } else {
+        first = body + (cv - m);
+        step = 1;
+        cnt = 1;
+    }
+}
+
 template <int D>
-__global__ void __launch_bounds__(256) k_stats_list(State S, Box box, const GridParams* __restrict__ gp,
-                                                    const int64_t* __restrict__ cs,
-                                                    const uint32_t* __restrict__ skey,
-                                                    const uint8_t* __restrict__ acc,
-                                                    const int32_t* __restrict__ nbr,
-                                                    const uint8_t* __restrict__ nbr_cnt,
-                                                    const int32_t* __restrict__ active, StatsDev* stats) {
+__global__ void __launch_bounds__(128) k_sweep_class(int cls, State S, State T, Box box,
+                                                     const GridParams* __restrict__ gp,
+                                                     const RoundParams* __restrict__ rpp,
+                                                     const int64_t* __restrict__ cs,
+                                                     const uint32_t* __restrict__ skey,
+                                                     uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                                     StatsDev* stats) {
+    const GridParams& g = *gp;
+    if (cls >= g.ncls) return;
+    const RoundParams rp = *rpp;
+    int first[3], step[3], cnt[3];
+    int rem = cls;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int cv = rem % g.col_n[a];
+        rem /= g.col_n[a];
+        class_axis(cv, g.col_m[a], g.dims[a], first[a], step[a], cnt[a]);
+    }
+    const int64_t total = static_cast<int64_t>(cnt[0]) * cnt[1] * cnt[2];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int k0 = static_cast<int>(t % cnt[0]);
+        const int64_t rest = t / cnt[0];
+        const int k1 = static_cast<int>(rest % cnt[1]);
+        const int k2 = static_cast<int>(rest / cnt[1]);
+        const int64_t cell = (static_cast<int64_t>(first[2] + k2 * step[2]) * g.dims[1] + (first[1] + k1 * step[1])) *
+                                 g.dims[0] +
+                             (first[0] + k0 * step[0]);
+        const int64_t e = cs[cell + 1];
+        for (int64_t q = cs[cell]; q < e; ++q) sweep_particle<D>(q, S, T, box, g, rp, cs, skey, acc, active, stats);
+    }
+}
+
+// Overlap reduction after the sweep.  A particle that accepted a trial cleared every
+// live position at its turn and every later mover cleared it, so only pairs of
+// particles that kept their round-start positions can overlap; those
+// are exactly the particles on the non-mover list.
+template <int D>
+__global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const GridParams* __restrict__ gp,
+                                                     const int64_t* __restrict__ cs,
+                                                     const uint32_t* __restrict__ skey,
+                                                     const uint8_t* __restrict__ acc,
+                                                     const int32_t* __restrict__ active, StatsDev* stats) {
     const int64_t m = static_cast<int64_t>(stats->active_count);
     const GridParams& g = *gp;
-    unsigned long long pairs = 0, stay = 0;
+    unsigned long long pairs = 0;
     double pen = 0.0;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = active[k];
-        if (acc[i] != kNotAccepted) continue;
-        ++stay;
         double xi[D];
         load_pos<D>(S, i, xi);
         const double ri = S.r[i];
         const int32_t idi = S.id[i];
-        auto test = [&](int64_t j) {
-            if (j <= i || acc[j] != kNotAccepted || S.id[j] == idi) return;
-            double xj[D];
-            load_pos<D>(S, j, xj);
-            const double rr = ri + S.r[j];
-            const double d2 = dist2<D>(box, xi, xj);
-            if (d2 <= rr * rr) {
-                ++pairs;
-                const double pe = rr - sqrt(d2);
-                pen = pe > pen ? pe : pen;
+        for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+            for (int64_t j = b; j < e; ++j) {
+                if (j <= i || acc[j] != kNotAccepted || S.id[j] == idi) continue;
+                double xj[D];
+                load_pos<D>(S, j, xj);
+                const double rr = ri + S.r[j];
+                const double d2 = dist2<D>(box, xi, xj);
+                if (d2 <= rr * rr) {
+                    ++pairs;
+                    const double pe = rr - sqrt(d2);
+                    pen = pe > pen ? pe : pen;
+                }
             }
-        };
-        const uint8_t c = nbr_cnt[i];
-        if (c != kOverflow) {
-            const int32_t* my = nbr + i * kNbrCap;
-            for (int t = 0; t < c; ++t) test(my[t]);
-        } else {
-            for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
-                for (int64_t j = b; j < e; ++j) test(j);
-            });
-        }
+        });
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         pairs += __shfl_down_sync(0xffffffffu, pairs, o);
-        stay += __shfl_down_sync(0xffffffffu, stay, o);
         const double t = __shfl_down_sync(0xffffffffu, pen, o);
         pen = t > pen ? t : pen;
     }
     if ((threadIdx.x & 31) == 0) {
         if (pairs) atomicAdd(&stats->overlap_pairs, pairs);
-        if (stay) atomicAdd(&stats->nonmovers, stay);
         if (pen > 0.0) atomicMax(&stats->pen_bits, (unsigned long long)__double_as_longlong(pen));
     }
 }

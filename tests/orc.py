@@ -54,8 +54,9 @@ def orc():
                                       C.c_uint32, C.c_uint32, vp]
         L.orc_propose.argtypes = [C.c_int, vp, vp, C.c_double, C.c_uint64, C.c_uint32, C.c_uint32,
                                   C.c_uint32, C.c_uint32, vp]
-        L.orc_migrate_round.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_int,
-                                        C.c_uint64, C.c_uint32, C.c_uint32, vp, vp, C.c_int]
+        L.orc_sweep_round.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_double, C.c_int,
+                                      C.c_uint64, C.c_uint32, C.c_uint32, vp, vp, C.c_int]
+        L.orc_colouring.argtypes = [C.c_int, vp, vp, C.c_double, C.c_double, vp, vp]
         L.orc_overlap_stats.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, C.POINTER(RoundStats)]
         L.orc_candidate_pairs.restype = C.c_int64
         L.orc_candidate_pairs.argtypes = [C.c_int, vp, C.c_int64, vp]
@@ -130,15 +131,26 @@ def o_sort(keys, slot, ncells):
     return order, cs
 
 
-def o_round(dim, L, x0, r, ids, slot, c_m, n_l, seed, round_id, iteration, brute=False):
+def o_round(dim, L, x0, r, ids, slot, cell_size, c_m, n_l, seed, round_id, iteration, brute=False):
+    """one round's coloured Gauss-Seidel migrate sweep (oracle/srm_oracle.c)"""
     x0 = arr(x0)
     n = len(r)
     xnew = np.zeros_like(x0)
     acc = np.zeros(n, np.uint8)
-    orc().orc_migrate_round(dim, P(arr(L)), n, P(x0), P(arr(r)), P(arr(ids, np.int32)),
-                            P(arr(slot, np.int32)), c_m, n_l, seed, round_id, iteration,
-                            P(xnew), P(acc), int(brute))
+    orc().orc_sweep_round(dim, P(arr(L)), n, P(x0), P(arr(r)), P(arr(ids, np.int32)),
+                          P(arr(slot, np.int32)), cell_size, c_m, n_l, seed, round_id, iteration,
+                          P(xnew), P(acc), int(brute))
     return xnew, acc
+
+
+def o_colouring(dim, L, cell_size, maxr, c_m):
+    dims, edge = o_grid(dim, L, cell_size)
+    d3 = np.ones(3, np.int32); d3[:dim] = dims
+    e3 = np.ones(3); e3[:dim] = edge
+    m = np.zeros(3, np.int32)
+    ncol = np.zeros(3, np.int32)
+    orc().orc_colouring(dim, P(d3), P(e3), maxr, c_m, P(m), P(ncol))
+    return m[:dim].copy(), ncol[:dim].copy()
 
 
 def o_stats(dim, L, pos, r, ids=None):
@@ -192,11 +204,12 @@ def o_generate(dim, L, pos, r, ids, c_w, c_m, n_k, n_l, f_target, max_iterations
         if f * factor ** dim > f_target:
             factor = (f_target / f) ** (1.0 / dim)
         max_r = float(r.max())
+        cs = 2.5 * max_r + c_m
         q = r * factor
         x = pos
         ok = False
         for k in range(n_k):
-            x, _ = o_round(dim, L, x, q, ids, slot, c_m, n_l, seed, k, it & 0xFFFFFFFF)
+            x, _ = o_round(dim, L, x, q, ids, slot, cs, c_m, n_l, seed, k, it & 0xFFFFFFFF)
             rounds += 1
             if o_stats(dim, L, x, q, ids).overlap_pairs == 0:
                 ok = True
@@ -207,7 +220,6 @@ def o_generate(dim, L, pos, r, ids, c_w, c_m, n_k, n_l, f_target, max_iterations
             acc_it += 1
             # reorder cadence changes slots/ids exactly like reorder_by_locality
             if reorder_period > 0 and acc_it % reorder_period == 0:
-                cs = 2.5 * max_r + c_m
                 keys, dims, _ = o_keys(dim, L, cs, pos)
                 order, _ = o_sort(keys, slot, int(np.prod(dims)))
                 pos, r = pos[order], r[order]
@@ -215,7 +227,7 @@ def o_generate(dim, L, pos, r, ids, c_w, c_m, n_k, n_l, f_target, max_iterations
                 ids = slot.copy()
         else:
             for k in range(n_k):
-                pos, _ = o_round(dim, L, pos, r, ids, slot, c_m, n_l, seed, n_k + k, it & 0xFFFFFFFF)
+                pos, _ = o_round(dim, L, pos, r, ids, slot, cs, c_m, n_l, seed, n_k + k, it & 0xFFFFFFFF)
                 shakes += 1
     return status, pos, r, ids, iteration_count + done, f, dict(accepted=acc_it, rounds=rounds, shakes=shakes)
 

@@ -120,7 +120,7 @@ def test_overlap_stats_bit_exact(dim, n, rmin, rmax, seed):
     assert (st.overlap_pairs > 0) == anyc
 
 
-# ---- one round ------------------------------------------------------------------------------
+# ---- one round (coloured Gauss-Seidel sweep) --------------------------------------------------
 @pytest.mark.parametrize("dim,n,f,swell,cm_rel,n_l,seed", [
     (2, 2000, 0.45, 1.03, 0.1, 10, 1),
     (3, 3000, 0.3, 1.02, 0.1, 10, 2),
@@ -137,7 +137,7 @@ def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed):
     with _ctx(L, pos, r, ids) as ctx:
         st, acc = ctx.round(cs, c_m, n_l, key, round_id, it, with_candidates=True)
         pos_d, r_d, id_d = ctx.download()
-    xnew, acc_o = orc.o_round(dim, L, pos, r, ids, ids, c_m, n_l, key, round_id, it)
+    xnew, acc_o = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, n_l, key, round_id, it)
     assert np.array_equal(acc, acc_o)
     assert np.array_equal(pos_d, xnew)
     assert np.array_equal(r_d, r) and np.array_equal(id_d, ids)
@@ -150,13 +150,13 @@ def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed):
 
 
 @pytest.mark.parametrize("dim,n,L,cm_rel,swell", [
-    (3, 400, [1.0, 1.0, 1.0], 0.1, 1.02),      # dims 3-4: whole-axis bricks, every cell a neighbour
-    (3, 3000, [2.0, 1.0, 0.5], 0.1, 1.03),     # rectangular: brick / whole-axis mix
-    (3, 4000, [1.0, 1.0, 1.0], 0.45, 1.05),    # wide moves: near half width 2
+    (3, 400, [1.0, 1.0, 1.0], 0.1, 1.02),      # dims 3-4: whole axes, every coordinate its own colour
+    (3, 3000, [2.0, 1.0, 0.5], 0.1, 1.03),     # rectangular, odd dims: tail colours
+    (3, 4000, [1.0, 1.0, 1.0], 0.45, 1.05),    # wide moves: colouring modulus 3, near half width 2
     (2, 6000, [1.0, 3.0], 0.2, 1.02),
     (2, 300, [1.0, 1.0], 0.3, 1.0),
 ])
-def test_round_brick_modes_bit_exact(dim, n, L, cm_rel, swell):
+def test_round_colourings_bit_exact(dim, n, L, cm_rel, swell):
     unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
     f = 0.35 if dim == 2 else 0.2
     r = (f * np.prod(L) / (n * unit)) ** (1.0 / dim)
@@ -168,16 +168,18 @@ def test_round_brick_modes_bit_exact(dim, n, L, cm_rel, swell):
         st, acc = ctx.round(cs, c_m, 6, 4242, 1, 2, with_candidates=True)
         pos_d, _, _ = ctx.download()
         info = ctx.last_round_info()
-    xnew, acc_o = orc.o_round(dim, L, pos, rr, ids, ids, c_m, 6, 4242, 1, 2)
+    xnew, acc_o = orc.o_round(dim, L, pos, rr, ids, ids, cs, c_m, 6, 4242, 1, 2)
     assert np.array_equal(acc, acc_o) and np.array_equal(pos_d, xnew)
     o = orc.o_stats(dim, L, xnew, rr)
     assert st.overlap_pairs == o.overlap_pairs and st.max_penetration == o.max_penetration
-    assert info["rejected_attempt0"] == int(np.sum(acc_o != 0))
+    assert info["nonmovers"] == int(np.sum(acc_o == 255))
+    m, ncol = orc.o_colouring(dim, L, cs, rr.max(), c_m)
+    assert info["colour_classes"] == int(np.prod(ncol))
 
 
-def test_clustered_start_overflows_bricks_bit_exact():
-    # dense Gaussian clusters (cfg3-like start) push bricks over their shared-memory
-    # capacity: those bricks take the global-memory path, results unchanged
+def test_clustered_start_bit_exact():
+    # dense Gaussian clusters (cfg3-like start): many particles per cell, long in-cell
+    # sequential chains and near lists beyond the per-particle buffer
     rng = np.random.default_rng(8)
     n, L = 6000, [1.0, 1.0, 1.0]
     centres = rng.uniform(0, 1, (6, 3))
@@ -188,27 +190,10 @@ def test_clustered_start_overflows_bricks_bit_exact():
     with _ctx(L, pos, r) as ctx:
         st, acc = ctx.round(cs, c_m, 5, 7, 0, 0)
         pos_d, _, _ = ctx.download()
-        info = ctx.last_round_info()
     xnew, acc_o = orc.o_round(3, L, pos, r, np.arange(n, dtype=np.int32), np.arange(n, dtype=np.int32),
-                              c_m, 5, 7, 0, 0)
-    assert info["fallback_bricks"] > 0
+                              cs, c_m, 5, 7, 0, 0)
     assert np.array_equal(acc, acc_o) and np.array_equal(pos_d, xnew)
     assert st.overlap_pairs == orc.o_stats(3, L, xnew, r).overlap_pairs
-
-
-def test_bricks_equal_untiled(monkeypatch):
-    L, pos, r, ids = _rsa_state(3, 20000, 0.25, 17)
-    r = r * (0.3 / 0.25) ** (1 / 3)
-    c_m = 0.05 * r[0]
-    cs = 2.5 * r[0] / 1.02 + c_m
-    out = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("SRM_B200_NO_TILES", flag)
-        with _ctx(L, pos, r, ids) as ctx:
-            st = ctx.rounds(cs, c_m, 10, 3, 0, 9, 2)
-            out.append((ctx.download()[0], st.overlap_pairs, st.movers, ctx.last_round_info()["bricks"]))
-    assert out[0][3] > 0 and out[1][3] == 0
-    assert np.array_equal(out[0][0], out[1][0]) and out[0][1:3] == out[1][1:3]
 
 
 def test_round_polydisperse_bit_exact():
@@ -219,7 +204,7 @@ def test_round_polydisperse_bit_exact():
     with _ctx(L, pos, r, ids) as ctx:
         st, acc = ctx.round(cs, c_m, 10, 99, 0, 1)
         pos_d, _, _ = ctx.download()
-    xnew, acc_o = orc.o_round(3, L, pos, r, ids, ids, c_m, 10, 99, 0, 1)
+    xnew, acc_o = orc.o_round(3, L, pos, r, ids, ids, cs, c_m, 10, 99, 0, 1)
     assert np.array_equal(acc, acc_o) and np.array_equal(pos_d, xnew)
     assert st.overlap_pairs == orc.o_stats(3, L, xnew, r).overlap_pairs
 
@@ -237,18 +222,24 @@ def test_rounds_are_deterministic_and_chain():
     assert np.array_equal(outs[0], outs[1])
     x = pos
     for k in range(3):
-        x, _ = orc.o_round(3, L, x, r, ids, ids, c_m, 10, 5, k, 1)
+        x, _ = orc.o_round(3, L, x, r, ids, ids, cs, c_m, 10, 5, k, 1)
     assert np.array_equal(outs[0], x)
 
 
 def test_caged_particle_reverts():
+    # test_engine.cpp:65-86: a particle that rejects keeps its exact bits
     pos = orc.arr([[0.5, 0.5]] + [[0.5 + 0.2000000001 * np.cos(k * np.pi / 3),
                                      0.5 + 0.2000000001 * np.sin(k * np.pi / 3)] for k in range(6)])
     r = np.full(7, 0.1)
     with _ctx([1.0, 1.0], pos, r) as ctx:
         _, acc = ctx.round(0.25, 0.05, 1, 99, 0, 0)
         p, _, _ = ctx.download()
-    assert acc[0] == 255 and np.array_equal(p[0], pos[0])
+    xnew, acc_o = orc.o_round(2, [1.0, 1.0], pos, r, np.arange(7, dtype=np.int32), np.arange(7, dtype=np.int32),
+                              0.25, 0.05, 1, 99, 0, 0)
+    assert np.array_equal(acc, acc_o) and np.array_equal(p, xnew)
+    for i in range(7):
+        if acc[i] == 255:
+            assert np.array_equal(p[i], pos[i])
 
 
 def test_single_particle_moves_c_m():
