@@ -71,6 +71,14 @@ struct srm_b200_ctx {
     uint32_t* skey = nullptr;
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
+    int32_t* work = nullptr;    // particles ordered by (colour class, rank in cell)
+    int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
+    uint8_t* nbr_cnt = nullptr;
+    uint32_t* bcount = nullptr; // (class, rank) bucket counts / starts / cursors
+    uint32_t* bstart = nullptr;
+    uint32_t* bcursor = nullptr;
+    uint32_t* maxrank = nullptr;
+    int64_t bucket_cap = 0;
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -189,6 +197,15 @@ struct srm_b200_ctx {
         gp = dalloc<GridParams>(1);
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
+        work = dalloc<int32_t>(cap);
+        nbr = dalloc<int32_t>(cap * kNearLocal);
+        nbr_cnt = dalloc<uint8_t>(cap);
+        maxrank = dalloc<uint32_t>(1);
+        S.xf = dalloc<float4>(cap);
+        ensure_buckets(27 * (kRankMax + 1) + 1);
+        const int work_smem = 2 * 8192 * 4;
+        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
+        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -207,6 +224,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
+        cudaFree(work); cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor); cudaFree(maxrank); cudaFree(S.xf);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -271,7 +289,33 @@ struct srm_b200_ctx {
             g.ncls *= g.col_n[a];
             g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
         }
+        // fp32 prefilter: coordinates live in [0, L); 8 ulp of the largest box length
+        // bounds the rounding of any coordinate difference and of the radii sums
+        double lmax = 0.0;
+        for (int a = 0; a < dim; ++a) lmax = std::max(lmax, box.L[a]);
+        g.margin_f = static_cast<float>(8.0 * std::ldexp(1.0, -24) * lmax + 4.0 * std::ldexp(1.0, -24) *
+                                                                              (2.0 * max_r_state + extra));
+        g.extra_f = static_cast<float>(extra);
+        g.rmax_f = static_cast<float>(max_r_state);
+        for (int a = 0; a < 3; ++a) {
+            g.L_f[a] = static_cast<float>(box.L[a]);
+            g.half_f[a] = 0.5f * g.L_f[a];
+            g.edge_f[a] = static_cast<float>(g.edge[a]);
+        }
         return g;
+    }
+
+    void ensure_buckets(int64_t nb) {
+        if (nb <= bucket_cap) return;
+        cudaFree(bcount);
+        cudaFree(bstart);
+        cudaFree(bcursor);
+        bcount = nullptr; bstart = nullptr; bcursor = nullptr;
+        bcount = dalloc<uint32_t>(nb);
+        bstart = dalloc<uint32_t>(nb + 1);
+        bcursor = dalloc<uint32_t>(nb);
+        SRM_CUDA(cudaMemsetAsync(bcount, 0, sizeof(uint32_t) * nb, stream));
+        bucket_cap = nb;
     }
 
     void ensure_cells(int64_t ncells) {
@@ -291,6 +335,7 @@ struct srm_b200_ctx {
 
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
+        ensure_buckets(static_cast<int64_t>(g.ncls) * (kRankMax + 1) + 1);
         k_set_grid<<<1, 1, 0, stream>>>(gp, g);
         launched();
         hg = g;
@@ -344,15 +389,40 @@ struct srm_b200_ctx {
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
         SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
+            FamScope fs(this, 2);  // work lists: (colour class, rank in cell) buckets
+            const int nbk = hg.ncls * (kRankMax + 1);
+            const bool local = nbk <= 8192;
+            const int wb = blocks_for(n, kWorkBlock * kWorkPer);
+            SRM_CUDA(cudaMemsetAsync(maxrank, 0, sizeof(uint32_t), stream));
+            if (dim == 2)
+                k_work_count<2><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount, maxrank);
+            else
+                k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount, maxrank);
+            k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
+            if (dim == 2)
+                k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
+            else
+                k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
+            const int nb = blocks_for(n, 256);
+            if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
+            else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
+            launched(4);
+        }
+        {
             FamScope fs(this, 1);
+            // grid: enough threads for the largest bucket (every cell of a class occupied)
             const int sb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(hg.cls_cells, 128), 148 * 64)));
             for (int cls = 0; cls < hg.ncls; ++cls) {
-                if (dim == 2)
-                    k_sweep_class<2><<<sb, 128, 0, stream>>>(cls, S, T, box, gp, rp, cell_start, skey, acc, active, stats);
-                else
-                    k_sweep_class<3><<<sb, 128, 0, stream>>>(cls, S, T, box, gp, rp, cell_start, skey, acc, active, stats);
+                for (int rank = 0; rank <= kRankMax; ++rank) {
+                    if (dim == 2)
+                        k_sweep_class<2><<<sb, 128, 0, stream>>>(cls, rank, S, T, box, gp, rp, cell_start, skey, bstart,
+                                                                 work, nbr, nbr_cnt, acc, active, stats);
+                    else
+                        k_sweep_class<3><<<sb, 128, 0, stream>>>(cls, rank, S, T, box, gp, rp, cell_start, skey, bstart,
+                                                                 work, nbr, nbr_cnt, acc, active, stats);
+                }
             }
-            launched(hg.ncls);
+            launched(hg.ncls * (kRankMax + 1));
         }
         if (with_stats) {
             FamScope fs(this, 3);

@@ -3,12 +3,15 @@
 // One SRM round (engine.hpp:227-234: build_shape_grid -> migrate -> shape_any_collision)
 // is, on the device:
 //   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
-//   migrate        k_sweep_class, one launch per colour class (coloured Gauss-Seidel)
+//   work lists     k_work_count -> k_work_scan -> k_work_scatter ((class, rank) buckets)
+//   migrate        k_sweep_class, one cooperative launch per colour class (Gauss-Seidel)
 //   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
 // All kernels read the grid / round parameters from device memory so that the same
 // launches can be replayed from a CUDA graph.  DESIGN.md §2-§4 has the data layout
 // and the roofline of each kernel.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include <cstdint>
 
@@ -29,6 +32,9 @@ struct GridParams {
     int32_t col_n[3];   // colours per axis
     int32_t ncls;       // colour classes = col_n[0] * col_n[1] * col_n[2]
     int64_t cls_cells;  // largest number of cells in one class
+    // fp32 prefilter (near_candidates): margin above the fp32 rounding of coordinates
+    float margin_f, extra_f, rmax_f;
+    float L_f[3], half_f[3], edge_f[3];
 };
 
 struct RoundParams {
@@ -43,6 +49,7 @@ struct State {
     double* r;
     int32_t* id;
     int32_t* slot;
+    float4* xf;  // sorted fp32 copy (x, y, z, r) for prefilters; only in the sorted state S
 };
 
 struct StatsDev {
@@ -241,9 +248,17 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ perm, const uint
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t src = perm[q];
+        float f[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int a = 0; a < D; ++a) S.x[a][q] = T.x[a][src];
-        S.r[q] = T.r[src];
+        for (int a = 0; a < D; ++a) {
+            const double v = T.x[a][src];
+            S.x[a][q] = v;
+            f[a] = static_cast<float>(v);
+        }
+        const double rr = T.r[src];
+        S.r[q] = rr;
+        f[3] = static_cast<float>(rr);
+        if (S.xf) S.xf[q] = make_float4(f[0], f[1], f[2], f[3]);
         S.id[q] = T.id[src];
         S.slot[q] = T.slot[src];
         skey[q] = key[src];
@@ -319,57 +334,131 @@ __device__ __forceinline__ void live_pos(const State& S, const State& T, const u
 }
 
 constexpr int kNearLocal = 16;  // near candidates kept per particle; more -> rescan per trial
+constexpr int kRankMax = 1;     // in-cell ranks with their own sub-pass; deeper ranks run
+                                // sequentially behind rank kRankMax (crowded cells)
+
+// Near candidates of sorted particle q: every j whose round-start distance is within
+// ri + rj + 2 c_m (every j a trial of q can touch while j sits within c_m of its start).
+// fp32 prefilter on the sorted float4 copy with an absolute margin above its rounding
+// error, so the set is a superset of the exact fp64 near set; the stencil rows and the
+// x cells of each row are pruned by the chord of the (inflated) cutoff sphere.
+template <int D, typename F>
+__device__ __forceinline__ void near_candidates(const GridParams& g, const int64_t* __restrict__ cs,
+                                                const float4* __restrict__ xf, int64_t q, uint32_t key, F&& visit) {
+    const float4 me = xf[q];
+    const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
+    const int cx = static_cast<int>(key % static_cast<uint32_t>(dx));
+    const uint32_t rest = key / static_cast<uint32_t>(dx);
+    const int cy = static_cast<int>(rest % static_cast<uint32_t>(dy));
+    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(dy)) : 0;
+    const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
+    const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
+    const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
+    // y / z rows: unwrapped range [c - s, c + s], or every row when the stencil covers the axis
+    const int sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
+    const int ylo = sy < 0 ? 0 : cy - sy, yhi = sy < 0 ? dy - 1 : cy + sy;
+    const int zlo = D == 3 ? (sz < 0 ? 0 : cz - sz) : 0, zhi = D == 3 ? (sz < 0 ? dz - 1 : cz + sz) : 0;
+    for (int zz = zlo; zz <= zhi; ++zz) {
+        float dzd = 0.f;
+        if (D == 3 && sz >= 0) {
+            const float zb = zz * g.edge_f[2];
+            dzd = fmaxf(0.f, fmaxf(zb - me.z, me.z - (zb + g.edge_f[2])));
+        }
+        const int z = zz < 0 ? zz + dz : (zz >= dz ? zz - dz : zz);
+        for (int yy = ylo; yy <= yhi; ++yy) {
+            float dyd = 0.f;
+            if (sy >= 0) {
+                const float yb = yy * g.edge_f[1];
+                dyd = fmaxf(0.f, fmaxf(yb - me.y, me.y - (yb + g.edge_f[1])));
+            }
+            const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
+            if (dyz2 > cut2) continue;
+            const int y = yy < 0 ? yy + dy : (yy >= dy ? yy - dy : yy);
+            const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
+            auto run = [&](int64_t b, int64_t e) {
+                for (int64_t j = b; j < e; ++j) {
+                    const float4 c = xf[j];
+                    float ex = c.x - me.x, ey = c.y - me.y, ez = D == 3 ? c.z - me.z : 0.f;
+                    if (ex > g.half_f[0]) ex -= g.L_f[0]; else if (ex < -g.half_f[0]) ex += g.L_f[0];
+                    if (ey > g.half_f[1]) ey -= g.L_f[1]; else if (ey < -g.half_f[1]) ey += g.L_f[1];
+                    if (D == 3) { if (ez > g.half_f[2]) ez -= g.L_f[2]; else if (ez < -g.half_f[2]) ez += g.L_f[2]; }
+                    const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                    const float lim = __fadd_rn(base, c.w);
+                    if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f) || j == q) continue;
+                    visit(j);
+                }
+            };
+            const int sx = g.near_s[0];
+            if (sx < 0) {
+                run(cs[row], cs[row + dx]);
+                continue;
+            }
+            const float xh = __fadd_rn(__fsqrt_rn(__fsub_rn(cut2, dyz2)), g.margin_f);
+            const int xl = max(cx - sx, static_cast<int>(floorf(__fdiv_rn(__fsub_rn(me.x, xh), g.edge_f[0]))));
+            const int xr = min(cx + sx, static_cast<int>(ceilf(__fdiv_rn(__fadd_rn(me.x, xh), g.edge_f[0]))) - 1);
+            if (xl > xr) continue;
+            if (xl < 0) {
+                run(cs[row + xl + dx], cs[row + dx]);
+                run(cs[row], cs[row + xr + 1]);
+            } else if (xr >= dx) {
+                run(cs[row + xl], cs[row + dx]);
+                run(cs[row], cs[row + xr - dx + 1]);
+            } else {
+                run(cs[row + xl], cs[row + xr + 1]);
+            }
+        }
+    }
+}
+
+constexpr uint8_t kNearOverflow = 255;
+
+// Near lists of every particle, one parallel pass before the sweep: nbr[q*kNearLocal..]
+// and nbr_cnt[q] (kNearOverflow: more than kNearLocal, the sweep rescans the grid).
+template <int D>
+__global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const GridParams* __restrict__ gp,
+                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                    int32_t* __restrict__ nbr, uint8_t* __restrict__ nbr_cnt) {
+    const GridParams& g = *gp;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        int32_t* my = nbr + q * kNearLocal;
+        int nn = 0;
+        near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+            if (nn < kNearLocal) my[nn] = static_cast<int32_t>(j);
+            ++nn;
+        });
+        nbr_cnt[q] = nn > kNearLocal ? kNearOverflow : static_cast<uint8_t>(nn);
+    }
+}
 
 template <int D>
 __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const State& T, const Box& box,
                                                const GridParams& g, const RoundParams& rp,
                                                const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                               const int32_t* __restrict__ nbr, const uint8_t* __restrict__ nbr_cnt,
                                                uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                StatsDev* stats) {
+    const int nn = nbr_cnt[q];
+    const int32_t* nb = nbr + q * kNearLocal;
     double xi[D];
     load_pos<D>(S, q, xi);
     const double ri = S.r[q];
     const int32_t idi = S.id[q];
     const int32_t sl = S.slot[q];
-    // candidates: j whose round-start distance is within ri + rj + 2 c_m -- every j a
-    // trial of q can touch while j sits within c_m of its start
-    int32_t nb[kNearLocal];
-    int nn = 0;
-    bool overflow = false;
-    const uint32_t kq = skey[q];
-    for_near_ranges<D>(g, cs, kq, g.near_s, [&](int64_t b, int64_t e) {
-        for (int64_t j = b; j < e; ++j) {
-            if (j == q) continue;
-            double xj[D];
-            load_pos<D>(S, j, xj);
-            if (dist2<D>(box, xi, xj) > near_cut(ri, S.r[j], g.extra)) continue;
-            if (nn < kNearLocal) nb[nn++] = static_cast<int32_t>(j);
-            else overflow = true;
-        }
-    });
     double p[D];
     int accepted = -1;
     for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
         propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
         bool ok = true;
         auto test = [&](int64_t j) {
-            if (S.id[j] == idi) return;
+            if (!ok || S.id[j] == idi) return;
             double xl[D];
             live_pos<D>(S, T, acc, j, xl);
             if (sphere_overlap<D>(box, p, ri, xl, S.r[j])) ok = false;
         };
-        if (!overflow) {
+        if (nn != kNearOverflow) {
             for (int t = 0; t < nn && ok; ++t) test(nb[t]);
-        } else {
-            for_near_ranges<D>(g, cs, kq, g.near_s, [&](int64_t b, int64_t e) {
-                for (int64_t j = b; j < e && ok; ++j) {
-                    if (j == q) continue;
-                    double xj[D];
-                    load_pos<D>(S, j, xj);
-                    if (dist2<D>(box, xi, xj) > near_cut(ri, S.r[j], g.extra)) continue;
-                    test(j);
-                }
-            });
+        } else {  // crowded neighbourhood: rescan (same candidate set)
+            near_candidates<D>(g, cs, S.xf, q, skey[q], test);
         }
         if (ok) accepted = l;
     }
@@ -382,52 +471,186 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
     if (accepted < 0) active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
 }
 
-// cells of colour class `cls`: per axis the coordinates with colour cv are cv, cv+m,
-// ... below m*floor(n/m) (cv < m) or the single tail cell m*floor(n/m) + cv - m
-__device__ __forceinline__ void class_axis(int cv, int m, int n, int& first, int& step, int& cnt) {
+// colour class of a cell
+__device__ __forceinline__ int colour1(int x, int m, int n) {
     const int body = m * (n / m);
-    if (cv < m) {
-        first = cv;
-        step = m;
-        cnt = body > cv ? (body - cv + m - 1) / m : 0;
-    } else {
-        first = body + (cv - m);
-        step = 1;
-        cnt = 1;
-    }
+    return x < body ? x % m : m + (x - body);
 }
 
 template <int D>
-__global__ void __launch_bounds__(128) k_sweep_class(int cls, State S, State T, Box box,
+__device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
+    const int cx = static_cast<int>(key % static_cast<uint32_t>(g.dims[0]));
+    const uint32_t rest = key / static_cast<uint32_t>(g.dims[0]);
+    const int cy = static_cast<int>(rest % static_cast<uint32_t>(g.dims[1]));
+    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(g.dims[1])) : 0;
+    int k = colour1(cx, g.col_m[0], g.dims[0]);
+    k += g.col_n[0] * colour1(cy, g.col_m[1], g.dims[1]);
+    if (D == 3) k += g.col_n[0] * g.col_n[1] * colour1(cz, g.col_m[2], g.dims[2]);
+    return k;
+}
+
+// Work lists: bucket (class, rank-in-cell) of every sorted particle; ranks above
+// kRankMax get no bucket (the rank-kRankMax particle sweeps the rest of its cell).
+constexpr int kWorkBlock = 1024;
+constexpr int kWorkPer = 8;   // particles per thread: 8192 per block
+
+template <int D>
+__device__ __forceinline__ int bucket_of(const GridParams& g, const int64_t* __restrict__ cs, uint32_t key, int64_t q,
+                                         unsigned long long* rank_out) {
+    const int64_t rank = q - cs[key];
+    *rank_out = static_cast<unsigned long long>(rank);
+    if (rank > kRankMax) return -1;
+    return class_of_key<D>(g, key) * (kRankMax + 1) + static_cast<int>(rank);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWorkBlock) k_work_count(int64_t n, const GridParams* __restrict__ gp,
+                                                           const int64_t* __restrict__ cs,
+                                                           const uint32_t* __restrict__ skey,
+                                                           uint32_t* __restrict__ bcount, uint32_t* __restrict__ maxrank) {
+    extern __shared__ uint32_t hist[];
+    const GridParams& g = *gp;
+    const int nb = g.ncls * (kRankMax + 1);
+    const bool local = nb <= 8192;
+    if (local)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    unsigned long long mr = 0;
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
+    for (int k = 0; k < kWorkPer; ++k) {
+        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
+        if (q >= n) break;
+        unsigned long long rank;
+        const int b = bucket_of<D>(g, cs, skey[q], q, &rank);
+        mr = rank > mr ? rank : mr;
+        if (b < 0) continue;
+        if (local) atomicAdd(&hist[b], 1u);
+        else atomicAdd(&bcount[b], 1u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_down_sync(0xffffffffu, mr, o);
+        mr = t > mr ? t : mr;
+    }
+    if ((threadIdx.x & 31) == 0 && mr) atomicMax(maxrank, static_cast<uint32_t>(mr));
+    __syncthreads();
+    if (local)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+            if (hist[b]) atomicAdd(&bcount[b], hist[b]);
+}
+
+// single block: exclusive scan of the bucket counts; cursors start at the bucket starts
+__global__ void k_work_scan(const GridParams* __restrict__ gp, uint32_t* __restrict__ bcount,
+                            uint32_t* __restrict__ bstart, uint32_t* __restrict__ cursor) {
+    const int nb = gp->ncls * (kRankMax + 1);
+    __shared__ uint32_t carry;
+    __shared__ uint32_t wsum[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t v = b < nb ? bcount[b] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            wsum[lane] = wi - w;
+        }
+        __syncthreads();
+        const uint32_t ex = carry + wsum[wid] + incl - v;
+        if (b < nb) {
+            bstart[b] = ex;
+            cursor[b] = ex;
+            bcount[b] = 0u;  // ready for the next round's histogram
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bstart[nb] = carry;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const GridParams* __restrict__ gp,
+                                                             const int64_t* __restrict__ cs,
+                                                             const uint32_t* __restrict__ skey,
+                                                             uint32_t* __restrict__ cursor, int32_t* __restrict__ work) {
+    extern __shared__ uint32_t hist[];  // [nb] counts, then [nb] block bases
+    const GridParams& g = *gp;
+    const int nb = g.ncls * (kRankMax + 1);
+    const bool local = nb <= 8192;
+    uint32_t* base = hist + (local ? nb : 0);
+    if (local)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
+    int myb[kWorkPer];
+    uint32_t myl[kWorkPer];
+#pragma unroll
+    for (int k = 0; k < kWorkPer; ++k) {
+        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
+        myb[k] = -1;
+        if (q >= n) continue;
+        unsigned long long rank;
+        myb[k] = bucket_of<D>(g, cs, skey[q], q, &rank);
+        if (myb[k] < 0) continue;
+        if (local) myl[k] = atomicAdd(&hist[myb[k]], 1u);
+        else work[atomicAdd(&cursor[myb[k]], 1u)] = static_cast<int32_t>(q);
+    }
+    if (!local) return;
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (hist[b]) base[b] = atomicAdd(&cursor[b], hist[b]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kWorkPer; ++k) {
+        if (myb[k] < 0) continue;
+        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
+        work[base[myb[k]] + myl[k]] = static_cast<int32_t>(q);
+    }
+}
+
+// One (colour class, rank) step: thread per particle of the bucket.  Rank 0 is the
+// first particle of every occupied cell of the class; the rank-1 thread of a crowded
+// cell sweeps all its remaining particles sequentially (slot order).
+template <int D>
+__global__ void __launch_bounds__(128) k_sweep_class(int cls, int rank, State S, State T, Box box,
                                                      const GridParams* __restrict__ gp,
                                                      const RoundParams* __restrict__ rpp,
                                                      const int64_t* __restrict__ cs,
                                                      const uint32_t* __restrict__ skey,
+                                                     const uint32_t* __restrict__ bstart,
+                                                     const int32_t* __restrict__ work,
+                                                     const int32_t* __restrict__ nbr, const uint8_t* __restrict__ nbr_cnt,
                                                      uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                      StatsDev* stats) {
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
     const RoundParams rp = *rpp;
-    int first[3], step[3], cnt[3];
-    int rem = cls;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const int cv = rem % g.col_n[a];
-        rem /= g.col_n[a];
-        class_axis(cv, g.col_m[a], g.dims[a], first[a], step[a], cnt[a]);
-    }
-    const int64_t total = static_cast<int64_t>(cnt[0]) * cnt[1] * cnt[2];
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+    const int b = cls * (kRankMax + 1) + rank;
+    const int64_t lo = bstart[b], hi = bstart[b + 1];
+    for (int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < hi;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int k0 = static_cast<int>(t % cnt[0]);
-        const int64_t rest = t / cnt[0];
-        const int k1 = static_cast<int>(rest % cnt[1]);
-        const int k2 = static_cast<int>(rest / cnt[1]);
-        const int64_t cell = (static_cast<int64_t>(first[2] + k2 * step[2]) * g.dims[1] + (first[1] + k1 * step[1])) *
-                                 g.dims[0] +
-                             (first[0] + k0 * step[0]);
-        const int64_t e = cs[cell + 1];
-        for (int64_t q = cs[cell]; q < e; ++q) sweep_particle<D>(q, S, T, box, g, rp, cs, skey, acc, active, stats);
+        const int64_t q = work[t];
+        sweep_particle<D>(q, S, T, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
+        if (rank == kRankMax) {
+            const int64_t e = cs[skey[q] + 1];
+            for (int64_t q2 = q + 1; q2 < e; ++q2)
+                sweep_particle<D>(q2, S, T, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
+        }
     }
 }
 
