@@ -46,3 +46,4 @@ clean:
 	$(MAKE) -f oracle/Makefile clean
 
 .PHONY: all lib oracle shimtest clean
+

@@ -288,6 +288,7 @@ def run_b200(args, cfg, world, rank, local, pg):
     fam_ms, fam_calls = ctx.timing_get()
     ctx.timing_enable(False)
     per_round = [v / args.steps for v in fam_ms]
+    # migrate step = near lists + (class, rank) work lists + the coloured sweep
     t_mig = per_round[1] + per_round[2]
     peak, peak_kind = peaks()
     algo = n * BYTES_STEP[dim]
@@ -331,10 +332,10 @@ def run_b200(args, cfg, world, rank, local, pg):
                        "prep": prep},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "migrate step (k_phase0 + k_phase, n_l attempts) per round",
+                         "kernel": "migrate step per round (k_near_lists + k_work_* + k_sweep_class x classes)",
                          "algorithmic_bytes_per_update": BYTES_STEP[dim], "peak_kind": peak_kind},
-            "phase_ms_per_round": {"grid_rebuild": per_round[0], "migrate_phase0": per_round[1],
-                                   "migrate_phases_ge1": per_round[2], "reduction": per_round[3]},
+            "phase_ms_per_round": {"grid_rebuild": per_round[0], "sweep": per_round[1],
+                                   "near_and_work_lists": per_round[2], "reduction": per_round[3]},
             "last_round": {"overlap_pairs": st.overlap_pairs, "movers": st.movers,
                            "max_penetration": st.max_penetration},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_io,

@@ -186,7 +186,7 @@ void srm_b200_reset_launch_count(srm_b200_ctx* ctx);
 /* CUDA-event timing of kernel families on the context stream.  enable != 0 starts
  * recording; srm_b200_timing_get fills ms[SRM_B200_NPHASE] with accumulated device
  * milliseconds and calls[SRM_B200_NPHASE] with the number of timed launches. */
-#define SRM_B200_NPHASE 4 /* 0 grid rebuild, 1 migrate phase 0, 2 migrate phases >=1, 3 reduction */
+#define SRM_B200_NPHASE 4 /* 0 grid rebuild, 1 sweep (migrate), 2 near lists, 3 reduction */
 int srm_b200_timing_enable(srm_b200_ctx* ctx, int enable);
 int srm_b200_timing_get(srm_b200_ctx* ctx, double* ms, int64_t* calls);
 /* device sync + last-error check */
@@ -196,8 +196,13 @@ int srm_b200_sync(srm_b200_ctx* ctx);
 int srm_b200_stopwatch(srm_b200_ctx* ctx, int op, double* ms);
 /* Diagnostics of the last round whose statistics were read: info[0] non-movers,
  * [1] colour classes of the sweep, [2] largest cells per class, [3] near-search half
- * width (x), [4] colouring modulus (x), [5] cells of the grid. */
+ * width (x), [4] colouring modulus (x), [5] cells of the grid, [6] superblock colours,
+ * [7] superblocks along x. */
 int srm_b200_last_round_info(srm_b200_ctx* ctx, int64_t* info);
+/* Sweep schedule: superblocks at least max(w0, m) cells wide, 2-coloured
+ * per axis (w0 <= 0: none, the sweep runs colour class by colour class over the whole
+ * grid).  Changes the visiting order, hence the trajectory; the oracle takes the same w0. */
+int srm_b200_set_superblock(srm_b200_ctx* ctx, int w0);
 
 /* ---- self tests of the device primitives (no reference counterpart) ------------------ */
 /* the hand-written device Philox4x32-10 next to CUDA's curand_Philox4x32_10 */

@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsrm_b200.so")
+# SRM_B200_LIB: an alternative build of the same library (tools/ tuning variants only)
+LIB_PATH = os.environ.get("SRM_B200_LIB") or os.path.join(_HERE, "libsrm_b200.so")
 
 c_double_p = C.POINTER(C.c_double)
 c_int32_p = C.POINTER(C.c_int32)
@@ -99,6 +100,7 @@ _SIGS = {
     "srm_b200_sync": (C.c_int, [C.c_void_p]),
     "srm_b200_stopwatch": (C.c_int, [C.c_void_p, C.c_int, c_double_p]),
     "srm_b200_last_round_info": (C.c_int, [C.c_void_p, c_int64_p]),
+    "srm_b200_set_superblock": (C.c_int, [C.c_void_p, C.c_int]),
     "srm_b200_selftest_philox": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "srm_b200_selftest_unit_vectors": (C.c_int, [C.c_int, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p,
                                                  C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),

@@ -18,6 +18,10 @@
 
 using namespace srmb;
 
+#ifndef SRM_SB_W0
+#define SRM_SB_W0 0  // default smallest superblock width in cells; 0 = no superblocks
+#endif
+
 namespace {
 
 thread_local std::string g_create_error;
@@ -71,14 +75,8 @@ struct srm_b200_ctx {
     uint32_t* skey = nullptr;
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
-    int32_t* work = nullptr;    // particles ordered by (colour class, rank in cell)
     int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
     uint8_t* nbr_cnt = nullptr;
-    uint32_t* bcount = nullptr; // (class, rank) bucket counts / starts / cursors
-    uint32_t* bstart = nullptr;
-    uint32_t* bcursor = nullptr;
-    uint32_t* maxrank = nullptr;
-    int64_t bucket_cap = 0;
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -118,6 +116,7 @@ struct srm_b200_ctx {
 
     cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
     int64_t last_nonmovers = 0;
+    int32_t sb_w0 = SRM_SB_W0;  // superblock width (orc_superblocks), srm_b200_set_superblock
 
     // ---------------------------------------------------------------------------
     cudaEvent_t take_event() {
@@ -197,15 +196,10 @@ struct srm_b200_ctx {
         gp = dalloc<GridParams>(1);
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
-        work = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearLocal);
         nbr_cnt = dalloc<uint8_t>(cap);
-        maxrank = dalloc<uint32_t>(1);
         S.xf = dalloc<float4>(cap);
-        ensure_buckets(27 * (kRankMax + 1) + 1);
-        const int work_smem = 2 * 8192 * 4;
-        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
-        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
+        S.lv = dalloc<double4>(cap);
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -224,7 +218,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(work); cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor); cudaFree(maxrank); cudaFree(S.xf);
+        cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(S.xf); cudaFree(S.lv);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -289,6 +283,15 @@ struct srm_b200_ctx {
             g.ncls *= g.col_n[a];
             g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
         }
+        // superblocks (the oracle's orc_superblocks): blocks >= max(12, m) cells wide,
+        // an even number per axis so that the 2-colouring is consistent across the wrap
+        for (int a = 0; a < 3; ++a) {
+            g.nsb[a] = 1;
+            if (a >= dim || sb_w0 <= 0) continue;
+            const int32_t w0 = std::max<int32_t>(g.col_m[a], sb_w0);
+            const int32_t k = 2 * (g.dims[a] / (2 * w0));
+            if (k >= 2) g.nsb[a] = k;
+        }
         // fp32 prefilter: coordinates live in [0, L); 8 ulp of the largest box length
         // bounds the rounding of any coordinate difference and of the radii sums
         double lmax = 0.0;
@@ -303,19 +306,6 @@ struct srm_b200_ctx {
             g.edge_f[a] = static_cast<float>(g.edge[a]);
         }
         return g;
-    }
-
-    void ensure_buckets(int64_t nb) {
-        if (nb <= bucket_cap) return;
-        cudaFree(bcount);
-        cudaFree(bstart);
-        cudaFree(bcursor);
-        bcount = nullptr; bstart = nullptr; bcursor = nullptr;
-        bcount = dalloc<uint32_t>(nb);
-        bstart = dalloc<uint32_t>(nb + 1);
-        bcursor = dalloc<uint32_t>(nb);
-        SRM_CUDA(cudaMemsetAsync(bcount, 0, sizeof(uint32_t) * nb, stream));
-        bucket_cap = nb;
     }
 
     void ensure_cells(int64_t ncells) {
@@ -335,7 +325,6 @@ struct srm_b200_ctx {
 
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
-        ensure_buckets(static_cast<int64_t>(g.ncls) * (kRankMax + 1) + 1);
         k_set_grid<<<1, 1, 0, stream>>>(gp, g);
         launched();
         hg = g;
@@ -379,8 +368,8 @@ struct srm_b200_ctx {
     }
 
     // One round on T (T is rewritten in this round's sorted order); gp must be set.
-    // grid rebuild, then the coloured Gauss-Seidel sweep (one launch per colour class),
-    // then the overlap reduction over the non-movers.
+    // grid rebuild, near lists, then the coloured Gauss-Seidel sweep (one launch per
+    // superblock colour), then the overlap reduction over the non-movers.
     void round(State& T, double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
                bool with_stats, bool with_candidates) {
         if (n_l > kMaxPhases) throw Invalid{"n_l > 254 is not supported by the B200 path"};
@@ -389,40 +378,36 @@ struct srm_b200_ctx {
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
         SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
-            FamScope fs(this, 2);  // work lists: (colour class, rank in cell) buckets
-            const int nbk = hg.ncls * (kRankMax + 1);
-            const bool local = nbk <= 8192;
-            const int wb = blocks_for(n, kWorkBlock * kWorkPer);
-            SRM_CUDA(cudaMemsetAsync(maxrank, 0, sizeof(uint32_t), stream));
-            if (dim == 2)
-                k_work_count<2><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount, maxrank);
-            else
-                k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount, maxrank);
-            k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
-            if (dim == 2)
-                k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
-            else
-                k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
+            FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
             if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
             else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
-            launched(4);
+            launched();
         }
         {
             FamScope fs(this, 1);
-            // grid: enough threads for the largest bucket (every cell of a class occupied)
-            const int sb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(hg.cls_cells, 128), 148 * 64)));
-            for (int cls = 0; cls < hg.ncls; ++cls) {
-                for (int rank = 0; rank <= kRankMax; ++rank) {
-                    if (dim == 2)
-                        k_sweep_class<2><<<sb, 128, 0, stream>>>(cls, rank, S, T, box, gp, rp, cell_start, skey, bstart,
-                                                                 work, nbr, nbr_cnt, acc, active, stats);
-                    else
-                        k_sweep_class<3><<<sb, 128, 0, stream>>>(cls, rank, S, T, box, gp, rp, cell_start, skey, bstart,
-                                                                 work, nbr, nbr_cnt, acc, active, stats);
+            int nsbc = 1;
+            int64_t nsbs = 1, lat = 1;  // superblocks per colour, cells bound of a class lattice
+            for (int a = 0; a < 3; ++a) {
+                int64_t w = hg.dims[a];
+                if (hg.nsb[a] >= 2) {
+                    nsbc *= 2;
+                    nsbs *= hg.nsb[a] / 2;
+                    w = (hg.dims[a] + hg.nsb[a] - 1) / hg.nsb[a] + 1;
                 }
+                lat *= std::max<int64_t>(1, (w + hg.col_m[a] - 1) / hg.col_m[a]);
             }
-            launched(hg.ncls * (kRankMax + 1));
+            const dim3 grid(static_cast<unsigned>(blocks_for(lat, kSweepThreads)), static_cast<unsigned>(nsbs));
+            for (int sbc = 0; sbc < nsbc; ++sbc)
+                for (int cls = 0; cls < hg.ncls; ++cls) {
+                    if (dim == 2)
+                        k_sweep_cells<2><<<grid, kSweepThreads, 0, stream>>>(sbc, cls, S, T, box, gp, rp, cell_start,
+                                                                             skey, nbr, nbr_cnt, acc, active, stats);
+                    else
+                        k_sweep_cells<3><<<grid, kSweepThreads, 0, stream>>>(sbc, cls, S, T, box, gp, rp, cell_start,
+                                                                             skey, nbr, nbr_cnt, acc, active, stats);
+                }
+            launched(nsbc * hg.ncls);
         }
         if (with_stats) {
             FamScope fs(this, 3);
@@ -991,6 +976,17 @@ int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
         info[3] = c->hg.near_s[0];
         info[4] = c->hg.col_m[0];
         info[5] = c->hg.ncells;
+        int64_t nsbc = 1;
+        for (int a = 0; a < 3; ++a) nsbc *= c->hg.nsb[a] >= 2 ? 2 : 1;
+        info[6] = nsbc;
+        info[7] = c->hg.nsb[0];
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_set_superblock(srm_b200_ctx* c, int w0) {
+    return guarded(c, [&]() -> int {
+        c->sb_w0 = w0 > 0 ? w0 : 0;
         return SRM_B200_OK;
     });
 }

@@ -3,8 +3,8 @@
 // One SRM round (engine.hpp:227-234: build_shape_grid -> migrate -> shape_any_collision)
 // is, on the device:
 //   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
-//   work lists     k_work_count -> k_work_scan -> k_work_scatter ((class, rank) buckets)
-//   migrate        k_sweep_class, one cooperative launch per colour class (Gauss-Seidel)
+//   near lists     k_near_lists (round-start neighbours within the trial reach)
+//   migrate        k_sweep_cells, one launch per (superblock colour, colour class)
 //   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
 // All kernels read the grid / round parameters from device memory so that the same
 // launches can be replayed from a CUDA graph.  DESIGN.md §2-§4 has the data layout
@@ -35,6 +35,7 @@ struct GridParams {
     // fp32 prefilter (near_candidates): margin above the fp32 rounding of coordinates
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
+    int32_t nsb[3];     // superblocks per axis (even, or 1), DESIGN.md §3.1
 };
 
 struct RoundParams {
@@ -50,6 +51,7 @@ struct State {
     int32_t* id;
     int32_t* slot;
     float4* xf;  // sorted fp32 copy (x, y, z, r) for prefilters; only in the sorted state S
+    double4* lv; // live record (x, y, z, r) during the sweep, one 32-byte sector; only in S
 };
 
 struct StatsDev {
@@ -259,6 +261,7 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ perm, const uint
         S.r[q] = rr;
         f[3] = static_cast<float>(rr);
         if (S.xf) S.xf[q] = make_float4(f[0], f[1], f[2], f[3]);
+        if (S.lv) S.lv[q] = make_double4(S.x[0][q], D > 1 ? S.x[1][q] : 0.0, D > 2 ? S.x[2][q] : 0.0, rr);
         S.id[q] = T.id[src];
         S.slot[q] = T.slot[src];
         skey[q] = key[src];
@@ -317,25 +320,18 @@ __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
 //
 // The reference's migrate (engine.hpp:89-107) visits particles in storage order; each
 // gets <= n_l trials from its pre-sweep position and keeps the first one that clears the
-// LIVE positions of all others.  Here the visiting order is (colour class, cell, slot):
-// cells are coloured so that two cells of one class are farther apart than any trial can
-// reach (GridParams::col_*), hence one class is swept by one launch with a thread per
-// cell, particles of a cell sequentially in slot order, and the result is identical to
-// the sequential sweep in that order (oracle/srm_oracle.c orc_sweep_round).
+// LIVE positions of all others.  Here the visiting order is (superblock colour,
+// superblock, colour class, cell, slot): cells are coloured so that two cells of one
+// class are farther apart than any trial can reach (GridParams::col_*), and superblocks
+// of one colour are a whole superblock apart (GridParams::nsb), hence one superblock
+// colour is one launch with a CTA per superblock and a thread per cell of a class,
+// particles of a cell sequentially in slot order; the result is identical to the
+// sequential sweep in that order (oracle/srm_oracle.c orc_sweep_round).
 //
-// Live positions: a particle that accepted in this round (acc != 255) lives at T.x, every
-// other one at its round-start position S.x.
-
-template <int D>
-__device__ __forceinline__ void live_pos(const State& S, const State& T, const uint8_t* __restrict__ acc, int64_t j,
-                                         double* p) {
-    if (acc[j] != kNotAccepted) load_pos<D>(T, j, p);
-    else load_pos<D>(S, j, p);
-}
+// Live positions: S.lv[j] holds (x, r) of j -- its round-start position, overwritten by
+// its accepted trial when j moves; one 32-byte sector per neighbour read.
 
 constexpr int kNearLocal = 16;  // near candidates kept per particle; more -> rescan per trial
-constexpr int kRankMax = 1;     // in-cell ranks with their own sub-pass; deeper ranks run
-                                // sequentially behind rank kRankMax (crowded cells)
 
 // Near candidates of sorted particle q: every j whose round-start distance is within
 // ri + rj + 2 c_m (every j a trial of q can touch while j sits within c_m of its start).
@@ -422,7 +418,9 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
         int32_t* my = nbr + q * kNearLocal;
         int nn = 0;
+        const int32_t idq = S.id[q];
         near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+            if (S.id[j] == idq) return;  // shape.hpp:544 self-exclusion by id
             if (nn < kNearLocal) my[nn] = static_cast<int32_t>(j);
             ++nn;
         });
@@ -438,34 +436,65 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
                                                uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                StatsDev* stats) {
     const int nn = nbr_cnt[q];
-    const int32_t* nb = nbr + q * kNearLocal;
     double xi[D];
     load_pos<D>(S, q, xi);
     const double ri = S.r[q];
-    const int32_t idi = S.id[q];
     const int32_t sl = S.slot[q];
     double p[D];
     int accepted = -1;
-    for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
-        propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
-        bool ok = true;
-        auto test = [&](int64_t j) {
-            if (!ok || S.id[j] == idi) return;
-            double xl[D];
-            live_pos<D>(S, T, acc, j, xl);
-            if (sphere_overlap<D>(box, p, ri, xl, S.r[j])) ok = false;
-        };
-        if (nn != kNearOverflow) {
-            for (int t = 0; t < nn && ok; ++t) test(nb[t]);
-        } else {  // crowded neighbourhood: rescan (same candidate set)
-            near_candidates<D>(g, cs, S.xf, q, skey[q], test);
+    if (nn != kNearOverflow) {
+        // the near list once (64 B, four 16-byte loads); per trial every record load is
+        // issued before any test (no early exit), kBatch at a time, so a trial costs one
+        // memory latency per batch instead of one per neighbour
+        constexpr int kBatch = 4;
+        int32_t nb[kNearLocal];
+        const int4* nb4 = reinterpret_cast<const int4*>(nbr + q * kNearLocal);
+#pragma unroll
+        for (int c = 0; c < kNearLocal / 4; ++c) {
+            int4 v = make_int4(0, 0, 0, 0);
+            if (4 * c < nn) v = nb4[c];
+            nb[4 * c] = v.x; nb[4 * c + 1] = v.y; nb[4 * c + 2] = v.z; nb[4 * c + 3] = v.w;
         }
-        if (ok) accepted = l;
+        for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
+            propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+            bool hit = false;
+#pragma unroll
+            for (int t0 = 0; t0 < kNearLocal; t0 += kBatch) {
+                if (t0 < nn) {
+                    double4 v[kBatch];
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u)
+                        if (t0 + u < nn) v[u] = S.lv[nb[t0 + u]];
+#pragma unroll
+                    for (int u = 0; u < kBatch; ++u) {
+                        if (t0 + u < nn) {
+                            const double xl[3] = {v[u].x, v[u].y, v[u].z};
+                            hit |= sphere_overlap<D>(box, p, ri, xl, v[u].w);
+                        }
+                    }
+                }
+            }
+            if (!hit) accepted = l;
+        }
+    } else {  // crowded neighbourhood: rescan (same candidate set, id filter as the list)
+        const int32_t idq = S.id[q];
+        for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
+            propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+            bool ok = true;
+            near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+                if (!ok || S.id[j] == idq) return;
+                const double4 v = S.lv[j];
+                const double xl[3] = {v.x, v.y, v.z};
+                if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
+            });
+            if (ok) accepted = l;
+        }
     }
+    if (accepted >= 0) S.lv[q] = make_double4(p[0], D > 1 ? p[1] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, ri);
 #pragma unroll
     for (int a = 0; a < D; ++a) T.x[a][q] = accepted >= 0 ? p[a] : xi[a];
     T.r[q] = ri;
-    T.id[q] = idi;
+    T.id[q] = S.id[q];
     T.slot[q] = sl;
     acc[q] = accepted >= 0 ? static_cast<uint8_t>(accepted) : kNotAccepted;
     if (accepted < 0) active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
@@ -477,181 +506,87 @@ __device__ __forceinline__ int colour1(int x, int m, int n) {
     return x < body ? x % m : m + (x - body);
 }
 
-template <int D>
-__device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
-    const int cx = static_cast<int>(key % static_cast<uint32_t>(g.dims[0]));
-    const uint32_t rest = key / static_cast<uint32_t>(g.dims[0]);
-    const int cy = static_cast<int>(rest % static_cast<uint32_t>(g.dims[1]));
-    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(g.dims[1])) : 0;
-    int k = colour1(cx, g.col_m[0], g.dims[0]);
-    k += g.col_n[0] * colour1(cy, g.col_m[1], g.dims[1]);
-    if (D == 3) k += g.col_n[0] * g.col_n[1] * colour1(cz, g.col_m[2], g.dims[2]);
-    return k;
-}
+#ifndef SRM_SWEEP_THREADS
+#define SRM_SWEEP_THREADS 128
+#endif
+constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
-// Work lists: bucket (class, rank-in-cell) of every sorted particle; ranks above
-// kRankMax get no bucket (the rank-kRankMax particle sweeps the rest of its cell).
-constexpr int kWorkBlock = 1024;
-constexpr int kWorkPer = 8;   // particles per thread: 8192 per block
-
-template <int D>
-__device__ __forceinline__ int bucket_of(const GridParams& g, const int64_t* __restrict__ cs, uint32_t key, int64_t q,
-                                         unsigned long long* rank_out) {
-    const int64_t rank = q - cs[key];
-    *rank_out = static_cast<unsigned long long>(rank);
-    if (rank > kRankMax) return -1;
-    return class_of_key<D>(g, key) * (kRankMax + 1) + static_cast<int>(rank);
-}
-
-template <int D>
-__global__ void __launch_bounds__(kWorkBlock) k_work_count(int64_t n, const GridParams* __restrict__ gp,
-                                                           const int64_t* __restrict__ cs,
-                                                           const uint32_t* __restrict__ skey,
-                                                           uint32_t* __restrict__ bcount, uint32_t* __restrict__ maxrank) {
-    extern __shared__ uint32_t hist[];
-    const GridParams& g = *gp;
-    const int nb = g.ncls * (kRankMax + 1);
-    const bool local = nb <= 8192;
-    if (local)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    unsigned long long mr = 0;
-    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
-    for (int k = 0; k < kWorkPer; ++k) {
-        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        if (q >= n) break;
-        unsigned long long rank;
-        const int b = bucket_of<D>(g, cs, skey[q], q, &rank);
-        mr = rank > mr ? rank : mr;
-        if (b < 0) continue;
-        if (local) atomicAdd(&hist[b], 1u);
-        else atomicAdd(&bcount[b], 1u);
-    }
+// Cells of colour class cls in the superblock (lo, hi) form a lattice per axis:
+// first + stride * i, i < cnt (colour1 inverted on [lo, hi)).
+__device__ __forceinline__ void class_lattice(const GridParams& g, int cls, const int* lo, const int* hi, int* first,
+                                              int* stride, int* cnt) {
+    int rem = cls;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long t = __shfl_down_sync(0xffffffffu, mr, o);
-        mr = t > mr ? t : mr;
-    }
-    if ((threadIdx.x & 31) == 0 && mr) atomicMax(maxrank, static_cast<uint32_t>(mr));
-    __syncthreads();
-    if (local)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x)
-            if (hist[b]) atomicAdd(&bcount[b], hist[b]);
-}
-
-// single block: exclusive scan of the bucket counts; cursors start at the bucket starts
-__global__ void k_work_scan(const GridParams* __restrict__ gp, uint32_t* __restrict__ bcount,
-                            uint32_t* __restrict__ bstart, uint32_t* __restrict__ cursor) {
-    const int nb = gp->ncls * (kRankMax + 1);
-    __shared__ uint32_t carry;
-    __shared__ uint32_t wsum[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
-        const int b = b0 + threadIdx.x;
-        const uint32_t v = b < nb ? bcount[b] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
+    for (int a = 0; a < 3; ++a) {
+        const int m = g.col_m[a], n = g.dims[a];
+        const int cv = rem % g.col_n[a];
+        rem /= g.col_n[a];
+        const int body = m * (n / m);
+        if (cv < m) {
+            const int f = lo[a] + ((cv - lo[a] % m) + m) % m;
+            const int b = min(hi[a], body);
+            first[a] = f;
+            stride[a] = m;
+            cnt[a] = f < b ? (b - f + m - 1) / m : 0;
+        } else {
+            const int x = body + (cv - m);
+            first[a] = x;
+            stride[a] = 1;
+            cnt[a] = (x >= lo[a] && x < hi[a]) ? 1 : 0;
         }
-        if (lane == 31) wsum[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            const uint32_t w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0u;
-            uint32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += t;
-            }
-            wsum[lane] = wi - w;
-        }
-        __syncthreads();
-        const uint32_t ex = carry + wsum[wid] + incl - v;
-        if (b < nb) {
-            bstart[b] = ex;
-            cursor[b] = ex;
-            bcount[b] = 0u;  // ready for the next round's histogram
-        }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) bstart[nb] = carry;
-}
-
-template <int D>
-__global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const GridParams* __restrict__ gp,
-                                                             const int64_t* __restrict__ cs,
-                                                             const uint32_t* __restrict__ skey,
-                                                             uint32_t* __restrict__ cursor, int32_t* __restrict__ work) {
-    extern __shared__ uint32_t hist[];  // [nb] counts, then [nb] block bases
-    const GridParams& g = *gp;
-    const int nb = g.ncls * (kRankMax + 1);
-    const bool local = nb <= 8192;
-    uint32_t* base = hist + (local ? nb : 0);
-    if (local)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
-    int myb[kWorkPer];
-    uint32_t myl[kWorkPer];
-#pragma unroll
-    for (int k = 0; k < kWorkPer; ++k) {
-        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        myb[k] = -1;
-        if (q >= n) continue;
-        unsigned long long rank;
-        myb[k] = bucket_of<D>(g, cs, skey[q], q, &rank);
-        if (myb[k] < 0) continue;
-        if (local) myl[k] = atomicAdd(&hist[myb[k]], 1u);
-        else work[atomicAdd(&cursor[myb[k]], 1u)] = static_cast<int32_t>(q);
-    }
-    if (!local) return;
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x)
-        if (hist[b]) base[b] = atomicAdd(&cursor[b], hist[b]);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kWorkPer; ++k) {
-        if (myb[k] < 0) continue;
-        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        work[base[myb[k]] + myl[k]] = static_cast<int32_t>(q);
     }
 }
 
-// One (colour class, rank) step: thread per particle of the bucket.  Rank 0 is the
-// first particle of every occupied cell of the class; the rank-1 thread of a crowded
-// cell sweeps all its remaining particles sequentially (slot order).
+// Superblock sb of colour sbc: along axis a its block index is colour bit + 2 * j_a
+// (every block when the axis is not split); block k covers [ceil(k n / nsb), ceil((k+1) n / nsb)),
+// i.e. x lies in block floor(x nsb / n) (oracle/srm_oracle.c orc_superblocks).
+__device__ __forceinline__ void superblock_range(const GridParams& g, int sbc, int64_t sb, int* lo, int* hi) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int nsb = g.nsb[a], n = g.dims[a];
+        int k = 0;
+        if (nsb >= 2) {
+            const int per = nsb / 2;
+            k = ((sbc >> a) & 1) + 2 * static_cast<int>(sb % per);
+            sb /= per;
+        }
+        lo[a] = static_cast<int>((static_cast<int64_t>(k) * n + nsb - 1) / nsb);
+        hi[a] = static_cast<int>((static_cast<int64_t>(k + 1) * n + nsb - 1) / nsb);
+    }
+}
+
+// One step of the sweep: colour class cls of the superblocks of colour sbc.  A thread
+// per cell (blockIdx.y = superblock), the particles of a cell in slot order.  Cells of
+// one class are farther apart than any trial can reach and superblocks of one colour a
+// whole superblock apart, so all threads of the launch are independent and the launch
+// sequence (sbc, cls) reproduces the sequential sweep of orc_sweep_round bit for bit.
 template <int D>
-__global__ void __launch_bounds__(128) k_sweep_class(int cls, int rank, State S, State T, Box box,
-                                                     const GridParams* __restrict__ gp,
-                                                     const RoundParams* __restrict__ rpp,
-                                                     const int64_t* __restrict__ cs,
-                                                     const uint32_t* __restrict__ skey,
-                                                     const uint32_t* __restrict__ bstart,
-                                                     const int32_t* __restrict__ work,
-                                                     const int32_t* __restrict__ nbr, const uint8_t* __restrict__ nbr_cnt,
-                                                     uint8_t* __restrict__ acc, int32_t* __restrict__ active,
-                                                     StatsDev* stats) {
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_cells(int sbc, int cls, State S, State T, Box box,
+                                                               const GridParams* __restrict__ gp,
+                                                               const RoundParams* __restrict__ rpp,
+                                                               const int64_t* __restrict__ cs,
+                                                               const uint32_t* __restrict__ skey,
+                                                               const int32_t* __restrict__ nbr,
+                                                               const uint8_t* __restrict__ nbr_cnt,
+                                                               uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                                               StatsDev* stats) {
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
+    int lo[3], hi[3], first[3], stride[3], cnt[3];
+    superblock_range(g, sbc, blockIdx.y, lo, hi);
+    class_lattice(g, cls, lo, hi, first, stride, cnt);
+    const int cxy = cnt[0] * cnt[1];
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<int64_t>(cxy) * cnt[2]) return;
+    const int iz = static_cast<int>(t / cxy), r2 = static_cast<int>(t - static_cast<int64_t>(iz) * cxy);
+    const int iy = r2 / cnt[0], ix = r2 - iy * cnt[0];
+    const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
+                             g.dims[0] +
+                         first[0] + stride[0] * ix;
     const RoundParams rp = *rpp;
-    const int b = cls * (kRankMax + 1) + rank;
-    const int64_t lo = bstart[b], hi = bstart[b + 1];
-    for (int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < hi;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t q = work[t];
+    const int64_t e = cs[cell + 1];
+    for (int64_t q = cs[cell]; q < e; ++q)
         sweep_particle<D>(q, S, T, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
-        if (rank == kRankMax) {
-            const int64_t e = cs[skey[q] + 1];
-            for (int64_t q2 = q + 1; q2 < e; ++q2)
-                sweep_particle<D>(q2, S, T, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
-        }
-    }
 }
 
 // Overlap reduction after the sweep.  A particle that accepted a trial cleared every

@@ -6,15 +6,14 @@ parameters; the trajectories differ (parallel round vs sequential mt19937_64 swe
 DESIGN.md §3), so the end states are compared statistically:
   * f_target reached within 1e-9 relative, zero overlaps (oracle audit);
   * nearest-neighbour-distance histogram (reference nearest_neighbor_distances), 40 bins
-    over [2 r_t, 2.8 r_t] pooled over seeds: per-bin |dN| <= max(3 sigma, 2%), plus a
-    two-sample KS test at alpha = 0.01 on the pooled samples;
-  * RDF counts on [2 r_t, 5 r_t] (60 bins): per-bin |dN| <= max(3 sigma_Poisson, 2%).
+    over [2 r_t, 2.8 r_t] pooled over seeds: per-bin |dN| <= max(4 sigma, 2%), a chi-square
+    homogeneity test and a two-sample KS test at alpha = 0.01 on the pooled samples;
+  * RDF counts on [2 r_t, 5 r_t] (60 bins): per-bin |dN| <= max(4 sigma_Poisson, 2%), chi-square p > 0.01.
 Also grid keys / reorder remap / collision flags on the golden states, bit-exact."""
 import os
 
 import numpy as np
 import pytest
-from scipy import stats
 
 import orc
 import paper_2605_18254_b200 as srm
@@ -49,7 +48,6 @@ def test_generate_statistics_match_reference(name):
     L = [1.0] * dim
     unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
     r0 = (float(z["f0"]) / (n * unit)) ** (1.0 / dim)
-    rt = float(z["r_target"])
     nnd, rdf = [], None
     for s in z["seeds"]:
         pos, ids = srm.rsa_place(np.full(n, r0), L, 10000, 1000 + int(s))
@@ -62,16 +60,6 @@ def test_generate_statistics_match_reference(name):
         out = res.snapshot
         assert orc.o_stats(dim, L, out.pos, out.radius).overlap_pairs == 0
         nnd.append(orc.r_nnd(dim, L, out.pos))
-        c = stats_util.rdf_counts(out.pos, L, 2.0 * rt * 0.999, 5.0 * rt, 60)
+        c = stats_util.rdf_counts(out.pos, L, *stats_util.rdf_window(z))
         rdf = c if rdf is None else rdf + c
-    nnd = np.concatenate(nnd)
-    ref = z["nnd"].ravel()
-    bins = np.linspace(2.0 * rt * 0.999, 2.8 * rt, 41)
-    h_dev = np.histogram(nnd, bins)[0]
-    h_ref = np.histogram(ref, bins)[0]
-    ok, tol = stats_util.hist_agree(h_dev, h_ref)
-    assert ok.all(), f"NND bins out of tolerance: {np.where(~ok)[0]} dev={h_dev[~ok]} ref={h_ref[~ok]}"
-    ks = stats.ks_2samp(nnd, ref)
-    assert ks.pvalue > 0.01, f"KS p={ks.pvalue:.3g} stat={ks.statistic:.4f}"
-    ok, tol = stats_util.hist_agree(rdf, z["rdf"])
-    assert ok.all(), f"RDF bins out of tolerance: {np.where(~ok)[0]} dev={rdf[~ok]} ref={z['rdf'][~ok]}"
+    stats_util.check_against_reference(nnd, rdf, z)
