@@ -61,6 +61,18 @@ def radius_for(f, n, dim, L=1.0):
     return (f * L ** dim / (n * unit_measure(dim))) ** (1.0 / dim)
 
 
+def step_traffic():
+    """ncu DRAM bytes per particle-update of the migrate step (near lists + sweep), from the
+    newest committed profiles/*_traffic.json (one `ncu` capture of tools/profile_round.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as fh:
+        d = json.load(fh)
+    return float(d["step_dram_bytes_per_update"]), os.path.relpath(files[-1], ROOT)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -288,7 +300,8 @@ def run_b200(args, cfg, world, rank, local, pg):
     fam_ms, fam_calls = ctx.timing_get()
     ctx.timing_enable(False)
     per_round = [v / args.steps for v in fam_ms]
-    # migrate step = near lists + (class, rank) work lists + the coloured sweep
+    # migrate step = near lists (family 2) + the coloured sweep (family 1, one launch per
+    # colour class); per-round device time from CUDA events on the context stream
     t_mig = per_round[1] + per_round[2]
     peak, peak_kind = peaks()
     algo = n * BYTES_STEP[dim]
@@ -315,6 +328,9 @@ def run_b200(args, cfg, world, rank, local, pg):
     bytes_io = n * (8 * dim + 8 + 4)
     e2e_value = world * n * N_K / (e2e_ms * 1e-3)
 
+    tb, tsrc = step_traffic()
+    traffic = tb * n if tb else None  # DRAM bytes (read + write) of one step (one round), ncu
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, c_m)
@@ -331,11 +347,15 @@ def run_b200(args, cfg, world, rank, local, pg):
                        "l2": f"inputs larger than L2 (state {n * (8 * dim + 16) / 1e6:.0f} MB)",
                        "prep": prep},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "migrate step per round (k_near_lists + k_work_* + k_sweep_class x classes)",
-                         "algorithmic_bytes_per_update": BYTES_STEP[dim], "peak_kind": peak_kind},
+                         "frac": achieved / peak,
+                         "traffic": traffic,
+                         "kernel": "migrate step per round: k_near_lists + k_sweep_cells x colour classes",
+                         "traffic_unit": "bytes per step (one round of near lists + sweep), ncu dram__bytes_read+write",
+                         "algorithmic_bytes_per_step": algo,
+                         "algorithmic_bytes_per_update": BYTES_STEP[dim], "step_ms_per_round": t_mig,
+                         "traffic_bytes_per_update": tb, "traffic_source": tsrc, "peak_kind": peak_kind},
             "phase_ms_per_round": {"grid_rebuild": per_round[0], "sweep": per_round[1],
-                                   "near_and_work_lists": per_round[2], "reduction": per_round[3]},
+                                   "near_lists": per_round[2], "reduction": per_round[3]},
             "last_round": {"overlap_pairs": st.overlap_pairs, "movers": st.movers,
                            "max_penetration": st.max_penetration},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_io,

@@ -14,8 +14,10 @@
 //   rsa_place           rsa.hpp:21-61       (seeded form; bit-identical to Rng(seed))
 //
 // Differences the caller can observe:
-//   * migrate is the parallel round: decisions depend on (key, slot), not on storage
-//     order, and trajectories differ from the sequential mt19937_64 sweep;
+//   * migrate is the coloured Gauss-Seidel sweep: the reference's
+//     per-particle rule in (colour class, cell, slot) order with Philox trials keyed by
+//     (key, slot, attempt, round, iteration), so trajectories differ from the
+//     storage-order mt19937_64 sweep (statistically equal, tests/test_gpu_e2e.py);
 //   * errors: ValidationError / PlacementFailure / std::invalid_argument as in the
 //     reference; device failures throw srm::b200::DeviceError.
 // Disks and spheres (SphereShape<2>, SphereShape<3>) are supported.
@@ -141,8 +143,8 @@ GenerateResult<S> srm_generate(const Snapshot<S>& initial, const SrmParams& para
     return result;
 }
 
-// engine.hpp:89-107: one migration sweep against `grid` (its cell size), the parallel
-// round of DESIGN.md §3 keyed by one draw of rng.  Returns the accepted flags.
+// engine.hpp:89-107: one migration sweep against `grid` (its cell size), the coloured
+// Gauss-Seidel round of DESIGN.md §3.1 keyed by one draw of rng.  Returns the accepted flags.
 template <ShapeModel S>
 std::vector<std::uint8_t> migrate(std::vector<typename S::ParticleT>& particles, const CellGrid<S::dim>& grid,
                                   double c_m, double /*c_r*/, int n_l, Rng& rng) {
