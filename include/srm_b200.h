@@ -196,13 +196,8 @@ int srm_b200_sync(srm_b200_ctx* ctx);
 int srm_b200_stopwatch(srm_b200_ctx* ctx, int op, double* ms);
 /* Diagnostics of the last round whose statistics were read: info[0] non-movers,
  * [1] colour classes of the sweep, [2] largest cells per class, [3] near-search half
- * width (x), [4] colouring modulus (x), [5] cells of the grid, [6] superblock colours,
- * [7] superblocks along x. */
+ * width (x), [4] colouring modulus (x), [5] cells of the grid. */
 int srm_b200_last_round_info(srm_b200_ctx* ctx, int64_t* info);
-/* Sweep schedule: superblocks at least max(w0, m) cells wide, 2-coloured
- * per axis (w0 <= 0: none, the sweep runs colour class by colour class over the whole
- * grid).  Changes the visiting order, hence the trajectory; the oracle takes the same w0. */
-int srm_b200_set_superblock(srm_b200_ctx* ctx, int w0);
 
 /* ---- self tests of the device primitives (no reference counterpart) ------------------ */
 /* the hand-written device Philox4x32-10 next to CUDA's curand_Philox4x32_10 */

@@ -333,33 +333,17 @@ static int colour1(int x, int m, int n) {
     return x < body ? x % m : m + (x - body);
 }
 
-/* Superblocks: per axis an even number nsb = 2 floor(dims / 24) of
- * blocks of >= 12 cells (or one block when dims < 24); coordinate x lies in block
- * floor(x * nsb / dims); blocks are 2-coloured by parity, so two blocks of one colour
- * are separated by a whole block (>= 12 cells, far beyond any trial's reach).        */
-void orc_superblocks(int dim, const int32_t* dims, const int32_t* col_m, int32_t sb_w0, int32_t* nsb) {
-    for (int a = 0; a < 3; ++a) {
-        if (a >= dim || sb_w0 <= 0) { nsb[a] = 1; continue; }
-        /* blocks at least max(sb_w0, m) cells wide: two blocks of one colour are a whole
-           block (> s = m - 1 cells, the interaction reach) apart */
-        const int32_t w0 = col_m[a] > sb_w0 ? col_m[a] : sb_w0;
-        const int32_t k = 2 * (dims[a] / (2 * w0));
-        nsb[a] = k >= 2 ? k : 1;
-    }
-}
-
 /* One SRM round's migrate as a coloured Gauss-Seidel sweep: the
  * reference's migrate (engine.hpp:89-107) -- per particle <= n_l trials from its
  * pre-sweep position, each tested against the LIVE positions of all other particles
  * (shape.hpp:539-546, trial first), first clear trial kept, otherwise an exact revert --
- * in the order (superblock colour, superblock, cell class, cell, slot) of the round
- * grid of cell size `cell_size` instead of storage order.  Superblocks of one colour
- * and cells of one class within a superblock never interact, so the GPU runs them
+ * in the order (cell class, cell, slot) of the round grid of cell size `cell_size`
+ * instead of storage order.  Cells of one class never interact, so the GPU runs them
  * concurrently and equals this sequential sweep bit for bit.  Trials draw Philox
  * (orc_propose) instead of mt19937_64.  brute != 0: all-pairs candidate search.      */
 void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
                      const int32_t* id, const int32_t* slot, double cell_size, double c_m, int n_l,
-                     uint64_t seed, uint32_t round_id, uint32_t iteration, int32_t sb_w0, double* xnew,
+                     uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
                      uint8_t* acc, int brute) {
     int32_t dims[3] = {1, 1, 1};
     double edge[3] = {1.0, 1.0, 1.0};
@@ -381,30 +365,21 @@ void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, cons
     /* class of every particle, then a stable pass per class in (cell, slot) order */
     int32_t* cls = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
     int64_t nclass = (int64_t)ncol[0] * ncol[1] * ncol[2];
-    int32_t nsb[3];
-    orc_superblocks(dim, dims, m, sb_w0, nsb);
-    int32_t* sbc = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
     for (int64_t i = 0; i < n; ++i) {
         int32_t c[3];
         orc_cell_coords(dim, dims, edge, x0 + i * dim, c);
-        int64_t k = 0, b = 0;
-        for (int a = dim - 1; a >= 0; --a) {
-            k = k * ncol[a] + colour1(c[a], m[a], dims[a]);
-            b = b * 2 + (nsb[a] >= 2 ? ((int64_t)c[a] * nsb[a] / dims[a]) % 2 : 0);
-        }
+        int64_t k = 0;
+        for (int a = dim - 1; a >= 0; --a) k = k * ncol[a] + colour1(c[a], m[a], dims[a]);
         cls[i] = (int32_t)k;
-        sbc[i] = (int32_t)b;
     }
     memcpy(xnew, x0, sizeof(double) * (size_t)(n * dim));
     for (int64_t i = 0; i < n; ++i) acc[i] = ORC_NOT_ACCEPTED;
     double p[3];
-    /* order: (superblock colour, [superblock], cell class, cell, slot); superblocks of
-       one colour never interact, so they are visited interleaved here */
-    for (int64_t sc = 0; sc < 8; ++sc)
+    /* order: (cell class, cell, slot) */
     for (int64_t k = 0; k < nclass; ++k) {
         for (int64_t q = 0; q < n; ++q) { /* q walks the (cell, slot) order */
             const int64_t i = order[q];
-            if (cls[i] != k || sbc[i] != sc) continue;
+            if (cls[i] != k) continue;
             for (int l = 0; l < n_l; ++l) {
                 orc_propose(dim, L, x0 + i * dim, c_m, seed, (uint32_t)slot[i], (uint32_t)l, round_id,
                             iteration, p);
@@ -422,7 +397,7 @@ void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, cons
             }
         }
     }
-    free(keys); free(order); free(cstart); free(cls); free(sbc);
+    free(keys); free(order); free(cstart); free(cls);
     csr_free(&nb);
 }
 

@@ -72,8 +72,6 @@ typedef struct {
 void orc_colouring(int dim, const int32_t* dims, const double* edge, double maxr, double c_m,
                    int32_t* m_out, int32_t* ncol_out);
 
-/* Superblock partition of the round grid: blocks per axis. */
-void orc_superblocks(int dim, const int32_t* dims, const int32_t* col_m, int32_t sb_w0, int32_t* nsb);
 
 /* One SRM round's migrate for disks/spheres as the coloured Gauss-Seidel sweep of
  * DESIGN.md §3.1 on the round grid of cell size `cell_size`:
@@ -82,8 +80,8 @@ void orc_superblocks(int dim, const int32_t* dims, const int32_t* col_m, int32_t
  * brute != 0 forces the O(n^2) all-pairs candidate search. */
 void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, const double* r,
                      const int32_t* id, const int32_t* slot, double cell_size, double c_m, int n_l,
-                     uint64_t seed, uint32_t round_id, uint32_t iteration, int32_t sb_w0,
-                     double* xnew, uint8_t* acc, int brute);
+                     uint64_t seed, uint32_t round_id, uint32_t iteration, double* xnew,
+                     uint8_t* acc, int brute);
 
 /* Global overlap statistics of a state (all pairs, cell-list accelerated). */
 void orc_overlap_stats(int dim, const double* L, int64_t n, const double* x, const double* r,

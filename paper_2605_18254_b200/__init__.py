@@ -336,14 +336,10 @@ class Context:
         self._c(_native.lib().srm_b200_sync(self._h))
 
     def last_round_info(self) -> dict:
-        v = (C.c_int64 * 8)()
+        v = (C.c_int64 * 6)()
         self._c(_native.lib().srm_b200_last_round_info(self._h, v))
         return {"nonmovers": v[0], "colour_classes": v[1], "cells_per_class": v[2], "near_half_width": v[3],
-                "colour_modulus": v[4], "cells": v[5], "superblock_colours": v[6], "superblocks_x": v[7]}
-
-    def set_superblock(self, w0: int) -> None:
-        """sweep schedule: superblocks >= max(w0, m) cells wide (0: none), DESIGN.md §3.1"""
-        self._c(_native.lib().srm_b200_set_superblock(self._h, int(w0)))
+                "colour_modulus": v[4], "cells": v[5]}
 
     def stopwatch_start(self) -> None:
         """record a CUDA event on the context stream"""

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -18,9 +19,7 @@
 
 using namespace srmb;
 
-#ifndef SRM_SB_W0
-#define SRM_SB_W0 0  // default smallest superblock width in cells; 0 = no superblocks
-#endif
+
 
 namespace {
 
@@ -70,13 +69,18 @@ struct srm_b200_ctx {
     std::string err;
 
     State P{}, Q{}, S{};
-    double* xblock[3] = {nullptr, nullptr, nullptr};  // contiguous x storage of P, Q, S
     uint32_t* key = nullptr;
     uint32_t* skey = nullptr;
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
     uint8_t* nbr_cnt = nullptr;
+    int32_t* work = nullptr;     // (colour class, rank) work lists of the sweep, [cap]
+    uint32_t* bcount = nullptr;  // bucket counts / starts / cursors, [ncls * kRanks + 1]
+    uint32_t* bstart = nullptr;
+    uint32_t* bcursor = nullptr;
+    int64_t bucket_cap = 0;
+    std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -116,7 +120,6 @@ struct srm_b200_ctx {
 
     cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
     int64_t last_nonmovers = 0;
-    int32_t sb_w0 = SRM_SB_W0;  // superblock width (orc_superblocks), srm_b200_set_superblock
 
     // ---------------------------------------------------------------------------
     cudaEvent_t take_event() {
@@ -170,25 +173,29 @@ struct srm_b200_ctx {
     }
 
     // ---------------------------------------------------------------------------
-    void alloc_state(State& s, int slotx) {
-        xblock[slotx] = dalloc<double>(3 * cap);
-        for (int a = 0; a < 3; ++a) s.x[a] = xblock[slotx] + a * cap;
-        s.r = dalloc<double>(cap);
+    void alloc_state(State& s) {
+        s.rec = dalloc<double4>(cap);
         s.id = dalloc<int32_t>(cap);
         s.slot = dalloc<int32_t>(cap);
     }
     static void free_state(State& s) {
-        cudaFree(s.r);
+        cudaFree(s.rec);
         cudaFree(s.id);
         cudaFree(s.slot);
+    }
+    // exchange the particle buffers of two states (the sorted state's fp32 copy stays)
+    static void swap_state(State& a, State& b) {
+        std::swap(a.rec, b.rec);
+        std::swap(a.id, b.id);
+        std::swap(a.slot, b.slot);
     }
 
     void init() {
         SRM_CUDA(cudaSetDevice(device));
         SRM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-        alloc_state(P, 0);
-        alloc_state(Q, 1);
-        alloc_state(S, 2);
+        alloc_state(P);
+        alloc_state(Q);
+        alloc_state(S);
         key = dalloc<uint32_t>(cap);
         skey = dalloc<uint32_t>(cap);
         perm = dalloc<int32_t>(cap);
@@ -198,8 +205,11 @@ struct srm_b200_ctx {
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearLocal);
         nbr_cnt = dalloc<uint8_t>(cap);
+        work = dalloc<int32_t>(cap);
+        const int work_smem = 2 * kBucketSmem * 4;
+        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
+        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
         S.xf = dalloc<float4>(cap);
-        S.lv = dalloc<double4>(cap);
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -211,14 +221,13 @@ struct srm_b200_ctx {
     ~srm_b200_ctx() {
         if (device >= 0) cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        for (int k = 0; k < 3; ++k) cudaFree(xblock[k]);
         free_state(P);
         free_state(Q);
         free_state(S);
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(S.xf); cudaFree(S.lv);
+        cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(S.xf); cudaFree(work); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -283,15 +292,7 @@ struct srm_b200_ctx {
             g.ncls *= g.col_n[a];
             g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
         }
-        // superblocks (the oracle's orc_superblocks): blocks >= max(12, m) cells wide,
-        // an even number per axis so that the 2-colouring is consistent across the wrap
-        for (int a = 0; a < 3; ++a) {
-            g.nsb[a] = 1;
-            if (a >= dim || sb_w0 <= 0) continue;
-            const int32_t w0 = std::max<int32_t>(g.col_m[a], sb_w0);
-            const int32_t k = 2 * (g.dims[a] / (2 * w0));
-            if (k >= 2) g.nsb[a] = k;
-        }
+        g.nrank = kRanks;
         // fp32 prefilter: coordinates live in [0, L); 8 ulp of the largest box length
         // bounds the rounding of any coordinate difference and of the radii sums
         double lmax = 0.0;
@@ -325,6 +326,32 @@ struct srm_b200_ctx {
 
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
+        // cells per colour class: on each axis a body colour v < m has
+        // floor(n / m) cells, a remainder colour one; class offsets into the work lists
+        std::vector<int64_t> off(static_cast<size_t>(g.ncls) + 1, 0);
+        for (int64_t k = 0; k < g.ncls; ++k) {
+            int64_t rem = k, cells = 1;
+            for (int a = 0; a < 3; ++a) {
+                const int64_t v = rem % g.col_n[a];
+                rem /= g.col_n[a];
+                cells *= v < g.col_m[a] ? g.dims[a] / g.col_m[a] : 1;
+            }
+            off[k + 1] = off[k] + cells;
+        }
+        if (off[g.ncls] != g.ncells) throw std::logic_error("colour classes do not tile the grid");
+        const int64_t nbk = static_cast<int64_t>(g.ncls) * kRanks;
+        if (nbk + 1 > bucket_cap) {
+            cudaFree(bcount);
+            cudaFree(bstart);
+            cudaFree(bcursor);
+            bcount = nullptr; bstart = nullptr; bcursor = nullptr;
+            bucket_cap = nbk + 1;
+            bcount = dalloc<uint32_t>(bucket_cap);
+            bstart = dalloc<uint32_t>(bucket_cap);
+            bcursor = dalloc<uint32_t>(bucket_cap);
+            SRM_CUDA(cudaMemsetAsync(bcount, 0, sizeof(uint32_t) * bucket_cap, stream));  // k_work_scan re-zeroes
+        }
+        cls_cells_h.assign(off.begin(), off.end());
         k_set_grid<<<1, 1, 0, stream>>>(gp, g);
         launched();
         hg = g;
@@ -378,36 +405,39 @@ struct srm_b200_ctx {
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
         SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
-            FamScope fs(this, 2);  // near lists
+            FamScope fs(this, 2);  // near lists + (class, rank) work lists
+            const int nbk = hg.ncls * kRanks;
+            const bool local = nbk <= kBucketSmem;
+            const int wb = blocks_for(n, kWorkBlock * kWorkPer);
+            if (dim == 2)
+                k_work_count<2><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
+            else
+                k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
+            k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
+            if (dim == 2)
+                k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
+            else
+                k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
             const int nb = blocks_for(n, 256);
             if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
             else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
-            launched();
+            launched(4);
         }
         {
             FamScope fs(this, 1);
-            int nsbc = 1;
-            int64_t nsbs = 1, lat = 1;  // superblocks per colour, cells bound of a class lattice
-            for (int a = 0; a < 3; ++a) {
-                int64_t w = hg.dims[a];
-                if (hg.nsb[a] >= 2) {
-                    nsbc *= 2;
-                    nsbs *= hg.nsb[a] / 2;
-                    w = (hg.dims[a] + hg.nsb[a] - 1) / hg.nsb[a] + 1;
-                }
-                lat *= std::max<int64_t>(1, (w + hg.col_m[a] - 1) / hg.col_m[a]);
-            }
-            const dim3 grid(static_cast<unsigned>(blocks_for(lat, kSweepThreads)), static_cast<unsigned>(nsbs));
-            for (int sbc = 0; sbc < nsbc; ++sbc)
-                for (int cls = 0; cls < hg.ncls; ++cls) {
+            for (int cls = 0; cls < hg.ncls; ++cls) {
+                const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), 148 * 32)));
+                for (int rank = 0; rank < kRanks; ++rank) {
                     if (dim == 2)
-                        k_sweep_cells<2><<<grid, kSweepThreads, 0, stream>>>(sbc, cls, S, T, box, gp, rp, cell_start,
-                                                                             skey, nbr, nbr_cnt, acc, active, stats);
+                        k_sweep_work<2><<<grid, kSweepThreads, 0, stream>>>(cls, rank, S, box, gp, rp, cell_start, skey, bstart,
+                                                                            work, nbr, nbr_cnt, acc, active, stats);
                     else
-                        k_sweep_cells<3><<<grid, kSweepThreads, 0, stream>>>(sbc, cls, S, T, box, gp, rp, cell_start,
-                                                                             skey, nbr, nbr_cnt, acc, active, stats);
+                        k_sweep_work<3><<<grid, kSweepThreads, 0, stream>>>(cls, rank, S, box, gp, rp, cell_start, skey, bstart,
+                                                                            work, nbr, nbr_cnt, acc, active, stats);
                 }
-            launched(nsbc * hg.ncls);
+            }
+            launched(hg.ncls * kRanks);
         }
         if (with_stats) {
             FamScope fs(this, 3);
@@ -424,6 +454,8 @@ struct srm_b200_ctx {
                 launched();
             }
         }
+        // the sweep updated the sorted state in place: it is the round's output
+        swap_state(T, S);
     }
 
     srm_b200_round_stats read_stats(bool with_candidates) {
@@ -440,10 +472,10 @@ struct srm_b200_ctx {
         return o;
     }
 
-    // fixed-order reductions over T.r: {sum of measures, max radius}
+    // fixed-order reductions over the radii of T: {sum of measures, max radius}
     void reduce(const State& T, double* sum_measure, double* max_r) {
-        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, T.r, red_part_sum, red_part_max);
-        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, T.r, red_part_sum, red_part_max);
+        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, T.rec, red_part_sum, red_part_max);
+        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, T.rec, red_part_sum, red_part_max);
         k_reduce_final<<<1, 256, 0, stream>>>(red_part_sum, red_part_max, red_out);
         launched(2);
         SRM_CUDA(cudaMemcpyAsync(h_red, red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -468,7 +500,7 @@ struct srm_b200_ctx {
     }
 
     void scale_radius(State& T, double factor) {
-        k_scale_radius<<<blocks_for(n, 256), 256, 0, stream>>>(n, T.r, factor);
+        k_scale_radius<<<blocks_for(n, 256), 256, 0, stream>>>(n, T.rec, factor);
         launched();
     }
 };
@@ -575,17 +607,19 @@ int srm_b200_upload(srm_b200_ctx* c, int64_t n, const double* pos, const double*
         if (n > 0 && (!pos || !radius)) throw Invalid{"upload: null pointer"};
         c->n = n;
         if (n == 0) return SRM_B200_OK;
-        // stage through Q's buffers (scratch outside a generate call)
-        double* dpos = c->xblock[1];
+        // stage through the sorted state's buffers (scratch outside a round):
+        // positions at [0, dim n), radii at [3 cap, 3 cap + n) of S.rec viewed as doubles
+        double* dpos = reinterpret_cast<double*>(c->S.rec);
+        double* drad = dpos + 3 * c->cap;
         SRM_CUDA(cudaMemcpyAsync(dpos, pos, sizeof(double) * n * c->dim, cudaMemcpyHostToDevice, c->stream));
-        SRM_CUDA(cudaMemcpyAsync(c->Q.r, radius, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        SRM_CUDA(cudaMemcpyAsync(drad, radius, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         int32_t* did = nullptr;
         if (id) {
-            SRM_CUDA(cudaMemcpyAsync(c->Q.id, id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-            did = c->Q.id;
+            SRM_CUDA(cudaMemcpyAsync(c->S.id, id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+            did = c->S.id;
         }
-        if (c->dim == 2) k_unpack_soa<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, dpos, c->Q.r, did, c->P);
-        else k_unpack_soa<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, dpos, c->Q.r, did, c->P);
+        if (c->dim == 2) k_unpack_soa<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, dpos, drad, did, c->P);
+        else k_unpack_soa<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, dpos, drad, did, c->P);
         c->launched();
         c->sync();
         return SRM_B200_OK;
@@ -596,12 +630,13 @@ int srm_b200_download(srm_b200_ctx* c, double* pos, double* radius, int32_t* id)
     return guarded(c, [&]() -> int {
         const int64_t n = c->n;
         if (n == 0) return SRM_B200_OK;
-        double* dpos = c->xblock[2];
-        if (c->dim == 2) k_pack_soa<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, dpos, c->S.r, c->S.id);
-        else k_pack_soa<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, dpos, c->S.r, c->S.id);
+        double* dpos = reinterpret_cast<double*>(c->S.rec);
+        double* drad = dpos + 3 * c->cap;
+        if (c->dim == 2) k_pack_soa<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, dpos, drad, c->S.id);
+        else k_pack_soa<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, dpos, drad, c->S.id);
         c->launched();
         if (pos) SRM_CUDA(cudaMemcpyAsync(pos, dpos, sizeof(double) * n * c->dim, cudaMemcpyDeviceToHost, c->stream));
-        if (radius) SRM_CUDA(cudaMemcpyAsync(radius, c->S.r, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        if (radius) SRM_CUDA(cudaMemcpyAsync(radius, drad, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         if (id) SRM_CUDA(cudaMemcpyAsync(id, c->S.id, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
         c->sync();
         return SRM_B200_OK;
@@ -690,7 +725,7 @@ int srm_b200_grid_build(srm_b200_ctx* c, double cell_size, uint32_t* keys_out, i
             }
             if (order_out)
                 SRM_CUDA(cudaMemcpyAsync(order_out, c->S.slot, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
-            c->copy_state(c->S, c->P);  // keep the state physically sorted
+            c->swap_state(c->S, c->P);  // keep the state physically sorted
         } else {
             SRM_CUDA(cudaMemsetAsync(c->cell_start, 0, sizeof(int64_t) * (g.ncells + 1), c->stream));
         }
@@ -812,7 +847,7 @@ int srm_b200_reorder_by_locality(srm_b200_ctx* c, double cell_size, int32_t* rem
         SRM_CUDA(cudaMemcpyAsync(c->Q.slot, c->S.slot, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
         k_assign_slots<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, remap_dev, c->Q.slot);
         c->launched();
-        c->copy_state(c->S, c->P);
+        c->swap_state(c->S, c->P);
         if (remap_out) SRM_CUDA(cudaMemcpyAsync(remap_out, remap_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
         c->sync();
         return SRM_B200_OK;
@@ -889,7 +924,7 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
                 }
             }
             if (success) {
-                c->copy_state(c->Q, c->P);
+                c->swap_state(c->Q, c->P);  // commit (Q is rebuilt from P next iteration)
                 f = c->volume_fraction(c->P);
                 ++accepted_iters;
                 if (p.reorder_period > 0 && ++accepted_since_reorder >= p.reorder_period) {
@@ -899,7 +934,7 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
                     SRM_CUDA(cudaMemcpyAsync(c->Q.slot, c->S.slot, sizeof(int32_t) * c->n, cudaMemcpyDeviceToDevice, c->stream));
                     k_assign_slots<<<blocks_for(c->n, 256), 256, 0, c->stream>>>(c->n, c->S, nullptr, c->Q.slot);
                     c->launched();
-                    c->copy_state(c->S, c->P);
+                    c->swap_state(c->S, c->P);
                 }
             } else {
                 // shake: n_k sweeps on the pre-swell state with the same grid (engine.hpp:244-249)
@@ -976,17 +1011,6 @@ int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
         info[3] = c->hg.near_s[0];
         info[4] = c->hg.col_m[0];
         info[5] = c->hg.ncells;
-        int64_t nsbc = 1;
-        for (int a = 0; a < 3; ++a) nsbc *= c->hg.nsb[a] >= 2 ? 2 : 1;
-        info[6] = nsbc;
-        info[7] = c->hg.nsb[0];
-        return SRM_B200_OK;
-    });
-}
-
-int srm_b200_set_superblock(srm_b200_ctx* c, int w0) {
-    return guarded(c, [&]() -> int {
-        c->sb_w0 = w0 > 0 ? w0 : 0;
         return SRM_B200_OK;
     });
 }

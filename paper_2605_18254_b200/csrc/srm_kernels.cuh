@@ -4,7 +4,8 @@
 // is, on the device:
 //   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
 //   near lists     k_near_lists (round-start neighbours within the trial reach)
-//   migrate        k_sweep_cells, one launch per (superblock colour, colour class)
+//   near lists     k_near_lists (+ the (colour class, rank) work lists of the sweep)
+//   migrate        k_sweep_work, one launch per (colour class, rank in cell)
 //   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
 // All kernels read the grid / round parameters from device memory so that the same
 // launches can be replayed from a CUDA graph.  DESIGN.md §2-§4 has the data layout
@@ -35,7 +36,7 @@ struct GridParams {
     // fp32 prefilter (near_candidates): margin above the fp32 rounding of coordinates
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
-    int32_t nsb[3];     // superblocks per axis (even, or 1), DESIGN.md §3.1
+    int32_t nrank;      // ranks in cell with their own sweep step (kRanks)
 };
 
 struct RoundParams {
@@ -44,15 +45,21 @@ struct RoundParams {
     RngKey key;
 };
 
-// Per-particle SoA record set.  x[a] for a < D.
+// Per-particle state: one 32-byte record (x, y, z, r) per particle (z = 0 in 2D) -- a
+// single sector per gather / neighbour read -- plus the reference id and storage slot.
 struct State {
-    double* x[3];
-    double* r;
+    double4* rec;
     int32_t* id;
     int32_t* slot;
-    float4* xf;  // sorted fp32 copy (x, y, z, r) for prefilters; only in the sorted state S
-    double4* lv; // live record (x, y, z, r) during the sweep, one 32-byte sector; only in S
+    float4* xf;  // sorted fp32 copy (x, y, z, r) for the near-list prefilter; only in S
 };
+
+template <int D>
+__device__ __forceinline__ void rec_pos(const double4 v, double* p) {
+    p[0] = v.x;
+    if (D > 1) p[D > 1 ? 1 : 0] = v.y;
+    if (D > 2) p[D > 2 ? 2 : 0] = v.z;
+}
 
 struct StatsDev {
     unsigned long long overlap_pairs;
@@ -88,8 +95,7 @@ __global__ void k_keys(int64_t n, State T, const GridParams* __restrict__ gp,
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double p[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) p[a] = T.x[a][i];
+        rec_pos<D>(T.rec[i], p);
         const uint32_t k = cell_of<D>(g, p);
         key[i] = k;
         atomicAdd(&count[k], 1u);
@@ -250,18 +256,11 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ perm, const uint
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t src = perm[q];
-        float f[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-            const double v = T.x[a][src];
-            S.x[a][q] = v;
-            f[a] = static_cast<float>(v);
-        }
-        const double rr = T.r[src];
-        S.r[q] = rr;
-        f[3] = static_cast<float>(rr);
-        if (S.xf) S.xf[q] = make_float4(f[0], f[1], f[2], f[3]);
-        if (S.lv) S.lv[q] = make_double4(S.x[0][q], D > 1 ? S.x[1][q] : 0.0, D > 2 ? S.x[2][q] : 0.0, rr);
+        const double4 v = T.rec[src];
+        S.rec[q] = v;
+        if (S.xf)
+            S.xf[q] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y), static_cast<float>(v.z),
+                                  static_cast<float>(v.w));
         S.id[q] = T.id[src];
         S.slot[q] = T.slot[src];
         skey[q] = key[src];
@@ -311,8 +310,7 @@ __device__ __forceinline__ void for_near_ranges(const GridParams& g, const int64
 
 template <int D>
 __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) p[a] = S.x[a][i];
+    rec_pos<D>(S.rec[i], p);
 }
 
 // ---------------------------------------------------------------------------------
@@ -320,18 +318,20 @@ __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
 //
 // The reference's migrate (engine.hpp:89-107) visits particles in storage order; each
 // gets <= n_l trials from its pre-sweep position and keeps the first one that clears the
-// LIVE positions of all others.  Here the visiting order is (superblock colour,
-// superblock, colour class, cell, slot): cells are coloured so that two cells of one
-// class are farther apart than any trial can reach (GridParams::col_*), and superblocks
-// of one colour are a whole superblock apart (GridParams::nsb), hence one superblock
-// colour is one launch with a CTA per superblock and a thread per cell of a class,
-// particles of a cell sequentially in slot order; the result is identical to the
-// sequential sweep in that order (oracle/srm_oracle.c orc_sweep_round).
+// LIVE positions of all others.  Here the visiting order is (colour class, cell, slot):
+// cells are coloured so that two cells of one class are farther apart than any trial
+// can reach (GridParams::col_*), hence the rank-r particles of the cells of one class
+// are independent: one launch per (class, rank), a thread per particle, and the result
+// is identical to the sequential sweep in that order (oracle/srm_oracle.c
+// orc_sweep_round).
 //
-// Live positions: S.lv[j] holds (x, r) of j -- its round-start position, overwritten by
+// Live positions: S.rec[j] holds (x, r) of j -- its round-start position, overwritten by
 // its accepted trial when j moves; one 32-byte sector per neighbour read.
 
 constexpr int kNearLocal = 16;  // near candidates kept per particle; more -> rescan per trial
+constexpr int kRanks = 3;       // sweep steps per class: ranks 0, 1 and 2+ (the rank-2 thread
+                                // sweeps the rest of its cell in slot order)
+constexpr int kBucketSmem = 8192;  // (class, rank) buckets aggregated in shared memory
 
 // Near candidates of sorted particle q: every j whose round-start distance is within
 // ri + rj + 2 c_m (every j a trial of q can touch while j sits within c_m of its start).
@@ -408,6 +408,24 @@ __device__ __forceinline__ void near_candidates(const GridParams& g, const int64
 
 constexpr uint8_t kNearOverflow = 255;
 
+// colour class of a cell (DESIGN.md §3.1)
+__device__ __forceinline__ int colour1(int x, int m, int n) {
+    const int body = m * (n / m);
+    return x < body ? x % m : m + (x - body);
+}
+
+template <int D>
+__device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
+    const int cx = static_cast<int>(key % static_cast<uint32_t>(g.dims[0]));
+    const uint32_t rest = key / static_cast<uint32_t>(g.dims[0]);
+    const int cy = static_cast<int>(rest % static_cast<uint32_t>(g.dims[1]));
+    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(g.dims[1])) : 0;
+    int k = colour1(cx, g.col_m[0], g.dims[0]);
+    k += g.col_n[0] * colour1(cy, g.col_m[1], g.dims[1]);
+    if (D == 3) k += g.col_n[0] * g.col_n[1] * colour1(cz, g.col_m[2], g.dims[2]);
+    return k;
+}
+
 // Near lists of every particle, one parallel pass before the sweep: nbr[q*kNearLocal..]
 // and nbr_cnt[q] (kNearOverflow: more than kNearLocal, the sweep rescans the grid).
 template <int D>
@@ -428,17 +446,143 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
     }
 }
 
+// Work lists of the sweep: every particle of rank r < kRanks in its cell goes to bucket
+// (colour class c, r) = c * kRanks + r; buckets are laid out back to back (bstart, an
+// exclusive scan of the counts).  The order inside a bucket does not matter (cells of
+// one class never interact).  count -> scan -> scatter, CTA-aggregated atomics.
+constexpr int kWorkBlock = 1024;
+constexpr int kWorkPer = 8;  // particles per thread: 8192 per CTA
+
 template <int D>
-__device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const State& T, const Box& box,
+__device__ __forceinline__ int bucket_of(const GridParams& g, const int64_t* __restrict__ cs, uint32_t key,
+                                         int64_t q) {
+    const int64_t rank = q - cs[key];
+    if (rank >= kRanks) return -1;
+    return class_of_key<D>(g, key) * kRanks + static_cast<int>(rank);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWorkBlock) k_work_count(int64_t n, const GridParams* __restrict__ gp,
+                                                           const int64_t* __restrict__ cs,
+                                                           const uint32_t* __restrict__ skey,
+                                                           uint32_t* __restrict__ bcount) {
+    extern __shared__ uint32_t hist[];
+    const GridParams& g = *gp;
+    const int nb = g.ncls * kRanks;
+    const bool local = nb <= kBucketSmem;
+    if (local)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
+    for (int k = 0; k < kWorkPer; ++k) {
+        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
+        if (q >= n) break;
+        const int b = bucket_of<D>(g, cs, skey[q], q);
+        if (b < 0) continue;
+        if (local) atomicAdd(&hist[b], 1u);
+        else atomicAdd(&bcount[b], 1u);
+    }
+    __syncthreads();
+    if (local)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+            if (hist[b]) atomicAdd(&bcount[b], hist[b]);
+}
+
+// single CTA: exclusive scan of the bucket counts; cursors start at the bucket starts
+__global__ void k_work_scan(const GridParams* __restrict__ gp, uint32_t* __restrict__ bcount,
+                            uint32_t* __restrict__ bstart, uint32_t* __restrict__ cursor) {
+    const int nb = gp->ncls * kRanks;
+    __shared__ uint32_t carry;
+    __shared__ uint32_t wsum[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t v = b < nb ? bcount[b] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            wsum[lane] = wi - w;
+        }
+        __syncthreads();
+        const uint32_t ex = carry + wsum[wid] + incl - v;
+        if (b < nb) {
+            bstart[b] = ex;
+            cursor[b] = ex;
+            bcount[b] = 0u;  // ready for the next round's count
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bstart[nb] = carry;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const GridParams* __restrict__ gp,
+                                                             const int64_t* __restrict__ cs,
+                                                             const uint32_t* __restrict__ skey,
+                                                             uint32_t* __restrict__ cursor, int32_t* __restrict__ work) {
+    extern __shared__ uint32_t hist[];  // [nb] counts, then [nb] CTA bases
+    const GridParams& g = *gp;
+    const int nb = g.ncls * kRanks;
+    const bool local = nb <= kBucketSmem;
+    uint32_t* base = hist + (local ? nb : 0);
+    if (local)
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
+    int myb[kWorkPer];
+    uint32_t myl[kWorkPer];
+#pragma unroll
+    for (int k = 0; k < kWorkPer; ++k) {
+        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
+        myb[k] = -1;
+        if (q >= n) continue;
+        myb[k] = bucket_of<D>(g, cs, skey[q], q);
+        if (myb[k] < 0) continue;
+        if (local) myl[k] = atomicAdd(&hist[myb[k]], 1u);
+        else work[atomicAdd(&cursor[myb[k]], 1u)] = static_cast<int32_t>(q);
+    }
+    if (!local) return;
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (hist[b]) base[b] = atomicAdd(&cursor[b], hist[b]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kWorkPer; ++k) {
+        if (myb[k] < 0) continue;
+        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
+        work[base[myb[k]] + myl[k]] = static_cast<int32_t>(q);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const Box& box,
                                                const GridParams& g, const RoundParams& rp,
                                                const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                const int32_t* __restrict__ nbr, const uint8_t* __restrict__ nbr_cnt,
                                                uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                StatsDev* stats) {
     const int nn = nbr_cnt[q];
+    const double4 me = S.rec[q];  // round-start record; q is visited once
     double xi[D];
-    load_pos<D>(S, q, xi);
-    const double ri = S.r[q];
+    rec_pos<D>(me, xi);
+    const double ri = me.w;
     const int32_t sl = S.slot[q];
     double p[D];
     int accepted = -1;
@@ -464,7 +608,7 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
                     double4 v[kBatch];
 #pragma unroll
                     for (int u = 0; u < kBatch; ++u)
-                        if (t0 + u < nn) v[u] = S.lv[nb[t0 + u]];
+                        if (t0 + u < nn) v[u] = S.rec[nb[t0 + u]];
 #pragma unroll
                     for (int u = 0; u < kBatch; ++u) {
                         if (t0 + u < nn) {
@@ -483,27 +627,18 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
             bool ok = true;
             near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
                 if (!ok || S.id[j] == idq) return;
-                const double4 v = S.lv[j];
+                const double4 v = S.rec[j];
                 const double xl[3] = {v.x, v.y, v.z};
                 if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
             });
             if (ok) accepted = l;
         }
     }
-    if (accepted >= 0) S.lv[q] = make_double4(p[0], D > 1 ? p[1] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, ri);
-#pragma unroll
-    for (int a = 0; a < D; ++a) T.x[a][q] = accepted >= 0 ? p[a] : xi[a];
-    T.r[q] = ri;
-    T.id[q] = S.id[q];
-    T.slot[q] = sl;
     acc[q] = accepted >= 0 ? static_cast<uint8_t>(accepted) : kNotAccepted;
-    if (accepted < 0) active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
-}
-
-// colour class of a cell (DESIGN.md §3.1)
-__device__ __forceinline__ int colour1(int x, int m, int n) {
-    const int body = m * (n / m);
-    return x < body ? x % m : m + (x - body);
+    if (accepted >= 0)  // publish the live position (in place: the sorted state is the round's output)
+        S.rec[q] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, ri);
+    else
+        active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
 }
 
 #ifndef SRM_SWEEP_THREADS
@@ -511,82 +646,36 @@ __device__ __forceinline__ int colour1(int x, int m, int n) {
 #endif
 constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
-// Cells of colour class cls in the superblock (lo, hi) form a lattice per axis:
-// first + stride * i, i < cnt (colour1 inverted on [lo, hi)).
-__device__ __forceinline__ void class_lattice(const GridParams& g, int cls, const int* lo, const int* hi, int* first,
-                                              int* stride, int* cnt) {
-    int rem = cls;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const int m = g.col_m[a], n = g.dims[a];
-        const int cv = rem % g.col_n[a];
-        rem /= g.col_n[a];
-        const int body = m * (n / m);
-        if (cv < m) {
-            const int f = lo[a] + ((cv - lo[a] % m) + m) % m;
-            const int b = min(hi[a], body);
-            first[a] = f;
-            stride[a] = m;
-            cnt[a] = f < b ? (b - f + m - 1) / m : 0;
-        } else {
-            const int x = body + (cv - m);
-            first[a] = x;
-            stride[a] = 1;
-            cnt[a] = (x >= lo[a] && x < hi[a]) ? 1 : 0;
-        }
-    }
-}
-
-// Superblock sb of colour sbc: along axis a its block index is colour bit + 2 * j_a
-// (every block when the axis is not split); block k covers [ceil(k n / nsb), ceil((k+1) n / nsb)),
-// i.e. x lies in block floor(x nsb / n) (oracle/srm_oracle.c orc_superblocks).
-__device__ __forceinline__ void superblock_range(const GridParams& g, int sbc, int64_t sb, int* lo, int* hi) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const int nsb = g.nsb[a], n = g.dims[a];
-        int k = 0;
-        if (nsb >= 2) {
-            const int per = nsb / 2;
-            k = ((sbc >> a) & 1) + 2 * static_cast<int>(sb % per);
-            sb /= per;
-        }
-        lo[a] = static_cast<int>((static_cast<int64_t>(k) * n + nsb - 1) / nsb);
-        hi[a] = static_cast<int>((static_cast<int64_t>(k + 1) * n + nsb - 1) / nsb);
-    }
-}
-
-// One step of the sweep: colour class cls of the superblocks of colour sbc.  A thread
-// per cell (blockIdx.y = superblock), the particles of a cell in slot order.  Cells of
-// one class are farther apart than any trial can reach and superblocks of one colour a
-// whole superblock apart, so all threads of the launch are independent and the launch
-// sequence (sbc, cls) reproduces the sequential sweep of orc_sweep_round bit for bit.
+// One (colour class, rank) step of the sweep: a thread per particle of the bucket.  The
+// bucket holds the rank-`rank` particle of every cell of the class that has one (in no
+// particular order: cells of one class never interact); the last rank's thread also
+// sweeps the rest of its (crowded) cell, in slot order.  The launch sequence over
+// (class, rank) reproduces the sequential sweep of orc_sweep_round bit for bit.
 template <int D>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_cells(int sbc, int cls, State S, State T, Box box,
-                                                               const GridParams* __restrict__ gp,
-                                                               const RoundParams* __restrict__ rpp,
-                                                               const int64_t* __restrict__ cs,
-                                                               const uint32_t* __restrict__ skey,
-                                                               const int32_t* __restrict__ nbr,
-                                                               const uint8_t* __restrict__ nbr_cnt,
-                                                               uint8_t* __restrict__ acc, int32_t* __restrict__ active,
-                                                               StatsDev* stats) {
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_work(int cls, int rank, State S, Box box,
+                                                              const GridParams* __restrict__ gp,
+                                                              const RoundParams* __restrict__ rpp,
+                                                              const int64_t* __restrict__ cs,
+                                                              const uint32_t* __restrict__ skey,
+                                                              const uint32_t* __restrict__ bstart,
+                                                              const int32_t* __restrict__ work,
+                                                              const int32_t* __restrict__ nbr,
+                                                              const uint8_t* __restrict__ nbr_cnt,
+                                                              uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                                              StatsDev* stats) {
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
-    int lo[3], hi[3], first[3], stride[3], cnt[3];
-    superblock_range(g, sbc, blockIdx.y, lo, hi);
-    class_lattice(g, cls, lo, hi, first, stride, cnt);
-    const int cxy = cnt[0] * cnt[1];
-    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (t >= static_cast<int64_t>(cxy) * cnt[2]) return;
-    const int iz = static_cast<int>(t / cxy), r2 = static_cast<int>(t - static_cast<int64_t>(iz) * cxy);
-    const int iy = r2 / cnt[0], ix = r2 - iy * cnt[0];
-    const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
-                             g.dims[0] +
-                         first[0] + stride[0] * ix;
+    const int64_t lo = bstart[cls * kRanks + rank];
+    const int64_t cnt = bstart[cls * kRanks + rank + 1] - lo;
+    const int32_t* list = work + lo;
     const RoundParams rp = *rpp;
-    const int64_t e = cs[cell + 1];
-    for (int64_t q = cs[cell]; q < e; ++q)
-        sweep_particle<D>(q, S, T, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < cnt;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t q0 = list[t];
+        const int64_t e = rank == kRanks - 1 ? cs[skey[q0] + 1] : q0 + 1;
+        for (int64_t q = q0; q < e; ++q)
+            sweep_particle<D>(q, S, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
+    }
 }
 
 // Overlap reduction after the sweep.  A particle that accepted a trial cleared every
@@ -606,15 +695,17 @@ __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const Gri
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = active[k];
         double xi[D];
-        load_pos<D>(S, i, xi);
-        const double ri = S.r[i];
+        const double4 vi = S.rec[i];
+        rec_pos<D>(vi, xi);
+        const double ri = vi.w;
         const int32_t idi = S.id[i];
         for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
             for (int64_t j = b; j < e; ++j) {
                 if (j <= i || acc[j] != kNotAccepted || S.id[j] == idi) continue;
                 double xj[D];
-                load_pos<D>(S, j, xj);
-                const double rr = ri + S.r[j];
+                const double4 vj = S.rec[j];
+                rec_pos<D>(vj, xj);
+                const double rr = ri + vj.w;
                 const double d2 = dist2<D>(box, xi, xj);
                 if (d2 <= rr * rr) {
                     ++pairs;
@@ -669,15 +760,17 @@ __global__ void __launch_bounds__(256) k_overlap_full(int64_t n, State S, Box bo
     if (i < n) {
         const GridParams& g = *gp;
         double xi[D];
-        load_pos<D>(S, i, xi);
-        const double ri = S.r[i];
+        const double4 vi = S.rec[i];
+        rec_pos<D>(vi, xi);
+        const double ri = vi.w;
         const int32_t idi = S.id[i];
         for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
             for (int64_t j = b; j < e; ++j) {
                 if (j <= i || S.id[j] == idi) continue;
                 double xj[D];
-                load_pos<D>(S, j, xj);
-                const double rr = ri + S.r[j];
+                const double4 vj = S.rec[j];
+                rec_pos<D>(vj, xj);
+                const double rr = ri + vj.w;
                 const double d2 = dist2<D>(box, xi, xj);
                 if (d2 <= rr * rr) {
                     ++pairs;
@@ -719,9 +812,10 @@ __global__ void k_unpack_records(int64_t n, const char* __restrict__ rec, int64_
          i += (int64_t)gridDim.x * blockDim.x) {
         const char* b = rec + i * stride;
         T.id[i] = *reinterpret_cast<const int32_t*>(b + off_id);
+        double p[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-        for (int a = 0; a < D; ++a) T.x[a][i] = *reinterpret_cast<const double*>(b + off_pos + 8 * a);
-        T.r[i] = *reinterpret_cast<const double*>(b + off_r);
+        for (int a = 0; a < D; ++a) p[a] = *reinterpret_cast<const double*>(b + off_pos + 8 * a);
+        T.rec[i] = make_double4(p[0], p[1], p[2], *reinterpret_cast<const double*>(b + off_r));
         T.slot[i] = static_cast<int32_t>(i);
     }
 }
@@ -733,9 +827,11 @@ __global__ void k_pack_records(int64_t n, State T, char* __restrict__ rec, int64
          i += (int64_t)gridDim.x * blockDim.x) {
         char* b = rec + (int64_t)T.slot[i] * stride;
         *reinterpret_cast<int32_t*>(b + off_id) = T.id[i];
+        const double4 v = T.rec[i];
+        const double p[3] = {v.x, v.y, v.z};
 #pragma unroll
-        for (int a = 0; a < D; ++a) *reinterpret_cast<double*>(b + off_pos + 8 * a) = T.x[a][i];
-        *reinterpret_cast<double*>(b + off_r) = T.r[i];
+        for (int a = 0; a < D; ++a) *reinterpret_cast<double*>(b + off_pos + 8 * a) = p[a];
+        *reinterpret_cast<double*>(b + off_r) = v.w;
     }
 }
 
@@ -745,9 +841,10 @@ __global__ void k_unpack_soa(int64_t n, const double* __restrict__ pos, const do
                              const int32_t* __restrict__ id, State T) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
+        double p[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-        for (int a = 0; a < D; ++a) T.x[a][i] = pos[i * D + a];
-        T.r[i] = r[i];
+        for (int a = 0; a < D; ++a) p[a] = pos[i * D + a];
+        T.rec[i] = make_double4(p[0], p[1], p[2], r[i]);
         T.id[i] = id ? id[i] : static_cast<int32_t>(i);
         T.slot[i] = static_cast<int32_t>(i);
     }
@@ -759,26 +856,26 @@ __global__ void k_pack_soa(int64_t n, State T, double* __restrict__ pos, double*
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = T.slot[i];
+        const double4 v = T.rec[i];
+        const double p[3] = {v.x, v.y, v.z};
 #pragma unroll
-        for (int a = 0; a < D; ++a) pos[s * D + a] = T.x[a][i];
-        r[s] = T.r[i];
+        for (int a = 0; a < D; ++a) pos[s * D + a] = p[a];
+        r[s] = v.w;
         id[s] = T.id[i];
     }
 }
 
-__global__ void k_scale_radius(int64_t n, double* __restrict__ r, double factor) {
+__global__ void k_scale_radius(int64_t n, double4* __restrict__ rec, double factor) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        r[i] = r[i] * factor;  // engine.hpp:520 p.radius *= factor
+        rec[i].w = rec[i].w * factor;  // engine.hpp:520 p.radius *= factor
 }
 
 template <int D>
 __global__ void k_copy_state(int64_t n, State A, State B) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) B.x[a][i] = A.x[a][i];
-        B.r[i] = A.r[i];
+        B.rec[i] = A.rec[i];
         B.id[i] = A.id[i];
         B.slot[i] = A.slot[i];
     }
@@ -820,7 +917,7 @@ __device__ __forceinline__ double particle_measure(double r) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_reduce_partials(int64_t n, const double* __restrict__ r,
+__global__ void __launch_bounds__(256) k_reduce_partials(int64_t n, const double4* __restrict__ rec,
                                                          double* __restrict__ part_sum,
                                                          double* __restrict__ part_max) {
     __shared__ double ss[256], sm[256];
@@ -829,7 +926,7 @@ __global__ void __launch_bounds__(256) k_reduce_partials(int64_t n, const double
     const int64_t b1 = b0 + chunk < n ? b0 + chunk : n;
     double s = 0.0, m = 0.0;
     for (int64_t i = b0 + threadIdx.x; i < b1; i += 256) {
-        const double v = r[i];
+        const double v = rec[i].w;
         s = s + particle_measure<D>(v);
         m = v > m ? v : m;
     }

@@ -55,7 +55,7 @@ def orc():
         L.orc_propose.argtypes = [C.c_int, vp, vp, C.c_double, C.c_uint64, C.c_uint32, C.c_uint32,
                                   C.c_uint32, C.c_uint32, vp]
         L.orc_sweep_round.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_double, C.c_int,
-                                      C.c_uint64, C.c_uint32, C.c_uint32, C.c_int32, vp, vp, C.c_int]
+                                      C.c_uint64, C.c_uint32, C.c_uint32, vp, vp, C.c_int]
         L.orc_colouring.argtypes = [C.c_int, vp, vp, C.c_double, C.c_double, vp, vp]
         L.orc_overlap_stats.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, C.POINTER(RoundStats)]
         L.orc_candidate_pairs.restype = C.c_int64
@@ -131,16 +131,15 @@ def o_sort(keys, slot, ncells):
     return order, cs
 
 
-def o_round(dim, L, x0, r, ids, slot, cell_size, c_m, n_l, seed, round_id, iteration, brute=False, sb_w0=0):
-    """one round's coloured Gauss-Seidel migrate sweep (oracle/srm_oracle.c); sb_w0 is
-    the superblock width of the sweep schedule (0: none), as Context.set_superblock"""
+def o_round(dim, L, x0, r, ids, slot, cell_size, c_m, n_l, seed, round_id, iteration, brute=False):
+    """one round's coloured Gauss-Seidel migrate sweep (oracle/srm_oracle.c)"""
     x0 = arr(x0)
     n = len(r)
     xnew = np.zeros_like(x0)
     acc = np.zeros(n, np.uint8)
     orc().orc_sweep_round(dim, P(arr(L)), n, P(x0), P(arr(r)), P(arr(ids, np.int32)),
                           P(arr(slot, np.int32)), cell_size, c_m, n_l, seed, round_id, iteration,
-                          int(sb_w0), P(xnew), P(acc), int(brute))
+                          P(xnew), P(acc), int(brute))
     return xnew, acc
 
 

@@ -128,21 +128,16 @@ def test_overlap_stats_bit_exact(dim, n, rmin, rmax, seed):
     (2, 1500, 0.6, 1.0, 0.05, 4, 4),
     (3, 5000, 0.3, 1.0, 0.05, 1, 5),
 ])
-@pytest.mark.parametrize("sb_w0", [0, 3])
-def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed, sb_w0):
+def test_round_bit_exact_vs_oracle(dim, n, f, swell, cm_rel, n_l, seed):
     L, pos, r, ids = _rsa_state(dim, n, min(f, 0.45 if dim == 2 else 0.25), seed)
     r = r * (f / min(f, 0.45 if dim == 2 else 0.25)) ** (1 / dim) * swell
     c_m = cm_rel * r.max()
     cs = 2.5 * r.max() / swell + c_m
     key, round_id, it = 0x0123456789ABCDEF + seed, 3, 17
     with _ctx(L, pos, r, ids) as ctx:
-        ctx.set_superblock(sb_w0)
         st, acc = ctx.round(cs, c_m, n_l, key, round_id, it, with_candidates=True)
         pos_d, r_d, id_d = ctx.download()
-        info = ctx.last_round_info()
-    if sb_w0:
-        assert info["superblock_colours"] > 1  # the superblock schedule is exercised
-    xnew, acc_o = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, n_l, key, round_id, it, sb_w0=sb_w0)
+    xnew, acc_o = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, n_l, key, round_id, it)
     assert np.array_equal(acc, acc_o)
     assert np.array_equal(pos_d, xnew)
     assert np.array_equal(r_d, r) and np.array_equal(id_d, ids)

@@ -1,4 +1,4 @@
-"""The round semantics (coloured Gauss-Seidel sweep in superblock order)
+"""The round semantics (coloured Gauss-Seidel sweep)
 reproduce the reference's srm_generate statistically -- checked on the CPU with the
 oracle's generate loop (orc.o_generate) against the reference ensembles in
 tests/golden/e2e_*.npz, with the same tests the GPU end-to-end check applies."""

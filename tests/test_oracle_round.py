@@ -24,25 +24,22 @@ def _state(dim, n, f, seed, L=None):
 
 
 @pytest.mark.parametrize("dim,n,f", [(2, 400, 0.45), (3, 400, 0.3), (2, 300, 0.6)])
-@pytest.mark.parametrize("sb_w0", [0, 3])
-def test_cells_equal_brute(dim, n, f, sb_w0):
+def test_cells_equal_brute(dim, n, f):
     L, pos, r, ids = _state(dim, n, min(f, 0.5 if dim == 2 else 0.3), 3)
     r = r * (f / min(f, 0.5 if dim == 2 else 0.3)) ** (1 / dim)  # swell: some overlaps
     c_m = 0.2 * r[0]
     cs = 2.5 * r.max() + c_m
-    a = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, 8, 99, 2, 5, brute=False, sb_w0=sb_w0)
-    b = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, 8, 99, 2, 5, brute=True, sb_w0=sb_w0)
+    a = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, 8, 99, 2, 5, brute=False)
+    b = orc.o_round(dim, L, pos, r, ids, ids, cs, c_m, 8, 99, 2, 5, brute=True)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
 @pytest.mark.parametrize("dim,f,swell", [(2, 0.5, 1.02), (3, 0.3, 1.02), (2, 0.7, 1.0), (3, 0.35, 1.05)])
-@pytest.mark.parametrize("sb_w0", [0, 3])
-def test_round_never_creates_overlap(dim, f, swell, sb_w0):
+def test_round_never_creates_overlap(dim, f, swell):
     L, pos, r, ids = _state(dim, 600, min(f, 0.45 if dim == 2 else 0.3), 11)
     r = r * (f / min(f, 0.45 if dim == 2 else 0.3)) ** (1 / dim) * swell
     c_m = 0.1 * r[0]
-    xnew, acc = orc.o_round(dim, L, pos, r, ids, ids, 2.5 * r.max() / swell + c_m, c_m, 10, 1234, 0, 1,
-                            sb_w0=sb_w0)
+    xnew, acc = orc.o_round(dim, L, pos, r, ids, ids, 2.5 * r.max() / swell + c_m, c_m, 10, 1234, 0, 1)
     moved = acc != 255
     assert moved.sum() > 0
     # non-movers keep their exact bits, movers moved exactly one proposal

@@ -22,7 +22,6 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="particles (box scaled to keep the density)")
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--timing", action="store_true")
-    ap.add_argument("--sb", type=int, default=-1, help="superblock width (Context.set_superblock); -1 = default")
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
     n = args.n or cfg["n"]
@@ -31,8 +30,6 @@ def main():
     ctx, c_m, prep = bench.gpu_state(srm, cfg, 12345, 0, n=n, box=box)
     cs = 2.5 * ctx.max_bounding_radius() + c_m
     print("prep", prep, f"{time.time() - t0:.1f}s", flush=True)
-    if args.sb >= 0:
-        ctx.set_superblock(args.sb)
     if args.timing:
         ctx.timing_enable(True)
     import ctypes
