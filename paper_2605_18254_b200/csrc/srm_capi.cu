@@ -75,12 +75,14 @@ struct srm_b200_ctx {
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
     uint8_t* nbr_cnt = nullptr;
+    uint32_t* ncount = nullptr;  // pair-append counters of k_near_half
     int32_t* work = nullptr;     // (colour class, rank) work lists of the sweep, [cap]
     uint32_t* bcount = nullptr;  // bucket counts / starts / cursors, [ncls * kRanks + 1]
     uint32_t* bstart = nullptr;
     uint32_t* bcursor = nullptr;
     int64_t bucket_cap = 0;
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
+    int near_mode = std::getenv("SRM_B200_NEAR_THREAD") ? 1 : 0;  // 0: warp per cell, 1: thread per particle
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -205,6 +207,7 @@ struct srm_b200_ctx {
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearLocal);
         nbr_cnt = dalloc<uint8_t>(cap);
+        ncount = dalloc<uint32_t>(cap);
         work = dalloc<int32_t>(cap);
         const int work_smem = 2 * kBucketSmem * 4;
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
@@ -227,7 +230,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(S.xf); cudaFree(work); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor);
+        cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(ncount); cudaFree(S.xf); cudaFree(work); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -293,6 +296,14 @@ struct srm_b200_ctx {
             g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
         }
         g.nrank = kRanks;
+        for (int a = 0; a < 3; ++a) {
+            g.fd_dims[a] = make_fastdiv(static_cast<uint32_t>(g.dims[a]));
+            g.fd_m[a] = make_fastdiv(static_cast<uint32_t>(g.col_m[a]));
+            g.col_body[a] = g.col_m[a] * (g.dims[a] / g.col_m[a]);
+            for (const FastDiv& f : {g.fd_dims[a], g.fd_m[a]})  // cheap guard of the magic numbers
+                for (uint32_t v : {0u, 1u, f.d - 1, f.d, f.d + 1, 2 * f.d + 1, 0x7fffffffu, 0xfffffffeu, 0xffffffffu})
+                    if (fdiv(v, f) != v / f.d) throw std::logic_error("fast division self-check failed");
+        }
         // fp32 prefilter: coordinates live in [0, L); 8 ulp of the largest box length
         // bounds the rounding of any coordinate difference and of the radii sums
         double lmax = 0.0;
@@ -419,9 +430,19 @@ struct srm_b200_ctx {
             else
                 k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
             const int nb = blocks_for(n, 256);
-            if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
-            else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
-            launched(4);
+            bool half = near_mode == 0;
+            for (int a = 0; a < dim; ++a) half = half && hg.near_s[a] >= 0;
+            if (half) {  // pairs once, appended to both lists
+                SRM_CUDA(cudaMemsetAsync(ncount, 0, sizeof(uint32_t) * n, stream));
+                if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, ncount);
+                else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, ncount);
+                k_near_counts<<<nb, 256, 0, stream>>>(n, ncount, nbr_cnt);
+                launched(5);
+            } else {
+                if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
+                else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
+                launched(4);
+            }
         }
         {
             FamScope fs(this, 1);

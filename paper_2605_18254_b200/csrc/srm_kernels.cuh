@@ -22,6 +22,28 @@ namespace srmb {
 
 constexpr int kScanTile = 4096;  // cells per scan tile (1024 threads x 4)
 
+// Division by a grid constant d >= 1 as a multiply-high (Granlund & Montgomery 1994,
+// 33-bit multiplier): q = (umulhi(n, m) + n) >> l, exact for every 32-bit n.
+struct FastDiv {
+    uint32_t d, m, l;
+};
+
+__host__ __device__ inline uint32_t fdiv(uint32_t n, const FastDiv& f) {
+#ifdef __CUDA_ARCH__
+    const uint64_t hi = __umulhi(n, f.m);
+#else
+    const uint64_t hi = (static_cast<uint64_t>(n) * f.m) >> 32;
+#endif
+    return static_cast<uint32_t>((hi + n) >> f.l);
+}
+
+inline FastDiv make_fastdiv(uint32_t d) {
+    uint32_t l = 0;
+    while ((uint64_t{1} << l) < d) ++l;
+    const uint64_t m = ((uint64_t{1} << 32) * ((uint64_t{1} << l) - d)) / d + 1;
+    return FastDiv{d, static_cast<uint32_t>(m), l};
+}
+
 struct GridParams {
     int32_t dims[3];
     double edge[3];
@@ -37,7 +59,25 @@ struct GridParams {
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
     int32_t nrank;      // ranks in cell with their own sweep step (kRanks)
+    FastDiv fd_dims[3];  // division by dims[a]
+    FastDiv fd_m[3];     // division by col_m[a]
+    int32_t col_body[3]; // col_m * floor(dims / col_m): cells coloured x mod m
 };
+
+// cell coordinates of a flat key (x fastest, cell_grid.hpp:326-336)
+template <int D>
+__device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, int* c) {
+    const uint32_t r1 = fdiv(key, g.fd_dims[0]);
+    c[0] = static_cast<int>(key - r1 * static_cast<uint32_t>(g.dims[0]));
+    if (D == 3) {
+        const uint32_t r2 = fdiv(r1, g.fd_dims[1]);
+        c[1] = static_cast<int>(r1 - r2 * static_cast<uint32_t>(g.dims[1]));
+        c[2] = static_cast<int>(r2);
+    } else {
+        c[1] = static_cast<int>(r1);
+        c[2] = 0;
+    }
+}
 
 struct RoundParams {
     double c_m;
@@ -274,10 +314,9 @@ template <int D, typename F>
 __device__ __forceinline__ void for_near_ranges(const GridParams& g, const int64_t* __restrict__ cs,
                                                 uint32_t k, const int32_t* s, F&& f) {
     const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
-    const int cx = static_cast<int>(k % static_cast<uint32_t>(dx));
-    const uint32_t rest = k / static_cast<uint32_t>(dx);
-    const int cy = static_cast<int>(rest % static_cast<uint32_t>(dy));
-    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(dy)) : 0;
+    int cc_[3];
+    decode_key<D>(g, k, cc_);
+    const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
     const bool fy = s[1] < 0, fz = D == 3 ? s[2] < 0 : true;
     const int ylo = fy ? 0 : cy - s[1], yhi = fy ? dy - 1 : cy + s[1];
     const int zlo = D == 3 ? (fz ? 0 : cz - s[2]) : 0, zhi = D == 3 ? (fz ? dz - 1 : cz + s[2]) : 0;
@@ -343,10 +382,9 @@ __device__ __forceinline__ void near_candidates(const GridParams& g, const int64
                                                 const float4* __restrict__ xf, int64_t q, uint32_t key, F&& visit) {
     const float4 me = xf[q];
     const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
-    const int cx = static_cast<int>(key % static_cast<uint32_t>(dx));
-    const uint32_t rest = key / static_cast<uint32_t>(dx);
-    const int cy = static_cast<int>(rest % static_cast<uint32_t>(dy));
-    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(dy)) : 0;
+    int cc_[3];
+    decode_key<D>(g, key, cc_);
+    const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
     const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
     const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
     const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
@@ -409,20 +447,20 @@ __device__ __forceinline__ void near_candidates(const GridParams& g, const int64
 constexpr uint8_t kNearOverflow = 255;
 
 // colour class of a cell
-__device__ __forceinline__ int colour1(int x, int m, int n) {
-    const int body = m * (n / m);
-    return x < body ? x % m : m + (x - body);
+__device__ __forceinline__ int colour1(const GridParams& g, int a, int x) {
+    const int m = g.col_m[a];
+    if (x >= g.col_body[a]) return m + (x - g.col_body[a]);
+    return x - static_cast<int>(fdiv(static_cast<uint32_t>(x), g.fd_m[a])) * m;
 }
 
 template <int D>
 __device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
-    const int cx = static_cast<int>(key % static_cast<uint32_t>(g.dims[0]));
-    const uint32_t rest = key / static_cast<uint32_t>(g.dims[0]);
-    const int cy = static_cast<int>(rest % static_cast<uint32_t>(g.dims[1]));
-    const int cz = D == 3 ? static_cast<int>(rest / static_cast<uint32_t>(g.dims[1])) : 0;
-    int k = colour1(cx, g.col_m[0], g.dims[0]);
-    k += g.col_n[0] * colour1(cy, g.col_m[1], g.dims[1]);
-    if (D == 3) k += g.col_n[0] * g.col_n[1] * colour1(cz, g.col_m[2], g.dims[2]);
+    int cc_[3];
+    decode_key<D>(g, key, cc_);
+    const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
+    int k = colour1(g, 0, cx);
+    k += g.col_n[0] * colour1(g, 1, cy);
+    if (D == 3) k += g.col_n[0] * g.col_n[1] * colour1(g, 2, cz);
     return k;
 }
 
@@ -443,6 +481,105 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
             ++nn;
         });
         nbr_cnt[q] = nn > kNearLocal ? kNearOverflow : static_cast<uint8_t>(nn);
+    }
+}
+
+// Near lists by pairs: each thread scans the HALF stencil of its particle q (rows ahead
+// of q's row, the cells ahead of q's cell in its row, the particles after q in its cell),
+// so every candidate pair is screened once, and a pair that passes is appended to both
+// lists (atomic counters, ncount must be zero on entry).  Periodic images are resolved
+// per row / per x segment (a constant shift by +-L), not per candidate.  The screen
+// keeps near_candidates' cutoff, margin and factor, so the lists hold the same pairs as
+// k_near_lists, in another order (which the sweep does not observe).  Requires every
+// near_s >= 0 (no axis scanned whole); k_near_lists covers the other grids.
+template <int D>
+__global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const GridParams* __restrict__ gp,
+                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                   int32_t* __restrict__ nbr, uint32_t* __restrict__ ncount) {
+    const GridParams& g = *gp;
+    const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
+    const int sx = g.near_s[0], sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const float4 me = S.xf[q];
+        const int32_t idq = S.id[q];
+        const uint32_t key = skey[q];
+        int cc_[3];
+        decode_key<D>(g, key, cc_);
+        const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
+        const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
+        const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
+        const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
+        // screen [b, e) against me shifted by (shx, shy, shz); append pairs
+        auto run = [&](int64_t b, int64_t e, float ox, float oy, float oz) {
+            for (int64_t j = b; j < e; ++j) {
+                const float4 c = S.xf[j];
+                const float ex = __fsub_rn(c.x, ox), ey = __fsub_rn(c.y, oy);
+                const float ez = D == 3 ? __fsub_rn(c.z, oz) : 0.f;
+                const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                const float lim = __fadd_rn(base, c.w);
+                if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f)) continue;
+                if (S.id[j] == idq) continue;  // shape.hpp:544 self-exclusion by id
+                const uint32_t kq = atomicAdd(&ncount[q], 1u);
+                if (kq < kNearLocal) nbr[q * kNearLocal + kq] = static_cast<int32_t>(j);
+                const uint32_t kj = atomicAdd(&ncount[j], 1u);
+                if (kj < kNearLocal) nbr[j * kNearLocal + kj] = static_cast<int32_t>(q);
+            }
+        };
+        const int zhi = D == 3 ? cz + sz : 0;
+        for (int zz = cz; zz <= zhi; ++zz) {
+            float dzd = 0.f, oz = me.z;
+            if (D == 3) {
+                const float zb = zz * g.edge_f[2];
+                dzd = fmaxf(0.f, fmaxf(zb - me.z, me.z - (zb + g.edge_f[2])));
+            }
+            int z = zz;
+            if (D == 3 && z >= dz) {  // image above the box: candidates sit at z - L
+                z -= dz;
+                oz = __fsub_rn(me.z, g.L_f[2]);
+            }
+            const int ylo = zz == cz ? cy : cy - sy;
+            for (int yy = ylo; yy <= cy + sy; ++yy) {
+                const float yb = yy * g.edge_f[1];
+                const float dyd = fmaxf(0.f, fmaxf(yb - me.y, me.y - (yb + g.edge_f[1])));
+                const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
+                if (dyz2 > cut2) continue;
+                int y = yy;
+                float oy = me.y;
+                if (y < 0) {
+                    y += dy;
+                    oy = __fadd_rn(me.y, g.L_f[1]);
+                } else if (y >= dy) {
+                    y -= dy;
+                    oy = __fsub_rn(me.y, g.L_f[1]);
+                }
+                const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
+                const bool own = zz == cz && yy == cy;
+                const int xl = own ? cx : cx - sx, xr = cx + sx;
+                // cells [xl, xr] of the unwrapped row: up to three pieces (below 0, inside, above dx)
+                const int64_t first = own ? q + 1 : -1;  // own cell: only the particles after q
+                if (xl < 0) {
+                    const int e = min(xr, -1);
+                    run(cs[row + xl + dx], cs[row + e + 1 + dx], __fadd_rn(me.x, g.L_f[0]), oy, oz);
+                }
+                if (xr >= 0 && xl < dx) {
+                    const int b = max(xl, 0), e = min(xr, dx - 1);
+                    const int64_t bb = first >= 0 && b == cx ? first : cs[row + b];
+                    run(bb, cs[row + e + 1], me.x, oy, oz);
+                }
+                if (xr >= dx) {
+                    const int b = max(xl, dx);
+                    run(cs[row + b - dx], cs[row + xr - dx + 1], __fsub_rn(me.x, g.L_f[0]), oy, oz);
+                }
+            }
+        }
+    }
+}
+
+// counts -> the sweep's uint8 list lengths (kNearOverflow: rescan)
+__global__ void k_near_counts(int64_t n, const uint32_t* __restrict__ ncount, uint8_t* __restrict__ nbr_cnt) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = ncount[q];
+        nbr_cnt[q] = c > kNearLocal ? kNearOverflow : static_cast<uint8_t>(c);
     }
 }
 
@@ -587,36 +724,19 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
     double p[D];
     int accepted = -1;
     if (nn != kNearOverflow) {
-        // the near list once (64 B, four 16-byte loads); per trial every record load is
-        // issued before any test (no early exit), kBatch at a time, so a trial costs one
-        // memory latency per batch instead of one per neighbour
-        constexpr int kBatch = 4;
-        int32_t nb[kNearLocal];
-        const int4* nb4 = reinterpret_cast<const int4*>(nbr + q * kNearLocal);
-#pragma unroll
-        for (int c = 0; c < kNearLocal / 4; ++c) {
-            int4 v = make_int4(0, 0, 0, 0);
-            if (4 * c < nn) v = nb4[c];
-            nb[4 * c] = v.x; nb[4 * c + 1] = v.y; nb[4 * c + 2] = v.z; nb[4 * c + 3] = v.w;
-        }
+        // neighbours two at a time: both record loads issued before either test
+        const int32_t* nbq = nbr + q * kNearLocal;
         for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
             propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
             bool hit = false;
-#pragma unroll
-            for (int t0 = 0; t0 < kNearLocal; t0 += kBatch) {
-                if (t0 < nn) {
-                    double4 v[kBatch];
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u)
-                        if (t0 + u < nn) v[u] = S.rec[nb[t0 + u]];
-#pragma unroll
-                    for (int u = 0; u < kBatch; ++u) {
-                        if (t0 + u < nn) {
-                            const double xl[3] = {v[u].x, v[u].y, v[u].z};
-                            hit |= sphere_overlap<D>(box, p, ri, xl, v[u].w);
-                        }
-                    }
-                }
+            for (int t0 = 0; t0 < nn && !hit; t0 += 2) {
+                const int2 jj = *reinterpret_cast<const int2*>(nbq + t0);
+                const bool two = t0 + 1 < nn;
+                const double4 a = S.rec[jj.x];
+                const double4 b = two ? S.rec[jj.y] : a;
+                const double xa[3] = {a.x, a.y, a.z};
+                const double xb[3] = {b.x, b.y, b.z};
+                hit = sphere_overlap<D>(box, p, ri, xa, a.w) || (two && sphere_overlap<D>(box, p, ri, xb, b.w));
             }
             if (!hit) accepted = l;
         }
@@ -644,6 +764,9 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
 #ifndef SRM_SWEEP_THREADS
 #define SRM_SWEEP_THREADS 128
 #endif
+#ifndef SRM_SWEEP_MINB
+#define SRM_SWEEP_MINB 8
+#endif
 constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
 // One (colour class, rank) step of the sweep: a thread per particle of the bucket.  The
@@ -652,7 +775,7 @@ constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 // sweeps the rest of its (crowded) cell, in slot order.  The launch sequence over
 // (class, rank) reproduces the sequential sweep of orc_sweep_round bit for bit.
 template <int D>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_work(int cls, int rank, State S, Box box,
+__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_work(int cls, int rank, State S, Box box,
                                                               const GridParams* __restrict__ gp,
                                                               const RoundParams* __restrict__ rpp,
                                                               const int64_t* __restrict__ cs,
