@@ -74,15 +74,17 @@ struct srm_b200_ctx {
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
-    uint8_t* nbr_cnt = nullptr;
-    uint32_t* ncount = nullptr;  // pair-append counters of k_near_half
-    int32_t* work = nullptr;     // (colour class, rank) work lists of the sweep, [cap]
+    int2* work = nullptr;        // (colour class, rank) work lists of the sweep: (index, slot)
     uint32_t* bcount = nullptr;  // bucket counts / starts / cursors, [ncls * kRanks + 1]
     uint32_t* bstart = nullptr;
     uint32_t* bcursor = nullptr;
     int64_t bucket_cap = 0;
+    unsigned long long* qcursor = nullptr;  // per-class take cursors of k_sweep_queue
+    int64_t qcursor_cap = 0;
+    int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_queue (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
-    int near_mode = std::getenv("SRM_B200_NEAR_THREAD") ? 1 : 0;  // 0: warp per cell, 1: thread per particle
+    int near_mode = std::getenv("SRM_B200_NEAR_THREAD") ? 1 : 0;  // 0: half-stencil pairs, 1: full stencil
+    int sweep_mode = std::getenv("SRM_B200_SWEEP_RANKS") ? 1 : 0;  // 0: CTA work queue, 1: (class, rank) launches
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -205,13 +207,17 @@ struct srm_b200_ctx {
         gp = dalloc<GridParams>(1);
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
-        nbr = dalloc<int32_t>(cap * kNearLocal);
-        nbr_cnt = dalloc<uint8_t>(cap);
-        ncount = dalloc<uint32_t>(cap);
-        work = dalloc<int32_t>(cap);
+        nbr = dalloc<int32_t>(cap * kNearRow);
+        work = dalloc<int2>(cap);
         const int work_smem = 2 * kBucketSmem * 4;
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
+        {
+            int per_sm = 0, sms = 0;
+            SRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_queue<3>, kSweepThreads, 0));
+            SRM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+            queue_ctas = std::max(1, per_sm) * std::max(1, sms);
+        }
         S.xf = dalloc<float4>(cap);
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
@@ -230,7 +236,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(nbr); cudaFree(nbr_cnt); cudaFree(ncount); cudaFree(S.xf); cudaFree(work); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor);
+        cudaFree(nbr); cudaFree(S.xf); cudaFree(work); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor); cudaFree(qcursor);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -351,6 +357,12 @@ struct srm_b200_ctx {
         }
         if (off[g.ncls] != g.ncells) throw std::logic_error("colour classes do not tile the grid");
         const int64_t nbk = static_cast<int64_t>(g.ncls) * kRanks;
+        if (g.ncls > qcursor_cap) {
+            cudaFree(qcursor);
+            qcursor = nullptr;
+            qcursor_cap = g.ncls;
+            qcursor = dalloc<unsigned long long>(qcursor_cap);
+        }
         if (nbk + 1 > bucket_cap) {
             cudaFree(bcount);
             cudaFree(bstart);
@@ -369,10 +381,11 @@ struct srm_b200_ctx {
         hg_set = true;
     }
 
-    void set_round(double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration) {
+    void set_round(double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration, bool write_acc) {
         RoundParams v{};
         v.c_m = c_m;
         v.n_l = n_l;
+        v.write_acc = write_acc ? 1 : 0;
         v.key.k0 = static_cast<uint32_t>(seed);
         v.key.k1 = static_cast<uint32_t>(seed >> 32);
         v.key.round_id = round_id & 0xFFFFFFu;
@@ -406,15 +419,15 @@ struct srm_b200_ctx {
     }
 
     // One round on T (T is rewritten in this round's sorted order); gp must be set.
-    // grid rebuild, near lists, then the coloured Gauss-Seidel sweep (one launch per
-    // superblock colour), then the overlap reduction over the non-movers.
+    // grid rebuild, near lists + work lists, then the coloured Gauss-Seidel sweep (one
+    // launch per (colour class, rank)), then the overlap reduction over the non-movers.
     void round(State& T, double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
-               bool with_stats, bool with_candidates) {
+               bool with_stats, bool with_candidates, bool write_acc = false) {
         if (n_l > kMaxPhases) throw Invalid{"n_l > 254 is not supported by the B200 path"};
-        set_round(c_m, n_l, seed, round_id, iteration);
+        set_round(c_m, n_l, seed, round_id, iteration, write_acc);
         grid_build(T);
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
-        SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
+        if (write_acc) SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
             FamScope fs(this, 2);  // near lists + (class, rank) work lists
             const int nbk = hg.ncls * kRanks;
@@ -426,25 +439,39 @@ struct srm_b200_ctx {
                 k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
             k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
             if (dim == 2)
-                k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
+                k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot, bcursor, work);
             else
-                k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcursor, work);
+                k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot, bcursor, work);
             const int nb = blocks_for(n, 256);
             bool half = near_mode == 0;
             for (int a = 0; a < dim; ++a) half = half && hg.near_s[a] >= 0;
             if (half) {  // pairs once, appended to both lists
-                SRM_CUDA(cudaMemsetAsync(ncount, 0, sizeof(uint32_t) * n, stream));
-                if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, ncount);
-                else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, ncount);
-                k_near_counts<<<nb, 256, 0, stream>>>(n, ncount, nbr_cnt);
+                k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
+                if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 launched(5);
             } else {
-                if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
-                else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, nbr_cnt);
+                if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 launched(4);
             }
         }
-        {
+        if (sweep_mode == 0) {
+            FamScope fs(this, 1);
+            SRM_CUDA(cudaMemsetAsync(qcursor, 0, sizeof(unsigned long long) * hg.ncls, stream));
+            for (int cls = 0; cls < hg.ncls; ++cls) {
+                const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
+                // persistent CTAs: one full wave at most
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), queue_ctas)));
+                if (dim == 2)
+                    k_sweep_queue<2><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
+                                                                         work, qcursor + cls, nbr, acc, active, stats);
+                else
+                    k_sweep_queue<3><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
+                                                                         work, qcursor + cls, nbr, acc, active, stats);
+            }
+            launched(hg.ncls);
+        } else {
             FamScope fs(this, 1);
             for (int cls = 0; cls < hg.ncls; ++cls) {
                 const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
@@ -452,10 +479,10 @@ struct srm_b200_ctx {
                 for (int rank = 0; rank < kRanks; ++rank) {
                     if (dim == 2)
                         k_sweep_work<2><<<grid, kSweepThreads, 0, stream>>>(cls, rank, S, box, gp, rp, cell_start, skey, bstart,
-                                                                            work, nbr, nbr_cnt, acc, active, stats);
+                                                                            work, nbr, acc, active, stats);
                     else
                         k_sweep_work<3><<<grid, kSweepThreads, 0, stream>>>(cls, rank, S, box, gp, rp, cell_start, skey, bstart,
-                                                                            work, nbr, nbr_cnt, acc, active, stats);
+                                                                            work, nbr, acc, active, stats);
                 }
             }
             launched(hg.ncls * kRanks);
@@ -799,7 +826,7 @@ int srm_b200_round(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint6
             // complete under CellGrid's safety bound (cell_grid.hpp:288-293)
             if (cell_size < 2.0 * mr + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
             c->set_grid(g);
-            c->round(c->P, c_m, n_l, key, round_id, iteration, true, with_candidates != 0);
+            c->round(c->P, c_m, n_l, key, round_id, iteration, true, with_candidates != 0, accepted_out != nullptr);
             if (accepted_out) {
                 k_acc_by_slot<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P.slot, c->acc, reinterpret_cast<uint8_t*>(c->perm));
                 c->launched();

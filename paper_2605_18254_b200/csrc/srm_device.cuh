@@ -82,33 +82,76 @@ struct RngKey {
 
 // Unit vector with only +,-,*,/,sqrt (bit-identical to oracle/srm_oracle.c):
 //   3D Marsaglia (1972); 2D normalised point in the unit disk.
+// one rejection draw: the point (x1, x2) of draw `draw` and its squared norm s
+__device__ __forceinline__ double draw_point(const RngKey& key, uint32_t slot, uint32_t attempt, uint32_t stream,
+                                             uint32_t draw, double* x1, double* x2) {
+    const U4 o = philox4x32_10(U4{slot, attempt, key.round_id | (stream << 24) | (draw << 25), key.iteration},
+                               key.k0, key.k1);
+    const uint64_t a = ((static_cast<uint64_t>(o.x) << 32) | o.y) >> 11;
+    const uint64_t b = ((static_cast<uint64_t>(o.z) << 32) | o.w) >> 11;
+    *x1 = __dsub_rn(__dmul_rn(__ull2double_rn(a), 0x1p-52), 1.0);
+    *x2 = __dsub_rn(__dmul_rn(__ull2double_rn(b), 0x1p-52), 1.0);
+    return __dadd_rn(__dmul_rn(*x1, *x1), __dmul_rn(*x2, *x2));
+}
+
+template <int D>
+__device__ __forceinline__ bool draw_ok(double s) {
+    return D == 3 ? s < 1.0 : (s < 1.0 && s > 1e-24);
+}
+
+template <int D>
+__device__ __forceinline__ void point_to_unit(double x1, double x2, double s, double* u) {
+    if constexpr (D == 3) {
+        const double q = __dmul_rn(2.0, __dsqrt_rn(__dsub_rn(1.0, s)));
+        u[0] = __dmul_rn(x1, q);
+        u[1] = __dmul_rn(x2, q);
+        u[2] = __dsub_rn(1.0, __dmul_rn(2.0, s));
+    } else {
+        const double inv = __ddiv_rn(1.0, __dsqrt_rn(s));
+        u[0] = __dmul_rn(x1, inv);
+        u[1] = __dmul_rn(x2, inv);
+    }
+}
+
+// The first accepted of draws 0, 1, 2, ... (< 64).  SRM_DRAW_PAIRS: draws 0 and 1 are
+// computed together (no divergence for the ~21% of 3D trials whose first draw is
+// rejected, at the price of a second Philox call for the other 79%).
+#ifndef SRM_DRAW_PAIRS
+#define SRM_DRAW_PAIRS 0
+#endif
 template <int D>
 __device__ __forceinline__ void unit_vector(const RngKey& key, uint32_t slot, uint32_t attempt,
                                             uint32_t stream, double* u) {
-    for (uint32_t draw = 0; draw < 64; ++draw) {
-        const U4 o = philox4x32_10(
-            U4{slot, attempt, key.round_id | (stream << 24) | (draw << 25), key.iteration}, key.k0,
-            key.k1);
-        const uint64_t a = ((static_cast<uint64_t>(o.x) << 32) | o.y) >> 11;
-        const uint64_t b = ((static_cast<uint64_t>(o.z) << 32) | o.w) >> 11;
-        const double x1 = __dsub_rn(__dmul_rn(__ull2double_rn(a), 0x1p-52), 1.0);
-        const double x2 = __dsub_rn(__dmul_rn(__ull2double_rn(b), 0x1p-52), 1.0);
-        const double s = __dadd_rn(__dmul_rn(x1, x1), __dmul_rn(x2, x2));
-        if constexpr (D == 3) {
-            if (s < 1.0) {
-                const double q = __dmul_rn(2.0, __dsqrt_rn(__dsub_rn(1.0, s)));
-                u[0] = __dmul_rn(x1, q);
-                u[1] = __dmul_rn(x2, q);
-                u[2] = __dsub_rn(1.0, __dmul_rn(2.0, s));
+    if (!SRM_DRAW_PAIRS) {
+        for (uint32_t draw = 0; draw < 64; ++draw) {
+            double x1, x2;
+            const double s = draw_point(key, slot, attempt, stream, draw, &x1, &x2);
+            if (draw_ok<D>(s)) {
+                point_to_unit<D>(x1, x2, s, u);
                 return;
             }
-        } else {
-            if (s < 1.0 && s > 1e-24) {
-                const double inv = __ddiv_rn(1.0, __dsqrt_rn(s));
-                u[0] = __dmul_rn(x1, inv);
-                u[1] = __dmul_rn(x2, inv);
-                return;
-            }
+        }
+        u[0] = 1.0;
+#pragma unroll
+        for (int k = 1; k < D; ++k) u[k] = 0.0;
+        return;
+    }
+    double a1, a2, b1, b2;
+    const double sa = draw_point(key, slot, attempt, stream, 0, &a1, &a2);
+    const double sb = draw_point(key, slot, attempt, stream, 1, &b1, &b2);
+    if (draw_ok<D>(sa)) {
+        point_to_unit<D>(a1, a2, sa, u);
+        return;
+    }
+    if (draw_ok<D>(sb)) {
+        point_to_unit<D>(b1, b2, sb, u);
+        return;
+    }
+    for (uint32_t draw = 2; draw < 64; ++draw) {
+        const double s = draw_point(key, slot, attempt, stream, draw, &a1, &a2);
+        if (draw_ok<D>(s)) {
+            point_to_unit<D>(a1, a2, s, u);
+            return;
         }
     }
     u[0] = 1.0;

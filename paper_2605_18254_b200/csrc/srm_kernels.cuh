@@ -82,6 +82,7 @@ __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, in
 struct RoundParams {
     double c_m;
     int32_t n_l;
+    int32_t write_acc;  // also record the accepted trial per particle (parity outputs)
     RngKey key;
 };
 
@@ -367,7 +368,16 @@ __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
 // Live positions: S.rec[j] holds (x, r) of j -- its round-start position, overwritten by
 // its accepted trial when j moves; one 32-byte sector per neighbour read.
 
-constexpr int kNearLocal = 16;  // near candidates kept per particle; more -> rescan per trial
+// Near list row of a particle, kNearRow int32: [0] f = neighbours the particle found
+// itself (half stencil), [1] b = neighbours that found it (atomic appends), entries
+// [2, 2 + f) and [15 - k] for k < b.  f + b > kNearCap means overflow: the sweep
+// rescans the grid.  The first 32-byte sector holds both counts and six entries.
+constexpr int kNearRow = 16;
+constexpr int kNearCap = kNearRow - 2;
+
+__device__ __forceinline__ int32_t near_entry(const int32_t* row, int f, int t) {
+    return t < f ? row[2 + t] : row[kNearRow - 1 - (t - f)];
+}
 constexpr int kRanks = 3;       // sweep steps per class: ranks 0, 1 and 2+ (the rank-2 thread
                                 // sweeps the rest of its cell in slot order)
 constexpr int kBucketSmem = 8192;  // (class, rank) buckets aggregated in shared memory
@@ -444,8 +454,6 @@ __device__ __forceinline__ void near_candidates(const GridParams& g, const int64
     }
 }
 
-constexpr uint8_t kNearOverflow = 255;
-
 // colour class of a cell
 __device__ __forceinline__ int colour1(const GridParams& g, int a, int x) {
     const int m = g.col_m[a];
@@ -464,30 +472,31 @@ __device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
     return k;
 }
 
-// Near lists of every particle, one parallel pass before the sweep: nbr[q*kNearLocal..]
-// and nbr_cnt[q] (kNearOverflow: more than kNearLocal, the sweep rescans the grid).
+// Near lists of every particle, a thread per particle over its full stencil (grids with
+// an axis scanned whole; k_near_half covers the rest).  Row layout: see kNearRow.
 template <int D>
 __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const GridParams* __restrict__ gp,
                                                     const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                    int32_t* __restrict__ nbr, uint8_t* __restrict__ nbr_cnt) {
+                                                    int32_t* __restrict__ nbr) {
     const GridParams& g = *gp;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        int32_t* my = nbr + q * kNearLocal;
+        int32_t* my = nbr + q * kNearRow;
         int nn = 0;
         const int32_t idq = S.id[q];
         near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
             if (S.id[j] == idq) return;  // shape.hpp:544 self-exclusion by id
-            if (nn < kNearLocal) my[nn] = static_cast<int32_t>(j);
+            if (nn < kNearCap) my[2 + nn] = static_cast<int32_t>(j);
             ++nn;
         });
-        nbr_cnt[q] = nn > kNearLocal ? kNearOverflow : static_cast<uint8_t>(nn);
+        my[0] = nn;
+        my[1] = 0;
     }
 }
 
 // Near lists by pairs: each thread scans the HALF stencil of its particle q (rows ahead
 // of q's row, the cells ahead of q's cell in its row, the particles after q in its cell),
 // so every candidate pair is screened once, and a pair that passes is appended to both
-// lists (atomic counters, ncount must be zero on entry).  Periodic images are resolved
+// lists (atomic counters in word 0 of each row, which must be zero on entry).  Periodic images are resolved
 // per row / per x segment (a constant shift by +-L), not per candidate.  The screen
 // keeps near_candidates' cutoff, margin and factor, so the lists hold the same pairs as
 // k_near_lists, in another order (which the sweep does not observe).  Requires every
@@ -495,7 +504,7 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
 template <int D>
 __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const GridParams* __restrict__ gp,
                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                   int32_t* __restrict__ nbr, uint32_t* __restrict__ ncount) {
+                                                   int32_t* __restrict__ nbr) {
     const GridParams& g = *gp;
     const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
     const int sx = g.near_s[0], sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
@@ -509,7 +518,9 @@ __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const Gri
         const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
         const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
         const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
-        // screen [b, e) against me shifted by (shx, shy, shz); append pairs
+        // screen [b, e) against me shifted by (ox, oy, oz); keep the hits (q's forward list)
+        int32_t* myrow = nbr + q * kNearRow;
+        int nf = 0;
         auto run = [&](int64_t b, int64_t e, float ox, float oy, float oz) {
             for (int64_t j = b; j < e; ++j) {
                 const float4 c = S.xf[j];
@@ -519,10 +530,8 @@ __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const Gri
                 const float lim = __fadd_rn(base, c.w);
                 if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f)) continue;
                 if (S.id[j] == idq) continue;  // shape.hpp:544 self-exclusion by id
-                const uint32_t kq = atomicAdd(&ncount[q], 1u);
-                if (kq < kNearLocal) nbr[q * kNearLocal + kq] = static_cast<int32_t>(j);
-                const uint32_t kj = atomicAdd(&ncount[j], 1u);
-                if (kj < kNearLocal) nbr[j * kNearLocal + kj] = static_cast<int32_t>(q);
+                if (nf < kNearCap) myrow[2 + nf] = static_cast<int32_t>(j);
+                ++nf;
             }
         };
         const int zhi = D == 3 ? cz + sz : 0;
@@ -572,14 +581,27 @@ __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const Gri
                 }
             }
         }
+        myrow[0] = nf;
+        // q into the backward part of every forward neighbour's row: the atomics are
+        // independent, so they are issued back to back before any result is used
+        const int m = nf < kNearCap ? nf : kNearCap;
+        int kk[kNearCap];
+#pragma unroll
+        for (int t = 0; t < kNearCap; ++t)
+            if (t < m) kk[t] = atomicAdd(&nbr[static_cast<int64_t>(myrow[2 + t]) * kNearRow + 1], 1);
+#pragma unroll
+        for (int t = 0; t < kNearCap; ++t)
+            if (t < m && kk[t] < kNearCap)
+                nbr[static_cast<int64_t>(myrow[2 + t]) * kNearRow + kNearRow - 1 - kk[t]] = static_cast<int32_t>(q);
     }
 }
 
-// counts -> the sweep's uint8 list lengths (kNearOverflow: rescan)
-__global__ void k_near_counts(int64_t n, const uint32_t* __restrict__ ncount, uint8_t* __restrict__ nbr_cnt) {
+// zero the count word (the whole first sector) of every near-list row
+__global__ void k_near_zero(int64_t n, int32_t* __restrict__ nbr) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t c = ncount[q];
-        nbr_cnt[q] = c > kNearLocal ? kNearOverflow : static_cast<uint8_t>(c);
+        int4* r = reinterpret_cast<int4*>(nbr + q * kNearRow);
+        r[0] = make_int4(0, 0, 0, 0);
+        r[1] = make_int4(0, 0, 0, 0);
     }
 }
 
@@ -673,7 +695,8 @@ template <int D>
 __global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const GridParams* __restrict__ gp,
                                                              const int64_t* __restrict__ cs,
                                                              const uint32_t* __restrict__ skey,
-                                                             uint32_t* __restrict__ cursor, int32_t* __restrict__ work) {
+                                                             const int32_t* __restrict__ slot,
+                                                             uint32_t* __restrict__ cursor, int2* __restrict__ work) {
     extern __shared__ uint32_t hist[];  // [nb] counts, then [nb] CTA bases
     const GridParams& g = *gp;
     const int nb = g.ncls * kRanks;
@@ -693,7 +716,7 @@ __global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const Gr
         myb[k] = bucket_of<D>(g, cs, skey[q], q);
         if (myb[k] < 0) continue;
         if (local) myl[k] = atomicAdd(&hist[myb[k]], 1u);
-        else work[atomicAdd(&cursor[myb[k]], 1u)] = static_cast<int32_t>(q);
+        else work[atomicAdd(&cursor[myb[k]], 1u)] = make_int2(static_cast<int32_t>(q), slot[q]);
     }
     if (!local) return;
     __syncthreads();
@@ -704,41 +727,68 @@ __global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const Gr
     for (int k = 0; k < kWorkPer; ++k) {
         if (myb[k] < 0) continue;
         const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        work[base[myb[k]] + myl[k]] = static_cast<int32_t>(q);
+        work[base[myb[k]] + myl[k]] = make_int2(static_cast<int32_t>(q), slot[q]);
     }
 }
 
 template <int D>
-__device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const Box& box,
+__device__ __forceinline__ void sweep_particle(int64_t q, int32_t sl, const State& S, const Box& box,
                                                const GridParams& g, const RoundParams& rp,
                                                const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                               const int32_t* __restrict__ nbr, const uint8_t* __restrict__ nbr_cnt,
+                                               const int32_t* __restrict__ nbr,
                                                uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                StatsDev* stats) {
-    const int nn = nbr_cnt[q];
+    const int32_t* row = nbr + q * kNearRow;
+    const int4 h0 = *reinterpret_cast<const int4*>(row);  // counts + first two entries
+    const int nf = h0.x, nn = h0.x + h0.y;
     const double4 me = S.rec[q];  // round-start record; q is visited once
     double xi[D];
     rec_pos<D>(me, xi);
     const double ri = me.w;
-    const int32_t sl = S.slot[q];
     double p[D];
     int accepted = -1;
-    if (nn != kNearOverflow) {
-        // neighbours two at a time: both record loads issued before either test
-        const int32_t* nbq = nbr + q * kNearLocal;
-        for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
-            propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
-            bool hit = false;
-            for (int t0 = 0; t0 < nn && !hit; t0 += 2) {
-                const int2 jj = *reinterpret_cast<const int2*>(nbq + t0);
-                const bool two = t0 + 1 < nn;
-                const double4 a = S.rec[jj.x];
-                const double4 b = two ? S.rec[jj.y] : a;
-                const double xa[3] = {a.x, a.y, a.z};
-                const double xb[3] = {b.x, b.y, b.z};
-                hit = sphere_overlap<D>(box, p, ri, xa, a.w) || (two && sphere_overlap<D>(box, p, ri, xb, b.w));
+    if (nn <= kNearCap) {
+#ifndef SRM_TRIAL_PAIRS
+#define SRM_TRIAL_PAIRS 0
+#endif
+        if (SRM_TRIAL_PAIRS) {
+        // trials two at a time (speculatively: a trial after the first clear one has no
+            // effect), each neighbour record loaded once for both
+            for (int l = 0; l < rp.n_l && accepted < 0; l += 2) {
+                double pa[D], pb[D];
+                const bool second = l + 1 < rp.n_l;
+                propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), pa);
+                if (second) propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l + 1), pb);
+                bool hit_a = false, hit_b = !second;
+                for (int t = 0; t < nn && !(hit_a && hit_b); ++t) {
+                    const int32_t j = t == 0 ? (nf > 0 ? h0.z : row[kNearRow - 1]) : near_entry(row, nf, t);
+                    const double4 v = S.rec[j];
+                    const double xl[3] = {v.x, v.y, v.z};
+                    hit_a = hit_a || sphere_overlap<D>(box, pa, ri, xl, v.w);
+                    hit_b = hit_b || sphere_overlap<D>(box, pb, ri, xl, v.w);
+                }
+                if (!hit_a) {
+                    accepted = l;
+    #pragma unroll
+                    for (int a = 0; a < D; ++a) p[a] = pa[a];
+                } else if (!hit_b) {
+                    accepted = l + 1;
+    #pragma unroll
+                    for (int a = 0; a < D; ++a) p[a] = pb[a];
+                }
             }
-            if (!hit) accepted = l;
+        } else {
+            for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
+                propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+                bool hit = false;
+                for (int t = 0; t < nn && !hit; ++t) {
+                    const int32_t j = t == 0 ? (nf > 0 ? h0.z : row[kNearRow - 1]) : near_entry(row, nf, t);
+                    const double4 v = S.rec[j];
+                    const double xl[3] = {v.x, v.y, v.z};
+                    hit = sphere_overlap<D>(box, p, ri, xl, v.w);
+                }
+                if (!hit) accepted = l;
+            }
         }
     } else {  // crowded neighbourhood: rescan (same candidate set, id filter as the list)
         const int32_t idq = S.id[q];
@@ -754,7 +804,7 @@ __device__ __forceinline__ void sweep_particle(int64_t q, const State& S, const 
             if (ok) accepted = l;
         }
     }
-    acc[q] = accepted >= 0 ? static_cast<uint8_t>(accepted) : kNotAccepted;
+    if (rp.write_acc) acc[q] = accepted >= 0 ? static_cast<uint8_t>(accepted) : kNotAccepted;
     if (accepted >= 0)  // publish the live position (in place: the sorted state is the round's output)
         S.rec[q] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, ri);
     else
@@ -781,23 +831,153 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_work(in
                                                               const int64_t* __restrict__ cs,
                                                               const uint32_t* __restrict__ skey,
                                                               const uint32_t* __restrict__ bstart,
-                                                              const int32_t* __restrict__ work,
+                                                              const int2* __restrict__ work,
                                                               const int32_t* __restrict__ nbr,
-                                                              const uint8_t* __restrict__ nbr_cnt,
                                                               uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                               StatsDev* stats) {
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
     const int64_t lo = bstart[cls * kRanks + rank];
     const int64_t cnt = bstart[cls * kRanks + rank + 1] - lo;
-    const int32_t* list = work + lo;
+    const int2* list = work + lo;
     const RoundParams rp = *rpp;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < cnt;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t q0 = list[t];
-        const int64_t e = rank == kRanks - 1 ? cs[skey[q0] + 1] : q0 + 1;
-        for (int64_t q = q0; q < e; ++q)
-            sweep_particle<D>(q, S, box, g, rp, cs, skey, nbr, nbr_cnt, acc, active, stats);
+        const int2 w = list[t];  // (sorted index, storage slot)
+        sweep_particle<D>(w.x, w.y, S, box, g, rp, cs, skey, nbr, acc, active, stats);
+        if (rank == kRanks - 1) {  // the rest of a crowded cell, in slot order
+            const int64_t e = cs[skey[w.x] + 1];
+            for (int64_t q = w.x + 1; q < e; ++q)
+                sweep_particle<D>(q, S.slot[q], S, box, g, rp, cs, skey, nbr, acc, active, stats);
+        }
+    }
+}
+
+// One trial of particle q (slot sl, round-start position xi, radius ri): propose trial l
+// and test it against the live positions of q's near list (or, for an overflowed list,
+// of every candidate of its stencil).  Returns true when the trial is clear (p = trial).
+template <int D>
+__device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const double* xi, double ri,
+                                           const State& S, const Box& box, const GridParams& g,
+                                           const RoundParams& rp, const int64_t* __restrict__ cs,
+                                           const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
+                                           double* p) {
+    propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+    const int32_t* row = nbr + q * kNearRow;
+    const int4 h0 = *reinterpret_cast<const int4*>(row);
+    const int nf = h0.x, nn = h0.x + h0.y;
+    if (nn <= kNearCap) {
+        for (int t = 0; t < nn; ++t) {
+            const int32_t j = t == 0 ? (nf > 0 ? h0.z : row[kNearRow - 1]) : near_entry(row, nf, t);
+            const double4 v = S.rec[j];
+            const double xl[3] = {v.x, v.y, v.z};
+            if (sphere_overlap<D>(box, p, ri, xl, v.w)) return false;
+        }
+        return true;
+    }
+    const int32_t idq = S.id[q];  // crowded neighbourhood: rescan (same candidates, id filter)
+    bool ok = true;
+    near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+        if (!ok || S.id[j] == idq) return;
+        const double4 v = S.rec[j];
+        const double xl[3] = {v.x, v.y, v.z};
+        if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
+    });
+    return ok;
+}
+
+// One colour class of the sweep with a CTA-local work queue.  Items are (particle,
+// trial); the CTA starts with one rank-0 particle (first of its cell) per thread and
+// runs rounds of ONE trial per item: a clear trial publishes the move, a blocked one
+// re-queues (particle, trial + 1), an exhausted one reverts (non-mover list); a
+// particle that is done hands its cell on to the next particle (slot order).  So every
+// round keeps the live items dense in the warps whatever the trial counts and cell
+// occupancies.  Visiting order per cell and the trials of each particle are those of
+// the sequential sweep; cells of one class never interact, so the result equals
+// orc_sweep_round bit for bit.
+struct QItem {
+    int32_t q, l, sl, end;  // sorted index, next trial, storage slot, end of its cell
+};
+
+template <int D>
+__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_queue(int cls, State S, Box box,
+                                                                               const GridParams* __restrict__ gp,
+                                                                               const RoundParams* __restrict__ rpp,
+                                                                               const int64_t* __restrict__ cs,
+                                                                               const uint32_t* __restrict__ skey,
+                                                                               const uint32_t* __restrict__ bstart,
+                                                                               const int2* __restrict__ work,
+                                                                               unsigned long long* __restrict__ cursor,
+                                                                               const int32_t* __restrict__ nbr,
+                                                                               uint8_t* __restrict__ acc,
+                                                                               int32_t* __restrict__ active,
+                                                                               StatsDev* stats) {
+    __shared__ QItem qbuf[2][kSweepThreads];
+    __shared__ int qn[2];
+    __shared__ long long take_base;
+    __shared__ int take_n;
+    const GridParams& g = *gp;
+    if (cls >= g.ncls) return;
+    const RoundParams rp = *rpp;
+    const int64_t lo = bstart[cls * kRanks], cnt = bstart[cls * kRanks + 1] - lo;
+    int cur = 0;
+    if (threadIdx.x == 0) {
+        qn[0] = 0;
+        qn[1] = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        // refill the queue with fresh cells (persistent CTAs share the class's bucket)
+        if (threadIdx.x == 0) {
+            const int want = static_cast<int>(blockDim.x) - qn[cur];
+            take_n = 0;
+            if (want >= static_cast<int>(blockDim.x) / 4) {
+                const unsigned long long b = atomicAdd(cursor, static_cast<unsigned long long>(want));
+                take_base = static_cast<long long>(b);
+                const long long avail = cnt - static_cast<long long>(b);
+                take_n = avail <= 0 ? 0 : static_cast<int>(avail < want ? avail : want);
+            }
+        }
+        __syncthreads();
+        if (static_cast<int>(threadIdx.x) < take_n) {
+            const int2 w = work[lo + take_base + threadIdx.x];
+            qbuf[cur][qn[cur] + threadIdx.x] = QItem{w.x, 0, w.y, static_cast<int32_t>(cs[skey[w.x] + 1])};
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) qn[cur] += take_n;
+        __syncthreads();
+        const int m = qn[cur];
+        if (m == 0) break;
+        const int nxt = cur ^ 1;
+        if (static_cast<int>(threadIdx.x) < m) {
+            QItem it = qbuf[cur][threadIdx.x];
+            const double4 me = S.rec[it.q];  // round-start record (the particle has not moved)
+            double xi[D], p[D];
+            rec_pos<D>(me, xi);
+            const bool clear = trial_clear<D>(it.q, it.sl, it.l, xi, me.w, S, box, g, rp, cs, skey, nbr, p);
+            bool done = true;
+            if (clear) {
+                S.rec[it.q] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
+                if (rp.write_acc) acc[it.q] = static_cast<uint8_t>(it.l);
+            } else if (it.l + 1 < rp.n_l) {
+                ++it.l;
+                done = false;
+            } else {
+                if (rp.write_acc) acc[it.q] = kNotAccepted;
+                active[atomicAdd(&stats->active_count, 1ull)] = it.q;
+            }
+            if (done && it.q + 1 < it.end) {  // the next particle of the cell
+                it.q += 1;
+                it.l = 0;
+                it.sl = S.slot[it.q];
+                done = false;
+            }
+            if (!done) qbuf[nxt][atomicAdd(&qn[nxt], 1)] = it;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) qn[cur] = 0;
+        cur = nxt;
+        __syncthreads();
     }
 }
 
@@ -824,7 +1004,8 @@ __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const Gri
         const int32_t idi = S.id[i];
         for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
             for (int64_t j = b; j < e; ++j) {
-                if (j <= i || acc[j] != kNotAccepted || S.id[j] == idi) continue;
+                // movers never overlap anything: pairs with j > i suffice
+                if (j <= i || S.id[j] == idi) continue;
                 double xj[D];
                 const double4 vj = S.rec[j];
                 rec_pos<D>(vj, xj);
