@@ -84,7 +84,8 @@ struct srm_b200_ctx {
     int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_queue (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
     int near_mode = std::getenv("SRM_B200_NEAR_THREAD") ? 1 : 0;  // 0: half-stencil pairs, 1: full stencil
-    int sweep_mode = std::getenv("SRM_B200_SWEEP_RANKS") ? 1 : 0;  // 0: CTA work queue, 1: (class, rank) launches
+    // 2: warp queues (default), 0: CTA work queue, 1: (class, rank) launches
+    int sweep_mode = std::getenv("SRM_B200_SWEEP") ? std::atoi(std::getenv("SRM_B200_SWEEP")) : 2;
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -456,7 +457,21 @@ struct srm_b200_ctx {
                 launched(4);
             }
         }
-        if (sweep_mode == 0) {
+        if (sweep_mode == 2) {
+            FamScope fs(this, 1);
+            for (int cls = 0; cls < hg.ncls; ++cls) {
+                const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
+                // about 64 cells per warp, at most one wave of resident CTAs
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads * 2), queue_ctas)));
+                if (dim == 2)
+                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
+                                                                         work, nbr, acc, active, stats);
+                else
+                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
+                                                                         work, nbr, acc, active, stats);
+            }
+            launched(hg.ncls);
+        } else if (sweep_mode == 0) {
             FamScope fs(this, 1);
             SRM_CUDA(cudaMemsetAsync(qcursor, 0, sizeof(unsigned long long) * hg.ncls, stream));
             for (int cls = 0; cls < hg.ncls; ++cls) {

@@ -864,14 +864,22 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
                                            double* p) {
     propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
     const int32_t* row = nbr + q * kNearRow;
-    const int4 h0 = *reinterpret_cast<const int4*>(row);
+    const int2 h0 = *reinterpret_cast<const int2*>(row);
     const int nf = h0.x, nn = h0.x + h0.y;
     if (nn <= kNearCap) {
-        for (int t = 0; t < nn; ++t) {
-            const int32_t j = t == 0 ? (nf > 0 ? h0.z : row[kNearRow - 1]) : near_entry(row, nf, t);
-            const double4 v = S.rec[j];
-            const double xl[3] = {v.x, v.y, v.z};
-            if (sphere_overlap<D>(box, p, ri, xl, v.w)) return false;
+        // four neighbours at a time: all record loads issued before any test
+        for (int t0 = 0; t0 < nn; t0 += 4) {
+            double4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (t0 + u < nn) v[u] = S.rec[near_entry(row, nf, t0 + u)];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (t0 + u < nn) {
+                    const double xl[3] = {v[u].x, v[u].y, v[u].z};
+                    if (sphere_overlap<D>(box, p, ri, xl, v[u].w)) return false;
+                }
+            }
         }
         return true;
     }
@@ -978,6 +986,84 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_queue(i
         if (threadIdx.x == 0) qn[cur] = 0;
         cur = nxt;
         __syncthreads();
+    }
+}
+
+// The same class sweep with a queue per warp, kept in registers: each lane holds one
+// item (particle, next trial), every round runs one trial per item, the surviving items
+// are compacted to the low lanes with a ballot + shuffles, and the free lanes take fresh
+// cells from the warp's contiguous share of the class's bucket.  No barriers: warps
+// progress independently.  Same per-cell order and trials as k_sweep_queue.
+template <int D>
+__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls, State S, Box box,
+                                                                               const GridParams* __restrict__ gp,
+                                                                               const RoundParams* __restrict__ rpp,
+                                                                               const int64_t* __restrict__ cs,
+                                                                               const uint32_t* __restrict__ skey,
+                                                                               const uint32_t* __restrict__ bstart,
+                                                                               const int2* __restrict__ work,
+                                                                               const int32_t* __restrict__ nbr,
+                                                                               uint8_t* __restrict__ acc,
+                                                                               int32_t* __restrict__ active,
+                                                                               StatsDev* stats) {
+    const GridParams& g = *gp;
+    if (cls >= g.ncls) return;
+    const RoundParams rp = *rpp;
+    const int lane = threadIdx.x & 31;
+    const int64_t lo = bstart[cls * kRanks], cnt = bstart[cls * kRanks + 1] - lo;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int64_t next = cnt * w / nwarps;               // this warp's share [next, stop)
+    const int64_t stop = cnt * (w + 1) / nwarps;
+    int n = 0;                                      // live items in lanes [0, n)
+    int32_t iq = 0, il = 0, isl = 0, iend = 0;      // this lane's item
+    for (;;) {
+        const int64_t left = stop - next;
+        const int take = left < 32 - n ? static_cast<int>(left) : 32 - n;
+        if (take > 0) {
+            if (lane >= n && lane < n + take) {
+                const int2 wk = work[lo + next + (lane - n)];
+                iq = wk.x;
+                il = 0;
+                isl = wk.y;
+                iend = static_cast<int32_t>(cs[skey[wk.x] + 1]);
+            }
+            n += take;
+            next += take;
+        }
+        if (n == 0) break;
+        bool keep = false;
+        if (lane < n) {
+            const double4 me = S.rec[iq];  // round-start record (the particle has not moved)
+            double xi[D], p[D];
+            rec_pos<D>(me, xi);
+            const bool clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, p);
+            bool done = true;
+            if (clear) {
+                S.rec[iq] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
+                if (rp.write_acc) acc[iq] = static_cast<uint8_t>(il);
+            } else if (il + 1 < rp.n_l) {
+                ++il;
+                done = false;
+            } else {
+                if (rp.write_acc) acc[iq] = kNotAccepted;
+                active[atomicAdd(&stats->active_count, 1ull)] = iq;
+            }
+            if (done && iq + 1 < iend) {  // the next particle of the cell
+                iq += 1;
+                il = 0;
+                isl = S.slot[iq];
+                done = false;
+            }
+            keep = !done;
+        }
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        n = __popc(km);
+        const int src = lane < n ? static_cast<int>(__fns(km, 0, lane + 1)) : lane;
+        iq = __shfl_sync(0xffffffffu, iq, src);
+        il = __shfl_sync(0xffffffffu, il, src);
+        isl = __shfl_sync(0xffffffffu, isl, src);
+        iend = __shfl_sync(0xffffffffu, iend, src);
     }
 }
 
