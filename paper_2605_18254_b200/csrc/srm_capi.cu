@@ -74,7 +74,7 @@ struct srm_b200_ctx {
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
-    int2* work = nullptr;        // (colour class, rank) work lists of the sweep: (index, slot)
+    int4* work = nullptr;        // (colour class, rank) work lists: (index, slot, cell end, 0)
     uint32_t* bcount = nullptr;  // bucket counts / starts / cursors, [ncls * kRanks + 1]
     uint32_t* bstart = nullptr;
     uint32_t* bcursor = nullptr;
@@ -209,7 +209,7 @@ struct srm_b200_ctx {
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearRow);
-        work = dalloc<int2>(cap);
+        work = dalloc<int4>(cap);
         const int work_smem = 2 * kBucketSmem * 4;
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
@@ -430,19 +430,24 @@ struct srm_b200_ctx {
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
         if (write_acc) SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
-            FamScope fs(this, 2);  // near lists + (class, rank) work lists
-            const int nbk = hg.ncls * kRanks;
-            const bool local = nbk <= kBucketSmem;
-            const int wb = blocks_for(n, kWorkBlock * kWorkPer);
-            if (dim == 2)
-                k_work_count<2><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
-            else
-                k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
-            k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
-            if (dim == 2)
-                k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot, bcursor, work);
-            else
-                k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot, bcursor, work);
+            FamScope fs(this, 2);  // near lists (+ the (class, rank) work lists of sweep modes 0/1)
+            if (sweep_mode != 2) {  // the warp-queue sweep walks the class lattice itself
+                const int nbk = hg.ncls * kRanks;
+                const bool local = nbk <= kBucketSmem;
+                const int wb = blocks_for(n, kWorkBlock * kWorkPer);
+                if (dim == 2)
+                    k_work_count<2><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
+                else
+                    k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
+                k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
+                if (dim == 2)
+                    k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot,
+                                                                                           bcursor, work);
+                else
+                    k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot,
+                                                                                           bcursor, work);
+                launched(3);
+            }
             const int nb = blocks_for(n, 256);
             bool half = near_mode == 0;
             for (int a = 0; a < dim; ++a) half = half && hg.near_s[a] >= 0;
@@ -450,11 +455,11 @@ struct srm_b200_ctx {
                 k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
                 if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                launched(5);
+                launched(2);
             } else {
                 if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                launched(4);
+                launched(1);
             }
         }
         if (sweep_mode == 2) {
@@ -464,11 +469,11 @@ struct srm_b200_ctx {
                 // about 64 cells per warp, at most one wave of resident CTAs
                 const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads * 2), queue_ctas)));
                 if (dim == 2)
-                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
-                                                                         work, nbr, acc, active, stats);
+                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, nbr, acc,
+                                                                         active, stats);
                 else
-                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
-                                                                         work, nbr, acc, active, stats);
+                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, nbr, acc,
+                                                                         active, stats);
             }
             launched(hg.ncls);
         } else if (sweep_mode == 0) {

@@ -691,12 +691,18 @@ __global__ void k_work_scan(const GridParams* __restrict__ gp, uint32_t* __restr
     if (threadIdx.x == 0) bstart[nb] = carry;
 }
 
+// work item: (sorted index, storage slot, end of its cell, 0) -- one 16-byte load
+__device__ __forceinline__ int4 work_item(int64_t q, const int32_t* __restrict__ slot, const int64_t* __restrict__ cs,
+                                          const uint32_t* __restrict__ skey) {
+    return make_int4(static_cast<int32_t>(q), slot[q], static_cast<int32_t>(cs[skey[q] + 1]), 0);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const GridParams* __restrict__ gp,
                                                              const int64_t* __restrict__ cs,
                                                              const uint32_t* __restrict__ skey,
                                                              const int32_t* __restrict__ slot,
-                                                             uint32_t* __restrict__ cursor, int2* __restrict__ work) {
+                                                             uint32_t* __restrict__ cursor, int4* __restrict__ work) {
     extern __shared__ uint32_t hist[];  // [nb] counts, then [nb] CTA bases
     const GridParams& g = *gp;
     const int nb = g.ncls * kRanks;
@@ -716,7 +722,7 @@ __global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const Gr
         myb[k] = bucket_of<D>(g, cs, skey[q], q);
         if (myb[k] < 0) continue;
         if (local) myl[k] = atomicAdd(&hist[myb[k]], 1u);
-        else work[atomicAdd(&cursor[myb[k]], 1u)] = make_int2(static_cast<int32_t>(q), slot[q]);
+        else work[atomicAdd(&cursor[myb[k]], 1u)] = work_item(q, slot, cs, skey);
     }
     if (!local) return;
     __syncthreads();
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const Gr
     for (int k = 0; k < kWorkPer; ++k) {
         if (myb[k] < 0) continue;
         const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        work[base[myb[k]] + myl[k]] = make_int2(static_cast<int32_t>(q), slot[q]);
+        work[base[myb[k]] + myl[k]] = work_item(q, slot, cs, skey);
     }
 }
 
@@ -815,7 +821,7 @@ __device__ __forceinline__ void sweep_particle(int64_t q, int32_t sl, const Stat
 #define SRM_SWEEP_THREADS 128
 #endif
 #ifndef SRM_SWEEP_MINB
-#define SRM_SWEEP_MINB 8
+#define SRM_SWEEP_MINB 6
 #endif
 constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
@@ -831,7 +837,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_work(in
                                                               const int64_t* __restrict__ cs,
                                                               const uint32_t* __restrict__ skey,
                                                               const uint32_t* __restrict__ bstart,
-                                                              const int2* __restrict__ work,
+                                                              const int4* __restrict__ work,
                                                               const int32_t* __restrict__ nbr,
                                                               uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                               StatsDev* stats) {
@@ -839,15 +845,14 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_work(in
     if (cls >= g.ncls) return;
     const int64_t lo = bstart[cls * kRanks + rank];
     const int64_t cnt = bstart[cls * kRanks + rank + 1] - lo;
-    const int2* list = work + lo;
+    const int4* list = work + lo;
     const RoundParams rp = *rpp;
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < cnt;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int2 w = list[t];  // (sorted index, storage slot)
+        const int4 w = list[t];  // (sorted index, storage slot, cell end)
         sweep_particle<D>(w.x, w.y, S, box, g, rp, cs, skey, nbr, acc, active, stats);
         if (rank == kRanks - 1) {  // the rest of a crowded cell, in slot order
-            const int64_t e = cs[skey[w.x] + 1];
-            for (int64_t q = w.x + 1; q < e; ++q)
+            for (int64_t q = w.x + 1; q < w.z; ++q)
                 sweep_particle<D>(q, S.slot[q], S, box, g, rp, cs, skey, nbr, acc, active, stats);
         }
     }
@@ -914,7 +919,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_queue(i
                                                                                const int64_t* __restrict__ cs,
                                                                                const uint32_t* __restrict__ skey,
                                                                                const uint32_t* __restrict__ bstart,
-                                                                               const int2* __restrict__ work,
+                                                                               const int4* __restrict__ work,
                                                                                unsigned long long* __restrict__ cursor,
                                                                                const int32_t* __restrict__ nbr,
                                                                                uint8_t* __restrict__ acc,
@@ -948,8 +953,8 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_queue(i
         }
         __syncthreads();
         if (static_cast<int>(threadIdx.x) < take_n) {
-            const int2 w = work[lo + take_base + threadIdx.x];
-            qbuf[cur][qn[cur] + threadIdx.x] = QItem{w.x, 0, w.y, static_cast<int32_t>(cs[skey[w.x] + 1])};
+            const int4 w = work[lo + take_base + threadIdx.x];
+            qbuf[cur][qn[cur] + threadIdx.x] = QItem{w.x, 0, w.y, w.z};
         }
         __syncthreads();
         if (threadIdx.x == 0) qn[cur] += take_n;
@@ -994,14 +999,40 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_queue(i
 // are compacted to the low lanes with a ballot + shuffles, and the free lanes take fresh
 // cells from the warp's contiguous share of the class's bucket.  No barriers: warps
 // progress independently.  Same per-cell order and trials as k_sweep_queue.
+// The cells of colour class cls form a lattice per axis: first + stride * i, i < cnt
+// (colour1 inverted: a body colour v < m is x = v + m i, a remainder colour one cell).
+__device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int* first, int* stride, int* cnt) {
+    int rem = cls;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int m = g.col_m[a];
+        const int v = rem % g.col_n[a];
+        rem /= g.col_n[a];
+        if (v < m) {
+            first[a] = v;
+            stride[a] = m;
+            cnt[a] = g.col_body[a] / m;
+        } else {
+            first[a] = g.col_body[a] + (v - m);
+            stride[a] = 1;
+            cnt[a] = 1;
+        }
+    }
+}
+
+// The class sweep with a queue per warp, kept in registers: each lane holds one item
+// (particle, next trial, its cell's end), every round runs one trial per item, the
+// surviving items are compacted to the low lanes with a ballot + shuffles, and the free
+// lanes take the next cells of the warp's contiguous share of the class lattice (empty
+// cells are skipped, a done particle hands its cell on to the next one in slot order).
+// No barriers and no work lists: warps progress independently.  Per cell the visiting
+// order and the trials are those of the sequential sweep (orc_sweep_round).
 template <int D>
 __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls, State S, Box box,
                                                                                const GridParams* __restrict__ gp,
                                                                                const RoundParams* __restrict__ rpp,
                                                                                const int64_t* __restrict__ cs,
                                                                                const uint32_t* __restrict__ skey,
-                                                                               const uint32_t* __restrict__ bstart,
-                                                                               const int2* __restrict__ work,
                                                                                const int32_t* __restrict__ nbr,
                                                                                uint8_t* __restrict__ acc,
                                                                                int32_t* __restrict__ active,
@@ -1010,27 +1041,72 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
     if (cls >= g.ncls) return;
     const RoundParams rp = *rpp;
     const int lane = threadIdx.x & 31;
-    const int64_t lo = bstart[cls * kRanks], cnt = bstart[cls * kRanks + 1] - lo;
+    int first[3], stride[3], cnt[3];
+    class_lattice(g, cls, first, stride, cnt);
+    const int64_t cells = static_cast<int64_t>(cnt[0]) * cnt[1] * cnt[2];
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    int64_t next = cnt * w / nwarps;               // this warp's share [next, stop)
-    const int64_t stop = cnt * (w + 1) / nwarps;
-    int n = 0;                                      // live items in lanes [0, n)
-    int32_t iq = 0, il = 0, isl = 0, iend = 0;      // this lane's item
-    for (;;) {
-        const int64_t left = stop - next;
-        const int take = left < 32 - n ? static_cast<int>(left) : 32 - n;
-        if (take > 0) {
-            if (lane >= n && lane < n + take) {
-                const int2 wk = work[lo + next + (lane - n)];
-                iq = wk.x;
-                il = 0;
-                isl = wk.y;
-                iend = static_cast<int32_t>(cs[skey[wk.x] + 1]);
-            }
-            n += take;
-            next += take;
+    int64_t next = cells * w / nwarps;  // this warp's share of the lattice [next, stop)
+    const int64_t stop = cells * (w + 1) / nwarps;
+    int n = 0;  // live items in lanes [0, n)
+    int32_t iq = 0, il = 0, isl = 0, iend = 0;
+    // look-ahead window of 32 lattice cells: (wb, we) = cell range; loaded one round
+    // ahead of its use so the cell_start loads overlap the trials in flight
+    int wn = 0;
+    bool wraw = false;
+    int64_t wb = 0, we = 0;
+    const int64_t cxy = static_cast<int64_t>(cnt[0]) * cnt[1];
+    auto load_window = [&]() {
+        const int64_t t = next + lane;
+        wb = 0;
+        we = 0;
+        if (t < stop) {
+            const int iz = static_cast<int>(t / cxy);
+            const int64_t r2 = t - iz * cxy;
+            const int iy = static_cast<int>(r2 / cnt[0]), ix = static_cast<int>(r2 - static_cast<int64_t>(iy) * cnt[0]);
+            const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
+                                     g.dims[0] + first[0] + stride[0] * ix;
+            wb = cs[cell];
+            we = cs[cell + 1];
         }
+        const int64_t left = stop - next;
+        next += left < 32 ? left : 32;
+        wraw = true;
+    };
+    load_window();
+    for (;;) {
+        while (n < 32) {  // free lanes take the next non-empty cells of the window
+            if (wraw) {
+                const unsigned gm = __ballot_sync(0xffffffffu, wb < we);
+                wn = __popc(gm);
+                const int src = lane < wn ? static_cast<int>(__fns(gm, 0, lane + 1)) : lane;
+                wb = __shfl_sync(0xffffffffu, wb, src);
+                we = __shfl_sync(0xffffffffu, we, src);
+                wraw = false;
+            }
+            if (wn == 0) {
+                if (next >= stop) break;
+                load_window();
+                continue;
+            }
+            const int take = wn < 32 - n ? wn : 32 - n;
+            const int k = lane - n;
+            const bool mine = k >= 0 && k < take;
+            const int64_t tb = __shfl_sync(0xffffffffu, wb, mine ? k : lane);
+            const int64_t te = __shfl_sync(0xffffffffu, we, mine ? k : lane);
+            if (mine) {
+                iq = static_cast<int32_t>(tb);
+                iend = static_cast<int32_t>(te);
+                il = 0;
+                isl = S.slot[tb];
+            }
+            const int sh = lane + take < 32 ? lane + take : lane;
+            wb = __shfl_sync(0xffffffffu, wb, sh);
+            we = __shfl_sync(0xffffffffu, we, sh);
+            wn -= take;
+            n += take;
+        }
+        if (wn == 0 && !wraw && next < stop) load_window();  // consumed next round
         if (n == 0) break;
         bool keep = false;
         if (lane < n) {
