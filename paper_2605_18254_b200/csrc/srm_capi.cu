@@ -83,7 +83,9 @@ struct srm_b200_ctx {
     int64_t qcursor_cap = 0;
     int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_queue (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
-    int near_mode = std::getenv("SRM_B200_NEAR_THREAD") ? 1 : 0;  // 0: half-stencil pairs, 1: full stencil
+    // 0: shared-memory bricks (3D) / half-stencil pairs, 1: full stencil per particle,
+    // 2: half-stencil pairs per particle
+    int near_mode = std::getenv("SRM_B200_NEAR") ? std::atoi(std::getenv("SRM_B200_NEAR")) : 0;
     // 2: warp queues (default), 0: CTA work queue, 1: (class, rank) launches
     int sweep_mode = std::getenv("SRM_B200_SWEEP") ? std::atoi(std::getenv("SRM_B200_SWEEP")) : 2;
     uint8_t* acc = nullptr;
@@ -213,6 +215,7 @@ struct srm_b200_ctx {
         const int work_smem = 2 * kBucketSmem * 4;
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
         SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
+        SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
         {
             int per_sm = 0, sms = 0;
             SRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_queue<3>, kSweepThreads, 0));
@@ -449,9 +452,16 @@ struct srm_b200_ctx {
                 launched(3);
             }
             const int nb = blocks_for(n, 256);
-            bool half = near_mode == 0;
+            bool half = near_mode != 1;
             for (int a = 0; a < dim; ++a) half = half && hg.near_s[a] >= 0;
-            if (half) {  // pairs once, appended to both lists
+            const bool tiles = half && dim == 3 && near_mode == 0 && hg.near_s[0] == 1 && hg.near_s[1] == 1 &&
+                               hg.near_s[2] == 1 && hg.dims[0] >= kTX + 2 && hg.dims[1] >= kTY + 2 && hg.dims[2] >= kTZ + 1;
+            if (tiles) {  // pairs once, through shared-memory bricks
+                k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
+                const int ntiles = ((hg.dims[0] + kTX - 1) / kTX) * ((hg.dims[1] + kTY - 1) / kTY) * ((hg.dims[2] + kTZ - 1) / kTZ);
+                k_near_tiles<<<ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
+                launched(2);
+            } else if (half) {  // pairs once, appended to both lists
                 k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
                 if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);

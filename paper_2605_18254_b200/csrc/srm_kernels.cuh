@@ -501,98 +501,284 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
 // keeps near_candidates' cutoff, margin and factor, so the lists hold the same pairs as
 // k_near_lists, in another order (which the sweep does not observe).  Requires every
 // near_s >= 0 (no axis scanned whole); k_near_lists covers the other grids.
+// Publish q's forward list: its count, and q into the backward part of every forward
+// neighbour's row (two independent atomics in flight at a time).
+__device__ __forceinline__ void near_publish(int32_t* __restrict__ nbr, int64_t q, int nf, const int32_t* fwd) {
+    int32_t* myrow = nbr + q * kNearRow;
+    myrow[0] = nf;
+    const int m = nf < kNearCap ? nf : kNearCap;
+    for (int t0 = 0; t0 < m; t0 += 2) {  // two atomics in flight at a time
+        const int64_t ja = fwd[t0];
+        const int64_t jb = t0 + 1 < m ? fwd[t0 + 1] : -1;
+        const int ka = atomicAdd(&nbr[ja * kNearRow + 1], 1);
+        const int kb = jb >= 0 ? atomicAdd(&nbr[jb * kNearRow + 1], 1) : kNearCap;
+        if (ka < kNearCap) nbr[ja * kNearRow + kNearRow - 1 - ka] = static_cast<int32_t>(q);
+        if (kb < kNearCap) nbr[jb * kNearRow + kNearRow - 1 - kb] = static_cast<int32_t>(q);
+    }
+}
+
+// k_near_half for one particle q (global memory throughout).
+template <int D>
+__device__ __forceinline__ void near_half_particle(int64_t q, const State& S, const GridParams& g,
+                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                   int32_t* __restrict__ nbr) {
+    const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
+    const int sx = g.near_s[0], sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
+    const float4 me = S.xf[q];
+    const int32_t idq = S.id[q];
+    const uint32_t key = skey[q];
+    int cc_[3];
+    decode_key<D>(g, key, cc_);
+    const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
+    const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
+    const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
+    const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
+    // screen [b, e) against me shifted by (ox, oy, oz); keep the hits (q's forward list)
+    int32_t* myrow = nbr + q * kNearRow;
+    int nf = 0;
+    int32_t fwd[kNearCap];  // the forward list, also kept thread-locally for near_publish
+    auto run = [&](int64_t b, int64_t e, float ox, float oy, float oz) {
+        for (int64_t j = b; j < e; ++j) {
+            const float4 c = S.xf[j];
+            const float ex = __fsub_rn(c.x, ox), ey = __fsub_rn(c.y, oy);
+            const float ez = D == 3 ? __fsub_rn(c.z, oz) : 0.f;
+            const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+            const float lim = __fadd_rn(base, c.w);
+            if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f)) continue;
+            if (S.id[j] == idq) continue;  // shape.hpp:544 self-exclusion by id
+            if (nf < kNearCap) {
+                myrow[2 + nf] = static_cast<int32_t>(j);
+                fwd[nf] = static_cast<int32_t>(j);
+            }
+            ++nf;
+        }
+    };
+    const int zhi = D == 3 ? cz + sz : 0;
+    for (int zz = cz; zz <= zhi; ++zz) {
+        float dzd = 0.f, oz = me.z;
+        if (D == 3) {
+            const float zb = zz * g.edge_f[2];
+            dzd = fmaxf(0.f, fmaxf(zb - me.z, me.z - (zb + g.edge_f[2])));
+        }
+        int z = zz;
+        if (D == 3 && z >= dz) {  // image above the box: candidates sit at z - L
+            z -= dz;
+            oz = __fsub_rn(me.z, g.L_f[2]);
+        }
+        const int ylo = zz == cz ? cy : cy - sy;
+        for (int yy = ylo; yy <= cy + sy; ++yy) {
+            const float yb = yy * g.edge_f[1];
+            const float dyd = fmaxf(0.f, fmaxf(yb - me.y, me.y - (yb + g.edge_f[1])));
+            const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
+            if (dyz2 > cut2) continue;
+            int y = yy;
+            float oy = me.y;
+            if (y < 0) {
+                y += dy;
+                oy = __fadd_rn(me.y, g.L_f[1]);
+            } else if (y >= dy) {
+                y -= dy;
+                oy = __fsub_rn(me.y, g.L_f[1]);
+            }
+            const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
+            const bool own = zz == cz && yy == cy;
+            const int xl = own ? cx : cx - sx, xr = cx + sx;
+            // cells [xl, xr] of the unwrapped row: up to three pieces (below 0, inside, above dx)
+            const int64_t first = own ? q + 1 : -1;  // own cell: only the particles after q
+            if (xl < 0) {
+                const int e = min(xr, -1);
+                run(cs[row + xl + dx], cs[row + e + 1 + dx], __fadd_rn(me.x, g.L_f[0]), oy, oz);
+            }
+            if (xr >= 0 && xl < dx) {
+                const int b = max(xl, 0), e = min(xr, dx - 1);
+                const int64_t bb = first >= 0 && b == cx ? first : cs[row + b];
+                run(bb, cs[row + e + 1], me.x, oy, oz);
+            }
+            if (xr >= dx) {
+                const int b = max(xl, dx);
+                run(cs[row + b - dx], cs[row + xr - dx + 1], __fsub_rn(me.x, g.L_f[0]), oy, oz);
+            }
+        }
+    }
+    near_publish(nbr, q, nf, fwd);
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const GridParams* __restrict__ gp,
                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                    int32_t* __restrict__ nbr) {
     const GridParams& g = *gp;
-    const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
-    const int sx = g.near_s[0], sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        const float4 me = S.xf[q];
-        const int32_t idq = S.id[q];
-        const uint32_t key = skey[q];
-        int cc_[3];
-        decode_key<D>(g, key, cc_);
-        const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
-        const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
-        const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        near_half_particle<D>(q, S, g, cs, skey, nbr);
+}
+
+// The same pairs, tiled through shared memory (3D, a one-cell stencil on every axis).
+// A CTA takes a brick of kTX x kTY x kTZ cells, stages the fp32 records, ids and sorted
+// indices of the brick and its half-stencil halo (x +-1, y +-1, z +1) in shared
+// memory -- periodic images shifted by +-L on the way in, so pair distances are plain
+// differences -- and screens every interior particle against its half stencil there:
+// five contiguous shared ranges (own cell after i + next cell, the dy=+1 row, the three
+// dz=+1 rows).  Same screen, same pairs as k_near_half; a brick whose halo holds more
+// than kTileCap particles falls back to near_half_particle.
+constexpr int kTX = 16, kTY = 8, kTZ = 4;
+constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 1;
+constexpr int kHCells = kHX * kHY * kHZ;
+constexpr int kTileCap = 1792;
+constexpr int kTileThreads = 256;
+constexpr size_t kTileSmem = kTileCap * (16 + 4 + 4 + 2) + (kHCells + 2) * 4 + kHCells * 8;
+
+__global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const GridParams* __restrict__ gp,
+                                                             const int64_t* __restrict__ cs,
+                                                             const uint32_t* __restrict__ skey,
+                                                             int32_t* __restrict__ nbr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4* px = reinterpret_cast<float4*>(smem_raw);                       // [kTileCap]
+    int32_t* pj = reinterpret_cast<int32_t*>(px + kTileCap);                // [kTileCap] sorted index
+    int32_t* pid = pj + kTileCap;                                           // [kTileCap] reference id
+    uint16_t* phc = reinterpret_cast<uint16_t*>(pid + kTileCap);            // [kTileCap] halo cell
+    int32_t* hoff = reinterpret_cast<int32_t*>(phc + kTileCap);             // [kHCells + 1]
+    int64_t* hsrc = reinterpret_cast<int64_t*>(hoff + kHCells + 2);         // [kHCells] global first index
+    __shared__ int wsum[kTileThreads / 32];
+    __shared__ int rowoff[kTY * kTZ + 1];
+    const GridParams& g = *gp;
+    const int dx = g.dims[0], dy = g.dims[1], dz = g.dims[2];
+    const int ntx = (dx + kTX - 1) / kTX, nty = (dy + kTY - 1) / kTY;
+    const int tx = blockIdx.x % ntx, ty = (blockIdx.x / ntx) % nty, tz = blockIdx.x / (ntx * nty);
+    const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;
+    const int wx = min(kTX, dx - x0), wy = min(kTY, dy - y0), wz = min(kTZ, dz - z0);  // interior extent
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // 1. counts of the halo cells (cells outside the needed halo of a partial brick: 0)
+    int cnts[(kHCells + kTileThreads - 1) / kTileThreads];
+    int local = 0;
+#pragma unroll
+    for (int k = 0; k < (kHCells + kTileThreads - 1) / kTileThreads; ++k) {
+        const int hc = threadIdx.x * ((kHCells + kTileThreads - 1) / kTileThreads) + k;
+        int c = 0;
+        if (hc < kHCells) {
+            const int hx = hc % kHX, hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
+            if (hx <= wx + 1 && hy <= wy + 1 && hz <= wz) {
+                int X = x0 - 1 + hx, Y = y0 - 1 + hy, Z = z0 + hz;
+                X = X < 0 ? X + dx : (X >= dx ? X - dx : X);
+                Y = Y < 0 ? Y + dy : (Y >= dy ? Y - dy : Y);
+                Z = Z >= dz ? Z - dz : Z;
+                const int64_t cell = (static_cast<int64_t>(Z) * dy + Y) * dx + X;
+                const int64_t b = cs[cell];
+                c = static_cast<int>(cs[cell + 1] - b);
+                hsrc[hc] = b;
+            }
+        }
+        cnts[k] = c;
+        local += c;
+    }
+    // 2. exclusive scan over the halo cells (thread-contiguous chunks)
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int wbase = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kTileThreads / 32; ++w) {
+        if (w < wid) wbase += wsum[w];
+        total += wsum[w];
+    }
+    {
+        int off = wbase + incl - local;
+#pragma unroll
+        for (int k = 0; k < (kHCells + kTileThreads - 1) / kTileThreads; ++k) {
+            const int hc = threadIdx.x * ((kHCells + kTileThreads - 1) / kTileThreads) + k;
+            if (hc < kHCells) hoff[hc] = off;
+            off += cnts[k];
+        }
+        if (threadIdx.x == 0) hoff[kHCells] = total;
+    }
+    __syncthreads();
+    if (total > kTileCap) {  // crowded brick: the per-particle path over global memory
+        for (int r = 0; r < wy * wz; ++r) {
+            const int Y = y0 + r % wy, Z = z0 + r / wy;
+            const int64_t row = (static_cast<int64_t>(Z) * dy + Y) * dx;
+            const int64_t b = cs[row + x0], e = cs[row + x0 + wx];
+            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) near_half_particle<3>(q, S, g, cs, skey, nbr);
+        }
+        return;
+    }
+    // 3. stage the halo: a thread per halo cell copies its particles, shifted into the
+    //    brick's unwrapped frame
+    for (int hc = threadIdx.x; hc < kHCells; hc += blockDim.x) {
+        const int c = hoff[hc + 1] - hoff[hc];
+        if (c == 0) continue;
+        const int hx = hc % kHX, hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
+        const int X = x0 - 1 + hx, Y = y0 - 1 + hy, Z = z0 + hz;
+        const float sxf = X < 0 ? -g.L_f[0] : (X >= dx ? g.L_f[0] : 0.f);
+        const float syf = Y < 0 ? -g.L_f[1] : (Y >= dy ? g.L_f[1] : 0.f);
+        const float szf = Z >= dz ? g.L_f[2] : 0.f;
+        const int64_t b = hsrc[hc];
+        const int o = hoff[hc];
+        for (int k = 0; k < c; ++k) {
+            float4 v = S.xf[b + k];
+            v.x = __fadd_rn(v.x, sxf);
+            v.y = __fadd_rn(v.y, syf);
+            v.z = __fadd_rn(v.z, szf);
+            px[o + k] = v;
+            pj[o + k] = static_cast<int32_t>(b + k);
+            pid[o + k] = S.id[b + k];
+            phc[o + k] = static_cast<uint16_t>(hc);
+        }
+    }
+    // interior rows (hy in [1, wy], hz in [0, wz)): their particles are contiguous
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int r = 0; r < wy * wz; ++r) {
+            rowoff[r] = acc;
+            const int hy = 1 + r % wy, hz = r / wy;
+            const int h0 = (hz * kHY + hy) * kHX + 1;
+            acc += hoff[h0 + wx] - hoff[h0];
+        }
+        rowoff[wy * wz] = acc;
+    }
+    __syncthreads();
+    // 4. screen every interior particle against its half stencil in shared memory
+    const int nint = rowoff[wy * wz];
+    for (int f = threadIdx.x; f < nint; f += blockDim.x) {
+        int r = 0;  // the last interior row whose offset is <= f
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+            if (r + step < wy * wz && rowoff[r + step] <= f) r += step;
+        const int hy = 1 + r % wy, hz = r / wy;
+        const int i = hoff[(hz * kHY + hy) * kHX + 1] + (f - rowoff[r]);
+        const int hc = phc[i];
+        const float4 me = px[i];
+        const int32_t idi = pid[i];
         const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
-        // screen [b, e) against me shifted by (ox, oy, oz); keep the hits (q's forward list)
+        const int64_t q = pj[i];
         int32_t* myrow = nbr + q * kNearRow;
         int nf = 0;
-        auto run = [&](int64_t b, int64_t e, float ox, float oy, float oz) {
-            for (int64_t j = b; j < e; ++j) {
-                const float4 c = S.xf[j];
-                const float ex = __fsub_rn(c.x, ox), ey = __fsub_rn(c.y, oy);
-                const float ez = D == 3 ? __fsub_rn(c.z, oz) : 0.f;
+        int32_t fwd[kNearCap];
+        auto run = [&](int b, int e) {
+            for (int k = b; k < e; ++k) {
+                const float4 c = px[k];
+                const float ex = __fsub_rn(c.x, me.x), ey = __fsub_rn(c.y, me.y), ez = __fsub_rn(c.z, me.z);
                 const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
                 const float lim = __fadd_rn(base, c.w);
                 if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f)) continue;
-                if (S.id[j] == idq) continue;  // shape.hpp:544 self-exclusion by id
-                if (nf < kNearCap) myrow[2 + nf] = static_cast<int32_t>(j);
+                if (pid[k] == idi) continue;  // shape.hpp:544 self-exclusion by id
+                if (nf < kNearCap) {
+                    myrow[2 + nf] = pj[k];
+                    fwd[nf] = pj[k];
+                }
                 ++nf;
             }
         };
-        const int zhi = D == 3 ? cz + sz : 0;
-        for (int zz = cz; zz <= zhi; ++zz) {
-            float dzd = 0.f, oz = me.z;
-            if (D == 3) {
-                const float zb = zz * g.edge_f[2];
-                dzd = fmaxf(0.f, fmaxf(zb - me.z, me.z - (zb + g.edge_f[2])));
-            }
-            int z = zz;
-            if (D == 3 && z >= dz) {  // image above the box: candidates sit at z - L
-                z -= dz;
-                oz = __fsub_rn(me.z, g.L_f[2]);
-            }
-            const int ylo = zz == cz ? cy : cy - sy;
-            for (int yy = ylo; yy <= cy + sy; ++yy) {
-                const float yb = yy * g.edge_f[1];
-                const float dyd = fmaxf(0.f, fmaxf(yb - me.y, me.y - (yb + g.edge_f[1])));
-                const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
-                if (dyz2 > cut2) continue;
-                int y = yy;
-                float oy = me.y;
-                if (y < 0) {
-                    y += dy;
-                    oy = __fadd_rn(me.y, g.L_f[1]);
-                } else if (y >= dy) {
-                    y -= dy;
-                    oy = __fsub_rn(me.y, g.L_f[1]);
-                }
-                const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
-                const bool own = zz == cz && yy == cy;
-                const int xl = own ? cx : cx - sx, xr = cx + sx;
-                // cells [xl, xr] of the unwrapped row: up to three pieces (below 0, inside, above dx)
-                const int64_t first = own ? q + 1 : -1;  // own cell: only the particles after q
-                if (xl < 0) {
-                    const int e = min(xr, -1);
-                    run(cs[row + xl + dx], cs[row + e + 1 + dx], __fadd_rn(me.x, g.L_f[0]), oy, oz);
-                }
-                if (xr >= 0 && xl < dx) {
-                    const int b = max(xl, 0), e = min(xr, dx - 1);
-                    const int64_t bb = first >= 0 && b == cx ? first : cs[row + b];
-                    run(bb, cs[row + e + 1], me.x, oy, oz);
-                }
-                if (xr >= dx) {
-                    const int b = max(xl, dx);
-                    run(cs[row + b - dx], cs[row + xr - dx + 1], __fsub_rn(me.x, g.L_f[0]), oy, oz);
-                }
-            }
-        }
-        myrow[0] = nf;
-        // q into the backward part of every forward neighbour's row: the atomics are
-        // independent, so they are issued back to back before any result is used
-        const int m = nf < kNearCap ? nf : kNearCap;
-        int kk[kNearCap];
-#pragma unroll
-        for (int t = 0; t < kNearCap; ++t)
-            if (t < m) kk[t] = atomicAdd(&nbr[static_cast<int64_t>(myrow[2 + t]) * kNearRow + 1], 1);
-#pragma unroll
-        for (int t = 0; t < kNearCap; ++t)
-            if (t < m && kk[t] < kNearCap)
-                nbr[static_cast<int64_t>(myrow[2 + t]) * kNearRow + kNearRow - 1 - kk[t]] = static_cast<int32_t>(q);
+        run(i + 1, hoff[hc + 2]);                                   // own cell after i, then cell x+1
+        run(hoff[hc + kHX - 1], hoff[hc + kHX + 2]);                // dy = +1, dx = -1..+1
+        const int up = hc + kHX * kHY;                              // dz = +1
+        run(hoff[up - kHX - 1], hoff[up - kHX + 2]);
+        run(hoff[up - 1], hoff[up + 2]);
+        run(hoff[up + kHX - 1], hoff[up + kHX + 2]);
+        near_publish(nbr, q, nf, fwd);
     }
 }
 
