@@ -17,7 +17,8 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STEP = ("k_near_lists", "k_sweep_cells")
+STEP = ("k_near_lists", "k_near_half", "k_near_tiles", "k_near_zero", "k_sweep_cells", "k_sweep_work", "k_sweep_queue",
+        "k_sweep_warpq", "k_work_count", "k_work_scan", "k_work_scatter")
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "usecond": 1.0,
         "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}
 
