@@ -117,6 +117,13 @@ int srm_b200_generate(srm_b200_ctx* ctx, const srm_b200_params* params,
                       int64_t iteration_count_in, srm_b200_progress_fn progress, void* user,
                       srm_b200_generate_out* out);
 
+/* srm_b200_generate's loop: device_loop != 0 (default) runs the whole run as one CUDA
+ * graph whose controller kernels take every per-iteration decision on the device (no
+ * host round-trip per iteration; progress records are delivered after the run);
+ * device_loop == 0 drives the same kernels from the host, reading the round statistics
+ * after every round (progress delivered live).  Both follow engine.hpp:176-260. */
+int srm_b200_set_generate_mode(srm_b200_ctx* ctx, int device_loop);
+
 /* engine.hpp:112-122 relax_sweeps (and shake, engine.hpp:126-130, with sweeps = n_k):
  * `sweeps` x (rebuild grid sized 2.5*maxR + c_m, migrate).  The Rng& of the reference
  * signature becomes a 64-bit Philox key (the shim draws it with rng.raw()). */

@@ -341,6 +341,10 @@ class Context:
         return {"nonmovers": v[0], "colour_classes": v[1], "cells_per_class": v[2], "near_half_width": v[3],
                 "colour_modulus": v[4], "cells": v[5]}
 
+    def set_generate_mode(self, device_loop: bool) -> None:
+        """generate(): one device-resident CUDA graph (True, default) or the host-driven loop"""
+        self._c(_native.lib().srm_b200_set_generate_mode(self._h, 1 if device_loop else 0))
+
     def stopwatch_start(self) -> None:
         """record a CUDA event on the context stream"""
         self._c(_native.lib().srm_b200_stopwatch(self._h, 0, None))

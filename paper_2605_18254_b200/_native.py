@@ -100,6 +100,7 @@ _SIGS = {
     "srm_b200_sync": (C.c_int, [C.c_void_p]),
     "srm_b200_stopwatch": (C.c_int, [C.c_void_p, C.c_int, c_double_p]),
     "srm_b200_last_round_info": (C.c_int, [C.c_void_p, c_int64_p]),
+    "srm_b200_set_generate_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "srm_b200_selftest_philox": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "srm_b200_selftest_unit_vectors": (C.c_int, [C.c_int, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p,
                                                  C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),

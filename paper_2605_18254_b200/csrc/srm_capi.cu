@@ -86,6 +86,8 @@ struct srm_b200_ctx {
     // 0: shared-memory bricks (3D) / half-stencil pairs, 1: full stencil per particle,
     // 2: half-stencil pairs per particle
     int near_mode = std::getenv("SRM_B200_NEAR") ? std::atoi(std::getenv("SRM_B200_NEAR")) : 0;
+    // srm_generate: the device-resident graph loop (default) or the host-driven loop
+    bool device_loop = std::getenv("SRM_B200_HOST_LOOP") == nullptr;
     // 2: warp queues (default), 0: CTA work queue, 1: (class, rank) launches
     int sweep_mode = std::getenv("SRM_B200_SWEEP") ? std::atoi(std::getenv("SRM_B200_SWEEP")) : 2;
     uint8_t* acc = nullptr;
@@ -112,6 +114,7 @@ struct srm_b200_ctx {
     int64_t launches = 0;
 
     bool timing = false;
+    bool capturing = false;  // inside a graph capture: no timing events, no host syncs
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     struct Pending {
@@ -142,7 +145,7 @@ struct srm_b200_ctx {
         int fam;
         cudaEvent_t a = nullptr;
         FamScope(srm_b200_ctx* c_, int f) : c(c_), fam(f) {
-            if (c->timing) {
+            if (c->timing && !c->capturing) {
                 a = c->take_event();
                 SRM_CUDA(cudaEventRecord(a, c->stream));
             }
@@ -247,6 +250,10 @@ struct srm_b200_ctx {
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (sw_start) cudaEventDestroy(sw_start);
         if (sw_stop) cudaEventDestroy(sw_stop);
+        cudaFree(d_ctl);
+        cudaFree(d_recs);
+        for (auto st : cap_streams)
+            if (st) cudaStreamDestroy(st);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -255,78 +262,14 @@ struct srm_b200_ctx {
     // for a state whose largest radius is max_r_state and whose trial
     // moves have length c_m.  The colouring expression is the oracle's orc_colouring.
     GridParams make_grid(double cell_size, double max_r_state, double c_m) const {
-        const double extra = 2.0 * c_m;
-        if (!(cell_size > 0.0)) throw Invalid{"CellGrid: cell_size must be positive"};
         GridParams g{};
-        g.ncells = 1;
-        for (int a = 0; a < 3; ++a) {
-            if (a >= dim) {
-                g.dims[a] = 1;
-                g.edge[a] = 1.0;
-                g.near_s[a] = -1;
-                continue;
-            }
-            const double L = box.L[a];
-            int nn = static_cast<int>(std::floor(L / cell_size));
-            if (nn < 3) nn = 3;
-            g.dims[a] = nn;
-            g.edge[a] = L / nn;
-            g.ncells *= nn;
-            if (g.ncells > 4294967295LL)
-                throw Invalid{"CellGrid: more than 2^32 cells (radius too small for the box)"};
-        }
-        g.extra = extra;
-        g.rmax = max_r_state;
-        const double cut = ((max_r_state + max_r_state + extra) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
-        for (int a = 0; a < dim; ++a) {
-            int64_t s = 1;
-            while (static_cast<double>(s) * g.edge[a] < cut && 2 * s + 1 < g.dims[a]) ++s;
-            g.near_s[a] = (2 * s + 1 >= g.dims[a]) ? -1 : static_cast<int32_t>(s);
-        }
-        // colouring: two cells of one class are more than any trial's reach apart
-        const double cutc = ((max_r_state + max_r_state + 3.0 * c_m) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
-        g.ncls = 1;
-        g.cls_cells = 1;
-        for (int a = 0; a < 3; ++a) {
-            if (a >= dim) {
-                g.col_m[a] = 1;
-                g.col_n[a] = 1;
-                continue;
-            }
-            int64_t s = 1;
-            while (static_cast<double>(s) * g.edge[a] < cutc && 2 * s + 1 < g.dims[a]) ++s;
-            if (2 * s + 1 >= g.dims[a]) {
-                g.col_m[a] = g.dims[a];
-                g.col_n[a] = g.dims[a];
-            } else {
-                g.col_m[a] = static_cast<int32_t>(s + 1);
-                g.col_n[a] = g.col_m[a] + g.dims[a] % g.col_m[a];
-            }
-            g.ncls *= g.col_n[a];
-            g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
-        }
-        g.nrank = kRanks;
-        for (int a = 0; a < 3; ++a) {
-            g.fd_dims[a] = make_fastdiv(static_cast<uint32_t>(g.dims[a]));
-            g.fd_m[a] = make_fastdiv(static_cast<uint32_t>(g.col_m[a]));
-            g.col_body[a] = g.col_m[a] * (g.dims[a] / g.col_m[a]);
+        const int st = grid_params(cell_size, max_r_state, c_m, box, dim, near_mode, &g);
+        if (st == 1) throw Invalid{"CellGrid: cell_size must be positive"};
+        if (st == 2) throw Invalid{"CellGrid: more than 2^32 cells (radius too small for the box)"};
+        for (int a = 0; a < 3; ++a)
             for (const FastDiv& f : {g.fd_dims[a], g.fd_m[a]})  // cheap guard of the magic numbers
                 for (uint32_t v : {0u, 1u, f.d - 1, f.d, f.d + 1, 2 * f.d + 1, 0x7fffffffu, 0xfffffffeu, 0xffffffffu})
                     if (fdiv(v, f) != v / f.d) throw std::logic_error("fast division self-check failed");
-        }
-        // fp32 prefilter: coordinates live in [0, L); 8 ulp of the largest box length
-        // bounds the rounding of any coordinate difference and of the radii sums
-        double lmax = 0.0;
-        for (int a = 0; a < dim; ++a) lmax = std::max(lmax, box.L[a]);
-        g.margin_f = static_cast<float>(8.0 * std::ldexp(1.0, -24) * lmax + 4.0 * std::ldexp(1.0, -24) *
-                                                                              (2.0 * max_r_state + extra));
-        g.extra_f = static_cast<float>(extra);
-        g.rmax_f = static_cast<float>(max_r_state);
-        for (int a = 0; a < 3; ++a) {
-            g.L_f[a] = static_cast<float>(box.L[a]);
-            g.half_f[a] = 0.5f * g.L_f[a];
-            g.edge_f[a] = static_cast<float>(g.edge[a]);
-        }
         return g;
     }
 
@@ -399,13 +342,16 @@ struct srm_b200_ctx {
     }
 
     // grid rebuild T -> S (sorted) + skey; gp must be set
-    void grid_build(State& T) {
+    // ncells_bound: launch sizes for at least that many cells (graph capture: the largest
+    // grid of the run; every kernel reads the actual grid from gp)
+    void grid_build(State& T, int64_t ncells_bound = -1) {
         FamScope fs(this, 0);
+        const int64_t nc = ncells_bound >= 0 ? ncells_bound : hg.ncells;
         const int nb = blocks_for(n, 256);
-        const int cb = static_cast<int>(std::min<int64_t>(blocks_for(hg.ncells, 256), 148 * 64));
+        const int cb = static_cast<int>(std::min<int64_t>(blocks_for(nc, 256), 148 * 64));
         if (dim == 2) k_keys<2><<<nb, 256, 0, stream>>>(n, T, gp, key, count);
         else k_keys<3><<<nb, 256, 0, stream>>>(n, T, gp, key, count);
-        const int tiles = static_cast<int>((hg.ncells + kScanTile - 1) / kScanTile);
+        const int tiles = static_cast<int>((nc + kScanTile - 1) / kScanTile);
         k_scan_tiles<<<tiles, 1024, 0, stream>>>(count, gp, partial);
         k_scan_partials<<<1, 1024, 0, stream>>>(partial, tile_cap, gp, cell_start);
         k_scan_down<<<tiles, 1024, 0, stream>>>(count, partial, gp, cell_start);
@@ -452,16 +398,11 @@ struct srm_b200_ctx {
                 launched(3);
             }
             const int nb = blocks_for(n, 256);
-            bool half = near_mode != 1;
-            for (int a = 0; a < dim; ++a) half = half && hg.near_s[a] >= 0;
-            const bool tiles = half && dim == 3 && near_mode == 0 && hg.near_s[0] == 1 && hg.near_s[1] == 1 &&
-                               hg.near_s[2] == 1 && hg.dims[0] >= kTX + 2 && hg.dims[1] >= kTY + 2 && hg.dims[2] >= kTZ + 1;
-            if (tiles) {  // pairs once, through shared-memory bricks
+            if (hg.near_kind == 0) {  // pairs once, through shared-memory bricks
                 k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
-                const int ntiles = ((hg.dims[0] + kTX - 1) / kTX) * ((hg.dims[1] + kTY - 1) / kTY) * ((hg.dims[2] + kTZ - 1) / kTZ);
-                k_near_tiles<<<ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
+                k_near_tiles<<<hg.ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
                 launched(2);
-            } else if (half) {  // pairs once, appended to both lists
+            } else if (hg.near_kind == 1) {  // pairs once, appended to both lists
                 k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
                 if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
@@ -479,10 +420,10 @@ struct srm_b200_ctx {
                 // about 64 cells per warp, at most one wave of resident CTAs
                 const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads * 2), queue_ctas)));
                 if (dim == 2)
-                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, nbr, acc,
+                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
                 else
-                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, nbr, acc,
+                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
             }
             launched(hg.ncls);
@@ -534,6 +475,187 @@ struct srm_b200_ctx {
         }
         // the sweep updated the sorted state in place: it is the round's output
         swap_state(T, S);
+    }
+
+    // ---------------------------------------------------------------------------
+    // Device-resident srm_generate: one CUDA graph, conditional nodes.
+    //   WHILE(run) { k_gen_step; IF(active) { IF(copy) P->Q; IF(scale) Q *= factor;
+    //     round on Q (grid build, near lists, WHILE(cls) sweep class, stats, S->Q);
+    //     k_gen_after; IF(commit) Q->P; IF(f) volume fraction; IF(reorder) reorder P };
+    //     k_gen_end }
+    static cudaGraph_t add_conditional(cudaStream_t st, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type) {
+        cudaStreamCaptureStatus cst;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        cudaGraph_t g = nullptr;
+        SRM_CUDA(cudaStreamGetCaptureInfo(st, &cst, nullptr, &g, &deps, &ndeps));
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = type;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        SRM_CUDA(cudaGraphAddNode(&node, g, deps, ndeps, &np));
+        SRM_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+        return np.conditional.phGraph_out[0];
+    }
+    static cudaGraphConditionalHandle new_handle(cudaStream_t st, unsigned dflt) {
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t g = nullptr;
+        SRM_CUDA(cudaStreamGetCaptureInfo(st, &cst, nullptr, &g, nullptr, nullptr));
+        cudaGraphConditionalHandle h;
+        SRM_CUDA(cudaGraphConditionalHandleCreate(&h, g, dflt, cudaGraphCondAssignDefault));
+        return h;
+    }
+    // capture `body` into the (empty) graph `g` on stream st (which becomes `stream` meanwhile)
+    template <typename F>
+    void capture_into(cudaGraph_t g, cudaStream_t st, F&& body) {
+        SRM_CUDA(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        cudaStream_t saved = stream;
+        stream = st;
+        body();
+        stream = saved;
+        cudaGraph_t out = nullptr;
+        SRM_CUDA(cudaStreamEndCapture(st, &out));
+    }
+
+    GenCtl* d_ctl = nullptr;
+    GenProgress* d_recs = nullptr;
+    int64_t recs_cap = 0;
+    cudaStream_t cap_streams[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    // returns status; out counters filled from the controller
+    int generate_graph(const srm_b200_params& p, int64_t it0, double f0, double max_r0, int64_t* done_out,
+                       int64_t* acc_out, int64_t* rounds_out, int64_t* shakes_out, double* f_out,
+                       srm_b200_progress_fn progress, void* user) {
+        if (!d_ctl) d_ctl = dalloc<GenCtl>(1);
+        const int64_t want_recs = std::min<int64_t>(p.max_iterations, int64_t{1} << 20);
+        if (want_recs > recs_cap) {
+            cudaFree(d_recs);
+            d_recs = nullptr;
+            d_recs = dalloc<GenProgress>(want_recs);
+            recs_cap = want_recs;
+        }
+        for (auto& st : cap_streams)
+            if (!st) SRM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        GenCtl hc{};
+        hc.f_target = p.f_target;
+        hc.stop = p.f_target * (1.0 - 1e-12);
+        hc.c_w = p.c_w;
+        hc.c_m = p.c_m;
+        hc.box_measure = box_measure();
+        hc.max_iter = p.max_iterations;
+        hc.recs_cap = recs_cap;
+        hc.it0 = it0;
+        hc.n_k = p.n_k;
+        hc.n_l = p.n_l;
+        hc.reorder_period = p.reorder_period;
+        hc.dim = dim;
+        hc.near_mode = near_mode;
+        hc.seed = p.seed;
+        hc.f = f0;
+        hc.max_r = max_r0;
+        hc.recs = d_recs;
+        // the largest grid of the run is the first one (radii only grow): launch bounds
+        const GridParams g0 = make_grid(2.5 * max_r0 + p.c_m, max_r0, p.c_m);
+        ensure_cells(g0.ncells);
+        const int64_t nc_max = g0.ncells;
+        const int ntiles_max = std::max(1, g0.ntiles);
+        SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
+        SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
+
+        cudaGraph_t G;
+        SRM_CUDA(cudaGraphCreate(&G, 0));
+        capturing = true;
+        GenCtl* ctl = d_ctl;
+        const int nb = blocks_for(n, 256);
+        capture_into(G, cap_streams[0], [&]() {
+            const cudaGraphConditionalHandle h_run = new_handle(stream, 1);
+            k_gen_t0<<<1, 1, 0, stream>>>(ctl);
+            cudaGraph_t B = add_conditional(stream, h_run, cudaGraphCondTypeWhile);
+            capture_into(B, cap_streams[1], [&]() {
+                const cudaGraphConditionalHandle h_active = new_handle(stream, 0);
+                k_gen_step<<<1, 1, 0, stream>>>(ctl, gp, rp, stats, box, h_active);
+                cudaGraph_t A = add_conditional(stream, h_active, cudaGraphCondTypeIf);
+                capture_into(A, cap_streams[2], [&]() {
+                    const cudaGraphConditionalHandle h_copy = new_handle(stream, 0), h_scale = new_handle(stream, 0);
+                    const cudaGraphConditionalHandle h_cls = new_handle(stream, 0), h_commit = new_handle(stream, 0);
+                    const cudaGraphConditionalHandle h_f = new_handle(stream, 0), h_reorder = new_handle(stream, 0);
+                    k_gen_flags<<<1, 1, 0, stream>>>(ctl, h_copy, h_scale);
+                    capture_into(add_conditional(stream, h_copy, cudaGraphCondTypeIf), cap_streams[3],
+                                 [&]() { copy_state(P, Q); });
+                    capture_into(add_conditional(stream, h_scale, cudaGraphCondTypeIf), cap_streams[3], [&]() {
+                        k_scale_radius_ctl<<<nb, 256, 0, stream>>>(n, Q.rec, ctl);
+                    });
+                    // one round on Q
+                    grid_build(Q, nc_max);
+                    k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
+                    k_near_tiles<<<ntiles_max, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
+                    if (dim == 2) {
+                        k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                        k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                    } else {
+                        k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                        k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                    }
+                    k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
+                    capture_into(add_conditional(stream, h_cls, cudaGraphCondTypeWhile), cap_streams[3], [&]() {
+                        if (dim == 2)
+                            k_sweep_warpq<2><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
+                                                                                       skey, nbr, acc, active, stats);
+                        else
+                            k_sweep_warpq<3><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
+                                                                                       skey, nbr, acc, active, stats);
+                        k_gen_cls_next<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
+                    });
+                    const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
+                    if (dim == 2) k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
+                    else k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
+                    copy_state(S, Q);
+                    k_gen_after<<<1, 1, 0, stream>>>(ctl, stats, h_commit, h_f, h_reorder);
+                    capture_into(add_conditional(stream, h_commit, cudaGraphCondTypeIf), cap_streams[3],
+                                 [&]() { copy_state(Q, P); });
+                    capture_into(add_conditional(stream, h_f, cudaGraphCondTypeIf), cap_streams[3], [&]() {
+                        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, P.rec, red_part_sum, red_part_max);
+                        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, P.rec, red_part_sum, red_part_max);
+                        k_reduce_final<<<1, 256, 0, stream>>>(red_part_sum, red_part_max, red_out);
+                        k_gen_f<<<1, 1, 0, stream>>>(ctl, red_out);
+                    });
+                    capture_into(add_conditional(stream, h_reorder, cudaGraphCondTypeIf), cap_streams[3], [&]() {
+                        k_gen_grid_iter<<<1, 1, 0, stream>>>(ctl, gp);
+                        grid_build(P, nc_max);
+                        SRM_CUDA(cudaMemcpyAsync(Q.slot, S.slot, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, stream));
+                        k_assign_slots<<<nb, 256, 0, stream>>>(n, S, nullptr, Q.slot);
+                        copy_state(S, P);
+                    });
+                });
+                k_gen_end<<<1, 1, 0, stream>>>(ctl, h_run);
+            });
+        });
+        capturing = false;
+        cudaGraphExec_t X;
+        SRM_CUDA(cudaGraphInstantiate(&X, G, 0));
+        SRM_CUDA(cudaGraphLaunch(X, stream));
+        SRM_CUDA(cudaStreamSynchronize(stream));
+        SRM_CUDA(cudaGetLastError());
+        cudaGraphExecDestroy(X);
+        cudaGraphDestroy(G);
+        SRM_CUDA(cudaMemcpy(&hc, d_ctl, sizeof(GenCtl), cudaMemcpyDeviceToHost));
+        *done_out = hc.done;
+        *acc_out = hc.accepted;
+        *rounds_out = hc.rounds;
+        *shakes_out = hc.shakes;
+        *f_out = hc.f;
+        if (progress && hc.done > 0) {  // the iteration records, delivered after the run
+            std::vector<GenProgress> recs(static_cast<size_t>(std::min(hc.done, recs_cap)));
+            SRM_CUDA(cudaMemcpy(recs.data(), d_recs, sizeof(GenProgress) * recs.size(), cudaMemcpyDeviceToHost));
+            for (const auto& r : recs) {
+                srm_b200_progress_record rec{r.iteration, r.volume_fraction, r.accepted, (r.t_ns - hc.t0) * 1e-9, r.rounds};
+                progress(&rec, user);
+            }
+        }
+        if (hc.status == 2) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
+        return hc.status == 1 ? SRM_B200_ITERATION_LIMIT : SRM_B200_OK;
     }
 
     srm_b200_round_stats read_stats(bool with_candidates) {
@@ -969,6 +1091,19 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
         int64_t done = 0, accepted_iters = 0, rounds = 0, shakes = 0;
         int accepted_since_reorder = 0;
         int status = SRM_B200_OK;
+        if (c->device_loop && f < stop) {  // one CUDA graph, no host round-trip per iteration
+            status = c->generate_graph(p, iteration_count_in, f, c->max_radius(c->P), &done, &accepted_iters, &rounds,
+                                       &shakes, &f, progress, user);
+            if (out) {
+                out->status = status;
+                out->volume_fraction = f;
+                out->iteration_count = iteration_count_in + done;
+                out->accepted_iterations = accepted_iters;
+                out->rounds = rounds;
+                out->shake_rounds = shakes;
+            }
+            return status;
+        }
         while (f < stop) {
             if (done >= p.max_iterations) {
                 status = SRM_B200_ITERATION_LIMIT;
@@ -1077,6 +1212,13 @@ int srm_b200_timing_get(srm_b200_ctx* c, double* ms, int64_t* calls) {
 int srm_b200_sync(srm_b200_ctx* c) {
     return guarded(c, [&]() -> int {
         c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_set_generate_mode(srm_b200_ctx* c, int device_loop) {
+    return guarded(c, [&]() -> int {
+        c->device_loop = device_loop != 0;
         return SRM_B200_OK;
     });
 }

@@ -37,7 +37,7 @@ __host__ __device__ inline uint32_t fdiv(uint32_t n, const FastDiv& f) {
     return static_cast<uint32_t>((hi + n) >> f.l);
 }
 
-inline FastDiv make_fastdiv(uint32_t d) {
+__host__ __device__ inline FastDiv make_fastdiv(uint32_t d) {
     uint32_t l = 0;
     while ((uint64_t{1} << l) < d) ++l;
     const uint64_t m = ((uint64_t{1} << 32) * ((uint64_t{1} << l) - d)) / d + 1;
@@ -59,6 +59,8 @@ struct GridParams {
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
     int32_t nrank;      // ranks in cell with their own sweep step (kRanks)
+    int32_t near_kind;   // near lists: 0 shared-memory bricks, 1 half stencil, 2 full stencil
+    int32_t ntiles;      // bricks of k_near_tiles (near_kind 0)
     FastDiv fd_dims[3];  // division by dims[a]
     FastDiv fd_m[3];     // division by col_m[a]
     int32_t col_body[3]; // col_m * floor(dims / col_m): cells coloured x mod m
@@ -77,6 +79,94 @@ __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, in
         c[1] = static_cast<int>(r1);
         c[2] = 0;
     }
+}
+
+// CellGrid ctor (cell_grid.hpp:288-309) + the near-search stencil, the colouring
+// and the near-list kernel choice for a state whose largest radius is
+// max_r_state and whose trial moves have length c_m.  The colouring expression is the
+// oracle's orc_colouring.  Host and device (the device-resident generate loop) share it.
+// Returns 0, or 1 (cell_size <= 0), 2 (more than 2^32 cells).
+constexpr int kTX = 16, kTY = 8, kTZ = 4;  // k_near_tiles brick (cells)
+__host__ __device__ inline int grid_params(double cell_size, double max_r_state, double c_m, const Box& box, int dim,
+                                           int near_mode, GridParams* out) {
+    const double extra = 2.0 * c_m;
+    if (!(cell_size > 0.0)) return 1;
+    GridParams g{};
+    g.ncells = 1;
+    for (int a = 0; a < 3; ++a) {
+        if (a >= dim) {
+            g.dims[a] = 1;
+            g.edge[a] = 1.0;
+            g.near_s[a] = -1;
+            continue;
+        }
+        const double L = box.L[a];
+        const double fl = floor(L / cell_size);
+        if (!(fl < 4294967296.0)) return 2;
+        int nn = static_cast<int>(fl);
+        if (nn < 3) nn = 3;
+        g.dims[a] = nn;
+        g.edge[a] = L / nn;
+        g.ncells *= nn;
+        if (g.ncells > 4294967295LL) return 2;
+    }
+    g.extra = extra;
+    g.rmax = max_r_state;
+    const double cut = ((max_r_state + max_r_state + extra) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
+    for (int a = 0; a < dim; ++a) {
+        int64_t s = 1;
+        while (static_cast<double>(s) * g.edge[a] < cut && 2 * s + 1 < g.dims[a]) ++s;
+        g.near_s[a] = (2 * s + 1 >= g.dims[a]) ? -1 : static_cast<int32_t>(s);
+    }
+    // colouring: two cells of one class are more than any trial's reach apart
+    const double cutc = ((max_r_state + max_r_state + 3.0 * c_m) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
+    g.ncls = 1;
+    g.cls_cells = 1;
+    for (int a = 0; a < 3; ++a) {
+        if (a >= dim) {
+            g.col_m[a] = 1;
+            g.col_n[a] = 1;
+            continue;
+        }
+        int64_t s = 1;
+        while (static_cast<double>(s) * g.edge[a] < cutc && 2 * s + 1 < g.dims[a]) ++s;
+        if (2 * s + 1 >= g.dims[a]) {
+            g.col_m[a] = g.dims[a];
+            g.col_n[a] = g.dims[a];
+        } else {
+            g.col_m[a] = static_cast<int32_t>(s + 1);
+            g.col_n[a] = g.col_m[a] + g.dims[a] % g.col_m[a];
+        }
+        g.ncls *= g.col_n[a];
+        g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
+    }
+    g.nrank = 3;
+    for (int a = 0; a < 3; ++a) {
+        g.fd_dims[a] = make_fastdiv(static_cast<uint32_t>(g.dims[a]));
+        g.fd_m[a] = make_fastdiv(static_cast<uint32_t>(g.col_m[a]));
+        g.col_body[a] = g.col_m[a] * (g.dims[a] / g.col_m[a]);
+    }
+    // fp32 prefilter: coordinates live in [0, L); 8 ulp of the largest box length
+    // bounds the rounding of any coordinate difference and of the radii sums
+    double lmax = 0.0;
+    for (int a = 0; a < dim; ++a) lmax = lmax > box.L[a] ? lmax : box.L[a];
+    const double ulp = 5.9604644775390625e-08;  // 2^-24
+    g.margin_f = static_cast<float>(8.0 * ulp * lmax + 4.0 * ulp * (2.0 * max_r_state + extra));
+    g.extra_f = static_cast<float>(extra);
+    g.rmax_f = static_cast<float>(max_r_state);
+    for (int a = 0; a < 3; ++a) {
+        g.L_f[a] = static_cast<float>(box.L[a]);
+        g.half_f[a] = 0.5f * g.L_f[a];
+        g.edge_f[a] = static_cast<float>(g.edge[a]);
+    }
+    bool half = near_mode != 1;
+    for (int a = 0; a < dim; ++a) half = half && g.near_s[a] >= 0;
+    const bool tiles = half && dim == 3 && near_mode == 0 && g.near_s[0] == 1 && g.near_s[1] == 1 &&
+                       g.near_s[2] == 1 && g.dims[0] >= kTX + 2 && g.dims[1] >= kTY + 2 && g.dims[2] >= kTZ + 1;
+    g.near_kind = tiles ? 0 : (half ? 1 : 2);
+    g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ) : 0;
+    *out = g;
+    return 0;
 }
 
 struct RoundParams {
@@ -479,6 +569,7 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
                                                     const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                     int32_t* __restrict__ nbr) {
     const GridParams& g = *gp;
+    if (g.near_kind != 2) return;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
         int32_t* my = nbr + q * kNearRow;
         int nn = 0;
@@ -608,6 +699,7 @@ __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const Gri
                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                    int32_t* __restrict__ nbr) {
     const GridParams& g = *gp;
+    if (g.near_kind != 1) return;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
         near_half_particle<D>(q, S, g, cs, skey, nbr);
 }
@@ -620,7 +712,6 @@ __global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const Gri
 // five contiguous shared ranges (own cell after i + next cell, the dy=+1 row, the three
 // dz=+1 rows).  Same screen, same pairs as k_near_half; a brick whose halo holds more
 // than kTileCap particles falls back to near_half_particle.
-constexpr int kTX = 16, kTY = 8, kTZ = 4;
 constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 1;
 constexpr int kHCells = kHX * kHY * kHZ;
 constexpr int kTileCap = 1792;
@@ -641,6 +732,7 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
     __shared__ int wsum[kTileThreads / 32];
     __shared__ int rowoff[kTY * kTZ + 1];
     const GridParams& g = *gp;
+    if (g.near_kind != 0 || static_cast<int>(blockIdx.x) >= g.ntiles) return;  // (graph launches: upper bounds)
     const int dx = g.dims[0], dy = g.dims[1], dz = g.dims[2];
     const int ntx = (dx + kTX - 1) / kTX, nty = (dy + kTY - 1) / kTY;
     const int tx = blockIdx.x % ntx, ty = (blockIdx.x / ntx) % nty, tz = blockIdx.x / (ntx * nty);
@@ -1214,7 +1306,8 @@ __device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int*
 // No barriers and no work lists: warps progress independently.  Per cell the visiting
 // order and the trials are those of the sequential sweep (orc_sweep_round).
 template <int D>
-__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls, State S, Box box,
+__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls_arg, const int* __restrict__ cls_dev,
+                                                                               State S, Box box,
                                                                                const GridParams* __restrict__ gp,
                                                                                const RoundParams* __restrict__ rpp,
                                                                                const int64_t* __restrict__ cs,
@@ -1223,6 +1316,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                                                                                uint8_t* __restrict__ acc,
                                                                                int32_t* __restrict__ active,
                                                                                StatsDev* stats) {
+    const int cls = cls_dev ? *cls_dev : cls_arg;  // (device-resident loop: from the controller)
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
     const RoundParams rp = *rpp;
@@ -1327,6 +1421,189 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
         isl = __shfl_sync(0xffffffffu, isl, src);
         iend = __shfl_sync(0xffffffffu, iend, src);
     }
+}
+
+// ---------------------------------------------------------------------------------
+// Device-resident srm_generate (engine.hpp:176-260): a controller kept in device memory
+// drives a CUDA graph of conditional nodes; every decision the host loop takes between
+// rounds (swell factor and clamp, grid of the iteration, success, shake, commit, volume
+// fraction, reorder cadence, iteration budget) is taken here, so a whole run is one
+// graph launch with no host round-trip.  A "step" is one round: a growth round on the
+// working state W (a copy of P, swollen), or a shake round (W = P), see GenCtl::phase.
+struct GenProgress {
+    int64_t iteration;
+    double volume_fraction;
+    int32_t accepted;
+    int32_t rounds;
+    uint64_t t_ns;  // globaltimer at the end of the iteration
+};
+
+struct GenCtl {
+    // inputs
+    double f_target, stop, c_w, c_m, box_measure;
+    int64_t max_iter, it0;
+    int32_t n_k, n_l, reorder_period, dim, near_mode, pad0;
+    uint64_t seed;
+    // state
+    double f, max_r, factor, cs;
+    int64_t done, accepted, rounds, shakes;
+    int32_t phase;  // 0 new iteration, 1 growth rounds, 2 shake rounds, 3 finished
+    int32_t k;      // round index in the phase
+    int32_t reorder_since;
+    int32_t status;  // 0 ok, 1 iteration budget exhausted, 2 invalid grid (CellGrid safety bound)
+    int32_t cls;     // colour class of the running sweep launch
+    int32_t iter_done;  // an iteration ended in this step (progress record)
+    int32_t success;
+    int32_t rounds_this;
+    int32_t do_copy, do_scale;  // this step starts with W <- P (and W *= factor)
+    uint64_t t0;
+    GridParams g_iter;  // the grid of the current iteration (growth rounds and reorder)
+    GenProgress* recs;
+    int64_t recs_cap;
+};
+
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Start of a step: phase logic before the round; writes the grid and round parameters.
+__global__ void k_gen_step(GenCtl* c, GridParams* gp, RoundParams* rp, StatsDev* stats, Box box,
+                           cudaGraphConditionalHandle h_active) {
+    bool active = true, copy = false, scale = false;
+    c->iter_done = 0;
+    if (c->phase == 0) {  // a new iteration (engine.hpp:205-224)
+        c->done += 1;
+        double factor = 1.0 + c->c_w;
+        const double N = static_cast<double>(c->dim);
+        if (c->f * pow(factor, N) > c->f_target) factor = pow(c->f_target / c->f, 1.0 / N);
+        c->factor = factor;
+        c->cs = 2.5 * c->max_r + c->c_m;
+        GridParams g{};
+        if (c->cs < 2.0 * (c->max_r * factor) + c->c_m ||
+            grid_params(c->cs, c->max_r * factor, c->c_m, box, c->dim, c->near_mode, &g) != 0) {
+            c->status = 2;
+            c->phase = 3;
+            active = false;
+        } else {
+            c->g_iter = g;
+            *gp = g;
+            c->phase = 1;
+            c->k = 0;
+            c->rounds_this = 0;
+            copy = true;
+            scale = true;
+        }
+    } else if (c->phase == 2 && c->k == 0) {  // shake on P with the pre-swell grid (engine.hpp:244-249)
+        GridParams g{};
+        grid_params(c->cs, c->max_r, c->c_m, box, c->dim, c->near_mode, &g);
+        *gp = g;
+        copy = true;
+    }
+    if (active) {
+        RoundParams v{};
+        v.c_m = c->c_m;
+        v.n_l = c->n_l;
+        v.write_acc = 0;
+        v.key.k0 = static_cast<uint32_t>(c->seed);
+        v.key.k1 = static_cast<uint32_t>(c->seed >> 32);
+        v.key.round_id = static_cast<uint32_t>(c->phase == 1 ? c->k : c->n_k + c->k) & 0xFFFFFFu;
+        v.key.iteration = static_cast<uint32_t>(c->it0 + c->done);
+        *rp = v;
+        *stats = StatsDev{0, 0, 0, 0};
+    }
+    c->do_copy = copy ? 1 : 0;
+    c->do_scale = scale ? 1 : 0;
+    cudaGraphSetConditional(h_active, active ? 1u : 0u);
+}
+
+__global__ void k_gen_flags(const GenCtl* c, cudaGraphConditionalHandle h_copy, cudaGraphConditionalHandle h_scale) {
+    cudaGraphSetConditional(h_copy, c->do_copy ? 1u : 0u);
+    cudaGraphSetConditional(h_scale, c->do_scale ? 1u : 0u);
+}
+
+__global__ void k_gen_t0(GenCtl* c) { c->t0 = global_ns(); }
+
+__global__ void k_gen_cls_begin(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls) {
+    c->cls = 0;
+    cudaGraphSetConditional(h_cls, gp->ncls > 0 ? 1u : 0u);
+}
+
+__global__ void k_gen_cls_next(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls) {
+    c->cls += 1;
+    cudaGraphSetConditional(h_cls, c->cls < gp->ncls ? 1u : 0u);
+}
+
+// After the round: success / shake / commit decisions (engine.hpp:227-249).
+__global__ void k_gen_after(GenCtl* c, const StatsDev* __restrict__ stats, cudaGraphConditionalHandle h_commit,
+                            cudaGraphConditionalHandle h_f, cudaGraphConditionalHandle h_reorder) {
+    bool commit = false, newf = false, reorder = false;
+    c->rounds_this += 1;
+    if (c->phase == 1) {
+        c->rounds += 1;
+        c->k += 1;
+        if (stats->overlap_pairs == 0) {  // accepted: P <- W, f, reorder cadence
+            commit = true;
+            newf = true;
+            c->success = 1;
+            c->accepted += 1;
+            c->max_r = c->max_r * c->factor;  // == max of the swollen radii (rounding is monotone)
+            if (c->reorder_period > 0 && ++c->reorder_since >= c->reorder_period) {
+                c->reorder_since = 0;
+                reorder = true;
+            }
+            c->phase = 0;
+            c->iter_done = 1;
+        } else if (c->k >= c->n_k) {  // failed: shake
+            c->phase = 2;
+            c->k = 0;
+            c->rounds_this = 0;
+        }
+    } else if (c->phase == 2) {
+        c->shakes += 1;
+        c->k += 1;
+        if (c->k >= c->n_k) {
+            commit = true;  // the shaken W back into P
+            c->success = 0;
+            c->phase = 0;
+            c->iter_done = 1;
+        }
+    }
+    cudaGraphSetConditional(h_commit, commit ? 1u : 0u);
+    cudaGraphSetConditional(h_f, newf ? 1u : 0u);
+    cudaGraphSetConditional(h_reorder, reorder ? 1u : 0u);
+}
+
+__global__ void k_gen_f(GenCtl* c, const double* __restrict__ red_out) { c->f = red_out[0] / c->box_measure; }
+
+__global__ void k_gen_grid_iter(const GenCtl* c, GridParams* gp) { *gp = c->g_iter; }
+
+// End of a step: progress record, loop condition (engine.hpp:202-211).
+__global__ void k_gen_end(GenCtl* c, cudaGraphConditionalHandle h_run) {
+    if (c->iter_done) {
+        GenProgress r;
+        r.iteration = c->it0 + c->done;
+        r.volume_fraction = c->f;
+        r.accepted = c->success;
+        r.rounds = c->rounds_this;
+        r.t_ns = global_ns();
+        if (c->done - 1 < c->recs_cap) c->recs[c->done - 1] = r;
+    }
+    if (c->phase == 0) {
+        if (!(c->f < c->stop)) c->phase = 3;
+        else if (c->done >= c->max_iter) {
+            c->status = 1;
+            c->phase = 3;
+        }
+    }
+    cudaGraphSetConditional(h_run, c->phase != 3 ? 1u : 0u);
+}
+
+__global__ void k_scale_radius_ctl(int64_t n, double4* __restrict__ rec, const GenCtl* __restrict__ c) {
+    const double factor = c->factor;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        rec[i].w = rec[i].w * factor;  // engine.hpp:520 p.radius *= factor
 }
 
 // Overlap reduction after the sweep.  A particle that accepted a trial cleared every
