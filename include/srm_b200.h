@@ -42,7 +42,10 @@ typedef enum {
     SRM_B200_NO_DEVICE = 5        /* no CUDA device: the product has no CPU fallback         */
 } srm_b200_status;
 
-typedef enum { SRM_B200_SPHERE = 0 /* Disk (dim 2) / Ball (dim 3), shape.hpp:503-527 */ } srm_b200_shape;
+typedef enum {
+    SRM_B200_SPHERE = 0,  /* Disk (dim 2) / Ball (dim 3), shape.hpp:503-527 */
+    SRM_B200_PLATELET = 1 /* thin circular platelet, SpherodiskShape (spherodisk.hpp:72-99), dim 3 */
+} srm_b200_shape;
 
 /* engine.hpp:22-32 SrmParams, field for field. */
 typedef struct {
@@ -102,6 +105,16 @@ const char* srm_b200_create_error(void);
 int srm_b200_upload(srm_b200_ctx* ctx, int64_t n, const double* pos, const double* radius,
                     const int32_t* id);
 int srm_b200_download(srm_b200_ctx* ctx, double* pos, double* radius, int32_t* id);
+/* platelet contexts (SRM_B200_PLATELET): centre[3n], unit normal[3n], diameter[n],
+ * thickness[n] (Spherodisk, spherodisk.hpp:16-22) */
+int srm_b200_upload_platelets(srm_b200_ctx* ctx, int64_t n, const double* pos, const double* normal,
+                              const double* diameter, const double* thickness, const int32_t* id);
+int srm_b200_download_platelets(srm_b200_ctx* ctx, double* pos, double* normal, double* diameter,
+                                double* thickness, int32_t* id);
+/* rotation angle c_r of platelet moves for srm_b200_round / srm_b200_rounds (SrmParams::c_r;
+ * srm_b200_generate and srm_b200_relax_sweeps take it from their own arguments) */
+int srm_b200_set_rotation(srm_b200_ctx* ctx, double c_r);
+
 /* array-of-structs variants: one cudaMemcpy of the raw records + an unpack kernel */
 int srm_b200_upload_records(srm_b200_ctx* ctx, int64_t n, const void* records, int64_t stride,
                             int64_t off_id, int64_t off_pos, int64_t off_radius);
@@ -183,6 +196,12 @@ int srm_b200_rounds(srm_b200_ctx* ctx, double cell_size, double c_m, int n_l, ui
 int srm_b200_rsa_place(int dim, const double* box_lengths, int64_t n, const double* radii,
                        int64_t max_attempts, uint64_t seed, double* pos_out, int32_t* id_out,
                        int64_t* placed_out);
+/* recipes.cpp:107-148 rsa_platelets with Rng(seed): n platelets of one diameter and
+ * aspect ratio (diameter / thickness) in the box; bit-identical to the reference.
+ * Returns OK / INVALID / PLACEMENT_FAILURE (placed_out = platelets placed). */
+int srm_b200_rsa_platelets(int64_t n, double diameter, double aspect_ratio, const double* box_lengths,
+                           int64_t max_attempts, uint64_t seed, double* pos_out, double* normal_out,
+                           int32_t* id_out, int64_t* placed_out);
 /* random.hpp:84-89 mix_seed */
 uint64_t srm_b200_mix_seed(uint64_t seed, uint64_t stream);
 

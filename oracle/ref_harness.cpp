@@ -16,6 +16,7 @@
 #include "srm/engine.hpp"
 #include "srm/geometry.hpp"
 #include "srm/random.hpp"
+#include "srm/recipes.hpp"
 #include "srm/rsa.hpp"
 #include "srm/shape.hpp"
 #include "srm/spherodisk.hpp"
@@ -309,6 +310,110 @@ double ref_bench_rounds(int dim, const double* L, int64_t n, const double* pos, 
                                               accepted_total);
     return bench_rounds_impl<3>(L, n, pos, r, id, c_m, n_l, rounds, seed, threads,
                                 accepted_total);
+}
+
+
+// ---- platelets (spherodisk.hpp, spherodisk.cpp, recipes.cpp:107-148) ------------------
+static Spherodisk make_pl(const double* p, const double* nrm, double D, double t, int id = 0) {
+    Spherodisk q;
+    q.id = id;
+    for (int a = 0; a < 3; ++a) {
+        q.pos[a] = p[a];
+        q.normal[a] = nrm[a];
+    }
+    q.diameter = D;
+    q.thickness = t;
+    return q;
+}
+
+int ref_pl_overlap(const double* L, const double* pa, const double* na, double Da, double ta, const double* pb,
+                   const double* nb, double Db, double tb) {
+    return SpherodiskShape::overlap(make_pl(pa, na, Da, ta), make_pl(pb, nb, Db, tb), make_box<3>(L)) ? 1 : 0;
+}
+
+int ref_pl_disks_within(const double* c1, const double* n1, double r1, const double* c2, const double* n2, double r2,
+                        double threshold) {
+    auto v = [](const double* x) { return Vec3{{x[0], x[1], x[2]}}; };
+    return disks_within(v(c1), v(n1), r1, v(c2), v(n2), r2, threshold) ? 1 : 0;
+}
+
+double ref_pl_disk_distance(const double* c1, const double* n1, double r1, const double* c2, const double* n2,
+                            double r2) {
+    auto v = [](const double* x) { return Vec3{{x[0], x[1], x[2]}}; };
+    return disk_disk_distance(v(c1), v(n1), r1, v(c2), v(n2), r2);
+}
+
+double ref_pl_measure(double D, double t) {
+    Spherodisk q;
+    q.diameter = D;
+    q.thickness = t;
+    return spherodisk_measure(q);
+}
+
+void ref_pl_rotate(const double* v, const double* axis, double angle, double* out) {
+    const Vec3 r = rotate_about_axis(Vec3{{v[0], v[1], v[2]}}, Vec3{{axis[0], axis[1], axis[2]}}, angle);
+    for (int a = 0; a < 3; ++a) out[a] = r[a];
+}
+
+static void store_pl(const std::vector<Spherodisk>& ps, double* pos, double* nrm, double* D, double* t, int32_t* id) {
+    for (size_t i = 0; i < ps.size(); ++i) {
+        for (int a = 0; a < 3; ++a) {
+            if (pos) pos[3 * i + a] = ps[i].pos[a];
+            if (nrm) nrm[3 * i + a] = ps[i].normal[a];
+        }
+        if (D) D[i] = ps[i].diameter;
+        if (t) t[i] = ps[i].thickness;
+        if (id) id[i] = ps[i].id;
+    }
+}
+
+// rsa_platelets with Rng(seed); 0 ok, 1 placement failure, 2 invalid
+int ref_rsa_platelets(int64_t n, double diameter, double aspect, const double* L, int64_t max_attempts, uint64_t seed,
+                      double* pos, double* nrm, int32_t* id) {
+    try {
+        Rng rng(seed);
+        auto snap = rsa_platelets(n, diameter, aspect, make_box<3>(L), static_cast<std::size_t>(max_attempts), rng);
+        store_pl(snap.particles, pos, nrm, nullptr, nullptr, id);
+        return 0;
+    } catch (const PlacementFailure&) {
+        return 1;
+    } catch (const ValidationError&) {
+        return 2;
+    }
+}
+
+// srm_generate<SpherodiskShape> (engine.hpp:176-260); state in/out
+int ref_generate_platelets(const double* L, int64_t n, double* pos, double* nrm, double* D, double* t, int32_t* id,
+                           double c_w, double c_m, double c_r, int n_k, int n_l, double f_target, int64_t max_iterations,
+                           uint64_t seed, int reorder_period, int64_t* iterations_out, double* f_out) {
+    PlateletSnapshot snap;
+    snap.box = make_box<3>(L);
+    snap.particles.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) snap.particles[i] = make_pl(pos + 3 * i, nrm + 3 * i, D[i], t[i], id[i]);
+    snap.refresh_volume_fraction();
+    SrmParams p;
+    p.c_w = c_w; p.c_m = c_m; p.c_r = c_r; p.n_k = n_k; p.n_l = n_l; p.f_target = f_target;
+    p.max_iterations = max_iterations; p.seed = seed; p.reorder_period = reorder_period;
+    try {
+        auto res = srm_generate<SpherodiskShape>(snap, p);
+        store_pl(res.snapshot.particles, pos, nrm, D, t, id);
+        if (iterations_out) *iterations_out = res.snapshot.iteration_count;
+        if (f_out) *f_out = res.snapshot.volume_fraction;
+        return res.status == GenerateStatus::Converged ? 0 : 1;
+    } catch (const ValidationError&) {
+        return 2;
+    }
+}
+
+// shape_any_collision<SpherodiskShape> over a grid of cell size cs
+int ref_pl_any_collision(const double* L, double cs, int64_t n, const double* pos, const double* nrm, const double* D,
+                         const double* t, const int32_t* id) {
+    std::vector<Spherodisk> ps(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) ps[i] = make_pl(pos + 3 * i, nrm + 3 * i, D[i], t[i], id[i]);
+    const auto box = make_box<3>(L);
+    CellGrid<3> g(box, cs);
+    build_shape_grid<SpherodiskShape>(g, ps);
+    return shape_any_collision<SpherodiskShape>(std::span<const Spherodisk>(ps), g) ? 1 : 0;
 }
 
 }  // extern "C"

@@ -479,3 +479,218 @@ double orc_volume_fraction_seq(int dim, const double* L, int64_t n, const double
     for (int a = 0; a < dim; ++a) m *= L[a];
     return sum / m;
 }
+
+/* ==================================================================================
+ * Thin circular platelets (spherodisks): the reference's SpherodiskShape restated
+ * (spherodisk.hpp:16-99, spherodisk.cpp:14-112).  Vectors are double[3]; every
+ * expression keeps the reference's operation order.                                  */
+typedef struct { double v[3]; } pv3;
+
+/* geometry.hpp:117-125 minimum image of one coordinate difference */
+static double orc_min_image(double d, double L) {
+    const double half = 0.5 * L;
+    if (d > half) d -= L;
+    if (d < -half) d += L;
+    return d;
+}
+
+static pv3 pv(double x, double y, double z) { pv3 r; r.v[0] = x; r.v[1] = y; r.v[2] = z; return r; }
+static pv3 pv_add(pv3 a, pv3 b) { for (int i = 0; i < 3; ++i) a.v[i] += b.v[i]; return a; }
+static pv3 pv_sub(pv3 a, pv3 b) { for (int i = 0; i < 3; ++i) a.v[i] -= b.v[i]; return a; }
+static pv3 pv_mul(pv3 a, double s) { for (int i = 0; i < 3; ++i) a.v[i] *= s; return a; }
+static double pv_dot(pv3 a, pv3 b) { double s = 0.0; for (int i = 0; i < 3; ++i) s += a.v[i] * b.v[i]; return s; }
+static double pv_norm(pv3 a) { return sqrt(pv_dot(a, a)); }
+static pv3 pv_cross(pv3 a, pv3 b) {
+    return pv(a.v[1] * b.v[2] - a.v[2] * b.v[1], a.v[2] * b.v[0] - a.v[0] * b.v[2], a.v[0] * b.v[1] - a.v[1] * b.v[0]);
+}
+
+/* spherodisk.cpp:14-21 */
+static pv3 pl_closest(pv3 c, pv3 n, double r, pv3 p) {
+    const pv3 w = pv_sub(p, c);
+    pv3 in_plane = pv_sub(w, pv_mul(n, pv_dot(w, n)));
+    const double d2 = pv_dot(in_plane, in_plane);
+    if (d2 > r * r) in_plane = pv_mul(in_plane, r / sqrt(d2));
+    return pv_add(c, in_plane);
+}
+
+/* spherodisk.cpp:29-40 */
+static double pl_alternate(pv3 c1, pv3 n1, double r1, pv3 c2, pv3 n2, double r2, pv3 p2, double tol, int max_iter) {
+    double prev = INFINITY;
+    for (int it = 0; it < max_iter; ++it) {
+        const pv3 p1 = pl_closest(c1, n1, r1, p2);
+        p2 = pl_closest(c2, n2, r2, p1);
+        const double d = pv_norm(pv_sub(p1, p2));
+        if (prev - d <= tol) return d;
+        prev = d;
+    }
+    return prev;
+}
+
+static double pl_max3(double a, double b, double c) {
+    double m = a;
+    if (m < b) m = b;
+    if (m < c) m = c;
+    return m;
+}
+
+/* spherodisk.cpp:70-112 */
+static int pl_disks_within(pv3 c1, pv3 n1, double r1, pv3 c2, pv3 n2, double r2, double threshold) {
+    const pv3 d = pv_sub(c2, c1);
+    if (pv_norm(d) - r1 - r2 > threshold) return 0;
+    const double ndot = pv_dot(n1, n2);
+    const double t = 1.0 - ndot * ndot;
+    const double sin_tilt = sqrt(0.0 < t ? t : 0.0);
+    if (fabs(pv_dot(n1, d)) - r2 * sin_tilt > threshold) return 0;
+    if (fabs(pv_dot(n2, d)) - r1 * sin_tilt > threshold) return 0;
+    const double tol = 1e-12 * pl_max3(r1, r2, 1e-30);
+    pv3 p2 = pl_closest(c2, n2, r2, c1);
+    double prev = INFINITY;
+    int converged = 0;
+    for (int it = 0; it < 200; ++it) {
+        const pv3 p1 = pl_closest(c1, n1, r1, p2);
+        p2 = pl_closest(c2, n2, r2, p1);
+        const double dist = pv_norm(pv_sub(p1, p2));
+        if (dist <= threshold) return 1;
+        if (prev - dist <= tol) { converged = 1; break; }
+        prev = dist;
+    }
+    if (converged) return 0;
+    pv3 u = fabs(n2.v[0]) < 0.9 ? pv(1.0, 0.0, 0.0) : pv(0.0, 1.0, 0.0);
+    u = pv_sub(u, pv_mul(n2, pv_dot(u, n2)));
+    u = pv_mul(u, 1.0 / pv_norm(u));
+    const pv3 v = pv_cross(n2, u);
+    const double pi = 3.141592653589793238462643383279502884;
+    for (int k = 0; k < 32; ++k) {
+        const double a = 2.0 * pi * k / 32;
+        const pv3 seed = pv_add(c2, pv_mul(pv_add(pv_mul(u, cos(a)), pv_mul(v, sin(a))), r2));
+        if (pl_alternate(c1, n1, r1, c2, n2, r2, seed, tol, 64) <= threshold) return 1;
+    }
+    return 0;
+}
+
+/* spherodisk.hpp:62-68 with the minimum image of geometry.hpp:117-125 */
+int orc_pl_overlap(const double* L, const double* pa, const double* na, double Da, double ta,
+                   const double* pb, const double* nb, double Db, double tb) {
+    pv3 d;
+    for (int k = 0; k < 3; ++k) d.v[k] = orc_min_image(pb[k] - pa[k], L[k]);
+    const double cull = 0.5 * (Da + Db + ta + tb);
+    if (pv_dot(d, d) > cull * cull) return 0;
+    return pl_disks_within(pv(0.0, 0.0, 0.0), pv(na[0], na[1], na[2]), 0.5 * (Da - ta), d, pv(nb[0], nb[1], nb[2]),
+                           0.5 * (Db - tb), 0.5 * (ta + tb));
+}
+
+double orc_pl_disks_within(const double* c1, const double* n1, double r1, const double* c2, const double* n2, double r2,
+                           double threshold) {
+    return pl_disks_within(pv(c1[0], c1[1], c1[2]), pv(n1[0], n1[1], n1[2]), r1, pv(c2[0], c2[1], c2[2]),
+                           pv(n2[0], n2[1], n2[2]), r2, threshold);
+}
+
+/* spherodisk.hpp:29-34 */
+double orc_pl_measure(double D, double t) {
+    const double pi = 3.141592653589793238462643383279502884;
+    const double a = 0.5 * (D - t);
+    const double s = 0.5 * t;
+    return 2.0 * pi * a * a * s + pi * pi * a * s * s + (4.0 / 3.0) * pi * s * s * s;
+}
+
+/* spherodisk.hpp:84-91 propose_move with Philox draws: translation = unit vector of
+ * stream 0 (as spheres), rotation axis = unit vector of stream 1, angle c_r (cos/sin
+ * given), normal renormalised. */
+void orc_pl_propose(const double* L, const double* x, const double* nrm, double c_m, double cos_r, double sin_r,
+                    uint64_t seed, uint32_t slot, uint32_t attempt, uint32_t round_id, uint32_t iteration,
+                    double* pout, double* nout) {
+    orc_propose(3, L, x, c_m, seed, slot, attempt, round_id, iteration, pout);
+    double ax[3];
+    orc_unit_vector(3, seed, slot, attempt, 1, round_id, iteration, ax);
+    const pv3 axis = pv(ax[0], ax[1], ax[2]), v = pv(nrm[0], nrm[1], nrm[2]);
+    const pv3 r = pv_add(pv_add(pv_mul(v, cos_r), pv_mul(pv_cross(axis, v), sin_r)),
+                         pv_mul(axis, pv_dot(axis, v) * (1.0 - cos_r)));
+    const pv3 nn = pv_mul(r, 1.0 / pv_norm(r));
+    for (int k = 0; k < 3; ++k) nout[k] = nn.v[k];
+}
+
+/* One platelet round: the sphere sweep's visiting order (class, cell, slot) on the
+ * grid of cell size cell_size with bounding radii rb = (D + t) / 2 (shape.hpp:91-96),
+ * each trial tested as overlap(trial, other) (shape.hpp:539-546, trial first). */
+void orc_pl_sweep_round(const double* L, int64_t n, const double* x0, const double* n0, const double* D,
+                        const double* t, const int32_t* id, const int32_t* slot, double cell_size, double c_m,
+                        double cos_r, double sin_r, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
+                        double* xnew, double* nnew, uint8_t* acc) {
+    const int dim = 3;
+    double* rb = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    for (int64_t i = 0; i < n; ++i) rb[i] = 0.5 * (D[i] + t[i]);
+    int32_t dims[3] = {1, 1, 1};
+    double edge[3] = {1.0, 1.0, 1.0};
+    orc_grid_dims(dim, L, cell_size, dims, edge);
+    const double maxr = orc_max_radius(n, rb);
+    int32_t m[3], ncol[3];
+    orc_colouring(dim, dims, edge, maxr, c_m, m, ncol);
+    orc_csr nb;
+    build_pairs(dim, L, n, x0, rb, 2.0 * c_m, 0, &nb);
+    int64_t ncells = 1;
+    for (int a = 0; a < dim; ++a) ncells *= dims[a];
+    uint32_t* keys = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(n + 1));
+    orc_keys(dim, dims, edge, n, x0, keys);
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int64_t* cstart = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ncells + 1));
+    orc_sort_by_cell(n, keys, slot, ncells, order, cstart);
+    int32_t* cls = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    const int64_t nclass = (int64_t)ncol[0] * ncol[1] * ncol[2];
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t c[3];
+        orc_cell_coords(dim, dims, edge, x0 + i * dim, c);
+        int64_t k = 0;
+        for (int a = dim - 1; a >= 0; --a) k = k * ncol[a] + colour1(c[a], m[a], dims[a]);
+        cls[i] = (int32_t)k;
+    }
+    memcpy(xnew, x0, sizeof(double) * (size_t)(n * 3));
+    memcpy(nnew, n0, sizeof(double) * (size_t)(n * 3));
+    for (int64_t i = 0; i < n; ++i) acc[i] = ORC_NOT_ACCEPTED;
+    double p[3], q[3];
+    for (int64_t k = 0; k < nclass; ++k) {
+        for (int64_t qq = 0; qq < n; ++qq) {
+            const int64_t i = order[qq];
+            if (cls[i] != k) continue;
+            for (int l = 0; l < n_l; ++l) {
+                orc_pl_propose(L, x0 + i * 3, n0 + i * 3, c_m, cos_r, sin_r, seed, (uint32_t)slot[i], (uint32_t)l,
+                               round_id, iteration, p, q);
+                int ok = 1;
+                for (int64_t tt = nb.start[i]; tt < nb.start[i + 1] && ok; ++tt) {
+                    const int64_t j = nb.nbr[tt];
+                    if (id[j] == id[i]) continue;
+                    if (orc_pl_overlap(L, p, q, D[i], t[i], xnew + j * 3, nnew + j * 3, D[j], t[j])) ok = 0;
+                }
+                if (ok) {
+                    memcpy(xnew + i * 3, p, sizeof(double) * 3);
+                    memcpy(nnew + i * 3, q, sizeof(double) * 3);
+                    acc[i] = (uint8_t)l;
+                    break;
+                }
+            }
+        }
+    }
+    free(rb); free(keys); free(order); free(cstart); free(cls);
+    csr_free(&nb);
+}
+
+/* Any-collision in counting form for platelets: unordered pairs {i, j} with
+ * overlap(i, j) or overlap(j, i) (shape_any_collision tests every ordered pair). */
+int64_t orc_pl_overlap_pairs(const double* L, int64_t n, const double* x, const double* nrm, const double* D,
+                             const double* t, const int32_t* id) {
+    double* rb = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+    for (int64_t i = 0; i < n; ++i) rb[i] = 0.5 * (D[i] + t[i]);
+    orc_csr nb;
+    build_pairs(3, L, n, x, rb, 0.0, 0, &nb);
+    int64_t pairs = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t tt = nb.start[i]; tt < nb.start[i + 1]; ++tt) {
+            const int64_t j = nb.nbr[tt];
+            if (j <= i || id[j] == id[i]) continue;
+            if (orc_pl_overlap(L, x + i * 3, nrm + i * 3, D[i], t[i], x + j * 3, nrm + j * 3, D[j], t[j]) ||
+                orc_pl_overlap(L, x + j * 3, nrm + j * 3, D[j], t[j], x + i * 3, nrm + i * 3, D[i], t[i]))
+                ++pairs;
+        }
+    free(rb);
+    csr_free(&nb);
+    return pairs;
+}

@@ -90,6 +90,24 @@ void orc_overlap_stats(int dim, const double* L, int64_t n, const double* x, con
 /* candidate pair count for the given grid (integer, exact) */
 int64_t orc_candidate_pairs(int dim, const int32_t* dims, int64_t n, const uint32_t* keys);
 
+/* ---- platelets (spherodisk.hpp:16-99, spherodisk.cpp:14-112) ---------------------- */
+/* SpherodiskShape::overlap(a, b) on the periodic box L (argument order matters) */
+int orc_pl_overlap(const double* L, const double* pa, const double* na, double Da, double ta,
+                   const double* pb, const double* nb, double Db, double tb);
+/* disks_within (returns 0/1) */
+double orc_pl_disks_within(const double* c1, const double* n1, double r1, const double* c2, const double* n2,
+                           double r2, double threshold);
+double orc_pl_measure(double D, double t);
+void orc_pl_propose(const double* L, const double* x, const double* nrm, double c_m, double cos_r, double sin_r,
+                    uint64_t seed, uint32_t slot, uint32_t attempt, uint32_t round_id, uint32_t iteration,
+                    double* pout, double* nout);
+void orc_pl_sweep_round(const double* L, int64_t n, const double* x0, const double* n0, const double* D,
+                        const double* t, const int32_t* id, const int32_t* slot, double cell_size, double c_m,
+                        double cos_r, double sin_r, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
+                        double* xnew, double* nnew, uint8_t* acc);
+int64_t orc_pl_overlap_pairs(const double* L, int64_t n, const double* x, const double* nrm, const double* D,
+                             const double* t, const int32_t* id);
+
 /* ---- reductions ---------------------------------------------------------------- */
 double orc_max_radius(int64_t n, const double* r);
 /* volume fraction with the reference's sequential summation order (shape.hpp:557-563) */

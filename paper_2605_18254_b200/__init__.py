@@ -30,7 +30,8 @@ __all__ = [
     "Error", "ValidationError", "PlacementFailure", "CudaError", "NoDeviceError",
     "SrmParams", "Snapshot", "GenerateStatus", "GenerateResult", "ProgressRecord",
     "Context", "srm_generate", "relax_sweeps", "shake", "swell_all", "reorder_by_locality",
-    "rsa_place", "mix_seed", "K_RSA_DEFAULT_ATTEMPTS",
+    "rsa_place", "mix_seed", "K_RSA_DEFAULT_ATTEMPTS", "PlateletSnapshot", "srm_generate_platelets",
+    "rsa_platelets",
 ]
 
 K_RSA_DEFAULT_ATTEMPTS = 10000  # rsa.hpp:15 kRsaDefaultAttempts
@@ -178,13 +179,16 @@ class GenerateResult:
 class Context:
     """One device-resident particle state on one CUDA stream (srm_b200_ctx)."""
 
-    def __init__(self, box: Sequence[float], capacity: int, device: int = 0):
+    def __init__(self, box: Sequence[float], capacity: int, device: int = 0, shape: str = "sphere"):
+        """shape: "sphere" (disks in 2D, spheres in 3D) or "platelet" (SpherodiskShape, 3D)"""
         lib = _native.lib()
         self.box = tuple(float(v) for v in box)
         self.dim = len(self.box)
+        self.shape = shape
+        kind = {"sphere": 0, "platelet": 1}[shape]
         L = (C.c_double * self.dim)(*self.box)
         h = C.c_void_p()
-        _check(lib.srm_b200_create(self.dim, 0, L, int(capacity), int(device), C.byref(h)))
+        _check(lib.srm_b200_create(self.dim, kind, L, int(capacity), int(device), C.byref(h)))
         self._h = h
         self.capacity = int(capacity)
         self.n = 0
@@ -214,6 +218,37 @@ class Context:
         return _check(status, self._h, allow_iter_limit)
 
     # ---- state --------------------------------------------------------------------
+    def upload_platelets(self, pos, normal, diameter, thickness, id=None) -> None:
+        """platelet state: centres (n, 3), unit normals (n, 3), diameters, thicknesses"""
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        normal = np.ascontiguousarray(normal, dtype=np.float64).reshape(-1, 3)
+        n = len(pos)
+        dia = np.ascontiguousarray(np.broadcast_to(np.asarray(diameter, np.float64), (n,)))
+        thk = np.ascontiguousarray(np.broadcast_to(np.asarray(thickness, np.float64), (n,)))
+        idp = None
+        if id is not None:
+            id = np.ascontiguousarray(id, dtype=np.int32)
+            idp = _ptr(id)
+        self._c(_native.lib().srm_b200_upload_platelets(self._h, n, _ptr(pos), _ptr(normal), _ptr(dia), _ptr(thk),
+                                                        idp))
+        self.n = n
+
+    def download_platelets(self):
+        """(pos, normal, diameter, thickness, id) in storage-slot order"""
+        n = self.n
+        pos = np.empty((n, 3))
+        nrm = np.empty((n, 3))
+        dia = np.empty(n)
+        thk = np.empty(n)
+        ids = np.empty(n, np.int32)
+        self._c(_native.lib().srm_b200_download_platelets(self._h, _ptr(pos), _ptr(nrm), _ptr(dia), _ptr(thk),
+                                                          _ptr(ids)))
+        return pos, nrm, dia, thk, ids
+
+    def set_rotation(self, c_r: float) -> None:
+        """rotation angle of platelet moves for round()/rounds()"""
+        self._c(_native.lib().srm_b200_set_rotation(self._h, float(c_r)))
+
     def upload(self, pos: np.ndarray, radius: np.ndarray, id: Optional[np.ndarray] = None) -> None:
         pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, self.dim)
         radius = np.ascontiguousarray(radius, dtype=np.float64).reshape(-1)
@@ -363,11 +398,85 @@ def _ctx_for(snap: Snapshot, device: int) -> Context:
     return ctx
 
 
+@dataclass
+class PlateletSnapshot:
+    """engine.hpp:53-65 Snapshot<SpherodiskShape> (snapshots.hpp:11): thin circular platelets."""
+
+    box: Sequence[float]
+    pos: np.ndarray
+    normal: np.ndarray
+    diameter: np.ndarray
+    thickness: np.ndarray
+    id: Optional[np.ndarray] = None
+    volume_fraction: float = 0.0
+    iteration_count: int = 0
+    params: SrmParams = field(default_factory=SrmParams)
+    seed: int = 0
+
+    def __post_init__(self):
+        self.box = tuple(float(v) for v in self.box)
+        self.pos = np.ascontiguousarray(self.pos, dtype=np.float64).reshape(-1, 3)
+        self.normal = np.ascontiguousarray(self.normal, dtype=np.float64).reshape(-1, 3)
+        n = len(self.pos)
+        self.diameter = np.ascontiguousarray(np.broadcast_to(np.asarray(self.diameter, np.float64), (n,)))
+        self.thickness = np.ascontiguousarray(np.broadcast_to(np.asarray(self.thickness, np.float64), (n,)))
+        if self.id is None:
+            self.id = np.arange(n, dtype=np.int32)
+        self.id = np.ascontiguousarray(self.id, dtype=np.int32)
+
+    @property
+    def dim(self) -> int:
+        return 3
+
+    @property
+    def n(self) -> int:
+        return len(self.pos)
+
+    def refresh_volume_fraction(self) -> None:
+        """shape.hpp:83-89 with spherodisk_measure (spherodisk.hpp:29-34), sequential sum"""
+        pi = 3.141592653589793238462643383279502884
+        s = 0.0
+        for D, t in zip(self.diameter.tolist(), self.thickness.tolist()):
+            a = 0.5 * (D - t)
+            h = 0.5 * t
+            s += 2.0 * pi * a * a * h + pi * pi * a * h * h + (4.0 / 3.0) * pi * h * h * h
+        m = 1.0
+        for L in self.box:
+            m *= L
+        self.volume_fraction = s / m
+
+    def copy(self) -> "PlateletSnapshot":
+        return PlateletSnapshot(self.box, self.pos.copy(), self.normal.copy(), self.diameter.copy(),
+                                self.thickness.copy(), self.id.copy(), self.volume_fraction, self.iteration_count,
+                                self.params, self.seed)
+
+
+def srm_generate_platelets(initial: PlateletSnapshot, params: SrmParams,
+                           progress: Optional[Callable[[ProgressRecord], None]] = None,
+                           device: int = 0) -> GenerateResult:
+    """engine.hpp:176-260 srm_generate<SpherodiskShape> on the GPU."""
+    with Context(initial.box, max(initial.n, 1), device, shape="platelet") as ctx:
+        if initial.n:
+            ctx.upload_platelets(initial.pos, initial.normal, initial.diameter, initial.thickness, initial.id)
+        out = ctx.generate(params, initial.iteration_count, progress)
+        snap = initial.copy()
+        if initial.n:
+            snap.pos, snap.normal, snap.diameter, snap.thickness, snap.id = ctx.download_platelets()
+    snap.params = params
+    snap.seed = params.seed
+    snap.volume_fraction = out.volume_fraction
+    snap.iteration_count = out.iteration_count
+    status = GenerateStatus.Converged if out.status == OK else GenerateStatus.IterationLimitExceeded
+    return GenerateResult(status, snap, out.accepted_iterations, out.rounds, out.shake_rounds)
+
+
 def srm_generate(initial: Snapshot, params: SrmParams,
                  progress: Optional[Callable[[ProgressRecord], None]] = None,
                  device: int = 0) -> GenerateResult:
     """engine.hpp:176-260 srm_generate<S>: the initial snapshot is copied in and the
     result returned by value; the loop runs on the GPU."""
+    if isinstance(initial, PlateletSnapshot):
+        return srm_generate_platelets(initial, params, progress, device)
     with _ctx_for(initial, device) as ctx:
         out = ctx.generate(params, initial.iteration_count, progress)
         snap = initial.copy()
@@ -434,6 +543,26 @@ def rsa_place(radii, box: Sequence[float], max_attempts: int, seed: int):
         raise ValidationError("rsa_place: invalid radii or box")
     _check(st)
     return pos[:n], ids[:n]
+
+
+def rsa_platelets(n: int, diameter: float, aspect_ratio: float, box: Sequence[float], max_attempts: int, seed: int):
+    """recipes.cpp:107-148 with Rng(seed): returns (pos, normal, id); thickness =
+    diameter / aspect_ratio.  Bit-identical to the reference."""
+    L = (C.c_double * 3)(*[float(v) for v in box])
+    pos = np.empty((max(n, 1), 3))
+    nrm = np.empty((max(n, 1), 3))
+    ids = np.empty(max(n, 1), np.int32)
+    placed = C.c_int64()
+    st = _native.lib().srm_b200_rsa_platelets(int(n), float(diameter), float(aspect_ratio), L, int(max_attempts),
+                                              seed & 0xFFFFFFFFFFFFFFFF, _ptr(pos), _ptr(nrm), _ptr(ids),
+                                              C.byref(placed))
+    if st == PLACEMENT_FAILURE:
+        raise PlacementFailure(f"rsa_platelets: exceeded attempt budget at particle {placed.value}", placed.value,
+                               max_attempts)
+    if st == INVALID:
+        raise ValidationError("rsa_platelets: invalid size, aspect ratio or box")
+    _check(st)
+    return pos[:n], nrm[:n], ids[:n]
 
 
 def mix_seed(seed: int, stream: int) -> int:

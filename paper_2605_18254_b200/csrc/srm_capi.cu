@@ -61,6 +61,7 @@ T* dalloc(int64_t count) {
 struct srm_b200_ctx {
     int dim = 3;
     int shape = 0;
+    double c_r = 0.0;  // rotation angle of platelet moves (srm_b200_set_rotation / params.c_r)
     int device = 0;
     Box box{};
     int64_t cap = 0;
@@ -74,22 +75,13 @@ struct srm_b200_ctx {
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
-    int4* work = nullptr;        // (colour class, rank) work lists: (index, slot, cell end, 0)
-    uint32_t* bcount = nullptr;  // bucket counts / starts / cursors, [ncls * kRanks + 1]
-    uint32_t* bstart = nullptr;
-    uint32_t* bcursor = nullptr;
-    int64_t bucket_cap = 0;
-    unsigned long long* qcursor = nullptr;  // per-class take cursors of k_sweep_queue
-    int64_t qcursor_cap = 0;
-    int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_queue (set in init)
+    int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_warpq (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
     // 0: shared-memory bricks (3D) / half-stencil pairs, 1: full stencil per particle,
     // 2: half-stencil pairs per particle
     int near_mode = std::getenv("SRM_B200_NEAR") ? std::atoi(std::getenv("SRM_B200_NEAR")) : 0;
     // srm_generate: the device-resident graph loop (default) or the host-driven loop
     bool device_loop = std::getenv("SRM_B200_HOST_LOOP") == nullptr;
-    // 2: warp queues (default), 0: CTA work queue, 1: (class, rank) launches
-    int sweep_mode = std::getenv("SRM_B200_SWEEP") ? std::atoi(std::getenv("SRM_B200_SWEEP")) : 2;
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
@@ -183,26 +175,39 @@ struct srm_b200_ctx {
     }
 
     // ---------------------------------------------------------------------------
+    bool platelets() const { return shape == SRM_B200_PLATELET; }
     void alloc_state(State& s) {
         s.rec = dalloc<double4>(cap);
         s.id = dalloc<int32_t>(cap);
         s.slot = dalloc<int32_t>(cap);
+        if (platelets()) s.aux = dalloc<double4>(cap);
     }
     static void free_state(State& s) {
         cudaFree(s.rec);
         cudaFree(s.id);
         cudaFree(s.slot);
+        cudaFree(s.aux);
     }
     // exchange the particle buffers of two states (the sorted state's fp32 copy stays)
     static void swap_state(State& a, State& b) {
         std::swap(a.rec, b.rec);
         std::swap(a.id, b.id);
         std::swap(a.slot, b.slot);
+        std::swap(a.aux, b.aux);
     }
 
     void init() {
         SRM_CUDA(cudaSetDevice(device));
         SRM_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        if (platelets()) {  // spherodisk.cpp:60-66 rim seed angles 2 pi k / 32 through the host libm
+            pl::SeedTable t;
+            for (int k = 0; k < pl::kSeeds; ++k) {
+                const double a = 2.0 * 3.141592653589793238462643383279502884 * k / pl::kSeeds;
+                t.c[k] = std::cos(a);
+                t.s[k] = std::sin(a);
+            }
+            SRM_CUDA(cudaMemcpyToSymbol(c_seed_table, &t, sizeof(t)));
+        }
         alloc_state(P);
         alloc_state(Q);
         alloc_state(S);
@@ -214,14 +219,10 @@ struct srm_b200_ctx {
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearRow);
-        work = dalloc<int4>(cap);
-        const int work_smem = 2 * kBucketSmem * 4;
-        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
-        SRM_CUDA(cudaFuncSetAttribute(k_work_scatter<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, work_smem));
         SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
         {
             int per_sm = 0, sms = 0;
-            SRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_queue<3>, kSweepThreads, 0));
+            SRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_warpq<3>, kSweepThreads, 0));
             SRM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
             queue_ctas = std::max(1, per_sm) * std::max(1, sms);
         }
@@ -243,7 +244,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(nbr); cudaFree(S.xf); cudaFree(work); cudaFree(bcount); cudaFree(bstart); cudaFree(bcursor); cudaFree(qcursor);
+        cudaFree(nbr); cudaFree(S.xf); 
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -291,7 +292,7 @@ struct srm_b200_ctx {
     void set_grid(const GridParams& g) {
         ensure_cells(g.ncells);
         // cells per colour class: on each axis a body colour v < m has
-        // floor(n / m) cells, a remainder colour one; class offsets into the work lists
+        // floor(n / m) cells, a remainder colour one (sweep launch sizes)
         std::vector<int64_t> off(static_cast<size_t>(g.ncls) + 1, 0);
         for (int64_t k = 0; k < g.ncls; ++k) {
             int64_t rem = k, cells = 1;
@@ -303,24 +304,6 @@ struct srm_b200_ctx {
             off[k + 1] = off[k] + cells;
         }
         if (off[g.ncls] != g.ncells) throw std::logic_error("colour classes do not tile the grid");
-        const int64_t nbk = static_cast<int64_t>(g.ncls) * kRanks;
-        if (g.ncls > qcursor_cap) {
-            cudaFree(qcursor);
-            qcursor = nullptr;
-            qcursor_cap = g.ncls;
-            qcursor = dalloc<unsigned long long>(qcursor_cap);
-        }
-        if (nbk + 1 > bucket_cap) {
-            cudaFree(bcount);
-            cudaFree(bstart);
-            cudaFree(bcursor);
-            bcount = nullptr; bstart = nullptr; bcursor = nullptr;
-            bucket_cap = nbk + 1;
-            bcount = dalloc<uint32_t>(bucket_cap);
-            bstart = dalloc<uint32_t>(bucket_cap);
-            bcursor = dalloc<uint32_t>(bucket_cap);
-            SRM_CUDA(cudaMemsetAsync(bcount, 0, sizeof(uint32_t) * bucket_cap, stream));  // k_work_scan re-zeroes
-        }
         cls_cells_h.assign(off.begin(), off.end());
         k_set_grid<<<1, 1, 0, stream>>>(gp, g);
         launched();
@@ -337,6 +320,8 @@ struct srm_b200_ctx {
         v.key.k1 = static_cast<uint32_t>(seed >> 32);
         v.key.round_id = round_id & 0xFFFFFFu;
         v.key.iteration = iteration;
+        v.cos_r = std::cos(c_r);  // spherodisk.hpp:50-51, host libm as the reference
+        v.sin_r = std::sin(c_r);
         k_set_round<<<1, 1, 0, stream>>>(rp, v);
         launched();
     }
@@ -369,8 +354,8 @@ struct srm_b200_ctx {
     }
 
     // One round on T (T is rewritten in this round's sorted order); gp must be set.
-    // grid rebuild, near lists + work lists, then the coloured Gauss-Seidel sweep (one
-    // launch per (colour class, rank)), then the overlap reduction over the non-movers.
+    // grid rebuild, near lists, then the coloured Gauss-Seidel sweep (one launch per
+    // colour class), then the overlap reduction (non-movers; all pairs for platelets).
     void round(State& T, double c_m, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,
                bool with_stats, bool with_candidates, bool write_acc = false) {
         if (n_l > kMaxPhases) throw Invalid{"n_l > 254 is not supported by the B200 path"};
@@ -379,24 +364,7 @@ struct srm_b200_ctx {
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
         if (write_acc) SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
         {
-            FamScope fs(this, 2);  // near lists (+ the (class, rank) work lists of sweep modes 0/1)
-            if (sweep_mode != 2) {  // the warp-queue sweep walks the class lattice itself
-                const int nbk = hg.ncls * kRanks;
-                const bool local = nbk <= kBucketSmem;
-                const int wb = blocks_for(n, kWorkBlock * kWorkPer);
-                if (dim == 2)
-                    k_work_count<2><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
-                else
-                    k_work_count<3><<<wb, kWorkBlock, local ? nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, bcount);
-                k_work_scan<<<1, 1024, 0, stream>>>(gp, bcount, bstart, bcursor);
-                if (dim == 2)
-                    k_work_scatter<2><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot,
-                                                                                           bcursor, work);
-                else
-                    k_work_scatter<3><<<wb, kWorkBlock, local ? 2 * nbk * 4 : 0, stream>>>(n, gp, cell_start, skey, S.slot,
-                                                                                           bcursor, work);
-                launched(3);
-            }
+            FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
             if (hg.near_kind == 0) {  // pairs once, through shared-memory bricks
                 k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
@@ -413,7 +381,7 @@ struct srm_b200_ctx {
                 launched(1);
             }
         }
-        if (sweep_mode == 2) {
+        {
             FamScope fs(this, 1);
             for (int cls = 0; cls < hg.ncls; ++cls) {
                 const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
@@ -422,46 +390,21 @@ struct srm_b200_ctx {
                 if (dim == 2)
                     k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
+                else if (platelets())
+                    k_sweep_warpq<3, true><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr,
+                                                                               acc, active, stats);
                 else
                     k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
             }
             launched(hg.ncls);
-        } else if (sweep_mode == 0) {
-            FamScope fs(this, 1);
-            SRM_CUDA(cudaMemsetAsync(qcursor, 0, sizeof(unsigned long long) * hg.ncls, stream));
-            for (int cls = 0; cls < hg.ncls; ++cls) {
-                const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
-                // persistent CTAs: one full wave at most
-                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), queue_ctas)));
-                if (dim == 2)
-                    k_sweep_queue<2><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
-                                                                         work, qcursor + cls, nbr, acc, active, stats);
-                else
-                    k_sweep_queue<3><<<grid, kSweepThreads, 0, stream>>>(cls, S, box, gp, rp, cell_start, skey, bstart,
-                                                                         work, qcursor + cls, nbr, acc, active, stats);
-            }
-            launched(hg.ncls);
-        } else {
-            FamScope fs(this, 1);
-            for (int cls = 0; cls < hg.ncls; ++cls) {
-                const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
-                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), 148 * 32)));
-                for (int rank = 0; rank < kRanks; ++rank) {
-                    if (dim == 2)
-                        k_sweep_work<2><<<grid, kSweepThreads, 0, stream>>>(cls, rank, S, box, gp, rp, cell_start, skey, bstart,
-                                                                            work, nbr, acc, active, stats);
-                    else
-                        k_sweep_work<3><<<grid, kSweepThreads, 0, stream>>>(cls, rank, S, box, gp, rp, cell_start, skey, bstart,
-                                                                            work, nbr, acc, active, stats);
-                }
-            }
-            launched(hg.ncls * kRanks);
         }
         if (with_stats) {
             FamScope fs(this, 3);
             const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
-            if (dim == 2)
+            if (platelets())
+                k_overlap_pl<<<blocks_for(n, 256), 256, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
+            else if (dim == 2)
                 k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
             else
                 k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
@@ -553,6 +496,8 @@ struct srm_b200_ctx {
         hc.dim = dim;
         hc.near_mode = near_mode;
         hc.seed = p.seed;
+        hc.cos_r = std::cos(p.c_r);
+        hc.sin_r = std::sin(p.c_r);
         hc.f = f0;
         hc.max_r = max_r0;
         hc.recs = d_recs;
@@ -585,7 +530,7 @@ struct srm_b200_ctx {
                     capture_into(add_conditional(stream, h_copy, cudaGraphCondTypeIf), cap_streams[3],
                                  [&]() { copy_state(P, Q); });
                     capture_into(add_conditional(stream, h_scale, cudaGraphCondTypeIf), cap_streams[3], [&]() {
-                        k_scale_radius_ctl<<<nb, 256, 0, stream>>>(n, Q.rec, ctl);
+                        k_scale_radius_ctl<<<nb, 256, 0, stream>>>(n, Q.rec, Q.aux, ctl);
                     });
                     // one round on Q
                     grid_build(Q, nc_max);
@@ -603,6 +548,10 @@ struct srm_b200_ctx {
                         if (dim == 2)
                             k_sweep_warpq<2><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
                                                                                        skey, nbr, acc, active, stats);
+                        else if (platelets())
+                            k_sweep_warpq<3, true><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp,
+                                                                                             cell_start, skey, nbr, acc, active,
+                                                                                             stats);
                         else
                             k_sweep_warpq<3><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
                                                                                        skey, nbr, acc, active, stats);
@@ -610,14 +559,16 @@ struct srm_b200_ctx {
                     });
                     const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
                     if (dim == 2) k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
+                    else if (platelets())
+                        k_overlap_pl<<<blocks_for(n, 256), 256, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
                     else k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
                     copy_state(S, Q);
                     k_gen_after<<<1, 1, 0, stream>>>(ctl, stats, h_commit, h_f, h_reorder);
                     capture_into(add_conditional(stream, h_commit, cudaGraphCondTypeIf), cap_streams[3],
                                  [&]() { copy_state(Q, P); });
                     capture_into(add_conditional(stream, h_f, cudaGraphCondTypeIf), cap_streams[3], [&]() {
-                        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, P.rec, red_part_sum, red_part_max);
-                        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, P.rec, red_part_sum, red_part_max);
+                        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, P.rec, red_part_sum, red_part_max, P.aux);
+                        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, P.rec, red_part_sum, red_part_max, P.aux);
                         k_reduce_final<<<1, 256, 0, stream>>>(red_part_sum, red_part_max, red_out);
                         k_gen_f<<<1, 1, 0, stream>>>(ctl, red_out);
                     });
@@ -674,8 +625,8 @@ struct srm_b200_ctx {
 
     // fixed-order reductions over the radii of T: {sum of measures, max radius}
     void reduce(const State& T, double* sum_measure, double* max_r) {
-        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, T.rec, red_part_sum, red_part_max);
-        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, T.rec, red_part_sum, red_part_max);
+        if (dim == 2) k_reduce_partials<2><<<kRedBlocks, 256, 0, stream>>>(n, T.rec, red_part_sum, red_part_max, T.aux);
+        else k_reduce_partials<3><<<kRedBlocks, 256, 0, stream>>>(n, T.rec, red_part_sum, red_part_max, T.aux);
         k_reduce_final<<<1, 256, 0, stream>>>(red_part_sum, red_part_max, red_out);
         launched(2);
         SRM_CUDA(cudaMemcpyAsync(h_red, red_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -700,7 +651,7 @@ struct srm_b200_ctx {
     }
 
     void scale_radius(State& T, double factor) {
-        k_scale_radius<<<blocks_for(n, 256), 256, 0, stream>>>(n, T.rec, factor);
+        k_scale_radius<<<blocks_for(n, 256), 256, 0, stream>>>(n, T.rec, T.aux, factor);
         launched();
     }
 };
@@ -756,7 +707,11 @@ int srm_b200_create(int dim, int shape_kind, const double* box_lengths, int64_t 
     if (!out) return SRM_B200_INVALID;
     *out = nullptr;
     if (dim != 2 && dim != 3) { g_create_error = "dim must be 2 or 3"; return SRM_B200_INVALID; }
-    if (shape_kind != SRM_B200_SPHERE) { g_create_error = "unsupported shape kind"; return SRM_B200_INVALID; }
+    if (shape_kind != SRM_B200_SPHERE && shape_kind != SRM_B200_PLATELET) {
+        g_create_error = "unsupported shape kind";
+        return SRM_B200_INVALID;
+    }
+    if (shape_kind == SRM_B200_PLATELET && dim != 3) { g_create_error = "platelets are 3D"; return SRM_B200_INVALID; }
     if (capacity < 1) { g_create_error = "capacity must be >= 1"; return SRM_B200_INVALID; }
     for (int a = 0; a < dim; ++a)
         if (!(box_lengths[a] > 0.0)) {
@@ -803,6 +758,7 @@ int64_t srm_b200_count(const srm_b200_ctx* ctx) { return ctx ? ctx->n : 0; }
 
 int srm_b200_upload(srm_b200_ctx* c, int64_t n, const double* pos, const double* radius, const int32_t* id) {
     return guarded(c, [&]() -> int {
+        if (c->platelets()) throw Invalid{"upload: platelet context (use srm_b200_upload_platelets)"};
         if (n < 0 || n > c->cap) throw Invalid{"upload: n exceeds the context capacity"};
         if (n > 0 && (!pos || !radius)) throw Invalid{"upload: null pointer"};
         c->n = n;
@@ -839,6 +795,63 @@ int srm_b200_download(srm_b200_ctx* c, double* pos, double* radius, int32_t* id)
         if (radius) SRM_CUDA(cudaMemcpyAsync(radius, drad, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         if (id) SRM_CUDA(cudaMemcpyAsync(id, c->S.id, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
         c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_upload_platelets(srm_b200_ctx* c, int64_t n, const double* pos, const double* normal,
+                              const double* diameter, const double* thickness, const int32_t* id) {
+    return guarded(c, [&]() -> int {
+        if (!c->platelets()) throw Invalid{"upload_platelets: not a platelet context"};
+        if (n < 0 || n > c->cap) throw Invalid{"upload: n exceeds the context capacity"};
+        if (n > 0 && (!pos || !normal || !diameter || !thickness)) throw Invalid{"upload: null pointer"};
+        c->n = n;
+        if (n == 0) return SRM_B200_OK;
+        // stage through the sorted state's buffers: pos at [0, 3n), normal at [3 cap, ...)
+        double* st = reinterpret_cast<double*>(c->S.rec);
+        double* sa = reinterpret_cast<double*>(c->S.aux);
+        SRM_CUDA(cudaMemcpyAsync(st, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+        SRM_CUDA(cudaMemcpyAsync(st + 3 * c->cap, diameter, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        SRM_CUDA(cudaMemcpyAsync(sa, normal, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+        SRM_CUDA(cudaMemcpyAsync(sa + 3 * c->cap, thickness, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        int32_t* did = nullptr;
+        if (id) {
+            SRM_CUDA(cudaMemcpyAsync(c->S.id, id, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+            did = c->S.id;
+        }
+        k_unpack_pl<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, st, sa, st + 3 * c->cap, sa + 3 * c->cap, did, c->P);
+        c->launched();
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_download_platelets(srm_b200_ctx* c, double* pos, double* normal, double* diameter, double* thickness,
+                                int32_t* id) {
+    return guarded(c, [&]() -> int {
+        if (!c->platelets()) throw Invalid{"download_platelets: not a platelet context"};
+        const int64_t n = c->n;
+        if (n == 0) return SRM_B200_OK;
+        double* st = reinterpret_cast<double*>(c->S.rec);
+        double* sa = reinterpret_cast<double*>(c->S.aux);
+        k_pack_pl<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->P, st, sa, st + 3 * c->cap, sa + 3 * c->cap, c->S.id);
+        c->launched();
+        if (pos) SRM_CUDA(cudaMemcpyAsync(pos, st, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (normal) SRM_CUDA(cudaMemcpyAsync(normal, sa, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+        if (diameter)
+            SRM_CUDA(cudaMemcpyAsync(diameter, st + 3 * c->cap, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        if (thickness)
+            SRM_CUDA(cudaMemcpyAsync(thickness, sa + 3 * c->cap, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        if (id) SRM_CUDA(cudaMemcpyAsync(id, c->S.id, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_set_rotation(srm_b200_ctx* c, double c_r) {
+    return guarded(c, [&]() -> int {
+        if (!(c_r >= 0.0)) throw Invalid{"params: c_r must be >= 0"};
+        c->c_r = c_r;
         return SRM_B200_OK;
     });
 }
@@ -950,7 +963,10 @@ int srm_b200_overlap_stats(srm_b200_ctx* c, double cell_size, srm_b200_round_sta
             SRM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(StatsDev), c->stream));
             {
                 srm_b200_ctx::FamScope fs(c, 3);
-                if (c->dim == 2)
+                if (c->platelets())
+                    k_overlap_pl<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey,
+                                                                          c->stats);
+                else if (c->dim == 2)
                     k_overlap_full<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, 1, c->stats);
                 else
                     k_overlap_full<3><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, 1, c->stats);
@@ -1011,6 +1027,7 @@ int srm_b200_rounds(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint
 }
 
 int srm_b200_relax_sweeps(srm_b200_ctx* c, double c_m, double c_r, int n_l, int sweeps, uint64_t key) {
+    if (c) c->c_r = c_r;  // platelet rotation angle (ignored by disks/spheres)
     (void)c_r;  // rotation rate is ignored by disks/spheres (shape.hpp:500-502)
     return guarded(c, [&]() -> int {
         const int64_t n = c->n;
@@ -1074,6 +1091,7 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
     return guarded(c, [&]() -> int {
         if (!params) throw Invalid{"params: null"};
         const srm_b200_params p = *params;
+        c->c_r = p.c_r;
         validate_params(p);
         const int N = c->dim;
         double min_len = c->box.L[0];

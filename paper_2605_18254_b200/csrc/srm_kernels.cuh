@@ -5,7 +5,7 @@
 //   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
 //   near lists     k_near_lists (round-start neighbours within the trial reach)
 //   near lists     k_near_lists (+ the (colour class, rank) work lists of the sweep)
-//   migrate        k_sweep_work, one launch per (colour class, rank in cell)
+//   migrate        k_sweep_warpq, one launch per colour class (warp queues)
 //   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
 // All kernels read the grid / round parameters from device memory so that the same
 // launches can be replayed from a CUDA graph.  DESIGN.md §2-§4 has the data layout
@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "srm_device.cuh"
+#include "srm_platelet.cuh"
 
 namespace srmb {
 
@@ -58,7 +59,6 @@ struct GridParams {
     // fp32 prefilter (near_candidates): margin above the fp32 rounding of coordinates
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
-    int32_t nrank;      // ranks in cell with their own sweep step (kRanks)
     int32_t near_kind;   // near lists: 0 shared-memory bricks, 1 half stencil, 2 full stencil
     int32_t ntiles;      // bricks of k_near_tiles (near_kind 0)
     FastDiv fd_dims[3];  // division by dims[a]
@@ -140,7 +140,6 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
         g.ncls *= g.col_n[a];
         g.cls_cells *= (g.dims[a] + g.col_m[a] - 1) / g.col_m[a];
     }
-    g.nrank = 3;
     for (int a = 0; a < 3; ++a) {
         g.fd_dims[a] = make_fastdiv(static_cast<uint32_t>(g.dims[a]));
         g.fd_m[a] = make_fastdiv(static_cast<uint32_t>(g.col_m[a]));
@@ -174,16 +173,25 @@ struct RoundParams {
     int32_t n_l;
     int32_t write_acc;  // also record the accepted trial per particle (parity outputs)
     RngKey key;
+    double cos_r, sin_r;  // platelets: cos/sin of the rotation angle c_r (host libm)
 };
 
 // Per-particle state: one 32-byte record (x, y, z, r) per particle (z = 0 in 2D) -- a
 // single sector per gather / neighbour read -- plus the reference id and storage slot.
 struct State {
-    double4* rec;
+    double4* rec;   // (x, y, z, r) -- platelets: (x, y, z, diameter)
     int32_t* id;
     int32_t* slot;
-    float4* xf;  // sorted fp32 copy (x, y, z, r) for the near-list prefilter; only in S
+    float4* xf;     // sorted fp32 copy (x, y, z, bounding radius) for the near-list screen; only in S
+    double4* aux;   // platelets only: (nx, ny, nz, thickness); null for disks/spheres
 };
+
+// rim-seed cos/sin table of the platelet overlap fallback (set from the host, glibc)
+__constant__ pl::SeedTable c_seed_table;
+
+__device__ __forceinline__ double bounding_radius(const double4 r, const double4* aux, int64_t i) {
+    return aux ? 0.5 * (r.w + aux[i].w) : r.w;  // shape.hpp:91-96 / spherodisk.hpp:94-96
+}
 
 template <int D>
 __device__ __forceinline__ void rec_pos(const double4 v, double* p) {
@@ -389,9 +397,15 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ perm, const uint
         const int32_t src = perm[q];
         const double4 v = T.rec[src];
         S.rec[q] = v;
+        double rb = v.w;
+        if (T.aux) {
+            const double4 a = T.aux[src];
+            S.aux[q] = a;
+            rb = 0.5 * (v.w + a.w);
+        }
         if (S.xf)
             S.xf[q] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y), static_cast<float>(v.z),
-                                  static_cast<float>(v.w));
+                                  static_cast<float>(rb));
         S.id[q] = T.id[src];
         S.slot[q] = T.slot[src];
         skey[q] = key[src];
@@ -468,9 +482,6 @@ constexpr int kNearCap = kNearRow - 2;
 __device__ __forceinline__ int32_t near_entry(const int32_t* row, int f, int t) {
     return t < f ? row[2 + t] : row[kNearRow - 1 - (t - f)];
 }
-constexpr int kRanks = 3;       // sweep steps per class: ranks 0, 1 and 2+ (the rank-2 thread
-                                // sweeps the rest of its cell in slot order)
-constexpr int kBucketSmem = 8192;  // (class, rank) buckets aggregated in shared memory
 
 // Near candidates of sorted particle q: every j whose round-start distance is within
 // ri + rj + 2 c_m (every j a trial of q can touch while j sits within c_m of its start).
@@ -883,137 +894,7 @@ __global__ void k_near_zero(int64_t n, int32_t* __restrict__ nbr) {
     }
 }
 
-// Work lists of the sweep: every particle of rank r < kRanks in its cell goes to bucket
-// (colour class c, r) = c * kRanks + r; buckets are laid out back to back (bstart, an
-// exclusive scan of the counts).  The order inside a bucket does not matter (cells of
-// one class never interact).  count -> scan -> scatter, CTA-aggregated atomics.
-constexpr int kWorkBlock = 1024;
-constexpr int kWorkPer = 8;  // particles per thread: 8192 per CTA
 
-template <int D>
-__device__ __forceinline__ int bucket_of(const GridParams& g, const int64_t* __restrict__ cs, uint32_t key,
-                                         int64_t q) {
-    const int64_t rank = q - cs[key];
-    if (rank >= kRanks) return -1;
-    return class_of_key<D>(g, key) * kRanks + static_cast<int>(rank);
-}
-
-template <int D>
-__global__ void __launch_bounds__(kWorkBlock) k_work_count(int64_t n, const GridParams* __restrict__ gp,
-                                                           const int64_t* __restrict__ cs,
-                                                           const uint32_t* __restrict__ skey,
-                                                           uint32_t* __restrict__ bcount) {
-    extern __shared__ uint32_t hist[];
-    const GridParams& g = *gp;
-    const int nb = g.ncls * kRanks;
-    const bool local = nb <= kBucketSmem;
-    if (local)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
-    for (int k = 0; k < kWorkPer; ++k) {
-        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        if (q >= n) break;
-        const int b = bucket_of<D>(g, cs, skey[q], q);
-        if (b < 0) continue;
-        if (local) atomicAdd(&hist[b], 1u);
-        else atomicAdd(&bcount[b], 1u);
-    }
-    __syncthreads();
-    if (local)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x)
-            if (hist[b]) atomicAdd(&bcount[b], hist[b]);
-}
-
-// single CTA: exclusive scan of the bucket counts; cursors start at the bucket starts
-__global__ void k_work_scan(const GridParams* __restrict__ gp, uint32_t* __restrict__ bcount,
-                            uint32_t* __restrict__ bstart, uint32_t* __restrict__ cursor) {
-    const int nb = gp->ncls * kRanks;
-    __shared__ uint32_t carry;
-    __shared__ uint32_t wsum[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
-        const int b = b0 + threadIdx.x;
-        const uint32_t v = b < nb ? bcount[b] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) wsum[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            const uint32_t w = lane < static_cast<int>(blockDim.x >> 5) ? wsum[lane] : 0u;
-            uint32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += t;
-            }
-            wsum[lane] = wi - w;
-        }
-        __syncthreads();
-        const uint32_t ex = carry + wsum[wid] + incl - v;
-        if (b < nb) {
-            bstart[b] = ex;
-            cursor[b] = ex;
-            bcount[b] = 0u;  // ready for the next round's count
-        }
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = ex + v;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) bstart[nb] = carry;
-}
-
-// work item: (sorted index, storage slot, end of its cell, 0) -- one 16-byte load
-__device__ __forceinline__ int4 work_item(int64_t q, const int32_t* __restrict__ slot, const int64_t* __restrict__ cs,
-                                          const uint32_t* __restrict__ skey) {
-    return make_int4(static_cast<int32_t>(q), slot[q], static_cast<int32_t>(cs[skey[q] + 1]), 0);
-}
-
-template <int D>
-__global__ void __launch_bounds__(kWorkBlock) k_work_scatter(int64_t n, const GridParams* __restrict__ gp,
-                                                             const int64_t* __restrict__ cs,
-                                                             const uint32_t* __restrict__ skey,
-                                                             const int32_t* __restrict__ slot,
-                                                             uint32_t* __restrict__ cursor, int4* __restrict__ work) {
-    extern __shared__ uint32_t hist[];  // [nb] counts, then [nb] CTA bases
-    const GridParams& g = *gp;
-    const int nb = g.ncls * kRanks;
-    const bool local = nb <= kBucketSmem;
-    uint32_t* base = hist + (local ? nb : 0);
-    if (local)
-        for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kWorkBlock * kWorkPer;
-    int myb[kWorkPer];
-    uint32_t myl[kWorkPer];
-#pragma unroll
-    for (int k = 0; k < kWorkPer; ++k) {
-        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        myb[k] = -1;
-        if (q >= n) continue;
-        myb[k] = bucket_of<D>(g, cs, skey[q], q);
-        if (myb[k] < 0) continue;
-        if (local) myl[k] = atomicAdd(&hist[myb[k]], 1u);
-        else work[atomicAdd(&cursor[myb[k]], 1u)] = work_item(q, slot, cs, skey);
-    }
-    if (!local) return;
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x)
-        if (hist[b]) base[b] = atomicAdd(&cursor[b], hist[b]);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kWorkPer; ++k) {
-        if (myb[k] < 0) continue;
-        const int64_t q = b0 + static_cast<int64_t>(k) * kWorkBlock + threadIdx.x;
-        work[base[myb[k]] + myl[k]] = work_item(q, slot, cs, skey);
-    }
-}
 
 template <int D>
 __device__ __forceinline__ void sweep_particle(int64_t q, int32_t sl, const State& S, const Box& box,
@@ -1103,38 +984,6 @@ __device__ __forceinline__ void sweep_particle(int64_t q, int32_t sl, const Stat
 #endif
 constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
-// One (colour class, rank) step of the sweep: a thread per particle of the bucket.  The
-// bucket holds the rank-`rank` particle of every cell of the class that has one (in no
-// particular order: cells of one class never interact); the last rank's thread also
-// sweeps the rest of its (crowded) cell, in slot order.  The launch sequence over
-// (class, rank) reproduces the sequential sweep of orc_sweep_round bit for bit.
-template <int D>
-__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_work(int cls, int rank, State S, Box box,
-                                                              const GridParams* __restrict__ gp,
-                                                              const RoundParams* __restrict__ rpp,
-                                                              const int64_t* __restrict__ cs,
-                                                              const uint32_t* __restrict__ skey,
-                                                              const uint32_t* __restrict__ bstart,
-                                                              const int4* __restrict__ work,
-                                                              const int32_t* __restrict__ nbr,
-                                                              uint8_t* __restrict__ acc, int32_t* __restrict__ active,
-                                                              StatsDev* stats) {
-    const GridParams& g = *gp;
-    if (cls >= g.ncls) return;
-    const int64_t lo = bstart[cls * kRanks + rank];
-    const int64_t cnt = bstart[cls * kRanks + rank + 1] - lo;
-    const int4* list = work + lo;
-    const RoundParams rp = *rpp;
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < cnt;
-         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int4 w = list[t];  // (sorted index, storage slot, cell end)
-        sweep_particle<D>(w.x, w.y, S, box, g, rp, cs, skey, nbr, acc, active, stats);
-        if (rank == kRanks - 1) {  // the rest of a crowded cell, in slot order
-            for (int64_t q = w.x + 1; q < w.z; ++q)
-                sweep_particle<D>(q, S.slot[q], S, box, g, rp, cs, skey, nbr, acc, active, stats);
-        }
-    }
-}
 
 // One trial of particle q (slot sl, round-start position xi, radius ri): propose trial l
 // and test it against the live positions of q's near list (or, for an overflowed list,
@@ -1177,106 +1026,43 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     return ok;
 }
 
-// One colour class of the sweep with a CTA-local work queue.  Items are (particle,
-// trial); the CTA starts with one rank-0 particle (first of its cell) per thread and
-// runs rounds of ONE trial per item: a clear trial publishes the move, a blocked one
-// re-queues (particle, trial + 1), an exhausted one reverts (non-mover list); a
-// particle that is done hands its cell on to the next particle (slot order).  So every
-// round keeps the live items dense in the warps whatever the trial counts and cell
-// occupancies.  Visiting order per cell and the trials of each particle are those of
-// the sequential sweep; cells of one class never interact, so the result equals
-// orc_sweep_round bit for bit.
-struct QItem {
-    int32_t q, l, sl, end;  // sorted index, next trial, storage slot, end of its cell
-};
-
-template <int D>
-__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_queue(int cls, State S, Box box,
-                                                                               const GridParams* __restrict__ gp,
-                                                                               const RoundParams* __restrict__ rpp,
-                                                                               const int64_t* __restrict__ cs,
-                                                                               const uint32_t* __restrict__ skey,
-                                                                               const uint32_t* __restrict__ bstart,
-                                                                               const int4* __restrict__ work,
-                                                                               unsigned long long* __restrict__ cursor,
-                                                                               const int32_t* __restrict__ nbr,
-                                                                               uint8_t* __restrict__ acc,
-                                                                               int32_t* __restrict__ active,
-                                                                               StatsDev* stats) {
-    __shared__ QItem qbuf[2][kSweepThreads];
-    __shared__ int qn[2];
-    __shared__ long long take_base;
-    __shared__ int take_n;
-    const GridParams& g = *gp;
-    if (cls >= g.ncls) return;
-    const RoundParams rp = *rpp;
-    const int64_t lo = bstart[cls * kRanks], cnt = bstart[cls * kRanks + 1] - lo;
-    int cur = 0;
-    if (threadIdx.x == 0) {
-        qn[0] = 0;
-        qn[1] = 0;
+// Platelet version of trial_clear: trial l of q = translation by c_m along the unit
+// vector of Philox stream 0 and rotation of the normal by c_r about the unit vector of
+// stream 1 (spherodisk.hpp:84-91); tested as overlap(trial, other) against the live
+// (centre, normal, diameter, thickness) of q's near list.
+__device__ __forceinline__ bool trial_clear_pl(int64_t q, int32_t sl, int l, const double* xi, const double4 ni,
+                                               double Di, const State& S, const Box& box, const GridParams& g,
+                                               const RoundParams& rp, const int64_t* __restrict__ cs,
+                                               const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
+                                               double* p, pl::V3* pn) {
+    propose<3>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+    double ax[3];
+    unit_vector<3>(rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), 1, ax);
+    *pn = pl::rotate_normal(pl::V3{ni.x, ni.y, ni.z}, pl::V3{ax[0], ax[1], ax[2]}, rp.cos_r, rp.sin_r);
+    const double ti = ni.w;
+    auto hit = [&](int64_t j) {
+        const double4 v = S.rec[j], a = S.aux[j];
+        const pl::V3 d{min_image1(v.x - p[0], box.L[0], box.half[0]), min_image1(v.y - p[1], box.L[1], box.half[1]),
+                       min_image1(v.z - p[2], box.L[2], box.half[2])};
+        return pl::spherodisk_overlap(d, *pn, Di, ti, pl::V3{a.x, a.y, a.z}, v.w, a.w, c_seed_table);
+    };
+    const int32_t* row = nbr + q * kNearRow;
+    const int2 h0 = *reinterpret_cast<const int2*>(row);
+    const int nf = h0.x, nn = h0.x + h0.y;
+    if (nn <= kNearCap) {
+        for (int t = 0; t < nn; ++t)
+            if (hit(near_entry(row, nf, t))) return false;
+        return true;
     }
-    __syncthreads();
-    for (;;) {
-        // refill the queue with fresh cells (persistent CTAs share the class's bucket)
-        if (threadIdx.x == 0) {
-            const int want = static_cast<int>(blockDim.x) - qn[cur];
-            take_n = 0;
-            if (want >= static_cast<int>(blockDim.x) / 4) {
-                const unsigned long long b = atomicAdd(cursor, static_cast<unsigned long long>(want));
-                take_base = static_cast<long long>(b);
-                const long long avail = cnt - static_cast<long long>(b);
-                take_n = avail <= 0 ? 0 : static_cast<int>(avail < want ? avail : want);
-            }
-        }
-        __syncthreads();
-        if (static_cast<int>(threadIdx.x) < take_n) {
-            const int4 w = work[lo + take_base + threadIdx.x];
-            qbuf[cur][qn[cur] + threadIdx.x] = QItem{w.x, 0, w.y, w.z};
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) qn[cur] += take_n;
-        __syncthreads();
-        const int m = qn[cur];
-        if (m == 0) break;
-        const int nxt = cur ^ 1;
-        if (static_cast<int>(threadIdx.x) < m) {
-            QItem it = qbuf[cur][threadIdx.x];
-            const double4 me = S.rec[it.q];  // round-start record (the particle has not moved)
-            double xi[D], p[D];
-            rec_pos<D>(me, xi);
-            const bool clear = trial_clear<D>(it.q, it.sl, it.l, xi, me.w, S, box, g, rp, cs, skey, nbr, p);
-            bool done = true;
-            if (clear) {
-                S.rec[it.q] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
-                if (rp.write_acc) acc[it.q] = static_cast<uint8_t>(it.l);
-            } else if (it.l + 1 < rp.n_l) {
-                ++it.l;
-                done = false;
-            } else {
-                if (rp.write_acc) acc[it.q] = kNotAccepted;
-                active[atomicAdd(&stats->active_count, 1ull)] = it.q;
-            }
-            if (done && it.q + 1 < it.end) {  // the next particle of the cell
-                it.q += 1;
-                it.l = 0;
-                it.sl = S.slot[it.q];
-                done = false;
-            }
-            if (!done) qbuf[nxt][atomicAdd(&qn[nxt], 1)] = it;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) qn[cur] = 0;
-        cur = nxt;
-        __syncthreads();
-    }
+    const int32_t idq = S.id[q];  // crowded neighbourhood: rescan (same candidates, id filter)
+    bool ok = true;
+    near_candidates<3>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+        if (!ok || S.id[j] == idq) return;
+        if (hit(j)) ok = false;
+    });
+    return ok;
 }
 
-// The same class sweep with a queue per warp, kept in registers: each lane holds one
-// item (particle, next trial), every round runs one trial per item, the surviving items
-// are compacted to the low lanes with a ballot + shuffles, and the free lanes take fresh
-// cells from the warp's contiguous share of the class's bucket.  No barriers: warps
-// progress independently.  Same per-cell order and trials as k_sweep_queue.
 // The cells of colour class cls form a lattice per axis: first + stride * i, i < cnt
 // (colour1 inverted: a body colour v < m is x = v + m i, a remainder colour one cell).
 __device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int* first, int* stride, int* cnt) {
@@ -1305,7 +1091,7 @@ __device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int*
 // cells are skipped, a done particle hands its cell on to the next one in slot order).
 // No barriers and no work lists: warps progress independently.  Per cell the visiting
 // order and the trials are those of the sequential sweep (orc_sweep_round).
-template <int D>
+template <int D, bool PL = false>
 __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls_arg, const int* __restrict__ cls_dev,
                                                                                State S, Box box,
                                                                                const GridParams* __restrict__ gp,
@@ -1393,7 +1179,15 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
             const double4 me = S.rec[iq];  // round-start record (the particle has not moved)
             double xi[D], p[D];
             rec_pos<D>(me, xi);
-            const bool clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, p);
+            bool clear;
+            if constexpr (PL) {  // platelets: the normal turns too
+                const double4 ni = S.aux[iq];
+                pl::V3 pn;
+                clear = trial_clear_pl(iq, isl, il, xi, ni, me.w, S, box, g, rp, cs, skey, nbr, p, &pn);
+                if (clear) S.aux[iq] = make_double4(pn.x, pn.y, pn.z, ni.w);
+            } else {
+                clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, p);
+            }
             bool done = true;
             if (clear) {
                 S.rec[iq] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
@@ -1444,6 +1238,7 @@ struct GenCtl {
     int64_t max_iter, it0;
     int32_t n_k, n_l, reorder_period, dim, near_mode, pad0;
     uint64_t seed;
+    double cos_r, sin_r;  // platelet rotation angle (host libm)
     // state
     double f, max_r, factor, cs;
     int64_t done, accepted, rounds, shakes;
@@ -1510,6 +1305,8 @@ __global__ void k_gen_step(GenCtl* c, GridParams* gp, RoundParams* rp, StatsDev*
         v.key.k1 = static_cast<uint32_t>(c->seed >> 32);
         v.key.round_id = static_cast<uint32_t>(c->phase == 1 ? c->k : c->n_k + c->k) & 0xFFFFFFu;
         v.key.iteration = static_cast<uint32_t>(c->it0 + c->done);
+        v.cos_r = c->cos_r;
+        v.sin_r = c->sin_r;
         *rp = v;
         *stats = StatsDev{0, 0, 0, 0};
     }
@@ -1600,10 +1397,13 @@ __global__ void k_gen_end(GenCtl* c, cudaGraphConditionalHandle h_run) {
     cudaGraphSetConditional(h_run, c->phase != 3 ? 1u : 0u);
 }
 
-__global__ void k_scale_radius_ctl(int64_t n, double4* __restrict__ rec, const GenCtl* __restrict__ c) {
+__global__ void k_scale_radius_ctl(int64_t n, double4* __restrict__ rec, double4* __restrict__ aux,
+                                   const GenCtl* __restrict__ c) {
     const double factor = c->factor;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         rec[i].w = rec[i].w * factor;  // engine.hpp:520 p.radius *= factor
+        if (aux) aux[i].w = aux[i].w * factor;
+    }
 }
 
 // Overlap reduction after the sweep.  A particle that accepted a trial cleared every
@@ -1729,6 +1529,66 @@ __global__ void __launch_bounds__(256) k_overlap_full(int64_t n, State S, Box bo
     }
 }
 
+// Overlap statistics of a platelet state: unordered pairs {i, j > i} with overlap(i, j)
+// or overlap(j, i) -- shape_any_collision tests every ordered pair, and the platelet
+// test is not symmetric in its arguments (spherodisk.cpp), so the non-mover shortcut
+// of the spheres does not apply.  Penetration is not defined for platelets (0).
+__global__ void __launch_bounds__(256) k_overlap_pl(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
+                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                    StatsDev* stats) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long pairs = 0;
+    if (i < n) {
+        const GridParams& g = *gp;
+        const double4 vi = S.rec[i], ai = S.aux[i];
+        const int32_t idi = S.id[i];
+        for_near_ranges<3>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+            for (int64_t j = b; j < e; ++j) {
+                if (j <= i || S.id[j] == idi) continue;
+                const double4 vj = S.rec[j], aj = S.aux[j];
+                const pl::V3 dij{min_image1(vj.x - vi.x, box.L[0], box.half[0]),
+                                 min_image1(vj.y - vi.y, box.L[1], box.half[1]),
+                                 min_image1(vj.z - vi.z, box.L[2], box.half[2])};
+                const pl::V3 dji{min_image1(vi.x - vj.x, box.L[0], box.half[0]),
+                                 min_image1(vi.y - vj.y, box.L[1], box.half[1]),
+                                 min_image1(vi.z - vj.z, box.L[2], box.half[2])};
+                const pl::V3 ni{ai.x, ai.y, ai.z}, nj{aj.x, aj.y, aj.z};
+                if (pl::spherodisk_overlap(dij, ni, vi.w, ai.w, nj, vj.w, aj.w, c_seed_table) ||
+                    pl::spherodisk_overlap(dji, nj, vj.w, aj.w, ni, vi.w, ai.w, c_seed_table))
+                    ++pairs;
+            }
+        });
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, o);
+    if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(&stats->overlap_pairs, pairs);
+}
+
+// platelet records (host layout) <-> device state, scattered back to slot order
+__global__ void k_unpack_pl(int64_t n, const double* __restrict__ pos, const double* __restrict__ nrm,
+                            const double* __restrict__ dia, const double* __restrict__ thk,
+                            const int32_t* __restrict__ id, State T) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        T.rec[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], dia[i]);
+        T.aux[i] = make_double4(nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2], thk[i]);
+        T.id[i] = id ? id[i] : static_cast<int32_t>(i);
+        T.slot[i] = static_cast<int32_t>(i);
+    }
+}
+
+__global__ void k_pack_pl(int64_t n, State T, double* __restrict__ pos, double* __restrict__ nrm,
+                          double* __restrict__ dia, double* __restrict__ thk, int32_t* __restrict__ id) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = T.slot[i];
+        const double4 v = T.rec[i], a = T.aux[i];
+        pos[3 * s] = v.x; pos[3 * s + 1] = v.y; pos[3 * s + 2] = v.z;
+        nrm[3 * s] = a.x; nrm[3 * s + 1] = a.y; nrm[3 * s + 2] = a.z;
+        dia[s] = v.w;
+        thk[s] = a.w;
+        id[s] = T.id[i];
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // Small utility kernels.
 __global__ void k_set_grid(GridParams* gp, GridParams v) { *gp = v; }
@@ -1794,10 +1654,12 @@ __global__ void k_pack_soa(int64_t n, State T, double* __restrict__ pos, double*
     }
 }
 
-__global__ void k_scale_radius(int64_t n, double4* __restrict__ rec, double factor) {
+__global__ void k_scale_radius(int64_t n, double4* __restrict__ rec, double4* __restrict__ aux, double factor) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        rec[i].w = rec[i].w * factor;  // engine.hpp:520 p.radius *= factor
+         i += (int64_t)gridDim.x * blockDim.x) {
+        rec[i].w = rec[i].w * factor;              // engine.hpp:520 p.radius *= factor
+        if (aux) aux[i].w = aux[i].w * factor;     // spherodisk.hpp:88-91 diameter, thickness
+    }
 }
 
 template <int D>
@@ -1805,6 +1667,7 @@ __global__ void k_copy_state(int64_t n, State A, State B) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         B.rec[i] = A.rec[i];
+        if (A.aux) B.aux[i] = A.aux[i];
         B.id[i] = A.id[i];
         B.slot[i] = A.slot[i];
     }
@@ -1848,7 +1711,8 @@ __device__ __forceinline__ double particle_measure(double r) {
 template <int D>
 __global__ void __launch_bounds__(256) k_reduce_partials(int64_t n, const double4* __restrict__ rec,
                                                          double* __restrict__ part_sum,
-                                                         double* __restrict__ part_max) {
+                                                         double* __restrict__ part_max,
+                                                         const double4* __restrict__ aux = nullptr) {
     __shared__ double ss[256], sm[256];
     const int64_t chunk = (n + kRedBlocks - 1) / kRedBlocks;
     const int64_t b0 = blockIdx.x * chunk;
@@ -1856,8 +1720,15 @@ __global__ void __launch_bounds__(256) k_reduce_partials(int64_t n, const double
     double s = 0.0, m = 0.0;
     for (int64_t i = b0 + threadIdx.x; i < b1; i += 256) {
         const double v = rec[i].w;
-        s = s + particle_measure<D>(v);
-        m = v > m ? v : m;
+        if (aux) {  // platelets: swept volume, bounding radius (spherodisk.hpp:29-34, 94-96)
+            const double t = aux[i].w;
+            s = s + pl::spherodisk_measure(v, t);
+            const double b = 0.5 * (v + t);
+            m = b > m ? b : m;
+        } else {
+            s = s + particle_measure<D>(v);
+            m = v > m ? v : m;
+        }
     }
     ss[threadIdx.x] = s;
     sm[threadIdx.x] = m;

@@ -1,4 +1,5 @@
-// srm_rsa.cpp -- host-side initial-state generator: rsa_place (rsa.hpp:21-69).
+// srm_rsa.cpp -- host-side initial-state generators: rsa_place (rsa.hpp:21-69) and
+// rsa_platelets (recipes.cpp:107-148).
 //
 // Random sequential adsorption is sequential by definition (each acceptance changes
 // the next candidate's test), so it stays on the host, as input generation whose time
@@ -14,6 +15,7 @@
 #include <vector>
 
 #include "../../include/srm_b200.h"
+#include "srm_platelet.cuh"
 
 namespace {
 
@@ -132,6 +134,133 @@ int srm_b200_rsa_place(int dim, const double* L, int64_t count, const double* ra
         if (id_out) id_out[i] = static_cast<int32_t>(i);
         int c[3] = {0, 0, 0};
         for (int a = 0; a < dim; ++a) c[a] = g.coord(a, cand[a]);
+        const int64_t cell = (static_cast<int64_t>(c[2]) * g.n[1] + c[1]) * g.n[0] + c[0];
+        g.next[i] = g.head[cell];
+        g.head[cell] = static_cast<int32_t>(i);
+    }
+    if (placed_out) *placed_out = count;
+    return SRM_B200_OK;
+}
+
+
+int srm_b200_rsa_platelets(int64_t count, double diameter, double aspect_ratio, const double* L, int64_t max_attempts,
+                           uint64_t seed, double* pos_out, double* normal_out, int32_t* id_out, int64_t* placed_out) {
+    using namespace srmb::pl;
+    if (placed_out) *placed_out = 0;
+    if (count < 1) return SRM_B200_INVALID;                  // recipes.cpp:109
+    if (!(aspect_ratio > 1.0)) return SRM_B200_INVALID;      // recipes.cpp:110-111
+    const double thickness = diameter / aspect_ratio;
+    const double bound = 0.5 * (diameter + thickness);
+    double min_len = L[0];
+    for (int a = 1; a < 3; ++a) min_len = std::min(min_len, L[a]);
+    if (!(bound < min_len / 4.0)) return SRM_B200_INVALID;   // recipes.cpp:116-117
+
+    // Rng (random.hpp:16-52): mt19937_64, 53-bit uniforms, Box-Muller with a cached spare
+    std::mt19937_64 gen(seed);
+    auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+    bool have_spare = false;
+    double spare = 0.0;
+    auto gaussian = [&]() {
+        if (have_spare) {
+            have_spare = false;
+            return spare;
+        }
+        double u1 = uniform();
+        while (u1 == 0.0) u1 = uniform();
+        const double u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double a = 2.0 * 3.141592653589793238462643383279502884 * u2;
+        spare = r * std::sin(a);
+        have_spare = true;
+        return r * std::cos(a);
+    };
+    SeedTable tab;  // spherodisk.cpp:60-66 rim seeds
+    for (int k = 0; k < kSeeds; ++k) {
+        const double a = 2.0 * 3.141592653589793238462643383279502884 * k / kSeeds;
+        tab.c[k] = std::cos(a);
+        tab.s[k] = std::sin(a);
+    }
+
+    RsaGrid g;  // any complete neighbour search decides like CellGrid(box, 2.5 bound)
+    g.dim = 3;
+    int64_t ncells = 1;
+    for (int a = 0; a < 3; ++a) {
+        int k = static_cast<int>(std::floor(L[a] / (2.0 * bound)));
+        k = std::max(1, std::min(k, 1 << 10));
+        g.n[a] = k;
+        g.edge[a] = L[a] / k;
+        ncells *= k;
+    }
+    g.head.assign(static_cast<size_t>(ncells), -1);
+    g.next.assign(static_cast<size_t>(count), -1);
+
+    double cand[3];
+    V3 cn{0.0, 0.0, 0.0};
+    for (int64_t i = 0; i < count; ++i) {
+        bool accepted = false;
+        for (int64_t attempt = 0; attempt < max_attempts; ++attempt) {
+            for (int a = 0; a < 3; ++a) cand[a] = uniform() * L[a];  // random.hpp:56-61 random_point
+            for (int a = 0; a < 3; ++a) {
+                if (cand[a] < 0.0) cand[a] += L[a];
+                if (cand[a] >= L[a]) cand[a] -= L[a];
+            }
+            for (;;) {  // random.hpp:70-76 random_unit_vector<3>
+                const V3 gv{gaussian(), gaussian(), gaussian()};
+                const double n2 = dot(gv, gv);
+                if (n2 > 1e-24) {
+                    cn = mul(gv, 1.0 / std::sqrt(n2));
+                    break;
+                }
+            }
+            int c[3];
+            for (int a = 0; a < 3; ++a) c[a] = g.coord(a, cand[a]);
+            bool hit = false;
+            for (int dz = -1; dz <= 1 && !hit; ++dz) {
+                if (g.n[2] < 3 && dz != 0 && (g.n[2] == 1 || dz == 1)) continue;
+                const int z = ((c[2] + dz) % g.n[2] + g.n[2]) % g.n[2];
+                for (int dy = -1; dy <= 1 && !hit; ++dy) {
+                    if (g.n[1] < 3 && dy != 0 && (g.n[1] == 1 || dy == 1)) continue;
+                    const int y = ((c[1] + dy) % g.n[1] + g.n[1]) % g.n[1];
+                    for (int dx = -1; dx <= 1 && !hit; ++dx) {
+                        if (g.n[0] < 3 && dx != 0 && (g.n[0] == 1 || dx == 1)) continue;
+                        const int x = ((c[0] + dx) % g.n[0] + g.n[0]) % g.n[0];
+                        const int64_t cell = (static_cast<int64_t>(z) * g.n[1] + y) * g.n[0] + x;
+                        for (int32_t j = g.head[cell]; j >= 0 && !hit; j = g.next[j]) {
+                            // shape_collides (shape.hpp:64-73): overlap(candidate, placed)
+                            const double* pj = pos_out + 3 * static_cast<int64_t>(j);
+                            V3 d;
+                            double dd[3];
+                            for (int a = 0; a < 3; ++a) {
+                                double v = pj[a] - cand[a];
+                                const double half = 0.5 * L[a];
+                                if (v > half) v -= L[a];
+                                if (v < -half) v += L[a];
+                                dd[a] = v;
+                            }
+                            d = V3{dd[0], dd[1], dd[2]};
+                            const double* nj = normal_out + 3 * static_cast<int64_t>(j);
+                            hit = spherodisk_overlap(d, cn, diameter, thickness, V3{nj[0], nj[1], nj[2]}, diameter,
+                                                     thickness, tab);
+                        }
+                    }
+                }
+            }
+            if (!hit) {
+                accepted = true;
+                break;
+            }
+        }
+        if (!accepted) {
+            if (placed_out) *placed_out = i;
+            return SRM_B200_PLACEMENT_FAILURE;
+        }
+        for (int a = 0; a < 3; ++a) pos_out[3 * i + a] = cand[a];
+        normal_out[3 * i] = cn.x;
+        normal_out[3 * i + 1] = cn.y;
+        normal_out[3 * i + 2] = cn.z;
+        if (id_out) id_out[i] = static_cast<int32_t>(i);
+        int c[3];
+        for (int a = 0; a < 3; ++a) c[a] = g.coord(a, cand[a]);
         const int64_t cell = (static_cast<int64_t>(c[2]) * g.n[1] + c[1]) * g.n[0] + c[0];
         g.next[i] = g.head[cell];
         g.head[cell] = static_cast<int32_t>(i);

@@ -64,6 +64,19 @@ def orc():
         L.orc_max_radius.argtypes = [C.c_int64, vp]
         L.orc_volume_fraction_seq.restype = C.c_double
         L.orc_volume_fraction_seq.argtypes = [C.c_int, vp, C.c_int64, vp]
+        d = C.c_double
+        L.orc_pl_overlap.restype = C.c_int
+        L.orc_pl_overlap.argtypes = [vp, vp, vp, d, d, vp, vp, d, d]
+        L.orc_pl_disks_within.restype = d
+        L.orc_pl_disks_within.argtypes = [vp, vp, d, vp, vp, d, d]
+        L.orc_pl_measure.restype = d
+        L.orc_pl_measure.argtypes = [d, d]
+        L.orc_pl_propose.argtypes = [vp, vp, vp, d, d, d, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     vp, vp]
+        L.orc_pl_sweep_round.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, d, d, d, d, C.c_int, C.c_uint64,
+                                         C.c_uint32, C.c_uint32, vp, vp, vp]
+        L.orc_pl_overlap_pairs.restype = C.c_int64
+        L.orc_pl_overlap_pairs.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp]
         _orc = L
     return _orc
 
@@ -97,6 +110,23 @@ def ref():
         L.ref_bench_rounds.restype = C.c_double
         L.ref_bench_rounds.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, C.c_double, C.c_int, C.c_int,
                                        C.c_uint64, C.c_int, vp]
+        d = C.c_double
+        L.ref_pl_overlap.restype = C.c_int
+        L.ref_pl_overlap.argtypes = [vp, vp, vp, d, d, vp, vp, d, d]
+        L.ref_pl_disks_within.restype = C.c_int
+        L.ref_pl_disks_within.argtypes = [vp, vp, d, vp, vp, d, d]
+        L.ref_pl_disk_distance.restype = d
+        L.ref_pl_disk_distance.argtypes = [vp, vp, d, vp, vp, d]
+        L.ref_pl_measure.restype = d
+        L.ref_pl_measure.argtypes = [d, d]
+        L.ref_pl_rotate.argtypes = [vp, vp, d, vp]
+        L.ref_rsa_platelets.restype = C.c_int
+        L.ref_rsa_platelets.argtypes = [C.c_int64, d, d, vp, C.c_int64, C.c_uint64, vp, vp, vp]
+        L.ref_generate_platelets.restype = C.c_int
+        L.ref_generate_platelets.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, d, d, d, C.c_int, C.c_int, d,
+                                             C.c_int64, C.c_uint64, C.c_int, vp, vp]
+        L.ref_pl_any_collision.restype = C.c_int
+        L.ref_pl_any_collision.argtypes = [vp, d, C.c_int64, vp, vp, vp, vp, vp]
         _ref = L
     return _ref
 
@@ -315,3 +345,39 @@ def random_particles(n, dim, rmin, rmax, L, seed):
         col[col >= L[a]] -= L[a]
     r = rmin + (rmax - rmin) * u[:, dim]
     return np.ascontiguousarray(pos), np.ascontiguousarray(r)
+
+
+# ---- platelets -------------------------------------------------------------------------
+def o_pl_overlap(L, pa, na, Da, ta, pb, nb, Db, tb):
+    return orc().orc_pl_overlap(P(arr(L)), P(arr(pa)), P(arr(na)), Da, ta, P(arr(pb)), P(arr(nb)), Db, tb)
+
+
+def r_pl_overlap(L, pa, na, Da, ta, pb, nb, Db, tb):
+    return ref().ref_pl_overlap(P(arr(L)), P(arr(pa)), P(arr(na)), Da, ta, P(arr(pb)), P(arr(nb)), Db, tb)
+
+
+def o_pl_round(L, x0, n0, D, t, ids, slot, cell_size, c_m, c_r, n_l, seed, round_id, iteration):
+    import math
+    x0, n0 = arr(x0), arr(n0)
+    n = len(D)
+    xnew, nnew = np.zeros_like(x0), np.zeros_like(n0)
+    acc = np.zeros(n, np.uint8)
+    orc().orc_pl_sweep_round(P(arr(L)), n, P(x0), P(n0), P(arr(D)), P(arr(t)), P(arr(ids, np.int32)),
+                             P(arr(slot, np.int32)), cell_size, c_m, math.cos(c_r), math.sin(c_r), n_l, seed,
+                             round_id, iteration, P(xnew), P(nnew), P(acc))
+    return xnew, nnew, acc
+
+
+def o_pl_pairs(L, x, nrm, D, t, ids=None):
+    n = len(D)
+    ids = np.arange(n, dtype=np.int32) if ids is None else ids
+    return orc().orc_pl_overlap_pairs(P(arr(L)), n, P(arr(x)), P(arr(nrm)), P(arr(D)), P(arr(t)),
+                                      P(arr(ids, np.int32)))
+
+
+def r_rsa_platelets(n, diameter, aspect, L, max_attempts, seed):
+    pos = np.zeros((n, 3))
+    nrm = np.zeros((n, 3))
+    ids = np.zeros(n, np.int32)
+    st = ref().ref_rsa_platelets(n, diameter, aspect, P(arr(L)), max_attempts, seed, P(pos), P(nrm), P(ids))
+    return st, pos, nrm, ids
