@@ -220,6 +220,7 @@ struct srm_b200_ctx {
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearRow);
         SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
+        SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         {
             int per_sm = 0, sms = 0;
             SRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_warpq<3>, kSweepThreads, 0));
@@ -366,15 +367,9 @@ struct srm_b200_ctx {
         {
             FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
-            if (hg.near_kind == 0) {  // pairs once, through shared-memory bricks
-                k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
+            if (hg.near_kind == 0) {  // shared-memory bricks
                 k_near_tiles<<<hg.ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
-                launched(2);
-            } else if (hg.near_kind == 1) {  // pairs once, appended to both lists
-                k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
-                if (dim == 2) k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                else k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                launched(2);
+                launched(1);
             } else {
                 if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                 else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
@@ -505,7 +500,11 @@ struct srm_b200_ctx {
         const GridParams g0 = make_grid(2.5 * max_r0 + p.c_m, max_r0, p.c_m);
         ensure_cells(g0.ncells);
         const int64_t nc_max = g0.ncells;
-        const int ntiles_max = std::max(1, g0.ntiles);
+        // (brick count of the first grid, whether or not it takes the bricks: a later grid
+        // of the run may, and its dims are no larger)
+        const int ntiles_max = dim == 3 ? ((g0.dims[0] + kTX - 1) / kTX) * ((g0.dims[1] + kTY - 1) / kTY) *
+                                              ((g0.dims[2] + kTZ - 1) / kTZ)
+                                        : 1;
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
@@ -534,15 +533,9 @@ struct srm_b200_ctx {
                     });
                     // one round on Q
                     grid_build(Q, nc_max);
-                    k_near_zero<<<nb, 256, 0, stream>>>(n, nbr);
                     k_near_tiles<<<ntiles_max, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
-                    if (dim == 2) {
-                        k_near_half<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                        k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                    } else {
-                        k_near_half<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                        k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                    }
+                    if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                    else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
                     k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
                     capture_into(add_conditional(stream, h_cls, cudaGraphCondTypeWhile), cap_streams[3], [&]() {
                         if (dim == 2)

@@ -3,8 +3,7 @@
 // One SRM round (engine.hpp:227-234: build_shape_grid -> migrate -> shape_any_collision)
 // is, on the device:
 //   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
-//   near lists     k_near_lists (round-start neighbours within the trial reach)
-//   near lists     k_near_lists (+ the (colour class, rank) work lists of the sweep)
+//   near lists     k_near_tiles / k_near_lists (round-start neighbours within the trial reach)
 //   migrate        k_sweep_warpq, one launch per colour class (warp queues)
 //   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
 // All kernels read the grid / round parameters from device memory so that the same
@@ -59,7 +58,7 @@ struct GridParams {
     // fp32 prefilter (near_candidates): margin above the fp32 rounding of coordinates
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
-    int32_t near_kind;   // near lists: 0 shared-memory bricks, 1 half stencil, 2 full stencil
+    int32_t near_kind;   // near lists: 0 shared-memory bricks, 2 full stencil from global memory
     int32_t ntiles;      // bricks of k_near_tiles (near_kind 0)
     FastDiv fd_dims[3];  // division by dims[a]
     FastDiv fd_m[3];     // division by col_m[a]
@@ -86,7 +85,16 @@ __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, in
 // max_r_state and whose trial moves have length c_m.  The colouring expression is the
 // oracle's orc_colouring.  Host and device (the device-resident generate loop) share it.
 // Returns 0, or 1 (cell_size <= 0), 2 (more than 2^32 cells).
-constexpr int kTX = 16, kTY = 8, kTZ = 4;  // k_near_tiles brick (cells)
+#ifndef SRM_TILE_X
+#define SRM_TILE_X 16
+#endif
+#ifndef SRM_TILE_Y
+#define SRM_TILE_Y 8
+#endif
+#ifndef SRM_TILE_Z
+#define SRM_TILE_Z 4
+#endif
+constexpr int kTX = SRM_TILE_X, kTY = SRM_TILE_Y, kTZ = SRM_TILE_Z;  // k_near_tiles brick (cells)
 __host__ __device__ inline int grid_params(double cell_size, double max_r_state, double c_m, const Box& box, int dim,
                                            int near_mode, GridParams* out) {
     const double extra = 2.0 * c_m;
@@ -158,11 +166,9 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
         g.half_f[a] = 0.5f * g.L_f[a];
         g.edge_f[a] = static_cast<float>(g.edge[a]);
     }
-    bool half = near_mode != 1;
-    for (int a = 0; a < dim; ++a) half = half && g.near_s[a] >= 0;
-    const bool tiles = half && dim == 3 && near_mode == 0 && g.near_s[0] == 1 && g.near_s[1] == 1 &&
-                       g.near_s[2] == 1 && g.dims[0] >= kTX + 2 && g.dims[1] >= kTY + 2 && g.dims[2] >= kTZ + 1;
-    g.near_kind = tiles ? 0 : (half ? 1 : 2);
+    const bool tiles = dim == 3 && near_mode == 0 && g.near_s[0] == 1 && g.near_s[1] == 1 && g.near_s[2] == 1 &&
+                       g.dims[0] >= kTX + 2 && g.dims[1] >= kTY + 2 && g.dims[2] >= kTZ + 2;
+    g.near_kind = tiles ? 0 : 2;
     g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ) : 0;
     *out = g;
     return 0;
@@ -472,16 +478,30 @@ __device__ __forceinline__ void load_pos(const State& S, int64_t i, double* p) {
 // Live positions: S.rec[j] holds (x, r) of j -- its round-start position, overwritten by
 // its accepted trial when j moves; one 32-byte sector per neighbour read.
 
-// Near list row of a particle, kNearRow int32: [0] f = neighbours the particle found
-// itself (half stencil), [1] b = neighbours that found it (atomic appends), entries
-// [2, 2 + f) and [15 - k] for k < b.  f + b > kNearCap means overflow: the sweep
-// rescans the grid.  The first 32-byte sector holds both counts and six entries.
-constexpr int kNearRow = 16;
-constexpr int kNearCap = kNearRow - 2;
+// Near list row of a particle: kNearRow int32 = one 32-byte sector, [0] = n = number of
+// near neighbours (round-start distance within ri + rj + 2 c_m, fp32 screen with a
+// margin: a superset of the exact near set), entries [1, 1 + n) = their sorted indices.
+// n > kNearCap means overflow: the sweep rescans the stencil.  At the bench window the
+// mean list length is below one, so one sector holds a row.
+constexpr int kNearRow = 8;
+constexpr int kNearCap = kNearRow - 1;
 
-__device__ __forceinline__ int32_t near_entry(const int32_t* row, int f, int t) {
-    return t < f ? row[2 + t] : row[kNearRow - 1 - (t - f)];
-}
+// append j to a register-held list (no dynamically indexed local arrays)
+struct NearList {
+    int n = 0;
+    int32_t e[kNearCap];
+    __device__ __forceinline__ void add(int32_t j) {
+#pragma unroll
+        for (int s = 0; s < kNearCap; ++s)
+            if (n == s) e[s] = j;
+        ++n;
+    }
+    __device__ __forceinline__ void store(int32_t* row) const {
+        int4* r = reinterpret_cast<int4*>(row);
+        r[0] = make_int4(n, e[0], e[1], e[2]);
+        r[1] = make_int4(e[3], e[4], e[5], e[6]);
+    }
+};
 
 // Near candidates of sorted particle q: every j whose round-start distance is within
 // ri + rj + 2 c_m (every j a trial of q can touch while j sits within c_m of its start).
@@ -573,175 +593,85 @@ __device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
     return k;
 }
 
-// Near lists of every particle, a thread per particle over its full stencil (grids with
-// an axis scanned whole; k_near_half covers the rest).  Row layout: see kNearRow.
+// Near list of sorted particle q over its full stencil from global memory (grids that
+// k_near_tiles does not cover, and its crowded bricks).
+template <int D>
+__device__ __forceinline__ void near_full_particle(int64_t q, const State& S, const GridParams& g,
+                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                   int32_t* __restrict__ nbr) {
+    NearList nl;
+    const int32_t idq = S.id[q];
+    near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+        if (S.id[j] == idq) return;  // shape.hpp:544 self-exclusion by id
+        nl.add(static_cast<int32_t>(j));
+    });
+    nl.store(nbr + q * kNearRow);
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const GridParams* __restrict__ gp,
                                                     const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                     int32_t* __restrict__ nbr) {
     const GridParams& g = *gp;
     if (g.near_kind != 2) return;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        int32_t* my = nbr + q * kNearRow;
-        int nn = 0;
-        const int32_t idq = S.id[q];
-        near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
-            if (S.id[j] == idq) return;  // shape.hpp:544 self-exclusion by id
-            if (nn < kNearCap) my[2 + nn] = static_cast<int32_t>(j);
-            ++nn;
-        });
-        my[0] = nn;
-        my[1] = 0;
-    }
-}
-
-// Near lists by pairs: each thread scans the HALF stencil of its particle q (rows ahead
-// of q's row, the cells ahead of q's cell in its row, the particles after q in its cell),
-// so every candidate pair is screened once, and a pair that passes is appended to both
-// lists (atomic counters in word 0 of each row, which must be zero on entry).  Periodic images are resolved
-// per row / per x segment (a constant shift by +-L), not per candidate.  The screen
-// keeps near_candidates' cutoff, margin and factor, so the lists hold the same pairs as
-// k_near_lists, in another order (which the sweep does not observe).  Requires every
-// near_s >= 0 (no axis scanned whole); k_near_lists covers the other grids.
-// Publish q's forward list: its count, and q into the backward part of every forward
-// neighbour's row (two independent atomics in flight at a time).
-__device__ __forceinline__ void near_publish(int32_t* __restrict__ nbr, int64_t q, int nf, const int32_t* fwd) {
-    int32_t* myrow = nbr + q * kNearRow;
-    myrow[0] = nf;
-    const int m = nf < kNearCap ? nf : kNearCap;
-    for (int t0 = 0; t0 < m; t0 += 2) {  // two atomics in flight at a time
-        const int64_t ja = fwd[t0];
-        const int64_t jb = t0 + 1 < m ? fwd[t0 + 1] : -1;
-        const int ka = atomicAdd(&nbr[ja * kNearRow + 1], 1);
-        const int kb = jb >= 0 ? atomicAdd(&nbr[jb * kNearRow + 1], 1) : kNearCap;
-        if (ka < kNearCap) nbr[ja * kNearRow + kNearRow - 1 - ka] = static_cast<int32_t>(q);
-        if (kb < kNearCap) nbr[jb * kNearRow + kNearRow - 1 - kb] = static_cast<int32_t>(q);
-    }
-}
-
-// k_near_half for one particle q (global memory throughout).
-template <int D>
-__device__ __forceinline__ void near_half_particle(int64_t q, const State& S, const GridParams& g,
-                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                   int32_t* __restrict__ nbr) {
-    const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
-    const int sx = g.near_s[0], sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
-    const float4 me = S.xf[q];
-    const int32_t idq = S.id[q];
-    const uint32_t key = skey[q];
-    int cc_[3];
-    decode_key<D>(g, key, cc_);
-    const int cx = cc_[0], cy = cc_[1], cz = cc_[2];
-    const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(me.w, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
-    const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
-    const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
-    // screen [b, e) against me shifted by (ox, oy, oz); keep the hits (q's forward list)
-    int32_t* myrow = nbr + q * kNearRow;
-    int nf = 0;
-    int32_t fwd[kNearCap];  // the forward list, also kept thread-locally for near_publish
-    auto run = [&](int64_t b, int64_t e, float ox, float oy, float oz) {
-        for (int64_t j = b; j < e; ++j) {
-            const float4 c = S.xf[j];
-            const float ex = __fsub_rn(c.x, ox), ey = __fsub_rn(c.y, oy);
-            const float ez = D == 3 ? __fsub_rn(c.z, oz) : 0.f;
-            const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-            const float lim = __fadd_rn(base, c.w);
-            if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f)) continue;
-            if (S.id[j] == idq) continue;  // shape.hpp:544 self-exclusion by id
-            if (nf < kNearCap) {
-                myrow[2 + nf] = static_cast<int32_t>(j);
-                fwd[nf] = static_cast<int32_t>(j);
-            }
-            ++nf;
-        }
-    };
-    const int zhi = D == 3 ? cz + sz : 0;
-    for (int zz = cz; zz <= zhi; ++zz) {
-        float dzd = 0.f, oz = me.z;
-        if (D == 3) {
-            const float zb = zz * g.edge_f[2];
-            dzd = fmaxf(0.f, fmaxf(zb - me.z, me.z - (zb + g.edge_f[2])));
-        }
-        int z = zz;
-        if (D == 3 && z >= dz) {  // image above the box: candidates sit at z - L
-            z -= dz;
-            oz = __fsub_rn(me.z, g.L_f[2]);
-        }
-        const int ylo = zz == cz ? cy : cy - sy;
-        for (int yy = ylo; yy <= cy + sy; ++yy) {
-            const float yb = yy * g.edge_f[1];
-            const float dyd = fmaxf(0.f, fmaxf(yb - me.y, me.y - (yb + g.edge_f[1])));
-            const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
-            if (dyz2 > cut2) continue;
-            int y = yy;
-            float oy = me.y;
-            if (y < 0) {
-                y += dy;
-                oy = __fadd_rn(me.y, g.L_f[1]);
-            } else if (y >= dy) {
-                y -= dy;
-                oy = __fsub_rn(me.y, g.L_f[1]);
-            }
-            const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
-            const bool own = zz == cz && yy == cy;
-            const int xl = own ? cx : cx - sx, xr = cx + sx;
-            // cells [xl, xr] of the unwrapped row: up to three pieces (below 0, inside, above dx)
-            const int64_t first = own ? q + 1 : -1;  // own cell: only the particles after q
-            if (xl < 0) {
-                const int e = min(xr, -1);
-                run(cs[row + xl + dx], cs[row + e + 1 + dx], __fadd_rn(me.x, g.L_f[0]), oy, oz);
-            }
-            if (xr >= 0 && xl < dx) {
-                const int b = max(xl, 0), e = min(xr, dx - 1);
-                const int64_t bb = first >= 0 && b == cx ? first : cs[row + b];
-                run(bb, cs[row + e + 1], me.x, oy, oz);
-            }
-            if (xr >= dx) {
-                const int b = max(xl, dx);
-                run(cs[row + b - dx], cs[row + xr - dx + 1], __fsub_rn(me.x, g.L_f[0]), oy, oz);
-            }
-        }
-    }
-    near_publish(nbr, q, nf, fwd);
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) k_near_half(int64_t n, State S, const GridParams* __restrict__ gp,
-                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                   int32_t* __restrict__ nbr) {
-    const GridParams& g = *gp;
-    if (g.near_kind != 1) return;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-        near_half_particle<D>(q, S, g, cs, skey, nbr);
+        near_full_particle<D>(q, S, g, cs, skey, nbr);
 }
 
-// The same pairs, tiled through shared memory (3D, a one-cell stencil on every axis).
-// A CTA takes a brick of kTX x kTY x kTZ cells, stages the fp32 records, ids and sorted
-// indices of the brick and its half-stencil halo (x +-1, y +-1, z +1) in shared
-// memory -- periodic images shifted by +-L on the way in, so pair distances are plain
-// differences -- and screens every interior particle against its half stencil there:
-// five contiguous shared ranges (own cell after i + next cell, the dy=+1 row, the three
-// dz=+1 rows).  Same screen, same pairs as k_near_half; a brick whose halo holds more
-// than kTileCap particles falls back to near_half_particle.
-constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 1;
+// Near lists through shared memory (3D, a one-cell stencil on every axis).  A CTA takes a
+// brick of kTX x kTY x kTZ cells and stages the fp32 records, sorted indices and ids of
+// the brick and its full one-cell halo (the particles of a row of halo cells are one to
+// three contiguous runs of the sorted state: the periodic images at x = -1 and x >= dims),
+// shifted by +-L on the way in so that pair distances are plain differences.  Every interior particle is then screened against the nine contiguous
+// shared-memory ranges of its 3x3x3 stencil and writes its own row (one sector, no
+// atomics).  Same screen as near_candidates (cutoff, margin, factor), so the lists hold
+// the same pairs as k_near_lists.  A brick whose halo holds more than kTileCap particles
+// takes near_full_particle.
+constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 2;
 constexpr int kHCells = kHX * kHY * kHZ;
-constexpr int kTileCap = 1792;
-constexpr int kTileThreads = 256;
-constexpr size_t kTileSmem = kTileCap * (16 + 4 + 4 + 2) + (kHCells + 2) * 4 + kHCells * 8;
+constexpr int kHRows = kHY * kHZ;
+#ifndef SRM_TILE_THREADS
+#define SRM_TILE_THREADS 256
+#endif
+#ifndef SRM_TILE_CAP
+#define SRM_TILE_CAP 2048
+#endif
+#ifndef SRM_NEAR_PRUNE
+#define SRM_NEAR_PRUNE 0
+#endif
+constexpr int kTileCap = SRM_TILE_CAP;  // staged particles (2.1 per halo cell at the defaults)
+constexpr int kTileThreads = SRM_TILE_THREADS;
+constexpr int kCellsPerThread = (kHCells + kTileThreads - 1) / kTileThreads;
+constexpr size_t kTileSmem = kTileCap * (16 + 4) + (kHCells + 1) * 4 +
+                             (kHCells * 4 > kTileThreads * (kNearCap + 1) * 2 ? kHCells * 4 : kTileThreads * (kNearCap + 1) * 2);
+static_assert(kTileCap <= 65536, "16-bit hit slots");
+static_assert(kHRows <= kTileThreads && kHRows <= 64, "a thread per halo row; 6-step row search");
+static_assert(kTY * kTZ <= 32 && kTX <= 16, "one warp scans the interior rows; 4-step cell search");
+
+// staged slot -> sorted index of one row of halo cells (k_near_tiles)
+struct RowMap {
+    int64_t sa, sb, sc;  // sorted index - slot in the runs [.., ka), [ka, kc), [kc, ..)
+    int32_t ka, kc;
+    float sy, sz;        // periodic image shift of the row
+};
 
 __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const GridParams* __restrict__ gp,
                                                              const int64_t* __restrict__ cs,
                                                              const uint32_t* __restrict__ skey,
                                                              int32_t* __restrict__ nbr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float4* px = reinterpret_cast<float4*>(smem_raw);                       // [kTileCap]
-    int32_t* pj = reinterpret_cast<int32_t*>(px + kTileCap);                // [kTileCap] sorted index
-    int32_t* pid = pj + kTileCap;                                           // [kTileCap] reference id
-    uint16_t* phc = reinterpret_cast<uint16_t*>(pid + kTileCap);            // [kTileCap] halo cell
-    int32_t* hoff = reinterpret_cast<int32_t*>(phc + kTileCap);             // [kHCells + 1]
-    int64_t* hsrc = reinterpret_cast<int64_t*>(hoff + kHCells + 2);         // [kHCells] global first index
+    // shifted fp32 records of staged slots 2p, 2p + 1, interleaved for f32x2 arithmetic:
+    // pxy[p] = (x0, x1, y0, y1), pzw[p] = (z0, z1, w0, w1)
+    float4* pxy = reinterpret_cast<float4*>(smem_raw);             // [kTileCap / 2]
+    float4* pzw = pxy + kTileCap / 2;                               // [kTileCap / 2]
+    int32_t* pj = reinterpret_cast<int32_t*>(pzw + kTileCap / 2);  // [kTileCap] sorted index of a slot
+    int32_t* hoff = pj + kTileCap;                                  // [kHCells + 1] staged offset of a cell
+    int32_t* hsrc = hoff + kHCells + 1;                             // [kHCells] first sorted index of a cell
+    uint16_t* lst = reinterpret_cast<uint16_t*>(hsrc);              // [kNearCap + 1][kTileThreads] hit slots
+                                                                    // (aliases hsrc: used after the staging)
     __shared__ int wsum[kTileThreads / 32];
     __shared__ int rowoff[kTY * kTZ + 1];
+    __shared__ RowMap rmap[kHRows];
     const GridParams& g = *gp;
     if (g.near_kind != 0 || static_cast<int>(blockIdx.x) >= g.ntiles) return;  // (graph launches: upper bounds)
     const int dx = g.dims[0], dy = g.dims[1], dz = g.dims[2];
@@ -750,30 +680,31 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
     const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;
     const int wx = min(kTX, dx - x0), wy = min(kTY, dy - y0), wz = min(kTZ, dz - z0);  // interior extent
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // 1. counts of the halo cells (cells outside the needed halo of a partial brick: 0)
-    int cnts[(kHCells + kTileThreads - 1) / kTileThreads];
+    // 1. counts of the halo cells (cells outside the halo of a partial brick: 0); a
+    //    thread owns kCellsPerThread consecutive cells
+    int cnts[kCellsPerThread];
     int local = 0;
 #pragma unroll
-    for (int k = 0; k < (kHCells + kTileThreads - 1) / kTileThreads; ++k) {
-        const int hc = threadIdx.x * ((kHCells + kTileThreads - 1) / kTileThreads) + k;
+    for (int k = 0; k < kCellsPerThread; ++k) {
+        const int hc = threadIdx.x * kCellsPerThread + k;
         int c = 0;
         if (hc < kHCells) {
             const int hx = hc % kHX, hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
-            if (hx <= wx + 1 && hy <= wy + 1 && hz <= wz) {
-                int X = x0 - 1 + hx, Y = y0 - 1 + hy, Z = z0 + hz;
+            if (hx <= wx + 1 && hy <= wy + 1 && hz <= wz + 1) {
+                int X = x0 - 1 + hx, Y = y0 - 1 + hy, Z = z0 - 1 + hz;
                 X = X < 0 ? X + dx : (X >= dx ? X - dx : X);
                 Y = Y < 0 ? Y + dy : (Y >= dy ? Y - dy : Y);
-                Z = Z >= dz ? Z - dz : Z;
+                Z = Z < 0 ? Z + dz : (Z >= dz ? Z - dz : Z);
                 const int64_t cell = (static_cast<int64_t>(Z) * dy + Y) * dx + X;
                 const int64_t b = cs[cell];
                 c = static_cast<int>(cs[cell + 1] - b);
-                hsrc[hc] = b;
+                hsrc[hc] = static_cast<int32_t>(b);
             }
         }
         cnts[k] = c;
         local += c;
     }
-    // 2. exclusive scan over the halo cells (thread-contiguous chunks)
+    // 2. exclusive scan over the halo cells
     int incl = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -791,8 +722,8 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
     {
         int off = wbase + incl - local;
 #pragma unroll
-        for (int k = 0; k < (kHCells + kTileThreads - 1) / kTileThreads; ++k) {
-            const int hc = threadIdx.x * ((kHCells + kTileThreads - 1) / kTileThreads) + k;
+        for (int k = 0; k < kCellsPerThread; ++k) {
+            const int hc = threadIdx.x * kCellsPerThread + k;
             if (hc < kHCells) hoff[hc] = off;
             off += cnts[k];
         }
@@ -804,176 +735,188 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
             const int Y = y0 + r % wy, Z = z0 + r / wy;
             const int64_t row = (static_cast<int64_t>(Z) * dy + Y) * dx;
             const int64_t b = cs[row + x0], e = cs[row + x0 + wx];
-            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) near_half_particle<3>(q, S, g, cs, skey, nbr);
+            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) near_full_particle<3>(q, S, g, cs, skey, nbr);
         }
         return;
     }
-    // 3. stage the halo: a thread per halo cell copies its particles, shifted into the
-    //    brick's unwrapped frame
-    for (int hc = threadIdx.x; hc < kHCells; hc += blockDim.x) {
-        const int c = hoff[hc + 1] - hoff[hc];
-        if (c == 0) continue;
-        const int hx = hc % kHX, hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
-        const int X = x0 - 1 + hx, Y = y0 - 1 + hy, Z = z0 + hz;
-        const float sxf = X < 0 ? -g.L_f[0] : (X >= dx ? g.L_f[0] : 0.f);
-        const float syf = Y < 0 ? -g.L_f[1] : (Y >= dy ? g.L_f[1] : 0.f);
-        const float szf = Z >= dz ? g.L_f[2] : 0.f;
-        const int64_t b = hsrc[hc];
-        const int o = hoff[hc];
-        for (int k = 0; k < c; ++k) {
-            float4 v = S.xf[b + k];
-            v.x = __fadd_rn(v.x, sxf);
-            v.y = __fadd_rn(v.y, syf);
-            v.z = __fadd_rn(v.z, szf);
-            px[o + k] = v;
-            pj[o + k] = static_cast<int32_t>(b + k);
-            pid[o + k] = S.id[b + k];
-            phc[o + k] = static_cast<uint16_t>(hc);
-        }
-    }
-    // interior rows (hy in [1, wy], hz in [0, wz)): their particles are contiguous
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int r = 0; r < wy * wz; ++r) {
-            rowoff[r] = acc;
-            const int hy = 1 + r % wy, hz = r / wy;
-            const int h0 = (hz * kHY + hy) * kHX + 1;
-            acc += hoff[h0 + wx] - hoff[h0];
-        }
-        rowoff[wy * wz] = acc;
+    // 3. stage the halo.  Along x a row of halo cells holds up to three runs of
+    //    consecutive sorted indices: [0, xa) the image of the last column (shift -L),
+    //    [xa, xc) the body, [xc, kHX) the image of the first columns (+L).  A table per
+    //    row (a thread per row) maps a staged slot to its sorted index; then every thread
+    //    copies a strided set of slots, all loads in flight before any store.
+    if (threadIdx.x < kHRows) {
+        const int r = threadIdx.x, hy = r % kHY, hz = r / kHY;
+        const int xa = x0 == 0 ? 1 : 0, xc = min(kHX, dx - x0 + 1);
+        const int h0 = r * kHX;
+        RowMap m;
+        m.ka = hoff[h0 + xa];
+        m.kc = hoff[h0 + xc];
+        const bool used = hy <= wy + 1 && hz <= wz + 1;
+        m.sa = used && xa ? hsrc[h0] - hoff[h0] : 0;
+        m.sb = used && xa < kHX ? hsrc[h0 + xa] - m.ka : 0;
+        m.sc = used && xc < kHX ? hsrc[h0 + xc] - m.kc : 0;
+        const int Y = y0 - 1 + hy, Z = z0 - 1 + hz;
+        m.sy = Y < 0 ? -g.L_f[1] : (Y >= dy ? g.L_f[1] : 0.f);
+        m.sz = Z < 0 ? -g.L_f[2] : (Z >= dz ? g.L_f[2] : 0.f);
+        rmap[r] = m;
     }
     __syncthreads();
-    // 4. screen every interior particle against its half stencil in shared memory
-    const int nint = rowoff[wy * wz];
+    for (int k0 = 0; k0 < total; k0 += 4 * kTileThreads) {
+        float4 v[4];
+        int32_t src[4];
+        float sxf[4], syf[4], szf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + threadIdx.x + u * kTileThreads;
+            if (k < total) {
+                int r = 0;  // the last row whose first slot is <= k
+#pragma unroll
+                for (int step = 32; step > 0; step >>= 1)
+                    if (r + step < kHRows && hoff[(r + step) * kHX] <= k) r += step;
+                const RowMap& m = rmap[r];
+                src[u] = static_cast<int32_t>(k + (k < m.ka ? m.sa : (k < m.kc ? m.sb : m.sc)));
+                sxf[u] = k < m.ka ? -g.L_f[0] : (k < m.kc ? 0.f : g.L_f[0]);
+                syf[u] = m.sy;
+                szf[u] = m.sz;
+                v[u] = S.xf[src[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + threadIdx.x + u * kTileThreads;
+            if (k < total) {
+                float* a = reinterpret_cast<float*>(pxy + (k >> 1)) + (k & 1);
+                float* b = reinterpret_cast<float*>(pzw + (k >> 1)) + (k & 1);
+                a[0] = __fadd_rn(v[u].x, sxf[u]);
+                a[2] = __fadd_rn(v[u].y, syf[u]);
+                b[0] = __fadd_rn(v[u].z, szf[u]);
+                b[2] = v[u].w;
+                pj[k] = src[u];
+            }
+        }
+    }
+    // interior rows (hy in [1, wy], hz in [1, wz]) hold contiguous particles
+    if (wid == 0) {
+        const int nr = wy * wz;  // <= 32
+        int c = 0;
+        if (lane < nr) {
+            const int h0 = ((1 + lane / wy) * kHY + 1 + lane % wy) * kHX + 1;
+            c = hoff[h0 + wx] - hoff[h0];
+        }
+        int in = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, in, o);
+            if (lane >= o) in += t;
+        }
+        if (lane < nr) rowoff[lane] = in - c;
+        if (lane == nr - 1) rowoff[nr] = in;
+    }
+    __syncthreads();
+    // 4. screen every interior particle against its 3x3x3 stencil in shared memory
+    const int nr = wy * wz;
+    const int nint = rowoff[nr];
     for (int f = threadIdx.x; f < nint; f += blockDim.x) {
         int r = 0;  // the last interior row whose offset is <= f
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1)
-            if (r + step < wy * wz && rowoff[r + step] <= f) r += step;
-        const int hy = 1 + r % wy, hz = r / wy;
-        const int i = hoff[(hz * kHY + hy) * kHX + 1] + (f - rowoff[r]);
-        const int hc = phc[i];
-        const float4 me = px[i];
-        const int32_t idi = pid[i];
-        const float base = __fadd_rn(__fadd_rn(me.w, g.extra_f), g.margin_f);  // + r_j
-        const int64_t q = pj[i];
-        int32_t* myrow = nbr + q * kNearRow;
-        int nf = 0;
-        int32_t fwd[kNearCap];
-        auto run = [&](int b, int e) {
-            for (int k = b; k < e; ++k) {
-                const float4 c = px[k];
-                const float ex = __fsub_rn(c.x, me.x), ey = __fsub_rn(c.y, me.y), ez = __fsub_rn(c.z, me.z);
-                const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
-                const float lim = __fadd_rn(base, c.w);
-                if (d2 > __fmul_rn(__fmul_rn(lim, lim), 1.00001f)) continue;
-                if (pid[k] == idi) continue;  // shape.hpp:544 self-exclusion by id
-                if (nf < kNearCap) {
-                    myrow[2 + nf] = pj[k];
-                    fwd[nf] = pj[k];
-                }
-                ++nf;
-            }
-        };
-        run(i + 1, hoff[hc + 2]);                                   // own cell after i, then cell x+1
-        run(hoff[hc + kHX - 1], hoff[hc + kHX + 2]);                // dy = +1, dx = -1..+1
-        const int up = hc + kHX * kHY;                              // dz = +1
-        run(hoff[up - kHX - 1], hoff[up - kHX + 2]);
-        run(hoff[up - 1], hoff[up + 2]);
-        run(hoff[up + kHX - 1], hoff[up + kHX + 2]);
-        near_publish(nbr, q, nf, fwd);
-    }
-}
-
-// zero the count word (the whole first sector) of every near-list row
-__global__ void k_near_zero(int64_t n, int32_t* __restrict__ nbr) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
-        int4* r = reinterpret_cast<int4*>(nbr + q * kNearRow);
-        r[0] = make_int4(0, 0, 0, 0);
-        r[1] = make_int4(0, 0, 0, 0);
-    }
-}
-
-
-
-template <int D>
-__device__ __forceinline__ void sweep_particle(int64_t q, int32_t sl, const State& S, const Box& box,
-                                               const GridParams& g, const RoundParams& rp,
-                                               const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                               const int32_t* __restrict__ nbr,
-                                               uint8_t* __restrict__ acc, int32_t* __restrict__ active,
-                                               StatsDev* stats) {
-    const int32_t* row = nbr + q * kNearRow;
-    const int4 h0 = *reinterpret_cast<const int4*>(row);  // counts + first two entries
-    const int nf = h0.x, nn = h0.x + h0.y;
-    const double4 me = S.rec[q];  // round-start record; q is visited once
-    double xi[D];
-    rec_pos<D>(me, xi);
-    const double ri = me.w;
-    double p[D];
-    int accepted = -1;
-    if (nn <= kNearCap) {
-#ifndef SRM_TRIAL_PAIRS
-#define SRM_TRIAL_PAIRS 0
+            if (r + step < nr && rowoff[r + step] <= f) r += step;
+        const int rb = ((1 + r / wy) * kHY + 1 + r % wy) * kHX;
+        const int i = hoff[rb + 1] + (f - rowoff[r]);
+        int hx = 1;  // the cell of i in its row: the last x with hoff <= i
+#pragma unroll
+        for (int step = 8; step > 0; step >>= 1)
+            if (hx + step <= wx && hoff[rb + hx + step] <= i) hx += step;
+        const int hc = rb + hx;
+        const float mx = reinterpret_cast<const float*>(pxy + (i >> 1))[i & 1];
+        const float my = reinterpret_cast<const float*>(pxy + (i >> 1))[2 + (i & 1)];
+        const float mz = reinterpret_cast<const float*>(pzw + (i >> 1))[i & 1];
+        const float mw = reinterpret_cast<const float*>(pzw + (i >> 1))[2 + (i & 1)];
+        const int32_t qi = pj[i];
+        const float base = __fadd_rn(__fadd_rn(mw, g.extra_f), g.margin_f);  // + r_j
+        const float2 nmx = make_float2(-mx, -mx), nmy = make_float2(-my, -my), nmz = make_float2(-mz, -mz);
+        const float2 base2 = make_float2(base, base), fac2 = make_float2(1.00001f, 1.00001f);
+        // hits are rare per lane but common per warp: record the hit slots branch-free
+        // (a store to the current list slot every test, the count advances on a hit; slot
+        // kNearCap absorbs the overflow), resolve them after the scan
+        uint16_t* ql = lst + threadIdx.x;
+        int nn = 0, at = 0;
+        // stencil pruning (conservative: margins above the fp32 rounding of the cell
+        // bounds): a row of three cells is skipped when its slab lies beyond the largest
+        // reach of i, and its end cells when the chord of the reach sphere misses them
+        const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(mw, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
+        const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
+        const int hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
+        const float fx = __fsub_rn(mx, __fmul_rn(static_cast<float>(x0 - 1 + hx), g.edge_f[0]));
+        const float fy = __fsub_rn(my, __fmul_rn(static_cast<float>(y0 - 1 + hy), g.edge_f[1]));
+        const float fz = __fsub_rn(mz, __fmul_rn(static_cast<float>(z0 - 1 + hz), g.edge_f[2]));
+        const float gx = __fsub_rn(g.edge_f[0], fx), gy = __fsub_rn(g.edge_f[1], fy), gz = __fsub_rn(g.edge_f[2], fz);
+#pragma unroll
+        for (int ddz = -1; ddz <= 1; ++ddz) {
+#pragma unroll
+            for (int ddy = -1; ddy <= 1; ++ddy) {
+                const int c = hc + ddy * kHX + ddz * kHX * kHY;
+#if SRM_NEAR_PRUNE
+                const float dyd = fmaxf(0.f, __fsub_rn(ddy < 0 ? fy : (ddy > 0 ? gy : 0.f), g.margin_f));
+                const float dzd = fmaxf(0.f, __fsub_rn(ddz < 0 ? fz : (ddz > 0 ? gz : 0.f), g.margin_f));
+                const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
+                if (dyz2 > cut2) continue;
+                float h;  // chord half length; sqrt.approx (rel. error < 2^-22) scaled up by 2^-20
+                asm("sqrt.approx.f32 %0, %1;" : "=f"(h) : "f"(__fsub_rn(cut2, dyz2)));
+                h = __fadd_rn(__fmul_rn(h, 1.000001f), __fmul_rn(2.f, g.margin_f));
+                const int kb = hoff[fx < h ? c - 1 : c], ke = hoff[gx < h ? c + 2 : c + 1];
+#else
+                const int kb = hoff[c - 1], ke = hoff[c + 2];
 #endif
-        if (SRM_TRIAL_PAIRS) {
-        // trials two at a time (speculatively: a trial after the first clear one has no
-            // effect), each neighbour record loaded once for both
-            for (int l = 0; l < rp.n_l && accepted < 0; l += 2) {
-                double pa[D], pb[D];
-                const bool second = l + 1 < rp.n_l;
-                propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), pa);
-                if (second) propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l + 1), pb);
-                bool hit_a = false, hit_b = !second;
-                for (int t = 0; t < nn && !(hit_a && hit_b); ++t) {
-                    const int32_t j = t == 0 ? (nf > 0 ? h0.z : row[kNearRow - 1]) : near_entry(row, nf, t);
-                    const double4 v = S.rec[j];
-                    const double xl[3] = {v.x, v.y, v.z};
-                    hit_a = hit_a || sphere_overlap<D>(box, pa, ri, xl, v.w);
-                    hit_b = hit_b || sphere_overlap<D>(box, pb, ri, xl, v.w);
+                // slots [kb, ke) two at a time (pairs 2p, 2p + 1; the ends masked)
+                for (int p = kb >> 1; 2 * p < ke; ++p) {
+                    const float4 A = pxy[p], B = pzw[p];
+                    const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                    const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                    const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                    const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                    const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                    const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                    const int k0 = 2 * p;
+                    ql[at * kTileThreads] = static_cast<uint16_t>(k0);
+                    nn += (d2.x <= l2.x && k0 >= kb && k0 != i) ? 1 : 0;
+                    at = min(nn, kNearCap);
+                    ql[at * kTileThreads] = static_cast<uint16_t>(k0 + 1);
+                    nn += (d2.y <= l2.y && k0 + 1 < ke && k0 + 1 != i) ? 1 : 0;
+                    at = min(nn, kNearCap);
                 }
-                if (!hit_a) {
-                    accepted = l;
-    #pragma unroll
-                    for (int a = 0; a < D; ++a) p[a] = pa[a];
-                } else if (!hit_b) {
-                    accepted = l + 1;
-    #pragma unroll
-                    for (int a = 0; a < D; ++a) p[a] = pb[a];
+            }
+        }
+        // resolve: sorted indices, and shape.hpp:544 self-exclusion by id
+        int32_t e[kNearCap];
+        int m = 0;
+        if (nn <= kNearCap) {
+            const int32_t idi = S.id[qi];
+#pragma unroll
+            for (int t = 0; t < kNearCap; ++t) {
+                e[t] = 0;
+                if (t < nn) {
+                    const int32_t j = pj[ql[t * kTileThreads]];
+                    if (S.id[j] != idi) e[t] = j;
+                    else e[t] = -1;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kNearCap; ++t) {  // compact out the (rare) same-id entries
+                if (t < nn && e[t] >= 0) {
+#pragma unroll
+                    for (int u = 0; u < kNearCap; ++u)
+                        if (u == m) e[u] = e[t];
+                    ++m;
                 }
             }
         } else {
-            for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
-                propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
-                bool hit = false;
-                for (int t = 0; t < nn && !hit; ++t) {
-                    const int32_t j = t == 0 ? (nf > 0 ? h0.z : row[kNearRow - 1]) : near_entry(row, nf, t);
-                    const double4 v = S.rec[j];
-                    const double xl[3] = {v.x, v.y, v.z};
-                    hit = sphere_overlap<D>(box, p, ri, xl, v.w);
-                }
-                if (!hit) accepted = l;
-            }
+            m = nn;  // overflow: the sweep rescans
         }
-    } else {  // crowded neighbourhood: rescan (same candidate set, id filter as the list)
-        const int32_t idq = S.id[q];
-        for (int l = 0; l < rp.n_l && accepted < 0; ++l) {
-            propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
-            bool ok = true;
-            near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
-                if (!ok || S.id[j] == idq) return;
-                const double4 v = S.rec[j];
-                const double xl[3] = {v.x, v.y, v.z};
-                if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
-            });
-            if (ok) accepted = l;
-        }
+        int4* row = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
+        row[0] = make_int4(m, e[0], e[1], e[2]);
+        row[1] = make_int4(e[3], e[4], e[5], e[6]);
     }
-    if (rp.write_acc) acc[q] = accepted >= 0 ? static_cast<uint8_t>(accepted) : kNotAccepted;
-    if (accepted >= 0)  // publish the live position (in place: the sorted state is the round's output)
-        S.rec[q] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, ri);
-    else
-        active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
 }
 
 #ifndef SRM_SWEEP_THREADS
@@ -984,6 +927,23 @@ __device__ __forceinline__ void sweep_particle(int64_t q, int32_t sl, const Stat
 #endif
 constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
+
+// Crowded neighbourhood (overflowed near list): test trial p of q against every
+// candidate of its stencil (same candidates, id filter).
+template <int D>
+__device__ __forceinline__ bool trial_clear_rescan(int64_t q, const double* p, double ri, const State& S, const Box& box,
+                                                const GridParams& g, const int64_t* __restrict__ cs,
+                                                const uint32_t* __restrict__ skey) {
+    const int32_t idq = S.id[q];
+    bool ok = true;
+    near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+        if (!ok || S.id[j] == idq) return;
+        const double4 v = S.rec[j];
+        const double xl[3] = {v.x, v.y, v.z};
+        if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
+    });
+    return ok;
+}
 
 // One trial of particle q (slot sl, round-start position xi, radius ri): propose trial l
 // and test it against the live positions of q's near list (or, for an overflowed list,
@@ -996,34 +956,29 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
                                            double* p) {
     propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
     const int32_t* row = nbr + q * kNearRow;
-    const int2 h0 = *reinterpret_cast<const int2*>(row);
-    const int nf = h0.x, nn = h0.x + h0.y;
+    const int4 h0 = *reinterpret_cast<const int4*>(row);  // (n, e0, e1, e2)
+    const int nn = h0.x;
     if (nn <= kNearCap) {
-        // four neighbours at a time: all record loads issued before any test
-        for (int t0 = 0; t0 < nn; t0 += 4) {
-            double4 v[4];
+        // the first three neighbours: every record load issued before any test
+        double4 v[3];
+        if (nn > 0) v[0] = S.rec[h0.y];
+        if (nn > 1) v[1] = S.rec[h0.z];
+        if (nn > 2) v[2] = S.rec[h0.w];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (t0 + u < nn) v[u] = S.rec[near_entry(row, nf, t0 + u)];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (t0 + u < nn) {
-                    const double xl[3] = {v[u].x, v[u].y, v[u].z};
-                    if (sphere_overlap<D>(box, p, ri, xl, v[u].w)) return false;
-                }
+        for (int u = 0; u < 3; ++u) {
+            if (u < nn) {
+                const double xl[3] = {v[u].x, v[u].y, v[u].z};
+                if (sphere_overlap<D>(box, p, ri, xl, v[u].w)) return false;
             }
+        }
+        for (int t = 3; t < nn; ++t) {  // the rest of the row (rare at the bench window)
+            const double4 w = S.rec[row[1 + t]];
+            const double xl[3] = {w.x, w.y, w.z};
+            if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
         }
         return true;
     }
-    const int32_t idq = S.id[q];  // crowded neighbourhood: rescan (same candidates, id filter)
-    bool ok = true;
-    near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
-        if (!ok || S.id[j] == idq) return;
-        const double4 v = S.rec[j];
-        const double xl[3] = {v.x, v.y, v.z};
-        if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
-    });
-    return ok;
+    return trial_clear_rescan<D>(q, p, ri, S, box, g, cs, skey);
 }
 
 // Platelet version of trial_clear: trial l of q = translation by c_m along the unit
@@ -1047,11 +1002,10 @@ __device__ __forceinline__ bool trial_clear_pl(int64_t q, int32_t sl, int l, con
         return pl::spherodisk_overlap(d, *pn, Di, ti, pl::V3{a.x, a.y, a.z}, v.w, a.w, c_seed_table);
     };
     const int32_t* row = nbr + q * kNearRow;
-    const int2 h0 = *reinterpret_cast<const int2*>(row);
-    const int nf = h0.x, nn = h0.x + h0.y;
+    const int nn = row[0];
     if (nn <= kNearCap) {
         for (int t = 0; t < nn; ++t)
-            if (hit(near_entry(row, nf, t))) return false;
+            if (hit(row[1 + t])) return false;
         return true;
     }
     const int32_t idq = S.id[q];  // crowded neighbourhood: rescan (same candidates, id filter)
