@@ -1038,13 +1038,15 @@ __device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int*
     }
 }
 
-// The class sweep with a queue per warp, kept in registers: each lane holds one item
-// (particle, next trial, its cell's end), every round runs one trial per item, the
-// surviving items are compacted to the low lanes with a ballot + shuffles, and the free
-// lanes take the next cells of the warp's contiguous share of the class lattice (empty
-// cells are skipped, a done particle hands its cell on to the next one in slot order).
-// No barriers and no work lists: warps progress independently.  Per cell the visiting
-// order and the trials are those of the sequential sweep (orc_sweep_round).
+// The class sweep with a queue per warp: each lane holds one item (particle, next trial,
+// its cell's end) and every round runs one trial per item.  A lane whose particle is
+// done takes the next particle of its cell (slot order) or, when the cell is finished,
+// claims the next non-empty cell of the warp's share of the class lattice from a
+// 32-cell window in shared memory (free lanes rank themselves with a ballot; items never
+// move between lanes).  The window's cell ranges are loaded one window ahead so that the
+// cell_start loads overlap the trials in flight.  No barriers and no work lists: warps
+// progress independently.  Per cell the visiting order and the trials are those of the
+// sequential sweep (orc_sweep_round).
 template <int D, bool PL = false>
 __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls_arg, const int* __restrict__ cls_dev,
                                                                                State S, Box box,
@@ -1056,80 +1058,78 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                                                                                uint8_t* __restrict__ acc,
                                                                                int32_t* __restrict__ active,
                                                                                StatsDev* stats) {
+    __shared__ int2 win_s[kSweepThreads];  // per warp: 32 (begin, end) cell ranges
     const int cls = cls_dev ? *cls_dev : cls_arg;  // (device-resident loop: from the controller)
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
     const RoundParams rp = *rpp;
     const int lane = threadIdx.x & 31;
+    int2* win = win_s + (threadIdx.x & ~31);
+    const unsigned lt = (1u << lane) - 1u;
     int first[3], stride[3], cnt[3];
     class_lattice(g, cls, first, stride, cnt);
-    const int64_t cells = static_cast<int64_t>(cnt[0]) * cnt[1] * cnt[2];
-    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    int64_t next = cells * w / nwarps;  // this warp's share of the lattice [next, stop)
-    const int64_t stop = cells * (w + 1) / nwarps;
-    int n = 0;  // live items in lanes [0, n)
-    int32_t iq = 0, il = 0, isl = 0, iend = 0;
-    // look-ahead window of 32 lattice cells: (wb, we) = cell range; loaded one round
-    // ahead of its use so the cell_start loads overlap the trials in flight
-    int wn = 0;
-    bool wraw = false;
-    int64_t wb = 0, we = 0;
-    const int64_t cxy = static_cast<int64_t>(cnt[0]) * cnt[1];
-    auto load_window = [&]() {
-        const int64_t t = next + lane;
-        wb = 0;
-        we = 0;
+    const uint32_t cells = static_cast<uint32_t>(cnt[0]) * cnt[1] * cnt[2];
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t next = static_cast<uint32_t>(static_cast<uint64_t>(cells) * w / nwarps);  // [next, stop)
+    const uint32_t stop = static_cast<uint32_t>(static_cast<uint64_t>(cells) * (w + 1) / nwarps);
+    const FastDiv fdx = make_fastdiv(static_cast<uint32_t>(cnt[0])), fdxy = make_fastdiv(static_cast<uint32_t>(cnt[0] * cnt[1]));
+    // raw window entry of this lane (the lattice cell next + lane), loaded ahead
+    int32_t rb = 0, re = 0;
+    auto load_raw = [&]() {
+        const uint32_t t = next + lane;
+        rb = 0;
+        re = 0;
         if (t < stop) {
-            const int iz = static_cast<int>(t / cxy);
-            const int64_t r2 = t - iz * cxy;
-            const int iy = static_cast<int>(r2 / cnt[0]), ix = static_cast<int>(r2 - static_cast<int64_t>(iy) * cnt[0]);
-            const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
-                                     g.dims[0] + first[0] + stride[0] * ix;
-            wb = cs[cell];
-            we = cs[cell + 1];
+            const uint32_t iz = fdiv(t, fdxy);
+            const uint32_t r2 = t - iz * static_cast<uint32_t>(cnt[0] * cnt[1]);
+            const uint32_t iy = fdiv(r2, fdx), ix = r2 - iy * static_cast<uint32_t>(cnt[0]);
+            const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * static_cast<int>(iz)) * g.dims[1] + first[1] +
+                                  stride[1] * static_cast<int>(iy)) * g.dims[0] + first[0] + stride[0] * static_cast<int>(ix);
+            rb = static_cast<int32_t>(cs[cell]);
+            re = static_cast<int32_t>(cs[cell + 1]);
         }
-        const int64_t left = stop - next;
-        next += left < 32 ? left : 32;
-        wraw = true;
+        next = stop - next < 32u ? stop : next + 32u;
     };
-    load_window();
+    bool have_raw = next < stop;
+    if (have_raw) load_raw();
+    int wn = 0, wofs = 0;  // window entries [wofs, wn) not yet claimed
+    bool valid = false;
+    int32_t iq = 0, il = 0, isl = 0, iend = 0;
     for (;;) {
-        while (n < 32) {  // free lanes take the next non-empty cells of the window
-            if (wraw) {
-                const unsigned gm = __ballot_sync(0xffffffffu, wb < we);
+        // free lanes claim cells (warp-uniform loop)
+        for (;;) {
+            const unsigned fm = __ballot_sync(0xffffffffu, !valid);
+            if (fm == 0) break;
+            if (wofs == wn) {
+                if (!have_raw) break;
+                // publish the raw window: the non-empty ranges, in lattice order
+                const bool ne = rb < re;
+                const unsigned gm = __ballot_sync(0xffffffffu, ne);
+                __syncwarp();
+                if (ne) win[__popc(gm & lt)] = make_int2(rb, re);
+                __syncwarp();
                 wn = __popc(gm);
-                const int src = lane < wn ? static_cast<int>(__fns(gm, 0, lane + 1)) : lane;
-                wb = __shfl_sync(0xffffffffu, wb, src);
-                we = __shfl_sync(0xffffffffu, we, src);
-                wraw = false;
-            }
-            if (wn == 0) {
-                if (next >= stop) break;
-                load_window();
+                wofs = 0;
+                have_raw = next < stop;
+                if (have_raw) load_raw();  // the next window, in flight behind the trials
                 continue;
             }
-            const int take = wn < 32 - n ? wn : 32 - n;
-            const int k = lane - n;
-            const bool mine = k >= 0 && k < take;
-            const int64_t tb = __shfl_sync(0xffffffffu, wb, mine ? k : lane);
-            const int64_t te = __shfl_sync(0xffffffffu, we, mine ? k : lane);
-            if (mine) {
-                iq = static_cast<int32_t>(tb);
-                iend = static_cast<int32_t>(te);
+            const int rank = __popc(fm & lt);
+            const int avail = wn - wofs;
+            if (!valid && rank < avail) {
+                const int2 c = win[wofs + rank];
+                iq = c.x;
+                iend = c.y;
                 il = 0;
-                isl = S.slot[tb];
+                isl = S.slot[iq];
+                valid = true;
             }
-            const int sh = lane + take < 32 ? lane + take : lane;
-            wb = __shfl_sync(0xffffffffu, wb, sh);
-            we = __shfl_sync(0xffffffffu, we, sh);
-            wn -= take;
-            n += take;
+            const int nf = __popc(fm);
+            wofs += nf < avail ? nf : avail;
         }
-        if (wn == 0 && !wraw && next < stop) load_window();  // consumed next round
-        if (n == 0) break;
-        bool keep = false;
-        if (lane < n) {
+        if (__ballot_sync(0xffffffffu, valid) == 0) break;
+        if (valid) {
             const double4 me = S.rec[iq];  // round-start record (the particle has not moved)
             double xi[D], p[D];
             rec_pos<D>(me, xi);
@@ -1153,21 +1153,16 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                 if (rp.write_acc) acc[iq] = kNotAccepted;
                 active[atomicAdd(&stats->active_count, 1ull)] = iq;
             }
-            if (done && iq + 1 < iend) {  // the next particle of the cell
-                iq += 1;
-                il = 0;
-                isl = S.slot[iq];
-                done = false;
+            if (done) {
+                if (iq + 1 < iend) {  // the next particle of the cell
+                    iq += 1;
+                    il = 0;
+                    isl = S.slot[iq];
+                } else {
+                    valid = false;
+                }
             }
-            keep = !done;
         }
-        const unsigned km = __ballot_sync(0xffffffffu, keep);
-        n = __popc(km);
-        const int src = lane < n ? static_cast<int>(__fns(km, 0, lane + 1)) : lane;
-        iq = __shfl_sync(0xffffffffu, iq, src);
-        il = __shfl_sync(0xffffffffu, il, src);
-        isl = __shfl_sync(0xffffffffu, isl, src);
-        iend = __shfl_sync(0xffffffffu, iend, src);
     }
 }
 
