@@ -920,10 +920,13 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
 }
 
 #ifndef SRM_SWEEP_THREADS
-#define SRM_SWEEP_THREADS 128
+#define SRM_SWEEP_THREADS 64
+#endif
+#ifndef SRM_SERPENTINE
+#define SRM_SERPENTINE 1
 #endif
 #ifndef SRM_SWEEP_MINB
-#define SRM_SWEEP_MINB 6
+#define SRM_SWEEP_MINB 10
 #endif
 constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
@@ -1074,13 +1077,17 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
     uint32_t next = static_cast<uint32_t>(static_cast<uint64_t>(cells) * w / nwarps);  // [next, stop)
     const uint32_t stop = static_cast<uint32_t>(static_cast<uint64_t>(cells) * (w + 1) / nwarps);
     const FastDiv fdx = make_fastdiv(static_cast<uint32_t>(cnt[0])), fdxy = make_fastdiv(static_cast<uint32_t>(cnt[0] * cnt[1]));
+    // odd classes walk the share backwards: they start where the previous class launch
+    // ended, whose records are still in L2 (the order of independent cells is free)
+    const uint32_t flip = (SRM_SERPENTINE && (cls & 1)) ? next + stop - 1 : 0;
     // raw window entry of this lane (the lattice cell next + lane), loaded ahead
     int32_t rb = 0, re = 0;
     auto load_raw = [&]() {
-        const uint32_t t = next + lane;
+        uint32_t t = next + lane;
         rb = 0;
         re = 0;
         if (t < stop) {
+            if (flip) t = flip - t;
             const uint32_t iz = fdiv(t, fdxy);
             const uint32_t r2 = t - iz * static_cast<uint32_t>(cnt[0] * cnt[1]);
             const uint32_t iy = fdiv(r2, fdx), ix = r2 - iy * static_cast<uint32_t>(cnt[0]);
