@@ -349,7 +349,7 @@ def run_b200(args, cfg, world, rank, local, pg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic,
-                         "kernel": "migrate step per round: near lists (k_near_zero + k_near_tiles) + k_sweep_warpq x colour classes",
+                         "kernel": "migrate step per round: near lists (k_near_tiles) + k_sweep_warpq x colour classes",
                          "traffic_unit": "bytes per step (one round of near lists + sweep), ncu dram__bytes_read+write",
                          "algorithmic_bytes_per_step": algo,
                          "algorithmic_bytes_per_update": BYTES_STEP[dim], "step_ms_per_round": t_mig,
