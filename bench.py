@@ -36,21 +36,58 @@ sys.path.insert(0, ROOT)
 METRIC = "particle-updates/sec per SRM iteration (1 B200) and % of HBM roofline"
 UNIT = "particle-updates/s"
 
-# BASELINE.json configs (SURVEY.md §8d synthetic inputs)
+# BASELINE.json configs (SURVEY.md §8d synthetic inputs).  cfg4 is the bench workload;
+# the others run with --config (parity cases at full size, and their throughput).
 CONFIGS = {
     "cfg1": dict(desc="2D monodisperse disks N=1e4, unit square, f_target 0.50, c_m=0.1 r_t",
-                 dim=2, n=10_000, f_target=0.50, cm_rel=0.10, f0=0.1),
+                 kind="mono", dim=2, n=10_000, f_target=0.50, cm_rel=0.10, f0=0.1),
     "cfg2": dict(desc="3D monodisperse spheres N=1e6, unit cube, f_target 0.40, c_m=0.1 r_t",
-                 dim=3, n=1_000_000, f_target=0.40, cm_rel=0.10, f0=0.1),
+                 kind="mono", dim=3, n=1_000_000, f_target=0.40, cm_rel=0.10, f0=0.1),
+    "cfg3": dict(desc="3D polydisperse spheres N=1e6, lognormal radii (mean 1, CV 0.2, clipped to [0.5, 2]), "
+                      "clustered start (1000 Gaussian clusters, sigma 3), f_target 0.50, c_m=0.1",
+                 kind="poly", dim=3, n=1_000_000, f_target=0.50, cm_abs=0.10, f0=0.05, clusters=1000, sigma=3.0,
+                 sample_n=20_000, prep_iters=400),
     "cfg4": dict(desc="3D monodisperse spheres N=1e7, unit cube, f_target 0.30, c_m=0.05 r_t",
-                 dim=3, n=10_000_000, f_target=0.30, cm_rel=0.05, f0=0.1),
+                 kind="mono", dim=3, n=10_000_000, f_target=0.30, cm_rel=0.05, f0=0.1),
+    "cfg5": dict(desc="3D thin platelets N=1e5, thickness/diameter 0.01, box 25.01, normals uniform, f_target 0.05, "
+                      "rsa_platelets start at rho 3.5, grown with the reference recipe's grow stage (c_w=0.008, "
+                      "c_m=0.01, c_r=0.012, n_k=n_l=20; recipes.cpp:205-213)",
+                 kind="platelet", dim=3, n=100_000, f_target=0.05, L=25.01, aspect=100.0, cm_abs=0.01, c_r=0.012,
+                 c_w=0.008, rho0=3.5, rho_cpu=3.5, n_l=20, n_k=20, sample_n=4_000, prep_iters=400),
 }
 F_WINDOW = 0.98   # steady-state window at 0.98 f_target
 N_K = 10          # rounds per iteration / shake sweeps (srmgen.cpp:407-410)
 N_L = 10          # attempts per particle per round
 C_W = 0.02        # SrmParams default swelling rate (engine.hpp:23)
 SAMPLE_N = 100_000  # CPU sample size (same density, radius and c_m as the workload)
-BYTES_STEP = {2: 40, 3: 56}  # algorithmic HBM bytes per particle-update, migrate step (§8d)
+BYTES_STEP = {2: 40, 3: 56, "platelet": 112}  # algorithmic HBM bytes per particle-update, migrate step (§8d)
+
+
+def poly_radii(n, seed):
+    """cfg3 radii: lognormal with mean 1 and CV 0.2 (sigma^2 = ln 1.04, mu = -sigma^2 / 2),
+    clipped to [0.5, 2]; numpy PCG64 seeded."""
+    s2 = math.log(1.04)
+    rng = np.random.default_rng(seed & 0xFFFFFFFF)
+    return np.clip(rng.lognormal(-0.5 * s2, math.sqrt(s2), n), 0.5, 2.0)
+
+
+def platelet_measure(D, t):
+    """spherodisk_measure (spherodisk.hpp:29-34): a = (D - t) / 2, s = t / 2,
+    2 pi a^2 s + pi^2 a s^2 + 4/3 pi s^3."""
+    a, h = 0.5 * (D - t), 0.5 * t
+    return 2.0 * math.pi * a * a * h + math.pi * math.pi * a * h * h + 4.0 / 3.0 * math.pi * h ** 3
+
+
+def platelet_diameter(f, n, L, aspect):
+    """Diameter at which n platelets of the aspect ratio fill fraction f of an L^3 box."""
+    lo, hi = 1e-6, L
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if n * platelet_measure(mid, mid / aspect) / L ** 3 < f:
+            lo = mid
+        else:
+            hi = mid
+    return lo
 
 
 def unit_measure(dim):
@@ -176,6 +213,14 @@ def ref_lib():
     L.ref_bench_rounds.restype = C.c_double
     L.ref_bench_rounds.argtypes = [C.c_int, vp, C.c_int64, vp, vp, vp, C.c_double, C.c_int, C.c_int,
                                    C.c_uint64, C.c_int, vp]
+    L.ref_rsa_platelets.restype = C.c_int
+    L.ref_rsa_platelets.argtypes = [C.c_int64, C.c_double, C.c_double, vp, C.c_int64, C.c_uint64, vp, vp, vp]
+    L.ref_generate_platelets.restype = C.c_int
+    L.ref_generate_platelets.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, C.c_double, C.c_double, C.c_double,
+                                         C.c_int, C.c_int, C.c_double, C.c_int64, C.c_uint64, C.c_int, vp, vp]
+    L.ref_pl_bench_rounds.restype = C.c_double
+    L.ref_pl_bench_rounds.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, C.c_double, C.c_double, C.c_int, C.c_int,
+                                      C.c_uint64, C.c_int, vp]
     return L
 
 
@@ -183,36 +228,61 @@ def _p(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def sample_n(cfg):
+    return cfg.get("sample_n", SAMPLE_N)
+
+
 def ref_sample_state(cfg, seed):
-    """SAMPLE_N spheres at the workload's number density, radius and c_m, prepared by
-    the reference itself: rsa_place at f0, then srm_generate to the window."""
+    """A bounded sample of the workload (sample_n(cfg) particles at its number density,
+    radii and c_m), prepared by the reference itself: rsa_place / rsa_platelets, then
+    srm_generate to the window.  Returns (lib, state) for ref_rounds."""
     L = ref_lib()
-    dim, n = cfg["dim"], SAMPLE_N
-    box = (n / cfg["n"]) ** (1.0 / dim)
+    dim, n, kind = cfg["dim"], sample_n(cfg), cfg["kind"]
+    it = np.zeros(1, np.int64)
+    f = np.zeros(1)
+    acc = np.zeros(1, np.int64)
+    if kind == "platelet":
+        box = cfg["L"] * (n / cfg["n"]) ** (1.0 / 3.0)
+        Lb = np.full(3, box)
+        # the reference's platelet srm_generate needs tens of minutes even for a few
+        # thousand platelets, so its sample is its own RSA state at the recipe's start
+        # density rho = min(0.7 rho_target, 3.5) (recipes.cpp:192-197), not the window
+        D0 = (cfg["rho_cpu"] * box ** 3 / n) ** (1.0 / 3.0)
+        pos, nrm, ids = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(n, np.int32)
+        st = L.ref_rsa_platelets(n, D0, cfg["aspect"], _p(Lb), 100000, seed, _p(pos), _p(nrm), _p(ids))
+        assert st == 0, "reference rsa_platelets failed"
+        D, t = np.full(n, D0), np.full(n, D0 / cfg["aspect"])
+        return L, dict(kind=kind, Lb=Lb, pos=pos, nrm=nrm, D=D, t=t, ids=ids, c_m=cfg["cm_abs"], c_r=cfg["c_r"],
+                       n_l=cfg["n_l"])
+    if kind == "poly":
+        radii_t = poly_radii(n, seed)
+        box = (np.sum(4.0 / 3.0 * math.pi * radii_t ** 3) / cfg["f_target"]) ** (1.0 / 3.0)
+        radii = radii_t * (cfg["f0"] / cfg["f_target"]) ** (1.0 / 3.0)
+        c_m = cfg["cm_abs"]
+    else:
+        box = (n / cfg["n"]) ** (1.0 / dim)
+        r_t = radius_for(cfg["f_target"], cfg["n"], dim)
+        radii = np.full(n, radius_for(cfg["f0"], cfg["n"], dim))
+        c_m = cfg["cm_rel"] * r_t
     Lb = np.full(dim, box)
-    r_t = radius_for(cfg["f_target"], cfg["n"], dim)
-    r0 = radius_for(cfg["f0"], cfg["n"], dim)
-    radii = np.full(n, r0)
     pos = np.zeros((n, dim))
     ids = np.zeros(n, np.int32)
     placed = np.zeros(1, np.int64)
     st = L.ref_rsa_place(dim, _p(Lb), n, _p(radii), 10000, seed, _p(pos), _p(ids), _p(placed))
     assert st == 0, "reference rsa_place failed"
-    it = np.zeros(1, np.int64)
-    f = np.zeros(1)
-    acc = np.zeros(1, np.int64)
-    c_m = cfg["cm_rel"] * r_t
     st = L.ref_generate(dim, _p(Lb), n, _p(pos), _p(radii), _p(ids), C_W, c_m, N_K, N_L,
                         F_WINDOW * cfg["f_target"], 100000, seed + 1, 16, _p(it), _p(f), _p(acc))
     assert st == 0, "reference srm_generate failed"
-    return L, Lb, pos, radii, ids, c_m
+    return L, dict(kind=kind, Lb=Lb, pos=pos, radii=radii, ids=ids, c_m=c_m, n_l=N_L)
 
 
-def ref_rounds(L, Lb, pos, radii, ids, c_m, rounds, threads, seed):
+def ref_rounds(L, S, rounds, threads, seed):
     acc = np.zeros(1, np.int64)
-    secs = L.ref_bench_rounds(len(Lb), _p(Lb), len(radii), _p(pos), _p(radii), _p(ids), c_m, N_L,
-                              rounds, seed, threads, _p(acc))
-    return secs
+    if S["kind"] == "platelet":
+        return L.ref_pl_bench_rounds(_p(S["Lb"]), len(S["D"]), _p(S["pos"]), _p(S["nrm"]), _p(S["D"]), _p(S["t"]),
+                                     _p(S["ids"]), S["c_m"], S["c_r"], S["n_l"], rounds, seed, threads, _p(acc))
+    return L.ref_bench_rounds(len(S["Lb"]), _p(S["Lb"]), len(S["radii"]), _p(S["pos"]), _p(S["radii"]), _p(S["ids"]),
+                              S["c_m"], S["n_l"], rounds, seed, threads, _p(acc))
 
 
 def run_reference(args, cfg, world, rank, pg):
@@ -221,22 +291,24 @@ def run_reference(args, cfg, world, rank, pg):
     threads = os.cpu_count() or 1
     seed = 20260101
     t0 = time.time()
-    L, Lb, pos, radii, ids, c_m = ref_sample_state(cfg, seed)
+    L, S = ref_sample_state(cfg, seed)
+    c_m, ns = S["c_m"], sample_n(cfg)
     prep = time.time() - t0
     if args.warmup > 0:
-        ref_rounds(L, Lb, pos, radii, ids, c_m, args.warmup, threads, seed + 7)
-    secs = ref_rounds(L, Lb, pos, radii, ids, c_m, args.steps, threads, seed + 9)
-    value = threads * SAMPLE_N * args.steps / secs
+        ref_rounds(L, S, args.warmup, threads, seed + 7)
+    secs = ref_rounds(L, S, args.steps, threads, seed + 9)
+    value = threads * ns * args.steps / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded reference rsa_place at f0 + reference srm_generate to 0.98 f_target)",
+        "data": ("synthetic (seeded reference rsa_platelets at rho 3.5)" if S["kind"] == "platelet" else
+                 "synthetic (seeded reference rsa_place at f0 + reference srm_generate to 0.98 f_target)"),
         "config": {"workload": args.config + ": " + cfg["desc"], "n_workload": cfg["n"],
-                   "n_sample_per_replica": SAMPLE_N, "replicas": threads, "n_l": N_L,
+                   "n_sample_per_replica": ns, "replicas": threads, "n_l": S["n_l"],
                    "c_m": c_m, "step": "one SRM round (build_shape_grid -> migrate -> shape_any_collision) per replica"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{threads} replicas x {SAMPLE_N} spheres (workload density/radius/c_m), "
+                         "sample": f"{threads} replicas x {ns} particles (workload density/radii/c_m), "
                                    f"{args.steps} rounds each; state prep {prep:.1f}s untimed"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -246,20 +318,43 @@ def run_reference(args, cfg, world, rank, pg):
 
 # ---- B200 arm ------------------------------------------------------------------------------
 def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
-    dim = cfg["dim"]
+    """The workload's start state (host RSA: rsa_place / rsa_clustered / rsa_platelets),
+    uploaded and grown on the device by srm_generate to 0.98 f_target.  n, box: a scaled
+    copy at the same density (tools/ only)."""
+    dim, kind = cfg["dim"], cfg["kind"]
     n = n or cfg["n"]
-    Lb = [box] * dim
-    r_t = radius_for(cfg["f_target"], cfg["n"], dim)
-    r0 = radius_for(cfg["f0"], cfg["n"], dim)
-    c_m = cfg["cm_rel"] * r_t
     t0 = time.time()
-    pos, ids = srm.rsa_place(np.full(n, r0), Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
-    t_rsa = time.time() - t0
-    ctx = srm.Context(Lb, n, device)
-    ctx.upload(pos, np.full(n, r0), ids)
+    if kind == "platelet":
+        Lb = [cfg["L"] * box] * 3
+        D0 = (cfg["rho0"] * Lb[0] ** 3 / n) ** (1.0 / 3.0)
+        pos, nrm, ids = srm.rsa_platelets(n, D0, cfg["aspect"], Lb, 100000, seed)
+        t_rsa = time.time() - t0
+        ctx = srm.Context(Lb, n, device, shape="platelet")
+        ctx.upload_platelets(pos, nrm, np.full(n, D0), np.full(n, D0 / cfg["aspect"]), ids)
+        c_m, n_k, n_l = cfg["cm_abs"], cfg["n_k"], cfg["n_l"]
+        params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, c_r=cfg["c_r"], n_k=n_k, n_l=n_l,
+                               f_target=F_WINDOW * cfg["f_target"], max_iterations=cfg.get("prep_iters", 100000),
+                               seed=seed + 1, reorder_period=16)
+        ctx.set_rotation(cfg["c_r"])
+    else:
+        if kind == "poly":
+            r_t = poly_radii(n, seed)
+            L = (np.sum(4.0 / 3.0 * math.pi * r_t ** 3) / cfg["f_target"]) ** (1.0 / 3.0)
+            r0 = r_t * (cfg["f0"] / cfg["f_target"]) ** (1.0 / 3.0)
+            Lb = [L] * dim
+            pos, ids = srm.rsa_clustered(r0, Lb, cfg["clusters"], cfg["sigma"], 10000, seed)
+            c_m = cfg["cm_abs"]
+        else:
+            Lb = [box] * dim
+            r0 = np.full(n, radius_for(cfg["f0"], cfg["n"], dim))
+            pos, ids = srm.rsa_place(r0, Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
+            c_m = cfg["cm_rel"] * radius_for(cfg["f_target"], cfg["n"], dim)
+        t_rsa = time.time() - t0
+        ctx = srm.Context(Lb, n, device)
+        ctx.upload(pos, r0, ids)
+        params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, n_k=N_K, n_l=N_L, f_target=F_WINDOW * cfg["f_target"],
+                               max_iterations=cfg.get("prep_iters", 100000), seed=seed + 1, reorder_period=16)
     t0 = time.time()
-    params = srm.SrmParams(c_w=C_W, c_m=c_m, n_k=N_K, n_l=N_L, f_target=F_WINDOW * cfg["f_target"],
-                           max_iterations=100000, seed=seed + 1, reorder_period=16)
     out = ctx.generate(params)
     t_gen = time.time() - t0
     info = {"rsa_s": round(t_rsa, 2), "generate_s": round(t_gen, 3), "generate_iterations": out.iteration_count,
@@ -270,7 +365,8 @@ def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
 
 def run_b200(args, cfg, world, rank, local, pg):
     import paper_2605_18254_b200 as srm
-    dim, n = cfg["dim"], cfg["n"]
+    dim, n, kind = cfg["dim"], cfg["n"], cfg["kind"]
+    n_l, n_k = cfg.get("n_l", N_L), cfg.get("n_k", N_K)
     seed = srm.mix_seed(20260101, rank)
     ctx, c_m, prep = gpu_state(srm, cfg, seed, local)
     max_r = ctx.max_bounding_radius()
@@ -279,14 +375,14 @@ def run_b200(args, cfg, world, rank, local, pg):
 
     # warm-up rounds, then exactly K timed rounds bracketed by barrier + sync
     if args.warmup:
-        ctx.rounds(cs, c_m, N_L, key, 0, 1, args.warmup)
+        ctx.rounds(cs, c_m, n_l, key, 0, 1, args.warmup)
     ctx.sync()
     barrier(pg)
     clocks = Clocks(local)
     clocks.start()
     l0 = ctx.launch_count()
     ctx.stopwatch_start()
-    st = ctx.rounds(cs, c_m, N_L, key, 1000, 1, args.steps)
+    st = ctx.rounds(cs, c_m, n_l, key, 1000, 1, args.steps)
     ms = ctx.stopwatch_stop()
     launches = ctx.launch_count() - l0
     clk = clocks.stop()
@@ -296,7 +392,7 @@ def run_b200(args, cfg, world, rank, local, pg):
 
     # per-kernel-family split (separate pass: the events sit between kernels)
     ctx.timing_enable(True)
-    ctx.rounds(cs, c_m, N_L, key, 2000, 1, args.steps)
+    ctx.rounds(cs, c_m, n_l, key, 2000, 1, args.steps)
     fam_ms, fam_calls = ctx.timing_get()
     ctx.timing_enable(False)
     per_round = [v / args.steps for v in fam_ms]
@@ -304,31 +400,53 @@ def run_b200(args, cfg, world, rank, local, pg):
     # colour class); per-round device time from CUDA events on the context stream
     t_mig = per_round[1] + per_round[2]
     peak, peak_kind = peaks()
-    algo = n * BYTES_STEP[dim]
+    bpu = BYTES_STEP["platelet" if kind == "platelet" else dim]
+    algo = n * bpu
     achieved = algo / (t_mig * 1e-3) / 1e9 if t_mig > 0 else 0.0
 
     # e2e through the C ABI with host buffers: H2D of the state, n_k rounds (one
     # iteration's worth, like shake()), D2H of the state + the round statistics
     import torch
-    pos_h = torch.empty((n, dim), dtype=torch.float64, pin_memory=True).numpy()
-    r_h = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
-    id_h = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
-    ctx.download(pos_h, r_h, id_h)
+
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+
+    if kind == "platelet":
+        bufs = (pinned((n, 3), torch.float64), pinned((n, 3), torch.float64), pinned(n, torch.float64),
+                pinned(n, torch.float64), pinned(n, torch.int32))
+        bytes_io = n * (8 * 8 + 4)
+
+        def down():
+            p, q, d, t, i = ctx.download_platelets()
+            for dst, src in zip(bufs, (p, q, d, t, i)):
+                dst[...] = src
+
+        def up():
+            ctx.upload_platelets(*bufs)
+    else:
+        bufs = (pinned((n, dim), torch.float64), pinned(n, torch.float64), pinned(n, torch.int32))
+        bytes_io = n * (8 * dim + 8 + 4)
+
+        def down():
+            ctx.download(*bufs)
+
+        def up():
+            ctx.upload(*bufs)
     e2e_steps = max(2, min(args.steps, 5))
-    ctx.upload(pos_h, r_h, id_h)
-    ctx.rounds(cs, c_m, N_L, key, 3000, 1, N_K)
-    ctx.download(pos_h, r_h, id_h)
+    down()
+    up()
+    ctx.rounds(cs, c_m, n_l, key, 3000, 1, n_k)
+    down()
     barrier(pg)
     ctx.stopwatch_start()
     for s in range(e2e_steps):
-        ctx.upload(pos_h, r_h, id_h)
-        ctx.rounds(cs, c_m, N_L, key, 4000 + s * N_K, 1, N_K)
-        ctx.download(pos_h, r_h, id_h)
+        up()
+        ctx.rounds(cs, c_m, n_l, key, 4000 + s * n_k, 1, n_k)
+        down()
     e2e_ms = max_over_ranks(pg, ctx.stopwatch_stop()) / e2e_steps
-    bytes_io = n * (8 * dim + 8 + 4)
-    e2e_value = world * n * N_K / (e2e_ms * 1e-3)
+    e2e_value = world * n * n_k / (e2e_ms * 1e-3)
 
-    tb, tsrc = step_traffic()
+    tb, tsrc = step_traffic() if args.config == "cfg4" else (None, None)  # profiled on cfg4 only
     traffic = tb * n if tb else None  # DRAM bytes (read + write) of one step (one round), ncu
 
     cpu = None
@@ -340,9 +458,9 @@ def run_b200(args, cfg, world, rank, local, pg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded rsa_place at f0=0.1, grown on device by srm_generate to 0.98 f_target)",
+            "data": "synthetic (seeded host RSA start, grown on device by srm_generate to 0.98 f_target)",
             "config": {"workload": args.config + ": " + cfg["desc"], "n": n, "dim": dim,
-                       "f_window": prep["f_window"], "c_m": c_m, "n_l": N_L, "cell_size": cs,
+                       "f_window": prep["f_window"], "c_m": c_m, "n_l": n_l, "cell_size": cs,
                        "parallelism": f"replicas x{world}", "step": "one SRM round: grid rebuild + migrate (n_l attempts) + overlap reduction",
                        "l2": f"inputs larger than L2 (state {n * (8 * dim + 16) / 1e6:.0f} MB)",
                        "prep": prep},
@@ -352,14 +470,14 @@ def run_b200(args, cfg, world, rank, local, pg):
                          "kernel": "migrate step per round: near lists (k_near_tiles) + k_sweep_warpq x colour classes",
                          "traffic_unit": "bytes per step (one round of near lists + sweep), ncu dram__bytes_read+write",
                          "algorithmic_bytes_per_step": algo,
-                         "algorithmic_bytes_per_update": BYTES_STEP[dim], "step_ms_per_round": t_mig,
+                         "algorithmic_bytes_per_update": bpu, "step_ms_per_round": t_mig,
                          "traffic_bytes_per_update": tb, "traffic_source": tsrc, "peak_kind": peak_kind},
             "phase_ms_per_round": {"grid_rebuild": per_round[0], "sweep": per_round[1],
                                    "near_lists": per_round[2], "reduction": per_round[3]},
             "last_round": {"overlap_pairs": st.overlap_pairs, "movers": st.movers,
                            "max_penetration": st.max_penetration},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_io,
-                    "d2h_bytes_per_step": bytes_io, "rounds_per_step": N_K,
+                    "d2h_bytes_per_step": bytes_io, "rounds_per_step": n_k,
                     "api": "srm_b200_upload + srm_b200_rounds(n_k) + srm_b200_download"},
             "gpu_launches": launches,
             "clocks": clk,
@@ -374,13 +492,17 @@ def run_b200(args, cfg, world, rank, local, pg):
 def cpu_baseline(cfg, c_m):
     """oracle/_ref (the reference engine) on 1 host core, bounded sample ~10-20 s."""
     try:
-        L, Lb, pos, radii, ids, c_m_s = ref_sample_state(cfg, 777)
-        t1 = ref_rounds(L, Lb, pos, radii, ids, c_m_s, 2, 1, 5) / 2
+        L, S = ref_sample_state(cfg, 777)
+        ns = sample_n(cfg)
+        t1 = ref_rounds(L, S, 2, 1, 5) / 2
         rounds = int(max(3, min(200, 12.0 / max(t1, 1e-6))))
-        secs = ref_rounds(L, Lb, pos, radii, ids, c_m_s, rounds, 1, 6)
-        return {"value": SAMPLE_N * rounds / secs, "unit": UNIT, "cores": 1, "kind": "reference",
-                "sample": f"{SAMPLE_N} spheres at the workload's density/radius/c_m, {rounds} rounds "
-                          f"(build_shape_grid -> migrate -> shape_any_collision), 1 thread"}
+        secs = ref_rounds(L, S, rounds, 1, 6)
+        what = ("platelets at rho 3.5 (reference rsa_platelets state)" if S["kind"] == "platelet" else
+                ("spheres" if cfg["dim"] == 3 else "disks") + " at the workload's density/radii/c_m (reference start: "
+                "uniform RSA + srm_generate to the window)")
+        return {"value": ns * rounds / secs, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"{ns} {what}, {rounds} rounds (build_shape_grid -> migrate -> shape_any_collision), "
+                          f"1 thread"}
     except Exception as e:  # the baseline is reported, never required
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
 

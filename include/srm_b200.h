@@ -202,6 +202,14 @@ int srm_b200_rsa_place(int dim, const double* box_lengths, int64_t n, const doub
 int srm_b200_rsa_platelets(int64_t n, double diameter, double aspect_ratio, const double* box_lengths,
                            int64_t max_attempts, uint64_t seed, double* pos_out, double* normal_out,
                            int32_t* id_out, int64_t* placed_out);
+/* Clustered RSA (BASELINE.json configs[2] start; builder-defined, no reference
+ * counterpart): cluster centres uniform, particle i in cluster i mod n_clusters, candidates
+ * wrap(centre + sigma * gaussian), strictly non-touching as rsa_place.  Rng(seed) =
+ * std::mt19937_64 with the reference's uniform / Box-Muller gaussian (random.hpp:16-61).
+ * Returns OK / INVALID / PLACEMENT_FAILURE (placed_out = particles placed). */
+int srm_b200_rsa_clustered(int dim, const double* box_lengths, int64_t n, const double* radii,
+                           int64_t n_clusters, double sigma, int64_t max_attempts, uint64_t seed,
+                           double* pos_out, int32_t* id_out, int64_t* placed_out);
 /* random.hpp:84-89 mix_seed */
 uint64_t srm_b200_mix_seed(uint64_t seed, uint64_t stream);
 

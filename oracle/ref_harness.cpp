@@ -405,6 +405,43 @@ int ref_generate_platelets(const double* L, int64_t n, double* pos, double* nrm,
     }
 }
 
+// CPU baseline for platelets: `threads` replicas x `rounds` SRM rounds at fixed size
+// (build_shape_grid -> migrate -> shape_any_collision with SpherodiskShape).  Wall s.
+double ref_pl_bench_rounds(const double* L, int64_t n, const double* pos, const double* nrm, const double* D,
+                           const double* t, const int32_t* id, double c_m, double c_r, int n_l, int rounds,
+                           uint64_t seed, int threads, int64_t* accepted_total) {
+    std::vector<Spherodisk> start(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) start[i] = make_pl(pos + 3 * i, nrm + 3 * i, D[i], t[i], id[i]);
+    const auto box = make_box<3>(L);
+    std::atomic<int64_t> acc{0};
+    auto worker = [&](int th) {
+        auto P = start;
+        Rng rng(mix_seed(seed, 10000 + static_cast<std::uint64_t>(th)));
+        const double max_r = max_bounding_radius<SpherodiskShape>(P);
+        CellGrid<3> grid(box, 2.5 * max_r + c_m, max_r, c_m);
+        int64_t local = 0;
+        for (int k = 0; k < rounds; ++k) {
+            build_shape_grid<SpherodiskShape>(grid, P);
+            const auto a = migrate<SpherodiskShape>(P, grid, c_m, c_r, n_l, rng);
+            for (auto v : a) local += v;
+            volatile bool any = shape_any_collision<SpherodiskShape>(std::span<const Spherodisk>(P), grid);
+            (void)any;
+        }
+        acc += local;
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    if (threads <= 1) {
+        worker(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (int th = 0; th < threads; ++th) pool.emplace_back(worker, th);
+        for (auto& th : pool) th.join();
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (accepted_total) *accepted_total = acc.load();
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
 // shape_any_collision<SpherodiskShape> over a grid of cell size cs
 int ref_pl_any_collision(const double* L, double cs, int64_t n, const double* pos, const double* nrm, const double* D,
                          const double* t, const int32_t* id) {

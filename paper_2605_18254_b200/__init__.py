@@ -31,7 +31,7 @@ __all__ = [
     "SrmParams", "Snapshot", "GenerateStatus", "GenerateResult", "ProgressRecord",
     "Context", "srm_generate", "relax_sweeps", "shake", "swell_all", "reorder_by_locality",
     "rsa_place", "mix_seed", "K_RSA_DEFAULT_ATTEMPTS", "PlateletSnapshot", "srm_generate_platelets",
-    "rsa_platelets",
+    "rsa_platelets", "rsa_clustered",
 ]
 
 K_RSA_DEFAULT_ATTEMPTS = 10000  # rsa.hpp:15 kRsaDefaultAttempts
@@ -541,6 +541,28 @@ def rsa_place(radii, box: Sequence[float], max_attempts: int, seed: int):
             "initial volume fraction too high", placed.value, max_attempts)
     if st == INVALID:
         raise ValidationError("rsa_place: invalid radii or box")
+    _check(st)
+    return pos[:n], ids[:n]
+
+
+def rsa_clustered(radii, box: Sequence[float], n_clusters: int, sigma: float, max_attempts: int, seed: int):
+    """Clustered RSA (BASELINE.json configs[2] start; builder-defined): particle i is drawn
+    around cluster centre i mod n_clusters with a Gaussian of width sigma and accepted
+    when strictly non-touching (the rsa_place predicate).  Returns (pos, id)."""
+    radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+    dim = len(box)
+    L = (C.c_double * dim)(*[float(v) for v in box])
+    n = len(radii)
+    pos = np.empty((max(n, 1), dim), np.float64)
+    ids = np.empty(max(n, 1), np.int32)
+    placed = C.c_int64()
+    st = _native.lib().srm_b200_rsa_clustered(dim, L, n, _ptr(radii), int(n_clusters), float(sigma), int(max_attempts),
+                                              seed & 0xFFFFFFFFFFFFFFFF, _ptr(pos), _ptr(ids), C.byref(placed))
+    if st == PLACEMENT_FAILURE:
+        raise PlacementFailure(f"rsa_clustered: exceeded {max_attempts} attempts after placing {placed.value} particles",
+                               placed.value, max_attempts)
+    if st == INVALID:
+        raise ValidationError("rsa_clustered: invalid radii, clusters or box")
     _check(st)
     return pos[:n], ids[:n]
 

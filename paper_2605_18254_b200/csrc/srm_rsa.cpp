@@ -143,6 +143,119 @@ int srm_b200_rsa_place(int dim, const double* L, int64_t count, const double* ra
 }
 
 
+// Clustered random sequential adsorption (BASELINE.json configs[2]: the clustered,
+// non-equilibrium start of the polydisperse config; the reference has no generator
+// for it, so this is builder-defined).  Cluster centres: the first n_clusters * dim
+// uniforms of Rng(seed) (random_point, random.hpp:56-61); particle i belongs to cluster
+// i mod n_clusters and its candidates are wrap(centre + sigma * gaussian per axis)
+// (Rng::gaussian, Box-Muller with a cached spare, random.hpp:30-52), accepted when
+// strictly non-touching every placed particle (the rsa_place predicate).
+int srm_b200_rsa_clustered(int dim, const double* L, int64_t count, const double* radii, int64_t n_clusters,
+                           double sigma, int64_t max_attempts, uint64_t seed, double* pos_out, int32_t* id_out,
+                           int64_t* placed_out) {
+    if (placed_out) *placed_out = 0;
+    if (dim != 2 && dim != 3) return SRM_B200_INVALID;
+    if (count < 1 || n_clusters < 1 || !(sigma >= 0.0)) return SRM_B200_INVALID;
+    double max_r = radii[0];
+    for (int64_t i = 1; i < count; ++i) max_r = std::max(max_r, radii[i]);
+    double min_len = L[0];
+    for (int a = 1; a < dim; ++a) min_len = std::min(min_len, L[a]);
+    for (int64_t i = 0; i < count; ++i)
+        if (!(radii[i] > 0.0)) return SRM_B200_INVALID;
+    if (!(max_r < min_len / 4.0)) return SRM_B200_INVALID;
+
+    RsaGrid g;
+    g.dim = dim;
+    int64_t ncells = 1;
+    for (int a = 0; a < dim; ++a) {
+        int k = static_cast<int>(std::floor(L[a] / (2.0 * max_r)));
+        k = std::max(1, std::min(k, 1 << 12));
+        g.n[a] = k;
+        g.edge[a] = L[a] / k;
+        ncells *= k;
+    }
+    g.head.assign(static_cast<size_t>(ncells), -1);
+    g.next.assign(static_cast<size_t>(count), -1);
+
+    std::mt19937_64 gen(seed);
+    auto uniform = [&]() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+    bool have_spare = false;
+    double spare = 0.0;
+    auto gaussian = [&]() {
+        if (have_spare) {
+            have_spare = false;
+            return spare;
+        }
+        double u1 = uniform();
+        while (u1 == 0.0) u1 = uniform();
+        const double u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double a = 2.0 * 3.141592653589793238462643383279502884 * u2;
+        spare = r * std::sin(a);
+        have_spare = true;
+        return r * std::cos(a);
+    };
+    std::vector<double> centre(static_cast<size_t>(n_clusters) * dim);
+    for (int64_t k = 0; k < n_clusters; ++k)
+        for (int a = 0; a < dim; ++a) centre[k * dim + a] = uniform() * L[a];
+
+    double cand[3];
+    for (int64_t i = 0; i < count; ++i) {
+        const double ri = radii[i];
+        const double* c0 = &centre[(i % n_clusters) * dim];
+        bool accepted = false;
+        for (int64_t attempt = 0; attempt < max_attempts; ++attempt) {
+            for (int a = 0; a < dim; ++a) {
+                double p = c0[a] + sigma * gaussian();
+                p = std::fmod(p, L[a]);  // far tails: back into [0, L)
+                if (p < 0.0) p += L[a];
+                if (p >= L[a]) p -= L[a];
+                cand[a] = p;
+            }
+            int c[3] = {0, 0, 0};
+            for (int a = 0; a < dim; ++a) c[a] = g.coord(a, cand[a]);
+            bool hit = false;
+            for (int dz = (dim == 3 ? -1 : 0); dz <= (dim == 3 ? 1 : 0) && !hit; ++dz) {
+                if (dim == 3 && g.n[2] < 3 && dz != 0 && (dz == 1 || g.n[2] == 1)) continue;
+                const int z = dim == 3 ? ((c[2] + dz) % g.n[2] + g.n[2]) % g.n[2] : 0;
+                for (int dy = -1; dy <= 1 && !hit; ++dy) {
+                    if (g.n[1] < 3 && dy != 0 && (dy == 1 || g.n[1] == 1)) continue;
+                    const int y = ((c[1] + dy) % g.n[1] + g.n[1]) % g.n[1];
+                    for (int dx = -1; dx <= 1 && !hit; ++dx) {
+                        if (g.n[0] < 3 && dx != 0 && (dx == 1 || g.n[0] == 1)) continue;
+                        const int x = ((c[0] + dx) % g.n[0] + g.n[0]) % g.n[0];
+                        const int64_t cell = (static_cast<int64_t>(z) * g.n[1] + y) * g.n[0] + x;
+                        for (int32_t j = g.head[cell]; j >= 0; j = g.next[j]) {
+                            const double rr = ri + radii[j];
+                            if (min_image_dist2(dim, L, cand, pos_out + static_cast<int64_t>(j) * dim) <= rr * rr) {
+                                hit = true;
+                                break;
+                            }
+                        }
+                    }
+                }
+            }
+            if (!hit) {
+                accepted = true;
+                break;
+            }
+        }
+        if (!accepted) {
+            if (placed_out) *placed_out = i;
+            return SRM_B200_PLACEMENT_FAILURE;
+        }
+        for (int a = 0; a < dim; ++a) pos_out[i * dim + a] = cand[a];
+        if (id_out) id_out[i] = static_cast<int32_t>(i);
+        int c[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a) c[a] = g.coord(a, cand[a]);
+        const int64_t cell = (static_cast<int64_t>(c[2]) * g.n[1] + c[1]) * g.n[0] + c[0];
+        g.next[i] = g.head[cell];
+        g.head[cell] = static_cast<int32_t>(i);
+    }
+    if (placed_out) *placed_out = count;
+    return SRM_B200_OK;
+}
+
 int srm_b200_rsa_platelets(int64_t count, double diameter, double aspect_ratio, const double* L, int64_t max_attempts,
                            uint64_t seed, double* pos_out, double* normal_out, int32_t* id_out, int64_t* placed_out) {
     using namespace srmb::pl;

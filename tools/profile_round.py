@@ -37,7 +37,7 @@ def main():
     ctx.sync()
     rt.cudaProfilerStart()  # ncu --profile-from-start off captures only the timed rounds
     ctx.stopwatch_start()
-    st = ctx.rounds(cs, c_m, bench.N_L, 77, 0, 1, args.rounds)
+    st = ctx.rounds(cs, c_m, cfg.get("n_l", bench.N_L), 77, 0, 1, args.rounds)
     ms = ctx.stopwatch_stop()
     rt.cudaProfilerStop()
     print(f"{args.rounds} rounds: {ms:.3f} ms ({ms / args.rounds:.3f} ms/round), overlaps {st.overlap_pairs}, "
