@@ -46,14 +46,14 @@ CONFIGS = {
     "cfg3": dict(desc="3D polydisperse spheres N=1e6, lognormal radii (mean 1, CV 0.2, clipped to [0.5, 2]), "
                       "clustered start (1000 Gaussian clusters, sigma 3), f_target 0.50, c_m=0.1",
                  kind="poly", dim=3, n=1_000_000, f_target=0.50, cm_abs=0.10, f0=0.05, clusters=1000, sigma=3.0,
-                 sample_n=20_000, prep_iters=400),
+                 sample_n=20_000, prep_iters=150),
     "cfg4": dict(desc="3D monodisperse spheres N=1e7, unit cube, f_target 0.30, c_m=0.05 r_t",
                  kind="mono", dim=3, n=10_000_000, f_target=0.30, cm_rel=0.05, f0=0.1),
     "cfg5": dict(desc="3D thin platelets N=1e5, thickness/diameter 0.01, box 25.01, normals uniform, f_target 0.05, "
                       "rsa_platelets start at rho 3.5, grown with the reference recipe's grow stage (c_w=0.008, "
                       "c_m=0.01, c_r=0.012, n_k=n_l=20; recipes.cpp:205-213)",
                  kind="platelet", dim=3, n=100_000, f_target=0.05, L=25.01, aspect=100.0, cm_abs=0.01, c_r=0.012,
-                 c_w=0.008, rho0=3.5, rho_cpu=3.5, n_l=20, n_k=20, sample_n=4_000, prep_iters=400),
+                 c_w=0.008, rho0=3.5, rho_cpu=3.5, n_l=20, n_k=20, sample_n=4_000, prep_iters=40),
 }
 F_WINDOW = 0.98   # steady-state window at 0.98 f_target
 N_K = 10          # rounds per iteration / shake sweeps (srmgen.cpp:407-410)

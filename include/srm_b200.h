@@ -189,6 +189,18 @@ int srm_b200_rounds(srm_b200_ctx* ctx, double cell_size, double c_m, int n_l, ui
                     uint32_t first_round, uint32_t iteration, int rounds,
                     srm_b200_round_stats* last);
 
+/* ---- parity statistics on the device ---------------------------- */
+/* descriptors.hpp:96-115 nearest_neighbor_distances of the context's state (exact: the
+ * minimum over all other centres, as the reference's ring search) and, when counts_out is
+ * given, descriptors.hpp:254-277 histogram(nnd, bins, lo, hi) (counts[bins], total,
+ * in_range).  nnd_out (nullable): n distances in download order.  Spheres/disks. */
+int srm_b200_nnd_histogram(srm_b200_ctx* ctx, int bins, double lo, double hi, int64_t* counts_out,
+                           int64_t* total_out, int64_t* in_range_out, double* nnd_out);
+/* Unordered centre-pair distances (min image) binned on edges[0..bins] with
+ * numpy.histogram's rule (last bin closed): the RDF counts of the parity tests
+ * (tests/stats_util.py rdf_counts; the reference has no RDF). */
+int srm_b200_pair_counts(srm_b200_ctx* ctx, const double* edges, int bins, int64_t* counts_out);
+
 /* ---- initial states (rsa.hpp:21-69) ------------------------------------------------ */
 /* rsa_place with Rng(seed) (std::mt19937_64): bit-identical to the reference for the
  * same seed.  Host code (input generation; excluded from the metric).

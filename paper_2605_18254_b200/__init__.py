@@ -376,6 +376,29 @@ class Context:
         return {"nonmovers": v[0], "colour_classes": v[1], "cells_per_class": v[2], "near_half_width": v[3],
                 "colour_modulus": v[4], "cells": v[5]}
 
+    def nearest_neighbor_distances(self) -> np.ndarray:
+        """descriptors.hpp:96-115 on the device (download order)."""
+        out = np.empty(max(self.n, 1))
+        self._c(_native.lib().srm_b200_nnd_histogram(self._h, 0, 0.0, 0.0, None, None, None, _ptr(out)))
+        return out[:self.n]
+
+    def nnd_histogram(self, bins: int, lo: float, hi: float):
+        """descriptors.hpp:254-277 histogram of the device NND: (counts, total, in_range)."""
+        counts = np.zeros(bins, np.int64)
+        tot, inr = C.c_int64(), C.c_int64()
+        self._c(_native.lib().srm_b200_nnd_histogram(self._h, int(bins), float(lo), float(hi), _ptr(counts),
+                                                     C.byref(tot), C.byref(inr), None))
+        return counts, tot.value, inr.value
+
+    def pair_counts(self, edges) -> np.ndarray:
+        """Unordered centre-pair distances binned on `edges` (numpy.histogram's rule)."""
+        edges = np.ascontiguousarray(edges, dtype=np.float64)
+        bins = len(edges) - 1
+        counts = np.zeros(bins, np.int64)
+        L = (C.c_double * len(edges))(*edges)
+        self._c(_native.lib().srm_b200_pair_counts(self._h, L, bins, _ptr(counts)))
+        return counts
+
     def set_generate_mode(self, device_loop: bool) -> None:
         """generate(): one device-resident CUDA graph (True, default) or the host-driven loop"""
         self._c(_native.lib().srm_b200_set_generate_mode(self._h, 1 if device_loop else 0))

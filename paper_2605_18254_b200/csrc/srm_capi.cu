@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/srm_b200.h"
+#include "srm_descriptors.cuh"
 #include "srm_kernels.cuh"
 
 using namespace srmb;
@@ -56,6 +57,13 @@ T* dalloc(int64_t count) {
     return static_cast<T*>(p);
 }
 
+template <typename T>
+struct DevBuf {  // device scratch of one call
+    T* p = nullptr;
+    explicit DevBuf(int64_t count) { p = dalloc<T>(count > 0 ? count : 1); }
+    ~DevBuf() { cudaFree(p); }
+};
+
 }  // namespace
 
 struct srm_b200_ctx {
@@ -74,7 +82,7 @@ struct srm_b200_ctx {
     uint32_t* skey = nullptr;
     int32_t* perm = nullptr;
     int32_t* active = nullptr;  // non-mover list of the current round
-    int32_t* nbr = nullptr;     // near lists (kNearLocal per particle) and their lengths
+    int32_t* nbr = nullptr;     // near-list rows (kNearRow int32 per particle)
     int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_warpq (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
     // 0: shared-memory bricks (3D) / half-stencil pairs, 1: full stencil per particle,
@@ -969,6 +977,90 @@ int srm_b200_overlap_stats(srm_b200_ctx* c, double cell_size, srm_b200_round_sta
             o.movers = 0;
         }
         if (out) *out = o;
+        return SRM_B200_OK;
+    });
+}
+
+// ---- parity statistics on the device (srm_descriptors.cuh) ------------------------------
+int srm_b200_nnd_histogram(srm_b200_ctx* c, int bins, double lo, double hi, int64_t* counts_out, int64_t* total_out,
+                           int64_t* in_range_out, double* nnd_out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (n < 2) throw Invalid{"nearest_neighbor_distances: need at least 2 particles"};
+        if (counts_out && bins < 1) throw Invalid{"histogram: bin_count must be >= 1"};
+        if (counts_out && !(hi > lo)) throw Invalid{"histogram: need hi > lo"};
+        if (c->platelets()) throw Invalid{"nnd: spheres and disks only"};
+        const double mr = c->max_radius(c->P);
+        // any grid gives the exact answer; about one particle per cell, as descriptor_grid
+        double vol = 1.0;
+        for (int a = 0; a < c->dim; ++a) vol *= c->box.L[a];
+        double cell = std::pow(vol / static_cast<double>(n), 1.0 / c->dim);
+        cell = std::max(cell, 1e-3 * mr);
+        c->set_grid(c->make_grid(cell, mr, 0.0));
+        c->grid_build(c->P);
+        DevBuf<double> d(n);
+        const int nb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 16));
+        if (c->dim == 2) k_nnd<2><<<nb, 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, d.p);
+        else k_nnd<3><<<nb, 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, d.p);
+        c->launched();
+        if (counts_out) {
+            DevBuf<unsigned long long> h(bins + 2);
+            SRM_CUDA(cudaMemsetAsync(h.p, 0, sizeof(unsigned long long) * (bins + 2), c->stream));
+            k_histogram<<<nb, 256, 0, c->stream>>>(n, d.p, bins, lo, hi, h.p, h.p + bins);
+            c->launched();
+            std::vector<unsigned long long> hh(static_cast<size_t>(bins) + 2);
+            SRM_CUDA(cudaMemcpyAsync(hh.data(), h.p, sizeof(unsigned long long) * hh.size(), cudaMemcpyDeviceToHost,
+                                     c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+            for (int b = 0; b < bins; ++b) counts_out[b] = static_cast<int64_t>(hh[b]);
+            if (total_out) *total_out = static_cast<int64_t>(hh[bins]);
+            if (in_range_out) *in_range_out = static_cast<int64_t>(hh[bins + 1]);
+        }
+        if (nnd_out)
+            SRM_CUDA(cudaMemcpyAsync(nnd_out, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        SRM_CUDA(cudaStreamSynchronize(c->stream));
+        return SRM_B200_OK;
+    });
+}
+
+int srm_b200_pair_counts(srm_b200_ctx* c, const double* edges, int bins, int64_t* counts_out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (bins < 1 || !(edges[bins] > edges[0]) || !(edges[0] >= 0.0)) throw Invalid{"pair_counts: bad edges"};
+        if (c->platelets()) throw Invalid{"pair_counts: spheres and disks only"};
+        std::vector<unsigned long long> hh(static_cast<size_t>(bins), 0ull);
+        if (n >= 2) {
+            const double hi = edges[bins];
+            const double mr = c->max_radius(c->P);
+            c->set_grid(c->make_grid(hi, mr, 0.0));
+            c->grid_build(c->P);
+            const GridParams& g = c->hg;
+            int32_t sw[3] = {-1, -1, -1};
+            for (int a = 0; a < c->dim; ++a) {  // the cells within hi, or the whole axis
+                int s = 1;
+                while (static_cast<double>(s) * g.edge[a] < hi && 2 * s + 1 < g.dims[a]) ++s;
+                sw[a] = 2 * s + 1 >= g.dims[a] ? -1 : s;
+            }
+            DevBuf<int32_t> dsw(3);
+            DevBuf<double> de(bins + 1);
+            DevBuf<unsigned long long> h(bins);
+            SRM_CUDA(cudaMemcpyAsync(dsw.p, sw, sizeof(sw), cudaMemcpyHostToDevice, c->stream));
+            SRM_CUDA(cudaMemcpyAsync(de.p, edges, sizeof(double) * (bins + 1), cudaMemcpyHostToDevice, c->stream));
+            SRM_CUDA(cudaMemsetAsync(h.p, 0, sizeof(unsigned long long) * bins, c->stream));
+            const int nb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
+            const size_t sh = sizeof(unsigned long long) * bins;
+            if (sh > 48 * 1024) throw Invalid{"pair_counts: at most 6144 bins"};
+            if (c->dim == 2)
+                k_pair_counts<2><<<nb, 256, sh, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, de.p, bins,
+                                                             dsw.p, h.p);
+            else
+                k_pair_counts<3><<<nb, 256, sh, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, de.p, bins,
+                                                             dsw.p, h.p);
+            c->launched();
+            SRM_CUDA(cudaMemcpyAsync(hh.data(), h.p, sizeof(unsigned long long) * bins, cudaMemcpyDeviceToHost, c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        for (int b = 0; b < bins; ++b) counts_out[b] = static_cast<int64_t>(hh[b]);
         return SRM_B200_OK;
     });
 }
