@@ -37,9 +37,12 @@ oracle:
 
 shimtest: tests/cpp/shim_test
 
-tests/cpp/shim_test: tests/cpp/shim_test.cpp include/srm/b200/engine.hpp include/srm_b200.h $(LIB)
+# (the reference side of the comparisons -- spherodisk.cpp, recipes.cpp -- from the
+#  checker library oracle/_ref/libsrm_ref.so, built from the reference's own sources)
+tests/cpp/shim_test: tests/cpp/shim_test.cpp include/srm/b200/engine.hpp include/srm_b200.h $(LIB) oracle
 	g++ -std=gnu++20 -O2 -I$(REF)/core/include -Iinclude -o $@ tests/cpp/shim_test.cpp \
-	    -L$(PKG) -lsrm_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
+	    -L$(PKG) -lsrm_b200 -Loracle/_ref -lsrm_ref \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle/_ref'
 
 clean:
 	rm -f $(CSRC)/*.o $(LIB) $(CSRC)/ptxas.log tests/cpp/shim_test

@@ -12,6 +12,8 @@
 //   reorder_by_locality engine.hpp:144-166
 //   shape_any_collision shape.hpp:549-555
 //   rsa_place           rsa.hpp:21-61       (seeded form; bit-identical to Rng(seed))
+//   rsa_platelets       recipes.cpp:107-148 (seeded form; bit-identical to Rng(seed))
+//   nearest_neighbor_distances  descriptors.hpp:96-115 (exact, on the device)
 //
 // Differences the caller can observe:
 //   * migrate is the coloured Gauss-Seidel sweep: the reference's
@@ -20,7 +22,7 @@
 //     storage-order mt19937_64 sweep (statistically equal, tests/test_gpu_e2e.py);
 //   * errors: ValidationError / PlacementFailure / std::invalid_argument as in the
 //     reference; device failures throw srm::b200::DeviceError.
-// Disks and spheres (SphereShape<2>, SphereShape<3>) are supported.
+// Disks, spheres and thin platelets (SphereShape<2>, SphereShape<3>, SpherodiskShape).
 #pragma once
 
 #include <cstddef>
@@ -36,7 +38,10 @@
 #include "srm/errors.hpp"
 #include "srm/geometry.hpp"
 #include "srm/random.hpp"
+#include "srm/descriptors.hpp"
+#include "srm/recipes.hpp"
 #include "srm/rsa.hpp"
+#include "srm/spherodisk.hpp"
 #include "srm/shape.hpp"
 #include "srm_b200.h"
 
@@ -48,6 +53,8 @@ struct DeviceError : srm::Error {
 
 template <typename S>
 inline constexpr bool is_sphere_shape_v = std::is_same_v<S, SphereShape<S::dim>>;
+template <typename S>
+inline constexpr bool is_supported_shape_v = is_sphere_shape_v<S> || std::is_same_v<S, SpherodiskShape>;
 
 namespace detail {
 
@@ -61,15 +68,18 @@ inline void check(int st, const srm_b200_ctx* c, bool invalid_argument = false) 
     throw DeviceError("srm_b200 status " + std::to_string(st) + ": " + msg);
 }
 
-// RAII over one device context holding a copy of the particles
-template <int N>
+// RAII over one device context holding a copy of the particles of shape S
+template <typename S>
 class Device {
+    static constexpr int N = S::dim;
+    static constexpr bool kPlatelet = std::is_same_v<S, SpherodiskShape>;
+
   public:
     Device(const PeriodicBox<N>& box, std::size_t capacity, int device = 0) {
         double L[3] = {1.0, 1.0, 1.0};
         for (int a = 0; a < N; ++a) L[a] = box.length(a);
-        check(srm_b200_create(N, SRM_B200_SPHERE, L, static_cast<int64_t>(capacity < 1 ? 1 : capacity), device,
-                              &ctx_),
+        check(srm_b200_create(N, kPlatelet ? SRM_B200_PLATELET : SRM_B200_SPHERE, L,
+                              static_cast<int64_t>(capacity < 1 ? 1 : capacity), device, &ctx_),
               nullptr);
     }
     ~Device() { srm_b200_destroy(ctx_); }
@@ -78,17 +88,50 @@ class Device {
 
     srm_b200_ctx* get() const { return ctx_; }
 
-    // Particle<N> is {int id; Vec<N> pos; double radius} (geometry.hpp:139-144)
-    void upload(std::span<const Particle<N>> ps) {
-        check(srm_b200_upload_records(ctx_, static_cast<int64_t>(ps.size()), ps.data(), sizeof(Particle<N>),
-                                      offsetof(Particle<N>, id), offsetof(Particle<N>, pos),
-                                      offsetof(Particle<N>, radius)),
-              ctx_);
+    void upload(std::span<const typename S::ParticleT> ps) {
+        if constexpr (kPlatelet) {  // Spherodisk (spherodisk.hpp:16-22) as SoA
+            const std::size_t n = ps.size();
+            std::vector<double> pos(3 * n), nrm(3 * n), D(n), t(n);
+            std::vector<int32_t> id(n);
+            for (std::size_t i = 0; i < n; ++i) {
+                for (int a = 0; a < 3; ++a) {
+                    pos[3 * i + a] = ps[i].pos[a];
+                    nrm[3 * i + a] = ps[i].normal[a];
+                }
+                D[i] = ps[i].diameter;
+                t[i] = ps[i].thickness;
+                id[i] = ps[i].id;
+            }
+            check(srm_b200_upload_platelets(ctx_, static_cast<int64_t>(n), pos.data(), nrm.data(), D.data(), t.data(),
+                                            id.data()),
+                  ctx_);
+        } else {  // Particle<N> is {int id; Vec<N> pos; double radius} (geometry.hpp:139-144)
+            check(srm_b200_upload_records(ctx_, static_cast<int64_t>(ps.size()), ps.data(), sizeof(Particle<N>),
+                                          offsetof(Particle<N>, id), offsetof(Particle<N>, pos),
+                                          offsetof(Particle<N>, radius)),
+                  ctx_);
+        }
     }
-    void download(std::vector<Particle<N>>& ps) {
-        check(srm_b200_download_records(ctx_, ps.data(), sizeof(Particle<N>), offsetof(Particle<N>, id),
-                                        offsetof(Particle<N>, pos), offsetof(Particle<N>, radius)),
-              ctx_);
+    void download(std::vector<typename S::ParticleT>& ps) {
+        if constexpr (kPlatelet) {
+            const std::size_t n = ps.size();
+            std::vector<double> pos(3 * n), nrm(3 * n), D(n), t(n);
+            std::vector<int32_t> id(n);
+            check(srm_b200_download_platelets(ctx_, pos.data(), nrm.data(), D.data(), t.data(), id.data()), ctx_);
+            for (std::size_t i = 0; i < n; ++i) {
+                for (int a = 0; a < 3; ++a) {
+                    ps[i].pos[a] = pos[3 * i + a];
+                    ps[i].normal[a] = nrm[3 * i + a];
+                }
+                ps[i].diameter = D[i];
+                ps[i].thickness = t[i];
+                ps[i].id = id[i];
+            }
+        } else {
+            check(srm_b200_download_records(ctx_, ps.data(), sizeof(Particle<N>), offsetof(Particle<N>, id),
+                                            offsetof(Particle<N>, pos), offsetof(Particle<N>, radius)),
+                  ctx_);
+        }
     }
 
   private:
@@ -120,14 +163,14 @@ inline void progress_trampoline(const srm_b200_progress_record* rec, void* user)
 template <ShapeModel S>
 GenerateResult<S> srm_generate(const Snapshot<S>& initial, const SrmParams& params,
                                const ProgressSink& progress = {}) {
-    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");
     constexpr int N = S::dim;
     GenerateResult<S> result;
     result.snapshot = initial;
     Snapshot<S>& snap = result.snapshot;
     snap.params = params;
     snap.seed = params.seed;
-    detail::Device<N> dev(initial.box, initial.particles.size());
+    detail::Device<S> dev(initial.box, initial.particles.size());
     dev.upload(initial.particles);
     const srm_b200_params cp = detail::to_c(params);
     srm_b200_generate_out out{};
@@ -147,15 +190,16 @@ GenerateResult<S> srm_generate(const Snapshot<S>& initial, const SrmParams& para
 // Gauss-Seidel round of DESIGN.md §3.1 keyed by one draw of rng.  Returns the accepted flags.
 template <ShapeModel S>
 std::vector<std::uint8_t> migrate(std::vector<typename S::ParticleT>& particles, const CellGrid<S::dim>& grid,
-                                  double c_m, double /*c_r*/, int n_l, Rng& rng) {
-    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+                                  double c_m, double c_r, int n_l, Rng& rng) {
+    static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");
     constexpr int N = S::dim;
     std::vector<std::uint8_t> acc(particles.size(), 0);
     if (particles.empty()) return acc;
     const std::uint64_t key = rng.raw();
-    detail::Device<N> dev(grid.box(), particles.size());
+    detail::Device<S> dev(grid.box(), particles.size());
     dev.upload(particles);
     srm_b200_round_stats st{};
+    detail::check(srm_b200_set_rotation(dev.get(), c_r), dev.get(), true);
     detail::check(srm_b200_round(dev.get(), grid.cell_size(), c_m, n_l, key, 0, 0, 0, acc.data(), &st), dev.get(),
                   true);
     dev.download(particles);
@@ -167,10 +211,10 @@ std::vector<std::uint8_t> migrate(std::vector<typename S::ParticleT>& particles,
 template <ShapeModel S>
 void relax_sweeps(std::vector<typename S::ParticleT>& particles, const PeriodicBox<S::dim>& box, double c_m,
                   double c_r, int n_l, int sweeps, Rng& rng) {
-    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");
     if (particles.empty() || sweeps < 1) return;
     const std::uint64_t key = rng.raw();
-    detail::Device<S::dim> dev(box, particles.size());
+    detail::Device<S> dev(box, particles.size());
     dev.upload(particles);
     detail::check(srm_b200_relax_sweeps(dev.get(), c_m, c_r, n_l, sweeps, key), dev.get(), true);
     dev.download(particles);
@@ -186,9 +230,9 @@ void shake(std::vector<typename S::ParticleT>& particles, const PeriodicBox<S::d
 // engine.hpp:134-138 (on the device; radius *= 1 + c_w)
 template <ShapeModel S>
 void swell_all(std::vector<typename S::ParticleT>& particles, double c_w) {
-    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");
     if (particles.empty()) return;
-    detail::Device<S::dim> dev(PeriodicBox<S::dim>::unit(), particles.size());
+    detail::Device<S> dev(PeriodicBox<S::dim>::unit(), particles.size());
     dev.upload(particles);
     detail::check(srm_b200_swell_all(dev.get(), c_w), dev.get());
     dev.download(particles);
@@ -197,10 +241,10 @@ void swell_all(std::vector<typename S::ParticleT>& particles, double c_w) {
 // engine.hpp:144-166
 template <ShapeModel S>
 std::vector<int> reorder_by_locality(std::vector<typename S::ParticleT>& particles, const CellGrid<S::dim>& grid) {
-    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");
     std::vector<int> remap(particles.size());
     if (particles.empty()) return remap;
-    detail::Device<S::dim> dev(grid.box(), particles.size());
+    detail::Device<S> dev(grid.box(), particles.size());
     dev.upload(particles);
     detail::check(srm_b200_reorder_by_locality(dev.get(), grid.cell_size(), remap.data()), dev.get(), true);
     dev.download(particles);
@@ -210,9 +254,9 @@ std::vector<int> reorder_by_locality(std::vector<typename S::ParticleT>& particl
 // shape.hpp:549-555 (the device counts overlapping pairs; any collision <=> count > 0)
 template <ShapeModel S>
 bool shape_any_collision(std::span<const typename S::ParticleT> particles, const CellGrid<S::dim>& grid) {
-    static_assert(is_sphere_shape_v<S>, "srm::b200 supports disks and spheres");
+    static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");
     if (particles.empty()) return false;
-    detail::Device<S::dim> dev(grid.box(), particles.size());
+    detail::Device<S> dev(grid.box(), particles.size());
     dev.upload(particles);
     srm_b200_round_stats st{};
     detail::check(srm_b200_overlap_stats(dev.get(), grid.cell_size(), &st), dev.get(), true);
@@ -243,6 +287,49 @@ std::vector<Particle<N>> rsa_place(std::span<const double> radii, const Periodic
         for (int a = 0; a < N; ++a) out[i].pos[a] = pos[i * N + a];
         out[i].radius = radii[i];
     }
+    return out;
+}
+
+// recipes.cpp:107-148 with Rng(seed): bit-identical to srm::rsa_platelets for a fresh Rng(seed)
+inline PlateletSnapshot rsa_platelets(std::int64_t n, double diameter, double aspect_ratio, const PeriodicBox3& box,
+                                      std::size_t max_attempts_per_particle, std::uint64_t seed) {
+    double L[3] = {box.length(0), box.length(1), box.length(2)};
+    const std::size_t m = n > 0 ? static_cast<std::size_t>(n) : 0;
+    std::vector<double> pos(3 * m), nrm(3 * m);
+    std::vector<int32_t> ids(m);
+    int64_t placed = 0;
+    const int st = srm_b200_rsa_platelets(n, diameter, aspect_ratio, L, static_cast<int64_t>(max_attempts_per_particle),
+                                          seed, pos.data(), nrm.data(), ids.data(), &placed);
+    if (st == SRM_B200_PLACEMENT_FAILURE)
+        throw PlacementFailure("rsa_platelets: exceeded attempt budget", static_cast<std::size_t>(placed),
+                               max_attempts_per_particle);
+    if (st == SRM_B200_INVALID) throw ValidationError("rsa_platelets: invalid size, aspect ratio or box");
+    PlateletSnapshot snap;
+    snap.box = box;
+    snap.particles.resize(m);
+    for (std::size_t i = 0; i < m; ++i) {
+        auto& q = snap.particles[i];
+        q.id = ids[i];
+        for (int a = 0; a < 3; ++a) {
+            q.pos[a] = pos[3 * i + a];
+            q.normal[a] = nrm[3 * i + a];
+        }
+        q.diameter = diameter;
+        q.thickness = diameter / aspect_ratio;
+    }
+    snap.refresh_volume_fraction();
+    return snap;
+}
+
+// descriptors.hpp:96-115 on the device: exact (the minimum over all other centres)
+template <ShapeModel S>
+std::vector<double> nearest_neighbor_distances(const Snapshot<S>& snap) {
+    static_assert(is_sphere_shape_v<S>, "nearest_neighbor_distances: disks and spheres");
+    if (snap.particles.size() < 2) throw ValidationError("nearest_neighbor_distances: need at least 2 particles");
+    detail::Device<S> dev(snap.box, snap.particles.size());
+    dev.upload(snap.particles);
+    std::vector<double> out(snap.particles.size());
+    detail::check(srm_b200_nnd_histogram(dev.get(), 0, 0.0, 0.0, nullptr, nullptr, nullptr, out.data()), dev.get());
     return out;
 }
 

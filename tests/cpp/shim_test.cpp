@@ -10,7 +10,9 @@
 #include <vector>
 
 #include "srm/b200/engine.hpp"
+#include "srm/descriptors.hpp"
 #include "srm/engine.hpp"
+#include "srm/recipes.hpp"
 #include "srm/rsa.hpp"
 
 using namespace srm;
@@ -156,6 +158,44 @@ int main() {
         bool same = true;
         for (std::size_t i = 0; i < before.size(); ++i) same = same && before[i].pos == snap.particles[i].pos;
         CHECK(same);
+    }
+    // nearest_neighbor_distances on the device: bit-identical to the reference's
+    {
+        auto snap = disk_start(500, 0.35, 31);
+        const auto mine = srm::b200::nearest_neighbor_distances(snap);
+        const auto ref = srm::nearest_neighbor_distances(snap);
+        CHECK(mine.size() == ref.size());
+        bool same = mine.size() == ref.size();
+        for (std::size_t i = 0; same && i < ref.size(); ++i) same = mine[i] == ref[i];
+        CHECK(same);
+    }
+    // platelets (SpherodiskShape): rsa_platelets bit-identical to the reference's for
+    // Rng(seed); srm_generate to a target fraction, no overlap by the reference's own test
+    {
+        const PeriodicBox3 box = PeriodicBox3::cube(6.0);
+        Rng rng(5);
+        const auto ref = srm::rsa_platelets(120, 1.0, 20.0, box, 10000, rng);
+        const auto mine = srm::b200::rsa_platelets(120, 1.0, 20.0, box, 10000, 5);
+        bool same = ref.particles.size() == mine.particles.size();
+        for (std::size_t i = 0; same && i < ref.particles.size(); ++i)
+            same = ref.particles[i].pos == mine.particles[i].pos && ref.particles[i].normal == mine.particles[i].normal;
+        CHECK(same);
+        SrmParams p;
+        p.c_w = 0.01;
+        p.c_m = 0.05;
+        p.c_r = 0.05;
+        p.n_k = 10;
+        p.n_l = 10;
+        p.f_target = 1.2 * mine.volume_fraction;
+        p.seed = 9;
+        const auto res = srm::b200::srm_generate(mine, p);
+        CHECK(res.status == GenerateStatus::Converged);
+        CHECK(res.snapshot.volume_fraction >= p.f_target * (1.0 - 1e-12));
+        const double max_r = max_bounding_radius<SpherodiskShape>(res.snapshot.particles);
+        CellGrid<3> grid(box, 2.5 * max_r);
+        build_shape_grid<SpherodiskShape>(grid, res.snapshot.particles);
+        CHECK(!srm::shape_any_collision<SpherodiskShape>(std::span<const Spherodisk>(res.snapshot.particles), grid));
+        CHECK(!srm::b200::shape_any_collision<SpherodiskShape>(res.snapshot.particles, grid));
     }
     std::printf("shim_test: %d/%d checks passed\n", checks - failures, checks);
     return failures == 0 ? 0 : 1;

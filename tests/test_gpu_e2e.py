@@ -6,18 +6,26 @@ parameters; the trajectories differ (parallel round vs sequential mt19937_64 swe
 DESIGN.md §3), so the end states are compared statistically:
   * f_target reached within 1e-9 relative, zero overlaps (oracle audit);
   * nearest-neighbour-distance histogram (reference nearest_neighbor_distances), 40 bins
-    over [2 r_t, 2.8 r_t] pooled over seeds: per-bin |dN| <= max(4 sigma, 2%), a chi-square
-    homogeneity test and a two-sample KS test at alpha = 0.01 on the pooled samples;
-  * RDF counts on [2 r_t, 5 r_t] (60 bins): per-bin |dN| <= max(4 sigma_Poisson, 2%), chi-square p > 0.01.
+    over [2 r_t, 2.8 r_t]: pooled per-bin |dN| <= max(4 sigma, 2%) and an ensemble
+    chi-square over the per-seed histograms (p > 1e-3); per-seed NND quantiles and
+    near-contact fraction by Welch t-tests across the seeds (p > 1e-3 each).  The
+    configuration, not the particle, is the independent sample: pooled KS / Poisson
+    chi-square tests fail the reference against itself (stats_util.ensemble_chi2);
+  * RDF counts on [2 r_t, 5 r_t] (60 bins): pooled per-bin |dN| <= max(4 sigma, 2%),
+    ensemble chi-square p > 1e-3.
 Also grid keys / reorder remap / collision flags on the golden states, bit-exact."""
 import os
 
 import numpy as np
 import pytest
 
+import sys
+
 import orc
 import paper_2605_18254_b200 as srm
 import stats_util
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
 
 pytestmark = pytest.mark.gpu
 G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -41,14 +49,14 @@ def test_device_grid_vs_golden(name):
     assert (st.overlap_pairs > 0) == bool(z["any"])
 
 
-@pytest.mark.parametrize("name", ["e2e_2d", "e2e_3d"])
+@pytest.mark.parametrize("name", ["e2e_2d", "e2e_3d", "e2e_cfg4"])
 def test_generate_statistics_match_reference(name):
     z = load(name)
     dim, n = int(z["dim"]), int(z["n"])
     L = [1.0] * dim
     unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
     r0 = (float(z["f0"]) / (n * unit)) ** (1.0 / dim)
-    nnd, rdf = [], None
+    nnd, rdf = [], []
     for s in z["seeds"]:
         pos, ids = srm.rsa_place(np.full(n, r0), L, 10000, 1000 + int(s))
         snap = srm.Snapshot(L, pos, np.full(n, r0), ids)
@@ -61,5 +69,97 @@ def test_generate_statistics_match_reference(name):
         assert orc.o_stats(dim, L, out.pos, out.radius).overlap_pairs == 0
         nnd.append(orc.r_nnd(dim, L, out.pos))
         c = stats_util.rdf_counts(out.pos, L, *stats_util.rdf_window(z))
-        rdf = c if rdf is None else rdf + c
+        rdf.append(c)
     stats_util.check_against_reference(nnd, rdf, z)
+
+
+def test_large_n_spot_check_cfg4():
+    """The bench workload's parameters at N = 10^6 (SURVEY.md §8d "spot-check large N"):
+    one device srm_generate run from the reference's own 10^6-sphere start (rsa_place,
+    bit-identical) at f0 = 0.1 to f_t = 0.30 with c_m = 0.05 r_t, zero overlaps, against
+    the reference's srm_generate on the same start (tests/golden/e2e_cfg4_large.npz).
+    Statistics on the device (srm_b200_nnd_histogram, srm_b200_pair_counts, pinned in
+    tests/test_gpu_descriptors.py), in units of r_t: the NND summaries, the 40-bin NND
+    histogram and the 60-bin pair counts.  One configuration per side, so the tolerance
+    is the configuration-to-configuration spread, measured on the reference's 12 x 4000
+    ensemble (e2e_cfg4): 4 sqrt(2) of it (see below)."""
+    zl, z = load("e2e_cfg4_large"), load("e2e_cfg4")
+    n = int(zl["n"])
+    L = [1.0, 1.0, 1.0]
+    unit = 4.0 / 3.0 * np.pi
+    r0 = (float(zl["f0"]) / (n * unit)) ** (1.0 / 3.0)
+    rt = float(zl["r_target"])
+    rt_small = float(z["r_target"])
+    pos, ids = srm.rsa_place(np.full(n, r0), L, 10000, 1000 + int(zl["seeds"][0]))
+    p = srm.SrmParams(c_w=float(zl["c_w"]), c_m=float(zl["cm_rel"]) * rt, n_k=int(zl["n_k"]), n_l=int(zl["n_l"]),
+                      f_target=float(zl["f_t"]), max_iterations=100000, seed=77, reorder_period=16)
+    with srm.Context(L, n) as ctx:
+        ctx.upload(pos, np.full(n, r0), ids)
+        out = ctx.generate(p)
+        assert abs(out.volume_fraction / float(zl["f_t"]) - 1.0) < 1e-9
+        assert ctx.overlap_stats(2.5 * ctx.max_bounding_radius()).overlap_pairs == 0
+        nnd = ctx.nearest_neighbor_distances() / rt
+        h = ctx.nnd_histogram(40, 2.0 * 0.999 * rt, 2.8 * rt)[0]
+        rdf = ctx.pair_counts(np.linspace(2.0 * 0.999, 5.0, 61) * rt)
+    # tolerance: 4 sqrt(2) x the reference's configuration-to-configuration spread at N = 4000
+    # (e2e_cfg4), NOT scaled down to N = 10^6: part of it -- the number of growth
+    # iterations and shake rounds of a run -- is one draw per configuration at any N
+    # (the reference needs 19-22 iterations at N = 4000, 26 at 10^6); counts scale with N
+    k = 4.0 * np.sqrt(2.0)
+    scale = n / float(z["n"])
+    small = stats_util.ensemble_stats(list(z["nnd"]), rt_small)
+    tol = k * small.std(0, ddof=1)
+    d = np.abs(stats_util.ensemble_stats([nnd], 1.0)[0] - zl["summary"])
+    assert (d <= tol).all(), f"NND summaries: |d| = {d}, tolerance {tol}"
+    e = np.linspace(2.0 * 0.999, 2.8, 41)
+    hs = np.array([np.histogram(a / rt_small, e)[0] for a in z["nnd"]])
+    # (+ the Poisson spread of the two large histograms, which dominates in sparse bins)
+    tol = k * np.sqrt((hs.std(0, ddof=1) * scale) ** 2 + h + zl["nnd_hist"]) + 3.0
+    d = np.abs(h - zl["nnd_hist"])
+    bad = np.where(d > tol)[0]
+    assert bad.size == 0, f"NND histogram bins {bad}: {h[bad]} vs {zl['nnd_hist'][bad]}, tolerance {tol[bad]}"
+    tol = k * np.sqrt((z["rdf_seeds"].std(0, ddof=1) * scale) ** 2 + rdf + zl["rdf"]) + 3.0
+    d = np.abs(rdf - zl["rdf"])
+    bad = np.where(d > tol)[0]
+    assert bad.size == 0, f"pair-count bins {bad}: {rdf[bad]} vs {zl['rdf'][bad]}, tolerance {tol[bad]}"
+    print(f"spot check 1e6: NND summaries {stats_util.ensemble_stats([nnd], 1.0)[0]} vs reference {zl['summary']}; "
+          f"iterations {out.iteration_count} vs {int(zl['iterations'])}")
+
+
+def test_polydisperse_clustered_statistics_match_reference():
+    """Scaled-down cfg 3 (tests/golden/make_golden.py POLY): polydisperse lognormal radii,
+    clustered starts (rsa_clustered, the same starts as the reference's), device
+    srm_generate vs the reference's on each seed; f_t within 1e-9, zero overlaps (oracle
+    audit); NND in units of the mean radius: 40 bins on [1, 3] per-bin within
+    max(4 sigma, 2%) and ensemble chi-square p > 1e-3, per-seed quantiles by Welch t-tests
+    (stats_util.ensemble_agree); pair counts on [1.8, 10] mean radii (60 bins) per-bin
+    and ensemble chi-square."""
+    import make_golden
+    z = load("e2e_poly")
+    c = make_golden.POLY
+    nnd, rdf = [], []
+    for s in c["seeds"]:
+        L, pos, r0, ids = make_golden.poly_start(c, s)
+        snap = srm.Snapshot(L, pos, r0, ids)
+        p = srm.SrmParams(c_w=c["c_w"], c_m=c["c_m"], n_k=c["n_k"], n_l=c["n_l"], f_target=c["f_t"],
+                          max_iterations=100000, seed=s, reorder_period=16)
+        res = srm.srm_generate(snap, p)
+        assert res.status == srm.GenerateStatus.Converged
+        assert abs(res.snapshot.volume_fraction / c["f_t"] - 1.0) < 1e-9
+        out = res.snapshot
+        assert orc.o_stats(3, L, out.pos, out.radius).overlap_pairs == 0
+        rm = float(out.radius.mean())
+        nnd.append(orc.r_nnd(3, L, out.pos) / rm)
+        rdf.append(stats_util.rdf_counts(out.pos / rm, np.array(L) / rm, 0.9 * 2, 5.0 * 2, 60))
+    ps = stats_util.ensemble_agree(stats_util.ensemble_stats(nnd, 1.0, None),
+                                   stats_util.ensemble_stats(list(z["nnd"]), 1.0, None))
+    assert min(ps) > 1e-3, f"per-seed NND summaries differ: Welch p = {ps}"
+    edges = np.linspace(1.0, 3.0, 41)
+    h_dev = np.array([np.histogram(a, edges)[0] for a in nnd])
+    h_ref = np.array([np.histogram(a, edges)[0] for a in z["nnd"]])
+    ok, _ = stats_util.hist_agree(h_dev.sum(0), h_ref.sum(0))
+    assert ok.all(), f"NND bins out of tolerance: {np.where(~ok)[0]}"
+    assert stats_util.ensemble_chi2(h_dev, h_ref) > 1e-3
+    ok, _ = stats_util.hist_agree(np.sum(rdf, axis=0), z["rdf"])
+    assert ok.all(), f"pair-count bins out of tolerance: {np.where(~ok)[0]}"
+    assert stats_util.ensemble_chi2(rdf, z["rdf_seeds"]) > 1e-3

@@ -21,7 +21,7 @@ def test_oracle_generate_statistics_match_reference(name):
     L = [1.0] * dim
     unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
     r0 = (float(z["f0"]) / (n * unit)) ** (1.0 / dim)
-    nnd, rdf = [], None
+    nnd, rdf = [], []
     for s in z["seeds"]:
         pos, ids = srm.rsa_place(np.full(n, r0), L, 10000, 1000 + int(s))
         status, p, r, _, _, f, _ = orc.o_generate(dim, L, pos, np.full(n, r0), ids, float(z["c_w"]), float(z["c_m"]),
@@ -31,5 +31,5 @@ def test_oracle_generate_statistics_match_reference(name):
         assert orc.o_stats(dim, L, p, r).overlap_pairs == 0
         nnd.append(orc.r_nnd(dim, L, p))
         c = stats_util.rdf_counts(p, L, *stats_util.rdf_window(z))
-        rdf = c if rdf is None else rdf + c
+        rdf.append(c)
     stats_util.check_against_reference(nnd, rdf, z)
