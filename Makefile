@@ -14,6 +14,9 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-ffp-contract=off \
            --expt-relaxed-constexpr -Xptxas -v
 CXXFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off
+# nlohmann::json 3.11.3 (header only; the reference's JSON library and version) for the
+# snapshot header -- the copy vendored in the image's cudnn_frontend package
+JSON_INC ?= $(firstword $(wildcard /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty))
 
 all: lib oracle
 	@if [ -d "$(REF)/core/include" ]; then $(MAKE) shimtest; else echo "shimtest: $(REF) absent, keeping prebuilt binary (if any)"; fi
@@ -29,11 +32,14 @@ $(CSRC)/srm_selftest.o: $(CSRC)/srm_selftest.cu $(CSRC)/srm_device.cuh include/s
 $(CSRC)/srm_rsa.o: $(CSRC)/srm_rsa.cpp include/srm_b200.h
 	g++ $(CXXFLAGS) -c $< -o $@
 
-$(LIB): $(CSRC)/srm_capi.o $(CSRC)/srm_selftest.o $(CSRC)/srm_rsa.o
+$(CSRC)/srm_snapshot.o: $(CSRC)/srm_snapshot.cpp include/srm_b200.h
+	g++ $(CXXFLAGS) -I$(JSON_INC) -c $< -o $@
+
+$(LIB): $(CSRC)/srm_capi.o $(CSRC)/srm_selftest.o $(CSRC)/srm_rsa.o $(CSRC)/srm_snapshot.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
 
 oracle:
-	$(MAKE) -f oracle/Makefile REF=$(REF)
+	$(MAKE) -f oracle/Makefile REF=$(REF) JSON_INC=$(JSON_INC)
 
 shimtest: tests/cpp/shim_test
 

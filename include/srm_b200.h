@@ -39,7 +39,8 @@ typedef enum {
     SRM_B200_INVALID = 2,         /* ValidationError / std::invalid_argument                */
     SRM_B200_CUDA_ERROR = 3,      /* device failure (no reference counterpart)              */
     SRM_B200_PLACEMENT_FAILURE = 4, /* PlacementFailure (errors.hpp:15-23)                  */
-    SRM_B200_NO_DEVICE = 5        /* no CUDA device: the product has no CPU fallback         */
+    SRM_B200_NO_DEVICE = 5,       /* no CUDA device: the product has no CPU fallback         */
+    SRM_B200_IO_ERROR = 6         /* IoError (errors.hpp): snapshot file I/O or format       */
 } srm_b200_status;
 
 typedef enum {
@@ -188,6 +189,36 @@ int srm_b200_round(srm_b200_ctx* ctx, double cell_size, double c_m, int n_l, uin
 int srm_b200_rounds(srm_b200_ctx* ctx, double cell_size, double c_m, int n_l, uint64_t key,
                     uint32_t first_round, uint32_t iteration, int rounds,
                     srm_b200_round_stats* last);
+
+/* ---- snapshots: the reference's file format (snapshot_io.cpp) ------- */
+/* the Snapshot fields a file carries besides the particles (snapshot_io.cpp:128-148) */
+typedef struct {
+    double volume_fraction;
+    int64_t iteration_count;
+    uint64_t seed;
+    srm_b200_params params;
+} srm_b200_snapshot_meta;
+/* dimension, shape kind and box of a context */
+int srm_b200_describe(const srm_b200_ctx* ctx, int* dim, int* shape_kind, double* box_lengths);
+/* snapshot_io.cpp:170-191 snapshot_to_binary (binary != 0) or :150-167 snapshot_to_text of
+ * host arrays (spheres/disks: pos, radius; platelets: pos, normal, diameter, thickness),
+ * byte-identical to the reference's.  out == NULL: *len_inout = the size needed. */
+int srm_b200_snapshot_encode(int dim, int shape_kind, const double* box_lengths, int64_t n,
+                             const double* pos, const double* radius, const double* normal,
+                             const double* diameter, const double* thickness, const int32_t* id,
+                             const srm_b200_snapshot_meta* meta, int binary, char* out,
+                             int64_t* len_inout);
+/* save_snapshot (snapshot_io.cpp:421-426): the context's state, written atomically */
+int srm_b200_save_snapshot(srm_b200_ctx* ctx, const char* path, const srm_b200_snapshot_meta* meta,
+                           int binary);
+/* load_snapshot (snapshot_io.cpp:414-420), binary or text: the header (dim, shape kind,
+ * count, box, meta) ... */
+int srm_b200_snapshot_info(const char* path, int* dim, int* shape_kind, int64_t* count,
+                           double* box_lengths, srm_b200_snapshot_meta* meta);
+/* ... and the particles into a context of the same shape and box (count <= capacity) */
+int srm_b200_load_snapshot(srm_b200_ctx* ctx, const char* path);
+/* message of the last SRM_B200_IO_ERROR (thread-local) */
+const char* srm_b200_io_error(void);
 
 /* ---- parity statistics on the device ---------------------------- */
 /* descriptors.hpp:96-115 nearest_neighbor_distances of the context's state (exact: the

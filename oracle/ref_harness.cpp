@@ -19,6 +19,7 @@
 #include "srm/recipes.hpp"
 #include "srm/rsa.hpp"
 #include "srm/shape.hpp"
+#include "srm/snapshot_io.hpp"
 #include "srm/spherodisk.hpp"
 
 using namespace srm;
@@ -440,6 +441,46 @@ double ref_pl_bench_rounds(const double* L, int64_t n, const double* pos, const 
     const auto t1 = std::chrono::steady_clock::now();
     if (accepted_total) *accepted_total = acc.load();
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// snapshot_io.cpp snapshot_to_binary / snapshot_to_text of a state (spheres/disks: pos, r;
+// platelets (shape 1): pos, nrm, D, t); returns the byte count, copies up to cap bytes
+static void fill_meta(SrmParams& p, const double* pd, const int64_t* pi) {
+    p.c_w = pd[0]; p.c_m = pd[1]; p.c_r = pd[2]; p.f_target = pd[3];
+    p.n_k = static_cast<int>(pi[0]); p.n_l = static_cast<int>(pi[1]); p.max_iterations = pi[2];
+    p.seed = static_cast<std::uint64_t>(pi[3]); p.reorder_period = static_cast<int>(pi[4]);
+}
+
+int64_t ref_snapshot_bytes(int dim, int shape, const double* L, int64_t n, const double* pos, const double* r,
+                           const double* nrm, const double* D, const double* t, const int32_t* id, double f,
+                           int64_t iterations, uint64_t seed, const double* pd, const int64_t* pi, int binary,
+                           char* out, int64_t cap) {
+    std::string bytes;
+    if (shape == 1) {
+        PlateletSnapshot s;
+        s.box = make_box<3>(L);
+        s.particles.resize(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) s.particles[i] = make_pl(pos + 3 * i, nrm + 3 * i, D[i], t[i], id[i]);
+        s.volume_fraction = f; s.iteration_count = iterations; s.seed = seed;
+        fill_meta(s.params, pd, pi);
+        bytes = binary ? snapshot_to_binary(s) : snapshot_to_text(s);
+    } else if (dim == 2) {
+        DiskSnapshot s;
+        s.box = make_box<2>(L);
+        s.particles = make_particles<2>(n, pos, r, id);
+        s.volume_fraction = f; s.iteration_count = iterations; s.seed = seed;
+        fill_meta(s.params, pd, pi);
+        bytes = binary ? snapshot_to_binary(s) : snapshot_to_text(s);
+    } else {
+        SphereSnapshot s;
+        s.box = make_box<3>(L);
+        s.particles = make_particles<3>(n, pos, r, id);
+        s.volume_fraction = f; s.iteration_count = iterations; s.seed = seed;
+        fill_meta(s.params, pd, pi);
+        bytes = binary ? snapshot_to_binary(s) : snapshot_to_text(s);
+    }
+    if (out) std::memcpy(out, bytes.data(), std::min<size_t>(bytes.size(), static_cast<size_t>(cap)));
+    return static_cast<int64_t>(bytes.size());
 }
 
 // shape_any_collision<SpherodiskShape> over a grid of cell size cs

@@ -18,6 +18,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -31,12 +32,13 @@ __all__ = [
     "SrmParams", "Snapshot", "GenerateStatus", "GenerateResult", "ProgressRecord",
     "Context", "srm_generate", "relax_sweeps", "shake", "swell_all", "reorder_by_locality",
     "rsa_place", "mix_seed", "K_RSA_DEFAULT_ATTEMPTS", "PlateletSnapshot", "srm_generate_platelets",
-    "rsa_platelets", "rsa_clustered",
+    "rsa_platelets", "rsa_clustered", "IoError", "snapshot_bytes", "snapshot_info",
 ]
 
 K_RSA_DEFAULT_ATTEMPTS = 10000  # rsa.hpp:15 kRsaDefaultAttempts
 
-OK, ITER_LIMIT, INVALID, CUDA_ERROR, PLACEMENT_FAILURE, NO_DEVICE = range(6)
+OK, ITER_LIMIT, INVALID, CUDA_ERROR, PLACEMENT_FAILURE, NO_DEVICE, IO_ERROR = range(7)
+SPHERE, PLATELET = 0, 1  # srm_b200_shape
 
 
 class Error(RuntimeError):
@@ -58,6 +60,10 @@ class PlacementFailure(Error):
 
 class CudaError(Error):
     """device failure (no reference counterpart)"""
+
+
+class IoError(Error):
+    """errors.hpp IoError: snapshot file I/O or format (snapshot_io.cpp)"""
 
 
 class NoDeviceError(CudaError):
@@ -376,6 +382,23 @@ class Context:
         return {"nonmovers": v[0], "colour_classes": v[1], "cells_per_class": v[2], "near_half_width": v[3],
                 "colour_modulus": v[4], "cells": v[5]}
 
+    def save_snapshot(self, path: str, volume_fraction: float = 0.0, iteration_count: int = 0, seed: int = 0,
+                      params: Optional[SrmParams] = None, binary: bool = True) -> None:
+        """save_snapshot (snapshot_io.cpp): the context's state in the reference's file
+        format, written atomically."""
+        m = _meta(volume_fraction, iteration_count, seed, params)
+        st = _native.lib().srm_b200_save_snapshot(self._h, os.fsencode(path), C.byref(m), 1 if binary else 0)
+        _check_io(st)
+
+    def load_snapshot(self, path: str) -> None:
+        """load_snapshot (snapshot_io.cpp): the file's particles into this context (same
+        shape and box)."""
+        st = _native.lib().srm_b200_load_snapshot(self._h, os.fsencode(path))
+        if st == INVALID:
+            raise ValidationError(_native.lib().srm_b200_io_error().decode() or "load_snapshot: invalid")
+        _check_io(st)
+        self.n = int(_native.lib().srm_b200_count(self._h))
+
     def nearest_neighbor_distances(self) -> np.ndarray:
         """descriptors.hpp:96-115 on the device (download order)."""
         out = np.empty(max(self.n, 1))
@@ -566,6 +589,56 @@ def rsa_place(radii, box: Sequence[float], max_attempts: int, seed: int):
         raise ValidationError("rsa_place: invalid radii or box")
     _check(st)
     return pos[:n], ids[:n]
+
+
+def _meta(volume_fraction, iteration_count, seed, params):
+    m = _native.SnapshotMeta()
+    m.volume_fraction = float(volume_fraction)
+    m.iteration_count = int(iteration_count)
+    m.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    m.params = (params or SrmParams()).to_c()
+    return m
+
+
+def snapshot_bytes(box, pos, radius=None, id=None, *, normal=None, diameter=None, thickness=None,
+                   volume_fraction=0.0, iteration_count=0, seed=0, params=None, binary=True) -> bytes:
+    """snapshot_io.cpp snapshot_to_binary / snapshot_to_text of a state: the reference's
+    SRMSNAP file bytes (spheres/disks: pos, radius; platelets: pos, normal, diameter,
+    thickness).  Byte-identical to the reference's encoder (tests/test_snapshot.py)."""
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    n, dim = pos.shape
+    plate = normal is not None
+    ids = np.ascontiguousarray(np.arange(n, dtype=np.int32) if id is None else id, dtype=np.int32)
+    arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+            for a in (radius, normal, diameter, thickness)]
+    L = (C.c_double * dim)(*[float(v) for v in box])
+    m = _meta(volume_fraction, iteration_count, seed, params)
+    ln = C.c_int64(0)
+    args = [dim, PLATELET if plate else SPHERE, L, n, _ptr(pos)] + [_ptr(a) for a in arrs] + [_ptr(ids), C.byref(m),
+                                                                                              1 if binary else 0]
+    _check(_native.lib().srm_b200_snapshot_encode(*args, None, C.byref(ln)))
+    buf = C.create_string_buffer(ln.value)
+    _check(_native.lib().srm_b200_snapshot_encode(*args, buf, C.byref(ln)))
+    return buf.raw[:ln.value]
+
+
+def snapshot_info(path: str) -> dict:
+    """Header of a snapshot file (binary or text): dim, shape, count, box, meta."""
+    dim, kind, cnt = C.c_int(), C.c_int(), C.c_int64()
+    L = (C.c_double * 3)()
+    m = _native.SnapshotMeta()
+    st = _native.lib().srm_b200_snapshot_info(os.fsencode(path), C.byref(dim), C.byref(kind), C.byref(cnt), L,
+                                              C.byref(m))
+    _check_io(st)
+    return dict(dim=dim.value, shape="platelet" if kind.value == PLATELET else "sphere", count=cnt.value,
+                box=[L[a] for a in range(dim.value)], volume_fraction=m.volume_fraction,
+                iteration_count=m.iteration_count, seed=m.seed, params=m.params)
+
+
+def _check_io(st):
+    if st == IO_ERROR:
+        raise IoError(_native.lib().srm_b200_io_error().decode())
+    _check(st)
 
 
 def rsa_clustered(radii, box: Sequence[float], n_clusters: int, sigma: float, max_attempts: int, seed: int):

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("SRM_B200_LIB") or os.path.join(_HERE, "libsrm_b200.so
 c_double_p = C.POINTER(C.c_double)
 c_int32_p = C.POINTER(C.c_int32)
 c_int64_p = C.POINTER(C.c_int64)
+c_int_p = C.POINTER(C.c_int)
 c_uint32_p = C.POINTER(C.c_uint32)
 c_uint8_p = C.POINTER(C.c_uint8)
 
@@ -34,6 +35,17 @@ class Params(C.Structure):
         ("max_iterations", C.c_int64),
         ("seed", C.c_uint64),
         ("reorder_period", C.c_int32),
+    ]
+
+
+class SnapshotMeta(C.Structure):
+    """srm_b200_snapshot_meta: the Snapshot fields a file carries (snapshot_io.cpp:128-148)."""
+
+    _fields_ = [
+        ("volume_fraction", C.c_double),
+        ("iteration_count", C.c_int64),
+        ("seed", C.c_uint64),
+        ("params", Params),
     ]
 
 
@@ -92,6 +104,14 @@ _SIGS = {
     "srm_b200_round": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.c_void_p, C.POINTER(RoundStats)]),
     "srm_b200_rounds": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(RoundStats)]),
     "srm_b200_rsa_place": (C.c_int, [C.c_int, c_double_p, C.c_int64, C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p, c_int64_p]),
+    "srm_b200_describe": (C.c_int, [C.c_void_p, c_int_p, c_int_p, c_double_p]),
+    "srm_b200_snapshot_encode": (C.c_int, [C.c_int, C.c_int, c_double_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                           c_int64_p]),
+    "srm_b200_save_snapshot": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int]),
+    "srm_b200_snapshot_info": (C.c_int, [C.c_char_p, c_int_p, c_int_p, c_int64_p, c_double_p, C.c_void_p]),
+    "srm_b200_load_snapshot": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "srm_b200_io_error": (C.c_char_p, []),
     "srm_b200_nnd_histogram": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_void_p, c_int64_p, c_int64_p,
                                          C.c_void_p]),
     "srm_b200_pair_counts": (C.c_int, [C.c_void_p, c_double_p, C.c_int, C.c_void_p]),

@@ -80,7 +80,8 @@ struct srm_b200_ctx {
     State P{}, Q{}, S{};
     uint32_t* key = nullptr;
     uint32_t* skey = nullptr;
-    int32_t* perm = nullptr;
+    int32_t* perm = nullptr;             // scratch (remap, accept flags by slot)
+    unsigned long long* perm64 = nullptr;  // grid build: slot << 32 | source index, cell-sorted
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near-list rows (kNearRow int32 per particle)
     int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_warpq (set in init)
@@ -222,6 +223,7 @@ struct srm_b200_ctx {
         key = dalloc<uint32_t>(cap);
         skey = dalloc<uint32_t>(cap);
         perm = dalloc<int32_t>(cap);
+        perm64 = dalloc<unsigned long long>(cap);
         acc = dalloc<uint8_t>(cap);
         gp = dalloc<GridParams>(1);
         rp = dalloc<RoundParams>(1);
@@ -250,7 +252,7 @@ struct srm_b200_ctx {
         free_state(P);
         free_state(Q);
         free_state(S);
-        cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(acc);
+        cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(perm64); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
         cudaFree(nbr); cudaFree(S.xf); 
@@ -292,8 +294,8 @@ struct srm_b200_ctx {
         const int64_t c = ncells + ncells / 8 + 1024;
         count = dalloc<uint32_t>(c);
         cell_start = dalloc<int64_t>(c + 1);
-        tile_cap = (c + kScanTile - 1) / kScanTile;
-        partial = dalloc<uint64_t>(tile_cap);
+        tile_cap = (c + kLbTile - 1) / kLbTile;
+        partial = dalloc<uint64_t>(tile_cap + 1);  // look-back status words + the tile counter
         SRM_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * c, stream));
         cell_cap = c;
     }
@@ -345,15 +347,15 @@ struct srm_b200_ctx {
         const int cb = static_cast<int>(std::min<int64_t>(blocks_for(nc, 256), 148 * 64));
         if (dim == 2) k_keys<2><<<nb, 256, 0, stream>>>(n, T, gp, key, count);
         else k_keys<3><<<nb, 256, 0, stream>>>(n, T, gp, key, count);
-        const int tiles = static_cast<int>((nc + kScanTile - 1) / kScanTile);
-        k_scan_tiles<<<tiles, 1024, 0, stream>>>(count, gp, partial);
-        k_scan_partials<<<1, 1024, 0, stream>>>(partial, tile_cap, gp, cell_start);
-        k_scan_down<<<tiles, 1024, 0, stream>>>(count, partial, gp, cell_start);
-        k_scatter<<<nb, 256, 0, stream>>>(n, key, cell_start, count, perm);
-        k_cellsort<<<cb, 256, 0, stream>>>(gp, cell_start, T.slot, perm);
-        if (dim == 2) k_gather<2><<<nb, 256, 0, stream>>>(n, perm, key, T, S, skey);
-        else k_gather<3><<<nb, 256, 0, stream>>>(n, perm, key, T, S, skey);
-        launched(7);
+        const int tiles = static_cast<int>((nc + kLbTile - 1) / kLbTile);
+        SRM_CUDA(cudaMemsetAsync(partial, 0, sizeof(uint64_t) * (tiles + 1), stream));
+        k_scan_lookback<<<tiles, kLbThreads, 0, stream>>>(count, gp, reinterpret_cast<unsigned long long*>(partial),
+                                                         cell_start);
+        k_scatter<<<nb, 256, 0, stream>>>(n, key, T.slot, cell_start, count, perm64);
+        k_cellsort<<<cb, 256, 0, stream>>>(gp, cell_start, perm64);
+        if (dim == 2) k_gather<2><<<nb, 256, 0, stream>>>(n, perm64, key, T, S, skey);
+        else k_gather<3><<<nb, 256, 0, stream>>>(n, perm64, key, T, S, skey);
+        launched(5);
     }
 
     void copy_state(State& A, State& B) {
@@ -388,8 +390,9 @@ struct srm_b200_ctx {
             FamScope fs(this, 1);
             for (int cls = 0; cls < hg.ncls; ++cls) {
                 const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
-                // about 64 cells per warp, at most one wave of resident CTAs
-                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads * 2), queue_ctas)));
+                // a cell per lane (the cells of a class are its parallelism: a cell's
+                // particles are visited in order), at most one wave of resident CTAs
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), queue_ctas)));
                 if (dim == 2)
                     k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
@@ -756,6 +759,15 @@ void srm_b200_destroy(srm_b200_ctx* ctx) { delete ctx; }
 const char* srm_b200_last_error(const srm_b200_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int64_t srm_b200_count(const srm_b200_ctx* ctx) { return ctx ? ctx->n : 0; }
+
+int srm_b200_describe(const srm_b200_ctx* ctx, int* dim, int* shape_kind, double* box_lengths) {
+    if (!ctx) return SRM_B200_INVALID;
+    if (dim) *dim = ctx->dim;
+    if (shape_kind) *shape_kind = ctx->platelets() ? SRM_B200_PLATELET : SRM_B200_SPHERE;
+    if (box_lengths)
+        for (int a = 0; a < ctx->dim; ++a) box_lengths[a] = ctx->box.L[a];
+    return SRM_B200_OK;
+}
 
 int srm_b200_upload(srm_b200_ctx* c, int64_t n, const double* pos, const double* radius, const int32_t* id) {
     return guarded(c, [&]() -> int {

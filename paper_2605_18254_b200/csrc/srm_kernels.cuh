@@ -2,7 +2,7 @@
 //
 // One SRM round (engine.hpp:227-234: build_shape_grid -> migrate -> shape_any_collision)
 // is, on the device:
-//   grid rebuild   k_keys -> k_scan_* -> k_scatter -> k_cellsort -> k_gather
+//   grid rebuild   k_keys -> k_scan_lookback -> k_scatter -> k_cellsort -> k_gather
 //   near lists     k_near_tiles / k_near_lists (round-start neighbours within the trial reach)
 //   migrate        k_sweep_warpq, one launch per colour class (warp queues)
 //   reduction      k_stats_sweep (overlap pairs, max penetration over the non-movers)
@@ -20,7 +20,6 @@
 
 namespace srmb {
 
-constexpr int kScanTile = 4096;  // cells per scan tile (1024 threads x 4)
 
 // Division by a grid constant d >= 1 as a multiply-high (Granlund & Montgomery 1994,
 // 33-bit multiplier): q = (umulhi(n, m) + n) >> l, exact for every 32-bit n.
@@ -247,147 +246,132 @@ __global__ void k_keys(int64_t n, State T, const GridParams* __restrict__ gp,
     }
 }
 
-// ---- exclusive scan of count[ncells] -> cell_start[ncells+1] (3 passes) ----------
-__global__ void k_scan_tiles(const uint32_t* __restrict__ count, const GridParams* __restrict__ gp,
-                             uint64_t* __restrict__ partial) {
-    const int64_t ncells = gp->ncells;
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    uint64_t s = 0;
-    if (base < ncells) {
-#pragma unroll
-        for (int k = 0; k < kScanTile / 1024; ++k) {
-            const int64_t c = base + (int64_t)k * 1024 + threadIdx.x;
-            if (c < ncells) s += count[c];
-        }
-    }
-    // block reduce
-    __shared__ uint64_t red[32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        uint64_t v = red[threadIdx.x];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) partial[blockIdx.x] = v;
-    }
-}
+// Single-pass exclusive scan of count[ncells] -> cell_start[ncells + 1] with decoupled
+// look-back (Merrill & Garland 2016): a block per tile of kLbTile cells, tile ids in
+// launch order from a counter (so a tile only waits on tiles that are running or done);
+// each tile publishes its aggregate, then its inclusive prefix, as one 64-bit word
+// (2-bit state | 62-bit value) in status[1 + tile].  status[0] is the tile counter.
+// status[] must be zero on entry (one memset per scan).
+constexpr int kLbThreads = 256, kLbPer = 16, kLbTile = kLbThreads * kLbPer;
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbPrefix = 2ull << 62, kLbMask = (1ull << 62) - 1;
 
-// single block: exclusive scan of the tile sums, in chunks of 1024
-__global__ void k_scan_partials(uint64_t* __restrict__ partial, int64_t ntiles_cap,
-                                const GridParams* __restrict__ gp, int64_t* __restrict__ cell_start) {
+__global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const uint32_t* __restrict__ count,
+                                                              const GridParams* __restrict__ gp,
+                                                              unsigned long long* __restrict__ status,
+                                                              int64_t* __restrict__ cell_start) {
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long warp_tot[kLbThreads / 32];
+    __shared__ unsigned long long excl_s;
     const int64_t ncells = gp->ncells;
-    const int64_t ntiles = (ncells + kScanTile - 1) / kScanTile;
-    (void)ntiles_cap;
-    __shared__ uint64_t warp_tot[32];
-    __shared__ uint64_t carry_s;
-    if (threadIdx.x == 0) carry_s = 0;
+    const int64_t ntiles = (ncells + kLbTile - 1) / kLbTile;
+    if (threadIdx.x == 0) tile_s = atomicAdd(reinterpret_cast<unsigned*>(status), 1u);
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int64_t b0 = 0; b0 < ntiles; b0 += 1024) {
-        const int64_t t = b0 + threadIdx.x;
-        const uint64_t v = t < ntiles ? partial[t] : 0;
-        uint64_t incl = v;
+    const int64_t tile = tile_s;
+    if (tile >= ntiles) return;
+    const int64_t base = tile * kLbTile + static_cast<int64_t>(threadIdx.x) * kLbPer;
+    uint32_t v[kLbPer];
+    if (base + kLbPer <= ncells) {
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += u;
+        for (int k = 0; k < kLbPer; k += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(count + base + k);
+            v[k] = q.x;
+            v[k + 1] = q.y;
+            v[k + 2] = q.z;
+            v[k + 3] = q.w;
         }
-        if (lane == 31) warp_tot[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            const uint64_t w = warp_tot[lane];
-            uint64_t wi = w;
+    } else {
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t u = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += u;
-            }
-            warp_tot[lane] = wi - w;
-        }
-        __syncthreads();
-        const uint64_t carry = carry_s;
-        const uint64_t excl = carry + warp_tot[wid] + incl - v;
-        if (t < ntiles) partial[t] = excl;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry_s = excl + v;
-        __syncthreads();
+        for (int k = 0; k < kLbPer; ++k) v[k] = base + k < ncells ? count[base + k] : 0u;
     }
-    if (threadIdx.x == 0) cell_start[ncells] = (int64_t)carry_s;
-}
-
-__global__ void k_scan_down(const uint32_t* __restrict__ count, const uint64_t* __restrict__ partial,
-                            const GridParams* __restrict__ gp, int64_t* __restrict__ cell_start) {
-    const int64_t ncells = gp->ncells;
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    if (base >= ncells) return;
-    __shared__ uint64_t warp_tot[32];
+    unsigned long long t = 0;
+#pragma unroll
+    for (int k = 0; k < kLbPer; ++k) t += v[k];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // thread t owns cells base + 4t .. base + 4t + 3 (contiguous)
-    uint32_t v[4];
-    uint64_t s = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int64_t c = base + 4 * (int64_t)threadIdx.x + k;
-        v[k] = c < ncells ? count[c] : 0u;
-        s += v[k];
-    }
-    uint64_t incl = s;
+    unsigned long long incl = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += u;
     }
     if (lane == 31) warp_tot[wid] = incl;
     __syncthreads();
-    if (wid == 0) {
-        const uint64_t w = warp_tot[lane];
-        uint64_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t u = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += u;
+    if (threadIdx.x == 0) {
+        unsigned long long total = 0;
+        for (int w = 0; w < kLbThreads / 32; ++w) {
+            const unsigned long long x = warp_tot[w];
+            warp_tot[w] = total;
+            total += x;
         }
-        warp_tot[lane] = wi - w;
+        volatile unsigned long long* st = status + 1;
+        unsigned long long excl = 0;
+        if (tile == 0) {
+            st[0] = kLbPrefix | total;
+        } else {
+            st[tile] = kLbAgg | total;
+            for (int64_t j = tile - 1; j >= 0; --j) {
+                unsigned long long w;
+                do {
+                    w = st[j];
+                } while ((w & ~kLbMask) == 0);
+                excl += w & kLbMask;
+                if ((w & ~kLbMask) == kLbPrefix) break;
+            }
+            st[tile] = kLbPrefix | (excl + total);
+        }
+        excl_s = excl;
+        if (tile == ntiles - 1) cell_start[ncells] = static_cast<int64_t>(excl + total);
     }
     __syncthreads();
-    uint64_t run = partial[blockIdx.x] + warp_tot[wid] + incl - s;
+    unsigned long long run = excl_s + warp_tot[wid] + incl - t;
+    if (base + kLbPer <= ncells) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int64_t c = base + 4 * (int64_t)threadIdx.x + k;
-        if (c < ncells) cell_start[c] = (int64_t)run;
-        run += v[k];
+        for (int k = 0; k < kLbPer; k += 2) {
+            longlong2 o;
+            o.x = static_cast<long long>(run);
+            run += v[k];
+            o.y = static_cast<long long>(run);
+            run += v[k + 1];
+            *reinterpret_cast<longlong2*>(cell_start + base + k) = o;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kLbPer; ++k) {
+            if (base + k < ncells) cell_start[base + k] = static_cast<int64_t>(run);
+            run += v[k];
+        }
     }
 }
 
-// atomic scatter into cell ranges; count[] returns to zero for the next histogram
-__global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key,
+// atomic scatter into cell ranges (count[] returns to zero for the next histogram); the
+// entry carries the sort key of the within-cell order with it: slot << 32 | source index
+__global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const int32_t* __restrict__ slot,
                           const int64_t* __restrict__ cell_start, uint32_t* __restrict__ count,
-                          int32_t* __restrict__ perm) {
+                          unsigned long long* __restrict__ perm) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = key[i];
         const uint32_t r = atomicSub(&count[k], 1u) - 1u;
-        perm[cell_start[k] + r] = static_cast<int32_t>(i);
+        perm[cell_start[k] + r] = (static_cast<unsigned long long>(static_cast<uint32_t>(slot[i])) << 32) |
+                                  static_cast<uint32_t>(i);
     }
 }
 
-// deterministic within-cell order: ascending slot (== engine.hpp:151-163 stability
-// when slot is the storage index)
+// deterministic within-cell order: ascending slot (== engine.hpp:151-163 stability when
+// slot is the storage index); the entries hold their slots, so the insertion sort makes
+// no dependent loads
 __global__ void k_cellsort(const GridParams* __restrict__ gp, const int64_t* __restrict__ cell_start,
-                           const int32_t* __restrict__ slot, int32_t* __restrict__ perm) {
+                           unsigned long long* __restrict__ perm) {
     const int64_t ncells = gp->ncells;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncells;
          c += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = cell_start[c], e = cell_start[c + 1];
         if (e - b < 2) continue;
         for (int64_t q = b + 1; q < e; ++q) {
-            const int32_t v = perm[q];
-            const int32_t sv = slot[v];
+            const unsigned long long v = perm[q];
             int64_t k = q - 1;
-            while (k >= b && slot[perm[k]] > sv) {
-                perm[k + 1] = perm[k];
+            unsigned long long w;
+            while (k >= b && (w = perm[k]) > v) {
+                perm[k + 1] = w;
                 --k;
             }
             perm[k + 1] = v;
@@ -396,11 +380,11 @@ __global__ void k_cellsort(const GridParams* __restrict__ gp, const int64_t* __r
 }
 
 template <int D>
-__global__ void k_gather(int64_t n, const int32_t* __restrict__ perm, const uint32_t* __restrict__ key,
+__global__ void k_gather(int64_t n, const unsigned long long* __restrict__ perm, const uint32_t* __restrict__ key,
                          State T, State S, uint32_t* __restrict__ skey) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t src = perm[q];
+        const int32_t src = static_cast<int32_t>(perm[q] & 0xffffffffull);
         const double4 v = T.rec[src];
         S.rec[q] = v;
         double rb = v.w;
@@ -957,16 +941,21 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
                                            const RoundParams& rp, const int64_t* __restrict__ cs,
                                            const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
                                            double* p) {
-    propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+    // the row and the first three neighbours' live records are loaded before the
+    // proposal is computed, so the Philox arithmetic runs while they are in flight (the
+    // neighbours cannot move during q's visit: they belong to other classes, or to q's
+    // cell and were visited by this lane before q)
     const int32_t* row = nbr + q * kNearRow;
     const int4 h0 = *reinterpret_cast<const int4*>(row);  // (n, e0, e1, e2)
     const int nn = h0.x;
+    double4 v[3];
     if (nn <= kNearCap) {
-        // the first three neighbours: every record load issued before any test
-        double4 v[3];
         if (nn > 0) v[0] = S.rec[h0.y];
         if (nn > 1) v[1] = S.rec[h0.z];
         if (nn > 2) v[2] = S.rec[h0.w];
+    }
+    propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+    if (nn <= kNearCap) {
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
             if (u < nn) {
