@@ -295,31 +295,45 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const uint32_t* __
     }
     if (lane == 31) warp_tot[wid] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (wid == 0) {  // warp 0: publish the aggregate, look back 32 tiles at a time
         unsigned long long total = 0;
+#pragma unroll
         for (int w = 0; w < kLbThreads / 32; ++w) {
             const unsigned long long x = warp_tot[w];
-            warp_tot[w] = total;
+            __syncwarp();
+            if (lane == 0) warp_tot[w] = total;
             total += x;
         }
         volatile unsigned long long* st = status + 1;
         unsigned long long excl = 0;
         if (tile == 0) {
-            st[0] = kLbPrefix | total;
+            if (lane == 0) st[0] = kLbPrefix | total;
         } else {
-            st[tile] = kLbAgg | total;
-            for (int64_t j = tile - 1; j >= 0; --j) {
-                unsigned long long w;
-                do {
-                    w = st[j];
-                } while ((w & ~kLbMask) == 0);
-                excl += w & kLbMask;
-                if ((w & ~kLbMask) == kLbPrefix) break;
+            if (lane == 0) st[tile] = kLbAgg | total;
+            int64_t j0 = tile - 1;  // window [j0 - 31, j0], lane l reads tile j0 - l
+            for (;;) {
+                const int64_t j = j0 - lane;
+                unsigned long long w = kLbPrefix;  // (before tile 0: an empty prefix)
+                if (j >= 0) {
+                    do {
+                        w = st[j];
+                    } while ((w & ~kLbMask) == 0);
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, (w & ~kLbMask) == kLbPrefix);
+                const int stop = pm ? __ffs(pm) - 1 : 32;  // the nearest prefix in the window
+                unsigned long long v = lane <= stop && j >= 0 ? (w & kLbMask) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                excl += __shfl_sync(0xffffffffu, v, 0);
+                if (pm) break;
+                j0 -= 32;
             }
-            st[tile] = kLbPrefix | (excl + total);
+            if (lane == 0) st[tile] = kLbPrefix | (excl + total);
         }
-        excl_s = excl;
-        if (tile == ntiles - 1) cell_start[ncells] = static_cast<int64_t>(excl + total);
+        if (lane == 0) {
+            excl_s = excl;
+            if (tile == ntiles - 1) cell_start[ncells] = static_cast<int64_t>(excl + total);
+        }
     }
     __syncthreads();
     unsigned long long run = excl_s + warp_tot[wid] + incl - t;
