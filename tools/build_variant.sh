@@ -10,5 +10,5 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++
   -Xcompiler -fPIC,-ffp-contract=off --expt-relaxed-constexpr -Xptxas -v "$@" \
   -c paper_2605_18254_b200/csrc/srm_capi.cu -o exp/capi_$name.o 2> exp/ptxas_$name.log
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o exp/libsrm_b200_$name.so exp/capi_$name.o \
-  paper_2605_18254_b200/csrc/srm_selftest.o paper_2605_18254_b200/csrc/srm_rsa.o -lcudart
+  paper_2605_18254_b200/csrc/srm_selftest.o paper_2605_18254_b200/csrc/srm_rsa.o paper_2605_18254_b200/csrc/srm_snapshot.o -lcudart
 grep -A2 k_near_tiles exp/ptxas_$name.log | grep -E "Used|spill" | head -2 | sed "s/^/$name: /"
