@@ -397,8 +397,10 @@ struct srm_b200_ctx {
                     k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
                 else if (platelets())
-                    k_sweep_warpq<3, true><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr,
-                                                                               acc, active, stats);
+                    k_sweep_pl_team<<<static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+                                          blocks_for(cells * kPlTeam, kSweepThreads), 148 * 32))),
+                                      kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
+                                                                  active, stats);
                 else
                     k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
                                                                          active, stats);
@@ -553,7 +555,7 @@ struct srm_b200_ctx {
                             k_sweep_warpq<2><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
                                                                                        skey, nbr, acc, active, stats);
                         else if (platelets())
-                            k_sweep_warpq<3, true><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp,
+                            k_sweep_pl_team<<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp,
                                                                                              cell_start, skey, nbr, acc, active,
                                                                                              stats);
                         else

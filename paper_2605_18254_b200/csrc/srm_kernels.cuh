@@ -508,7 +508,8 @@ struct NearList {
 // x cells of each row are pruned by the chord of the (inflated) cutoff sphere.
 template <int D, typename F>
 __device__ __forceinline__ void near_candidates(const GridParams& g, const int64_t* __restrict__ cs,
-                                                const float4* __restrict__ xf, int64_t q, uint32_t key, F&& visit) {
+                                                const float4* __restrict__ xf, int64_t q, uint32_t key, F&& visit,
+                                                int j0 = 0, int js = 1) {
     const float4 me = xf[q];
     const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
     int cc_[3];
@@ -538,8 +539,8 @@ __device__ __forceinline__ void near_candidates(const GridParams& g, const int64
             if (dyz2 > cut2) continue;
             const int y = yy < 0 ? yy + dy : (yy >= dy ? yy - dy : yy);
             const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
-            auto run = [&](int64_t b, int64_t e) {
-                for (int64_t j = b; j < e; ++j) {
+            auto run = [&](int64_t b, int64_t e) {  // (a team lane takes every js-th candidate from j0)
+                for (int64_t j = b + j0; j < e; j += js) {
                     const float4 c = xf[j];
                     float ex = c.x - me.x, ey = c.y - me.y, ez = D == 3 ? c.z - me.z : 0.f;
                     if (ex > g.half_f[0]) ex -= g.L_f[0]; else if (ex < -g.half_f[0]) ex += g.L_f[0];
@@ -1172,6 +1173,99 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                     valid = false;
                 }
             }
+        }
+    }
+}
+
+// The platelet class sweep with a team of kPlTeam lanes per particle.  The exact
+// disk-disk test (spherodisk.cpp) dominates a platelet trial and a class holds few cells
+// (27 classes of ~1700 cells at cfg 5), so one lane per cell leaves the GPU idle: here a
+// team walks its share of the class's cells in order, and for each trial the team's
+// lanes split q's candidates (the near list, or the rescanned stencil) and vote with a
+// ballot.  Every lane computes the same proposal, and "no candidate overlaps" does not
+// depend on who tests what, so the decisions are those of k_sweep_warpq<3, true> and of
+// the oracle's orc_pl_sweep_round.
+#ifndef SRM_PL_TEAM
+#define SRM_PL_TEAM 32
+#endif
+constexpr int kPlTeam = SRM_PL_TEAM;
+
+__global__ void __launch_bounds__(kSweepThreads) k_sweep_pl_team(int cls_arg, const int* __restrict__ cls_dev, State S,
+                                                                 Box box, const GridParams* __restrict__ gp,
+                                                                 const RoundParams* __restrict__ rpp,
+                                                                 const int64_t* __restrict__ cs,
+                                                                 const uint32_t* __restrict__ skey,
+                                                                 const int32_t* __restrict__ nbr,
+                                                                 uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                                                 StatsDev* stats) {
+    const int cls = cls_dev ? *cls_dev : cls_arg;
+    const GridParams& g = *gp;
+    if (cls >= g.ncls) return;
+    const RoundParams rp = *rpp;
+    const int lane = threadIdx.x & 31, tl = lane & (kPlTeam - 1);
+    const unsigned tm = ((1u << kPlTeam) - 1u) << (lane & ~(kPlTeam - 1));
+    int first[3], stride[3], cnt[3];
+    class_lattice(g, cls, first, stride, cnt);
+    const uint32_t cells = static_cast<uint32_t>(cnt[0]) * cnt[1] * cnt[2];
+    const uint32_t nteams = (gridDim.x * blockDim.x) / kPlTeam;
+    const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / kPlTeam;
+    const uint32_t c0 = static_cast<uint32_t>(static_cast<uint64_t>(cells) * team / nteams);
+    const uint32_t c1 = static_cast<uint32_t>(static_cast<uint64_t>(cells) * (team + 1) / nteams);
+    const int cx = cnt[0], cxy = cnt[0] * cnt[1];
+    for (uint32_t t = c0; t < c1; ++t) {
+        const int iz = static_cast<int>(t / cxy), r2 = static_cast<int>(t - static_cast<uint32_t>(iz) * cxy);
+        const int iy = r2 / cx, ix = r2 - iy * cx;
+        const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
+                                 g.dims[0] + first[0] + stride[0] * ix;
+        const int64_t b = cs[cell], e = cs[cell + 1];
+        for (int64_t q = b; q < e; ++q) {
+            const double4 me = S.rec[q], ni = S.aux[q];
+            const int32_t sl = S.slot[q], idq = S.id[q];
+            const int32_t* row = nbr + q * kNearRow;
+            const int nn = row[0];
+            const double xi[3] = {me.x, me.y, me.z};
+            int accepted = -1;
+            double p[3];
+            pl::V3 pn{0.0, 0.0, 0.0};
+            for (int l = 0; l < rp.n_l; ++l) {
+                propose<3>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+                double ax[3];
+                unit_vector<3>(rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), 1, ax);
+                pn = pl::rotate_normal(pl::V3{ni.x, ni.y, ni.z}, pl::V3{ax[0], ax[1], ax[2]}, rp.cos_r, rp.sin_r);
+                bool hit = false;
+                auto test = [&](int64_t j) {
+                    const double4 v = S.rec[j], a = S.aux[j];
+                    const pl::V3 d{min_image1(v.x - p[0], box.L[0], box.half[0]),
+                                   min_image1(v.y - p[1], box.L[1], box.half[1]),
+                                   min_image1(v.z - p[2], box.L[2], box.half[2])};
+                    return pl::spherodisk_overlap(d, pn, me.w, ni.w, pl::V3{a.x, a.y, a.z}, v.w, a.w, c_seed_table);
+                };
+                if (nn <= kNearCap) {
+                    for (int k = tl; k < nn && !hit; k += kPlTeam) hit = test(row[1 + k]);
+                } else {  // crowded neighbourhood: the stencil, split over the team
+                    near_candidates<3>(
+                        g, cs, S.xf, q, skey[q],
+                        [&](int64_t j) {
+                            if (!hit && S.id[j] != idq) hit = test(j);
+                        },
+                        tl, kPlTeam);
+                }
+                if ((__ballot_sync(tm, hit) & tm) == 0u) {
+                    accepted = l;
+                    break;
+                }
+            }
+            if (tl == 0) {
+                if (accepted >= 0) {
+                    S.rec[q] = make_double4(p[0], p[1], p[2], me.w);
+                    S.aux[q] = make_double4(pn.x, pn.y, pn.z, ni.w);
+                    if (rp.write_acc) acc[q] = static_cast<uint8_t>(accepted);
+                } else {
+                    if (rp.write_acc) acc[q] = kNotAccepted;
+                    active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
+                }
+            }
+            __syncwarp(tm);  // the move is visible to the team before the cell's next particle
         }
     }
 }
