@@ -84,6 +84,7 @@ struct srm_b200_ctx {
     unsigned long long* perm64 = nullptr;  // grid build: slot << 32 | source index, cell-sorted
     int32_t* active = nullptr;  // non-mover list of the current round
     int32_t* nbr = nullptr;     // near-list rows (kNearRow int32 per particle)
+    NearPool pool{nullptr, 0};  // near-list overflow pool
     int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_warpq (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
     // 0: shared-memory bricks (3D) / half-stencil pairs, 1: full stencil per particle,
@@ -229,6 +230,8 @@ struct srm_b200_ctx {
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearRow);
+        pool.cap = 8 * cap + 32 * std::min<int64_t>(cap, 2000000);  // crowded (polydisperse, platelet) states
+        pool.e = dalloc<int32_t>(pool.cap);
         SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
         SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         {
@@ -255,7 +258,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(perm64); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(nbr); cudaFree(S.xf); 
+        cudaFree(nbr); cudaFree(pool.e); cudaFree(S.xf); 
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -378,11 +381,11 @@ struct srm_b200_ctx {
             FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
             if (hg.near_kind == 0) {  // shared-memory bricks
-                k_near_tiles<<<hg.ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
+                k_near_tiles<<<hg.ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr, pool, stats);
                 launched(1);
             } else {
-                if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
+                else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                 launched(1);
             }
         }
@@ -394,15 +397,15 @@ struct srm_b200_ctx {
                 // particles are visited in order), at most one wave of resident CTAs
                 const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), queue_ctas)));
                 if (dim == 2)
-                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
+                    k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
                                                                          active, stats);
                 else if (platelets())
                     k_sweep_pl_team<<<static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
                                           blocks_for(cells * kPlTeam, kSweepThreads), 148 * 32))),
-                                      kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
+                                      kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
                                                                   active, stats);
                 else
-                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, acc,
+                    k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
                                                                          active, stats);
             }
             launched(hg.ncls);
@@ -546,21 +549,21 @@ struct srm_b200_ctx {
                     });
                     // one round on Q
                     grid_build(Q, nc_max);
-                    k_near_tiles<<<ntiles_max, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr);
-                    if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
-                    else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr);
+                    k_near_tiles<<<ntiles_max, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr, pool, stats);
+                    if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
+                    else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                     k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
                     capture_into(add_conditional(stream, h_cls, cudaGraphCondTypeWhile), cap_streams[3], [&]() {
                         if (dim == 2)
                             k_sweep_warpq<2><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
-                                                                                       skey, nbr, acc, active, stats);
+                                                                                       skey, nbr, pool.e, acc, active, stats);
                         else if (platelets())
                             k_sweep_pl_team<<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp,
-                                                                                             cell_start, skey, nbr, acc, active,
+                                                                                             cell_start, skey, nbr, pool.e, acc, active,
                                                                                              stats);
                         else
                             k_sweep_warpq<3><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
-                                                                                       skey, nbr, acc, active, stats);
+                                                                                       skey, nbr, pool.e, acc, active, stats);
                         k_gen_cls_next<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
                     });
                     const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));

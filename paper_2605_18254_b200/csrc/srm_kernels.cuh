@@ -210,6 +210,15 @@ struct StatsDev {
     unsigned long long pen_bits;  // max penetration as the bits of a non-negative double
     unsigned long long candidate_pairs;
     unsigned long long active_count;  // non-movers: particles that kept their round-start position
+    unsigned long long pool_top;      // near-list overflow pool: entries taken this round
+};
+
+// Overflow pool of the near lists: a row whose list does not fit (n > kNearCap) keeps
+// its n entries at pool[row[1] ...] (row[1] = -1: the pool was full, the sweep rescans
+// the stencil).  Taken with an atomic bump on StatsDev::pool_top, zeroed every round.
+struct NearPool {
+    int32_t* e;
+    int64_t cap;
 };
 
 __device__ __forceinline__ double near_cut(double ri, double rj, double extra) {
@@ -594,27 +603,42 @@ __device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
 
 // Near list of sorted particle q over its full stencil from global memory (grids that
 // k_near_tiles does not cover, and its crowded bricks).
+// A list longer than the row goes to the overflow pool (a second scan writes it there).
 template <int D>
 __device__ __forceinline__ void near_full_particle(int64_t q, const State& S, const GridParams& g,
                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                   int32_t* __restrict__ nbr) {
+                                                   int32_t* __restrict__ nbr, NearPool pool, StatsDev* stats) {
     NearList nl;
     const int32_t idq = S.id[q];
     near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
         if (S.id[j] == idq) return;  // shape.hpp:544 self-exclusion by id
         nl.add(static_cast<int32_t>(j));
     });
+    if (nl.n > kNearCap) {
+        const int64_t off = static_cast<int64_t>(atomicAdd(&stats->pool_top, static_cast<unsigned long long>(nl.n)));
+        if (off + nl.n <= pool.cap) {
+            int32_t* dst = pool.e + off;
+            int k = 0;
+            near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
+                if (S.id[j] == idq) return;
+                dst[k++] = static_cast<int32_t>(j);
+            });
+            nl.e[0] = static_cast<int32_t>(off);
+        } else {
+            nl.e[0] = -1;
+        }
+    }
     nl.store(nbr + q * kNearRow);
 }
 
 template <int D>
 __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const GridParams* __restrict__ gp,
                                                     const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                    int32_t* __restrict__ nbr) {
+                                                    int32_t* __restrict__ nbr, NearPool pool, StatsDev* stats) {
     const GridParams& g = *gp;
     if (g.near_kind != 2) return;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-        near_full_particle<D>(q, S, g, cs, skey, nbr);
+        near_full_particle<D>(q, S, g, cs, skey, nbr, pool, stats);
 }
 
 // Near lists through shared memory (3D, a one-cell stencil on every axis).  A CTA takes a
@@ -654,10 +678,11 @@ struct RowMap {
     float sy, sz;        // periodic image shift of the row
 };
 
-__global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const GridParams* __restrict__ gp,
+__global__ void __launch_bounds__(kTileThreads, 4) k_near_tiles(State S, const GridParams* __restrict__ gp,
                                                              const int64_t* __restrict__ cs,
                                                              const uint32_t* __restrict__ skey,
-                                                             int32_t* __restrict__ nbr) {
+                                                             int32_t* __restrict__ nbr, NearPool pool,
+                                                             StatsDev* stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // shifted fp32 records of staged slots 2p, 2p + 1, interleaved for f32x2 arithmetic:
     // pxy[p] = (x0, x1, y0, y1), pzw[p] = (z0, z1, w0, w1)
@@ -734,7 +759,8 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
             const int Y = y0 + r % wy, Z = z0 + r / wy;
             const int64_t row = (static_cast<int64_t>(Z) * dy + Y) * dx;
             const int64_t b = cs[row + x0], e = cs[row + x0 + wx];
-            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) near_full_particle<3>(q, S, g, cs, skey, nbr);
+            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x)
+                near_full_particle<3>(q, S, g, cs, skey, nbr, pool, stats);
         }
         return;
     }
@@ -909,8 +935,9 @@ __global__ void __launch_bounds__(kTileThreads) k_near_tiles(State S, const Grid
                     ++m;
                 }
             }
-        } else {
-            m = nn;  // overflow: the sweep rescans
+        } else {  // a longer list (rare at the bench window): the global path, with the pool
+            near_full_particle<3>(qi, S, g, cs, skey, nbr, pool, stats);
+            continue;
         }
         int4* row = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
         row[0] = make_int4(m, e[0], e[1], e[2]);
@@ -955,7 +982,7 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
                                            const State& S, const Box& box, const GridParams& g,
                                            const RoundParams& rp, const int64_t* __restrict__ cs,
                                            const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
-                                           double* p) {
+                                           const int32_t* __restrict__ pool, double* p) {
     // the row and the first three neighbours' live records are loaded before the
     // proposal is computed, so the Philox arithmetic runs while they are in flight (the
     // neighbours cannot move during q's visit: they belong to other classes, or to q's
@@ -980,6 +1007,15 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
         }
         for (int t = 3; t < nn; ++t) {  // the rest of the row (rare at the bench window)
             const double4 w = S.rec[row[1 + t]];
+            const double xl[3] = {w.x, w.y, w.z};
+            if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
+        }
+        return true;
+    }
+    if (h0.y >= 0) {  // the list is in the overflow pool
+        const int32_t* e = pool + h0.y;
+        for (int t = 0; t < nn; ++t) {
+            const double4 w = S.rec[e[t]];
             const double xl[3] = {w.x, w.y, w.z};
             if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
         }
@@ -1062,6 +1098,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                                                                                const int64_t* __restrict__ cs,
                                                                                const uint32_t* __restrict__ skey,
                                                                                const int32_t* __restrict__ nbr,
+                                                                               const int32_t* __restrict__ pool,
                                                                                uint8_t* __restrict__ acc,
                                                                                int32_t* __restrict__ active,
                                                                                StatsDev* stats) {
@@ -1151,7 +1188,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                 clear = trial_clear_pl(iq, isl, il, xi, ni, me.w, S, box, g, rp, cs, skey, nbr, p, &pn);
                 if (clear) S.aux[iq] = make_double4(pn.x, pn.y, pn.z, ni.w);
             } else {
-                clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, p);
+                clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
             }
             bool done = true;
             if (clear) {
@@ -1196,6 +1233,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_pl_team(int cls_arg, co
                                                                  const int64_t* __restrict__ cs,
                                                                  const uint32_t* __restrict__ skey,
                                                                  const int32_t* __restrict__ nbr,
+                                                                 const int32_t* __restrict__ pool,
                                                                  uint8_t* __restrict__ acc, int32_t* __restrict__ active,
                                                                  StatsDev* stats) {
     const int cls = cls_dev ? *cls_dev : cls_arg;
@@ -1242,7 +1280,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_pl_team(int cls_arg, co
                 };
                 if (nn <= kNearCap) {
                     for (int k = tl; k < nn && !hit; k += kPlTeam) hit = test(row[1 + k]);
-                } else {  // crowded neighbourhood: the stencil, split over the team
+                } else if (row[1] >= 0) {  // the list is in the overflow pool
+                    const int32_t* e = pool + row[1];
+                    for (int k = tl; k < nn && !hit; k += kPlTeam) hit = test(e[k]);
+                } else {  // crowded neighbourhood, pool full: the stencil, split over the team
                     near_candidates<3>(
                         g, cs, S.xf, q, skey[q],
                         [&](int64_t j) {
