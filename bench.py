@@ -60,6 +60,7 @@ N_K = 10          # rounds per iteration / shake sweeps (srmgen.cpp:407-410)
 N_L = 10          # attempts per particle per round
 C_W = 0.02        # SrmParams default swelling rate (engine.hpp:23)
 SAMPLE_N = 100_000  # CPU sample size (same density, radius and c_m as the workload)
+DEVICE_RSA = False  # --device-rsa: the start state from the device RSA instead of the host's
 BYTES_STEP = {2: 40, 3: 56, "platelet": 112}  # algorithmic HBM bytes per particle-update, migrate step (§8d)
 
 
@@ -347,11 +348,14 @@ def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
         else:
             Lb = [box] * dim
             r0 = np.full(n, radius_for(cfg["f0"], cfg["n"], dim))
-            pos, ids = srm.rsa_place(r0, Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
+            pos, ids = (None, None) if DEVICE_RSA else srm.rsa_place(r0, Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
             c_m = cfg["cm_rel"] * radius_for(cfg["f_target"], cfg["n"], dim)
-        t_rsa = time.time() - t0
         ctx = srm.Context(Lb, n, device)
-        ctx.upload(pos, r0, ids)
+        if pos is None:  # --device-rsa: srm_b200_rsa_device
+            ctx.rsa_device(r0, seed)
+        else:
+            ctx.upload(pos, r0, ids)
+        t_rsa = time.time() - t0
         params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, n_k=N_K, n_l=N_L, f_target=F_WINDOW * cfg["f_target"],
                                max_iterations=cfg.get("prep_iters", 100000), seed=seed + 1, reorder_period=16)
     t0 = time.time()
@@ -515,7 +519,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--device-rsa", action="store_true",
+                    help="monodisperse starts from the device RSA (statistically equal, not bit-identical, to the "
+                         "reference's rsa_place)")
     args = ap.parse_args()
+    global DEVICE_RSA
+    DEVICE_RSA = args.device_rsa
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     cfg = CONFIGS[args.config]
     world, rank, local, pg = dist_setup()

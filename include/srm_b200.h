@@ -253,6 +253,15 @@ int srm_b200_rsa_platelets(int64_t n, double diameter, double aspect_ratio, cons
 int srm_b200_rsa_clustered(int dim, const double* box_lengths, int64_t n, const double* radii,
                            int64_t n_clusters, double sigma, int64_t max_attempts, uint64_t seed,
                            double* pos_out, int32_t* id_out, int64_t* placed_out);
+/* Random sequential adsorption on the device: rounds in which every
+ * unplaced particle draws a Philox candidate (seed, index, round), accepted iff strictly
+ * non-touching (rsa.hpp's predicate) every particle placed earlier and every accepted
+ * lower-index candidate of the round -- the sequential RSA that visits each round's
+ * unplaced particles in index order (oracle orc_rsa_rounds, bit for bit).  The state
+ * (id = index) is left in the context.  OK, or PLACEMENT_FAILURE after max_rounds
+ * (placed_out / rounds_out report), INVALID. */
+int srm_b200_rsa_device(srm_b200_ctx* ctx, int64_t n, const double* radii, uint64_t seed, int64_t max_rounds,
+                        int64_t* placed_out, int64_t* rounds_out);
 /* random.hpp:84-89 mix_seed */
 uint64_t srm_b200_mix_seed(uint64_t seed, uint64_t stream);
 

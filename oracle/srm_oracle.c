@@ -694,3 +694,52 @@ int64_t orc_pl_overlap_pairs(const double* L, int64_t n, const double* x, const 
     csr_free(&nb);
     return pairs;
 }
+
+/* ---- parallel RSA ------------------------------------------------------------------- */
+/* DESIGN.md §3.5.  The sequential restatement of the device's rounds: within a round the
+ * device accepts a candidate iff it clears the particles placed before the round and no
+ * lower-index candidate of the round that was itself accepted overlaps it -- which is
+ * exactly this loop in ascending index. */
+void orc_rsa_candidate(int dim, const double* L, uint64_t seed, uint32_t i, uint32_t r, double* out) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t o0[4], o1[4];
+    const uint32_t c0[4] = {i, r, 0xFFFFFFFFu, 0u}, c1[4] = {i, r, 0xFFFFFFFFu, 1u};
+    orc_philox4x32_10(c0, key, o0);
+    orc_philox4x32_10(c1, key, o1);
+    const uint64_t w[3] = {(((uint64_t)o0[0] << 32) | o0[1]) >> 11, (((uint64_t)o0[2] << 32) | o0[3]) >> 11,
+                           (((uint64_t)o1[0] << 32) | o1[1]) >> 11};
+    for (int a = 0; a < dim; ++a) {
+        double p = (double)w[a] * 0x1p-53 * L[a];
+        if (p < 0.0) p += L[a];
+        if (p >= L[a]) p -= L[a];
+        out[a] = p;
+    }
+}
+
+int64_t orc_rsa_rounds(int dim, const double* L, int64_t n, const double* radii, uint64_t seed, int64_t max_rounds,
+                       double* pos, uint8_t* placed, int64_t* rounds_out) {
+    int64_t count = 0, r = 0;
+    int64_t* list = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) placed[i] = 0;
+    for (r = 0; r < max_rounds && count < n; ++r) {
+        for (int64_t i = 0; i < n; ++i) {
+            if (placed[i]) continue;
+            double c[3] = {0.0, 0.0, 0.0};
+            orc_rsa_candidate(dim, L, seed, (uint32_t)i, (uint32_t)r, c);
+            int hit = 0;
+            for (int64_t k = 0; k < count && !hit; ++k) {
+                const int64_t j = list[k];
+                const double rr = radii[i] + radii[j];
+                hit = orc_min_image_dist2(dim, L, c, pos + j * dim) <= rr * rr;
+            }
+            if (!hit) {
+                for (int a = 0; a < dim; ++a) pos[i * dim + a] = c[a];
+                placed[i] = 1;
+                list[count++] = i;
+            }
+        }
+    }
+    free(list);
+    if (rounds_out) *rounds_out = r;
+    return count;
+}

@@ -108,6 +108,19 @@ void orc_pl_sweep_round(const double* L, int64_t n, const double* x0, const doub
 int64_t orc_pl_overlap_pairs(const double* L, int64_t n, const double* x, const double* nrm, const double* D,
                              const double* t, const int32_t* id);
 
+/* ---- parallel RSA (the device initial-state generator) ------------ */
+/* Candidate of particle i in RSA round r: uniforms from Philox4x32-10 with key = seed and
+ * counters (i, r, 0xFFFFFFFF, 0) and (i, r, 0xFFFFFFFF, 1), 53 bits each, times L, wrapped
+ * (random_point, random.hpp:56-61, with Philox instead of mt19937_64). */
+void orc_rsa_candidate(int dim, const double* L, uint64_t seed, uint32_t i, uint32_t r, double* out);
+/* Rounds r = 0, 1, ...: every unplaced particle draws its round-r candidate; in ascending
+ * index, a candidate is accepted iff it is strictly non-touching every particle placed in
+ * an earlier round or earlier in this round (rsa.hpp:45-55's predicate).  Stops when all
+ * are placed or after max_rounds.  pos[i] = particle i's position (placed ones); returns
+ * the number placed. */
+int64_t orc_rsa_rounds(int dim, const double* L, int64_t n, const double* radii, uint64_t seed, int64_t max_rounds,
+                       double* pos, uint8_t* placed, int64_t* rounds_out);
+
 /* ---- reductions ---------------------------------------------------------------- */
 double orc_max_radius(int64_t n, const double* r);
 /* volume fraction with the reference's sequential summation order (shape.hpp:557-563) */

@@ -399,6 +399,20 @@ class Context:
         _check_io(st)
         self.n = int(_native.lib().srm_b200_count(self._h))
 
+    def rsa_device(self, radii, seed: int, max_rounds: int = 100000):
+        """Random sequential adsorption on the device into this context
+        (id = index).  Returns the number of rounds; raises PlacementFailure."""
+        radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+        placed, rounds = C.c_int64(), C.c_int64()
+        st = _native.lib().srm_b200_rsa_device(self._h, len(radii), _ptr(radii), seed & 0xFFFFFFFFFFFFFFFF,
+                                               int(max_rounds), C.byref(placed), C.byref(rounds))
+        if st == PLACEMENT_FAILURE:
+            raise PlacementFailure(f"rsa_device: {placed.value} of {len(radii)} placed after {rounds.value} rounds",
+                                   placed.value, int(max_rounds))
+        self._c(st)
+        self.n = len(radii)
+        return rounds.value
+
     def nearest_neighbor_distances(self) -> np.ndarray:
         """descriptors.hpp:96-115 on the device (download order)."""
         out = np.empty(max(self.n, 1))

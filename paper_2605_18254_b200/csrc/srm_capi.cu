@@ -16,6 +16,7 @@
 
 #include "../../include/srm_b200.h"
 #include "srm_descriptors.cuh"
+#include "srm_rsa_device.cuh"
 #include "srm_kernels.cuh"
 
 using namespace srmb;
@@ -1037,6 +1038,76 @@ int srm_b200_nnd_histogram(srm_b200_ctx* c, int bins, double lo, double hi, int6
             SRM_CUDA(cudaMemcpyAsync(nnd_out, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         SRM_CUDA(cudaStreamSynchronize(c->stream));
         return SRM_B200_OK;
+    });
+}
+
+int srm_b200_rsa_device(srm_b200_ctx* c, int64_t n, const double* radii, uint64_t seed, int64_t max_rounds,
+                        int64_t* placed_out, int64_t* rounds_out) {
+    if (placed_out) *placed_out = 0;
+    if (rounds_out) *rounds_out = 0;
+    if (!c) return SRM_B200_INVALID;
+    return guarded(c, [&]() -> int {
+        if (c->platelets()) throw Invalid{"rsa_device: spheres and disks only"};
+        if (n < 1 || n > c->cap || !radii) throw Invalid{"rsa_device: need 1 <= n <= capacity radii"};
+        double max_r = 0.0, min_len = c->box.L[0];
+        for (int64_t i = 0; i < n; ++i) {
+            if (!(radii[i] > 0.0)) throw Invalid{"rsa_device: radii must be positive"};  // rsa.hpp:26-27
+            max_r = std::max(max_r, radii[i]);
+        }
+        for (int a = 1; a < c->dim; ++a) min_len = std::min(min_len, c->box.L[a]);
+        if (!(max_r < min_len / 4.0)) throw Invalid{"rsa_device: radius too large for the box"};  // rsa.hpp:28-29
+        {
+            std::vector<double> zero(static_cast<size_t>(n) * c->dim, 0.0);
+            std::vector<int32_t> ids(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) ids[i] = static_cast<int32_t>(i);
+            const int st = srm_b200_upload(c, n, zero.data(), radii, ids.data());
+            if (st != SRM_B200_OK) return st;
+        }
+        // cells of at least 2 max_r: every overlapping pair is in the one-cell stencil
+        c->set_grid(c->make_grid(2.0 * max_r * (1.0 + 1e-8), max_r, 0.0));
+        DevBuf<uint8_t> placed(n);
+        DevBuf<int8_t> state(n);
+        DevBuf<int32_t> conf(n * kRsaConf), nconf(n);
+        DevBuf<int64_t> where(n);
+        DevBuf<unsigned long long> count(1);
+        DevBuf<int> flag(1);
+        SRM_CUDA(cudaMemsetAsync(placed.p, 0, static_cast<size_t>(n), c->stream));
+        SRM_CUDA(cudaMemsetAsync(count.p, 0, sizeof(unsigned long long), c->stream));
+        const int nb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 16));
+        const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+        unsigned long long done = 0;
+        int64_t r = 0;
+        for (; r < max_rounds && static_cast<int64_t>(done) < n; ++r) {
+            k_rsa_propose<<<nb, 256, 0, c->stream>>>(n, c->dim, c->P.rec, placed.p, c->box, k0, k1, static_cast<uint32_t>(r));
+            c->grid_build(c->P);
+            if (c->dim == 2)
+                k_rsa_check<2><<<nb, 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, placed.p,
+                                                          state.p, conf.p, nconf.p, where.p);
+            else
+                k_rsa_check<3><<<nb, 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, placed.p,
+                                                          state.p, conf.p, nconf.p, where.p);
+            c->launched(2);
+            int h = 1;
+            while (h > 0) {  // the resolution reaches its fixed point in a few sweeps
+                SRM_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
+                if (c->dim == 2)
+                    k_rsa_resolve<2><<<nb, 256, 0, c->stream>>>(n, placed.p, state.p, conf.p, nconf.p, flag.p, c->S,
+                                                                c->box, c->gp, c->cell_start, c->skey, where.p);
+                else
+                    k_rsa_resolve<3><<<nb, 256, 0, c->stream>>>(n, placed.p, state.p, conf.p, nconf.p, flag.p, c->S,
+                                                                c->box, c->gp, c->cell_start, c->skey, where.p);
+                c->launched();
+                SRM_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                SRM_CUDA(cudaStreamSynchronize(c->stream));
+            }
+            k_rsa_commit<<<nb, 256, 0, c->stream>>>(n, placed.p, state.p, count.p);
+            c->launched();
+            SRM_CUDA(cudaMemcpyAsync(&done, count.p, sizeof(done), cudaMemcpyDeviceToHost, c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        if (placed_out) *placed_out = static_cast<int64_t>(done);
+        if (rounds_out) *rounds_out = r;
+        return static_cast<int64_t>(done) == n ? SRM_B200_OK : SRM_B200_PLACEMENT_FAILURE;
     });
 }
 

@@ -381,3 +381,17 @@ def r_rsa_platelets(n, diameter, aspect, L, max_attempts, seed):
     ids = np.zeros(n, np.int32)
     st = ref().ref_rsa_platelets(n, diameter, aspect, P(arr(L)), max_attempts, seed, P(pos), P(nrm), P(ids))
     return st, pos, nrm, ids
+
+
+def o_rsa_rounds(dim, L, radii, seed, max_rounds):
+    """oracle/srm_oracle.c orc_rsa_rounds: (placed count, rounds, pos, placed flags)"""
+    radii = arr(radii)
+    n = len(radii)
+    pos = np.zeros((n, dim))
+    placed = np.zeros(n, np.uint8)
+    rounds = C.c_int64()
+    f = orc().orc_rsa_rounds
+    f.restype = C.c_int64
+    cnt = f(dim, P(arr(L)), n, P(radii), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), int(max_rounds), P(pos), P(placed),
+            C.byref(rounds))
+    return cnt, rounds.value, pos, placed
