@@ -1024,42 +1024,6 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     return trial_clear_rescan<D>(q, p, ri, S, box, g, cs, skey);
 }
 
-// Platelet version of trial_clear: trial l of q = translation by c_m along the unit
-// vector of Philox stream 0 and rotation of the normal by c_r about the unit vector of
-// stream 1 (spherodisk.hpp:84-91); tested as overlap(trial, other) against the live
-// (centre, normal, diameter, thickness) of q's near list.
-__device__ __forceinline__ bool trial_clear_pl(int64_t q, int32_t sl, int l, const double* xi, const double4 ni,
-                                               double Di, const State& S, const Box& box, const GridParams& g,
-                                               const RoundParams& rp, const int64_t* __restrict__ cs,
-                                               const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
-                                               double* p, pl::V3* pn) {
-    propose<3>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
-    double ax[3];
-    unit_vector<3>(rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), 1, ax);
-    *pn = pl::rotate_normal(pl::V3{ni.x, ni.y, ni.z}, pl::V3{ax[0], ax[1], ax[2]}, rp.cos_r, rp.sin_r);
-    const double ti = ni.w;
-    auto hit = [&](int64_t j) {
-        const double4 v = S.rec[j], a = S.aux[j];
-        const pl::V3 d{min_image1(v.x - p[0], box.L[0], box.half[0]), min_image1(v.y - p[1], box.L[1], box.half[1]),
-                       min_image1(v.z - p[2], box.L[2], box.half[2])};
-        return pl::spherodisk_overlap(d, *pn, Di, ti, pl::V3{a.x, a.y, a.z}, v.w, a.w, c_seed_table);
-    };
-    const int32_t* row = nbr + q * kNearRow;
-    const int nn = row[0];
-    if (nn <= kNearCap) {
-        for (int t = 0; t < nn; ++t)
-            if (hit(row[1 + t])) return false;
-        return true;
-    }
-    const int32_t idq = S.id[q];  // crowded neighbourhood: rescan (same candidates, id filter)
-    bool ok = true;
-    near_candidates<3>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
-        if (!ok || S.id[j] == idq) return;
-        if (hit(j)) ok = false;
-    });
-    return ok;
-}
-
 // The cells of colour class cls form a lattice per axis: first + stride * i, i < cnt
 // (colour1 inverted: a body colour v < m is x = v + m i, a remainder colour one cell).
 __device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int* first, int* stride, int* cnt) {
@@ -1090,7 +1054,7 @@ __device__ __forceinline__ void class_lattice(const GridParams& g, int cls, int*
 // cell_start loads overlap the trials in flight.  No barriers and no work lists: warps
 // progress independently.  Per cell the visiting order and the trials are those of the
 // sequential sweep (orc_sweep_round).
-template <int D, bool PL = false>
+template <int D>
 __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(int cls_arg, const int* __restrict__ cls_dev,
                                                                                State S, Box box,
                                                                                const GridParams* __restrict__ gp,
@@ -1181,15 +1145,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
             const double4 me = S.rec[iq];  // round-start record (the particle has not moved)
             double xi[D], p[D];
             rec_pos<D>(me, xi);
-            bool clear;
-            if constexpr (PL) {  // platelets: the normal turns too
-                const double4 ni = S.aux[iq];
-                pl::V3 pn;
-                clear = trial_clear_pl(iq, isl, il, xi, ni, me.w, S, box, g, rp, cs, skey, nbr, p, &pn);
-                if (clear) S.aux[iq] = make_double4(pn.x, pn.y, pn.z, ni.w);
-            } else {
-                clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
-            }
+            const bool clear = trial_clear<D>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
             bool done = true;
             if (clear) {
                 S.rec[iq] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
@@ -1220,8 +1176,8 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
 // team walks its share of the class's cells in order, and for each trial the team's
 // lanes split q's candidates (the near list, or the rescanned stencil) and vote with a
 // ballot.  Every lane computes the same proposal, and "no candidate overlaps" does not
-// depend on who tests what, so the decisions are those of k_sweep_warpq<3, true> and of
-// the oracle's orc_pl_sweep_round.
+// depend on who tests what, so the decisions are those of the sequential sweep, the
+// oracle's orc_pl_sweep_round.
 #ifndef SRM_PL_TEAM
 #define SRM_PL_TEAM 32
 #endif
