@@ -1470,29 +1470,68 @@ __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const Gri
     const GridParams& g = *gp;
     unsigned long long pairs = 0;
     double pen = 0.0;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = active[k];
-        double xi[D];
-        const double4 vi = S.rec[i];
-        rec_pos<D>(vi, xi);
-        const double ri = vi.w;
-        const int32_t idi = S.id[i];
-        for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
-            for (int64_t j = b; j < e; ++j) {
-                // movers never overlap anything: pairs with j > i suffice
-                if (j <= i || S.id[j] == idi) continue;
-                double xj[D];
-                const double4 vj = S.rec[j];
-                rec_pos<D>(vj, xj);
-                const double rr = ri + vj.w;
-                const double d2 = dist2<D>(box, xi, xj);
-                if (d2 <= rr * rr) {
-                    ++pairs;
-                    const double pe = rr - sqrt(d2);
-                    pen = pe > pen ? pe : pen;
-                }
+    // the pair test of non-mover i against j > i (movers never overlap anything,
+    // DESIGN.md §3.3)
+    auto pair = [&](int64_t i, const double* xi, double ri, int32_t idi, int64_t j) {
+        if (j <= i || S.id[j] == idi) return;
+        double xj[D];
+        const double4 vj = S.rec[j];
+        rec_pos<D>(vj, xj);
+        const double rr = ri + vj.w;
+        const double d2 = dist2<D>(box, xi, xj);
+        if (d2 <= rr * rr) {
+            ++pairs;
+            const double pe = rr - sqrt(d2);
+            pen = pe > pen ? pe : pen;
+        }
+    };
+    const int sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
+    const int rows = (2 * sy + 1) * (2 * sz + 1);
+    if (g.near_s[0] >= 0 && sy >= 0 && sz >= 0 && rows <= 32) {
+        // a warp per non-mover, a lane per (y, z) row of its stencil: the rows' loads are
+        // independent, so one item costs two memory latencies instead of 2 x rows
+        const int lane = threadIdx.x & 31;
+        const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1, sx = g.near_s[0];
+        for (int64_t k = warp; k < m; k += nwarps) {
+            if (lane >= rows) continue;
+            const int64_t i = active[k];
+            double xi[D];
+            const double4 vi = S.rec[i];
+            rec_pos<D>(vi, xi);
+            const int32_t idi = S.id[i];
+            int c[3];
+            decode_key<D>(g, skey[i], c);
+            int y = c[1] + lane % (2 * sy + 1) - sy, z = D == 3 ? c[2] + lane / (2 * sy + 1) - sz : 0;
+            y = y < 0 ? y + dy : (y >= dy ? y - dy : y);
+            z = z < 0 ? z + dz : (z >= dz ? z - dz : z);
+            const int64_t row = (static_cast<int64_t>(z) * dy + y) * dx;
+            const int lo = c[0] - sx, hi = c[0] + sx;
+            auto run = [&](int64_t b, int64_t e) {
+                for (int64_t j = b; j < e; ++j) pair(i, xi, vi.w, idi, j);
+            };
+            if (lo < 0) {
+                run(cs[row + lo + dx], cs[row + dx]);
+                run(cs[row], cs[row + hi + 1]);
+            } else if (hi >= dx) {
+                run(cs[row + lo], cs[row + dx]);
+                run(cs[row], cs[row + hi - dx + 1]);
+            } else {
+                run(cs[row + lo], cs[row + hi + 1]);
             }
-        });
+        }
+    } else {  // wide stencils: a thread per non-mover
+        for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t i = active[k];
+            double xi[D];
+            const double4 vi = S.rec[i];
+            rec_pos<D>(vi, xi);
+            const int32_t idi = S.id[i];
+            for_near_ranges<D>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+                for (int64_t j = b; j < e; ++j) pair(i, xi, vi.w, idi, j);
+            });
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
