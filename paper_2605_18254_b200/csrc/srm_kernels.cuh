@@ -388,7 +388,26 @@ __global__ void k_cellsort(const GridParams* __restrict__ gp, const int64_t* __r
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncells;
          c += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = cell_start[c], e = cell_start[c + 1];
-        if (e - b < 2) continue;
+        const int64_t cnt = e - b;
+        if (cnt < 2) continue;
+        if (cnt <= 4) {  // the usual cell: loads in flight together, sorted in registers
+            unsigned long long v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = k < cnt ? perm[b + k] : ~0ull;
+#pragma unroll
+            for (int a = 1; a < 4; ++a)
+#pragma unroll
+                for (int k = a; k > 0; --k)
+                    if (v[k] < v[k - 1]) {
+                        const unsigned long long t = v[k];
+                        v[k] = v[k - 1];
+                        v[k - 1] = t;
+                    }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < cnt) perm[b + k] = v[k];
+            continue;
+        }
         for (int64_t q = b + 1; q < e; ++q) {
             const unsigned long long v = perm[q];
             int64_t k = q - 1;
