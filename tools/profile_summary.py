@@ -46,7 +46,11 @@ def full_table(rep):
     res = []
     for r in rows[2:]:
         d = dict(zip(h, r))
-        res.append((d["ID"], d["Kernel Name"].split("(")[0].replace("void ", ""), [d.get(k, "") for k in keys]))
+        try:  # global-load sectors per request (coalescing evidence)
+            spr = f"{float(d['l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum']) / float(d['l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum']):.2f}"
+        except (KeyError, ValueError, ZeroDivisionError):
+            spr = ""
+        res.append((d["ID"], d["Kernel Name"].split("(")[0].replace("void ", ""), [d.get(k, "") for k in keys] + [spr]))
     return keys, res, dict(zip(h, rows[1]))
 
 
@@ -83,7 +87,7 @@ def main(tag, lpath, rep, n, rounds):
     if rep and os.path.exists(rep):
         keys, res, units = full_table(rep)
         short = ["time", "dram rd", "dram wr", "L2 hit %", "SM %", "mem %", "warps active %", "regs",
-                 "threads/inst", "grid", "block"]
+                 "threads/inst", "grid", "block", "ld sectors/req"]
         out = [f"# {tag}: ncu --set full (one launch per kernel, timed rounds)", "",
                "| id | kernel | " + " | ".join(short) + " |", "|" + "---|" * (len(short) + 2)]
         for i, name, v in res:
