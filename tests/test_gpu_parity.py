@@ -268,3 +268,28 @@ def test_records_roundtrip():
     ctx.close()
     assert np.array_equal(out["pos"], pos) and np.array_equal(out["radius"], r)
     assert np.array_equal(out["id"], rec["id"])
+
+
+# ---- the large-grid kernels: shared-memory near-list bricks, the overflow pool ------------
+@pytest.mark.parametrize("n,f,swell,cm_rel,poly,seed", [
+    (40000, 0.25, 1.03, 0.05, False, 11),   # k_near_tiles (>= 18 x 10 x 6 cells, one-cell stencil)
+    (30000, 0.15, 1.05, 0.6, True, 12),     # polydisperse, long reach: crowded rows -> overflow pool
+    (60000, 0.3, 1.0, 0.02, False, 13),     # dense, small steps
+])
+def test_round_bit_exact_large_grids(n, f, swell, cm_rel, poly, seed):
+    L, pos, r, ids = _rsa_state(3, n, f, seed, poly=poly)
+    r = r * swell
+    c_m = cm_rel * r.max()
+    cs = 2.5 * r.max() / swell + c_m
+    with srm.Context(L, n) as ctx:
+        ctx.upload(pos, r, ids)
+        st, acc = ctx.round(cs, c_m, 10, 0xABC + seed, 3, 7)
+        p_d, r_d, id_d = ctx.download()
+        info = ctx.last_round_info()
+    xo, ao = orc.o_round(3, L, pos, r, ids, ids, cs, c_m, 10, 0xABC + seed, 3, 7)
+    assert np.array_equal(acc, ao)
+    assert np.array_equal(p_d, xo)
+    o = orc.o_stats(3, L, xo, r)
+    assert st.overlap_pairs == o.overlap_pairs and st.max_penetration == o.max_penetration
+    if not poly:
+        assert min(info["cells"], 10 ** 9) >= 18 * 10 * 6  # large enough for the bricks
