@@ -967,6 +967,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_near_tiles(State S, const G
 #ifndef SRM_SWEEP_THREADS
 #define SRM_SWEEP_THREADS 64
 #endif
+#ifndef SRM_PREFETCH
+#define SRM_PREFETCH 2  // neighbour records loaded before the proposal is computed (1..3)
+#endif
 #ifndef SRM_SERPENTINE
 #define SRM_SERPENTINE 1
 #endif
@@ -1009,22 +1012,22 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     const int32_t* row = nbr + q * kNearRow;
     const int4 h0 = *reinterpret_cast<const int4*>(row);  // (n, e0, e1, e2)
     const int nn = h0.x;
-    double4 v[3];
+    double4 v[SRM_PREFETCH];
     if (nn <= kNearCap) {
         if (nn > 0) v[0] = S.rec[h0.y];
-        if (nn > 1) v[1] = S.rec[h0.z];
-        if (nn > 2) v[2] = S.rec[h0.w];
+        if (SRM_PREFETCH > 1 && nn > 1) v[SRM_PREFETCH > 1 ? 1 : 0] = S.rec[h0.z];
+        if (SRM_PREFETCH > 2 && nn > 2) v[SRM_PREFETCH > 2 ? 2 : 0] = S.rec[h0.w];
     }
     propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
     if (nn <= kNearCap) {
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
+        for (int u = 0; u < SRM_PREFETCH; ++u) {
             if (u < nn) {
                 const double xl[3] = {v[u].x, v[u].y, v[u].z};
                 if (sphere_overlap<D>(box, p, ri, xl, v[u].w)) return false;
             }
         }
-        for (int t = 3; t < nn; ++t) {  // the rest of the row (rare at the bench window)
+        for (int t = SRM_PREFETCH; t < nn; ++t) {  // the rest of the row (rare at the bench window)
             const double4 w = S.rec[row[1 + t]];
             const double xl[3] = {w.x, w.y, w.z};
             if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
