@@ -968,7 +968,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_near_tiles(State S, const G
 #define SRM_SWEEP_THREADS 64
 #endif
 #ifndef SRM_PREFETCH
-#define SRM_PREFETCH 2  // neighbour records loaded before the proposal is computed (1..3)
+#define SRM_PREFETCH 3  // neighbour records loaded before the proposal is computed (1..3)
 #endif
 #ifndef SRM_SERPENTINE
 #define SRM_SERPENTINE 1
@@ -1096,14 +1096,20 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
     const int lane = threadIdx.x & 31;
     int2* win = win_s + (threadIdx.x & ~31);
     const unsigned lt = (1u << lane) - 1u;
-    int first[3], stride[3], cnt[3];
-    class_lattice(g, cls, first, stride, cnt);
-    const uint32_t cells = static_cast<uint32_t>(cnt[0]) * cnt[1] * cnt[2];
+    // the class lattice (constants of the launch) lives in shared memory, not registers
+    __shared__ int lat_s[9];
+    __shared__ FastDiv fd_s[2];
+    if (threadIdx.x == 0) {
+        class_lattice(g, cls, lat_s, lat_s + 3, lat_s + 6);
+        fd_s[0] = make_fastdiv(static_cast<uint32_t>(lat_s[6]));
+        fd_s[1] = make_fastdiv(static_cast<uint32_t>(lat_s[6] * lat_s[7]));
+    }
+    __syncthreads();
+    const uint32_t cells = static_cast<uint32_t>(lat_s[6]) * lat_s[7] * lat_s[8];
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t next = static_cast<uint32_t>(static_cast<uint64_t>(cells) * w / nwarps);  // [next, stop)
     const uint32_t stop = static_cast<uint32_t>(static_cast<uint64_t>(cells) * (w + 1) / nwarps);
-    const FastDiv fdx = make_fastdiv(static_cast<uint32_t>(cnt[0])), fdxy = make_fastdiv(static_cast<uint32_t>(cnt[0] * cnt[1]));
     // odd classes walk the share backwards: they start where the previous class launch
     // ended, whose records are still in L2 (the order of independent cells is free)
     const uint32_t flip = (SRM_SERPENTINE && (cls & 1)) ? next + stop - 1 : 0;
@@ -1115,11 +1121,12 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
         re = 0;
         if (t < stop) {
             if (flip) t = flip - t;
-            const uint32_t iz = fdiv(t, fdxy);
-            const uint32_t r2 = t - iz * static_cast<uint32_t>(cnt[0] * cnt[1]);
-            const uint32_t iy = fdiv(r2, fdx), ix = r2 - iy * static_cast<uint32_t>(cnt[0]);
-            const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * static_cast<int>(iz)) * g.dims[1] + first[1] +
-                                  stride[1] * static_cast<int>(iy)) * g.dims[0] + first[0] + stride[0] * static_cast<int>(ix);
+            const int cx = lat_s[6];
+            const uint32_t iz = fdiv(t, fd_s[1]);
+            const uint32_t r2 = t - iz * static_cast<uint32_t>(cx * lat_s[7]);
+            const uint32_t iy = fdiv(r2, fd_s[0]), ix = r2 - iy * static_cast<uint32_t>(cx);
+            const int64_t cell = (static_cast<int64_t>(lat_s[2] + lat_s[5] * static_cast<int>(iz)) * g.dims[1] + lat_s[1] +
+                                  lat_s[4] * static_cast<int>(iy)) * g.dims[0] + lat_s[0] + lat_s[3] * static_cast<int>(ix);
             rb = static_cast<int32_t>(cs[cell]);
             re = static_cast<int32_t>(cs[cell + 1]);
         }
