@@ -233,8 +233,12 @@ struct srm_b200_ctx {
         nbr = dalloc<int32_t>(cap * kNearRow);
         pool.cap = 8 * cap + 32 * std::min<int64_t>(cap, 2000000);  // crowded (polydisperse, platelet) states
         pool.e = dalloc<int32_t>(pool.cap);
-        SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTileSmem)));
-        SRM_CUDA(cudaFuncSetAttribute(k_near_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        SRM_CUDA(cudaFuncSetAttribute(tiles::k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(tiles::kTileSmem)));
+        SRM_CUDA(cudaFuncSetAttribute(tiles::k_near_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        SRM_CUDA(cudaFuncSetAttribute(ctiles::k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ctiles::kTileSmem)));
+        SRM_CUDA(cudaFuncSetAttribute(ctiles::k_near_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         {
             int per_sm = 0, sms = 0;
             SRM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_warpq<3>, kSweepThreads, 0));
@@ -279,7 +283,7 @@ struct srm_b200_ctx {
     // moves have length c_m.  The colouring expression is the oracle's orc_colouring.
     GridParams make_grid(double cell_size, double max_r_state, double c_m) const {
         GridParams g{};
-        const int st = grid_params(cell_size, max_r_state, c_m, box, dim, near_mode, &g);
+        const int st = grid_params(cell_size, max_r_state, c_m, box, dim, near_mode, &g, n);
         if (st == 1) throw Invalid{"CellGrid: cell_size must be positive"};
         if (st == 2) throw Invalid{"CellGrid: more than 2^32 cells (radius too small for the box)"};
         for (int a = 0; a < 3; ++a)
@@ -382,7 +386,12 @@ struct srm_b200_ctx {
             FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
             if (hg.near_kind == 0) {  // shared-memory bricks
-                k_near_tiles<<<hg.ntiles, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr, pool, stats);
+                tiles::k_near_tiles<<<hg.ntiles, tiles::kTileThreads, tiles::kTileSmem, stream>>>(S, gp, cell_start, skey,
+                                                                                                 nbr, pool, stats);
+                launched(1);
+            } else if (hg.near_kind == 3) {  // crowded: small bricks, large staging
+                ctiles::k_near_tiles<<<hg.ntiles, ctiles::kTileThreads, ctiles::kTileSmem, stream>>>(
+                    S, gp, cell_start, skey, nbr, pool, stats);
                 launched(1);
             } else {
                 if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
@@ -507,6 +516,7 @@ struct srm_b200_ctx {
         hc.reorder_period = p.reorder_period;
         hc.dim = dim;
         hc.near_mode = near_mode;
+        hc.n = n;
         hc.seed = p.seed;
         hc.cos_r = std::cos(p.c_r);
         hc.sin_r = std::sin(p.c_r);
@@ -521,6 +531,9 @@ struct srm_b200_ctx {
         // of the run may, and its dims are no larger)
         const int ntiles_max = dim == 3 ? ((g0.dims[0] + kTX - 1) / kTX) * ((g0.dims[1] + kTY - 1) / kTY) *
                                               ((g0.dims[2] + kTZ - 1) / kTZ)
+                                        : 1;
+        const int ctiles_max = dim == 3 ? ((g0.dims[0] + kCTX - 1) / kCTX) * ((g0.dims[1] + kCTY - 1) / kCTY) *
+                                              ((g0.dims[2] + kCTZ - 1) / kCTZ)
                                         : 1;
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
@@ -550,7 +563,10 @@ struct srm_b200_ctx {
                     });
                     // one round on Q
                     grid_build(Q, nc_max);
-                    k_near_tiles<<<ntiles_max, kTileThreads, kTileSmem, stream>>>(S, gp, cell_start, skey, nbr, pool, stats);
+                    tiles::k_near_tiles<<<ntiles_max, tiles::kTileThreads, tiles::kTileSmem, stream>>>(
+                        S, gp, cell_start, skey, nbr, pool, stats);
+                    ctiles::k_near_tiles<<<ctiles_max, ctiles::kTileThreads, ctiles::kTileSmem, stream>>>(
+                        S, gp, cell_start, skey, nbr, pool, stats);
                     if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                     else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                     k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls);

@@ -57,7 +57,7 @@ struct GridParams {
     // fp32 prefilter (near_candidates): margin above the fp32 rounding of coordinates
     float margin_f, extra_f, rmax_f;
     float L_f[3], half_f[3], edge_f[3];
-    int32_t near_kind;   // near lists: 0 shared-memory bricks, 2 full stencil from global memory
+    int32_t near_kind;   // near lists: 0 / 3 shared-memory bricks (sparse / crowded), 2 global memory
     int32_t ntiles;      // bricks of k_near_tiles (near_kind 0)
     FastDiv fd_dims[3];  // division by dims[a]
     FastDiv fd_m[3];     // division by col_m[a]
@@ -93,9 +93,11 @@ __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, in
 #ifndef SRM_TILE_Z
 #define SRM_TILE_Z 4
 #endif
-constexpr int kTX = SRM_TILE_X, kTY = SRM_TILE_Y, kTZ = SRM_TILE_Z;  // k_near_tiles brick (cells)
+constexpr int kTX = SRM_TILE_X, kTY = SRM_TILE_Y, kTZ = SRM_TILE_Z;  // tiles::k_near_tiles brick (cells)
+constexpr int kCTX = 4, kCTY = 4, kCTZ = 4, kCTileCap = 4096;         // ctiles::k_near_tiles (crowded)
+constexpr double kCrowded = 1.8;  // mean particles per cell above which the crowded bricks are used
 __host__ __device__ inline int grid_params(double cell_size, double max_r_state, double c_m, const Box& box, int dim,
-                                           int near_mode, GridParams* out) {
+                                           int near_mode, GridParams* out, int64_t n = 0) {
     const double extra = 2.0 * c_m;
     if (!(cell_size > 0.0)) return 1;
     GridParams g{};
@@ -165,10 +167,17 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
         g.half_f[a] = 0.5f * g.L_f[a];
         g.edge_f[a] = static_cast<float>(g.edge[a]);
     }
-    const bool tiles = dim == 3 && near_mode == 0 && g.near_s[0] == 1 && g.near_s[1] == 1 && g.near_s[2] == 1 &&
-                       g.dims[0] >= kTX + 2 && g.dims[1] >= kTY + 2 && g.dims[2] >= kTZ + 2;
-    g.near_kind = tiles ? 0 : 2;
-    g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ) : 0;
+    // near lists: 0 the 16 x 8 x 4 bricks, 3 the crowded 4 x 4 x 4 bricks (mean occupancy
+    // above kCrowded), 2 the per-particle global path
+    const bool one = dim == 3 && near_mode == 0 && g.near_s[0] == 1 && g.near_s[1] == 1 && g.near_s[2] == 1;
+    const bool crowded = static_cast<double>(n) > kCrowded * static_cast<double>(g.ncells);
+    const bool tiles = one && !crowded && g.dims[0] >= kTX + 2 && g.dims[1] >= kTY + 2 && g.dims[2] >= kTZ + 2;
+    const bool ctiles = one && crowded && g.dims[0] >= kCTX + 2 && g.dims[1] >= kCTY + 2 && g.dims[2] >= kCTZ + 2;
+    g.near_kind = tiles ? 0 : (ctiles ? 3 : 2);
+    g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ)
+                     : (ctiles ? ((g.dims[0] + kCTX - 1) / kCTX) * ((g.dims[1] + kCTY - 1) / kCTY) *
+                                     ((g.dims[2] + kCTZ - 1) / kCTZ)
+                               : 0);
     *out = g;
     return 0;
 }
@@ -660,18 +669,13 @@ __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const Gr
         near_full_particle<D>(q, S, g, cs, skey, nbr, pool, stats);
 }
 
-// Near lists through shared memory (3D, a one-cell stencil on every axis).  A CTA takes a
-// brick of kTX x kTY x kTZ cells and stages the fp32 records, sorted indices and ids of
-// the brick and its full one-cell halo (the particles of a row of halo cells are one to
-// three contiguous runs of the sorted state: the periodic images at x = -1 and x >= dims),
-// shifted by +-L on the way in so that pair distances are plain differences.  Every interior particle is then screened against the nine contiguous
-// shared-memory ranges of its 3x3x3 stencil and writes its own row (one sector, no
-// atomics).  Same screen as near_candidates (cutoff, margin, factor), so the lists hold
-// the same pairs as k_near_lists.  A brick whose halo holds more than kTileCap particles
-// takes near_full_particle.
-constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 2;
-constexpr int kHCells = kHX * kHY * kHZ;
-constexpr int kHRows = kHY * kHZ;
+// staged slot -> sorted index of one row of halo cells (k_near_tiles)
+struct RowMap {
+    int64_t sa, sb, sc;  // sorted index - slot in the runs [.., ka), [ka, kc), [kc, ..)
+    int32_t ka, kc;
+    float sy, sz;        // periodic image shift of the row
+};
+
 #ifndef SRM_TILE_THREADS
 #define SRM_TILE_THREADS 256
 #endif
@@ -681,288 +685,40 @@ constexpr int kHRows = kHY * kHZ;
 #ifndef SRM_NEAR_PRUNE
 #define SRM_NEAR_PRUNE 0
 #endif
-constexpr int kTileCap = SRM_TILE_CAP;  // staged particles (2.1 per halo cell at the defaults)
-constexpr int kTileThreads = SRM_TILE_THREADS;
-constexpr int kCellsPerThread = (kHCells + kTileThreads - 1) / kTileThreads;
-constexpr size_t kTileSmem = kTileCap * (16 + 4) + (kHCells + 1) * 4 +
-                             (kHCells * 4 > kTileThreads * (kNearCap + 1) * 2 ? kHCells * 4 : kTileThreads * (kNearCap + 1) * 2);
-static_assert(kTileCap <= 65536, "16-bit hit slots");
-static_assert(kHRows <= kTileThreads && kHRows <= 64, "a thread per halo row; 6-step row search");
-static_assert(kTY * kTZ <= 32 && kTX <= 16, "one warp scans the interior rows; 4-step cell search");
-
-// staged slot -> sorted index of one row of halo cells (k_near_tiles)
-struct RowMap {
-    int64_t sa, sb, sc;  // sorted index - slot in the runs [.., ka), [ka, kc), [kc, ..)
-    int32_t ka, kc;
-    float sy, sz;        // periodic image shift of the row
-};
-
-__global__ void __launch_bounds__(kTileThreads, 4) k_near_tiles(State S, const GridParams* __restrict__ gp,
-                                                             const int64_t* __restrict__ cs,
-                                                             const uint32_t* __restrict__ skey,
-                                                             int32_t* __restrict__ nbr, NearPool pool,
-                                                             StatsDev* stats) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    // shifted fp32 records of staged slots 2p, 2p + 1, interleaved for f32x2 arithmetic:
-    // pxy[p] = (x0, x1, y0, y1), pzw[p] = (z0, z1, w0, w1)
-    float4* pxy = reinterpret_cast<float4*>(smem_raw);             // [kTileCap / 2]
-    float4* pzw = pxy + kTileCap / 2;                               // [kTileCap / 2]
-    int32_t* pj = reinterpret_cast<int32_t*>(pzw + kTileCap / 2);  // [kTileCap] sorted index of a slot
-    int32_t* hoff = pj + kTileCap;                                  // [kHCells + 1] staged offset of a cell
-    int32_t* hsrc = hoff + kHCells + 1;                             // [kHCells] first sorted index of a cell
-    uint16_t* lst = reinterpret_cast<uint16_t*>(hsrc);              // [kNearCap + 1][kTileThreads] hit slots
-                                                                    // (aliases hsrc: used after the staging)
-    __shared__ int wsum[kTileThreads / 32];
-    __shared__ int rowoff[kTY * kTZ + 1];
-    __shared__ RowMap rmap[kHRows];
-    const GridParams& g = *gp;
-    if (g.near_kind != 0 || static_cast<int>(blockIdx.x) >= g.ntiles) return;  // (graph launches: upper bounds)
-    const int dx = g.dims[0], dy = g.dims[1], dz = g.dims[2];
-    const int ntx = (dx + kTX - 1) / kTX, nty = (dy + kTY - 1) / kTY;
-    const int tx = blockIdx.x % ntx, ty = (blockIdx.x / ntx) % nty, tz = blockIdx.x / (ntx * nty);
-    const int x0 = tx * kTX, y0 = ty * kTY, z0 = tz * kTZ;
-    const int wx = min(kTX, dx - x0), wy = min(kTY, dy - y0), wz = min(kTZ, dz - z0);  // interior extent
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // 1. counts of the halo cells (cells outside the halo of a partial brick: 0); a
-    //    thread owns kCellsPerThread consecutive cells
-    int cnts[kCellsPerThread];
-    int local = 0;
-#pragma unroll
-    for (int k = 0; k < kCellsPerThread; ++k) {
-        const int hc = threadIdx.x * kCellsPerThread + k;
-        int c = 0;
-        if (hc < kHCells) {
-            const int hx = hc % kHX, hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
-            if (hx <= wx + 1 && hy <= wy + 1 && hz <= wz + 1) {
-                int X = x0 - 1 + hx, Y = y0 - 1 + hy, Z = z0 - 1 + hz;
-                X = X < 0 ? X + dx : (X >= dx ? X - dx : X);
-                Y = Y < 0 ? Y + dy : (Y >= dy ? Y - dy : Y);
-                Z = Z < 0 ? Z + dz : (Z >= dz ? Z - dz : Z);
-                const int64_t cell = (static_cast<int64_t>(Z) * dy + Y) * dx + X;
-                const int64_t b = cs[cell];
-                c = static_cast<int>(cs[cell + 1] - b);
-                hsrc[hc] = static_cast<int32_t>(b);
-            }
-        }
-        cnts[k] = c;
-        local += c;
-    }
-    // 2. exclusive scan over the halo cells
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    int wbase = 0, total = 0;
-#pragma unroll
-    for (int w = 0; w < kTileThreads / 32; ++w) {
-        if (w < wid) wbase += wsum[w];
-        total += wsum[w];
-    }
-    {
-        int off = wbase + incl - local;
-#pragma unroll
-        for (int k = 0; k < kCellsPerThread; ++k) {
-            const int hc = threadIdx.x * kCellsPerThread + k;
-            if (hc < kHCells) hoff[hc] = off;
-            off += cnts[k];
-        }
-        if (threadIdx.x == 0) hoff[kHCells] = total;
-    }
-    __syncthreads();
-    if (total > kTileCap) {  // crowded brick: the per-particle path over global memory
-        for (int r = 0; r < wy * wz; ++r) {
-            const int Y = y0 + r % wy, Z = z0 + r / wy;
-            const int64_t row = (static_cast<int64_t>(Z) * dy + Y) * dx;
-            const int64_t b = cs[row + x0], e = cs[row + x0 + wx];
-            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x)
-                near_full_particle<3>(q, S, g, cs, skey, nbr, pool, stats);
-        }
-        return;
-    }
-    // 3. stage the halo.  Along x a row of halo cells holds up to three runs of
-    //    consecutive sorted indices: [0, xa) the image of the last column (shift -L),
-    //    [xa, xc) the body, [xc, kHX) the image of the first columns (+L).  A table per
-    //    row (a thread per row) maps a staged slot to its sorted index; then every thread
-    //    copies a strided set of slots, all loads in flight before any store.
-    if (threadIdx.x < kHRows) {
-        const int r = threadIdx.x, hy = r % kHY, hz = r / kHY;
-        const int xa = x0 == 0 ? 1 : 0, xc = min(kHX, dx - x0 + 1);
-        const int h0 = r * kHX;
-        RowMap m;
-        m.ka = hoff[h0 + xa];
-        m.kc = hoff[h0 + xc];
-        const bool used = hy <= wy + 1 && hz <= wz + 1;
-        m.sa = used && xa ? hsrc[h0] - hoff[h0] : 0;
-        m.sb = used && xa < kHX ? hsrc[h0 + xa] - m.ka : 0;
-        m.sc = used && xc < kHX ? hsrc[h0 + xc] - m.kc : 0;
-        const int Y = y0 - 1 + hy, Z = z0 - 1 + hz;
-        m.sy = Y < 0 ? -g.L_f[1] : (Y >= dy ? g.L_f[1] : 0.f);
-        m.sz = Z < 0 ? -g.L_f[2] : (Z >= dz ? g.L_f[2] : 0.f);
-        rmap[r] = m;
-    }
-    __syncthreads();
-    for (int k0 = 0; k0 < total; k0 += 4 * kTileThreads) {
-        float4 v[4];
-        int32_t src[4];
-        float sxf[4], syf[4], szf[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = k0 + threadIdx.x + u * kTileThreads;
-            if (k < total) {
-                int r = 0;  // the last row whose first slot is <= k
-#pragma unroll
-                for (int step = 32; step > 0; step >>= 1)
-                    if (r + step < kHRows && hoff[(r + step) * kHX] <= k) r += step;
-                const RowMap& m = rmap[r];
-                src[u] = static_cast<int32_t>(k + (k < m.ka ? m.sa : (k < m.kc ? m.sb : m.sc)));
-                sxf[u] = k < m.ka ? -g.L_f[0] : (k < m.kc ? 0.f : g.L_f[0]);
-                syf[u] = m.sy;
-                szf[u] = m.sz;
-                v[u] = S.xf[src[u]];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = k0 + threadIdx.x + u * kTileThreads;
-            if (k < total) {
-                float* a = reinterpret_cast<float*>(pxy + (k >> 1)) + (k & 1);
-                float* b = reinterpret_cast<float*>(pzw + (k >> 1)) + (k & 1);
-                a[0] = __fadd_rn(v[u].x, sxf[u]);
-                a[2] = __fadd_rn(v[u].y, syf[u]);
-                b[0] = __fadd_rn(v[u].z, szf[u]);
-                b[2] = v[u].w;
-                pj[k] = src[u];
-            }
-        }
-    }
-    // interior rows (hy in [1, wy], hz in [1, wz]) hold contiguous particles
-    if (wid == 0) {
-        const int nr = wy * wz;  // <= 32
-        int c = 0;
-        if (lane < nr) {
-            const int h0 = ((1 + lane / wy) * kHY + 1 + lane % wy) * kHX + 1;
-            c = hoff[h0 + wx] - hoff[h0];
-        }
-        int in = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, in, o);
-            if (lane >= o) in += t;
-        }
-        if (lane < nr) rowoff[lane] = in - c;
-        if (lane == nr - 1) rowoff[nr] = in;
-    }
-    __syncthreads();
-    // 4. screen every interior particle against its 3x3x3 stencil in shared memory
-    const int nr = wy * wz;
-    const int nint = rowoff[nr];
-    for (int f = threadIdx.x; f < nint; f += blockDim.x) {
-        int r = 0;  // the last interior row whose offset is <= f
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1)
-            if (r + step < nr && rowoff[r + step] <= f) r += step;
-        const int rb = ((1 + r / wy) * kHY + 1 + r % wy) * kHX;
-        const int i = hoff[rb + 1] + (f - rowoff[r]);
-        int hx = 1;  // the cell of i in its row: the last x with hoff <= i
-#pragma unroll
-        for (int step = 8; step > 0; step >>= 1)
-            if (hx + step <= wx && hoff[rb + hx + step] <= i) hx += step;
-        const int hc = rb + hx;
-        const float mx = reinterpret_cast<const float*>(pxy + (i >> 1))[i & 1];
-        const float my = reinterpret_cast<const float*>(pxy + (i >> 1))[2 + (i & 1)];
-        const float mz = reinterpret_cast<const float*>(pzw + (i >> 1))[i & 1];
-        const float mw = reinterpret_cast<const float*>(pzw + (i >> 1))[2 + (i & 1)];
-        const int32_t qi = pj[i];
-        const float base = __fadd_rn(__fadd_rn(mw, g.extra_f), g.margin_f);  // + r_j
-        const float2 nmx = make_float2(-mx, -mx), nmy = make_float2(-my, -my), nmz = make_float2(-mz, -mz);
-        const float2 base2 = make_float2(base, base), fac2 = make_float2(1.00001f, 1.00001f);
-        // hits are rare per lane but common per warp: record the hit slots branch-free
-        // (a store to the current list slot every test, the count advances on a hit; slot
-        // kNearCap absorbs the overflow), resolve them after the scan
-        uint16_t* ql = lst + threadIdx.x;
-        int nn = 0, at = 0;
-        // stencil pruning (conservative: margins above the fp32 rounding of the cell
-        // bounds): a row of three cells is skipped when its slab lies beyond the largest
-        // reach of i, and its end cells when the chord of the reach sphere misses them
-        const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(mw, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
-        const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
-        const int hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
-        const float fx = __fsub_rn(mx, __fmul_rn(static_cast<float>(x0 - 1 + hx), g.edge_f[0]));
-        const float fy = __fsub_rn(my, __fmul_rn(static_cast<float>(y0 - 1 + hy), g.edge_f[1]));
-        const float fz = __fsub_rn(mz, __fmul_rn(static_cast<float>(z0 - 1 + hz), g.edge_f[2]));
-        const float gx = __fsub_rn(g.edge_f[0], fx), gy = __fsub_rn(g.edge_f[1], fy), gz = __fsub_rn(g.edge_f[2], fz);
-#pragma unroll
-        for (int ddz = -1; ddz <= 1; ++ddz) {
-#pragma unroll
-            for (int ddy = -1; ddy <= 1; ++ddy) {
-                const int c = hc + ddy * kHX + ddz * kHX * kHY;
-#if SRM_NEAR_PRUNE
-                const float dyd = fmaxf(0.f, __fsub_rn(ddy < 0 ? fy : (ddy > 0 ? gy : 0.f), g.margin_f));
-                const float dzd = fmaxf(0.f, __fsub_rn(ddz < 0 ? fz : (ddz > 0 ? gz : 0.f), g.margin_f));
-                const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
-                if (dyz2 > cut2) continue;
-                float h;  // chord half length; sqrt.approx (rel. error < 2^-22) scaled up by 2^-20
-                asm("sqrt.approx.f32 %0, %1;" : "=f"(h) : "f"(__fsub_rn(cut2, dyz2)));
-                h = __fadd_rn(__fmul_rn(h, 1.000001f), __fmul_rn(2.f, g.margin_f));
-                const int kb = hoff[fx < h ? c - 1 : c], ke = hoff[gx < h ? c + 2 : c + 1];
-#else
-                const int kb = hoff[c - 1], ke = hoff[c + 2];
-#endif
-                // slots [kb, ke) two at a time (pairs 2p, 2p + 1; the ends masked)
-                for (int p = kb >> 1; 2 * p < ke; ++p) {
-                    const float4 A = pxy[p], B = pzw[p];
-                    const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
-                    const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
-                    const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
-                    const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
-                    const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
-                    const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
-                    const int k0 = 2 * p;
-                    ql[at * kTileThreads] = static_cast<uint16_t>(k0);
-                    nn += (d2.x <= l2.x && k0 >= kb && k0 != i) ? 1 : 0;
-                    at = min(nn, kNearCap);
-                    ql[at * kTileThreads] = static_cast<uint16_t>(k0 + 1);
-                    nn += (d2.y <= l2.y && k0 + 1 < ke && k0 + 1 != i) ? 1 : 0;
-                    at = min(nn, kNearCap);
-                }
-            }
-        }
-        // resolve: sorted indices, and shape.hpp:544 self-exclusion by id
-        int32_t e[kNearCap];
-        int m = 0;
-        if (nn <= kNearCap) {
-            const int32_t idi = S.id[qi];
-#pragma unroll
-            for (int t = 0; t < kNearCap; ++t) {
-                e[t] = 0;
-                if (t < nn) {
-                    const int32_t j = pj[ql[t * kTileThreads]];
-                    if (S.id[j] != idi) e[t] = j;
-                    else e[t] = -1;
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < kNearCap; ++t) {  // compact out the (rare) same-id entries
-                if (t < nn && e[t] >= 0) {
-#pragma unroll
-                    for (int u = 0; u < kNearCap; ++u)
-                        if (u == m) e[u] = e[t];
-                    ++m;
-                }
-            }
-        } else {  // a longer list (rare at the bench window): the global path, with the pool
-            near_full_particle<3>(qi, S, g, cs, skey, nbr, pool, stats);
-            continue;
-        }
-        int4* row = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
-        row[0] = make_int4(m, e[0], e[1], e[2]);
-        row[1] = make_int4(e[3], e[4], e[5], e[6]);
-    }
-}
+namespace tiles {  // sparse grids (~1-2 particles per cell): 16 x 8 x 4 bricks
+#define NT_X SRM_TILE_X
+#define NT_Y SRM_TILE_Y
+#define NT_Z SRM_TILE_Z
+#define NT_CAP SRM_TILE_CAP
+#define NT_THREADS SRM_TILE_THREADS
+#define NT_MINB 4
+#define NT_KIND 0
+#include "srm_near_tiles.cuh"
+#undef NT_X
+#undef NT_Y
+#undef NT_Z
+#undef NT_CAP
+#undef NT_THREADS
+#undef NT_MINB
+#undef NT_KIND
+}  // namespace tiles
+namespace ctiles {  // crowded grids: 4 x 4 x 4 bricks, 4096 staged particles
+#define NT_X kCTX
+#define NT_Y kCTY
+#define NT_Z kCTZ
+#define NT_CAP kCTileCap
+#define NT_THREADS 256
+#define NT_MINB 2
+#define NT_KIND 3
+#include "srm_near_tiles.cuh"
+#undef NT_X
+#undef NT_Y
+#undef NT_Z
+#undef NT_CAP
+#undef NT_THREADS
+#undef NT_MINB
+#undef NT_KIND
+}  // namespace ctiles
 
 #ifndef SRM_SWEEP_THREADS
 #define SRM_SWEEP_THREADS 64
@@ -1315,6 +1071,7 @@ struct GenCtl {
     // inputs
     double f_target, stop, c_w, c_m, box_measure;
     int64_t max_iter, it0;
+    int64_t n;  // particles (the near-list kernel choice depends on the occupancy)
     int32_t n_k, n_l, reorder_period, dim, near_mode, pad0;
     uint64_t seed;
     double cos_r, sin_r;  // platelet rotation angle (host libm)
@@ -1356,7 +1113,7 @@ __global__ void k_gen_step(GenCtl* c, GridParams* gp, RoundParams* rp, StatsDev*
         c->cs = 2.5 * c->max_r + c->c_m;
         GridParams g{};
         if (c->cs < 2.0 * (c->max_r * factor) + c->c_m ||
-            grid_params(c->cs, c->max_r * factor, c->c_m, box, c->dim, c->near_mode, &g) != 0) {
+            grid_params(c->cs, c->max_r * factor, c->c_m, box, c->dim, c->near_mode, &g, c->n) != 0) {
             c->status = 2;
             c->phase = 3;
             active = false;
@@ -1371,7 +1128,7 @@ __global__ void k_gen_step(GenCtl* c, GridParams* gp, RoundParams* rp, StatsDev*
         }
     } else if (c->phase == 2 && c->k == 0) {  // shake on P with the pre-swell grid (engine.hpp:244-249)
         GridParams g{};
-        grid_params(c->cs, c->max_r, c->c_m, box, c->dim, c->near_mode, &g);
+        grid_params(c->cs, c->max_r, c->c_m, box, c->dim, c->near_mode, &g, c->n);
         *gp = g;
         copy = true;
     }
