@@ -18,6 +18,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 STEP = ("k_near_lists", "k_near_half", "k_near_tiles", "k_near_zero", "k_sweep_cells", "k_sweep_work", "k_sweep_queue",
+        "k_sweep_pl_team",
         "k_sweep_warpq", "k_work_count", "k_work_scan", "k_work_scatter")
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "usecond": 1.0,
         "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}
@@ -72,7 +73,7 @@ def main(tag, lpath, rep, n, rounds):
     step_bytes = 0.0
     for name, a in sorted(agg.items(), key=lambda x: -x[1][1]):
         rd, wr = a[2] / rounds, a[3] / rounds
-        if name.split("<")[0] in STEP:
+        if name.split("<")[0].split("::")[-1] in STEP:
             step_bytes += rd + wr
         lines.append(f"| {name} | {a[0]} | {a[1] / rounds:.1f} | {a[1] / tot:.1%} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | "
                      f"{(rd + wr) / n:.1f} |")
