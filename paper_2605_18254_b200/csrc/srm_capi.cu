@@ -88,8 +88,8 @@ struct srm_b200_ctx {
     NearPool pool{nullptr, 0};  // near-list overflow pool
     int queue_ctas = 148 * 8;  // resident CTAs of k_sweep_warpq (set in init)
     std::vector<int64_t> cls_cells_h;  // cells before each colour class (launch sizes)
-    // 0: shared-memory bricks (3D) / half-stencil pairs, 1: full stencil per particle,
-    // 2: half-stencil pairs per particle
+    // near-list kernel choice (SRM_B200_NEAR): 0 the shared-memory bricks where they apply
+    // (GridParams::near_kind), otherwise the per-particle full stencil
     int near_mode = std::getenv("SRM_B200_NEAR") ? std::atoi(std::getenv("SRM_B200_NEAR")) : 0;
     // srm_generate: the device-resident graph loop (default) or the host-driven loop
     bool device_loop = std::getenv("SRM_B200_HOST_LOOP") == nullptr;
