@@ -196,6 +196,21 @@ int main() {
         build_shape_grid<SpherodiskShape>(grid, res.snapshot.particles);
         CHECK(!srm::shape_any_collision<SpherodiskShape>(std::span<const Spherodisk>(res.snapshot.particles), grid));
         CHECK(!srm::b200::shape_any_collision<SpherodiskShape>(res.snapshot.particles, grid));
+        // migrate and relax_sweeps on platelets keep the state valid (reference test) and
+        // keep unit normals
+        auto ps = res.snapshot.particles;
+        CellGrid<3> g2(box, 2.5 * max_r + 0.05, max_r, 0.05);
+        Rng rng2(3);
+        const auto acc = srm::b200::migrate<SpherodiskShape>(ps, g2, 0.05, 0.05, 10, rng2);
+        std::size_t moved = 0;
+        for (auto v : acc) moved += v;
+        CHECK(moved > 0);
+        srm::b200::relax_sweeps<SpherodiskShape>(ps, box, 0.05, 0.05, 10, 2, rng2);
+        build_shape_grid<SpherodiskShape>(grid, ps);
+        CHECK(!srm::shape_any_collision<SpherodiskShape>(std::span<const Spherodisk>(ps), grid));
+        bool unit = true;
+        for (const auto& q : ps) unit = unit && std::fabs(q.normal.norm() - 1.0) < 1e-12;
+        CHECK(unit);
     }
     std::printf("shim_test: %d/%d checks passed\n", checks - failures, checks);
     return failures == 0 ? 0 : 1;
