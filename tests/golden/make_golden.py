@@ -135,6 +135,52 @@ def e2e_large_case(name, c):
     print(name, out["summary"], out["iterations"])
 
 
+# scaled-down cfg 5: thin platelets (aspect 20), reference rsa_platelets start (D = 1,
+# box 7: rho = 1.17), grown to f = 0.14 (D ~ 1.46) with c_w 0.01, c_m = c_r = 0.05
+PLATE = dict(n=400, L=7.0, aspect=20.0, c_w=0.01, c_m=0.05, c_r=0.05, n_k=10, n_l=10, f_t=0.14,
+             seeds=list(range(1, 17)))
+
+
+def platelet_stats(pos, nrm, D, L):
+    """Per-configuration summaries of a platelet packing: centre NND quantiles in units of
+    D, the nematic order S2 (largest eigenvalue of <(3 n n - 1) / 2>), the mean |n . n'|
+    of nearest-neighbour pairs, and the fraction of centres closer than D / 2."""
+    nnd = orc.r_nnd(3, L, pos) / D
+    q = np.quantile(nnd, [0.1, 0.25, 0.5, 0.75, 0.9])
+    Q = (3.0 * np.einsum("ni,nj->ij", nrm, nrm) / len(nrm) - np.eye(3)) / 2.0
+    s2 = float(np.linalg.eigvalsh(Q)[-1])
+    from scipy.spatial import cKDTree
+    t = cKDTree(pos, boxsize=L[0])
+    _, j = t.query(pos, k=2)
+    align = float(np.abs(np.einsum("ni,ni->n", nrm, nrm[j[:, 1]])).mean())
+    close = float((nnd < 0.5).mean())
+    return np.concatenate([q, [s2, align, close]]), nnd
+
+
+def e2e_platelet_case(name, c):
+    import ctypes as C
+    stats, nnds = [], []
+    L = [c["L"]] * 3
+    for s in c["seeds"]:
+        st, pos, nrm, ids = orc.r_rsa_platelets(c["n"], 1.0, c["aspect"], L, 10000, 100 + s)
+        assert st == 0
+        D = np.full(c["n"], 1.0)
+        th = D / c["aspect"]
+        it = np.zeros(1, np.int64)
+        f = np.zeros(1)
+        P = orc.P
+        rc = orc.ref().ref_generate_platelets(P(orc.arr(L)), c["n"], P(pos), P(nrm), P(D), P(th), P(ids), c["c_w"],
+                                              c["c_m"], c["c_r"], c["n_k"], c["n_l"], c["f_t"], 100000, s, 16,
+                                              P(it), P(f))
+        assert rc == 0, f"reference platelet srm_generate did not converge (seed {s})"
+        row, nnd = platelet_stats(pos, nrm, float(D[0]), L)
+        stats.append(row)
+        nnds.append(nnd)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), stats=np.array(stats), nnd=np.array(nnds),
+                        **{k: np.array(v) for k, v in c.items()})
+    print(name, np.array(stats).mean(0))
+
+
 def grid_case(name, dim, n, rmin, rmax, cs, seed, L):
     pos, r = orc.random_particles(n, dim, rmin, rmax, L, seed)
     keys, _ = orc.r_keys(dim, L, cs, pos)
@@ -159,6 +205,8 @@ def main():
                 e2e_poly_case(name, POLY)
             elif name == "e2e_cfg4_large":
                 e2e_large_case(name, LARGE)
+            elif name == "e2e_platelet":
+                e2e_platelet_case(name, PLATE)
             else:
                 e2e_case(name, E2E[name])
         return
@@ -169,6 +217,7 @@ def main():
     for name, c in E2E.items():
         e2e_case(name, c)
     e2e_poly_case("e2e_poly", POLY)
+    e2e_platelet_case("e2e_platelet", PLATE)
 
 
 if __name__ == "__main__":

@@ -163,3 +163,44 @@ def test_polydisperse_clustered_statistics_match_reference():
     ok, _ = stats_util.hist_agree(np.sum(rdf, axis=0), z["rdf"])
     assert ok.all(), f"pair-count bins out of tolerance: {np.where(~ok)[0]}"
     assert stats_util.ensemble_chi2(rdf, z["rdf_seeds"]) > 1e-3
+
+
+def test_platelet_statistics_match_reference():
+    """Scaled-down cfg 5 (tests/golden/make_golden.py PLATE): thin platelets (aspect 20)
+    from the reference's rsa_platelets starts (bit-identical here), grown to f = 0.14 by
+    the device srm_generate and by the reference's, 16 seeds each; f within 1e-9, no
+    overlap (the reference's own collision test, oracle/_ref); per-seed centre NND
+    quantiles, nematic order, nearest-neighbour alignment and close-pair fraction by
+    Welch t-tests (p > 1e-3); NND histograms (40 bins on [0, 1.2] D) per-bin and by
+    ensemble chi-square."""
+    import ctypes as C
+    import make_golden
+    z = load("e2e_platelet")
+    c = make_golden.PLATE
+    L = [c["L"]] * 3
+    stats, nnds = [], []
+    for s in c["seeds"]:
+        pos, nrm, ids = srm.rsa_platelets(c["n"], 1.0, c["aspect"], L, 10000, 100 + s)
+        snap = srm.PlateletSnapshot(L, pos, nrm, 1.0, 1.0 / c["aspect"], ids)
+        snap.refresh_volume_fraction()
+        p = srm.SrmParams(c_w=c["c_w"], c_m=c["c_m"], c_r=c["c_r"], n_k=c["n_k"], n_l=c["n_l"], f_target=c["f_t"],
+                          max_iterations=100000, seed=s, reorder_period=16)
+        res = srm.srm_generate(snap, p)
+        assert res.status == srm.GenerateStatus.Converged
+        assert abs(res.snapshot.volume_fraction / c["f_t"] - 1.0) < 1e-9
+        out = res.snapshot
+        P = orc.P
+        cs = 2.5 * 0.5 * float(out.diameter.max() + out.thickness.max())
+        assert orc.ref().ref_pl_any_collision(P(orc.arr(L)), C.c_double(cs), c["n"], P(out.pos), P(out.normal),
+                                              P(out.diameter), P(out.thickness), P(out.id)) == 0
+        row, nnd = make_golden.platelet_stats(out.pos, out.normal, float(out.diameter[0]), L)
+        stats.append(row)
+        nnds.append(nnd)
+    ps = stats_util.ensemble_agree(np.array(stats), z["stats"])
+    assert min(ps) > 1e-3, f"platelet summaries differ: Welch p = {ps}"
+    e = np.linspace(0.0, 1.2, 41)
+    h_dev = np.array([np.histogram(a, e)[0] for a in nnds])
+    h_ref = np.array([np.histogram(a, e)[0] for a in z["nnd"]])
+    ok, _ = stats_util.hist_agree(h_dev.sum(0), h_ref.sum(0))
+    assert ok.all(), f"NND bins out of tolerance: {np.where(~ok)[0]}"
+    assert stats_util.ensemble_chi2(h_dev, h_ref) > 1e-3
