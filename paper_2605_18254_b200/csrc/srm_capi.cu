@@ -424,7 +424,7 @@ struct srm_b200_ctx {
             FamScope fs(this, 3);
             const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
             if (platelets())
-                k_overlap_pl<<<blocks_for(n, 256), 256, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
+                k_overlap_pl<<<blocks_for(n * 32, kOverlapPlThreads), kOverlapPlThreads, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
             else if (dim == 2)
                 k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
             else
@@ -586,7 +586,7 @@ struct srm_b200_ctx {
                     const int lb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
                     if (dim == 2) k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
                     else if (platelets())
-                        k_overlap_pl<<<blocks_for(n, 256), 256, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
+                        k_overlap_pl<<<blocks_for(n * 32, kOverlapPlThreads), kOverlapPlThreads, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
                     else k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
                     copy_state(S, Q);
                     k_gen_after<<<1, 1, 0, stream>>>(ctl, stats, h_commit, h_f, h_reorder);
@@ -999,7 +999,7 @@ int srm_b200_overlap_stats(srm_b200_ctx* c, double cell_size, srm_b200_round_sta
             {
                 srm_b200_ctx::FamScope fs(c, 3);
                 if (c->platelets())
-                    k_overlap_pl<<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey,
+                    k_overlap_pl<<<blocks_for(n * 32, kOverlapPlThreads), kOverlapPlThreads, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey,
                                                                           c->stats);
                 else if (c->dim == 2)
                     k_overlap_full<2><<<blocks_for(n, 256), 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, 1, c->stats);

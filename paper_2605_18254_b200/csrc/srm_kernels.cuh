@@ -967,8 +967,13 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
 #define SRM_PL_TEAM 32
 #endif
 constexpr int kPlTeam = SRM_PL_TEAM;
+// resident CTAs per SM the team kernel is compiled for (4: 210 registers, no spills;
+// without a bound ptxas caps it at 128 registers and spills)
+#ifndef SRM_PL_MINB
+#define SRM_PL_MINB 4
+#endif
 
-__global__ void __launch_bounds__(kSweepThreads) k_sweep_pl_team(int cls_arg, const int* __restrict__ cls_dev, State S,
+__global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(int cls_arg, const int* __restrict__ cls_dev, State S,
                                                                  Box box, const GridParams* __restrict__ gp,
                                                                  const RoundParams* __restrict__ rpp,
                                                                  const int64_t* __restrict__ cs,
@@ -1012,18 +1017,56 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep_pl_team(int cls_arg, co
                 unit_vector<3>(rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), 1, ax);
                 pn = pl::rotate_normal(pl::V3{ni.x, ni.y, ni.z}, pl::V3{ax[0], ax[1], ax[2]}, rp.cos_r, rp.sin_r);
                 bool hit = false;
-                auto test = [&](int64_t j) {
-                    const double4 v = S.rec[j], a = S.aux[j];
-                    const pl::V3 d{min_image1(v.x - p[0], box.L[0], box.half[0]),
-                                   min_image1(v.y - p[1], box.L[1], box.half[1]),
-                                   min_image1(v.z - p[2], box.L[2], box.half[2])};
-                    return pl::spherodisk_overlap(d, pn, me.w, ni.w, pl::V3{a.x, a.y, a.z}, v.w, a.w, c_seed_table);
+                auto cand = [&](int64_t j, pl::V3& d, pl::V3& nb, double4& v, double4& a) {
+                    v = S.rec[j];
+                    a = S.aux[j];
+                    d = pl::V3{min_image1(v.x - p[0], box.L[0], box.half[0]),
+                               min_image1(v.y - p[1], box.L[1], box.half[1]),
+                               min_image1(v.z - p[2], box.L[2], box.half[2])};
+                    nb = pl::V3{a.x, a.y, a.z};
                 };
-                if (nn <= kNearCap) {
-                    for (int k = tl; k < nn && !hit; k += kPlTeam) hit = test(row[1 + k]);
-                } else if (row[1] >= 0) {  // the list is in the overflow pool
-                    const int32_t* e = pool + row[1];
-                    for (int k = tl; k < nn && !hit; k += kPlTeam) hit = test(e[k]);
+                auto test = [&](int64_t j) {
+                    pl::V3 d, nb;
+                    double4 v, a;
+                    cand(j, d, nb, v, a);
+                    return pl::spherodisk_overlap(d, pn, me.w, ni.w, nb, v.w, a.w, c_seed_table);
+                };
+                if (nn <= kNearCap || row[1] >= 0) {
+                    // the list (in the row, or in the overflow pool), a candidate per lane per
+                    // pass; a pair the projections leave undecided (disks_within's rim-seed
+                    // fallback, 32 x 64 projections) is resolved by the whole team, a seed per
+                    // lane, unless another candidate of the pass already overlaps
+                    const int32_t* e = nn <= kNearCap ? row + 1 : pool + row[1];
+                    const double r1 = 0.5 * (me.w - ni.w);
+                    for (int base = 0; base < nn; base += kPlTeam) {
+                        const int k = base + tl;
+                        pl::V3 d{0.0, 0.0, 0.0}, nb{0.0, 0.0, 1.0};
+                        double r2 = 0.0, th = 0.0;
+                        int st = pl::kDwFalse;
+                        if (k < nn) {
+                            double4 v, a;
+                            cand(e[k], d, nb, v, a);
+                            st = pl::spherodisk_overlap_pre(d, pn, me.w, ni.w, nb, v.w, a.w);
+                            r2 = 0.5 * (v.w - a.w);
+                            th = 0.5 * (ni.w + a.w);
+                        }
+                        hit = (__ballot_sync(tm, st == pl::kDwTrue) & tm) != 0u;
+                        unsigned pend = __ballot_sync(tm, st == pl::kDwSeeds) & tm;
+                        while (pend && !hit) {
+                            const int src = __ffs(pend) - 1;
+                            pend &= pend - 1u;
+                            const pl::V3 sd{__shfl_sync(tm, d.x, src), __shfl_sync(tm, d.y, src),
+                                            __shfl_sync(tm, d.z, src)};
+                            const pl::V3 sn{__shfl_sync(tm, nb.x, src), __shfl_sync(tm, nb.y, src),
+                                            __shfl_sync(tm, nb.z, src)};
+                            const double sr2 = __shfl_sync(tm, r2, src), sth = __shfl_sync(tm, th, src);
+                            bool h = false;
+                            for (int sk = tl; sk < pl::kSeeds && !h; sk += kPlTeam)
+                                h = pl::rim_seed_within(pl::V3{0.0, 0.0, 0.0}, pn, r1, sd, sn, sr2, sth, c_seed_table, sk);
+                            hit = (__ballot_sync(tm, h) & tm) != 0u;
+                        }
+                        if (hit) break;
+                    }
                 } else {  // crowded neighbourhood, pool full: the stencil, split over the team
                     near_candidates<3>(
                         g, cs, S.xf, q, skey[q],
@@ -1407,36 +1450,78 @@ __global__ void __launch_bounds__(256) k_overlap_full(int64_t n, State S, Box bo
 // Overlap statistics of a platelet state: unordered pairs {i, j > i} with overlap(i, j)
 // or overlap(j, i) -- shape_any_collision tests every ordered pair, and the platelet
 // test is not symmetric in its arguments (spherodisk.cpp), so the non-mover shortcut
-// of the spheres does not apply.  Penetration is not defined for platelets (0).
-__global__ void __launch_bounds__(256) k_overlap_pl(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
-                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                                    StatsDev* stats) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// of the spheres does not apply.  Penetration is not defined for platelets (0).  A warp
+// per particle i, a candidate j per lane (the stencil's contiguous ranges, 32 at a
+// time); a pair the projections leave undecided in a direction goes to the rim-seed
+// fallback run by the whole warp, a seed per lane.  The count is an OR per pair, so it
+// does not depend on who decides what.
+constexpr int kOverlapPlThreads = 128;
+__global__ void __launch_bounds__(kOverlapPlThreads, 3) k_overlap_pl(int64_t n, State S, Box box,
+                                                                  const GridParams* __restrict__ gp,
+                                                                  const int64_t* __restrict__ cs,
+                                                                  const uint32_t* __restrict__ skey, StatsDev* stats) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;  // whole warps
     unsigned long long pairs = 0;
-    if (i < n) {
-        const GridParams& g = *gp;
-        const double4 vi = S.rec[i], ai = S.aux[i];
-        const int32_t idi = S.id[i];
-        for_near_ranges<3>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
-            for (int64_t j = b; j < e; ++j) {
-                if (j <= i || S.id[j] == idi) continue;
+    const GridParams& g = *gp;
+    const double4 vi = S.rec[i], ai = S.aux[i];
+    const int32_t idi = S.id[i];
+    const pl::V3 ni{ai.x, ai.y, ai.z};
+    const pl::V3 o{0.0, 0.0, 0.0};
+    for_near_ranges<3>(g, cs, skey[i], g.near_s, [&](int64_t b, int64_t e) {
+        for (int64_t base = b; base < e; base += 32) {
+            const int64_t j = base + lane;
+            // sa, sb: the stage of overlap(i, j) and overlap(j, i); kDwFalse for no pair
+            int sa = pl::kDwFalse, sb = pl::kDwFalse;
+            pl::V3 dij = o, dji = o, nj{0.0, 0.0, 1.0};
+            double Dj = 0.0, tj = 0.0;
+            if (j < e && j > i && S.id[j] != idi) {
                 const double4 vj = S.rec[j], aj = S.aux[j];
-                const pl::V3 dij{min_image1(vj.x - vi.x, box.L[0], box.half[0]),
-                                 min_image1(vj.y - vi.y, box.L[1], box.half[1]),
-                                 min_image1(vj.z - vi.z, box.L[2], box.half[2])};
-                const pl::V3 dji{min_image1(vi.x - vj.x, box.L[0], box.half[0]),
-                                 min_image1(vi.y - vj.y, box.L[1], box.half[1]),
-                                 min_image1(vi.z - vj.z, box.L[2], box.half[2])};
-                const pl::V3 ni{ai.x, ai.y, ai.z}, nj{aj.x, aj.y, aj.z};
-                if (pl::spherodisk_overlap(dij, ni, vi.w, ai.w, nj, vj.w, aj.w, c_seed_table) ||
-                    pl::spherodisk_overlap(dji, nj, vj.w, aj.w, ni, vi.w, ai.w, c_seed_table))
-                    ++pairs;
+                dij = pl::V3{min_image1(vj.x - vi.x, box.L[0], box.half[0]),
+                             min_image1(vj.y - vi.y, box.L[1], box.half[1]),
+                             min_image1(vj.z - vi.z, box.L[2], box.half[2])};
+                dji = pl::V3{min_image1(vi.x - vj.x, box.L[0], box.half[0]),
+                             min_image1(vi.y - vj.y, box.L[1], box.half[1]),
+                             min_image1(vi.z - vj.z, box.L[2], box.half[2])};
+                nj = pl::V3{aj.x, aj.y, aj.z};
+                Dj = vj.w;
+                tj = aj.w;
+                sa = pl::spherodisk_overlap_pre(dij, ni, vi.w, ai.w, nj, Dj, tj);
+                if (sa != pl::kDwTrue) sb = pl::spherodisk_overlap_pre(dji, nj, Dj, tj, ni, vi.w, ai.w);
             }
-        });
-    }
+            const bool hit = sa == pl::kDwTrue || sb == pl::kDwTrue;
+            pairs += hit ? 1 : 0;
+            unsigned pend = __ballot_sync(0xffffffffu, !hit && (sa == pl::kDwSeeds || sb == pl::kDwSeeds));
+            while (pend) {
+                const int src = __ffs(pend) - 1;
+                pend &= pend - 1u;
+                const int qa = __shfl_sync(0xffffffffu, sa, src), qb = __shfl_sync(0xffffffffu, sb, src);
+                const pl::V3 nq{__shfl_sync(0xffffffffu, nj.x, src), __shfl_sync(0xffffffffu, nj.y, src),
+                                __shfl_sync(0xffffffffu, nj.z, src)};
+                const double Dq = __shfl_sync(0xffffffffu, Dj, src), tq = __shfl_sync(0xffffffffu, tj, src);
+                bool found = false;
+                if (qa == pl::kDwSeeds) {  // overlap(i, j): disks (0, ni) and (dij, nj)
+                    const pl::V3 d{__shfl_sync(0xffffffffu, dij.x, src), __shfl_sync(0xffffffffu, dij.y, src),
+                                   __shfl_sync(0xffffffffu, dij.z, src)};
+                    const bool h = pl::rim_seed_within(o, ni, 0.5 * (vi.w - ai.w), d, nq, 0.5 * (Dq - tq),
+                                                       0.5 * (ai.w + tq), c_seed_table, lane);
+                    found = __ballot_sync(0xffffffffu, h) != 0u;
+                }
+                if (!found && qb == pl::kDwSeeds) {  // overlap(j, i): disks (0, nj) and (dji, ni)
+                    const pl::V3 d{__shfl_sync(0xffffffffu, dji.x, src), __shfl_sync(0xffffffffu, dji.y, src),
+                                   __shfl_sync(0xffffffffu, dji.z, src)};
+                    const bool h = pl::rim_seed_within(o, nq, 0.5 * (Dq - tq), d, ni, 0.5 * (vi.w - ai.w),
+                                                       0.5 * (tq + ai.w), c_seed_table, lane);
+                    found = __ballot_sync(0xffffffffu, h) != 0u;
+                }
+                if (found && lane == src) ++pairs;
+            }
+        }
+    });
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, o);
-    if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(&stats->overlap_pairs, pairs);
+    for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+    if (lane == 0 && pairs) atomicAdd(&stats->overlap_pairs, pairs);
 }
 
 // platelet records (host layout) <-> device state, scattered back to slot order

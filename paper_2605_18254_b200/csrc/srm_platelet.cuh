@@ -83,44 +83,54 @@ SRM_HD double max3(double a, double b, double c) {
     return m;
 }
 
-// spherodisk.cpp:70-112 disks_within: the medial disks are within `threshold`
-// (separation proofs, projections with early accept, then the rim-seed fallback)
-SRM_HD bool disks_within(V3 c1, V3 n1, double r1, V3 c2, V3 n2, double r2, double threshold, const SeedTable& tab) {
+// spherodisk.cpp:70-112 disks_within, in two stages so that a team of lanes can run the
+// rim seeds of the fallback side by side (the result is the OR over the seeds, so the
+// order they run in does not change it).  disks_within_pre: the separation proofs and
+// the projections with early accept; kDwFalse / kDwTrue decide, kDwSeeds sends the pair
+// to the fallback, rim_seed_within(k) = seed k of it.
+enum { kDwFalse = 0, kDwTrue = 1, kDwSeeds = 2 };
+
+SRM_HD double disks_tol(double r1, double r2) { return 1e-12 * max3(r1, r2, 1e-30); }
+
+SRM_HD int disks_within_pre(V3 c1, V3 n1, double r1, V3 c2, V3 n2, double r2, double threshold) {
     const V3 d = sub(c2, c1);
-    if (norm(d) - r1 - r2 > threshold) return false;
+    if (norm(d) - r1 - r2 > threshold) return kDwFalse;
     const double ndot = dot(n1, n2);
     const double t = 1.0 - ndot * ndot;
     const double sin_tilt = sqrt(t > 0.0 ? t : 0.0);
-    if (fabs(dot(n1, d)) - r2 * sin_tilt > threshold) return false;
-    if (fabs(dot(n2, d)) - r1 * sin_tilt > threshold) return false;
+    if (fabs(dot(n1, d)) - r2 * sin_tilt > threshold) return kDwFalse;
+    if (fabs(dot(n2, d)) - r1 * sin_tilt > threshold) return kDwFalse;
 
-    const double tol = 1e-12 * max3(r1, r2, 1e-30);
+    const double tol = disks_tol(r1, r2);
     V3 p2 = closest_on_disk(c2, n2, r2, c1);
     double prev = static_cast<double>(INFINITY);
-    bool converged = false;
     for (int it = 0; it < 200; ++it) {
         const V3 p1 = closest_on_disk(c1, n1, r1, p2);
         p2 = closest_on_disk(c2, n2, r2, p1);
         const double dist = norm(sub(p1, p2));
-        if (dist <= threshold) return true;
-        if (prev - dist <= tol) {
-            converged = true;
-            break;
-        }
+        if (dist <= threshold) return kDwTrue;
+        if (prev - dist <= tol) return kDwFalse;  // converged above the threshold
         prev = dist;
     }
-    if (converged) return false;
+    return kDwSeeds;
+}
 
+SRM_HD bool rim_seed_within(V3 c1, V3 n1, double r1, V3 c2, V3 n2, double r2, double threshold, const SeedTable& tab,
+                            int k) {
     V3 u = fabs(n2.x) < 0.9 ? V3{1.0, 0.0, 0.0} : V3{0.0, 1.0, 0.0};
     u = sub(u, mul(n2, dot(u, n2)));
     u = mul(u, 1.0 / norm(u));
     const V3 v = cross(n2, u);
-    for (int k = 0; k < kSeeds; ++k) {
-        const V3 seed = add(c2, mul(add(mul(u, tab.c[k]), mul(v, tab.s[k])), r2));
-        bool conv;
-        const double dist = alternate(c1, n1, r1, c2, n2, r2, seed, tol, 64, &conv);
-        if (dist <= threshold) return true;
-    }
+    const V3 seed = add(c2, mul(add(mul(u, tab.c[k]), mul(v, tab.s[k])), r2));
+    bool conv;
+    return alternate(c1, n1, r1, c2, n2, r2, seed, disks_tol(r1, r2), 64, &conv) <= threshold;
+}
+
+SRM_HD bool disks_within(V3 c1, V3 n1, double r1, V3 c2, V3 n2, double r2, double threshold, const SeedTable& tab) {
+    const int st = disks_within_pre(c1, n1, r1, c2, n2, r2, threshold);
+    if (st != kDwSeeds) return st == kDwTrue;
+    for (int k = 0; k < kSeeds; ++k)
+        if (rim_seed_within(c1, n1, r1, c2, n2, r2, threshold, tab, k)) return true;
     return false;
 }
 
@@ -130,6 +140,13 @@ SRM_HD bool spherodisk_overlap(V3 d, V3 na, double Da, double ta, V3 nb, double 
     const double cull = 0.5 * (Da + Db + ta + tb);
     if (dot(d, d) > cull * cull) return false;
     return disks_within(V3{0.0, 0.0, 0.0}, na, 0.5 * (Da - ta), d, nb, 0.5 * (Db - tb), 0.5 * (ta + tb), tab);
+}
+
+// spherodisk_overlap's first stage (disks_within_pre of the same medial disks)
+SRM_HD int spherodisk_overlap_pre(V3 d, V3 na, double Da, double ta, V3 nb, double Db, double tb) {
+    const double cull = 0.5 * (Da + Db + ta + tb);
+    if (dot(d, d) > cull * cull) return kDwFalse;
+    return disks_within_pre(V3{0.0, 0.0, 0.0}, na, 0.5 * (Da - ta), d, nb, 0.5 * (Db - tb), 0.5 * (ta + tb));
 }
 
 // spherodisk.hpp:29-34 swept-solid volume

@@ -42,6 +42,34 @@ def test_round_bit_exact_vs_oracle(n, L, swell, c_m, c_r, n_l, seed):
     assert 0 < int(np.sum(ao != 255)) <= n
 
 
+def test_round_bit_exact_rim_seed_fallback():
+    """cfg 5's regime (aspect 100, rsa start at rho 3.5, swollen by c_w): about 1 pair
+    in 4000 within reach leaves disks_within's 200 projections undecided (16 of the
+    57803 start pairs here), and the team sweep resolves those with a rim seed per lane
+    (k_sweep_pl_team); the round must still be the oracle's bit for bit."""
+    n, aspect = 8000, 100.0
+    L = 10.77 / 0.818  # cfg 5's number density in diameters
+    pos, nrm, ids = srm.rsa_platelets(n, 1.0, aspect, [L] * 3, 100000, 5)
+    D = np.full(n, 1.008)
+    t = D / aspect
+    cs = 2.5 * 0.5 * (D.max() + t.max()) + 0.01 / 0.818
+    c_m, c_r, n_l, key = 0.01 / 0.818, 0.012, 10, 77
+    with srm.Context([L] * 3, n, shape="platelet") as ctx:
+        ctx.upload_platelets(pos, nrm, D, t, ids)
+        ctx.set_rotation(c_r)
+        st0 = ctx.overlap_stats(cs)  # k_overlap_pl: the same fallback, a seed per lane
+        for rid in range(3):
+            st, acc = ctx.round(cs, c_m, n_l, key, rid, 9)
+        p_d, n_d, _, _, _ = ctx.download_platelets()
+    x, nm = pos, nrm
+    for rid in range(3):
+        x, nm, ao = orc.o_pl_round([L] * 3, x, nm, D, t, ids, ids, cs, c_m, c_r, n_l, key, rid, 9)
+    assert np.array_equal(acc, ao)
+    assert np.array_equal(p_d, x) and np.array_equal(n_d, nm)
+    assert st0.overlap_pairs == orc.o_pl_pairs([L] * 3, pos, nrm, D, t, ids) > 0
+    assert st.overlap_pairs == orc.o_pl_pairs([L] * 3, x, nm, D, t, ids)
+
+
 def test_overlap_stats_vs_oracle_and_reference():
     Lb, pos, nrm, D, t, ids = _state(600, 6.5, 4)
     for swell in (1.0, 1.3, 1.6):
