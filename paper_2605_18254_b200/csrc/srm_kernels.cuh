@@ -993,10 +993,10 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(in
     const uint32_t cells = static_cast<uint32_t>(cnt[0]) * cnt[1] * cnt[2];
     const uint32_t nteams = (gridDim.x * blockDim.x) / kPlTeam;
     const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / kPlTeam;
-    const uint32_t c0 = static_cast<uint32_t>(static_cast<uint64_t>(cells) * team / nteams);
-    const uint32_t c1 = static_cast<uint32_t>(static_cast<uint64_t>(cells) * (team + 1) / nteams);
+    // cells strided over the teams: with fewer cells than teams the busy teams are the
+    // first ones, packed into the first CTAs, so they are resident together
     const int cx = cnt[0], cxy = cnt[0] * cnt[1];
-    for (uint32_t t = c0; t < c1; ++t) {
+    for (uint32_t t = team; t < cells; t += nteams) {
         const int iz = static_cast<int>(t / cxy), r2 = static_cast<int>(t - static_cast<uint32_t>(iz) * cxy);
         const int iy = r2 / cx, ix = r2 - iy * cx;
         const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
