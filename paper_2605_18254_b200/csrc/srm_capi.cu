@@ -187,6 +187,8 @@ struct srm_b200_ctx {
 
     // ---------------------------------------------------------------------------
     bool platelets() const { return shape == SRM_B200_PLATELET; }
+    // crowded sphere grids (the 4x4x4-brick near kind) take the team sweep
+    static bool sphere_team(const GridParams& g) { return SRM_SPH_TEAM_ON && g.near_kind == 3; }
     void alloc_state(State& s) {
         s.rec = dalloc<double4>(cap);
         s.id = dalloc<int32_t>(cap);
@@ -414,6 +416,11 @@ struct srm_b200_ctx {
                                           blocks_for(cells * kPlTeam, kSweepThreads), 148 * 32))),
                                       kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
                                                                   active, stats);
+                else if (sphere_team(hg))
+                    k_sweep_team<<<static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+                                       blocks_for(cells * kSphTeam, kSweepThreads), 148 * 32))),
+                                   kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
+                                                               active, stats);
                 else
                     k_sweep_warpq<3><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
                                                                          active, stats);
@@ -535,6 +542,7 @@ struct srm_b200_ctx {
         const int ctiles_max = dim == 3 ? ((g0.dims[0] + kCTX - 1) / kCTX) * ((g0.dims[1] + kCTY - 1) / kCTY) *
                                               ((g0.dims[2] + kCTZ - 1) / kCTZ)
                                         : 1;
+        const bool team0 = dim == 3 && !platelets() && sphere_team(g0);
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
@@ -578,6 +586,9 @@ struct srm_b200_ctx {
                             k_sweep_pl_team<<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp,
                                                                                              cell_start, skey, nbr, pool.e, acc, active,
                                                                                              stats);
+                        else if (team0)  // (the first grid's kind decides for the run; either is exact)
+                            k_sweep_team<<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
+                                                                                  skey, nbr, pool.e, acc, active, stats);
                         else
                             k_sweep_warpq<3><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
                                                                                        skey, nbr, pool.e, acc, active, stats);

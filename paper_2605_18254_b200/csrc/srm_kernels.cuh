@@ -955,6 +955,97 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
     }
 }
 
+// The class sweep of crowded sphere grids (the ctiles near kind: several particles per
+// cell, long near lists in the overflow pool): a team of kSphTeam lanes per cell.  A
+// class then holds few cells of long chains (cfg 3's clusters: ~14 particles per cell),
+// so a lane per cell leaves most of the GPU idle; here the team's lanes split the
+// candidates of each trial and vote with a ballot.  Every lane computes the same
+// proposal, and "no candidate overlaps" does not depend on who tests what, so the
+// decisions are those of the sequential sweep (orc_sweep_round), like k_sweep_warpq's.
+#ifndef SRM_SPH_TEAM
+#define SRM_SPH_TEAM 16
+#endif
+#ifndef SRM_SPH_TEAM_ON
+#define SRM_SPH_TEAM_ON 1
+#endif
+constexpr int kSphTeam = SRM_SPH_TEAM;
+static_assert(kSphTeam >= 2 && kSphTeam <= 32 && (kSphTeam & (kSphTeam - 1)) == 0, "team: a power of two");
+
+__global__ void __launch_bounds__(kSweepThreads, 8) k_sweep_team(int cls_arg, const int* __restrict__ cls_dev, State S,
+                                                              Box box, const GridParams* __restrict__ gp,
+                                                              const RoundParams* __restrict__ rpp,
+                                                              const int64_t* __restrict__ cs,
+                                                              const uint32_t* __restrict__ skey,
+                                                              const int32_t* __restrict__ nbr,
+                                                              const int32_t* __restrict__ pool,
+                                                              uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                                              StatsDev* stats) {
+    const int cls = cls_dev ? *cls_dev : cls_arg;
+    const GridParams& g = *gp;
+    if (cls >= g.ncls) return;
+    const RoundParams rp = *rpp;
+    const int lane = threadIdx.x & 31, tl = lane & (kSphTeam - 1);
+    const unsigned tm = (kSphTeam == 32 ? 0xffffffffu : ((1u << (kSphTeam & 31)) - 1u)) << (lane & ~(kSphTeam - 1));
+    int first[3], stride[3], cnt[3];
+    class_lattice(g, cls, first, stride, cnt);
+    const uint32_t cells = static_cast<uint32_t>(cnt[0]) * cnt[1] * cnt[2];
+    const uint32_t nteams = (gridDim.x * blockDim.x) / kSphTeam;
+    const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / kSphTeam;
+    const int cx = cnt[0], cxy = cnt[0] * cnt[1];
+    for (uint32_t t = team; t < cells; t += nteams) {
+        const int iz = static_cast<int>(t / cxy), r2 = static_cast<int>(t - static_cast<uint32_t>(iz) * cxy);
+        const int iy = r2 / cx, ix = r2 - iy * cx;
+        const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
+                                 g.dims[0] + first[0] + stride[0] * ix;
+        const int64_t b = cs[cell], e = cs[cell + 1];
+        for (int64_t q = b; q < e; ++q) {
+            const double4 me = S.rec[q];
+            const int32_t sl = S.slot[q], idq = S.id[q];
+            const int32_t* row = nbr + q * kNearRow;
+            const int nn = row[0];
+            const int32_t* list = nn <= kNearCap ? row + 1 : (row[1] >= 0 ? pool + row[1] : nullptr);
+            const double xi[3] = {me.x, me.y, me.z};
+            int accepted = -1;
+            double p[3];
+            for (int l = 0; l < rp.n_l; ++l) {
+                propose<3>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
+                bool hit = false;
+                if (list) {
+                    for (int k = tl; k < nn && !hit; k += kSphTeam) {
+                        const double4 w = S.rec[list[k]];
+                        const double xl[3] = {w.x, w.y, w.z};
+                        hit = sphere_overlap<3>(box, p, me.w, xl, w.w);
+                    }
+                } else {  // overflowed list, pool full: the stencil, split over the team
+                    near_candidates<3>(
+                        g, cs, S.xf, q, skey[q],
+                        [&](int64_t j) {
+                            if (hit || S.id[j] == idq) return;
+                            const double4 w = S.rec[j];
+                            const double xl[3] = {w.x, w.y, w.z};
+                            hit = sphere_overlap<3>(box, p, me.w, xl, w.w);
+                        },
+                        tl, kSphTeam);
+                }
+                if ((__ballot_sync(tm, hit) & tm) == 0u) {
+                    accepted = l;
+                    break;
+                }
+            }
+            if (tl == 0) {
+                if (accepted >= 0) {
+                    S.rec[q] = make_double4(p[0], p[1], p[2], me.w);
+                    if (rp.write_acc) acc[q] = static_cast<uint8_t>(accepted);
+                } else {
+                    if (rp.write_acc) acc[q] = kNotAccepted;
+                    active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
+                }
+            }
+            __syncwarp(tm);  // the move is visible to the team before the cell's next particle
+        }
+    }
+}
+
 // The platelet class sweep with a team of kPlTeam lanes per particle.  The exact
 // disk-disk test (spherodisk.cpp) dominates a platelet trial and a class holds few cells
 // (27 classes of ~1700 cells at cfg 5), so one lane per cell leaves the GPU idle: here a

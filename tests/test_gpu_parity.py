@@ -209,6 +209,38 @@ def test_round_polydisperse_bit_exact():
     assert st.overlap_pairs == orc.o_stats(3, L, xnew, r).overlap_pairs
 
 
+@pytest.mark.parametrize("swell,n_l,seed", [(1.03, 10, 21), (1.12, 4, 22)])
+def test_round_crowded_spheres_team_sweep(swell, n_l, seed):
+    """Bidisperse spheres (1 in 20 four times larger): the cell edge follows the large
+    radius, so a cell holds ~16 particles -- the crowded near kind (4x4x4 bricks, lists in
+    the overflow pool) and the team sweep (k_sweep_team: a team of lanes per cell splits
+    each trial's candidates).  Two rounds, bit for bit against the oracle."""
+    n, nl, L = 12000, 600, [1.0, 1.0, 1.0]
+    rel = np.ones(n)
+    rel[:nl] = 4.0  # placed first
+    rs = (0.2 / (4.0 / 3.0 * np.pi * np.sum(rel ** 3))) ** (1.0 / 3.0)
+    r0 = rel * rs
+    pos, ids = srm.rsa_place(r0, L, 100000, seed)
+    r = r0 * swell
+    c_m = 0.1 * np.mean(r)
+    cs = 2.5 * r.max() / swell + c_m
+    key = 0x5EED + seed
+    with srm.Context(L, n) as ctx:
+        ctx.upload(pos, r, ids)
+        for rid in range(2):
+            st, acc = ctx.round(cs, c_m, n_l, key, rid, 3)
+        info = ctx.last_round_info()
+        p_d, _, _ = ctx.download()
+    assert n > 1.8 * info["cells"] and info["cells"] >= 6 ** 3  # the crowded kind
+    x = pos
+    for rid in range(2):
+        x, ao = orc.o_round(3, L, x, r, ids, ids, cs, c_m, n_l, key, rid, 3)
+    assert np.array_equal(acc, ao)
+    assert np.array_equal(p_d, x)
+    o = orc.o_stats(3, L, x, r)
+    assert st.overlap_pairs == o.overlap_pairs and st.max_penetration == o.max_penetration
+
+
 def test_rounds_are_deterministic_and_chain():
     L, pos, r, ids = _rsa_state(3, 6000, 0.3, 7)
     r = r * 1.02
