@@ -17,6 +17,10 @@ def _start(dim, n, f0, seed, poly=False):
     unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi
     r0 = (f0 / (n * unit)) ** (1.0 / dim)
     radii = np.full(n, r0) if not poly else r0 * rng.uniform(0.7, 1.2, n)
+    if poly == "bi":  # 1 in 20 four times larger: crowded cells (the team sweep)
+        rel = np.ones(n)
+        rel[: n // 20] = 4.0
+        radii = rel * (f0 / (unit * np.sum(rel ** dim))) ** (1.0 / dim)
     L = [1.0] * dim
     pos, ids = srm.rsa_place(radii, L, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
     return L, pos, radii, ids
@@ -33,7 +37,7 @@ def _run(L, pos, r, ids, params, device_loop, it0=0):
 
 
 @pytest.mark.parametrize("dim,n,f0,poly,reorder", [(2, 3000, 0.2, False, 4), (3, 6000, 0.15, False, 3),
-                                                    (3, 4000, 0.12, True, 0)])
+                                                    (3, 4000, 0.12, True, 0), (3, 12000, 0.15, "bi", 3)])
 def test_budget_limited_runs_are_identical(dim, n, f0, poly, reorder):
     L, pos, r, ids = _start(dim, n, f0, 11, poly)
     c_m = 0.1 * float(r.max())
