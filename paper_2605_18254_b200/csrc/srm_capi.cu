@@ -188,7 +188,26 @@ struct srm_b200_ctx {
     // ---------------------------------------------------------------------------
     bool platelets() const { return shape == SRM_B200_PLATELET; }
     // crowded sphere grids (the 4x4x4-brick near kind) take the team sweep
-    static bool sphere_team(const GridParams& g) { return SRM_SPH_TEAM_ON && g.near_kind == 3; }
+    // SRM_B200_SWEEP=lane|trials|team forces one sweep kernel (tests: every kernel is
+    // exact on any grid, the choice is only a matter of speed); unset: by the grid
+    int sweep_force = [] {
+        const char* v = std::getenv("SRM_B200_SWEEP");
+        if (!v) return 0;
+        const std::string s(v);
+        return s == "lane" ? 1 : (s == "trials" ? 2 : (s == "team" ? 3 : 0));
+    }();
+    bool sphere_team(const GridParams& g) const {
+        if (sweep_force) return sweep_force == 3 && dim == 3;
+        return SRM_SPH_TEAM_ON && g.near_kind == 3;
+    }
+    // small grids (not crowded): a lane per cell would leave the GPU mostly idle; a
+    // team per cell runs a particle's trials side by side (k_sweep_trials) while the
+    // teams of a class launch still fit one wave of resident CTAs
+    bool trial_team(const GridParams& g, int64_t class_cells_total) const {
+        if (sweep_force) return sweep_force == 2;
+        const int64_t per_class = class_cells_total / std::max(1, g.ncls);
+        return SRM_TRIAL_TEAM_ON && g.near_kind != 3 && per_class * kTrialTeam <= 148LL * 8 * kSweepThreads;
+    }
     void alloc_state(State& s) {
         s.rec = dalloc<double4>(cap);
         s.id = dalloc<int32_t>(cap);
@@ -408,7 +427,16 @@ struct srm_b200_ctx {
                 // a cell per lane (the cells of a class are its parallelism: a cell's
                 // particles are visited in order), at most one wave of resident CTAs
                 const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_for(cells, kSweepThreads), queue_ctas)));
-                if (dim == 2)
+                const int tgrid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+                    blocks_for(cells * kTrialTeam, kSweepThreads), 148 * 32)));
+                if (!platelets() && trial_team(hg, cls_cells_h[hg.ncls] - cls_cells_h[0])) {
+                    if (dim == 2)
+                        k_sweep_trials<2><<<tgrid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr,
+                                                                               pool.e, acc, active, stats);
+                    else
+                        k_sweep_trials<3><<<tgrid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr,
+                                                                               pool.e, acc, active, stats);
+                } else if (dim == 2)
                     k_sweep_warpq<2><<<grid, kSweepThreads, 0, stream>>>(cls, nullptr, S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
                                                                          active, stats);
                 else if (platelets())
@@ -543,6 +571,7 @@ struct srm_b200_ctx {
                                               ((g0.dims[2] + kCTZ - 1) / kCTZ)
                                         : 1;
         const bool team0 = dim == 3 && !platelets() && sphere_team(g0);
+        const bool trials0 = !platelets() && trial_team(g0, g0.ncells);
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
@@ -579,7 +608,13 @@ struct srm_b200_ctx {
                     else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                     k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
                     capture_into(add_conditional(stream, h_cls, cudaGraphCondTypeWhile), cap_streams[3], [&]() {
-                        if (dim == 2)
+                        if (trials0 && dim == 2)
+                            k_sweep_trials<2><<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
+                                                                                        skey, nbr, pool.e, acc, active, stats);
+                        else if (trials0)
+                            k_sweep_trials<3><<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
+                                                                                        skey, nbr, pool.e, acc, active, stats);
+                        else if (dim == 2)
                             k_sweep_warpq<2><<<queue_ctas, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,
                                                                                        skey, nbr, pool.e, acc, active, stats);
                         else if (platelets())

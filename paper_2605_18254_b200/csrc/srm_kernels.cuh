@@ -1046,6 +1046,78 @@ __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep_team(int cls_arg, co
     }
 }
 
+// The class sweep of small grids (a lane per cell would leave most of the GPU idle:
+// cfg 1's 10^4 disks hold ~1000 cells per class): a team of kTrialTeam lanes per cell,
+// a trial per lane.  A particle's trials are independent draws (Philox keyed by slot and
+// trial index) tested against the same live neighbours, so the team runs trials l0 ..
+// l0 + kTrialTeam - 1 at once and the lowest clear one is the sequential sweep's choice
+// (orc_sweep_round); its lane writes the move.  At dense windows most trials fail, so
+// the chain per particle shrinks from ~n_l trials to ~1.
+#ifndef SRM_TRIAL_TEAM
+#define SRM_TRIAL_TEAM 16
+#endif
+#ifndef SRM_TRIAL_TEAM_ON
+#define SRM_TRIAL_TEAM_ON 1
+#endif
+constexpr int kTrialTeam = SRM_TRIAL_TEAM;
+static_assert(kTrialTeam >= 2 && kTrialTeam <= 32 && (kTrialTeam & (kTrialTeam - 1)) == 0, "team: a power of two");
+
+template <int D>
+__global__ void __launch_bounds__(kSweepThreads, 8) k_sweep_trials(int cls_arg, const int* __restrict__ cls_dev, State S,
+                                                                   Box box, const GridParams* __restrict__ gp,
+                                                                   const RoundParams* __restrict__ rpp,
+                                                                   const int64_t* __restrict__ cs,
+                                                                   const uint32_t* __restrict__ skey,
+                                                                   const int32_t* __restrict__ nbr,
+                                                                   const int32_t* __restrict__ pool,
+                                                                   uint8_t* __restrict__ acc, int32_t* __restrict__ active,
+                                                                   StatsDev* stats) {
+    const int cls = cls_dev ? *cls_dev : cls_arg;
+    const GridParams& g = *gp;
+    if (cls >= g.ncls) return;
+    const RoundParams rp = *rpp;
+    const int lane = threadIdx.x & 31, tl = lane & (kTrialTeam - 1), t0 = lane & ~(kTrialTeam - 1);
+    const unsigned tm = (kTrialTeam == 32 ? 0xffffffffu : ((1u << (kTrialTeam & 31)) - 1u)) << t0;
+    int first[3], stride[3], cnt[3];
+    class_lattice(g, cls, first, stride, cnt);
+    const uint32_t cells = static_cast<uint32_t>(cnt[0]) * cnt[1] * cnt[2];
+    const uint32_t nteams = (gridDim.x * blockDim.x) / kTrialTeam;
+    const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / kTrialTeam;
+    const int cx = cnt[0], cxy = cnt[0] * cnt[1];
+    for (uint32_t t = team; t < cells; t += nteams) {
+        const int iz = static_cast<int>(t / cxy), r2 = static_cast<int>(t - static_cast<uint32_t>(iz) * cxy);
+        const int iy = r2 / cx, ix = r2 - iy * cx;
+        const int64_t cell = (static_cast<int64_t>(first[2] + stride[2] * iz) * g.dims[1] + first[1] + stride[1] * iy) *
+                                 g.dims[0] + first[0] + stride[0] * ix;
+        const int64_t b = cs[cell], e = cs[cell + 1];
+        for (int64_t q = b; q < e; ++q) {
+            const double4 me = S.rec[q];
+            const int32_t sl = S.slot[q];
+            double xi[D], p[D];
+            rec_pos<D>(me, xi);
+            bool done = false;
+            for (int l0 = 0; l0 < rp.n_l && !done; l0 += kTrialTeam) {
+                const int l = l0 + tl;
+                const bool clear = l < rp.n_l &&
+                                   trial_clear<D>(q, sl, l, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
+                const unsigned cm = __ballot_sync(tm, clear) & tm;
+                if (cm) {
+                    done = true;
+                    if (lane == __ffs(cm) - 1) {  // the lowest clear trial
+                        S.rec[q] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
+                        if (rp.write_acc) acc[q] = static_cast<uint8_t>(l);
+                    }
+                }
+            }
+            if (!done && tl == 0) {
+                if (rp.write_acc) acc[q] = kNotAccepted;
+                active[atomicAdd(&stats->active_count, 1ull)] = static_cast<int32_t>(q);
+            }
+            __syncwarp(tm);  // the move is visible to the team before the cell's next particle
+        }
+    }
+}
+
 // The platelet class sweep with a team of kPlTeam lanes per particle.  The exact
 // disk-disk test (spherodisk.cpp) dominates a platelet trial and a class holds few cells
 // (27 classes of ~1700 cells at cfg 5), so one lane per cell leaves the GPU idle: here a

@@ -12,6 +12,17 @@ import paper_2605_18254_b200 as srm
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["", "lane", "trials"])
+def sweep_kernel(request, monkeypatch):
+    """Every test once per sweep kernel (SRM_B200_SWEEP: "" = chosen by the grid, lane =
+    k_sweep_warpq, trials = k_sweep_trials, team = k_sweep_team): each is exact on any grid."""
+    if request.param:
+        monkeypatch.setenv("SRM_B200_SWEEP", request.param)
+    else:
+        monkeypatch.delenv("SRM_B200_SWEEP", raising=False)
+    return request.param
+
+
 def _start(dim, n, f0, seed, poly=False):
     rng = np.random.default_rng(seed)
     unit = np.pi if dim == 2 else 4.0 / 3.0 * np.pi

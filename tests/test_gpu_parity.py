@@ -14,6 +14,17 @@ from paper_2605_18254_b200 import _native
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["", "lane", "trials", "team"])
+def sweep_kernel(request, monkeypatch):
+    """Every test once per sweep kernel (SRM_B200_SWEEP: "" = chosen by the grid, lane =
+    k_sweep_warpq, trials = k_sweep_trials, team = k_sweep_team): each is exact on any grid."""
+    if request.param:
+        monkeypatch.setenv("SRM_B200_SWEEP", request.param)
+    else:
+        monkeypatch.delenv("SRM_B200_SWEEP", raising=False)
+    return request.param
+
+
 def _ctx(L, pos, r, ids=None):
     ctx = srm.Context(L, max(len(r), 1))
     ctx.upload(pos, r, ids)
