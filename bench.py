@@ -471,7 +471,7 @@ def run_b200(args, cfg, world, rank, local, pg):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic,
-                         "kernel": "migrate step per round: near lists (k_near_tiles) + k_sweep_warpq x colour classes",
+                         "kernel": "migrate step per round: near lists (k_near_tiles / k_near_lists) + the class sweep x colour classes (k_sweep_warpq; small grids k_sweep_trials, crowded k_sweep_team, platelets k_sweep_pl_team)",
                          "traffic_unit": "bytes per step (one round of near lists + sweep), ncu dram__bytes_read+write",
                          "algorithmic_bytes_per_step": algo,
                          "algorithmic_bytes_per_update": bpu, "step_ms_per_round": t_mig,
