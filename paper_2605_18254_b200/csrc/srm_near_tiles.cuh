@@ -284,8 +284,48 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                     ++m;
                 }
             }
-        } else {  // a longer list (rare at the bench window): the global path, with the pool
-            near_full_particle<3>(qi, S, g, cs, skey, nbr, pool, stats);
+        } else {  // a longer list (crowded grids: most particles): nn entries from the
+                  // overflow pool, filled by a second, scalar pass over the staged stencil
+                  // (the same fp32 screen, so the same pairs as near_full_particle)
+            const int32_t idi = S.id[qi];
+            int64_t off = static_cast<int64_t>(atomicAdd(&stats->pool_top, static_cast<unsigned long long>(nn)));
+            int4* row = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
+            if (off + nn > pool.cap) {  // pool full: the sweep rescans the stencil
+                row[0] = make_int4(nn, -1, 0, 0);
+                row[1] = make_int4(0, 0, 0, 0);
+                continue;
+            }
+            int32_t* dst = pool.e + off;
+#pragma unroll 1
+            for (int ddz = -1; ddz <= 1; ++ddz) {
+#pragma unroll 1
+                for (int ddy = -1; ddy <= 1; ++ddy) {
+                    const int c = hc + ddy * kHX + ddz * kHX * kHY;
+                    const int kb = hoff[c - 1], ke = hoff[c + 2];
+                    for (int k = kb; k < ke; ++k) {
+                        const float* a = reinterpret_cast<const float*>(pxy + (k >> 1)) + (k & 1);
+                        const float* b = reinterpret_cast<const float*>(pzw + (k >> 1)) + (k & 1);
+                        const float ex = __fadd_rn(a[0], -mx), ey = __fadd_rn(a[2], -my), ez = __fadd_rn(b[0], -mz);
+                        const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                        const float lim = __fadd_rn(b[2], base);
+                        const float l2 = __fmul_rn(__fmul_rn(lim, lim), 1.00001f);
+                        if (d2 <= l2 && k != i) {
+                            const int32_t j = pj[k];
+                            if (S.id[j] != idi) dst[m++] = j;
+                        }
+                    }
+                }
+            }
+            if (m > kNearCap) {
+                row[0] = make_int4(m, static_cast<int32_t>(off), 0, 0);
+                row[1] = make_int4(0, 0, 0, 0);
+            } else {  // same-id images removed: the list fits the row after all
+                int32_t e2[kNearCap];
+#pragma unroll
+                for (int t = 0; t < kNearCap; ++t) e2[t] = t < m ? dst[t] : 0;
+                row[0] = make_int4(m, e2[0], e2[1], e2[2]);
+                row[1] = make_int4(e2[3], e2[4], e2[5], e2[6]);
+            }
             continue;
         }
         int4* row = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
