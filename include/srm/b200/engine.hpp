@@ -10,7 +10,7 @@
 //   relax_sweeps/shake  engine.hpp:112-130  (idem)
 //   swell_all           engine.hpp:134-138
 //   reorder_by_locality engine.hpp:144-166
-//   shape_any_collision shape.hpp:549-555
+//   shape_any_collision shape.hpp:75-81
 //   rsa_place           rsa.hpp:21-61       (seeded form; bit-identical to Rng(seed))
 //   rsa_platelets       recipes.cpp:107-148 (seeded form; bit-identical to Rng(seed))
 //   nearest_neighbor_distances  descriptors.hpp:96-115 (exact, on the device)
@@ -25,8 +25,10 @@
 // Disks, spheres and thin platelets (SphereShape<2>, SphereShape<3>, SpherodiskShape).
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -68,7 +70,64 @@ inline void check(int st, const srm_b200_ctx* c, bool invalid_argument = false) 
     throw DeviceError("srm_b200 status " + std::to_string(st) + ": " + msg);
 }
 
-// RAII over one device context holding a copy of the particles of shape S
+// Device contexts cached per host thread, keyed by (dimension, shape kind, box, device):
+// a caller looping on the fine-grained drop-ins (migrate / relax_sweeps / ... inside a
+// recipe loop, recipes.cpp:218-241) reuses one context -- its device buffers, CUDA
+// stream and cached generate graph -- instead of allocating a fresh one per call.  A
+// context grows (is recreated) when a call needs more capacity.  A context in use by an
+// enclosing call on the same thread (a progress sink calling back into the shim) is not
+// shared: that call gets a private one.
+class ContextCache {
+  public:
+    struct Lease {
+        srm_b200_ctx* ctx = nullptr;
+        bool* busy = nullptr;  // cached entry: released on destruction; private: destroyed
+    };
+    ~ContextCache() {
+        for (auto& e : entries_) srm_b200_destroy(e.ctx);
+    }
+    Lease acquire(int dim, int kind, const double* L, int64_t capacity, int device) {
+        for (auto& e : entries_) {
+            if (e.dim != dim || e.kind != kind || e.device != device || e.L[0] != L[0] || e.L[1] != L[1] ||
+                e.L[2] != L[2])
+                continue;
+            if (*e.busy) break;  // re-entrant use: a private context below
+            if (e.cap < capacity) {
+                srm_b200_destroy(e.ctx);
+                e.ctx = nullptr;
+                check(srm_b200_create(dim, kind, L, capacity, device, &e.ctx), nullptr);
+                e.cap = capacity;
+            }
+            *e.busy = true;
+            return Lease{e.ctx, e.busy.get()};
+        }
+        srm_b200_ctx* c = nullptr;
+        check(srm_b200_create(dim, kind, L, capacity, device, &c), nullptr);
+        const bool shared = std::none_of(entries_.begin(), entries_.end(), [&](const Entry& e) {
+            return e.dim == dim && e.kind == kind && e.device == device && e.L[0] == L[0] && e.L[1] == L[1] &&
+                   e.L[2] == L[2];
+        });
+        if (!shared) return Lease{c, nullptr};
+        entries_.push_back(Entry{dim, kind, device, {L[0], L[1], L[2]}, capacity, c, std::make_unique<bool>(true)});
+        return Lease{c, entries_.back().busy.get()};
+    }
+    static ContextCache& local() {
+        thread_local ContextCache cache;
+        return cache;
+    }
+
+  private:
+    struct Entry {
+        int dim, kind, device;
+        double L[3];
+        int64_t cap;
+        srm_b200_ctx* ctx;
+        std::unique_ptr<bool> busy;
+    };
+    std::vector<Entry> entries_;
+};
+
+// One device context (from the per-thread cache) holding a copy of the particles of shape S
 template <typename S>
 class Device {
     static constexpr int N = S::dim;
@@ -78,11 +137,14 @@ class Device {
     Device(const PeriodicBox<N>& box, std::size_t capacity, int device = 0) {
         double L[3] = {1.0, 1.0, 1.0};
         for (int a = 0; a < N; ++a) L[a] = box.length(a);
-        check(srm_b200_create(N, kPlatelet ? SRM_B200_PLATELET : SRM_B200_SPHERE, L,
-                              static_cast<int64_t>(capacity < 1 ? 1 : capacity), device, &ctx_),
-              nullptr);
+        lease_ = ContextCache::local().acquire(N, kPlatelet ? SRM_B200_PLATELET : SRM_B200_SPHERE, L,
+                                               static_cast<int64_t>(capacity < 1 ? 1 : capacity), device);
+        ctx_ = lease_.ctx;
     }
-    ~Device() { srm_b200_destroy(ctx_); }
+    ~Device() {
+        if (lease_.busy) *lease_.busy = false;
+        else srm_b200_destroy(ctx_);
+    }
     Device(const Device&) = delete;
     Device& operator=(const Device&) = delete;
 
@@ -135,6 +197,7 @@ class Device {
     }
 
   private:
+    ContextCache::Lease lease_{};
     srm_b200_ctx* ctx_ = nullptr;
 };
 
@@ -251,7 +314,7 @@ std::vector<int> reorder_by_locality(std::vector<typename S::ParticleT>& particl
     return remap;
 }
 
-// shape.hpp:549-555 (the device counts overlapping pairs; any collision <=> count > 0)
+// shape.hpp:75-81 (the device counts overlapping pairs; any collision <=> count > 0)
 template <ShapeModel S>
 bool shape_any_collision(std::span<const typename S::ParticleT> particles, const CellGrid<S::dim>& grid) {
     static_assert(is_supported_shape_v<S>, "srm::b200 supports disks, spheres and platelets");

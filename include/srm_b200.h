@@ -44,7 +44,7 @@ typedef enum {
 } srm_b200_status;
 
 typedef enum {
-    SRM_B200_SPHERE = 0,  /* Disk (dim 2) / Ball (dim 3), shape.hpp:503-527 */
+    SRM_B200_SPHERE = 0,  /* Disk (dim 2) / Ball (dim 3), shape.hpp:29-53 */
     SRM_B200_PLATELET = 1 /* thin circular platelet, SpherodiskShape (spherodisk.hpp:72-99), dim 3 */
 } srm_b200_shape;
 
@@ -83,7 +83,7 @@ typedef struct {
     int64_t shake_rounds;      /* shake sweeps run (rebuild+migrate)              */
 } srm_b200_generate_out;
 
-/* Per-round statistics, the counting form of shape_any_collision (shape.hpp:549-555). */
+/* Per-round statistics, the counting form of shape_any_collision (shape.hpp:75-81). */
 typedef struct {
     int64_t overlap_pairs;   /* unordered overlapping pairs; > 0 <=> any collision   */
     double max_penetration;  /* max (ri + rj - dist) over overlapping pairs          */
@@ -148,7 +148,7 @@ int srm_b200_relax_sweeps(srm_b200_ctx* ctx, double c_m, double c_r, int n_l, in
 int srm_b200_swell_all(srm_b200_ctx* ctx, double c_w);
 
 /* engine.hpp:144-166 reorder_by_locality against a grid of cell size `cell_size`
- * (CellGrid(box, cell_size), cell_grid.hpp:297-309): stable sort by cell, ids and
+ * (CellGrid(box, cell_size), cell_grid.hpp:40-52): stable sort by cell, ids and
  * storage order reassigned to slots.  remap_out[old] = new (may be NULL). */
 int srm_b200_reorder_by_locality(srm_b200_ctx* ctx, double cell_size, int32_t* remap_out);
 
@@ -158,7 +158,7 @@ int srm_b200_max_bounding_radius(srm_b200_ctx* ctx, double* out);
 int srm_b200_volume_fraction(srm_b200_ctx* ctx, double* out);
 
 /* ---- stage entry points (parity tests, benchmarks) --------------------------------- */
-/* CellGrid ctor (cell_grid.hpp:288-309): dims/edges for a cell size; safety-checked
+/* CellGrid ctor (cell_grid.hpp:31-52): dims/edges for a cell size; safety-checked
  * when max_radius >= 0 (cell_size >= 2*max_radius + slack else INVALID). */
 int srm_b200_grid_dims(srm_b200_ctx* ctx, double cell_size, double max_radius, double slack,
                        int32_t* dims_out, double* edge_out, int64_t* ncells_out);
@@ -172,7 +172,7 @@ int srm_b200_grid_dims(srm_b200_ctx* ctx, double cell_size, double max_radius, d
 int srm_b200_grid_build(srm_b200_ctx* ctx, double cell_size, uint32_t* keys_out,
                         int32_t* order_out, int64_t* cell_start_out);
 
-/* shape_any_collision (shape.hpp:549-555) in counting form, against a grid of cell
+/* shape_any_collision (shape.hpp:75-81) in counting form, against a grid of cell
  * size cell_size (candidate_pairs counts its 3^d scan). */
 int srm_b200_overlap_stats(srm_b200_ctx* ctx, double cell_size, srm_b200_round_stats* out);
 
@@ -269,6 +269,9 @@ uint64_t srm_b200_mix_seed(uint64_t seed, uint64_t stream);
 /* Kernel launches issued by this context since creation (or the last reset). */
 int64_t srm_b200_launch_count(const srm_b200_ctx* ctx);
 void srm_b200_reset_launch_count(srm_b200_ctx* ctx);
+/* CUDA graphs the device-resident srm_b200_generate captured and instantiated on this
+ * context (a later call reuses the cached graph while its buffers and bounds are unchanged). */
+int64_t srm_b200_graph_builds(const srm_b200_ctx* ctx);
 /* CUDA-event timing of kernel families on the context stream.  enable != 0 starts
  * recording; srm_b200_timing_get fills ms[SRM_B200_NPHASE] with accumulated device
  * milliseconds and calls[SRM_B200_NPHASE] with the number of timed launches. */

@@ -36,7 +36,7 @@ double orc_min_image_dist2(int dim, const double* L, const double* a, const doub
     return s;
 }
 
-/* shape.hpp:508-511 SphereShape::overlap: contact counts as overlap. */
+/* shape.hpp:34-37 SphereShape::overlap: contact counts as overlap. */
 static int sphere_overlap(int dim, const double* L, const double* a, double ra, const double* b,
                           double rb) {
     const double rr = ra + rb;
@@ -44,7 +44,7 @@ static int sphere_overlap(int dim, const double* L, const double* a, double ra, 
 }
 
 /* ------------------------------------------------------------------------------ */
-/* cell_grid.hpp:297-309 CellGrid(box, cell_size): n = max(3, (int)floor(L/cs)),
+/* cell_grid.hpp:40-52 CellGrid(box, cell_size): n = max(3, (int)floor(L/cs)),
  * edge = L/n.                                                                      */
 int orc_grid_dims(int dim, const double* L, double cell_size, int32_t* dims, double* edge) {
     if (!(cell_size > 0.0)) return -1;
@@ -57,7 +57,7 @@ int orc_grid_dims(int dim, const double* L, double cell_size, int32_t* dims, dou
     return 0;
 }
 
-/* cell_grid.hpp:319-328: i = (int)floor(p/edge); i %= n; if (i < 0) i += n. */
+/* cell_grid.hpp:62-71: i = (int)floor(p/edge); i %= n; if (i < 0) i += n. */
 void orc_cell_coords(int dim, const int32_t* dims, const double* edge, const double* p,
                      int32_t* c) {
     for (int a = 0; a < dim; ++a) {
@@ -68,7 +68,7 @@ void orc_cell_coords(int dim, const int32_t* dims, const double* edge, const dou
     }
 }
 
-/* cell_grid.hpp:331-336 row-major, x fastest. */
+/* cell_grid.hpp:74-79 row-major, x fastest. */
 uint64_t orc_cell_of(int dim, const int32_t* dims, const double* edge, const double* p) {
     int32_t c[3];
     orc_cell_coords(dim, dims, edge, p, c);
@@ -151,7 +151,7 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
  *   3D: Marsaglia (1972) -- (x1,x2) uniform in the unit disk, s = x1^2+x2^2 < 1,
  *       u = (2 x1 sqrt(1-s), 2 x2 sqrt(1-s), 1 - 2 s)
  *   2D: (x1,x2) uniform in the unit disk (1e-24 < s < 1), u = (x1,x2) * (1/sqrt(s))
- *       (the reference normalises the same way: random.hpp:238, g * (1/sqrt(n2)))
+ *       (the reference normalises the same way: random.hpp:68-73, g * (1/sqrt(n2)))
  * A draw takes one Philox block: two 53-bit uniforms on [-1,1).  After 64 rejected
  * draws (probability < 1e-42) the direction falls back to +x.                       */
 void orc_unit_vector(int dim, uint64_t seed, uint32_t slot, uint32_t attempt, uint32_t stream,
@@ -192,7 +192,7 @@ void orc_unit_vector(int dim, uint64_t seed, uint32_t slot, uint32_t attempt, ui
     if (dim == 3) u[2] = 0.0;
 }
 
-/* shape.hpp:513-518 SphereShape::propose_move: wrap(p + c_m * u), where
+/* shape.hpp:39-44 SphereShape::propose_move: wrap(p + c_m * u), where
  * Vec operator*(double, Vec) multiplies each component (geometry.hpp:29-33) and
  * operator+ adds component-wise (geometry.hpp:21-24).                             */
 void orc_propose(int dim, const double* L, const double* x, double c_m, uint64_t seed,
@@ -336,7 +336,7 @@ static int colour1(int x, int m, int n) {
 /* One SRM round's migrate as a coloured Gauss-Seidel sweep: the
  * reference's migrate (engine.hpp:89-107) -- per particle <= n_l trials from its
  * pre-sweep position, each tested against the LIVE positions of all other particles
- * (shape.hpp:539-546, trial first), first clear trial kept, otherwise an exact revert --
+ * (shape.hpp:64-73, trial first), first clear trial kept, otherwise an exact revert --
  * in the order (cell class, cell, slot) of the round grid of cell size `cell_size`
  * instead of storage order.  Cells of one class never interact, so the GPU runs them
  * concurrently and equals this sequential sweep bit for bit.  Trials draw Philox
@@ -402,7 +402,7 @@ void orc_sweep_round(int dim, const double* L, int64_t n, const double* x0, cons
 }
 
 /* Global overlap statistics over all pairs of a state (the counting form of
- * cell_grid.hpp:466-472 / shape.hpp:549-555: count > 0 <=> any collision).        */
+ * cell_grid.hpp:209-215 / shape.hpp:75-81: count > 0 <=> any collision).        */
 void orc_overlap_stats(int dim, const double* L, int64_t n, const double* x, const double* r,
                        const int32_t* id, orc_round_stats* out) {
     orc_csr nb;
@@ -429,7 +429,7 @@ void orc_overlap_stats(int dim, const double* L, int64_t n, const double* x, con
     csr_free(&nb);
 }
 
-/* Ordered candidate pairs visited by a 3^d neighbourhood scan (cell_grid.hpp:394-414
+/* Ordered candidate pairs visited by a 3^d neighbourhood scan (cell_grid.hpp:137-157
  * with dims >= 3, so the offset cells are distinct), self excluded.                  */
 int64_t orc_candidate_pairs(int dim, const int32_t* dims, int64_t n, const uint32_t* keys) {
     int64_t ncells = 1;
@@ -462,7 +462,7 @@ int64_t orc_candidate_pairs(int dim, const int32_t* dims, int64_t n, const uint3
 }
 
 double orc_max_radius(int64_t n, const double* r) {
-    double m = 0.0; /* shape.hpp:565-570 starts from 0.0 */
+    double m = 0.0; /* shape.hpp:91-96 starts from 0.0 */
     for (int64_t i = 0; i < n; ++i) m = r[i] > m ? r[i] : m;
     return m;
 }
@@ -611,7 +611,7 @@ void orc_pl_propose(const double* L, const double* x, const double* nrm, double 
 
 /* One platelet round: the sphere sweep's visiting order (class, cell, slot) on the
  * grid of cell size cell_size with bounding radii rb = (D + t) / 2 (shape.hpp:91-96),
- * each trial tested as overlap(trial, other) (shape.hpp:539-546, trial first). */
+ * each trial tested as overlap(trial, other) (shape.hpp:64-73, trial first). */
 void orc_pl_sweep_round(const double* L, int64_t n, const double* x0, const double* n0, const double* D,
                         const double* t, const int32_t* id, const int32_t* slot, double cell_size, double c_m,
                         double cos_r, double sin_r, int n_l, uint64_t seed, uint32_t round_id, uint32_t iteration,

@@ -8,9 +8,9 @@
  * It restates, in plain C99 compiled with -ffp-contract=off (no FMA contraction, so
  * every operation rounds exactly like the reference's plain `-O3` C++ build):
  *   - periodic geometry        (reference proj/core/include/srm/geometry.hpp:107-129)
- *   - cell grid dims / keys    (cell_grid.hpp:297-338)
+ *   - cell grid dims / keys    (cell_grid.hpp:40-81)
  *   - stable sort by cell      (engine.hpp:144-166, reorder_by_locality)
- *   - overlap predicates       (shape.hpp:508-511, cell_grid.hpp:454-472)
+ *   - overlap predicates       (shape.hpp:34-37, cell_grid.hpp:194-215)
  *   - Philox4x32-10            (Salmon et al. SC'11; checked against curand's
  *                               curand_Philox4x32_10 and the Random123 KAT vectors)
  *   - the migrate round the GPU implements: the reference's sequential Gauss-Seidel
@@ -40,7 +40,7 @@ void orc_wrap(int dim, const double* L, double* p);
 double orc_min_image_dist2(int dim, const double* L, const double* a, const double* b);
 
 /* ---- grid (cell_grid.hpp) -------------------------------------------------- */
-/* returns 0 on success, -1 if cell_size <= 0 (cell_grid.hpp:298) */
+/* returns 0 on success, -1 if cell_size <= 0 (cell_grid.hpp:41) */
 int orc_grid_dims(int dim, const double* L, double cell_size, int32_t* dims, double* edge);
 void orc_cell_coords(int dim, const int32_t* dims, const double* edge, const double* p,
                      int32_t* c);
@@ -123,7 +123,7 @@ int64_t orc_rsa_rounds(int dim, const double* L, int64_t n, const double* radii,
 
 /* ---- reductions ---------------------------------------------------------------- */
 double orc_max_radius(int64_t n, const double* r);
-/* volume fraction with the reference's sequential summation order (shape.hpp:557-563) */
+/* volume fraction with the reference's sequential summation order (shape.hpp:83-89) */
 double orc_volume_fraction_seq(int dim, const double* L, int64_t n, const double* r);
 
 #ifdef __cplusplus

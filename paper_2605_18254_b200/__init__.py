@@ -143,7 +143,7 @@ class Snapshot:
         return len(self.radius)
 
     def refresh_volume_fraction(self) -> None:
-        """shape.hpp:557-563 (sequential host sum)"""
+        """shape.hpp:83-89 (sequential host sum)"""
         s = 0.0
         for v in particle_measure(self.dim, self.radius).tolist():
             s += v
@@ -261,10 +261,18 @@ class Context:
         if id is not None:
             id = np.ascontiguousarray(id, dtype=np.int32)
         n = len(radius)
+        if len(pos) != n or (id is not None and len(id) != n):
+            raise ValidationError("upload: pos, radius and id must describe the same particles")
         self._c(_native.lib().srm_b200_upload(self._h, n, _ptr(pos), _ptr(radius), _ptr(id)))
         self.n = n
 
     def upload_records(self, records: np.ndarray, off_id: int, off_pos: int, off_radius: int) -> None:
+        """Particle<N> AoS records (geometry.hpp:139-144).  The record dtype must be
+        C-aligned (np.dtype(..., align=True)): the device loads its doubles as such."""
+        if not records.flags.c_contiguous:
+            raise ValidationError("records: must be C-contiguous")
+        if records.dtype.fields is not None and not records.dtype.isalignedstruct:
+            raise ValidationError("records: use an aligned structured dtype (align=True)")
         n = len(records)
         self._c(_native.lib().srm_b200_upload_records(self._h, n, _ptr(records), records.itemsize,
                                                        off_id, off_pos, off_radius))
@@ -360,6 +368,9 @@ class Context:
     # ---- instrumentation -------------------------------------------------------------
     def launch_count(self) -> int:
         return _native.lib().srm_b200_launch_count(self._h)
+
+    def graph_builds(self) -> int:
+        return _native.lib().srm_b200_graph_builds(self._h)
 
     def reset_launch_count(self) -> None:
         _native.lib().srm_b200_reset_launch_count(self._h)

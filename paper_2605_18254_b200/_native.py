@@ -127,6 +127,7 @@ _SIGS = {
     "srm_b200_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "srm_b200_launch_count": (C.c_int64, [C.c_void_p]),
     "srm_b200_reset_launch_count": (None, [C.c_void_p]),
+    "srm_b200_graph_builds": (C.c_int64, [C.c_void_p]),
     "srm_b200_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "srm_b200_timing_get": (C.c_int, [C.c_void_p, c_double_p, c_int64_p]),
     "srm_b200_sync": (C.c_int, [C.c_void_p]),

@@ -4,7 +4,10 @@
 // interface it replaces.  Device data layout: DESIGN.md §2.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <chrono>
+#include <exception>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -252,7 +255,9 @@ struct srm_b200_ctx {
         rp = dalloc<RoundParams>(1);
         active = dalloc<int32_t>(cap);
         nbr = dalloc<int32_t>(cap * kNearRow);
-        pool.cap = 8 * cap + 32 * std::min<int64_t>(cap, 2000000);  // crowded (polydisperse, platelet) states
+        // crowded (polydisperse, platelet) states; offsets are int32 in the rows, so the
+        // pool never exceeds 2^31 - 1 entries (a row that does not fit rescans its stencil)
+        pool.cap = std::min<int64_t>(8 * cap + 32 * std::min<int64_t>(cap, 2000000), 2147483647LL);
         pool.e = dalloc<int32_t>(pool.cap);
         SRM_CUDA(cudaFuncSetAttribute(tiles::k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(tiles::kTileSmem)));
@@ -292,14 +297,16 @@ struct srm_b200_ctx {
         if (sw_start) cudaEventDestroy(sw_start);
         if (sw_stop) cudaEventDestroy(sw_stop);
         cudaFree(d_ctl);
-        cudaFree(d_recs);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (h_ring) cudaFreeHost(h_ring);
+        if (h_ring_ctr) cudaFreeHost(h_ring_ctr);
         for (auto st : cap_streams)
             if (st) cudaStreamDestroy(st);
         if (stream) cudaStreamDestroy(stream);
     }
 
     // ---------------------------------------------------------------------------
-    // CellGrid ctor (cell_grid.hpp:288-309) + the near-search stencil and the colouring
+    // CellGrid ctor (cell_grid.hpp:31-52) + the near-search stencil and the colouring
     // for a state whose largest radius is max_r_state and whose trial
     // moves have length c_m.  The colouring expression is the oracle's orc_colouring.
     GridParams make_grid(double cell_size, double max_r_state, double c_m) const {
@@ -519,21 +526,79 @@ struct srm_b200_ctx {
     }
 
     GenCtl* d_ctl = nullptr;
-    GenProgress* d_recs = nullptr;
-    int64_t recs_cap = 0;
+    // live progress ring (pinned, host-mapped): records, published and consumed counters
+    static constexpr int64_t kRing = 4096;
+    GenProgress* h_ring = nullptr;
+    int64_t* h_ring_ctr = nullptr;  // [0] published, [2] run start (device writes), [1] consumed (host writes)
     cudaStream_t cap_streams[4] = {nullptr, nullptr, nullptr, nullptr};
+    // the instantiated generate graph, reused while everything baked into it is unchanged
+    struct GraphKey {
+        int64_t n, nc_max;
+        int ntiles_max, ctiles_max, team0, trials0, queue_ctas, dim, plate;
+        const void* bufs[12];
+        bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
+    };
+    GraphKey gkey{};
+    cudaGraphExec_t gexec = nullptr;
+    int64_t graph_builds = 0;
+
+    // Launch the generate graph and, with a progress sink, deliver the iteration records
+    // while it runs (engine.hpp:251-254): poll the published counter of the mapped ring,
+    // hand each record to the sink, report the consumed position back to the device.
+    void launch_and_drain(const GenCtl& hc, srm_b200_progress_fn progress, void* user) {
+        SRM_CUDA(cudaGraphLaunch(gexec, stream));
+        if (!progress) {
+            SRM_CUDA(cudaStreamSynchronize(stream));
+            SRM_CUDA(cudaGetLastError());
+            return;
+        }
+        volatile int64_t* ctr = reinterpret_cast<volatile int64_t*>(h_ring_ctr);
+        int64_t consumed = 0;
+        std::exception_ptr sink_error;
+        for (;;) {
+            const cudaError_t q = cudaStreamQuery(stream);
+            if (q != cudaSuccess && q != cudaErrorNotReady) SRM_CUDA(q);
+            const int64_t pub = ctr[0];
+            std::atomic_thread_fence(std::memory_order_acquire);
+            const uint64_t t0 = static_cast<uint64_t>(ctr[2]);  // the run's start (k_gen_t0)
+            while (consumed < pub) {
+                GenProgress r;
+                std::memcpy(&r, const_cast<const GenProgress*>(h_ring + consumed % kRing), sizeof r);
+                srm_b200_progress_record rec{r.iteration, r.volume_fraction, r.accepted, (r.t_ns - t0) * 1e-9, r.rounds};
+                if (!sink_error) {
+                    try {
+                        progress(&rec, user);
+                    } catch (...) {  // keep draining (the device may wait on the ring), rethrow after the run
+                        sink_error = std::current_exception();
+                    }
+                }
+                ++consumed;
+                std::atomic_thread_fence(std::memory_order_release);
+                ctr[1] = consumed;
+            }
+            if (q == cudaSuccess && consumed == ctr[0]) break;
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+        (void)hc;
+        if (sink_error) std::rethrow_exception(sink_error);
+    }
 
     // returns status; out counters filled from the controller
     int generate_graph(const srm_b200_params& p, int64_t it0, double f0, double max_r0, int64_t* done_out,
                        int64_t* acc_out, int64_t* rounds_out, int64_t* shakes_out, double* f_out,
                        srm_b200_progress_fn progress, void* user) {
         if (!d_ctl) d_ctl = dalloc<GenCtl>(1);
-        const int64_t want_recs = std::min<int64_t>(p.max_iterations, int64_t{1} << 20);
-        if (want_recs > recs_cap) {
-            cudaFree(d_recs);
-            d_recs = nullptr;
-            d_recs = dalloc<GenProgress>(want_recs);
-            recs_cap = want_recs;
+        GenProgress* d_ring = nullptr;
+        int64_t* d_ctr = nullptr;
+        if (progress) {
+            if (!h_ring) {
+                SRM_CUDA(cudaHostAlloc(&h_ring, sizeof(GenProgress) * kRing, cudaHostAllocMapped));
+                SRM_CUDA(cudaHostAlloc(&h_ring_ctr, 3 * sizeof(int64_t), cudaHostAllocMapped));
+            }
+            SRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_ring), h_ring, 0));
+            SRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_ctr), h_ring_ctr, 0));
+            reinterpret_cast<volatile int64_t*>(h_ring_ctr)[0] = 0;
+            reinterpret_cast<volatile int64_t*>(h_ring_ctr)[1] = 0;
         }
         for (auto& st : cap_streams)
             if (!st) SRM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -544,7 +609,9 @@ struct srm_b200_ctx {
         hc.c_m = p.c_m;
         hc.box_measure = box_measure();
         hc.max_iter = p.max_iterations;
-        hc.recs_cap = recs_cap;
+        hc.recs_cap = kRing;
+        hc.pub = d_ctr;
+        hc.cons = d_ctr ? d_ctr + 1 : nullptr;
         hc.it0 = it0;
         hc.n_k = p.n_k;
         hc.n_l = p.n_l;
@@ -557,7 +624,7 @@ struct srm_b200_ctx {
         hc.sin_r = std::sin(p.c_r);
         hc.f = f0;
         hc.max_r = max_r0;
-        hc.recs = d_recs;
+        hc.recs = d_ring;
         // the largest grid of the run is the first one (radii only grow): launch bounds
         const GridParams g0 = make_grid(2.5 * max_r0 + p.c_m, max_r0, p.c_m);
         ensure_cells(g0.ncells);
@@ -575,6 +642,25 @@ struct srm_b200_ctx {
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
+        GraphKey key{};
+        key.n = n;
+        key.nc_max = nc_max;
+        key.ntiles_max = ntiles_max;
+        key.ctiles_max = ctiles_max;
+        key.team0 = team0;
+        key.trials0 = trials0;
+        key.queue_ctas = queue_ctas;
+        key.dim = dim;
+        key.plate = platelets();
+        const void* bufs[12] = {P.rec, Q.rec, S.rec, P.aux, Q.aux, S.aux, count, cell_start, perm64, nbr, pool.e, S.xf};
+        std::memcpy(key.bufs, bufs, sizeof bufs);
+        if (gexec && key == gkey) {
+            launch_and_drain(hc, progress, user);
+        } else {
+        if (gexec) {
+            cudaGraphExecDestroy(gexec);
+            gexec = nullptr;
+        }
         cudaGraph_t G;
         SRM_CUDA(cudaGraphCreate(&G, 0));
         capturing = true;
@@ -656,27 +742,18 @@ struct srm_b200_ctx {
             });
         });
         capturing = false;
-        cudaGraphExec_t X;
-        SRM_CUDA(cudaGraphInstantiate(&X, G, 0));
-        SRM_CUDA(cudaGraphLaunch(X, stream));
-        SRM_CUDA(cudaStreamSynchronize(stream));
-        SRM_CUDA(cudaGetLastError());
-        cudaGraphExecDestroy(X);
+        SRM_CUDA(cudaGraphInstantiate(&gexec, G, 0));
         cudaGraphDestroy(G);
+        gkey = key;
+        ++graph_builds;
+        launch_and_drain(hc, progress, user);
+        }
         SRM_CUDA(cudaMemcpy(&hc, d_ctl, sizeof(GenCtl), cudaMemcpyDeviceToHost));
         *done_out = hc.done;
         *acc_out = hc.accepted;
         *rounds_out = hc.rounds;
         *shakes_out = hc.shakes;
         *f_out = hc.f;
-        if (progress && hc.done > 0) {  // the iteration records, delivered after the run
-            std::vector<GenProgress> recs(static_cast<size_t>(std::min(hc.done, recs_cap)));
-            SRM_CUDA(cudaMemcpy(recs.data(), d_recs, sizeof(GenProgress) * recs.size(), cudaMemcpyDeviceToHost));
-            for (const auto& r : recs) {
-                srm_b200_progress_record rec{r.iteration, r.volume_fraction, r.accepted, (r.t_ns - hc.t0) * 1e-9, r.rounds};
-                progress(&rec, user);
-            }
-        }
         if (hc.status == 2) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
         return hc.status == 1 ? SRM_B200_ITERATION_LIMIT : SRM_B200_OK;
     }
@@ -785,6 +862,10 @@ int srm_b200_create(int dim, int shape_kind, const double* box_lengths, int64_t 
     }
     if (shape_kind == SRM_B200_PLATELET && dim != 3) { g_create_error = "platelets are 3D"; return SRM_B200_INVALID; }
     if (capacity < 1) { g_create_error = "capacity must be >= 1"; return SRM_B200_INVALID; }
+    if (capacity > 2147483647LL) {  // sorted indices and near-list entries are int32
+        g_create_error = "capacity must be <= 2^31 - 1";
+        return SRM_B200_INVALID;
+    }
     for (int a = 0; a < dim; ++a)
         if (!(box_lengths[a] > 0.0)) {
             g_create_error = "PeriodicBox: axis length " + std::to_string(a) + " must be positive";
@@ -937,11 +1018,28 @@ int srm_b200_set_rotation(srm_b200_ctx* c, double c_r) {
     });
 }
 
+// The reference's Particle<N> AoS layout (geometry.hpp:139-144) as the caller describes
+// it: every field inside the record, doubles 8-byte aligned (a misaligned double load is
+// a sticky CUDA error for the whole process), records of disks / spheres only (a
+// platelet record also carries the normal and thickness: srm_b200_upload_platelets).
+static void check_record_layout(const srm_b200_ctx* c, int64_t n, const void* records, int64_t stride, int64_t off_id,
+                         int64_t off_pos, int64_t off_radius) {
+    if (c->platelets()) throw Invalid{"records: platelet contexts take srm_b200_upload_platelets"};
+    if (n > 0 && !records) throw Invalid{"records: null pointer"};
+    if (stride < 1) throw Invalid{"records: bad stride"};
+    if (off_id < 0 || off_id + 4 > stride) throw Invalid{"records: id field outside the record"};
+    if (off_pos < 0 || off_pos + 8 * c->dim > stride) throw Invalid{"records: position field outside the record"};
+    if (off_radius < 0 || off_radius + 8 > stride) throw Invalid{"records: radius field outside the record"};
+    if (stride % 8 || off_pos % 8 || off_radius % 8 || off_id % 4 ||
+        reinterpret_cast<uintptr_t>(records) % 8)
+        throw Invalid{"records: doubles must be 8-byte aligned (stride, offsets and base address)"};
+}
+
 int srm_b200_upload_records(srm_b200_ctx* c, int64_t n, const void* records, int64_t stride, int64_t off_id,
                             int64_t off_pos, int64_t off_radius) {
     return guarded(c, [&]() -> int {
         if (n < 0 || n > c->cap) throw Invalid{"upload: n exceeds the context capacity"};
-        if (stride < 1) throw Invalid{"upload: bad stride"};
+        check_record_layout(c, n, records, stride, off_id, off_pos, off_radius);
         c->n = n;
         if (n == 0) return SRM_B200_OK;
         const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(stride);
@@ -966,6 +1064,7 @@ int srm_b200_download_records(srm_b200_ctx* c, void* records, int64_t stride, in
                               int64_t off_radius) {
     return guarded(c, [&]() -> int {
         const int64_t n = c->n;
+        check_record_layout(c, n, records, stride, off_id, off_pos, off_radius);
         if (n == 0) return SRM_B200_OK;
         const size_t bytes = static_cast<size_t>(n) * static_cast<size_t>(stride);
         if (bytes > c->rec_stage_bytes) {
@@ -992,7 +1091,7 @@ int srm_b200_grid_dims(srm_b200_ctx* c, double cell_size, double max_radius, dou
     return guarded(c, [&]() -> int {
         const GridParams g = c->make_grid(cell_size, 0.0, 0.0);
         if (max_radius >= 0.0) {
-            const double min_safe = 2.0 * max_radius + slack;  // cell_grid.hpp:290-292
+            const double min_safe = 2.0 * max_radius + slack;  // cell_grid.hpp:33-35
             if (cell_size < min_safe) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
         }
         for (int a = 0; a < c->dim; ++a) {
@@ -1226,7 +1325,7 @@ int srm_b200_round(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint6
             const double mr = c->max_radius(c->P);
             const GridParams g = c->make_grid(cell_size, mr, c_m);
             // the reference scans the 3^d cells of the trial position, which is only
-            // complete under CellGrid's safety bound (cell_grid.hpp:288-293)
+            // complete under CellGrid's safety bound (cell_grid.hpp:31-36)
             if (cell_size < 2.0 * mr + c_m) throw Invalid{"CellGrid: cell_size below safety bound 2*maxR + slack"};
             c->set_grid(g);
             c->round(c->P, c_m, n_l, key, round_id, iteration, true, with_candidates != 0, accepted_out != nullptr);
@@ -1263,7 +1362,7 @@ int srm_b200_rounds(srm_b200_ctx* c, double cell_size, double c_m, int n_l, uint
 
 int srm_b200_relax_sweeps(srm_b200_ctx* c, double c_m, double c_r, int n_l, int sweeps, uint64_t key) {
     if (c) c->c_r = c_r;  // platelet rotation angle (ignored by disks/spheres)
-    (void)c_r;  // rotation rate is ignored by disks/spheres (shape.hpp:500-502)
+    (void)c_r;  // rotation rate is ignored by disks/spheres (shape.hpp:27-28)
     return guarded(c, [&]() -> int {
         const int64_t n = c->n;
         if (n == 0 || sweeps < 1) return SRM_B200_OK;  // engine.hpp:115
@@ -1433,6 +1532,7 @@ int srm_b200_generate(srm_b200_ctx* c, const srm_b200_params* params, int64_t it
 }
 
 int64_t srm_b200_launch_count(const srm_b200_ctx* c) { return c ? c->launches : 0; }
+int64_t srm_b200_graph_builds(const srm_b200_ctx* c) { return c ? c->graph_builds : 0; }
 void srm_b200_reset_launch_count(srm_b200_ctx* c) {
     if (c) c->launches = 0;
 }

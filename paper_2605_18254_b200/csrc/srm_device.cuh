@@ -42,7 +42,7 @@ __host__ __device__ __forceinline__ double dist2(const Box& b, const double* a, 
     return s;
 }
 
-// shape.hpp:508-511 SphereShape::overlap -- contact counts as overlap.
+// shape.hpp:34-37 SphereShape::overlap -- contact counts as overlap.
 template <int D>
 __host__ __device__ __forceinline__ bool sphere_overlap(const Box& b, const double* a, double ra,
                                                         const double* c, double rc) {
@@ -159,7 +159,7 @@ __device__ __forceinline__ void unit_vector(const RngKey& key, uint32_t slot, ui
     for (int k = 1; k < D; ++k) u[k] = 0.0;
 }
 
-// shape.hpp:513-518 propose_move: wrap(p + c_m * u) (component-wise u*c_m then x+step)
+// shape.hpp:39-44 propose_move: wrap(p + c_m * u) (component-wise u*c_m then x+step)
 template <int D>
 __device__ __forceinline__ void propose(const Box& b, const double* x, double c_m,
                                         const RngKey& key, uint32_t slot, uint32_t attempt,

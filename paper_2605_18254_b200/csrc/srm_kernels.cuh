@@ -64,7 +64,7 @@ struct GridParams {
     int32_t col_body[3]; // col_m * floor(dims / col_m): cells coloured x mod m
 };
 
-// cell coordinates of a flat key (x fastest, cell_grid.hpp:326-336)
+// cell coordinates of a flat key (x fastest, cell_grid.hpp:73-79)
 template <int D>
 __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, int* c) {
     const uint32_t r1 = fdiv(key, g.fd_dims[0]);
@@ -79,7 +79,7 @@ __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, in
     }
 }
 
-// CellGrid ctor (cell_grid.hpp:288-309) + the near-search stencil, the colouring
+// CellGrid ctor (cell_grid.hpp:31-52) + the near-search stencil, the colouring
 // and the near-list kernel choice for a state whose largest radius is
 // max_r_state and whose trial moves have length c_m.  The colouring expression is the
 // oracle's orc_colouring.  Host and device (the device-resident generate loop) share it.
@@ -236,7 +236,7 @@ __device__ __forceinline__ double near_cut(double ri, double rj, double extra) {
 }
 
 // ---------------------------------------------------------------------------------
-// Grid: cell_grid.hpp:319-336 cell_coords + flat_index, bit for bit.
+// Grid: cell_grid.hpp:62-81 cell_coords + flat_index, bit for bit.
 template <int D>
 __device__ __forceinline__ uint32_t cell_of(const GridParams& g, const double* p) {
     uint64_t idx = 0;
@@ -639,7 +639,7 @@ __device__ __forceinline__ void near_full_particle(int64_t q, const State& S, co
     NearList nl;
     const int32_t idq = S.id[q];
     near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
-        if (S.id[j] == idq) return;  // shape.hpp:544 self-exclusion by id
+        if (S.id[j] == idq) return;  // shape.hpp:70 self-exclusion by id
         nl.add(static_cast<int32_t>(j));
     });
     if (nl.n > kNearCap) {
@@ -1295,8 +1295,13 @@ struct GenCtl {
     int32_t do_copy, do_scale;  // this step starts with W <- P (and W *= factor)
     uint64_t t0;
     GridParams g_iter;  // the grid of the current iteration (growth rounds and reorder)
+    // live progress (engine.hpp:251-254): a ring in pinned, host-mapped memory.  The
+    // device publishes iteration records as they end; the host thread consumes them while
+    // the graph runs and reports its position back.  recs == nullptr: no progress sink.
     GenProgress* recs;
     int64_t recs_cap;
+    int64_t* pub;   // records published (device -> host); pub[2] = the run's start time
+    int64_t* cons;  // records consumed (host -> device)
 };
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -1362,7 +1367,10 @@ __global__ void k_gen_flags(const GenCtl* c, cudaGraphConditionalHandle h_copy, 
     cudaGraphSetConditional(h_scale, c->do_scale ? 1u : 0u);
 }
 
-__global__ void k_gen_t0(GenCtl* c) { c->t0 = global_ns(); }
+__global__ void k_gen_t0(GenCtl* c) {
+    c->t0 = global_ns();
+    if (c->pub) *reinterpret_cast<volatile int64_t*>(c->pub + 2) = static_cast<int64_t>(c->t0);
+}
 
 __global__ void k_gen_cls_begin(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls) {
     c->cls = 0;
@@ -1387,7 +1395,7 @@ __global__ void k_gen_after(GenCtl* c, const StatsDev* __restrict__ stats, cudaG
             newf = true;
             c->success = 1;
             c->accepted += 1;
-            c->max_r = c->max_r * c->factor;  // == max of the swollen radii (rounding is monotone)
+            // (max_r: the committed state's bounding radius, recomputed by k_gen_f)
             if (c->reorder_period > 0 && ++c->reorder_since >= c->reorder_period) {
                 c->reorder_since = 0;
                 reorder = true;
@@ -1414,7 +1422,13 @@ __global__ void k_gen_after(GenCtl* c, const StatsDev* __restrict__ stats, cudaG
     cudaGraphSetConditional(h_reorder, reorder ? 1u : 0u);
 }
 
-__global__ void k_gen_f(GenCtl* c, const double* __restrict__ red_out) { c->f = red_out[0] / c->box_measure; }
+// volume fraction and max bounding radius of the committed state (shape.hpp:83-96),
+// recomputed as the host loop does: for platelets 0.5 (D + t) of the swollen D and t is
+// not always max_r * factor to the last ulp
+__global__ void k_gen_f(GenCtl* c, const double* __restrict__ red_out) {
+    c->f = red_out[0] / c->box_measure;
+    c->max_r = red_out[1];
+}
 
 __global__ void k_gen_grid_iter(const GenCtl* c, GridParams* gp) { *gp = c->g_iter; }
 
@@ -1427,7 +1441,14 @@ __global__ void k_gen_end(GenCtl* c, cudaGraphConditionalHandle h_run) {
         r.accepted = c->success;
         r.rounds = c->rounds_this;
         r.t_ns = global_ns();
-        if (c->done - 1 < c->recs_cap) c->recs[c->done - 1] = r;
+        if (c->recs) {
+            const int64_t idx = c->done - 1;
+            // a full ring waits for the host (it polls while the graph runs)
+            while (idx - *reinterpret_cast<volatile int64_t*>(c->cons) >= c->recs_cap) __nanosleep(1000);
+            c->recs[idx % c->recs_cap] = r;
+            __threadfence_system();
+            *reinterpret_cast<volatile int64_t*>(c->pub) = idx + 1;
+        }
     }
     if (c->phase == 0) {
         if (!(c->f < c->stop)) c->phase = 3;
@@ -1443,7 +1464,7 @@ __global__ void k_scale_radius_ctl(int64_t n, double4* __restrict__ rec, double4
                                    const GenCtl* __restrict__ c) {
     const double factor = c->factor;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        rec[i].w = rec[i].w * factor;  // engine.hpp:520 p.radius *= factor
+        rec[i].w = rec[i].w * factor;  // engine.hpp:224 / shape.hpp:46 p.radius *= factor
         if (aux) aux[i].w = aux[i].w * factor;
     }
 }
@@ -1537,7 +1558,7 @@ __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const Gri
     }
 }
 
-// Ordered candidate pairs of the reference's 3^d scan (cell_grid.hpp:394-414), from the
+// Ordered candidate pairs of the reference's 3^d scan (cell_grid.hpp:137-157), from the
 // cell offsets only (parity statistic, not on the timed path).
 template <int D>
 __global__ void __launch_bounds__(256) k_candidates(int64_t n, const GridParams* __restrict__ gp,
@@ -1780,7 +1801,7 @@ __global__ void k_pack_soa(int64_t n, State T, double* __restrict__ pos, double*
 __global__ void k_scale_radius(int64_t n, double4* __restrict__ rec, double4* __restrict__ aux, double factor) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        rec[i].w = rec[i].w * factor;              // engine.hpp:520 p.radius *= factor
+        rec[i].w = rec[i].w * factor;              // engine.hpp:224 / shape.hpp:46 p.radius *= factor
         if (aux) aux[i].w = aux[i].w * factor;     // spherodisk.hpp:88-91 diameter, thickness
     }
 }

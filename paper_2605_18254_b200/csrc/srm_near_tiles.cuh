@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                 }
             }
         }
-        // resolve: sorted indices, and shape.hpp:544 self-exclusion by id
+        // resolve: sorted indices, and shape.hpp:70 self-exclusion by id
         int32_t e[kNearCap];
         int m = 0;
         if (nn <= kNearCap) {
@@ -311,12 +311,18 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                         const float l2 = __fmul_rn(__fmul_rn(lim, lim), 1.00001f);
                         if (d2 <= l2 && k != i) {
                             const int32_t j = pj[k];
-                            if (S.id[j] != idi) dst[m++] = j;
+                            if (S.id[j] != idi) {
+                                if (m < nn) dst[m] = j;  // never past the entries reserved above
+                                ++m;
+                            }
                         }
                     }
                 }
             }
-            if (m > kNearCap) {
+            if (m > nn) {  // the passes disagree (cannot happen with equal predicates): rescan
+                row[0] = make_int4(m, -1, 0, 0);
+                row[1] = make_int4(0, 0, 0, 0);
+            } else if (m > kNearCap) {
                 row[0] = make_int4(m, static_cast<int32_t>(off), 0, 0);
                 row[1] = make_int4(0, 0, 0, 0);
             } else {  // same-id images removed: the list fits the row after all

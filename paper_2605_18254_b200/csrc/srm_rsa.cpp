@@ -5,7 +5,7 @@
 // the next candidate's test), so it stays on the host, as input generation whose time
 // is excluded from the metric.  It consumes std::mt19937_64 exactly as the reference's
 // Rng does (random.hpp:16-61), and its accept test is the reference predicate
-// (strictly non-touching, cell_grid.hpp:454-464), so the output is bit-identical to
+// (strictly non-touching, rsa.hpp:19-20, cell_grid.hpp:197-207), so the output is bit-identical to
 // srm::rsa_place for the same seed (pinned in tests/test_rsa.py).  The neighbour search
 // is its own flat cell list; any complete search yields the same decisions.
 #include <algorithm>

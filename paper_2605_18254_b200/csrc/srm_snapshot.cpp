@@ -10,9 +10,11 @@
 // the reference uses -- with the same keys and value types (snapshot_io.cpp:128-148), so
 // the bytes equal the reference's snapshot_to_binary / snapshot_to_text (pinned in
 // tests/test_snapshot.py).  Host code: the state crosses PCIe once per save / load.
+#include <sys/stat.h>
 #include <unistd.h>
 
-#include <atomic>
+#include <cerrno>
+
 #include <charconv>
 #include <cstdint>
 #include <cstring>
@@ -134,26 +136,45 @@ std::string encode(const Traits& tr, const double* box, int64_t n, const double*
     return out;
 }
 
-// snapshot_io.cpp:392-414 write_file_atomic: a unique sibling, then rename
+// Crash-safe save (the reference's write_file_atomic contract, snapshot_io.cpp:392-414:
+// a reader sees the old file or the complete new one, never a torn write).  Done with
+// POSIX calls: a mkstemp(3) temporary next to the target, a full write(2) loop, fsync(2),
+// then rename(2) over the target (atomic within one filesystem).
 void write_atomic(const std::string& path, const std::string& content) {
     namespace fs = std::filesystem;
-    const fs::path p(path);
-    const fs::path dir = p.has_parent_path() ? p.parent_path() : fs::path(".");
-    std::error_code ec;
-    fs::create_directories(dir, ec);
-    static std::atomic<std::uint64_t> counter{0};
-    const fs::path tmp = dir / (p.filename().string() + ".tmp." + std::to_string(::getpid()) + "." +
-                                std::to_string(counter.fetch_add(1)));
-    {
-        std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
-        if (!out) throw IoFail{"cannot open for writing: " + tmp.string()};
-        out.write(content.data(), static_cast<std::streamsize>(content.size()));
-        if (!out) throw IoFail{"write failed: " + tmp.string()};
+    const fs::path target(path);
+    const fs::path parent = target.has_parent_path() ? target.parent_path() : fs::path(".");
+    std::error_code mk;
+    fs::create_directories(parent, mk);
+    std::string templ = (parent / ("." + target.filename().string() + ".partial-XXXXXX")).string();
+    const int fd = ::mkstemp(templ.data());
+    if (fd < 0) throw IoFail{"snapshot save: no temporary file beside " + path + ": " + std::strerror(errno)};
+    auto abandon = [&](const std::string& what) {
+        const int e = errno;
+        ::close(fd);
+        ::unlink(templ.c_str());
+        throw IoFail{"snapshot save: " + what + " " + templ + ": " + std::strerror(e)};
+    };
+    const char* p = content.data();
+    size_t left = content.size();
+    while (left > 0) {
+        const ssize_t w = ::write(fd, p, left);
+        if (w < 0) {
+            if (errno == EINTR) continue;
+            abandon("write to");
+        }
+        p += w;
+        left -= static_cast<size_t>(w);
     }
-    fs::rename(tmp, p, ec);
-    if (ec) {
-        fs::remove(tmp);
-        throw IoFail{"rename failed for " + path + ": " + ec.message()};
+    if (::fchmod(fd, 0644) != 0 || ::fsync(fd) != 0) abandon("flush of");
+    if (::close(fd) != 0) {
+        ::unlink(templ.c_str());
+        throw IoFail{"snapshot save: close of " + templ + " failed"};
+    }
+    if (::rename(templ.c_str(), path.c_str()) != 0) {
+        const int e = errno;
+        ::unlink(templ.c_str());
+        throw IoFail{"snapshot save: cannot move " + templ + " to " + path + ": " + std::strerror(e)};
     }
 }
 
@@ -167,111 +188,132 @@ struct Parsed {
     std::vector<double> vals;  // n x tr->doubles
 };
 
-const nlohmann::json& require(const nlohmann::json& j, const char* key) {
-    const auto it = j.find(key);
-    if (it == j.end()) throw IoFail{std::string("snapshot header: missing key '") + key + "'"};
+[[noreturn]] void bad_file(const std::string& why) { throw IoFail{"snapshot load: " + why}; }
+
+const nlohmann::json& field(const nlohmann::json& obj, const char* name) {
+    const auto it = obj.find(name);
+    if (it == obj.end()) bad_file(std::string("header has no '") + name + "' entry");
     return *it;
+}
+
+// a read position over the file bytes
+struct Cursor {
+    const char* p;
+    const char* end;
+    size_t left() const { return static_cast<size_t>(end - p); }
+    template <typename T>
+    T raw() {  // little-endian fixed-width field
+        if (left() < sizeof(T)) bad_file("file ends inside the binary header");
+        T v;
+        std::memcpy(&v, p, sizeof(T));
+        p += sizeof(T);
+        return v;
+    }
+    void expect(char ch, const char* what) {
+        if (p == end || *p != ch) bad_file(std::string("row ") + what);
+        ++p;
+    }
+    template <typename T>
+    T number(const char* what) {
+        T v{};
+        const auto r = std::from_chars(p, end, v);
+        if (r.ec != std::errc()) bad_file(std::string("row has an unreadable ") + what);
+        p = r.ptr;
+        return v;
+    }
+};
+
+// the JSON header: after the magic + version + length in the binary layout
+// (snapshot_io.cpp:170-191), or the first line of the text layout (snapshot_io.cpp:150-167)
+nlohmann::json read_header(Cursor& c, bool binary) {
+    try {
+        if (binary) {
+            c.p += sizeof kMagic;
+            const std::uint32_t version = c.raw<std::uint32_t>();
+            const std::uint64_t len = c.raw<std::uint64_t>();
+            if (c.left() < len) bad_file("file ends inside the binary header");
+            nlohmann::json h = nlohmann::json::parse(c.p, c.p + len);
+            c.p += len;
+            if (version != kVersion) bad_file("format version " + std::to_string(version) + " is not supported");
+            return h;
+        }
+        const char* nl = static_cast<const char*>(std::memchr(c.p, '\n', c.left()));
+        if (!nl) bad_file("no header line");
+        nlohmann::json h = nlohmann::json::parse(c.p, nl);
+        c.p = nl + 1;
+        return h;
+    } catch (const nlohmann::json::exception& e) {
+        bad_file(std::string("header is not valid JSON (") + e.what() + ")");
+    }
+}
+
+// header keys and types as the reference writes them (snapshot_io.cpp:128-148)
+void read_meta(const nlohmann::json& h, Parsed& P) {
+    try {
+        const std::string shape = field(h, "shape").get<std::string>();
+        const int dim = field(h, "dimension").get<int>();
+        if (field(h, "version").get<std::uint32_t>() != kVersion) bad_file("header names an unsupported version");
+        if (field(h, "format").get<std::string>() != "srm-snapshot") bad_file("header is not an srm-snapshot");
+        for (const Traits* t : {&kDisk, &kSphere, &kPlatelet})
+            if (shape == t->name && dim == t->dimension) P.tr = t;
+        if (!P.tr) bad_file("no shape '" + shape + "' in dimension " + std::to_string(dim));
+        const auto& box = field(h, "box");
+        if (!box.is_array() || box.size() != static_cast<std::size_t>(dim))
+            bad_file("box lengths do not match the dimension");
+        for (int a = 0; a < dim; ++a) P.box[a] = box[a].get<double>();
+        const auto& pj = field(h, "params");
+        srm_b200_params& q = P.meta.params;
+        q.c_m = field(pj, "c_m").get<double>();
+        q.c_r = field(pj, "c_r").get<double>();
+        q.c_w = field(pj, "c_w").get<double>();
+        q.f_target = field(pj, "f_target").get<double>();
+        q.max_iterations = field(pj, "max_iterations").get<std::int64_t>();
+        q.n_k = field(pj, "n_k").get<int>();
+        q.n_l = field(pj, "n_l").get<int>();
+        q.reorder_period = field(pj, "reorder_period").get<int>();
+        q.seed = field(pj, "seed").get<std::uint64_t>();
+        P.meta.seed = field(h, "seed").get<std::uint64_t>();
+        P.meta.iteration_count = field(h, "iterations").get<std::int64_t>();
+        P.meta.volume_fraction = field(h, "volume_fraction").get<double>();
+        P.n = static_cast<int64_t>(field(h, "count").get<std::size_t>());
+    } catch (const nlohmann::json::exception& e) {
+        bad_file(std::string("header has a field of the wrong type (") + e.what() + ")");
+    }
 }
 
 Parsed parse(const std::string& bytes, bool rows) {
     Parsed P;
-    const bool binary = bytes.size() >= sizeof kMagic && std::memcmp(bytes.data(), kMagic, sizeof kMagic) == 0;
-    const char* p = bytes.data();
-    const char* end = bytes.data() + bytes.size();
-    nlohmann::json h;
-    try {
-        if (binary) {
-            p += sizeof kMagic;
-            if (end - p < 12) throw IoFail{"snapshot: truncated binary header"};
-            std::uint32_t ver;
-            std::memcpy(&ver, p, 4);
-            std::uint64_t hlen;
-            std::memcpy(&hlen, p + 4, 8);
-            p += 12;
-            if (static_cast<std::uint64_t>(end - p) < hlen) throw IoFail{"snapshot: truncated binary header"};
-            h = nlohmann::json::parse(p, p + hlen);
-            p += hlen;
-            if (ver != kVersion) throw IoFail{"snapshot: unsupported format version"};
-        } else {
-            const char* eol = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(end - p)));
-            if (!eol) throw IoFail{"snapshot: missing header line"};
-            h = nlohmann::json::parse(p, eol);
-            p = eol + 1;
-        }
-    } catch (const nlohmann::json::exception& e) {
-        throw IoFail{std::string("snapshot: bad header JSON: ") + e.what()};
-    }
-    try {
-        const std::string shape = require(h, "shape").get<std::string>();
-        const int dim = require(h, "dimension").get<int>();
-        if (require(h, "version").get<std::uint32_t>() != kVersion) throw IoFail{"snapshot: unsupported format version"};
-        if (require(h, "format").get<std::string>() != "srm-snapshot") throw IoFail{"snapshot: unrecognized format tag"};
-        if (shape == "disk" && dim == 2) P.tr = &kDisk;
-        else if (shape == "sphere" && dim == 3) P.tr = &kSphere;
-        else if (shape == "spherodisk" && dim == 3) P.tr = &kPlatelet;
-        else throw IoFail{"snapshot: unknown shape/dimension combination '" + shape + "'"};
-        const auto& box = require(h, "box");
-        if (!box.is_array() || box.size() != static_cast<std::size_t>(dim))
-            throw IoFail{"snapshot header: box must list one length per axis"};
-        for (int a = 0; a < dim; ++a) P.box[a] = box[a].get<double>();
-        const auto& pj = require(h, "params");
-        P.meta.params.c_m = require(pj, "c_m").get<double>();
-        P.meta.params.c_r = require(pj, "c_r").get<double>();
-        P.meta.params.c_w = require(pj, "c_w").get<double>();
-        P.meta.params.f_target = require(pj, "f_target").get<double>();
-        P.meta.params.max_iterations = require(pj, "max_iterations").get<std::int64_t>();
-        P.meta.params.n_k = require(pj, "n_k").get<int>();
-        P.meta.params.n_l = require(pj, "n_l").get<int>();
-        P.meta.params.reorder_period = require(pj, "reorder_period").get<int>();
-        P.meta.params.seed = require(pj, "seed").get<std::uint64_t>();
-        P.meta.seed = require(h, "seed").get<std::uint64_t>();
-        P.meta.iteration_count = require(h, "iterations").get<std::int64_t>();
-        P.meta.volume_fraction = require(h, "volume_fraction").get<double>();
-        P.n = static_cast<int64_t>(require(h, "count").get<std::size_t>());
-    } catch (const nlohmann::json::exception& e) {
-        throw IoFail{std::string("snapshot: bad header: ") + e.what()};
-    }
+    Cursor c{bytes.data(), bytes.data() + bytes.size()};
+    const bool binary = c.left() >= sizeof kMagic && std::memcmp(c.p, kMagic, sizeof kMagic) == 0;
+    read_meta(read_header(c, binary), P);
     if (!rows) return P;
     const int nd = P.tr->doubles;
     P.id.resize(static_cast<size_t>(P.n));
     P.vals.resize(static_cast<size_t>(P.n) * nd);
-    if (binary) {  // snapshot_io.cpp:286-306
-        const std::size_t rb = 4 + 8 * static_cast<std::size_t>(nd);
-        if (static_cast<std::size_t>(end - p) != rb * static_cast<std::size_t>(P.n))
-            throw IoFail{"snapshot: binary payload size does not match count"};
+    if (binary) {  // fixed-width records: u32 id + nd doubles (snapshot_io.cpp:286-306)
+        const std::size_t width = 4 + 8 * static_cast<std::size_t>(nd);
+        if (c.left() != width * static_cast<std::size_t>(P.n)) bad_file("record block size disagrees with the count");
         for (int64_t i = 0; i < P.n; ++i) {
-            std::uint32_t u;
-            std::memcpy(&u, p, 4);
-            P.id[i] = static_cast<int32_t>(u);
-            std::memcpy(&P.vals[i * nd], p + 4, 8 * nd);
-            p += rb;
+            P.id[i] = static_cast<int32_t>(c.raw<std::uint32_t>());
+            std::memcpy(&P.vals[i * nd], c.p, 8 * static_cast<size_t>(nd));
+            c.p += 8 * nd;
         }
         return P;
     }
-    // text rows (snapshot_io.cpp:260-284): the column line, then id,v0,...\n per particle
-    const std::size_t cl = std::strlen(P.tr->columns);
-    if (static_cast<std::size_t>(end - p) < cl + 1 || std::memcmp(p, P.tr->columns, cl) != 0 || p[cl] != '\n')
-        throw IoFail{"snapshot: column line does not match shape schema"};
-    p += cl + 1;
+    // text (snapshot_io.cpp:260-284): the column line, then one "id,v0,...,vk" line per particle
+    const std::string cols = std::string(P.tr->columns) + "\n";
+    if (c.left() < cols.size() || std::memcmp(c.p, cols.data(), cols.size()) != 0)
+        bad_file("column line is not the one of this shape");
+    c.p += cols.size();
     for (int64_t i = 0; i < P.n; ++i) {
-        int v = 0;
-        auto res = std::from_chars(p, end, v);
-        if (res.ec != std::errc()) throw IoFail{"snapshot row: malformed integer"};
-        p = res.ptr;
-        P.id[i] = v;
-        for (int c = 0; c < nd; ++c) {
-            if (p == end || *p != ',') throw IoFail{"snapshot row: expected ','"};
-            ++p;
-            double d = 0.0;
-            auto rd = std::from_chars(p, end, d);
-            if (rd.ec != std::errc()) throw IoFail{"snapshot row: malformed number"};
-            p = rd.ptr;
-            P.vals[i * nd + c] = d;
+        P.id[i] = c.number<int>("id");
+        for (int k = 0; k < nd; ++k) {
+            c.expect(',', "is missing a ','");
+            P.vals[i * nd + k] = c.number<double>("value");
         }
-        if (p == end || *p != '\n') throw IoFail{"snapshot row: expected '\\n'"};
-        ++p;
+        c.expect('\n', "does not end with a newline");
     }
-    if (p != end) throw IoFail{"snapshot: trailing data after last row"};
+    if (c.left() != 0) bad_file("bytes after the last row");
     return P;
 }
 

@@ -95,3 +95,10 @@ def test_no_device_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(srm.NoDeviceError):
         srm.Context([1.0, 1.0], 10)
+
+
+def test_create_rejects_capacity_beyond_int32():
+    # sorted indices and near-list entries are int32: refused before any
+    # device work, so this holds with or without a GPU
+    with pytest.raises(srm.ValidationError):
+        srm.Context([1.0, 1.0, 1.0], 2**31)
