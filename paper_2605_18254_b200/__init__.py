@@ -271,8 +271,10 @@ class Context:
         C-aligned (np.dtype(..., align=True)): the device loads its doubles as such."""
         if not records.flags.c_contiguous:
             raise ValidationError("records: must be C-contiguous")
-        if records.dtype.fields is not None and not records.dtype.isalignedstruct:
-            raise ValidationError("records: use an aligned structured dtype (align=True)")
+        if records.dtype.fields is not None:
+            for name, (ft, off, *_) in records.dtype.fields.items():
+                if off % min(8, ft.base.alignment or 1):
+                    raise ValidationError(f"records: field '{name}' is not aligned (use align=True)")
         n = len(records)
         self._c(_native.lib().srm_b200_upload_records(self._h, n, _ptr(records), records.itemsize,
                                                        off_id, off_pos, off_radius))

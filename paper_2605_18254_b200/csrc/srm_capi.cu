@@ -94,6 +94,11 @@ struct srm_b200_ctx {
     // near-list kernel choice (SRM_B200_NEAR): 0 the shared-memory bricks where they apply
     // (GridParams::near_kind), otherwise the per-particle full stencil
     int near_mode = std::getenv("SRM_B200_NEAR") ? std::atoi(std::getenv("SRM_B200_NEAR")) : 0;
+    // wavefront sweep (k_sweep_wave) where the grid allows it; SRM_B200_WAVE=0: class launches
+    int wave_mode = std::getenv("SRM_B200_WAVE") ? std::atoi(std::getenv("SRM_B200_WAVE")) : 1;
+    WaveCtl* wave_ctl = nullptr;
+    int32_t* wave_order = nullptr;  // rows in wave order (cell_cap entries)
+    unsigned* wave_done = nullptr;  // per row: the epoch of the sweep that finished it
     // srm_generate: the device-resident graph loop (default) or the host-driven loop
     bool device_loop = std::getenv("SRM_B200_HOST_LOOP") == nullptr;
     uint8_t* acc = nullptr;
@@ -197,8 +202,14 @@ struct srm_b200_ctx {
         const char* v = std::getenv("SRM_B200_SWEEP");
         if (!v) return 0;
         const std::string s(v);
-        return s == "lane" ? 1 : (s == "trials" ? 2 : (s == "team" ? 3 : 0));
+        return s == "lane" ? 1 : (s == "trials" ? 2 : (s == "team" ? 3 : (s == "wave" ? 4 : 0)));
     }();
+    // the wavefront sweep replaces the class launches of k_sweep_warpq (sparse sphere grids)
+    bool use_wave(const GridParams& g, int64_t class_cells_total) const {
+        if (platelets() || !g.wave) return false;
+        if (sweep_force) return sweep_force == 4;
+        return !sphere_team(g) && !trial_team(g, class_cells_total);
+    }
     bool sphere_team(const GridParams& g) const {
         if (sweep_force) return sweep_force == 3 && dim == 3;
         return SRM_SPH_TEAM_ON && g.near_kind == 3;
@@ -272,6 +283,8 @@ struct srm_b200_ctx {
             queue_ctas = std::max(1, per_sm) * std::max(1, sms);
         }
         S.xf = dalloc<float4>(cap);
+        wave_ctl = dalloc<WaveCtl>(1);
+        SRM_CUDA(cudaMemsetAsync(wave_ctl, 0, sizeof(WaveCtl), stream));
         stats = dalloc<StatsDev>(1);
         red_part_sum = dalloc<double>(kRedBlocks);
         red_part_max = dalloc<double>(kRedBlocks);
@@ -289,7 +302,7 @@ struct srm_b200_ctx {
         cudaFree(key); cudaFree(skey); cudaFree(perm); cudaFree(perm64); cudaFree(acc);
         cudaFree(count); cudaFree(cell_start); cudaFree(partial);
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
-        cudaFree(nbr); cudaFree(pool.e); cudaFree(S.xf); 
+        cudaFree(nbr); cudaFree(pool.e); cudaFree(S.xf); cudaFree(wave_ctl); cudaFree(wave_order); cudaFree(wave_done);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
@@ -311,7 +324,7 @@ struct srm_b200_ctx {
     // moves have length c_m.  The colouring expression is the oracle's orc_colouring.
     GridParams make_grid(double cell_size, double max_r_state, double c_m) const {
         GridParams g{};
-        const int st = grid_params(cell_size, max_r_state, c_m, box, dim, near_mode, &g, n);
+        const int st = grid_params(cell_size, max_r_state, c_m, box, dim, near_mode, &g, n, wave_mode);
         if (st == 1) throw Invalid{"CellGrid: cell_size must be positive"};
         if (st == 2) throw Invalid{"CellGrid: more than 2^32 cells (radius too small for the box)"};
         for (int a = 0; a < 3; ++a)
@@ -326,13 +339,18 @@ struct srm_b200_ctx {
         cudaFree(count);
         cudaFree(cell_start);
         cudaFree(partial);
-        count = nullptr; cell_start = nullptr; partial = nullptr;
+        cudaFree(wave_order);
+        cudaFree(wave_done);
+        count = nullptr; cell_start = nullptr; partial = nullptr; wave_order = nullptr; wave_done = nullptr;
         const int64_t c = ncells + ncells / 8 + 1024;
         count = dalloc<uint32_t>(c);
         cell_start = dalloc<int64_t>(c + 1);
         tile_cap = (c + kLbTile - 1) / kLbTile;
         partial = dalloc<uint64_t>(tile_cap + 1);  // look-back status words + the tile counter
         SRM_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * c, stream));
+        wave_order = dalloc<int32_t>(c);
+        wave_done = dalloc<unsigned>(c);
+        SRM_CUDA(cudaMemsetAsync(wave_done, 0, sizeof(unsigned) * c, stream));  // epochs start at 1
         cell_cap = c;
     }
 
@@ -427,7 +445,17 @@ struct srm_b200_ctx {
                 launched(1);
             }
         }
-        {
+        if (use_wave(hg, cls_cells_h[hg.ncls] - cls_cells_h[0])) {  // one persistent launch
+            FamScope fs(this, 1);
+            k_wave_order<<<1, kWaveOrderThreads, 0, stream>>>(gp, wave_ctl, wave_order);
+            if (dim == 2)
+                k_sweep_wave<2><<<queue_ctas, kSweepThreads, 0, stream>>>(S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
+                                                                          active, stats, wave_ctl, wave_order, wave_done);
+            else
+                k_sweep_wave<3><<<queue_ctas, kSweepThreads, 0, stream>>>(S, box, gp, rp, cell_start, skey, nbr, pool.e, acc,
+                                                                          active, stats, wave_ctl, wave_order, wave_done);
+            launched(2);
+        } else {
             FamScope fs(this, 1);
             for (int cls = 0; cls < hg.ncls; ++cls) {
                 const int64_t cells = cls_cells_h[cls + 1] - cls_cells_h[cls];
@@ -534,8 +562,8 @@ struct srm_b200_ctx {
     // the instantiated generate graph, reused while everything baked into it is unchanged
     struct GraphKey {
         int64_t n, nc_max;
-        int ntiles_max, ctiles_max, team0, trials0, queue_ctas, dim, plate;
-        const void* bufs[12];
+        int ntiles_max, ctiles_max, team0, trials0, queue_ctas, dim, plate, wave0;
+        const void* bufs[14];
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
     };
     GraphKey gkey{};
@@ -618,6 +646,7 @@ struct srm_b200_ctx {
         hc.reorder_period = p.reorder_period;
         hc.dim = dim;
         hc.near_mode = near_mode;
+        hc.wave_mode = wave_mode;
         hc.n = n;
         hc.seed = p.seed;
         hc.cos_r = std::cos(p.c_r);
@@ -639,6 +668,9 @@ struct srm_b200_ctx {
                                         : 1;
         const bool team0 = dim == 3 && !platelets() && sphere_team(g0);
         const bool trials0 = !platelets() && trial_team(g0, g0.ncells);
+        // the wavefront sweep where a round's grid allows it (the kernels test the grid);
+        // the class loop below runs otherwise
+        const bool wave0 = !platelets() && !team0 && !trials0 && (sweep_force == 0 || sweep_force == 4);
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
@@ -652,7 +684,9 @@ struct srm_b200_ctx {
         key.queue_ctas = queue_ctas;
         key.dim = dim;
         key.plate = platelets();
-        const void* bufs[12] = {P.rec, Q.rec, S.rec, P.aux, Q.aux, S.aux, count, cell_start, perm64, nbr, pool.e, S.xf};
+        key.wave0 = wave0;
+        const void* bufs[14] = {P.rec, Q.rec, S.rec, P.aux, Q.aux, S.aux, count, cell_start, perm64, nbr, pool.e, S.xf,
+                                wave_order, wave_done};
         std::memcpy(key.bufs, bufs, sizeof bufs);
         if (gexec && key == gkey) {
             launch_and_drain(hc, progress, user);
@@ -692,7 +726,18 @@ struct srm_b200_ctx {
                         S, gp, cell_start, skey, nbr, pool, stats);
                     if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                     else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
-                    k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls);
+                    if (wave0) {
+                        k_wave_order<<<1, kWaveOrderThreads, 0, stream>>>(gp, wave_ctl, wave_order);
+                        if (dim == 2)
+                            k_sweep_wave<2><<<queue_ctas, kSweepThreads, 0, stream>>>(S, box, gp, rp, cell_start, skey, nbr,
+                                                                                      pool.e, acc, active, stats, wave_ctl,
+                                                                                      wave_order, wave_done);
+                        else
+                            k_sweep_wave<3><<<queue_ctas, kSweepThreads, 0, stream>>>(S, box, gp, rp, cell_start, skey, nbr,
+                                                                                      pool.e, acc, active, stats, wave_ctl,
+                                                                                      wave_order, wave_done);
+                    }
+                    k_gen_cls_begin<<<1, 1, 0, stream>>>(ctl, gp, h_cls, wave0 ? 1 : 0);
                     capture_into(add_conditional(stream, h_cls, cudaGraphCondTypeWhile), cap_streams[3], [&]() {
                         if (trials0 && dim == 2)
                             k_sweep_trials<2><<<148 * 32, kSweepThreads, 0, stream>>>(0, &ctl->cls, S, box, gp, rp, cell_start,

@@ -62,6 +62,9 @@ struct GridParams {
     FastDiv fd_dims[3];  // division by dims[a]
     FastDiv fd_m[3];     // division by col_m[a]
     int32_t col_body[3]; // col_m * floor(dims / col_m): cells coloured x mod m
+    // wavefront sweep (k_sweep_wave): 1 = the whole sweep is one launch of
+    // row tasks in wave order; lag_y / lag_z = wave-time offsets per y / z colour step
+    int32_t wave, wave_lag_y, wave_lag_z, wave_pmax;
 };
 
 // cell coordinates of a flat key (x fastest, cell_grid.hpp:73-79)
@@ -96,8 +99,16 @@ __device__ __forceinline__ void decode_key(const GridParams& g, uint32_t key, in
 constexpr int kTX = SRM_TILE_X, kTY = SRM_TILE_Y, kTZ = SRM_TILE_Z;  // tiles::k_near_tiles brick (cells)
 constexpr int kCTX = 4, kCTY = 4, kCTZ = 4, kCTileCap = 4096;         // ctiles::k_near_tiles (crowded)
 constexpr double kCrowded = 1.8;  // mean particles per cell above which the crowded bricks are used
+#ifndef SRM_WAVE_LY
+#define SRM_WAVE_LY 2  // wave-time lag per y colour step (rows of one layer)
+#endif
+#ifndef SRM_WAVE_LZ
+#define SRM_WAVE_LZ 2  // extra wave-time lag per z colour step (beyond the minimum)
+#endif
+constexpr int kWaveMaxP = 8192;  // wave times per sweep (k_wave_order's histogram)
+constexpr int kWaveMaxDeps = 32; // dependency rows polled by one warp (a lane each)
 __host__ __device__ inline int grid_params(double cell_size, double max_r_state, double c_m, const Box& box, int dim,
-                                           int near_mode, GridParams* out, int64_t n = 0) {
+                                           int near_mode, GridParams* out, int64_t n = 0, int wave_mode = 1) {
     const double extra = 2.0 * c_m;
     if (!(cell_size > 0.0)) return 1;
     GridParams g{};
@@ -174,6 +185,19 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
     const bool tiles = one && !crowded && g.dims[0] >= kTX + 2 && g.dims[1] >= kTY + 2 && g.dims[2] >= kTZ + 2;
     const bool ctiles = one && crowded && g.dims[0] >= kCTX + 2 && g.dims[1] >= kCTY + 2 && g.dims[2] >= kCTZ + 2;
     g.near_kind = tiles ? 0 : (ctiles ? 3 : 2);
+    // wavefront sweep: rows of cells (x) are tasks; a row waits for the rows within the
+    // near reach (y, z) whose (z colour, y colour) is lower -- the class order of every
+    // pair that can interact.  Needs a finite reach on y and z (at most
+    // kWaveMaxDeps dependency rows) and is meant for sparse grids (crowded ones take the
+    // team sweep).
+    {
+        const int sy = g.near_s[1], sz = dim == 3 ? g.near_s[2] : 0;
+        const bool finite = sy >= 0 && sz >= 0 && (2 * sy + 1) * (2 * sz + 1) <= kWaveMaxDeps;
+        g.wave_lag_y = SRM_WAVE_LY;
+        g.wave_lag_z = (dim == 3 ? sz : 0) + 1 + g.wave_lag_y * (g.col_n[1] - 1) + SRM_WAVE_LZ;
+        g.wave_pmax = g.dims[2] / 2 + g.wave_lag_z * (g.col_n[2] - 1) + g.wave_lag_y * (g.col_n[1] - 1);
+        g.wave = wave_mode && finite && !crowded && g.wave_pmax < kWaveMaxP ? 1 : 0;
+    }
     g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ)
                      : (ctiles ? ((g.dims[0] + kCTX - 1) / kCTX) * ((g.dims[1] + kCTY - 1) / kCTY) *
                                      ((g.dims[2] + kCTZ - 1) / kCTZ)
@@ -737,7 +761,17 @@ constexpr int kSweepThreads = SRM_SWEEP_THREADS;
 
 // Crowded neighbourhood (overflowed near list): test trial p of q against every
 // candidate of its stencil (same candidates, id filter).
-template <int D>
+template <bool kLive>
+__device__ __forceinline__ double4 ld_rec(const double4* p) {
+    if (kLive) {  // two 16-byte L2-only loads of one 32-byte sector
+        const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+        return make_double4(a.x, a.y, b.x, b.y);
+    }
+    return *p;
+}
+
+template <int D, bool kLive = false>
 __device__ __forceinline__ bool trial_clear_rescan(int64_t q, const double* p, double ri, const State& S, const Box& box,
                                                 const GridParams& g, const int64_t* __restrict__ cs,
                                                 const uint32_t* __restrict__ skey) {
@@ -745,7 +779,7 @@ __device__ __forceinline__ bool trial_clear_rescan(int64_t q, const double* p, d
     bool ok = true;
     near_candidates<D>(g, cs, S.xf, q, skey[q], [&](int64_t j) {
         if (!ok || S.id[j] == idq) return;
-        const double4 v = S.rec[j];
+        const double4 v = ld_rec<kLive>(S.rec + j);
         const double xl[3] = {v.x, v.y, v.z};
         if (sphere_overlap<D>(box, p, ri, xl, v.w)) ok = false;
     });
@@ -755,7 +789,9 @@ __device__ __forceinline__ bool trial_clear_rescan(int64_t q, const double* p, d
 // One trial of particle q (slot sl, round-start position xi, radius ri): propose trial l
 // and test it against the live positions of q's near list (or, for an overflowed list,
 // of every candidate of its stencil).  Returns true when the trial is clear (p = trial).
-template <int D>
+// kLive: neighbours' records may be rewritten by other warps of the same launch
+// (k_sweep_wave), so they are read from L2 (ld.global.cg), never from a stale L1 line.
+template <int D, bool kLive = false>
 __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const double* xi, double ri,
                                            const State& S, const Box& box, const GridParams& g,
                                            const RoundParams& rp, const int64_t* __restrict__ cs,
@@ -770,9 +806,9 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     const int nn = h0.x;
     double4 v[SRM_PREFETCH];
     if (nn <= kNearCap) {
-        if (nn > 0) v[0] = S.rec[h0.y];
-        if (SRM_PREFETCH > 1 && nn > 1) v[SRM_PREFETCH > 1 ? 1 : 0] = S.rec[h0.z];
-        if (SRM_PREFETCH > 2 && nn > 2) v[SRM_PREFETCH > 2 ? 2 : 0] = S.rec[h0.w];
+        if (nn > 0) v[0] = ld_rec<kLive>(S.rec + h0.y);
+        if (SRM_PREFETCH > 1 && nn > 1) v[SRM_PREFETCH > 1 ? 1 : 0] = ld_rec<kLive>(S.rec + h0.z);
+        if (SRM_PREFETCH > 2 && nn > 2) v[SRM_PREFETCH > 2 ? 2 : 0] = ld_rec<kLive>(S.rec + h0.w);
     }
     propose<D>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(sl), static_cast<uint32_t>(l), p);
     if (nn <= kNearCap) {
@@ -784,7 +820,7 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
             }
         }
         for (int t = SRM_PREFETCH; t < nn; ++t) {  // the rest of the row (rare at the bench window)
-            const double4 w = S.rec[row[1 + t]];
+            const double4 w = ld_rec<kLive>(S.rec + row[1 + t]);
             const double xl[3] = {w.x, w.y, w.z};
             if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
         }
@@ -793,13 +829,13 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     if (h0.y >= 0) {  // the list is in the overflow pool
         const int32_t* e = pool + h0.y;
         for (int t = 0; t < nn; ++t) {
-            const double4 w = S.rec[e[t]];
+            const double4 w = ld_rec<kLive>(S.rec + e[t]);
             const double xl[3] = {w.x, w.y, w.z};
             if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
         }
         return true;
     }
-    return trial_clear_rescan<D>(q, p, ri, S, box, g, cs, skey);
+    return trial_clear_rescan<D, kLive>(q, p, ri, S, box, g, cs, skey);
 }
 
 // The cells of colour class cls form a lattice per axis: first + stride * i, i < cnt
@@ -952,6 +988,223 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                 }
             }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// Wavefront sweep: the whole coloured Gauss-Seidel sweep in ONE
+// persistent launch.  A task is a row of cells (all x at one (y, z)); its cells are swept
+// colour by colour along x (the row's cells of x colour v, then v + 1, ...).  The result
+// of the sequential class order (orc_sweep_round) depends only on the relative order of
+// particles that can interact, which sit in cells within the near reach g.near_s of each
+// other; two such rows have different (z colour, y colour) unless they are the same row,
+// and the class order runs them in increasing (cz, cy).  So a row may run once the rows
+// within reach with a lower (cz, cy) are done, and in any order otherwise.  Rows are
+// handed out by a ticket counter in increasing wave time
+//     P(y, z) = d(z) + lag_z * cz(z) + lag_y * cy(y),   d(z) = min(z, dims_z - z),
+// which puts every dependency of a row at a strictly smaller P (d changes by at most the
+// reach between rows within reach; lag_z exceeds the reach plus lag_y's whole range), so
+// a warp only ever waits for rows held by running or finished warps: no deadlock, no
+// residency assumption.  The lags keep the dependencies of a row several wave steps
+// behind it (waits are rare), and the wave keeps the rows being swept -- their records,
+// near-list rows and neighbours' records -- within a band of layers that stays in L2,
+// instead of streaming the whole domain once per colour class.
+struct WaveCtl {
+    unsigned ticket;  // next task
+    unsigned epoch;   // sweep number: a row is done in this sweep when done[row] == epoch
+};
+
+__device__ __forceinline__ int wave_time(const GridParams& g, int y, int z) {
+    const int dz = g.dims[2];
+    const int d = z < dz - z ? z : dz - z;
+    return d + g.wave_lag_z * colour1(g, 2, z) + g.wave_lag_y * colour1(g, 1, y);
+}
+
+// rows sorted by wave time (a counting sort; rows of equal time are independent, so their
+// order is free), the ticket counter reset, the sweep epoch advanced.  One CTA.
+constexpr int kWaveOrderThreads = 1024;
+__global__ void __launch_bounds__(kWaveOrderThreads) k_wave_order(const GridParams* __restrict__ gp, WaveCtl* wc,
+                                                                  int32_t* __restrict__ order) {
+    __shared__ int hist[kWaveMaxP];
+    __shared__ int wsum[kWaveOrderThreads / 32];
+    const GridParams& g = *gp;
+    if (!g.wave) return;
+    const int ny = g.dims[1], nrows = g.dims[1] * g.dims[2], np = g.wave_pmax + 1;
+    for (int p = threadIdx.x; p < np; p += blockDim.x) hist[p] = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < nrows; r += blockDim.x) atomicAdd(&hist[wave_time(g, r % ny, r / ny)], 1);
+    __syncthreads();
+    // exclusive scan of hist[0, np): a contiguous chunk per thread
+    const int per = (np + blockDim.x - 1) / blockDim.x, b = threadIdx.x * per, e = min(np, b + per);
+    int local = 0;
+    for (int p = b; p < e; ++p) local += hist[p];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wid; ++w) base += wsum[w];
+    int run = base + incl - local;
+    for (int p = b; p < e; ++p) {
+        const int c = hist[p];
+        hist[p] = run;
+        run += c;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nrows; r += blockDim.x) order[atomicAdd(&hist[wave_time(g, r % ny, r / ny)], 1)] = r;
+    if (threadIdx.x == 0) {
+        wc->ticket = 0;
+        wc->epoch += 1;
+    }
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_wave(State S, Box box,
+                                                                              const GridParams* __restrict__ gp,
+                                                                              const RoundParams* __restrict__ rpp,
+                                                                              const int64_t* __restrict__ cs,
+                                                                              const uint32_t* __restrict__ skey,
+                                                                              const int32_t* __restrict__ nbr,
+                                                                              const int32_t* __restrict__ pool,
+                                                                              uint8_t* __restrict__ acc,
+                                                                              int32_t* __restrict__ active,
+                                                                              StatsDev* stats, WaveCtl* wc,
+                                                                              const int32_t* __restrict__ order,
+                                                                              unsigned* __restrict__ done) {
+    __shared__ int2 win_s[kSweepThreads];  // per warp: 32 (begin, end) cell ranges
+    const GridParams& g = *gp;
+    if (!g.wave) return;
+    const RoundParams rp = *rpp;
+    const unsigned epoch = *reinterpret_cast<volatile unsigned*>(&wc->epoch);
+    const int lane = threadIdx.x & 31;
+    int2* win = win_s + (threadIdx.x & ~31);
+    const unsigned lt = (1u << lane) - 1u;
+    const int dxc = g.dims[0], dyc = g.dims[1], dzc = g.dims[2];
+    const unsigned nrows = static_cast<unsigned>(dyc) * static_cast<unsigned>(dzc);
+    const int sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
+    const int wy = 2 * sy + 1, ndep = wy * (2 * sz + 1);
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(&wc->ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= nrows) break;
+        const int row = __ldcg(order + t);
+        const int y = row % dyc, z = row / dyc;
+        // wait for the rows within reach with a lower (z colour, y colour): a lane each
+        if (lane < ndep) {
+            int yy = y + lane % wy - sy, zz = z + lane / wy - sz;
+            yy = yy < 0 ? yy + dyc : (yy >= dyc ? yy - dyc : yy);
+            zz = zz < 0 ? zz + dzc : (zz >= dzc ? zz - dzc : zz);
+            const int cz = colour1(g, 2, z), czz = colour1(g, 2, zz);
+            const bool lower = czz < cz || (czz == cz && colour1(g, 1, yy) < colour1(g, 1, y));
+            if (lower) {
+                const unsigned* f = done + (static_cast<int64_t>(zz) * dyc + yy);
+                while (ld_acquire(f) != epoch) __nanosleep(128);
+            }
+        }
+        __syncwarp();
+        const int64_t rowcell = static_cast<int64_t>(row) * dxc;
+        // the row's cells colour by colour along x
+        for (int v = 0; v < g.col_n[0]; ++v) {
+            const int m = g.col_m[0];
+            const int first = v < m ? v : g.col_body[0] + (v - m);
+            const int stride = v < m ? m : 1;
+            const uint32_t cells = v < m ? static_cast<uint32_t>(g.col_body[0] / m) : 1u;
+            uint32_t next = 0;
+            int32_t rb = 0, re = 0;
+            auto load_raw = [&]() {
+                const uint32_t c = next + lane;
+                rb = 0;
+                re = 0;
+                if (c < cells) {
+                    const int64_t cell = rowcell + first + stride * static_cast<int>(c);
+                    rb = static_cast<int32_t>(cs[cell]);
+                    re = static_cast<int32_t>(cs[cell + 1]);
+                }
+                next = cells - next < 32u ? cells : next + 32u;
+            };
+            bool have_raw = true;
+            load_raw();
+            int wn = 0, wofs = 0;
+            bool valid = false;
+            int32_t iq = 0, il = 0, isl = 0, iend = 0;
+            for (;;) {
+                for (;;) {  // free lanes claim cells (warp-uniform loop)
+                    const unsigned fm = __ballot_sync(0xffffffffu, !valid);
+                    if (fm == 0) break;
+                    if (wofs == wn) {
+                        if (!have_raw) break;
+                        const bool ne = rb < re;
+                        const unsigned gm = __ballot_sync(0xffffffffu, ne);
+                        __syncwarp();
+                        if (ne) win[__popc(gm & lt)] = make_int2(rb, re);
+                        __syncwarp();
+                        wn = __popc(gm);
+                        wofs = 0;
+                        have_raw = next < cells;
+                        if (have_raw) load_raw();
+                        continue;
+                    }
+                    const int rank = __popc(fm & lt);
+                    const int avail = wn - wofs;
+                    if (!valid && rank < avail) {
+                        const int2 c = win[wofs + rank];
+                        iq = c.x;
+                        iend = c.y;
+                        il = 0;
+                        isl = S.slot[iq];
+                        valid = true;
+                    }
+                    const int nf = __popc(fm);
+                    wofs += nf < avail ? nf : avail;
+                }
+                if (__ballot_sync(0xffffffffu, valid) == 0) break;
+                if (valid) {
+                    const double4 me = S.rec[iq];  // own record: only this lane writes it
+                    double xi[D], p[D];
+                    rec_pos<D>(me, xi);
+                    const bool clear = trial_clear<D, true>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
+                    bool fin = true;
+                    if (clear) {
+                        S.rec[iq] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
+                        if (rp.write_acc) acc[iq] = static_cast<uint8_t>(il);
+                    } else if (il + 1 < rp.n_l) {
+                        ++il;
+                        fin = false;
+                    } else {
+                        if (rp.write_acc) acc[iq] = kNotAccepted;
+                        active[atomicAdd(&stats->active_count, 1ull)] = iq;
+                    }
+                    if (fin) {
+                        if (iq + 1 < iend) {
+                            iq += 1;
+                            il = 0;
+                            isl = S.slot[iq];
+                        } else {
+                            valid = false;
+                        }
+                    }
+                }
+            }
+            __syncwarp();  // colour v's moves visible to the warp before colour v + 1
+        }
+        // publish the row: every lane's stores ordered before the release
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(done + row, epoch);
     }
 }
 
@@ -1278,7 +1531,7 @@ struct GenCtl {
     double f_target, stop, c_w, c_m, box_measure;
     int64_t max_iter, it0;
     int64_t n;  // particles (the near-list kernel choice depends on the occupancy)
-    int32_t n_k, n_l, reorder_period, dim, near_mode, pad0;
+    int32_t n_k, n_l, reorder_period, dim, near_mode, wave_mode;
     uint64_t seed;
     double cos_r, sin_r;  // platelet rotation angle (host libm)
     // state
@@ -1324,7 +1577,7 @@ __global__ void k_gen_step(GenCtl* c, GridParams* gp, RoundParams* rp, StatsDev*
         c->cs = 2.5 * c->max_r + c->c_m;
         GridParams g{};
         if (c->cs < 2.0 * (c->max_r * factor) + c->c_m ||
-            grid_params(c->cs, c->max_r * factor, c->c_m, box, c->dim, c->near_mode, &g, c->n) != 0) {
+            grid_params(c->cs, c->max_r * factor, c->c_m, box, c->dim, c->near_mode, &g, c->n, c->wave_mode) != 0) {
             c->status = 2;
             c->phase = 3;
             active = false;
@@ -1339,7 +1592,7 @@ __global__ void k_gen_step(GenCtl* c, GridParams* gp, RoundParams* rp, StatsDev*
         }
     } else if (c->phase == 2 && c->k == 0) {  // shake on P with the pre-swell grid (engine.hpp:244-249)
         GridParams g{};
-        grid_params(c->cs, c->max_r, c->c_m, box, c->dim, c->near_mode, &g, c->n);
+        grid_params(c->cs, c->max_r, c->c_m, box, c->dim, c->near_mode, &g, c->n, c->wave_mode);
         *gp = g;
         copy = true;
     }
@@ -1372,9 +1625,11 @@ __global__ void k_gen_t0(GenCtl* c) {
     if (c->pub) *reinterpret_cast<volatile int64_t*>(c->pub + 2) = static_cast<int64_t>(c->t0);
 }
 
-__global__ void k_gen_cls_begin(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls) {
+// wave_on: the graph swept this round with k_sweep_wave already when the grid allows it
+__global__ void k_gen_cls_begin(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls,
+                                int wave_on) {
     c->cls = 0;
-    cudaGraphSetConditional(h_cls, gp->ncls > 0 ? 1u : 0u);
+    cudaGraphSetConditional(h_cls, gp->ncls > 0 && !(wave_on && gp->wave) ? 1u : 0u);
 }
 
 __global__ void k_gen_cls_next(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls) {

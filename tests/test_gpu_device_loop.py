@@ -12,10 +12,11 @@ import paper_2605_18254_b200 as srm
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["", "lane", "trials"])
+@pytest.fixture(autouse=True, params=["", "lane", "trials", "wave"])
 def sweep_kernel(request, monkeypatch):
     """Every test once per sweep kernel (SRM_B200_SWEEP: "" = chosen by the grid, lane =
-    k_sweep_warpq, trials = k_sweep_trials, team = k_sweep_team): each is exact on any grid."""
+    k_sweep_warpq, trials = k_sweep_trials, team = k_sweep_team, wave = the one-launch wavefront
+    k_sweep_wave where the grid allows it): each is exact on any grid."""
     if request.param:
         monkeypatch.setenv("SRM_B200_SWEEP", request.param)
     else:
