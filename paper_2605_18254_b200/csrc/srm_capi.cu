@@ -95,7 +95,20 @@ struct srm_b200_ctx {
     // (GridParams::near_kind), otherwise the per-particle full stencil
     int near_mode = std::getenv("SRM_B200_NEAR") ? std::atoi(std::getenv("SRM_B200_NEAR")) : 0;
     // wavefront sweep (k_sweep_wave) where the grid allows it; SRM_B200_WAVE=0: class launches
-    int wave_mode = std::getenv("SRM_B200_WAVE") ? std::atoi(std::getenv("SRM_B200_WAVE")) : 1;
+    // (tuning: SRM_B200_WAVE=1:ly:lz sets the wave lags, GridParams::wave_lag_*)
+    int wave_mode = [] {
+        const char* v = std::getenv("SRM_B200_WAVE");
+        if (!v) return 1;  // (the grid marks where the wave can run; wave_default picks it)
+        int on = 1, ly = 0, lz = 0;
+        std::sscanf(v, "%d:%d:%d", &on, &ly, &lz);
+        return (on ? 1 : 0) | (std::min(std::max(ly, 0), 255) << 8) | (std::min(std::max(lz, 0), 255) << 16);
+    }();
+    // opt-in (SRM_B200_WAVE=1 or SRM_B200_SWEEP=wave): measured no faster than the class
+    // launches at cfg 4, so the class launches stay the default
+    bool wave_default = [] {
+        const char* v = std::getenv("SRM_B200_WAVE");
+        return v && std::atoi(v) != 0;
+    }();
     WaveCtl* wave_ctl = nullptr;
     int32_t* wave_order = nullptr;  // rows in wave order (cell_cap entries)
     unsigned* wave_done = nullptr;  // per row: the epoch of the sweep that finished it
@@ -141,6 +154,7 @@ struct srm_b200_ctx {
 
     cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
     int64_t last_nonmovers = 0;
+    int64_t last_wave_waits = 0, last_wave_polls = 0;
 
     // ---------------------------------------------------------------------------
     cudaEvent_t take_event() {
@@ -208,7 +222,7 @@ struct srm_b200_ctx {
     bool use_wave(const GridParams& g, int64_t class_cells_total) const {
         if (platelets() || !g.wave) return false;
         if (sweep_force) return sweep_force == 4;
-        return !sphere_team(g) && !trial_team(g, class_cells_total);
+        return wave_default && !sphere_team(g) && !trial_team(g, class_cells_total);
     }
     bool sphere_team(const GridParams& g) const {
         if (sweep_force) return sweep_force == 3 && dim == 3;
@@ -670,7 +684,7 @@ struct srm_b200_ctx {
         const bool trials0 = !platelets() && trial_team(g0, g0.ncells);
         // the wavefront sweep where a round's grid allows it (the kernels test the grid);
         // the class loop below runs otherwise
-        const bool wave0 = !platelets() && !team0 && !trials0 && (sweep_force == 0 || sweep_force == 4);
+        const bool wave0 = !platelets() && !team0 && !trials0 && (sweep_force == 4 || (sweep_force == 0 && wave_default));
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
@@ -814,6 +828,8 @@ struct srm_b200_ctx {
         o.candidate_pairs = with_candidates ? static_cast<int64_t>(h_stats->candidate_pairs) : -1;
         o.movers = n - static_cast<int64_t>(h_stats->active_count);
         last_nonmovers = static_cast<int64_t>(h_stats->active_count);
+        last_wave_waits = static_cast<int64_t>(h_stats->wave_waits);
+        last_wave_polls = static_cast<int64_t>(h_stats->wave_polls);
         return o;
     }
 
@@ -1629,6 +1645,8 @@ int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
         info[3] = c->hg.near_s[0];
         info[4] = c->hg.col_m[0];
         info[5] = c->hg.ncells;
+        info[6] = c->last_wave_waits;
+        info[7] = c->last_wave_polls;
         return SRM_B200_OK;
     });
 }

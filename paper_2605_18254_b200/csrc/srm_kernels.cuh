@@ -100,13 +100,14 @@ constexpr int kTX = SRM_TILE_X, kTY = SRM_TILE_Y, kTZ = SRM_TILE_Z;  // tiles::k
 constexpr int kCTX = 4, kCTY = 4, kCTZ = 4, kCTileCap = 4096;         // ctiles::k_near_tiles (crowded)
 constexpr double kCrowded = 1.8;  // mean particles per cell above which the crowded bricks are used
 #ifndef SRM_WAVE_LY
-#define SRM_WAVE_LY 2  // wave-time lag per y colour step (rows of one layer)
+#define SRM_WAVE_LY 64  // wave-time lag per y colour step (rows of one layer)
 #endif
 #ifndef SRM_WAVE_LZ
-#define SRM_WAVE_LZ 2  // extra wave-time lag per z colour step (beyond the minimum)
+#define SRM_WAVE_LZ 64  // extra wave-time lag per z colour step (beyond the minimum)
 #endif
 constexpr int kWaveMaxP = 8192;  // wave times per sweep (k_wave_order's histogram)
 constexpr int kWaveMaxDeps = 32; // dependency rows polled by one warp (a lane each)
+constexpr int kWaveMaxRow = 2048; // cells per row (the row's done-bitmap in shared memory)
 __host__ __device__ inline int grid_params(double cell_size, double max_r_state, double c_m, const Box& box, int dim,
                                            int near_mode, GridParams* out, int64_t n = 0, int wave_mode = 1) {
     const double extra = 2.0 * c_m;
@@ -192,11 +193,14 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
     // team sweep).
     {
         const int sy = g.near_s[1], sz = dim == 3 ? g.near_s[2] : 0;
-        const bool finite = sy >= 0 && sz >= 0 && (2 * sy + 1) * (2 * sz + 1) <= kWaveMaxDeps;
-        g.wave_lag_y = SRM_WAVE_LY;
-        g.wave_lag_z = (dim == 3 ? sz : 0) + 1 + g.wave_lag_y * (g.col_n[1] - 1) + SRM_WAVE_LZ;
-        g.wave_pmax = g.dims[2] / 2 + g.wave_lag_z * (g.col_n[2] - 1) + g.wave_lag_y * (g.col_n[1] - 1);
-        g.wave = wave_mode && finite && !crowded && g.wave_pmax < kWaveMaxP ? 1 : 0;
+        const bool finite = g.near_s[0] >= 0 && g.dims[0] <= kWaveMaxRow && sy >= 0 && sz >= 0 &&
+                            (2 * sy + 1) * (2 * sz + 1) <= kWaveMaxDeps;
+        // wave_mode: bit 0 on; bits 8-15 / 16-23 override lag_y / the extra z lag (tuning)
+        const int ly = (wave_mode >> 8) & 0xff, lz = (wave_mode >> 16) & 0xff;
+        g.wave_lag_y = ly ? ly : SRM_WAVE_LY;
+        g.wave_lag_z = (dim == 3 ? sz : 0) + 1 + g.wave_lag_y * (g.col_n[1] - 1) + (ly || lz ? lz : SRM_WAVE_LZ);
+        g.wave_pmax = g.dims[2] - 1 + g.wave_lag_z * (g.col_n[2] - 1) + g.wave_lag_y * (g.col_n[1] - 1);
+        g.wave = (wave_mode & 1) && finite && !crowded && g.wave_pmax < kWaveMaxP ? 1 : 0;
     }
     g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ)
                      : (ctiles ? ((g.dims[0] + kCTX - 1) / kCTX) * ((g.dims[1] + kCTY - 1) / kCTY) *
@@ -244,6 +248,8 @@ struct StatsDev {
     unsigned long long candidate_pairs;
     unsigned long long active_count;  // non-movers: particles that kept their round-start position
     unsigned long long pool_top;      // near-list overflow pool: entries taken this round
+    unsigned long long wave_waits;    // k_sweep_wave: dependency rows found unfinished (diagnostic)
+    unsigned long long wave_polls;    // k_sweep_wave: polls of unfinished dependency rows (diagnostic)
 };
 
 // Overflow pool of the near lists: a row whose list does not fit (n > kNearCap) keeps
@@ -993,31 +999,31 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
 
 // ---------------------------------------------------------------------------------
 // Wavefront sweep: the whole coloured Gauss-Seidel sweep in ONE
-// persistent launch.  A task is a row of cells (all x at one (y, z)); its cells are swept
-// colour by colour along x (the row's cells of x colour v, then v + 1, ...).  The result
-// of the sequential class order (orc_sweep_round) depends only on the relative order of
+// persistent launch.  A task is a row of cells (all x at one (y, z)).  The result of the
+// sequential class order (orc_sweep_round) depends only on the relative order of
 // particles that can interact, which sit in cells within the near reach g.near_s of each
 // other; two such rows have different (z colour, y colour) unless they are the same row,
 // and the class order runs them in increasing (cz, cy).  So a row may run once the rows
-// within reach with a lower (cz, cy) are done, and in any order otherwise.  Rows are
-// handed out by a ticket counter in increasing wave time
-//     P(y, z) = d(z) + lag_z * cz(z) + lag_y * cy(y),   d(z) = min(z, dims_z - z),
-// which puts every dependency of a row at a strictly smaller P (d changes by at most the
-// reach between rows within reach; lag_z exceeds the reach plus lag_y's whole range), so
-// a warp only ever waits for rows held by running or finished warps: no deadlock, no
-// residency assumption.  The lags keep the dependencies of a row several wave steps
-// behind it (waits are rare), and the wave keeps the rows being swept -- their records,
-// near-list rows and neighbours' records -- within a band of layers that stays in L2,
-// instead of streaming the whole domain once per colour class.
+// within reach with a lower (cz, cy) are done, and in any order otherwise; inside a row,
+// a cell may run once the cells within reach along x with a lower x colour are done.
+// Rows are handed out by a ticket counter in increasing wave time
+//     P(y, z) = z + lag_z * cz(z) + lag_y * cy(y),
+// which puts every dependency of a row at a strictly smaller P: between rows within reach
+// z changes by at most the reach, lag_z exceeds the reach plus lag_y's whole range, and
+// across the periodic seam the lower colour is always the cell near z = 0 (colour 0 at
+// x = 0, the remainder colours highest).  A warp therefore only ever waits for rows held
+// by running or finished warps: no deadlock and no residency assumption.  The lags keep a
+// row's dependencies several wave steps behind it (waits are rare), and the wave keeps the
+// rows being swept -- their records, near-list rows and their neighbours' records --
+// within a band of layers that stays in L2, instead of streaming the whole domain once
+// per colour class as the class launches do.
 struct WaveCtl {
     unsigned ticket;  // next task
     unsigned epoch;   // sweep number: a row is done in this sweep when done[row] == epoch
 };
 
 __device__ __forceinline__ int wave_time(const GridParams& g, int y, int z) {
-    const int dz = g.dims[2];
-    const int d = z < dz - z ? z : dz - z;
-    return d + g.wave_lag_z * colour1(g, 2, z) + g.wave_lag_y * colour1(g, 1, y);
+    return z + g.wave_lag_z * colour1(g, 2, z) + g.wave_lag_y * colour1(g, 1, y);
 }
 
 // rows sorted by wave time (a counting sort; rows of equal time are independent, so their
@@ -1067,6 +1073,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1084,18 +1095,25 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_wave(St
                                                                               StatsDev* stats, WaveCtl* wc,
                                                                               const int32_t* __restrict__ order,
                                                                               unsigned* __restrict__ done) {
-    __shared__ int2 win_s[kSweepThreads];  // per warp: 32 (begin, end) cell ranges
+    constexpr int kWarps = kSweepThreads / 32, kWords = kWaveMaxRow / 32;
+    __shared__ int2 win_s[kSweepThreads];             // per warp: 32 (begin, end) cell ranges
+    __shared__ int winx_s[kSweepThreads];             // ... and their x
+    __shared__ unsigned bits_s[kWarps][kWords];       // per warp: cells of the row already swept
     const GridParams& g = *gp;
     if (!g.wave) return;
     const RoundParams rp = *rpp;
     const unsigned epoch = *reinterpret_cast<volatile unsigned*>(&wc->epoch);
     const int lane = threadIdx.x & 31;
     int2* win = win_s + (threadIdx.x & ~31);
+    int* winx = winx_s + (threadIdx.x & ~31);
+    unsigned* bits = bits_s[threadIdx.x >> 5];
     const unsigned lt = (1u << lane) - 1u;
     const int dxc = g.dims[0], dyc = g.dims[1], dzc = g.dims[2];
     const unsigned nrows = static_cast<unsigned>(dyc) * static_cast<unsigned>(dzc);
-    const int sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
+    const int sx = g.near_s[0], sy = g.near_s[1], sz = D == 3 ? g.near_s[2] : 0;
     const int wy = 2 * sy + 1, ndep = wy * (2 * sz + 1);
+    const int m = g.col_m[0], nbody = g.col_body[0] / m;  // x colours: body v < m has nbody cells
+    const uint32_t ncl = static_cast<uint32_t>(dxc);
     for (;;) {
         unsigned t = 0;
         if (lane == 0) t = atomicAdd(&wc->ticket, 1u);
@@ -1103,6 +1121,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_wave(St
         if (t >= nrows) break;
         const int row = __ldcg(order + t);
         const int y = row % dyc, z = row / dyc;
+        for (int w = lane; w < kWords; w += 32) bits[w] = 0u;
         // wait for the rows within reach with a lower (z colour, y colour): a lane each
         if (lane < ndep) {
             int yy = y + lane % wy - sy, zz = z + lane / wy - sz;
@@ -1112,97 +1131,134 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_wave(St
             const bool lower = czz < cz || (czz == cz && colour1(g, 1, yy) < colour1(g, 1, y));
             if (lower) {
                 const unsigned* f = done + (static_cast<int64_t>(zz) * dyc + yy);
-                while (ld_acquire(f) != epoch) __nanosleep(128);
+                if (ld_relaxed(f) != epoch) {
+                    unsigned polls = 1, ns = 64;
+                    while (ld_relaxed(f) != epoch) {
+                        __nanosleep(ns);
+                        ns = ns < 1024 ? 2 * ns : ns;
+                        ++polls;
+                    }
+                    atomicAdd(&stats->wave_waits, 1ull);
+                    atomicAdd(&stats->wave_polls, static_cast<unsigned long long>(polls));
+                }
+                // acquire: the dependency's records (read from L2 below) after its release
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
         }
         __syncwarp();
         const int64_t rowcell = static_cast<int64_t>(row) * dxc;
-        // the row's cells colour by colour along x
-        for (int v = 0; v < g.col_n[0]; ++v) {
-            const int m = g.col_m[0];
-            const int first = v < m ? v : g.col_body[0] + (v - m);
-            const int stride = v < m ? m : 1;
-            const uint32_t cells = v < m ? static_cast<uint32_t>(g.col_body[0] / m) : 1u;
-            uint32_t next = 0;
-            int32_t rb = 0, re = 0;
-            auto load_raw = [&]() {
-                const uint32_t c = next + lane;
-                rb = 0;
-                re = 0;
-                if (c < cells) {
-                    const int64_t cell = rowcell + first + stride * static_cast<int>(c);
-                    rb = static_cast<int32_t>(cs[cell]);
-                    re = static_cast<int32_t>(cs[cell + 1]);
-                }
-                next = cells - next < 32u ? cells : next + 32u;
-            };
-            bool have_raw = true;
-            load_raw();
-            int wn = 0, wofs = 0;
-            bool valid = false;
-            int32_t iq = 0, il = 0, isl = 0, iend = 0;
-            for (;;) {
-                for (;;) {  // free lanes claim cells (warp-uniform loop)
-                    const unsigned fm = __ballot_sync(0xffffffffu, !valid);
-                    if (fm == 0) break;
-                    if (wofs == wn) {
-                        if (!have_raw) break;
-                        const bool ne = rb < re;
-                        const unsigned gm = __ballot_sync(0xffffffffu, ne);
-                        __syncwarp();
-                        if (ne) win[__popc(gm & lt)] = make_int2(rb, re);
-                        __syncwarp();
-                        wn = __popc(gm);
-                        wofs = 0;
-                        have_raw = next < cells;
-                        if (have_raw) load_raw();
-                        continue;
+        // x of the c-th cell in claim order (colour by colour); the cell may start when the
+        // cells within reach along x with a lower colour are done (bits)
+        auto cell_x = [&](uint32_t c) -> int {
+            const uint32_t body = static_cast<uint32_t>(m * nbody);
+            if (c >= body) return g.col_body[0] + static_cast<int>(c - body);
+            const uint32_t v = c / static_cast<uint32_t>(nbody), i = c - v * static_cast<uint32_t>(nbody);
+            return static_cast<int>(v) + m * static_cast<int>(i);
+        };
+        auto ready = [&](int x) -> bool {
+            const int cx = colour1(g, 0, x);
+            for (int d = -sx; d <= sx; ++d) {
+                if (d == 0) continue;
+                int xx = x + d;
+                xx = xx < 0 ? xx + dxc : (xx >= dxc ? xx - dxc : xx);
+                if (colour1(g, 0, xx) < cx && !((bits[xx >> 5] >> (xx & 31)) & 1u)) return false;
+            }
+            return true;
+        };
+        uint32_t next = 0;
+        int32_t rb = 0, re = 0, rx = 0;
+        auto load_raw = [&]() {
+            const uint32_t c = next + lane;
+            rb = 0;
+            re = 0;
+            rx = -1;
+            if (c < ncl) {
+                rx = cell_x(c);
+                const int64_t cell = rowcell + rx;
+                rb = static_cast<int32_t>(cs[cell]);
+                re = static_cast<int32_t>(cs[cell + 1]);
+            }
+            next = ncl - next < 32u ? ncl : next + 32u;
+        };
+        __syncwarp();
+        bool have_raw = true;
+        load_raw();
+        int wn = 0, wofs = 0;
+        bool valid = false, started = false;
+        int32_t iq = 0, il = 0, isl = 0, iend = 0, ix = 0;
+        for (;;) {
+            for (;;) {  // free lanes claim cells (warp-uniform loop)
+                const unsigned fm = __ballot_sync(0xffffffffu, !valid);
+                if (fm == 0) break;
+                if (wofs == wn) {
+                    if (!have_raw) break;
+                    const bool ne = rb < re;
+                    if (rx >= 0 && !ne) atomicOr(&bits[rx >> 5], 1u << (rx & 31));  // empty: done
+                    const unsigned gm = __ballot_sync(0xffffffffu, ne);
+                    __syncwarp();  // every lane is done reading the previous window
+                    if (ne) {
+                        win[__popc(gm & lt)] = make_int2(rb, re);
+                        winx[__popc(gm & lt)] = rx;
                     }
-                    const int rank = __popc(fm & lt);
-                    const int avail = wn - wofs;
-                    if (!valid && rank < avail) {
-                        const int2 c = win[wofs + rank];
-                        iq = c.x;
-                        iend = c.y;
+                    __syncwarp();
+                    wn = __popc(gm);
+                    wofs = 0;
+                    have_raw = next < ncl;
+                    if (have_raw) load_raw();
+                    continue;
+                }
+                const int rank = __popc(fm & lt);
+                const int avail = wn - wofs;
+                if (!valid && rank < avail) {
+                    const int2 c = win[wofs + rank];
+                    iq = c.x;
+                    iend = c.y;
+                    ix = winx[wofs + rank];
+                    il = 0;
+                    valid = true;
+                    started = false;
+                }
+                const int nf = __popc(fm);
+                wofs += nf < avail ? nf : avail;
+            }
+            if (__ballot_sync(0xffffffffu, valid) == 0) break;
+            if (valid && !started && ready(ix)) {
+                started = true;
+                isl = S.slot[iq];
+            }
+            bool cell_done = false;
+            if (valid && started) {
+                const double4 me = S.rec[iq];  // own record: only this lane writes it
+                double xi[D], p[D];
+                rec_pos<D>(me, xi);
+                const bool clear = trial_clear<D, true>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
+                bool fin = true;
+                if (clear) {
+                    S.rec[iq] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
+                    if (rp.write_acc) acc[iq] = static_cast<uint8_t>(il);
+                } else if (il + 1 < rp.n_l) {
+                    ++il;
+                    fin = false;
+                } else {
+                    if (rp.write_acc) acc[iq] = kNotAccepted;
+                    active[atomicAdd(&stats->active_count, 1ull)] = iq;
+                }
+                if (fin) {
+                    if (iq + 1 < iend) {
+                        iq += 1;
                         il = 0;
                         isl = S.slot[iq];
-                        valid = true;
-                    }
-                    const int nf = __popc(fm);
-                    wofs += nf < avail ? nf : avail;
-                }
-                if (__ballot_sync(0xffffffffu, valid) == 0) break;
-                if (valid) {
-                    const double4 me = S.rec[iq];  // own record: only this lane writes it
-                    double xi[D], p[D];
-                    rec_pos<D>(me, xi);
-                    const bool clear = trial_clear<D, true>(iq, isl, il, xi, me.w, S, box, g, rp, cs, skey, nbr, pool, p);
-                    bool fin = true;
-                    if (clear) {
-                        S.rec[iq] = make_double4(p[0], D > 1 ? p[D > 1 ? 1 : 0] : 0.0, D > 2 ? p[D > 2 ? 2 : 0] : 0.0, me.w);
-                        if (rp.write_acc) acc[iq] = static_cast<uint8_t>(il);
-                    } else if (il + 1 < rp.n_l) {
-                        ++il;
-                        fin = false;
                     } else {
-                        if (rp.write_acc) acc[iq] = kNotAccepted;
-                        active[atomicAdd(&stats->active_count, 1ull)] = iq;
-                    }
-                    if (fin) {
-                        if (iq + 1 < iend) {
-                            iq += 1;
-                            il = 0;
-                            isl = S.slot[iq];
-                        } else {
-                            valid = false;
-                        }
+                        valid = false;
+                        cell_done = true;
                     }
                 }
             }
-            __syncwarp();  // colour v's moves visible to the warp before colour v + 1
+            if (cell_done) atomicOr(&bits[ix >> 5], 1u << (ix & 31));
+            __syncwarp();  // the cell's moves visible to the warp before a dependent cell starts
         }
-        // publish the row: every lane's stores ordered before the release
-        __threadfence();
+        // publish the row: every lane's stores are ordered before lane 0's release by the
+        // warp barrier (bar.warp.sync orders memory among its threads)
         __syncwarp();
         if (lane == 0) st_release(done + row, epoch);
     }
