@@ -39,8 +39,9 @@ UNIT = "particle-updates/s"
 # BASELINE.json configs (SURVEY.md §8d synthetic inputs).  cfg4 is the bench workload;
 # the others run with --config (parity cases at full size, and their throughput).
 CONFIGS = {
-    "cfg1": dict(desc="2D monodisperse disks N=1e4, unit square, f_target 0.50, c_m=0.1 r_t",
-                 kind="mono", dim=2, n=10_000, f_target=0.50, cm_rel=0.10, f0=0.1),
+    "cfg1": dict(desc="2D monodisperse disks N=1e4, unit square, uniform random centres, radius grown from half "
+                      "the smallest centre distance to f_target 0.50, c_m=0.1 r_t",
+                 kind="mono", dim=2, n=10_000, f_target=0.50, cm_rel=0.10, f0=0.1, start="uniform"),
     "cfg2": dict(desc="3D monodisperse spheres N=1e6, unit cube, f_target 0.40, c_m=0.1 r_t",
                  kind="mono", dim=3, n=1_000_000, f_target=0.40, cm_rel=0.10, f0=0.1),
     "cfg3": dict(desc="3D polydisperse spheres N=1e6, lognormal radii (mean 1, CV 0.2, clipped to [0.5, 2]), "
@@ -70,6 +71,11 @@ def poly_radii(n, seed):
     s2 = math.log(1.04)
     rng = np.random.default_rng(seed & 0xFFFFFFFF)
     return np.clip(rng.lognormal(-0.5 * s2, math.sqrt(s2), n), 0.5, 2.0)
+
+
+def uniform_centres(n, dim, box, seed):
+    """BASELINE cfg 1's start: n uniform random centres in the box (numpy PCG64, seeded)."""
+    return np.random.default_rng(seed & 0xFFFFFFFF).random((n, dim)) * box
 
 
 def platelet_measure(D, t):
@@ -219,6 +225,8 @@ def ref_lib():
     L.ref_generate_platelets.restype = C.c_int
     L.ref_generate_platelets.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, C.c_double, C.c_double, C.c_double,
                                          C.c_int, C.c_int, C.c_double, C.c_int64, C.c_uint64, C.c_int, vp, vp]
+    L.ref_nnd.restype = None
+    L.ref_nnd.argtypes = [C.c_int, vp, C.c_int64, vp, vp]
     L.ref_pl_bench_rounds.restype = C.c_double
     L.ref_pl_bench_rounds.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, C.c_double, C.c_double, C.c_int, C.c_int,
                                       C.c_uint64, C.c_int, vp]
@@ -269,8 +277,15 @@ def ref_sample_state(cfg, seed):
     pos = np.zeros((n, dim))
     ids = np.zeros(n, np.int32)
     placed = np.zeros(1, np.int64)
-    st = L.ref_rsa_place(dim, _p(Lb), n, _p(radii), 10000, seed, _p(pos), _p(ids), _p(placed))
-    assert st == 0, "reference rsa_place failed"
+    if cfg.get("start") == "uniform":  # uniform centres, r0 = half the smallest centre distance
+        pos = uniform_centres(n, dim, box, seed)
+        ids = np.arange(n, dtype=np.int32)
+        d = np.zeros(n)
+        L.ref_nnd(dim, _p(Lb), n, _p(pos), _p(d))
+        radii = np.full(n, 0.5 * float(d.min()) * (1.0 - 1e-9))
+    else:
+        st = L.ref_rsa_place(dim, _p(Lb), n, _p(radii), 10000, seed, _p(pos), _p(ids), _p(placed))
+        assert st == 0, "reference rsa_place failed"
     st = L.ref_generate(dim, _p(Lb), n, _p(pos), _p(radii), _p(ids), C_W, c_m, N_K, N_L,
                         F_WINDOW * cfg["f_target"], 100000, seed + 1, 16, _p(it), _p(f), _p(acc))
     assert st == 0, "reference srm_generate failed"
@@ -345,6 +360,14 @@ def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
             Lb = [L] * dim
             pos, ids = srm.rsa_clustered(r0, Lb, cfg["clusters"], cfg["sigma"], 10000, seed)
             c_m = cfg["cm_abs"]
+        elif cfg.get("start") == "uniform":  # BASELINE cfg 1: uniform centres, radius from 0
+            Lb = [box] * dim
+            pos, ids = uniform_centres(n, dim, box, seed), np.arange(n, dtype=np.int32)
+            c_m = cfg["cm_rel"] * radius_for(cfg["f_target"], cfg["n"], dim)
+            ctx = srm.Context(Lb, n, device)
+            ctx.upload(pos, np.full(n, 1e-12), ids)  # half the smallest centre distance (device NND, exact)
+            r0 = np.full(n, 0.5 * float(ctx.nearest_neighbor_distances().min()) * (1.0 - 1e-9))
+            ctx.close()
         else:
             Lb = [box] * dim
             r0 = np.full(n, radius_for(cfg["f0"], cfg["n"], dim))

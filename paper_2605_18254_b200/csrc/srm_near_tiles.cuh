@@ -210,54 +210,49 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         const float base = __fadd_rn(__fadd_rn(mw, g.extra_f), g.margin_f);  // + r_j
         const float2 nmx = make_float2(-mx, -mx), nmy = make_float2(-my, -my), nmz = make_float2(-mz, -mz);
         const float2 base2 = make_float2(base, base), fac2 = make_float2(1.00001f, 1.00001f);
-        // hits are rare per lane but common per warp: record the hit slots branch-free
-        // (a store to the current list slot every test, the count advances on a hit; slot
-        // kNearCap absorbs the overflow), resolve them after the scan
+        // hits are rare (0.8 per particle at the bench window): the screen of a range sets a
+        // bit per hit in a register mask (16 slot pairs per mask) and the few hits are
+        // recorded after each chunk -- no store per candidate.  The list keeps the first
+        // kNearCap hits in slot order; nn counts them all.
         uint16_t* ql = lst + threadIdx.x;
-        int nn = 0, at = 0;
-        // stencil pruning (conservative: margins above the fp32 rounding of the cell
-        // bounds): a row of three cells is skipped when its slab lies beyond the largest
-        // reach of i, and its end cells when the chord of the reach sphere misses them
-        const float cutm = __fadd_rn(__fadd_rn(__fadd_rn(mw, g.rmax_f), g.extra_f), __fmul_rn(2.f, g.margin_f));
-        const float cut2 = __fmul_rn(__fmul_rn(cutm, cutm), 1.00001f);
-        const int hy = (hc / kHX) % kHY, hz = hc / (kHX * kHY);
-        const float fx = __fsub_rn(mx, __fmul_rn(static_cast<float>(x0 - 1 + hx), g.edge_f[0]));
-        const float fy = __fsub_rn(my, __fmul_rn(static_cast<float>(y0 - 1 + hy), g.edge_f[1]));
-        const float fz = __fsub_rn(mz, __fmul_rn(static_cast<float>(z0 - 1 + hz), g.edge_f[2]));
-        const float gx = __fsub_rn(g.edge_f[0], fx), gy = __fsub_rn(g.edge_f[1], fy), gz = __fsub_rn(g.edge_f[2], fz);
+        int nn = 0;
+        auto record = [&](int k) {
+            if (nn < kNearCap) ql[nn * kTileThreads] = static_cast<uint16_t>(k);
+            ++nn;
+        };
 #pragma unroll
         for (int ddz = -1; ddz <= 1; ++ddz) {
 #pragma unroll
             for (int ddy = -1; ddy <= 1; ++ddy) {
                 const int c = hc + ddy * kHX + ddz * kHX * kHY;
-#if SRM_NEAR_PRUNE
-                const float dyd = fmaxf(0.f, __fsub_rn(ddy < 0 ? fy : (ddy > 0 ? gy : 0.f), g.margin_f));
-                const float dzd = fmaxf(0.f, __fsub_rn(ddz < 0 ? fz : (ddz > 0 ? gz : 0.f), g.margin_f));
-                const float dyz2 = __fmaf_rn(dyd, dyd, __fmul_rn(dzd, dzd));
-                if (dyz2 > cut2) continue;
-                float h;  // chord half length; sqrt.approx (rel. error < 2^-22) scaled up by 2^-20
-                asm("sqrt.approx.f32 %0, %1;" : "=f"(h) : "f"(__fsub_rn(cut2, dyz2)));
-                h = __fadd_rn(__fmul_rn(h, 1.000001f), __fmul_rn(2.f, g.margin_f));
-                const int kb = hoff[fx < h ? c - 1 : c], ke = hoff[gx < h ? c + 2 : c + 1];
-#else
                 const int kb = hoff[c - 1], ke = hoff[c + 2];
-#endif
-                // slots [kb, ke) two at a time (pairs 2p, 2p + 1; the ends masked)
-                for (int p = kb >> 1; 2 * p < ke; ++p) {
-                    const float4 A = pxy[p], B = pzw[p];
-                    const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
-                    const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
-                    const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
-                    const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
-                    const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
-                    const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
-                    const int k0 = 2 * p;
-                    ql[at * kTileThreads] = static_cast<uint16_t>(k0);
-                    nn += (d2.x <= l2.x && k0 >= kb && k0 != i) ? 1 : 0;
-                    at = min(nn, kNearCap);
-                    ql[at * kTileThreads] = static_cast<uint16_t>(k0 + 1);
-                    nn += (d2.y <= l2.y && k0 + 1 < ke && k0 + 1 != i) ? 1 : 0;
-                    at = min(nn, kNearCap);
+                // slots [kb, ke) two at a time (pairs 2p, 2p + 1), 16 pairs per mask
+                for (int pb = kb >> 1; 2 * pb < ke; pb += 16) {
+                    const int pe = min((ke + 1) >> 1, pb + 16);
+                    unsigned hits = 0u, bit = 1u;
+                    for (int p = pb; p < pe; ++p) {
+                        const float4 A = pxy[p], B = pzw[p];
+                        const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                        const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                        const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                        const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                        const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                        const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                        if (d2.x <= l2.x) hits |= bit;
+                        if (d2.y <= l2.y) hits |= bit << 1;
+                        bit <<= 2;
+                    }
+                    if (hits) {  // the slots of the hits: in [kb, ke), not i itself
+                        const int k0 = 2 * pb;
+                        if (kb > k0) hits &= ~1u;
+                        const int top = ke - k0;  // slots k0 + top ... are past the range
+                        if (top < 32) hits &= (1u << top) - 1u;
+                        if (i >= k0 && i < k0 + 32) hits &= ~(1u << (i - k0));
+                        while (hits) {
+                            record(k0 + __ffs(hits) - 1);
+                            hits &= hits - 1u;
+                        }
+                    }
                 }
             }
         }

@@ -181,6 +181,74 @@ def e2e_platelet_case(name, c):
     print(name, np.array(stats).mean(0))
 
 
+# cfg 4's parameters at N = 10^6, an ensemble of reference runs (the spot check's
+# tolerance is the reference's own configuration-to-configuration spread AT this N)
+LARGE_ENS = dict(n=1_000_000, f0=0.1, f_t=0.3, cm_rel=0.05, c_w=0.02, n_k=10, n_l=10, seeds=[1, 2, 3, 4])
+
+
+def _large_one(args):
+    c, s = args
+    from scipy.spatial import cKDTree
+    n = c["n"]
+    L = [1.0] * 3
+    r0 = (c["f0"] / (n * unit(3))) ** (1.0 / 3.0)
+    rt = (c["f_t"] / (n * unit(3))) ** (1.0 / 3.0)
+    st, pos, ids, _ = orc.r_rsa(3, L, np.full(n, r0), 10000, 1000 + s)
+    assert st == 0
+    st, pos, r, ids, it, f, acc = orc.r_generate(3, L, pos, np.full(n, r0), ids, c["c_w"], c["cm_rel"] * rt,
+                                                 c["n_k"], c["n_l"], c["f_t"], 100000, s, 16)
+    assert st == 0
+    nnd = orc.r_nnd(3, L, pos) / rt
+    edges = np.linspace(2.0 * 0.999, 5.0, 61) * rt
+    cum = cKDTree(pos, boxsize=1.0).count_neighbors(cKDTree(pos, boxsize=1.0), edges)
+    return (stats_util.ensemble_stats([nnd], 1.0)[0], np.histogram(nnd, np.linspace(2.0 * 0.999, 2.8, 41))[0],
+            np.diff(cum) // 2, it)
+
+
+def e2e_large_ensemble(name, c):
+    from multiprocessing import Pool
+    with Pool(len(c["seeds"])) as pool:
+        res = pool.map(_large_one, [(c, s) for s in c["seeds"]])
+    rt = (c["f_t"] / (c["n"] * unit(3))) ** (1.0 / 3.0)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), r_target=rt, summary=np.array([r[0] for r in res]),
+                        nnd_hist=np.array([r[1] for r in res]), rdf=np.array([r[2] for r in res]),
+                        iterations=np.array([r[3] for r in res]), **{k: np.array(v) for k, v in c.items()})
+    print(name, np.array([r[0] for r in res]), [r[3] for r in res])
+
+
+# cfg 1 at full size with BASELINE's literal start: uniform random centres (numpy PCG64,
+# seed 5000 + s), radius grown from half the smallest centre distance (reference
+# nearest_neighbor_distances) x (1 - 1e-9) to f = 0.5; c_m = 0.1 r_t, c_w 0.02, n_k = n_l = 10
+CFG1 = dict(n=10_000, f_t=0.5, cm_rel=0.1, c_w=0.02, n_k=10, n_l=10, seeds=list(range(1, 13)))
+
+
+def cfg1_start(n, s):
+    pos = np.random.default_rng(5000 + s).random((n, 2))
+    return pos
+
+
+def e2e_cfg1_full(name, c):
+    n = c["n"]
+    L = [1.0, 1.0]
+    rt = (c["f_t"] / (n * np.pi)) ** 0.5
+    nnd, r0s, its, rdf_seeds = [], [], [], []
+    for s in c["seeds"]:
+        pos = cfg1_start(n, s)
+        r0 = 0.5 * float(orc.r_nnd(2, L, pos).min()) * (1.0 - 1e-9)
+        st, pos, r, ids, it, f, acc = orc.r_generate(2, L, pos, np.full(n, r0), np.arange(n, dtype=np.int32),
+                                                     c["c_w"], c["cm_rel"] * rt, c["n_k"], c["n_l"], c["f_t"],
+                                                     100000, s, 16)
+        assert st == 0
+        nnd.append(orc.r_nnd(2, L, pos))
+        rdf_seeds.append(stats_util.rdf_counts(pos, L, 2.0 * rt * 0.999, 5.0 * rt, 60))
+        r0s.append(r0)
+        its.append(it)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), nnd=np.array(nnd), r0=np.array(r0s),
+                        iterations=np.array(its), r_target=rt, c_m=c["cm_rel"] * rt, rdf=np.sum(rdf_seeds, 0),
+                        rdf_seeds=np.array(rdf_seeds), dim=2, f0=0.0, **{k: np.array(v) for k, v in c.items()})
+    print(name, its, r0s[:3])
+
+
 def grid_case(name, dim, n, rmin, rmax, cs, seed, L):
     pos, r = orc.random_particles(n, dim, rmin, rmax, L, seed)
     keys, _ = orc.r_keys(dim, L, cs, pos)
@@ -205,6 +273,10 @@ def main():
                 e2e_poly_case(name, POLY)
             elif name == "e2e_cfg4_large":
                 e2e_large_case(name, LARGE)
+            elif name == "e2e_cfg4_large_ens":
+                e2e_large_ensemble(name, LARGE_ENS)
+            elif name == "e2e_cfg1_full":
+                e2e_cfg1_full(name, CFG1)
             elif name == "e2e_platelet":
                 e2e_platelet_case(name, PLATE)
             else:

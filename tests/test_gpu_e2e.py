@@ -204,3 +204,72 @@ def test_platelet_statistics_match_reference():
     ok, _ = stats_util.hist_agree(h_dev.sum(0), h_ref.sum(0))
     assert ok.all(), f"NND bins out of tolerance: {np.where(~ok)[0]}"
     assert stats_util.ensemble_chi2(h_dev, h_ref) > 1e-3
+
+
+def test_cfg1_full_size_literal_start_matches_reference():
+    """BASELINE cfg 1 at its stated size and start: 10^4 disks, uniform random centres,
+    radius grown from half the smallest centre distance x (1 - 1e-9) to f = 0.5 with
+    c_m = 0.1 r_t (tests/golden/make_golden.py CFG1; the reference's srm_generate on the
+    same 12 starts in e2e_cfg1_full.npz).  The start radius comes from the device's exact
+    nearest-neighbour search and equals the reference's bit for bit; every run reaches
+    f_t within 1e-9 with zero overlaps (oracle audit); the ensemble statistics (NND and
+    RDF, check_against_reference) match the reference's."""
+    import make_golden
+    z = load("e2e_cfg1_full")
+    c = make_golden.CFG1
+    n, L = c["n"], [1.0, 1.0]
+    rt = float(z["r_target"])
+    nnd, rdf = [], []
+    for k, s in enumerate(c["seeds"]):
+        pos = make_golden.cfg1_start(n, s)
+        with srm.Context(L, n) as ctx:
+            ctx.upload(pos, np.full(n, 1e-12))
+            r0 = 0.5 * float(ctx.nearest_neighbor_distances().min()) * (1.0 - 1e-9)
+        assert r0 == float(z["r0"][k])
+        snap = srm.Snapshot(L, pos, np.full(n, r0))
+        p = srm.SrmParams(c_w=c["c_w"], c_m=c["cm_rel"] * rt, n_k=c["n_k"], n_l=c["n_l"], f_target=c["f_t"],
+                          max_iterations=100000, seed=s, reorder_period=16)
+        res = srm.srm_generate(snap, p)
+        assert res.status == srm.GenerateStatus.Converged
+        out = res.snapshot
+        assert abs(out.volume_fraction / c["f_t"] - 1.0) < 1e-9
+        assert orc.o_stats(2, L, out.pos, out.radius).overlap_pairs == 0
+        nnd.append(orc.r_nnd(2, L, out.pos))
+        rdf.append(stats_util.rdf_counts(out.pos, L, *stats_util.rdf_window(z)))
+    stats_util.check_against_reference(nnd, rdf, z)
+
+
+def test_large_n_ensemble_cfg4_parameters():
+    """cfg 4's parameters at N = 10^6 (f 0.1 -> 0.3, c_m = 0.05 r_t): 4 device runs from
+    the reference's own starts (rsa_place, bit-identical) against 4 reference runs at the
+    same N (tests/golden/e2e_cfg4_large_ens.npz).  The tolerance is the reference's
+    configuration-to-configuration spread at THIS N (not at 4000): per NND summary a
+    Welch t-test (p > 1e-3) and |mean difference| <= 4 x the standard error of the
+    difference; the NND histograms (40 bins over [2, 2.8] r_t, device srm_b200_nnd_histogram)
+    by ensemble chi-square.  Zero overlaps and f_t within 1e-9 on every run."""
+    z = load("e2e_cfg4_large_ens")
+    n = int(z["n"])
+    L = [1.0, 1.0, 1.0]
+    r0 = (float(z["f0"]) / (n * 4.0 / 3.0 * np.pi)) ** (1.0 / 3.0)
+    rt = float(z["r_target"])
+    summ, hists = [], []
+    for s in z["seeds"]:
+        pos, ids = srm.rsa_place(np.full(n, r0), L, 10000, 1000 + int(s))
+        p = srm.SrmParams(c_w=float(z["c_w"]), c_m=float(z["cm_rel"]) * rt, n_k=int(z["n_k"]), n_l=int(z["n_l"]),
+                          f_target=float(z["f_t"]), max_iterations=100000, seed=100 + int(s), reorder_period=16)
+        with srm.Context(L, n) as ctx:
+            ctx.upload(pos, np.full(n, r0), ids)
+            out = ctx.generate(p)
+            assert abs(out.volume_fraction / float(z["f_t"]) - 1.0) < 1e-9
+            assert ctx.overlap_stats(2.5 * ctx.max_bounding_radius()).overlap_pairs == 0
+            summ.append(stats_util.ensemble_stats([ctx.nearest_neighbor_distances() / rt], 1.0)[0])
+            hists.append(ctx.nnd_histogram(40, 2.0 * 0.999 * rt, 2.8 * rt)[0])
+    summ = np.array(summ)
+    ref = z["summary"]
+    ps = stats_util.ensemble_agree(summ, ref)
+    se = np.sqrt(summ.var(0, ddof=1) / len(summ) + ref.var(0, ddof=1) / len(ref))
+    d = np.abs(summ.mean(0) - ref.mean(0))
+    print(f"1e6 ensemble: device {summ.mean(0)} reference {ref.mean(0)} se {se} Welch p {ps}")
+    assert min(ps) > 1e-3, f"NND summaries differ: Welch p = {ps}"
+    assert (d <= 4.0 * se + 1e-12).all(), f"|d| = {d} > 4 se = {4 * se}"
+    assert stats_util.ensemble_chi2(np.array(hists), z["nnd_hist"]) > 1e-3
