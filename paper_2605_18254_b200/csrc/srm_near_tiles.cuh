@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         rmap[r] = m;
     }
     __syncthreads();
+    bool same_r = true;  // every staged radius equals the grid's largest: monodisperse brick
     for (int k0 = 0; k0 < total; k0 += 4 * kTileThreads) {
         float4 v[4];
         int32_t src[4];
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                 b[0] = __fadd_rn(v[u].z, szf[u]);
                 b[2] = v[u].w;
                 pj[k] = src[u];
+                same_r = same_r && v[u].w == g.rmax_f;
             }
         }
     }
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         if (lane < nr) rowoff[lane] = in - c;
         if (lane == nr - 1) rowoff[nr] = in;
     }
-    __syncthreads();
+    const bool mono = __syncthreads_and(same_r) != 0;
     // 4. screen every interior particle against its 3x3x3 stencil in shared memory
     const int nr = wy * wz;
     const int nint = rowoff[nr];
@@ -210,6 +212,8 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         const float base = __fadd_rn(__fadd_rn(mw, g.extra_f), g.margin_f);  // + r_j
         const float2 nmx = make_float2(-mx, -mx), nmy = make_float2(-my, -my), nmz = make_float2(-mz, -mz);
         const float2 base2 = make_float2(base, base), fac2 = make_float2(1.00001f, 1.00001f);
+        const float limm = __fadd_rn(g.rmax_f, base);  // (monodisperse bricks: r_j = rmax)
+        const float l2m = __fmul_rn(__fmul_rn(limm, limm), 1.00001f);
         // hits are rare (0.8 per particle at the bench window): the screen of a range sets a
         // bit per hit in a register mask (16 slot pairs per mask) and the few hits are
         // recorded after each chunk -- no store per candidate.  The list keeps the first
@@ -230,17 +234,31 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                 for (int pb = kb >> 1; 2 * pb < ke; pb += 16) {
                     const int pe = min((ke + 1) >> 1, pb + 16);
                     unsigned hits = 0u, bit = 1u;
-                    for (int p = pb; p < pe; ++p) {
-                        const float4 A = pxy[p], B = pzw[p];
-                        const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
-                        const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
-                        const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
-                        const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
-                        const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
-                        const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
-                        if (d2.x <= l2.x) hits |= bit;
-                        if (d2.y <= l2.y) hits |= bit << 1;
-                        bit <<= 2;
+                    if (mono) {  // the same cutoff for every candidate (bit for bit the general one)
+                        for (int p = pb; p < pe; ++p) {
+                            const float4 A = pxy[p];
+                            const float2 Bz = *reinterpret_cast<const float2*>(pzw + p);
+                            const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                            const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                            const float2 ez = __fadd2_rn(Bz, nmz);
+                            const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                            if (d2.x <= l2m) hits |= bit;
+                            if (d2.y <= l2m) hits |= bit << 1;
+                            bit <<= 2;
+                        }
+                    } else {
+                        for (int p = pb; p < pe; ++p) {
+                            const float4 A = pxy[p], B = pzw[p];
+                            const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                            const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                            const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                            const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                            const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                            const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                            if (d2.x <= l2.x) hits |= bit;
+                            if (d2.y <= l2.y) hits |= bit << 1;
+                            bit <<= 2;
+                        }
                     }
                     if (hits) {  // the slots of the hits: in [kb, ke), not i itself
                         const int k0 = 2 * pb;
