@@ -343,10 +343,13 @@ def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
     if kind == "platelet":
         Lb = [cfg["L"] * box] * 3
         D0 = (cfg["rho0"] * Lb[0] ** 3 / n) ** (1.0 / 3.0)
-        pos, nrm, ids = srm.rsa_platelets(n, D0, cfg["aspect"], Lb, 100000, seed)
-        t_rsa = time.time() - t0
         ctx = srm.Context(Lb, n, device, shape="platelet")
-        ctx.upload_platelets(pos, nrm, np.full(n, D0), np.full(n, D0 / cfg["aspect"]), ids)
+        if DEVICE_RSA:  # srm_b200_rsa_platelets_device
+            ctx.rsa_platelets_device(n, D0, cfg["aspect"], seed)
+        else:
+            pos, nrm, ids = srm.rsa_platelets(n, D0, cfg["aspect"], Lb, 100000, seed)
+            ctx.upload_platelets(pos, nrm, np.full(n, D0), np.full(n, D0 / cfg["aspect"]), ids)
+        t_rsa = time.time() - t0
         c_m, n_k, n_l = cfg["cm_abs"], cfg["n_k"], cfg["n_l"]
         params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, c_r=cfg["c_r"], n_k=n_k, n_l=n_l,
                                f_target=F_WINDOW * cfg["f_target"], max_iterations=cfg.get("prep_iters", 100000),
@@ -543,8 +546,8 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--device-rsa", action="store_true",
-                    help="monodisperse starts from the device RSA (statistically equal, not bit-identical, to the "
-                         "reference's rsa_place)")
+                    help="the start from the device RSA (rsa_place / rsa_platelets in rounds: statistically equal, "
+                         "not bit-identical, to the reference's)")
     args = ap.parse_args()
     global DEVICE_RSA
     DEVICE_RSA = args.device_rsa

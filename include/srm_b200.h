@@ -262,6 +262,14 @@ int srm_b200_rsa_clustered(int dim, const double* box_lengths, int64_t n, const 
  * (placed_out / rounds_out report), INVALID. */
 int srm_b200_rsa_device(srm_b200_ctx* ctx, int64_t n, const double* radii, uint64_t seed, int64_t max_rounds,
                         int64_t* placed_out, int64_t* rounds_out);
+/* rsa_platelets (recipes.cpp:107-148) on the device: the same rounds with candidate =
+ * (Philox centre, Philox unit normal), placed iff the reference's overlap(candidate, p)
+ * (candidate first) is false for every platelet placed before it in (round, index) order
+ * (oracle orc_rsa_pl_rounds, bit for bit).  Diameter D, thickness D / aspect_ratio for all;
+ * the state (id = index) is left in the platelet context.  OK, PLACEMENT_FAILURE after
+ * max_rounds (placed_out / rounds_out report), INVALID (recipes.cpp:109-117 checks). */
+int srm_b200_rsa_platelets_device(srm_b200_ctx* ctx, int64_t n, double diameter, double aspect_ratio, uint64_t seed,
+                                  int64_t max_rounds, int64_t* placed_out, int64_t* rounds_out);
 /* random.hpp:84-89 mix_seed */
 uint64_t srm_b200_mix_seed(uint64_t seed, uint64_t stream);
 

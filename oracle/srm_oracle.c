@@ -743,3 +743,41 @@ int64_t orc_rsa_rounds(int dim, const double* L, int64_t n, const double* radii,
     if (rounds_out) *rounds_out = r;
     return count;
 }
+
+/* Platelet RSA in rounds (the device's srm_b200_rsa_platelets_device; recipes.cpp:107-148
+ * restated the same way as orc_rsa_rounds): in round r every unplaced platelet i draws a
+ * centre (orc_rsa_candidate) and a normal (unit vector of slot i, attempt r, stream 1 with
+ * round_id 0xFFFFFF and iteration 0xFFFFFFFF) and is placed iff the reference's test
+ * overlap(candidate, p) (shape.hpp:64-73, candidate first) is false for every platelet p
+ * placed before it in (round, index) order.  All platelets share diameter D and
+ * thickness t = D / aspect (recipes.cpp:116-117). */
+int64_t orc_rsa_pl_rounds(const double* L, int64_t n, double D, double t, uint64_t seed, int64_t max_rounds,
+                          double* pos, double* nrm, uint8_t* placed, int64_t* rounds_out) {
+    int64_t count = 0, r = 0;
+    int64_t* list = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) placed[i] = 0;
+    for (r = 0; r < max_rounds && count < n; ++r) {
+        for (int64_t i = 0; i < n; ++i) {
+            if (placed[i]) continue;
+            double c[3], u[3];
+            orc_rsa_candidate(3, L, seed, (uint32_t)i, (uint32_t)r, c);
+            orc_unit_vector(3, seed, (uint32_t)i, (uint32_t)r, 1, 0xFFFFFFu, 0xFFFFFFFFu, u);
+            int hit = 0;
+            for (int64_t k = 0; k < count && !hit; ++k) {
+                const int64_t j = list[k];
+                hit = orc_pl_overlap(L, c, u, D, t, pos + 3 * j, nrm + 3 * j, D, t);
+            }
+            if (!hit) {
+                for (int a = 0; a < 3; ++a) {
+                    pos[3 * i + a] = c[a];
+                    nrm[3 * i + a] = u[a];
+                }
+                placed[i] = 1;
+                list[count++] = i;
+            }
+        }
+    }
+    free(list);
+    if (rounds_out) *rounds_out = r;
+    return count;
+}

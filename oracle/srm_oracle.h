@@ -120,6 +120,8 @@ void orc_rsa_candidate(int dim, const double* L, uint64_t seed, uint32_t i, uint
  * the number placed. */
 int64_t orc_rsa_rounds(int dim, const double* L, int64_t n, const double* radii, uint64_t seed, int64_t max_rounds,
                        double* pos, uint8_t* placed, int64_t* rounds_out);
+int64_t orc_rsa_pl_rounds(const double* L, int64_t n, double D, double t, uint64_t seed, int64_t max_rounds,
+                          double* pos, double* nrm, uint8_t* placed, int64_t* rounds_out);
 
 /* ---- reductions ---------------------------------------------------------------- */
 double orc_max_radius(int64_t n, const double* r);

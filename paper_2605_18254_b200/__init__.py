@@ -426,6 +426,22 @@ class Context:
         self.n = len(radii)
         return rounds.value
 
+    def rsa_platelets_device(self, n: int, diameter: float, aspect_ratio: float, seed: int,
+                             max_rounds: int = 100000) -> int:
+        """rsa_platelets (recipes.cpp:107-148) in rounds on the device into
+        this platelet context (id = index).  Returns the number of rounds; raises
+        PlacementFailure / ValidationError as the reference."""
+        placed, rounds = C.c_int64(), C.c_int64()
+        st = _native.lib().srm_b200_rsa_platelets_device(self._h, int(n), float(diameter), float(aspect_ratio),
+                                                         seed & 0xFFFFFFFFFFFFFFFF, int(max_rounds), C.byref(placed),
+                                                         C.byref(rounds))
+        if st == PLACEMENT_FAILURE:
+            raise PlacementFailure(f"rsa_platelets_device: {placed.value} of {n} placed after {rounds.value} rounds",
+                                   placed.value, int(max_rounds))
+        self._c(st)
+        self.n = int(n)
+        return rounds.value
+
     def nearest_neighbor_distances(self) -> np.ndarray:
         """descriptors.hpp:96-115 on the device (download order)."""
         out = np.empty(max(self.n, 1))

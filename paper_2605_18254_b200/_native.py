@@ -112,6 +112,8 @@ _SIGS = {
     "srm_b200_snapshot_info": (C.c_int, [C.c_char_p, c_int_p, c_int_p, c_int64_p, c_double_p, C.c_void_p]),
     "srm_b200_load_snapshot": (C.c_int, [C.c_void_p, C.c_char_p]),
     "srm_b200_io_error": (C.c_char_p, []),
+    "srm_b200_rsa_platelets_device": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_uint64, C.c_int64,
+                                                c_int64_p, c_int64_p]),
     "srm_b200_rsa_device": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64, C.c_int64, c_int64_p, c_int64_p]),
     "srm_b200_nnd_histogram": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_void_p, c_int64_p, c_int64_p,
                                          C.c_void_p]),

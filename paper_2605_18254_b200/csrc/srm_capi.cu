@@ -1333,6 +1333,73 @@ int srm_b200_rsa_device(srm_b200_ctx* c, int64_t n, const double* radii, uint64_
     });
 }
 
+// recipes.cpp:107-148 rsa_platelets, in rounds on the device
+int srm_b200_rsa_platelets_device(srm_b200_ctx* c, int64_t n, double diameter, double aspect_ratio, uint64_t seed,
+                                  int64_t max_rounds, int64_t* placed_out, int64_t* rounds_out) {
+    if (placed_out) *placed_out = 0;
+    if (rounds_out) *rounds_out = 0;
+    if (!c) return SRM_B200_INVALID;
+    return guarded(c, [&]() -> int {
+        if (!c->platelets()) throw Invalid{"rsa_platelets_device: a platelet context is required"};
+        if (n < 1 || n > c->cap) throw Invalid{"rsa_platelets: n must be >= 1"};  // recipes.cpp:109
+        if (!(aspect_ratio > 1.0)) throw Invalid{"rsa_platelets: aspect ratio must exceed 1"};
+        if (!(diameter > 0.0)) throw Invalid{"rsa_platelets: diameter must be positive"};
+        const double thickness = diameter / aspect_ratio;  // recipes.cpp:112-117
+        const double bound = 0.5 * (diameter + thickness);
+        double min_len = c->box.L[0];
+        for (int a = 1; a < 3; ++a) min_len = std::min(min_len, c->box.L[a]);
+        if (!(bound < min_len / 4.0)) throw Invalid{"rsa_platelets: platelet too large for the box"};
+        {
+            std::vector<double> zero(static_cast<size_t>(n) * 3, 0.0), up(static_cast<size_t>(n) * 3, 0.0);
+            for (int64_t i = 0; i < n; ++i) up[3 * i + 2] = 1.0;
+            std::vector<double> D(static_cast<size_t>(n), diameter), t(static_cast<size_t>(n), thickness);
+            std::vector<int32_t> ids(static_cast<size_t>(n));
+            for (int64_t i = 0; i < n; ++i) ids[i] = static_cast<int32_t>(i);
+            const int st = srm_b200_upload_platelets(c, n, zero.data(), up.data(), D.data(), t.data(), ids.data());
+            if (st != SRM_B200_OK) return st;
+        }
+        // cells of at least two bounding radii: every overlapping pair is in the one-cell stencil
+        c->set_grid(c->make_grid(2.0 * bound * (1.0 + 1e-8), bound, 0.0));
+        DevBuf<uint8_t> placed(n);
+        DevBuf<int8_t> state(n);
+        DevBuf<int32_t> conf(n * kRsaConf), nconf(n);
+        DevBuf<int64_t> where(n);
+        DevBuf<unsigned long long> count(1);
+        DevBuf<int> flag(1);
+        SRM_CUDA(cudaMemsetAsync(placed.p, 0, static_cast<size_t>(n), c->stream));
+        SRM_CUDA(cudaMemsetAsync(count.p, 0, sizeof(unsigned long long), c->stream));
+        const int nb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 16));
+        const int nbc = static_cast<int>(std::min<int64_t>(blocks_for(n, 128), 148 * 16));
+        const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+        unsigned long long done = 0;
+        int64_t r = 0;
+        for (; r < max_rounds && static_cast<int64_t>(done) < n; ++r) {
+            k_rsa_pl_propose<<<nb, 256, 0, c->stream>>>(n, c->P.rec, c->P.aux, placed.p, c->box, k0, k1,
+                                                        static_cast<uint32_t>(r));
+            c->grid_build(c->P);
+            k_rsa_pl_check<<<nbc, 128, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, placed.p,
+                                                       state.p, conf.p, nconf.p, where.p);
+            c->launched(2);
+            int h = 1;
+            while (h > 0) {
+                SRM_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
+                k_rsa_pl_resolve<<<nb, 256, 0, c->stream>>>(n, placed.p, state.p, conf.p, nconf.p, flag.p, c->S, c->box,
+                                                            c->gp, c->cell_start, c->skey, where.p);
+                c->launched();
+                SRM_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+                SRM_CUDA(cudaStreamSynchronize(c->stream));
+            }
+            k_rsa_commit<<<nb, 256, 0, c->stream>>>(n, placed.p, state.p, count.p);
+            c->launched();
+            SRM_CUDA(cudaMemcpyAsync(&done, count.p, sizeof(done), cudaMemcpyDeviceToHost, c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        if (placed_out) *placed_out = static_cast<int64_t>(done);
+        if (rounds_out) *rounds_out = r;
+        return static_cast<int64_t>(done) == n ? SRM_B200_OK : SRM_B200_PLACEMENT_FAILURE;
+    });
+}
+
 int srm_b200_pair_counts(srm_b200_ctx* c, const double* edges, int bins, int64_t* counts_out) {
     return guarded(c, [&]() -> int {
         const int64_t n = c->n;

@@ -142,4 +142,102 @@ __global__ void k_rsa_commit(int64_t n, uint8_t* __restrict__ placed, const int8
     if (c) atomicAdd(count, c);
 }
 
+// ---- platelets (rsa_platelets, recipes.cpp:107-148) ---------------------------------
+// The same rounds with candidate = (centre, normal): the centre as for spheres, the normal
+// the unit vector of (slot i, attempt r, stream 1) under the key (seed, round_id 0xFFFFFF,
+// iteration 0xFFFFFFFF) -- counters no sweep uses.  A candidate is placed iff the
+// reference's test overlap(candidate, p) (shape.hpp:64-73, candidate first; asymmetric)
+// is false for every platelet p placed before it in (round, index) order (oracle
+// orc_rsa_pl_rounds).  Records: rec = (centre, D), aux = (normal, t).
+__device__ __forceinline__ RngKey rsa_pl_key(uint32_t k0, uint32_t k1) { return RngKey{k0, k1, 0xFFFFFFu, 0xFFFFFFFFu}; }
+
+__global__ void k_rsa_pl_propose(int64_t n, double4* __restrict__ rec, double4* __restrict__ aux,
+                                 const uint8_t* __restrict__ placed, Box box, uint32_t k0, uint32_t k1,
+                                 uint32_t round) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (placed[i]) continue;
+        double c[3], u[3];
+        rsa_candidate(3, box, k0, k1, static_cast<uint32_t>(i), round, c);
+        unit_vector<3>(rsa_pl_key(k0, k1), static_cast<uint32_t>(i), round, 1, u);
+        rec[i] = make_double4(c[0], c[1], c[2], rec[i].w);
+        aux[i] = make_double4(u[0], u[1], u[2], aux[i].w);
+    }
+}
+
+// overlap(candidate at sorted q, platelet at sorted j) with the candidate first
+__device__ __forceinline__ bool rsa_pl_hits(const State& S, const Box& box, int64_t q, int64_t j) {
+    const double4 v = S.rec[q], a = S.aux[q], w = S.rec[j], b = S.aux[j];
+    const pl::V3 d{min_image1(w.x - v.x, box.L[0], box.half[0]), min_image1(w.y - v.y, box.L[1], box.half[1]),
+                   min_image1(w.z - v.z, box.L[2], box.half[2])};
+    return pl::spherodisk_overlap(d, pl::V3{a.x, a.y, a.z}, v.w, a.w, pl::V3{b.x, b.y, b.z}, w.w, b.w, c_seed_table);
+}
+
+__global__ void __launch_bounds__(256) k_rsa_pl_check(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
+                                                      const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                      const uint8_t* __restrict__ placed, int8_t* __restrict__ state,
+                                                      int32_t* __restrict__ conf, int32_t* __restrict__ nconf,
+                                                      int64_t* __restrict__ where) {
+    const GridParams& g = *gp;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = S.id[q];
+        if (placed[i]) continue;
+        where[i] = q;
+        bool clear = true;
+        int nc = 0;
+        for_near_ranges<3>(g, cs, skey[q], g.near_s, [&](int64_t b, int64_t e) {
+            for (int64_t j = b; j < e && clear; ++j) {
+                if (j == q) continue;
+                const int32_t k = S.id[j];
+                if (!placed[k] && k > i) continue;  // later candidates of the round do not matter to i
+                if (!rsa_pl_hits(S, box, q, j)) continue;
+                if (placed[k]) {
+                    clear = false;
+                } else {
+                    if (nc < kRsaConf) conf[static_cast<int64_t>(i) * kRsaConf + nc] = k;
+                    ++nc;
+                }
+            }
+        });
+        state[i] = clear ? 0 : 2;
+        nconf[i] = clear ? nc : 0;
+    }
+}
+
+__global__ void k_rsa_pl_resolve(int64_t n, const uint8_t* __restrict__ placed, int8_t* __restrict__ state,
+                                 const int32_t* __restrict__ conf, const int32_t* __restrict__ nconf,
+                                 int* __restrict__ undecided, State S, Box box, const GridParams* __restrict__ gp,
+                                 const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                 const int64_t* __restrict__ where) {
+    int left = 0;
+    const volatile int8_t* vs = state;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (placed[i] || state[i] != 0) continue;
+        const int nc = nconf[i];
+        bool all_rejected = true, any_accepted = false;
+        if (nc <= kRsaConf) {
+            for (int t = 0; t < nc; ++t) {
+                const int8_t st = vs[conf[i * kRsaConf + t]];
+                any_accepted = any_accepted || st == 1;
+                all_rejected = all_rejected && st == 2;
+            }
+        } else {  // more conflicts than kept: rescan the stencil for them
+            const int64_t q = where[i];
+            for_near_ranges<3>(*gp, cs, skey[q], gp->near_s, [&](int64_t b, int64_t e) {
+                for (int64_t j = b; j < e; ++j) {
+                    const int32_t k = S.id[j];
+                    if (j == q || k >= i || placed[k]) continue;
+                    if (!rsa_pl_hits(S, box, q, j)) continue;
+                    const int8_t st = vs[k];
+                    any_accepted = any_accepted || st == 1;
+                    all_rejected = all_rejected && st == 2;
+                }
+            });
+        }
+        if (any_accepted) state[i] = 2;
+        else if (all_rejected) state[i] = 1;
+        else ++left;
+    }
+    if (left) atomicAdd(undecided, left);
+}
+
 }  // namespace srmb

@@ -395,3 +395,18 @@ def o_rsa_rounds(dim, L, radii, seed, max_rounds):
     cnt = f(dim, P(arr(L)), n, P(radii), C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), int(max_rounds), P(pos), P(placed),
             C.byref(rounds))
     return cnt, rounds.value, pos, placed
+
+
+def o_rsa_pl_rounds(L, n, D, aspect, seed, max_rounds):
+    """oracle/srm_oracle.c orc_rsa_pl_rounds: (placed count, rounds, pos, normals, placed flags)"""
+    pos = np.zeros((n, 3))
+    nrm = np.zeros((n, 3))
+    placed = np.zeros(n, np.uint8)
+    rounds = C.c_int64()
+    f = orc().orc_rsa_pl_rounds
+    f.restype = C.c_int64
+    f.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p,
+                  C.c_void_p, C.c_void_p]
+    cnt = f(P(arr(L)), n, D, D / aspect, C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), int(max_rounds), P(pos), P(nrm),
+            P(placed), C.byref(rounds))
+    return cnt, rounds.value, pos, nrm, placed

@@ -57,3 +57,58 @@ def test_rsa_device_statistics_match_reference_rsa():
         ref.append(orc.r_nnd(3, L, pos))
     ps = stats_util.ensemble_agree(stats_util.ensemble_stats(dev, rt), stats_util.ensemble_stats(ref, rt))
     assert min(ps) > 1e-3, f"RSA NND summaries differ: Welch p = {ps}"
+
+
+# ---- platelets: rsa_platelets (recipes.cpp:107-148) in rounds ---------------------------
+@pytest.mark.parametrize("n,L,aspect,seed", [(300, 6.0, 20.0, 5), (500, 8.0, 100.0, 6), (2000, 12.0, 100.0, 7)])
+def test_rsa_platelets_device_bit_exact_vs_oracle(n, L, aspect, seed):
+    Lb = [L] * 3
+    with srm.Context(Lb, n, shape="platelet") as ctx:
+        rounds = ctx.rsa_platelets_device(n, 1.0, aspect, 0x77 + seed)
+        pos, nrm, D, t, ids = ctx.download_platelets()
+    cnt, orounds, opos, onrm, placed = orc.o_rsa_pl_rounds(Lb, n, 1.0, aspect, 0x77 + seed, 100000)
+    assert cnt == n and placed.all() and rounds == orounds
+    assert np.array_equal(ids, np.arange(n))
+    assert np.array_equal(pos, opos) and np.array_equal(nrm, onrm)
+    assert np.all(D == 1.0) and np.all(t == 1.0 / aspect)
+    assert orc.o_pl_pairs(Lb, pos, nrm, D, t, ids) == 0  # no ordered pair overlaps
+
+
+def test_rsa_platelets_device_statistics_match_reference():
+    """The same process as the reference's rsa_platelets with another random stream:
+    per-seed centre-NND quantiles and the nematic order parameter (isotropic start) by
+    Welch t-tests across 12 configurations of 1500 platelets (aspect 20, rho = 2)."""
+    n, aspect = 1500, 20.0
+    L = (n / 2.0) ** (1.0 / 3.0)
+    Lb = [L] * 3
+
+    def summary(pos, nrm):
+        nnd = orc.r_nnd(3, Lb, pos)
+        q = np.quantile(nnd, [0.1, 0.25, 0.5, 0.75, 0.9])
+        Q = 1.5 * (nrm[:, :, None] * nrm[:, None, :]).mean(0) - 0.5 * np.eye(3)
+        return np.concatenate([q, [np.linalg.eigvalsh(Q).max()]])
+
+    dev, ref = [], []
+    for s in range(12):
+        with srm.Context(Lb, n, shape="platelet") as ctx:
+            ctx.rsa_platelets_device(n, 1.0, aspect, 900 + s)
+            pos, nrm, _, _, _ = ctx.download_platelets()
+        dev.append(summary(pos, nrm))
+        st, rpos, rnrm, _ = orc.r_rsa_platelets(n, 1.0, aspect, Lb, 100000, 900 + s)
+        assert st == 0
+        ref.append(summary(rpos, rnrm))
+    ps = stats_util.ensemble_agree(np.array(dev), np.array(ref))
+    assert min(ps) > 1e-3, f"device vs reference rsa_platelets summaries: Welch p = {ps}"
+
+
+def test_rsa_platelets_device_errors():
+    with srm.Context([5.0] * 3, 10, shape="platelet") as ctx:
+        with pytest.raises(srm.ValidationError):
+            ctx.rsa_platelets_device(10, 1.0, 1.0, 1)  # aspect ratio must exceed 1
+        with pytest.raises(srm.ValidationError):
+            ctx.rsa_platelets_device(10, 2.0, 20.0, 1)  # too large for the box
+        with pytest.raises(srm.PlacementFailure):
+            ctx.rsa_platelets_device(10, 1.2, 20.0, 1, max_rounds=1)
+    with srm.Context([5.0] * 3, 10) as sph:
+        with pytest.raises(srm.ValidationError):
+            sph.rsa_platelets_device(10, 1.0, 20.0, 1)
