@@ -416,6 +416,7 @@ def run_b200(args, cfg, world, rank, local, pg):
     ms = ctx.stopwatch_stop()
     launches = ctx.launch_count() - l0
     clk = clocks.stop()
+    pair_tests = ctx.last_round_info()["pair_tests"]  # platelets: ordered pair tests of the last round
     barrier(pg)
     ms_max = max_over_ranks(pg, ms)
     value = world * n * args.steps / (ms_max * 1e-3)
@@ -512,6 +513,11 @@ def run_b200(args, cfg, world, rank, local, pg):
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if kind == "platelet":  # the platelet path's primary number
+            t_pl = (per_round[1] + per_round[3]) * 1e-3
+            line["pair_tests"] = {"per_round": pair_tests, "per_s": pair_tests / t_pl if t_pl > 0 else None,
+                                  "what": "ordered spherodisk_overlap tests (sweep trials + overlap reduction) per "
+                                          "round / (sweep + reduction device time)"}
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

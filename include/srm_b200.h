@@ -294,7 +294,9 @@ int srm_b200_stopwatch(srm_b200_ctx* ctx, int op, double* ms);
 /* Diagnostics of the last round whose statistics were read: info[0] non-movers,
  * [1] colour classes of the sweep, [2] largest cells per class, [3] near-search half
  * width (x), [4] colouring modulus (x), [5] cells of the grid, [6] / [7] wavefront sweep
- * dependency rows found unfinished / polls spent on them (0 without the wavefront sweep). */
+ * dependency rows found unfinished / polls spent on them (0 without the wavefront sweep),
+ * [8] platelets: ordered pair tests (spherodisk_overlap) of the round's sweep and reduction.
+ * info must hold 9 entries. */
 int srm_b200_last_round_info(srm_b200_ctx* ctx, int64_t* info);
 
 /* ---- self tests of the device primitives (no reference counterpart) ------------------ */

@@ -390,10 +390,11 @@ class Context:
         self._c(_native.lib().srm_b200_sync(self._h))
 
     def last_round_info(self) -> dict:
-        v = (C.c_int64 * 8)()
+        v = (C.c_int64 * 9)()
         self._c(_native.lib().srm_b200_last_round_info(self._h, v))
         return {"nonmovers": v[0], "colour_classes": v[1], "cells_per_class": v[2], "near_half_width": v[3],
-                "colour_modulus": v[4], "cells": v[5], "wave_waits": v[6], "wave_polls": v[7]}
+                "colour_modulus": v[4], "cells": v[5], "wave_waits": v[6], "wave_polls": v[7],
+                "pair_tests": v[8]}
 
     def save_snapshot(self, path: str, volume_fraction: float = 0.0, iteration_count: int = 0, seed: int = 0,
                       params: Optional[SrmParams] = None, binary: bool = True) -> None:

@@ -117,7 +117,7 @@ struct srm_b200_ctx {
     uint8_t* acc = nullptr;
 
     uint32_t* count = nullptr;
-    int64_t* cell_start = nullptr;
+    cell_t* cell_start = nullptr;
     uint64_t* partial = nullptr;
     int64_t cell_cap = 0;
     int64_t tile_cap = 0;
@@ -154,7 +154,7 @@ struct srm_b200_ctx {
 
     cudaEvent_t sw_start = nullptr, sw_stop = nullptr;  // srm_b200_stopwatch
     int64_t last_nonmovers = 0;
-    int64_t last_wave_waits = 0, last_wave_polls = 0;
+    int64_t last_wave_waits = 0, last_wave_polls = 0, last_pair_tests = 0;
 
     // ---------------------------------------------------------------------------
     cudaEvent_t take_event() {
@@ -358,7 +358,7 @@ struct srm_b200_ctx {
         count = nullptr; cell_start = nullptr; partial = nullptr; wave_order = nullptr; wave_done = nullptr;
         const int64_t c = ncells + ncells / 8 + 1024;
         count = dalloc<uint32_t>(c);
-        cell_start = dalloc<int64_t>(c + 1);
+        cell_start = dalloc<cell_t>(c + 1);
         tile_cap = (c + kLbTile - 1) / kLbTile;
         partial = dalloc<uint64_t>(tile_cap + 1);  // look-back status words + the tile counter
         SRM_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t) * c, stream));
@@ -830,6 +830,7 @@ struct srm_b200_ctx {
         last_nonmovers = static_cast<int64_t>(h_stats->active_count);
         last_wave_waits = static_cast<int64_t>(h_stats->wave_waits);
         last_wave_polls = static_cast<int64_t>(h_stats->wave_polls);
+        last_pair_tests = static_cast<int64_t>(h_stats->pair_tests);
         return o;
     }
 
@@ -1181,11 +1182,15 @@ int srm_b200_grid_build(srm_b200_ctx* c, double cell_size, uint32_t* keys_out, i
                 SRM_CUDA(cudaMemcpyAsync(order_out, c->S.slot, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
             c->swap_state(c->S, c->P);  // keep the state physically sorted
         } else {
-            SRM_CUDA(cudaMemsetAsync(c->cell_start, 0, sizeof(int64_t) * (g.ncells + 1), c->stream));
+            SRM_CUDA(cudaMemsetAsync(c->cell_start, 0, sizeof(cell_t) * (g.ncells + 1), c->stream));
         }
-        if (cell_start_out)
-            SRM_CUDA(cudaMemcpyAsync(cell_start_out, c->cell_start, sizeof(int64_t) * (g.ncells + 1),
-                                     cudaMemcpyDeviceToHost, c->stream));
+        if (cell_start_out) {  // the device keeps 32-bit offsets; the ABI reports int64
+            std::vector<cell_t> h(static_cast<size_t>(g.ncells) + 1);
+            SRM_CUDA(cudaMemcpyAsync(h.data(), c->cell_start, sizeof(cell_t) * h.size(), cudaMemcpyDeviceToHost,
+                                     c->stream));
+            c->sync();
+            for (size_t k = 0; k < h.size(); ++k) cell_start_out[k] = h[k];
+        }
         c->sync();
         return SRM_B200_OK;
     });
@@ -1714,6 +1719,7 @@ int srm_b200_last_round_info(srm_b200_ctx* c, int64_t* info) {
         info[5] = c->hg.ncells;
         info[6] = c->last_wave_waits;
         info[7] = c->last_wave_polls;
+        info[8] = c->last_pair_tests;
         return SRM_B200_OK;
     });
 }

@@ -15,7 +15,7 @@ namespace srmb {
 // Cells at Chebyshev distance exactly r from cell c, as contiguous sorted ranges (x runs
 // per (y, z) row).  Requires 2 r + 1 <= dims on every axis (no cell visited twice).
 template <int D, typename F>
-__device__ __forceinline__ void for_ring_ranges(const GridParams& g, const int64_t* __restrict__ cs, const int* c, int r,
+__device__ __forceinline__ void for_ring_ranges(const GridParams& g, const cell_t* __restrict__ cs, const int* c, int r,
                                                 F&& f) {
     const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
     const int rz = D == 3 ? r : 0;
@@ -55,7 +55,7 @@ __device__ __forceinline__ void for_ring_ranges(const GridParams& g, const int64
 // for the next ring falls back to all particles.
 template <int D>
 __global__ void __launch_bounds__(256) k_nnd(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
-                                             const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                             const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                              double* __restrict__ out) {
     const GridParams& g = *gp;
     double emin = g.edge[0];
@@ -118,7 +118,7 @@ __global__ void k_histogram(int64_t n, const double* __restrict__ v, int bins, d
 // by the lower sorted index; stencil half width s = the cells within e[bins].
 template <int D>
 __global__ void __launch_bounds__(256) k_pair_counts(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
-                                                     const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                     const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                      const double* __restrict__ edges, int bins, const int32_t* s,
                                                      unsigned long long* __restrict__ counts) {
     extern __shared__ unsigned long long hcount[];

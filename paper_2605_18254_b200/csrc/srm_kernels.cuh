@@ -20,6 +20,9 @@
 
 namespace srmb {
 
+// cell offsets into the sorted state: 32-bit (a context holds at most 2^31 - 1 particles)
+using cell_t = int32_t;
+
 
 // Division by a grid constant d >= 1 as a multiply-high (Granlund & Montgomery 1994,
 // 33-bit multiplier): q = (umulhi(n, m) + n) >> l, exact for every 32-bit n.
@@ -250,6 +253,7 @@ struct StatsDev {
     unsigned long long pool_top;      // near-list overflow pool: entries taken this round
     unsigned long long wave_waits;    // k_sweep_wave: dependency rows found unfinished (diagnostic)
     unsigned long long wave_polls;    // k_sweep_wave: polls of unfinished dependency rows (diagnostic)
+    unsigned long long pair_tests;    // platelets: ordered pair tests (spherodisk_overlap) of the sweep + reduction
 };
 
 // Overflow pool of the near lists: a row whose list does not fit (n > kNearCap) keeps
@@ -306,7 +310,7 @@ constexpr unsigned long long kLbAgg = 1ull << 62, kLbPrefix = 2ull << 62, kLbMas
 __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const uint32_t* __restrict__ count,
                                                               const GridParams* __restrict__ gp,
                                                               unsigned long long* __restrict__ status,
-                                                              int64_t* __restrict__ cell_start) {
+                                                              cell_t* __restrict__ cell_start) {
     __shared__ unsigned tile_s;
     __shared__ unsigned long long warp_tot[kLbThreads / 32];
     __shared__ unsigned long long excl_s;
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const uint32_t* __
         }
         if (lane == 0) {
             excl_s = excl;
-            if (tile == ntiles - 1) cell_start[ncells] = static_cast<int64_t>(excl + total);
+            if (tile == ntiles - 1) cell_start[ncells] = static_cast<cell_t>(excl + total);
         }
     }
     __syncthreads();
@@ -388,17 +392,17 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const uint32_t* __
     if (base + kLbPer <= ncells) {
 #pragma unroll
         for (int k = 0; k < kLbPer; k += 2) {
-            longlong2 o;
-            o.x = static_cast<long long>(run);
+            int2 o;
+            o.x = static_cast<int>(run);
             run += v[k];
-            o.y = static_cast<long long>(run);
+            o.y = static_cast<int>(run);
             run += v[k + 1];
-            *reinterpret_cast<longlong2*>(cell_start + base + k) = o;
+            *reinterpret_cast<int2*>(cell_start + base + k) = o;
         }
     } else {
 #pragma unroll
         for (int k = 0; k < kLbPer; ++k) {
-            if (base + k < ncells) cell_start[base + k] = static_cast<int64_t>(run);
+            if (base + k < ncells) cell_start[base + k] = static_cast<cell_t>(run);
             run += v[k];
         }
     }
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(kLbThreads) k_scan_lookback(const uint32_t* __
 // atomic scatter into cell ranges (count[] returns to zero for the next histogram); the
 // entry carries the sort key of the within-cell order with it: slot << 32 | source index
 __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const int32_t* __restrict__ slot,
-                          const int64_t* __restrict__ cell_start, uint32_t* __restrict__ count,
+                          const cell_t* __restrict__ cell_start, uint32_t* __restrict__ count,
                           unsigned long long* __restrict__ perm) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -421,7 +425,7 @@ __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const int
 // deterministic within-cell order: ascending slot (== engine.hpp:151-163 stability when
 // slot is the storage index); the entries hold their slots, so the insertion sort makes
 // no dependent loads
-__global__ void k_cellsort(const GridParams* __restrict__ gp, const int64_t* __restrict__ cell_start,
+__global__ void k_cellsort(const GridParams* __restrict__ gp, const cell_t* __restrict__ cell_start,
                            unsigned long long* __restrict__ perm) {
     const int64_t ncells = gp->ncells;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncells;
@@ -487,7 +491,7 @@ __global__ void k_gather(int64_t n, const unsigned long long* __restrict__ perm,
 // Stencil walk over the sorted cell ranges around cell `k`: half width g.near_s[a]
 // (or the whole axis), x-runs merged into contiguous particle ranges.
 template <int D, typename F>
-__device__ __forceinline__ void for_near_ranges(const GridParams& g, const int64_t* __restrict__ cs,
+__device__ __forceinline__ void for_near_ranges(const GridParams& g, const cell_t* __restrict__ cs,
                                                 uint32_t k, const int32_t* s, F&& f) {
     const int dx = g.dims[0], dy = g.dims[1], dz = D == 3 ? g.dims[2] : 1;
     int cc_[3];
@@ -574,7 +578,7 @@ struct NearList {
 // error, so the set is a superset of the exact fp64 near set; the stencil rows and the
 // x cells of each row are pruned by the chord of the (inflated) cutoff sphere.
 template <int D, typename F>
-__device__ __forceinline__ void near_candidates(const GridParams& g, const int64_t* __restrict__ cs,
+__device__ __forceinline__ void near_candidates(const GridParams& g, const cell_t* __restrict__ cs,
                                                 const float4* __restrict__ xf, int64_t q, uint32_t key, F&& visit,
                                                 int j0 = 0, int js = 1) {
     const float4 me = xf[q];
@@ -664,7 +668,7 @@ __device__ __forceinline__ int class_of_key(const GridParams& g, uint32_t key) {
 // A list longer than the row goes to the overflow pool (a second scan writes it there).
 template <int D>
 __device__ __forceinline__ void near_full_particle(int64_t q, const State& S, const GridParams& g,
-                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                   const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                    int32_t* __restrict__ nbr, NearPool pool, StatsDev* stats) {
     NearList nl;
     const int32_t idq = S.id[q];
@@ -691,7 +695,7 @@ __device__ __forceinline__ void near_full_particle(int64_t q, const State& S, co
 
 template <int D>
 __global__ void __launch_bounds__(256) k_near_lists(int64_t n, State S, const GridParams* __restrict__ gp,
-                                                    const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                    const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                     int32_t* __restrict__ nbr, NearPool pool, StatsDev* stats) {
     const GridParams& g = *gp;
     if (g.near_kind != 2) return;
@@ -712,9 +716,19 @@ struct RowMap {
 #ifndef SRM_TILE_CAP
 #define SRM_TILE_CAP 2048
 #endif
-#ifndef SRM_NEAR_PRUNE
-#define SRM_NEAR_PRUNE 0
+// near-list screen variants (tuning): 0 = a store per candidate, 1 = a hit
+// bitmask per 16 slot pairs; rows of the 3x3 stencil unrolled SRM_NEAR_ROWUNROLL times;
+// SRM_NEAR_MONO: a constant cutoff in bricks whose radii are all equal
+#ifndef SRM_NEAR_SCREEN
+#define SRM_NEAR_SCREEN 0
 #endif
+#ifndef SRM_NEAR_ROWUNROLL
+#define SRM_NEAR_ROWUNROLL 9
+#endif
+#ifndef SRM_NEAR_MONO
+#define SRM_NEAR_MONO 0
+#endif
+constexpr int kNearRowUnroll = SRM_NEAR_ROWUNROLL;
 namespace tiles {  // sparse grids (~1-2 particles per cell): 16 x 8 x 4 bricks
 #define NT_X SRM_TILE_X
 #define NT_Y SRM_TILE_Y
@@ -779,7 +793,7 @@ __device__ __forceinline__ double4 ld_rec(const double4* p) {
 
 template <int D, bool kLive = false>
 __device__ __forceinline__ bool trial_clear_rescan(int64_t q, const double* p, double ri, const State& S, const Box& box,
-                                                const GridParams& g, const int64_t* __restrict__ cs,
+                                                const GridParams& g, const cell_t* __restrict__ cs,
                                                 const uint32_t* __restrict__ skey) {
     const int32_t idq = S.id[q];
     bool ok = true;
@@ -800,7 +814,7 @@ __device__ __forceinline__ bool trial_clear_rescan(int64_t q, const double* p, d
 template <int D, bool kLive = false>
 __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const double* xi, double ri,
                                            const State& S, const Box& box, const GridParams& g,
-                                           const RoundParams& rp, const int64_t* __restrict__ cs,
+                                           const RoundParams& rp, const cell_t* __restrict__ cs,
                                            const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
                                            const int32_t* __restrict__ pool, double* p) {
     // the row and the first three neighbours' live records are loaded before the
@@ -879,7 +893,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_warpq(i
                                                                                State S, Box box,
                                                                                const GridParams* __restrict__ gp,
                                                                                const RoundParams* __restrict__ rpp,
-                                                                               const int64_t* __restrict__ cs,
+                                                                               const cell_t* __restrict__ cs,
                                                                                const uint32_t* __restrict__ skey,
                                                                                const int32_t* __restrict__ nbr,
                                                                                const int32_t* __restrict__ pool,
@@ -1086,7 +1100,7 @@ template <int D>
 __global__ void __launch_bounds__(kSweepThreads, SRM_SWEEP_MINB) k_sweep_wave(State S, Box box,
                                                                               const GridParams* __restrict__ gp,
                                                                               const RoundParams* __restrict__ rpp,
-                                                                              const int64_t* __restrict__ cs,
+                                                                              const cell_t* __restrict__ cs,
                                                                               const uint32_t* __restrict__ skey,
                                                                               const int32_t* __restrict__ nbr,
                                                                               const int32_t* __restrict__ pool,
@@ -1283,7 +1297,7 @@ static_assert(kSphTeam >= 2 && kSphTeam <= 32 && (kSphTeam & (kSphTeam - 1)) == 
 __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep_team(int cls_arg, const int* __restrict__ cls_dev, State S,
                                                               Box box, const GridParams* __restrict__ gp,
                                                               const RoundParams* __restrict__ rpp,
-                                                              const int64_t* __restrict__ cs,
+                                                              const cell_t* __restrict__ cs,
                                                               const uint32_t* __restrict__ skey,
                                                               const int32_t* __restrict__ nbr,
                                                               const int32_t* __restrict__ pool,
@@ -1375,7 +1389,7 @@ template <int D>
 __global__ void __launch_bounds__(kSweepThreads, 8) k_sweep_trials(int cls_arg, const int* __restrict__ cls_dev, State S,
                                                                    Box box, const GridParams* __restrict__ gp,
                                                                    const RoundParams* __restrict__ rpp,
-                                                                   const int64_t* __restrict__ cs,
+                                                                   const cell_t* __restrict__ cs,
                                                                    const uint32_t* __restrict__ skey,
                                                                    const int32_t* __restrict__ nbr,
                                                                    const int32_t* __restrict__ pool,
@@ -1448,7 +1462,7 @@ constexpr int kPlTeam = SRM_PL_TEAM;
 __global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(int cls_arg, const int* __restrict__ cls_dev, State S,
                                                                  Box box, const GridParams* __restrict__ gp,
                                                                  const RoundParams* __restrict__ rpp,
-                                                                 const int64_t* __restrict__ cs,
+                                                                 const cell_t* __restrict__ cs,
                                                                  const uint32_t* __restrict__ skey,
                                                                  const int32_t* __restrict__ nbr,
                                                                  const int32_t* __restrict__ pool,
@@ -1458,6 +1472,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(in
     const GridParams& g = *gp;
     if (cls >= g.ncls) return;
     const RoundParams rp = *rpp;
+    unsigned long long tests = 0;  // pair tests of this lane (StatsDev::pair_tests)
     const int lane = threadIdx.x & 31, tl = lane & (kPlTeam - 1);
     const unsigned tm = ((1u << kPlTeam) - 1u) << (lane & ~(kPlTeam - 1));
     int first[3], stride[3], cnt[3];
@@ -1519,6 +1534,7 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(in
                             double4 v, a;
                             cand(e[k], d, nb, v, a);
                             st = pl::spherodisk_overlap_pre(d, pn, me.w, ni.w, nb, v.w, a.w);
+                            ++tests;
                             r2 = 0.5 * (v.w - a.w);
                             th = 0.5 * (ni.w + a.w);
                         }
@@ -1543,7 +1559,10 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(in
                     near_candidates<3>(
                         g, cs, S.xf, q, skey[q],
                         [&](int64_t j) {
-                            if (!hit && S.id[j] != idq) hit = test(j);
+                            if (!hit && S.id[j] != idq) {
+                                hit = test(j);
+                                ++tests;
+                            }
                         },
                         tl, kPlTeam);
                 }
@@ -1565,6 +1584,9 @@ __global__ void __launch_bounds__(kSweepThreads, SRM_PL_MINB) k_sweep_pl_team(in
             __syncwarp(tm);  // the move is visible to the team before the cell's next particle
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tests += __shfl_down_sync(0xffffffffu, tests, o);
+    if (lane == 0 && tests) atomicAdd(&stats->pair_tests, tests);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1786,7 +1808,7 @@ __global__ void k_scale_radius_ctl(int64_t n, double4* __restrict__ rec, double4
 // are exactly the particles on the non-mover list.
 template <int D>
 __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const GridParams* __restrict__ gp,
-                                                     const int64_t* __restrict__ cs,
+                                                     const cell_t* __restrict__ cs,
                                                      const uint32_t* __restrict__ skey,
                                                      const uint8_t* __restrict__ acc,
                                                      const int32_t* __restrict__ active, StatsDev* stats) {
@@ -1873,7 +1895,7 @@ __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const Gri
 // cell offsets only (parity statistic, not on the timed path).
 template <int D>
 __global__ void __launch_bounds__(256) k_candidates(int64_t n, const GridParams* __restrict__ gp,
-                                                    const int64_t* __restrict__ cs,
+                                                    const cell_t* __restrict__ cs,
                                                     const uint32_t* __restrict__ skey, StatsDev* stats) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     unsigned long long cand = 0;
@@ -1893,7 +1915,7 @@ __global__ void __launch_bounds__(256) k_candidates(int64_t n, const GridParams*
 template <int D>
 __global__ void __launch_bounds__(256) k_overlap_full(int64_t n, State S, Box box,
                                                       const GridParams* __restrict__ gp,
-                                                      const int64_t* __restrict__ cs,
+                                                      const cell_t* __restrict__ cs,
                                                       const uint32_t* __restrict__ skey,
                                                       int with_candidates, StatsDev* stats) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1953,12 +1975,12 @@ __global__ void __launch_bounds__(256) k_overlap_full(int64_t n, State S, Box bo
 constexpr int kOverlapPlThreads = 128;
 __global__ void __launch_bounds__(kOverlapPlThreads, 3) k_overlap_pl(int64_t n, State S, Box box,
                                                                   const GridParams* __restrict__ gp,
-                                                                  const int64_t* __restrict__ cs,
+                                                                  const cell_t* __restrict__ cs,
                                                                   const uint32_t* __restrict__ skey, StatsDev* stats) {
     const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= n) return;  // whole warps
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, tests = 0;
     const GridParams& g = *gp;
     const double4 vi = S.rec[i], ai = S.aux[i];
     const int32_t idi = S.id[i];
@@ -1983,7 +2005,11 @@ __global__ void __launch_bounds__(kOverlapPlThreads, 3) k_overlap_pl(int64_t n, 
                 Dj = vj.w;
                 tj = aj.w;
                 sa = pl::spherodisk_overlap_pre(dij, ni, vi.w, ai.w, nj, Dj, tj);
-                if (sa != pl::kDwTrue) sb = pl::spherodisk_overlap_pre(dji, nj, Dj, tj, ni, vi.w, ai.w);
+                ++tests;
+                if (sa != pl::kDwTrue) {
+                    sb = pl::spherodisk_overlap_pre(dji, nj, Dj, tj, ni, vi.w, ai.w);
+                    ++tests;
+                }
             }
             const bool hit = sa == pl::kDwTrue || sb == pl::kDwTrue;
             pairs += hit ? 1 : 0;
@@ -2015,8 +2041,12 @@ __global__ void __launch_bounds__(kOverlapPlThreads, 3) k_overlap_pl(int64_t n, 
         }
     });
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+        tests += __shfl_down_sync(0xffffffffu, tests, off);
+    }
     if (lane == 0 && pairs) atomicAdd(&stats->overlap_pairs, pairs);
+    if (lane == 0 && tests) atomicAdd(&stats->pair_tests, tests);
 }
 
 // platelet records (host layout) <-> device state, scattered back to slot order

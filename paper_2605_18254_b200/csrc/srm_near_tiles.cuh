@@ -28,7 +28,7 @@ static_assert(kHRows <= kTileThreads && kHRows <= 64, "a thread per halo row; 6-
 static_assert(kTY * kTZ <= 32 && kTX <= 16, "one warp scans the interior rows; 4-step cell search");
 
 __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, const GridParams* __restrict__ gp,
-                                                             const int64_t* __restrict__ cs,
+                                                             const cell_t* __restrict__ cs,
                                                              const uint32_t* __restrict__ skey,
                                                              int32_t* __restrict__ nbr, NearPool pool,
                                                              StatsDev* stats) {
@@ -214,65 +214,95 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         const float2 base2 = make_float2(base, base), fac2 = make_float2(1.00001f, 1.00001f);
         const float limm = __fadd_rn(g.rmax_f, base);  // (monodisperse bricks: r_j = rmax)
         const float l2m = __fmul_rn(__fmul_rn(limm, limm), 1.00001f);
-        // hits are rare (0.8 per particle at the bench window): the screen of a range sets a
-        // bit per hit in a register mask (16 slot pairs per mask) and the few hits are
-        // recorded after each chunk -- no store per candidate.  The list keeps the first
-        // kNearCap hits in slot order; nn counts them all.
         uint16_t* ql = lst + threadIdx.x;
         int nn = 0;
+#if SRM_NEAR_SCREEN == 0
+        // hits are rare per lane but common per warp: record the hit slots branch-free (a
+        // store to the current list slot every test, the count advances on a hit; slot
+        // kNearCap absorbs the overflow), resolve them after the scan
+        int at = 0;
+#else
+        // the screen of a range sets a bit per hit in a register mask (16 slot pairs per
+        // mask); the few hits are recorded after each chunk
         auto record = [&](int k) {
             if (nn < kNearCap) ql[nn * kTileThreads] = static_cast<uint16_t>(k);
             ++nn;
         };
-#pragma unroll
-        for (int ddz = -1; ddz <= 1; ++ddz) {
-#pragma unroll
-            for (int ddy = -1; ddy <= 1; ++ddy) {
-                const int c = hc + ddy * kHX + ddz * kHX * kHY;
-                const int kb = hoff[c - 1], ke = hoff[c + 2];
-                // slots [kb, ke) two at a time (pairs 2p, 2p + 1), 16 pairs per mask
-                for (int pb = kb >> 1; 2 * pb < ke; pb += 16) {
-                    const int pe = min((ke + 1) >> 1, pb + 16);
-                    unsigned hits = 0u, bit = 1u;
-                    if (mono) {  // the same cutoff for every candidate (bit for bit the general one)
-                        for (int p = pb; p < pe; ++p) {
-                            const float4 A = pxy[p];
-                            const float2 Bz = *reinterpret_cast<const float2*>(pzw + p);
-                            const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
-                            const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
-                            const float2 ez = __fadd2_rn(Bz, nmz);
-                            const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
-                            if (d2.x <= l2m) hits |= bit;
-                            if (d2.y <= l2m) hits |= bit << 1;
-                            bit <<= 2;
-                        }
-                    } else {
-                        for (int p = pb; p < pe; ++p) {
-                            const float4 A = pxy[p], B = pzw[p];
-                            const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
-                            const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
-                            const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
-                            const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
-                            const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
-                            const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
-                            if (d2.x <= l2.x) hits |= bit;
-                            if (d2.y <= l2.y) hits |= bit << 1;
-                            bit <<= 2;
-                        }
+#endif
+#pragma unroll kNearRowUnroll
+        for (int row9 = 0; row9 < 9; ++row9) {
+            const int ddy = row9 % 3 - 1, ddz = row9 / 3 - 1;
+            const int c = hc + ddy * kHX + ddz * kHX * kHY;
+            const int kb = hoff[c - 1], ke = hoff[c + 2];
+#if SRM_NEAR_SCREEN == 0
+            // slots [kb, ke) two at a time (pairs 2p, 2p + 1; the ends masked)
+            for (int p = kb >> 1; 2 * p < ke; ++p) {
+                const float4 A = pxy[p], B = pzw[p];
+                const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                float2 l2;
+                if (SRM_NEAR_MONO && mono) {
+                    l2 = make_float2(l2m, l2m);
+                } else {
+                    const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                    l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                }
+                const int k0 = 2 * p;
+                ql[at * kTileThreads] = static_cast<uint16_t>(k0);
+                nn += (d2.x <= l2.x && k0 >= kb && k0 != i) ? 1 : 0;
+                at = min(nn, kNearCap);
+                ql[at * kTileThreads] = static_cast<uint16_t>(k0 + 1);
+                nn += (d2.y <= l2.y && k0 + 1 < ke && k0 + 1 != i) ? 1 : 0;
+                at = min(nn, kNearCap);
+            }
+#else
+            // slots [kb, ke) two at a time (pairs 2p, 2p + 1), 16 pairs per mask
+            for (int pb = kb >> 1; 2 * pb < ke; pb += 16) {
+                const int pe = min((ke + 1) >> 1, pb + 16);
+                unsigned hits = 0u, bit = 1u;
+                if (SRM_NEAR_MONO && mono) {  // the same cutoff for every candidate (bit for bit)
+#pragma unroll 2
+                    for (int p = pb; p < pe; ++p) {
+                        const float4 A = pxy[p];
+                        const float2 Bz = *reinterpret_cast<const float2*>(pzw + p);
+                        const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                        const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                        const float2 ez = __fadd2_rn(Bz, nmz);
+                        const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                        if (d2.x <= l2m) hits |= bit;
+                        if (d2.y <= l2m) hits |= bit << 1;
+                        bit <<= 2;
                     }
-                    if (hits) {  // the slots of the hits: in [kb, ke), not i itself
-                        const int k0 = 2 * pb;
-                        if (kb > k0) hits &= ~1u;
-                        const int top = ke - k0;  // slots k0 + top ... are past the range
-                        if (top < 32) hits &= (1u << top) - 1u;
-                        if (i >= k0 && i < k0 + 32) hits &= ~(1u << (i - k0));
-                        while (hits) {
-                            record(k0 + __ffs(hits) - 1);
-                            hits &= hits - 1u;
-                        }
+                } else {
+#pragma unroll 2
+                    for (int p = pb; p < pe; ++p) {
+                        const float4 A = pxy[p], B = pzw[p];
+                        const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                        const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                        const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                        const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                        const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                        const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                        if (d2.x <= l2.x) hits |= bit;
+                        if (d2.y <= l2.y) hits |= bit << 1;
+                        bit <<= 2;
+                    }
+                }
+                if (hits) {  // the slots of the hits: in [kb, ke), not i itself
+                    const int k0 = 2 * pb;
+                    if (kb > k0) hits &= ~1u;
+                    const int top = ke - k0;  // slots k0 + top ... are past the range
+                    if (top < 32) hits &= (1u << top) - 1u;
+                    if (i >= k0 && i < k0 + 32) hits &= ~(1u << (i - k0));
+                    while (hits) {
+                        record(k0 + __ffs(hits) - 1);
+                        hits &= hits - 1u;
                     }
                 }
             }
+#endif
         }
         // resolve: sorted indices, and shape.hpp:70 self-exclusion by id
         int32_t e[kNearCap];

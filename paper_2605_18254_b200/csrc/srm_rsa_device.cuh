@@ -46,7 +46,7 @@ __global__ void k_rsa_propose(int64_t n, int dim, double4* __restrict__ rec, con
 // that overlap candidate i (nconf[i] > kRsaConf: overflow, reported to the host)
 template <int D>
 __global__ void __launch_bounds__(256) k_rsa_check(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
-                                                   const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                   const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                    const uint8_t* __restrict__ placed, int8_t* __restrict__ state,
                                                    int32_t* __restrict__ conf, int32_t* __restrict__ nconf,
                                                    int64_t* __restrict__ where) {
@@ -89,7 +89,7 @@ template <int D>
 __global__ void k_rsa_resolve(int64_t n, const uint8_t* __restrict__ placed, int8_t* __restrict__ state,
                               const int32_t* __restrict__ conf, const int32_t* __restrict__ nconf,
                               int* __restrict__ undecided, State S, Box box, const GridParams* __restrict__ gp,
-                              const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                              const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                               const int64_t* __restrict__ where) {
     int left = 0;
     const volatile int8_t* vs = state;
@@ -173,7 +173,7 @@ __device__ __forceinline__ bool rsa_pl_hits(const State& S, const Box& box, int6
 }
 
 __global__ void __launch_bounds__(256) k_rsa_pl_check(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
-                                                      const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                      const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                                       const uint8_t* __restrict__ placed, int8_t* __restrict__ state,
                                                       int32_t* __restrict__ conf, int32_t* __restrict__ nconf,
                                                       int64_t* __restrict__ where) {
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_rsa_pl_check(int64_t n, State S, Box bo
 __global__ void k_rsa_pl_resolve(int64_t n, const uint8_t* __restrict__ placed, int8_t* __restrict__ state,
                                  const int32_t* __restrict__ conf, const int32_t* __restrict__ nconf,
                                  int* __restrict__ undecided, State S, Box box, const GridParams* __restrict__ gp,
-                                 const int64_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                 const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
                                  const int64_t* __restrict__ where) {
     int left = 0;
     const volatile int8_t* vs = state;
