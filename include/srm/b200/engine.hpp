@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdint>
+#include <exception>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -215,9 +216,23 @@ inline srm_b200_params to_c(const SrmParams& p) {
     return c;
 }
 
+// The sink runs on the calling thread while the device loop runs (records arrive live).
+// An exception it throws must not cross the C ABI: it is kept, later records are not
+// delivered, and srm_generate rethrows it after the run, as the reference's call would
+// have propagated it (engine.hpp:251-254).
+struct SinkCall {
+    const ProgressSink* sink;
+    std::exception_ptr error;
+};
+
 inline void progress_trampoline(const srm_b200_progress_record* rec, void* user) {
-    const auto* sink = static_cast<const ProgressSink*>(user);
-    (*sink)(ProgressRecord{rec->iteration, rec->volume_fraction, rec->accepted != 0, rec->elapsed_seconds});
+    auto* call = static_cast<SinkCall*>(user);
+    if (call->error) return;
+    try {
+        (*call->sink)(ProgressRecord{rec->iteration, rec->volume_fraction, rec->accepted != 0, rec->elapsed_seconds});
+    } catch (...) {
+        call->error = std::current_exception();
+    }
 }
 
 }  // namespace detail
@@ -237,9 +252,10 @@ GenerateResult<S> srm_generate(const Snapshot<S>& initial, const SrmParams& para
     dev.upload(initial.particles);
     const srm_b200_params cp = detail::to_c(params);
     srm_b200_generate_out out{};
+    detail::SinkCall call{&progress, nullptr};
     const int st = srm_b200_generate(dev.get(), &cp, initial.iteration_count,
-                                     progress ? &detail::progress_trampoline : nullptr,
-                                     const_cast<ProgressSink*>(&progress), &out);
+                                     progress ? &detail::progress_trampoline : nullptr, &call, &out);
+    if (call.error) std::rethrow_exception(call.error);
     detail::check(st, dev.get());
     dev.download(snap.particles);
     snap.volume_fraction = out.volume_fraction;

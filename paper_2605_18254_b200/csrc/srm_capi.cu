@@ -889,6 +889,8 @@ int guarded(srm_b200_ctx* c, F&& f) {
         return fail(c, SRM_B200_CUDA_ERROR, "host allocation failed");
     } catch (const std::exception& e) {
         return fail(c, SRM_B200_CUDA_ERROR, e.what());
+    } catch (...) {  // (a caller's callback threw a non-standard exception: never across the ABI)
+        return fail(c, SRM_B200_CUDA_ERROR, "unknown exception");
     }
 }
 

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdio>
 #include <numbers>
+#include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "srm/b200/engine.hpp"
@@ -211,6 +213,37 @@ int main() {
         bool unit = true;
         for (const auto& q : ps) unit = unit && std::fabs(q.normal.norm() - 1.0) < 1e-12;
         CHECK(unit);
+    }
+    // a progress sink that throws: srm_generate rethrows the sink's own exception after the
+    // run (engine.hpp:251-254 propagates it); the cached context stays usable
+    {
+        auto snap = disk_start(100, 0.1, 31);
+        SrmParams p;
+        p.c_w = 0.05;
+        p.c_m = 0.01;
+        p.f_target = 0.4;
+        int seen = 0;
+        bool threw = false;
+        try {
+            srm::b200::srm_generate<DiskShape>(snap, p, [&](const ProgressRecord& r) {
+                ++seen;
+                if (r.iteration == 3) throw std::runtime_error("sink stop");
+            });
+        } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()) == "sink stop";
+        }
+        CHECK(threw);
+        CHECK(seen == 3);
+        const auto again = srm::b200::srm_generate<DiskShape>(snap, p);
+        CHECK(again.status == GenerateStatus::Converged);
+    }
+    // fine-grained drop-ins in a loop reuse one cached device context per thread
+    {
+        auto snap = disk_start(400, 0.3, 32);
+        Rng rng(5);
+        for (int k = 0; k < 50; ++k)
+            srm::b200::relax_sweeps<DiskShape>(snap.particles, snap.box, 0.002, 0.0, 4, 1, rng);
+        CHECK(violations<2>(snap.particles, snap.box, 0.0) == 0);
     }
     std::printf("shim_test: %d/%d checks passed\n", checks - failures, checks);
     return failures == 0 ? 0 : 1;
