@@ -106,7 +106,7 @@ def test_rsa_platelets_device_errors():
         with pytest.raises(srm.ValidationError):
             ctx.rsa_platelets_device(10, 1.0, 1.0, 1)  # aspect ratio must exceed 1
         with pytest.raises(srm.ValidationError):
-            ctx.rsa_platelets_device(10, 2.0, 20.0, 1)  # too large for the box
+            ctx.rsa_platelets_device(10, 2.5, 20.0, 1)  # too large for the box (bound 1.31 > 5 / 4)
         with pytest.raises(srm.PlacementFailure):
             ctx.rsa_platelets_device(10, 1.2, 20.0, 1, max_rounds=1)
     with srm.Context([5.0] * 3, 10) as sph:
