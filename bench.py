@@ -47,7 +47,7 @@ CONFIGS = {
     "cfg3": dict(desc="3D polydisperse spheres N=1e6, lognormal radii (mean 1, CV 0.2, clipped to [0.5, 2]), "
                       "clustered start (1000 Gaussian clusters, sigma 3), f_target 0.50, c_m=0.1",
                  kind="poly", dim=3, n=1_000_000, f_target=0.50, cm_abs=0.10, f0=0.05, clusters=1000, sigma=3.0,
-                 sample_n=20_000, prep_iters=150),
+                 sample_n=20_000, n_k=50),  # n_k = 10 stalls at f = 0.45 at 10^6
     "cfg4": dict(desc="3D monodisperse spheres N=1e7, unit cube, f_target 0.30, c_m=0.05 r_t",
                  kind="mono", dim=3, n=10_000_000, f_target=0.30, cm_rel=0.05, f0=0.1),
     "cfg5": dict(desc="3D thin platelets N=1e5, thickness/diameter 0.01, box 25.01, normals uniform, f_target 0.05, "
@@ -333,13 +333,16 @@ def run_reference(args, cfg, world, rank, pg):
 
 
 # ---- B200 arm ------------------------------------------------------------------------------
-def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
-    """The workload's start state (host RSA: rsa_place / rsa_clustered / rsa_platelets),
-    uploaded and grown on the device by srm_generate to 0.98 f_target.  n, box: a scaled
-    copy at the same density (tools/ only)."""
+def e2e_start(srm, cfg, seed, device, n=None, box=1.0):
+    """The configuration's start state on the device (host RSA: rsa_place / rsa_clustered /
+    rsa_platelets, or the device RSA with --device-rsa; cfg 1: uniform centres) and its
+    end-to-end protocol to the FULL f_target.  Returns (ctx, c_m, params, start) where
+    start holds f0, the preparation seconds and, for host starts, the start arrays (for the
+    reference's run from the same start).  n, box: a scaled copy (tools/ only)."""
     dim, kind = cfg["dim"], cfg["kind"]
     n = n or cfg["n"]
     t0 = time.time()
+    start = {}
     if kind == "platelet":
         Lb = [cfg["L"] * box] * 3
         D0 = (cfg["rho0"] * Lb[0] ** 3 / n) ** (1.0 / 3.0)
@@ -349,13 +352,13 @@ def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
         else:
             pos, nrm, ids = srm.rsa_platelets(n, D0, cfg["aspect"], Lb, 100000, seed)
             ctx.upload_platelets(pos, nrm, np.full(n, D0), np.full(n, D0 / cfg["aspect"]), ids)
-        t_rsa = time.time() - t0
-        c_m, n_k, n_l = cfg["cm_abs"], cfg["n_k"], cfg["n_l"]
-        params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, c_r=cfg["c_r"], n_k=n_k, n_l=n_l,
-                               f_target=F_WINDOW * cfg["f_target"], max_iterations=cfg.get("prep_iters", 100000),
+        c_m = cfg["cm_abs"]
+        params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, c_r=cfg["c_r"], n_k=cfg["n_k"], n_l=cfg["n_l"],
+                               f_target=cfg["f_target"], max_iterations=cfg.get("e2e_iters", 100000),
                                seed=seed + 1, reorder_period=16)
         ctx.set_rotation(cfg["c_r"])
     else:
+        pos = None
         if kind == "poly":
             r_t = poly_radii(n, seed)
             L = (np.sum(4.0 / 3.0 * math.pi * r_t ** 3) / cfg["f_target"]) ** (1.0 / 3.0)
@@ -374,22 +377,35 @@ def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
         else:
             Lb = [box] * dim
             r0 = np.full(n, radius_for(cfg["f0"], cfg["n"], dim))
-            pos, ids = (None, None) if DEVICE_RSA else srm.rsa_place(r0, Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
+            if not DEVICE_RSA:
+                pos, ids = srm.rsa_place(r0, Lb, srm.K_RSA_DEFAULT_ATTEMPTS, seed)
             c_m = cfg["cm_rel"] * radius_for(cfg["f_target"], cfg["n"], dim)
         ctx = srm.Context(Lb, n, device)
         if pos is None:  # --device-rsa: srm_b200_rsa_device
             ctx.rsa_device(r0, seed)
         else:
             ctx.upload(pos, r0, ids)
-        t_rsa = time.time() - t0
-        params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, n_k=N_K, n_l=N_L, f_target=F_WINDOW * cfg["f_target"],
-                               max_iterations=cfg.get("prep_iters", 100000), seed=seed + 1, reorder_period=16)
+            start.update(pos=pos, radius=r0, ids=ids)
+        params = srm.SrmParams(c_w=cfg.get("c_w", C_W), c_m=c_m, n_k=cfg.get("n_k", N_K), n_l=cfg.get("n_l", N_L),
+                               f_target=cfg["f_target"], max_iterations=cfg.get("e2e_iters", 100000), seed=seed + 1,
+                               reorder_period=16)
+    start["f0"] = ctx.volume_fraction()
+    start["prep_s"] = time.time() - t0
+    return ctx, c_m, params, start
+
+
+def gpu_state(srm, cfg, seed, device, n=None, box=1.0):
+    """The workload's start (e2e_start) grown on the device by srm_generate to the
+    steady-state window, 0.98 f_target."""
+    ctx, c_m, params, start = e2e_start(srm, cfg, seed, device, n, box)
+    params.f_target = F_WINDOW * cfg["f_target"]
+    params.max_iterations = cfg.get("prep_iters", 100000)
     t0 = time.time()
     out = ctx.generate(params)
     t_gen = time.time() - t0
-    info = {"rsa_s": round(t_rsa, 2), "generate_s": round(t_gen, 3), "generate_iterations": out.iteration_count,
+    info = {"rsa_s": round(start["prep_s"], 2), "generate_s": round(t_gen, 3), "generate_iterations": out.iteration_count,
             "generate_rounds": out.rounds, "generate_shake_rounds": out.shake_rounds,
-            "f_window": out.volume_fraction}
+            "f_window": out.volume_fraction, "protocol": {"c_w": params.c_w, "n_k": params.n_k, "n_l": params.n_l}}
     return ctx, c_m, info
 
 
