@@ -26,6 +26,8 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1
 
 def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    while rows and rows[0][0] != "ID":  # (the profiled program's own output precedes the table)
+        rows.pop(0)
     h = rows[0]
     ix = {k: i for i, k in enumerate(h)}
     per = defaultdict(dict)
