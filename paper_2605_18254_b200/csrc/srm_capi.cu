@@ -102,13 +102,38 @@ struct srm_b200_ctx {
         int on = 1, ly = 0, lz = 0;
         std::sscanf(v, "%d:%d:%d", &on, &ly, &lz);
         return (on ? 1 : 0) | (std::min(std::max(ly, 0), 255) << 8) | (std::min(std::max(lz, 0), 255) << 16);
-    }();
+    }() | resolve_bits();
+    // dependency resolution (srm_resolve.cuh) on sparse 3D sphere grids: SRM_B200_RESOLVE=1,
+    // or SRM_B200_SWEEP=resolve (also on small grids, which otherwise take the trial teams)
+    static int resolve_bits() {
+        const char* f = std::getenv("SRM_B200_SWEEP");
+        const char* w = std::getenv("SRM_B200_WAVE");
+        const char* r = std::getenv("SRM_B200_RESOLVE");
+        if (f && *f) return std::string(f) == "resolve" ? 6 : 0;
+        if (w && std::atoi(w) != 0) return 0;
+        return r && std::atoi(r) != 0 ? 2 : 0;  // opt-in: measured slower than the class launches
+    }
+    double4* rec2 = nullptr;     // resolve: the round's new records (exchanged with S.rec)
+    uint8_t* dflag = nullptr;    // resolve: the pass that decided a particle
+    int32_t* list_a = nullptr;   // resolve: pending lists (ping-pong)
+    int32_t* list_b = nullptr;
+    int32_t* seg_cnt = nullptr;  // resolve: entries per CTA segment of the pending lists (ping-pong)
+    static constexpr int resolve_ctas = 148 * SRM_RESOLVE_MINB;
     // opt-in (SRM_B200_WAVE=1 or SRM_B200_SWEEP=wave): measured no faster than the class
     // launches at cfg 4, so the class launches stay the default
     bool wave_default = [] {
         const char* v = std::getenv("SRM_B200_WAVE");
         return v && std::atoi(v) != 0;
     }();
+    // unset: the wave on grids whose classes hold at most kWaveAutoLanes cells per resident
+    // lane, where class launches run short of work and end in long tails (sweep per round at
+    // cfg 4's density: 2 10^6 spheres 0.35 ms against 0.70 ms, 4 10^6 0.40 against 0.44; cfg 2
+    // 0.41 against 0.48; at 10^7 the class launches win, 0.75 against 0.81: DESIGN.md §3.6)
+    bool wave_auto = std::getenv("SRM_B200_WAVE") == nullptr;
+    bool wave_fits(int64_t cells_per_class) const {
+        return cells_per_class <= static_cast<int64_t>(kWaveAutoLanes) * queue_ctas * kSweepThreads;
+    }
+    static constexpr int kWaveAutoLanes = 6;
     WaveCtl* wave_ctl = nullptr;
     int32_t* wave_order = nullptr;  // rows in wave order (cell_cap entries)
     unsigned* wave_done = nullptr;  // per row: the epoch of the sweep that finished it
@@ -216,14 +241,18 @@ struct srm_b200_ctx {
         const char* v = std::getenv("SRM_B200_SWEEP");
         if (!v) return 0;
         const std::string s(v);
-        return s == "lane" ? 1 : (s == "trials" ? 2 : (s == "team" ? 3 : (s == "wave" ? 4 : 0)));
+        return s == "lane" ? 1 : (s == "trials" ? 2 : (s == "team" ? 3 : (s == "wave" ? 4 : (s == "resolve" ? 5 : 0))));
     }();
     // the wavefront sweep replaces the class launches of k_sweep_warpq (sparse sphere grids)
     bool use_wave(const GridParams& g, int64_t class_cells_total) const {
         if (platelets() || !g.wave) return false;
         if (sweep_force) return sweep_force == 4;
-        return wave_default && !sphere_team(g) && !trial_team(g, class_cells_total);
+        if (sphere_team(g) || trial_team(g, class_cells_total)) return false;
+        return wave_default || (wave_auto && wave_fits(class_cells_total / std::max(1, g.ncls)));
     }
+    // dependency resolution replaces the near-list kernel + class launches (the grid says where)
+    bool use_resolve(const GridParams& g) const { return !platelets() && dim == 3 && g.resolve; }
+    static int resolve_passes(const GridParams& g) { return g.ncls > 8 ? 20 : 12; }
     bool sphere_team(const GridParams& g) const {
         if (sweep_force) return sweep_force == 3 && dim == 3;
         return SRM_SPH_TEAM_ON && g.near_kind == 3;
@@ -268,6 +297,7 @@ struct srm_b200_ctx {
             }
             SRM_CUDA(cudaMemcpyToSymbol(c_seed_table, &t, sizeof(t)));
         }
+        if (platelets() || dim != 3) wave_mode &= ~6;  // (the dependency resolution: 3D spheres)
         alloc_state(P);
         alloc_state(Q);
         alloc_state(S);
@@ -297,6 +327,17 @@ struct srm_b200_ctx {
             queue_ctas = std::max(1, per_sm) * std::max(1, sms);
         }
         S.xf = dalloc<float4>(cap);
+        if (!platelets() && dim == 3) {
+            rec2 = dalloc<double4>(cap);
+            dflag = dalloc<uint8_t>(cap);
+            // (a CTA's segment is its index range rounded up to whole chunks)
+            list_a = dalloc<int32_t>(cap + static_cast<int64_t>(resolve_ctas) * kResolveThreads);
+            list_b = dalloc<int32_t>(cap + static_cast<int64_t>(resolve_ctas) * kResolveThreads);
+            seg_cnt = dalloc<int32_t>(2 * resolve_ctas);
+            SRM_CUDA(cudaFuncSetAttribute(rtiles::k_near_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(rtiles::kTileSmem)));
+            SRM_CUDA(cudaFuncSetAttribute(rtiles::k_near_tiles, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        }
         wave_ctl = dalloc<WaveCtl>(1);
         SRM_CUDA(cudaMemsetAsync(wave_ctl, 0, sizeof(WaveCtl), stream));
         stats = dalloc<StatsDev>(1);
@@ -318,6 +359,7 @@ struct srm_b200_ctx {
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
         cudaFree(nbr); cudaFree(pool.e); cudaFree(S.xf); cudaFree(wave_ctl); cudaFree(wave_order); cudaFree(wave_done);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
+        cudaFree(rec2); cudaFree(dflag); cudaFree(list_a); cudaFree(list_b); cudaFree(seg_cnt);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
         for (auto e : ev_pool) cudaEventDestroy(e);
@@ -432,6 +474,21 @@ struct srm_b200_ctx {
         launched();
     }
 
+    // passes 1 .. of the dependency resolution (srm_resolve.cuh); the last one finishes
+    // whatever is left
+    void resolve_passes_launch(const GridParams& g) {
+        const int np = resolve_passes(g);
+        // one contiguous range of particle indices per CTA, all CTAs resident
+        const int grid = static_cast<int>(std::min<int64_t>(blocks_for(n, kResolveThreads), resolve_ctas));
+        int64_t span = (n + grid - 1) / grid;
+        span = (span + kResolveThreads - 1) / kResolveThreads * kResolveThreads;
+        for (int pass = 1; pass <= np; ++pass)
+            k_resolve_pass<3><<<grid, kResolveThreads, 0, stream>>>(pass, pass == np ? 1 : 0, n, span, S, rec2, dflag, box, gp,
+                                                                    rp, cell_start, skey, nbr, pool.e, acc, active, list_a,
+                                                                    list_b, seg_cnt, stats);
+        launched(np);
+    }
+
     // One round on T (T is rewritten in this round's sorted order); gp must be set.
     // grid rebuild, near lists, then the coloured Gauss-Seidel sweep (one launch per
     // colour class), then the overlap reduction (non-movers; all pairs for platelets).
@@ -442,7 +499,18 @@ struct srm_b200_ctx {
         grid_build(T);
         SRM_CUDA(cudaMemsetAsync(stats, 0, sizeof(StatsDev), stream));
         if (write_acc) SRM_CUDA(cudaMemsetAsync(acc, kNotAccepted, static_cast<size_t>(n), stream));
-        {
+        const bool resolve = use_resolve(hg);
+        if (resolve) {
+            {  // pass 0: near lists + first trials + the particles nothing precedes
+                FamScope fs(this, 2);
+                rtiles::k_near_tiles<<<hg.ntiles, rtiles::kTileThreads, rtiles::kTileSmem, stream>>>(
+                    S, gp, cell_start, skey, nbr, pool, stats, box, rp, rec2, dflag, acc);
+                launched(1);
+            }
+            FamScope fs(this, 1);
+            resolve_passes_launch(hg);
+            std::swap(S.rec, rec2);  // the new records are the sorted state's
+        } else {
             FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
             if (hg.near_kind == 0) {  // shared-memory bricks
@@ -459,7 +527,8 @@ struct srm_b200_ctx {
                 launched(1);
             }
         }
-        if (use_wave(hg, cls_cells_h[hg.ncls] - cls_cells_h[0])) {  // one persistent launch
+        if (resolve) {
+        } else if (use_wave(hg, cls_cells_h[hg.ncls] - cls_cells_h[0])) {  // one persistent launch
             FamScope fs(this, 1);
             k_wave_order<<<1, kWaveOrderThreads, 0, stream>>>(gp, wave_ctl, wave_order);
             if (dim == 2)
@@ -576,8 +645,8 @@ struct srm_b200_ctx {
     // the instantiated generate graph, reused while everything baked into it is unchanged
     struct GraphKey {
         int64_t n, nc_max;
-        int ntiles_max, ctiles_max, team0, trials0, queue_ctas, dim, plate, wave0;
-        const void* bufs[14];
+        int ntiles_max, ctiles_max, team0, trials0, queue_ctas, dim, plate, wave0, resolve0, resolve_np;
+        const void* bufs[18];
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
     };
     GraphKey gkey{};
@@ -684,7 +753,11 @@ struct srm_b200_ctx {
         const bool trials0 = !platelets() && trial_team(g0, g0.ncells);
         // the wavefront sweep where a round's grid allows it (the kernels test the grid);
         // the class loop below runs otherwise
-        const bool wave0 = !platelets() && !team0 && !trials0 && (sweep_force == 4 || (sweep_force == 0 && wave_default));
+        const bool wave0 = !platelets() && !team0 && !trials0 &&
+                           (sweep_force == 4 || (sweep_force == 0 && (wave_default || (wave_auto && wave_fits(g0.ncells / std::max(1, g0.ncls))))));
+        // dependency resolution: captured whenever this context allows it; the grid of each
+        // round (GridParams::resolve, set on the device) says whether it runs
+        const bool resolve0 = !platelets() && dim == 3 && (wave_mode & 2) != 0;
         SRM_CUDA(cudaMemcpyAsync(d_ctl, &hc, sizeof(GenCtl), cudaMemcpyHostToDevice, stream));
         SRM_CUDA(cudaStreamSynchronize(stream));  // hc is a stack object
 
@@ -699,8 +772,11 @@ struct srm_b200_ctx {
         key.dim = dim;
         key.plate = platelets();
         key.wave0 = wave0;
-        const void* bufs[14] = {P.rec, Q.rec, S.rec, P.aux, Q.aux, S.aux, count, cell_start, perm64, nbr, pool.e, S.xf,
-                                wave_order, wave_done};
+        key.resolve0 = resolve0;
+        key.resolve_np = resolve_passes(g0);
+        const void* bufs[18] = {P.rec, Q.rec, S.rec, P.aux, Q.aux, S.aux, count, cell_start, perm64, nbr, pool.e, S.xf,
+                                wave_order, wave_done, rec2, dflag, list_a, list_b};
+        (void)seg_cnt;  // (allocated with list_a: the same lifetime)
         std::memcpy(key.bufs, bufs, sizeof bufs);
         if (gexec && key == gkey) {
             launch_and_drain(hc, progress, user);
@@ -740,6 +816,11 @@ struct srm_b200_ctx {
                         S, gp, cell_start, skey, nbr, pool, stats);
                     if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
                     else k_near_lists<3><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);
+                    if (resolve0) {  // (each kernel tests the round's grid: GridParams::resolve)
+                        rtiles::k_near_tiles<<<ntiles_max, rtiles::kTileThreads, rtiles::kTileSmem, stream>>>(
+                            S, gp, cell_start, skey, nbr, pool, stats, box, rp, rec2, dflag, acc);
+                        resolve_passes_launch(g0);
+                    }
                     if (wave0) {
                         k_wave_order<<<1, kWaveOrderThreads, 0, stream>>>(gp, wave_ctl, wave_order);
                         if (dim == 2)
@@ -778,8 +859,13 @@ struct srm_b200_ctx {
                     if (dim == 2) k_stats_sweep<2><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
                     else if (platelets())
                         k_overlap_pl<<<blocks_for(n * 32, kOverlapPlThreads), kOverlapPlThreads, 0, stream>>>(n, S, box, gp, cell_start, skey, stats);
-                    else k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats);
-                    copy_state(S, Q);
+                    else k_stats_sweep<3><<<lb, 256, 0, stream>>>(S, box, gp, cell_start, skey, acc, active, stats, rec2);
+                    if (resolve0) {  // the round's records are in rec2 when the resolution swept it
+                        k_copy_state<3><<<nb, 256, 0, stream>>>(n, S, Q, gp, rec2);
+                        launched();
+                    } else {
+                        copy_state(S, Q);
+                    }
                     k_gen_after<<<1, 1, 0, stream>>>(ctl, stats, h_commit, h_f, h_reorder);
                     capture_into(add_conditional(stream, h_commit, cudaGraphCondTypeIf), cap_streams[3],
                                  [&]() { copy_state(Q, P); });

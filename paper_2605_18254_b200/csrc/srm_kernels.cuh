@@ -68,6 +68,9 @@ struct GridParams {
     // wavefront sweep (k_sweep_wave): 1 = the whole sweep is one launch of
     // row tasks in wave order; lag_y / lag_z = wave-time offsets per y / z colour step
     int32_t wave, wave_lag_y, wave_lag_z, wave_pmax;
+    // dependency resolution (srm_resolve.cuh) instead of class launches:
+    // sparse 3D sphere grids on the shared-memory bricks
+    int32_t resolve;
 };
 
 // cell coordinates of a flat key (x fastest, cell_grid.hpp:73-79)
@@ -108,6 +111,14 @@ constexpr double kCrowded = 1.8;  // mean particles per cell above which the cro
 #ifndef SRM_WAVE_LZ
 #define SRM_WAVE_LZ 64  // extra wave-time lag per z colour step (beyond the minimum)
 #endif
+#ifndef SRM_SWEEP_THREADS
+#define SRM_SWEEP_THREADS 64
+#endif
+#ifndef SRM_TRIAL_TEAM
+#define SRM_TRIAL_TEAM 16
+#endif
+// a class with at most this many cells runs as one wave of 16-lane teams (k_sweep_trials)
+constexpr int64_t kSmallClassCells = 148LL * 8 * SRM_SWEEP_THREADS / SRM_TRIAL_TEAM;
 constexpr int kWaveMaxP = 8192;  // wave times per sweep (k_wave_order's histogram)
 constexpr int kWaveMaxDeps = 32; // dependency rows polled by one warp (a lane each)
 constexpr int kWaveMaxRow = 2048; // cells per row (the row's done-bitmap in shared memory)
@@ -205,6 +216,10 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
         g.wave_pmax = g.dims[2] - 1 + g.wave_lag_z * (g.col_n[2] - 1) + g.wave_lag_y * (g.col_n[1] - 1);
         g.wave = (wave_mode & 1) && finite && !crowded && g.wave_pmax < kWaveMaxP ? 1 : 0;
     }
+    // (wave_mode bit 1: allowed; bit 2: also on small grids, which otherwise take the trial teams)
+    g.resolve = (wave_mode & 2) && g.near_kind == 0 && g.ncls <= 255 &&
+                        ((wave_mode & 4) || g.ncells / g.ncls > kSmallClassCells)
+                    ? 1 : 0;
     g.ntiles = tiles ? ((g.dims[0] + kTX - 1) / kTX) * ((g.dims[1] + kTY - 1) / kTY) * ((g.dims[2] + kTZ - 1) / kTZ)
                      : (ctiles ? ((g.dims[0] + kCTX - 1) / kCTX) * ((g.dims[1] + kCTY - 1) / kCTY) *
                                      ((g.dims[2] + kCTZ - 1) / kCTZ)
@@ -254,6 +269,7 @@ struct StatsDev {
     unsigned long long wave_waits;    // k_sweep_wave: dependency rows found unfinished (diagnostic)
     unsigned long long wave_polls;    // k_sweep_wave: polls of unfinished dependency rows (diagnostic)
     unsigned long long pair_tests;    // platelets: ordered pair tests (spherodisk_overlap) of the sweep + reduction
+    unsigned long long pend[48];      // dependency resolution: pend[p] = particles still pending after pass p
 };
 
 // Overflow pool of the near lists: a row whose list does not fit (n > kNearCap) keeps
@@ -720,7 +736,10 @@ struct RowMap {
 // bitmask per 16 slot pairs; rows of the 3x3 stencil unrolled SRM_NEAR_ROWUNROLL times;
 // SRM_NEAR_MONO: a constant cutoff in bricks whose radii are all equal
 #ifndef SRM_NEAR_SCREEN
-#define SRM_NEAR_SCREEN 0
+#define SRM_NEAR_SCREEN 0  // the sparse bricks (2: a record per pair of slots -- fewer instructions, measured slower)
+#endif
+#ifndef SRM_CNEAR_SCREEN
+#define SRM_CNEAR_SCREEN 0  // the crowded bricks (most lists overflow: they need the hit count)
 #endif
 #ifndef SRM_NEAR_ROWUNROLL
 #define SRM_NEAR_ROWUNROLL 9
@@ -729,6 +748,13 @@ struct RowMap {
 #define SRM_NEAR_MONO 0
 #endif
 constexpr int kNearRowUnroll = SRM_NEAR_ROWUNROLL;
+#ifndef SRM_RTILE_MINB
+#define SRM_RTILE_MINB 3  // CTAs per SM of the fused brick kernel (85 registers)
+#endif
+#include "srm_resolve.cuh"
+static_assert(kResolveMaxPasses + 2 <= 48, "StatsDev::pend");
+#define NT_FUSED 0
+#define NT_SCREEN SRM_NEAR_SCREEN
 namespace tiles {  // sparse grids (~1-2 particles per cell): 16 x 8 x 4 bricks
 #define NT_X SRM_TILE_X
 #define NT_Y SRM_TILE_Y
@@ -746,6 +772,8 @@ namespace tiles {  // sparse grids (~1-2 particles per cell): 16 x 8 x 4 bricks
 #undef NT_MINB
 #undef NT_KIND
 }  // namespace tiles
+#undef NT_SCREEN
+#define NT_SCREEN SRM_CNEAR_SCREEN
 namespace ctiles {  // crowded grids: 4 x 4 x 4 bricks, 4096 staged particles
 #define NT_X kCTX
 #define NT_Y kCTY
@@ -763,6 +791,29 @@ namespace ctiles {  // crowded grids: 4 x 4 x 4 bricks, 4096 staged particles
 #undef NT_MINB
 #undef NT_KIND
 }  // namespace ctiles
+#undef NT_FUSED
+#undef NT_SCREEN
+#define NT_FUSED 1
+#define NT_SCREEN 0  // (hits recorded by the store-per-candidate screen: they carry the stencil row)
+namespace rtiles {  // the sparse bricks fused with pass 0 of the dependency resolution
+#define NT_X SRM_TILE_X
+#define NT_Y SRM_TILE_Y
+#define NT_Z SRM_TILE_Z
+#define NT_CAP SRM_TILE_CAP
+#define NT_THREADS SRM_TILE_THREADS
+#define NT_MINB SRM_RTILE_MINB
+#define NT_KIND 0
+#include "srm_near_tiles.cuh"
+#undef NT_X
+#undef NT_Y
+#undef NT_Z
+#undef NT_CAP
+#undef NT_THREADS
+#undef NT_MINB
+#undef NT_KIND
+}  // namespace rtiles
+#undef NT_FUSED
+#undef NT_SCREEN
 
 #ifndef SRM_SWEEP_THREADS
 #define SRM_SWEEP_THREADS 64
@@ -1707,7 +1758,7 @@ __global__ void k_gen_t0(GenCtl* c) {
 __global__ void k_gen_cls_begin(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls,
                                 int wave_on) {
     c->cls = 0;
-    cudaGraphSetConditional(h_cls, gp->ncls > 0 && !(wave_on && gp->wave) ? 1u : 0u);
+    cudaGraphSetConditional(h_cls, gp->ncls > 0 && !(wave_on && gp->wave) && !gp->resolve ? 1u : 0u);
 }
 
 __global__ void k_gen_cls_next(GenCtl* c, const GridParams* __restrict__ gp, cudaGraphConditionalHandle h_cls) {
@@ -1811,9 +1862,12 @@ __global__ void __launch_bounds__(256) k_stats_sweep(State S, Box box, const Gri
                                                      const cell_t* __restrict__ cs,
                                                      const uint32_t* __restrict__ skey,
                                                      const uint8_t* __restrict__ acc,
-                                                     const int32_t* __restrict__ active, StatsDev* stats) {
+                                                     const int32_t* __restrict__ active, StatsDev* stats,
+                                                     const double4* rec_alt = nullptr) {
     const int64_t m = static_cast<int64_t>(stats->active_count);
     const GridParams& g = *gp;
+    // (graph runs: a round swept by the dependency resolution left its records in rec_alt)
+    if (rec_alt && g.resolve) S.rec = const_cast<double4*>(rec_alt);
     unsigned long long pairs = 0;
     double pen = 0.0;
     // the pair test of non-mover i against j > i (movers never overlap anything,
@@ -2148,7 +2202,9 @@ __global__ void k_scale_radius(int64_t n, double4* __restrict__ rec, double4* __
 }
 
 template <int D>
-__global__ void k_copy_state(int64_t n, State A, State B) {
+__global__ void k_copy_state(int64_t n, State A, State B, const GridParams* sel_gp = nullptr,
+                             const double4* rec_alt = nullptr) {
+    if (sel_gp && sel_gp->resolve) A.rec = const_cast<double4*>(rec_alt);  // (graph runs, as k_stats_sweep)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         B.rec[i] = A.rec[i];

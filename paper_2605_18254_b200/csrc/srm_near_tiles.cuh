@@ -14,6 +14,12 @@
 // atomics).  Same screen as near_candidates (cutoff, margin, factor), so the lists hold
 // the same pairs as k_near_lists.  A brick whose halo holds more than kTileCap particles
 // takes near_full_particle.
+#undef NT_TAG
+#if NT_FUSED
+#define NT_TAG(row9) ((row9) << 12)  // the stencil row of a hit, beside its staged slot
+#else
+#define NT_TAG(row9) 0
+#endif
 constexpr int kTX = NT_X, kTY = NT_Y, kTZ = NT_Z;  // brick (cells)
 constexpr int kHX = kTX + 2, kHY = kTY + 2, kHZ = kTZ + 2;
 constexpr int kHCells = kHX * kHY * kHZ;
@@ -21,8 +27,13 @@ constexpr int kHRows = kHY * kHZ;
 constexpr int kTileCap = NT_CAP;  // staged particles
 constexpr int kTileThreads = NT_THREADS;
 constexpr int kCellsPerThread = (kHCells + kTileThreads - 1) / kTileThreads;
+// per-thread hit buffer (uint16 entries): screens 0 / 1 keep kNearCap + 1 hit slots; screen 2
+// keeps kPairCap + 1 pair records and, behind them, the kNearCap hit slots it resolves them to
+constexpr int kPairCap = 8;
+constexpr int kHitRows = NT_SCREEN == 2 ? kPairCap + 1 + kNearCap : kNearCap + 1;
 constexpr size_t kTileSmem = kTileCap * (16 + 4) + (kHCells + 1) * 4 +
-                             (kHCells * 4 > kTileThreads * (kNearCap + 1) * 2 ? kHCells * 4 : kTileThreads * (kNearCap + 1) * 2);
+                             (kHCells * 4 > kTileThreads * kHitRows * 2 ? kHCells * 4 : kTileThreads * kHitRows * 2);
+static_assert(NT_SCREEN != 2 || kTileCap <= 4096, "pair records: 11 bits of pair index + the stencil row");
 static_assert(kTileCap <= 65536, "16-bit hit slots");
 static_assert(kHRows <= kTileThreads && kHRows <= 64, "a thread per halo row; 6-step row search");
 static_assert(kTY * kTZ <= 32 && kTX <= 16, "one warp scans the interior rows; 4-step cell search");
@@ -31,7 +42,13 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                                                              const cell_t* __restrict__ cs,
                                                              const uint32_t* __restrict__ skey,
                                                              int32_t* __restrict__ nbr, NearPool pool,
-                                                             StatsDev* stats) {
+                                                             StatsDev* stats
+#if NT_FUSED
+                                                             , Box box, const RoundParams* __restrict__ rpp,
+                                                             double4* __restrict__ rec_new,
+                                                             uint8_t* __restrict__ dflag, uint8_t* __restrict__ acc
+#endif
+                                                             ) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // shifted fp32 records of staged slots 2p, 2p + 1, interleaved for f32x2 arithmetic:
     // pxy[p] = (x0, x1, y0, y1), pzw[p] = (z0, z1, w0, w1)
@@ -47,6 +64,15 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
     __shared__ RowMap rmap[kHRows];
     const GridParams& g = *gp;
     if (g.near_kind != NT_KIND || static_cast<int>(blockIdx.x) >= g.ntiles) return;  // (graph launches: upper bounds)
+#if NT_FUSED
+    if (!g.resolve) return;
+    __shared__ uint8_t hcls[kHCells];  // colour class of a halo cell (the sweep order between cells)
+    __shared__ RoundParams rp;
+    if (threadIdx.x == 0) rp = *rpp;
+    static_assert(kTileCap <= 4096, "hit slots carry the stencil row in bits 12-15");
+#else
+    if (NT_KIND == 0 && g.resolve) return;  // the fused variant (rtiles) has this grid
+#endif
     const int dx = g.dims[0], dy = g.dims[1], dz = g.dims[2];
     const int ntx = (dx + kTX - 1) / kTX, nty = (dy + kTY - 1) / kTY;
     const int tx = blockIdx.x % ntx, ty = (blockIdx.x / ntx) % nty, tz = blockIdx.x / (ntx * nty);
@@ -72,6 +98,9 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                 const int64_t b = cs[cell];
                 c = static_cast<int>(cs[cell + 1] - b);
                 hsrc[hc] = static_cast<int32_t>(b);
+#if NT_FUSED
+                hcls[hc] = static_cast<uint8_t>(colour1(g, 0, X) + g.col_n[0] * (colour1(g, 1, Y) + g.col_n[1] * colour1(g, 2, Z)));
+#endif
             }
         }
         cnts[k] = c;
@@ -108,8 +137,19 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
             const int Y = y0 + r % wy, Z = z0 + r / wy;
             const int64_t row = (static_cast<int64_t>(Z) * dy + Y) * dx;
             const int64_t b = cs[row + x0], e = cs[row + x0 + wx];
-            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x)
+            for (int64_t q = b + threadIdx.x; q < e; q += blockDim.x) {
                 near_full_particle<3>(q, S, g, cs, skey, nbr, pool, stats);
+#if NT_FUSED
+                {  // pending, with its first trial drawn (the row carries no precedence mask)
+                    const double4 me = S.rec[q];
+                    const double xi[3] = {me.x, me.y, me.z};
+                    double p[3];
+                    propose<3>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[q]), 0u, p);
+                    rec_new[q] = make_double4(p[0], p[1], p[2], me.w);
+                    dflag[q] = kUndecided;
+                }
+#endif
+            }
         }
         return;
     }
@@ -216,7 +256,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         const float l2m = __fmul_rn(__fmul_rn(limm, limm), 1.00001f);
         uint16_t* ql = lst + threadIdx.x;
         int nn = 0;
-#if SRM_NEAR_SCREEN == 0
+#if NT_SCREEN == 0 || NT_SCREEN == 2
         // hits are rare per lane but common per warp: record the hit slots branch-free (a
         // store to the current list slot every test, the count advances on a hit; slot
         // kNearCap absorbs the overflow), resolve them after the scan
@@ -234,7 +274,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
             const int ddy = row9 % 3 - 1, ddz = row9 / 3 - 1;
             const int c = hc + ddy * kHX + ddz * kHX * kHY;
             const int kb = hoff[c - 1], ke = hoff[c + 2];
-#if SRM_NEAR_SCREEN == 0
+#if NT_SCREEN == 0
             // slots [kb, ke) two at a time (pairs 2p, 2p + 1; the ends masked)
             for (int p = kb >> 1; 2 * p < ke; ++p) {
                 const float4 A = pxy[p], B = pzw[p];
@@ -250,12 +290,42 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                     l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
                 }
                 const int k0 = 2 * p;
-                ql[at * kTileThreads] = static_cast<uint16_t>(k0);
+                ql[at * kTileThreads] = static_cast<uint16_t>(k0 + NT_TAG(row9));
                 nn += (d2.x <= l2.x && k0 >= kb && k0 != i) ? 1 : 0;
                 at = min(nn, kNearCap);
-                ql[at * kTileThreads] = static_cast<uint16_t>(k0 + 1);
+                ql[at * kTileThreads] = static_cast<uint16_t>(k0 + 1 + NT_TAG(row9));
                 nn += (d2.y <= l2.y && k0 + 1 < ke && k0 + 1 != i) ? 1 : 0;
                 at = min(nn, kNearCap);
+            }
+#elif NT_SCREEN == 2
+            // slots [kb, ke) two at a time; ONE record per pair with a hit in either slot
+            // (pair index + stencil row).  The ends of the range, the particle itself and
+            // the slots proper are sorted out after the scan, from the few recorded pairs.
+            if (mono) {
+                for (int p = kb >> 1; 2 * p < ke; ++p) {
+                    const float4 A = pxy[p];
+                    const float2 Bz = *reinterpret_cast<const float2*>(pzw + p);
+                    const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                    const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                    const float2 ez = __fadd2_rn(Bz, nmz);
+                    const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                    ql[at * kTileThreads] = static_cast<uint16_t>(p + (row9 << 11));
+                    nn += (d2.x <= l2m || d2.y <= l2m) ? 1 : 0;
+                    at = min(nn, kPairCap);
+                }
+            } else {
+                for (int p = kb >> 1; 2 * p < ke; ++p) {
+                    const float4 A = pxy[p], B = pzw[p];
+                    const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                    const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                    const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                    const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                    const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                    const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                    ql[at * kTileThreads] = static_cast<uint16_t>(p + (row9 << 11));
+                    nn += (d2.x <= l2.x || d2.y <= l2.y) ? 1 : 0;
+                    at = min(nn, kPairCap);
+                }
             }
 #else
             // slots [kb, ke) two at a time (pairs 2p, 2p + 1), 16 pairs per mask
@@ -304,10 +374,118 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
             }
 #endif
         }
+#if NT_SCREEN == 2
+        {
+            // the recorded pairs -> hit slots (the same fp32 predicate per slot, now with the
+            // range ends and the particle itself excluded), kept behind the pair records
+            const int npairs = nn;
+            uint16_t* qh = ql + (kPairCap + 1) * kTileThreads;
+            nn = 0;
+            auto slot_hit = [&](int k) {
+                const float* a = reinterpret_cast<const float*>(pxy + (k >> 1)) + (k & 1);
+                const float* b = reinterpret_cast<const float*>(pzw + (k >> 1)) + (k & 1);
+                const float ex = __fadd_rn(a[0], -mx), ey = __fadd_rn(a[2], -my), ez = __fadd_rn(b[0], -mz);
+                const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                const float lim = __fadd_rn(b[2], base);
+                return d2 <= __fmul_rn(__fmul_rn(lim, lim), 1.00001f);
+            };
+            if (npairs <= kPairCap) {
+#pragma unroll 1
+                for (int t = 0; t < npairs; ++t) {
+                    const int tg = ql[t * kTileThreads];
+                    const int P = tg & 0x7ff, r9 = tg >> 11;
+                    const int c = hc + (r9 % 3 - 1) * kHX + (r9 / 3 - 1) * kHX * kHY;
+                    const int kb = hoff[c - 1], ke = hoff[c + 2];
+#pragma unroll
+                    for (int sub = 0; sub < 2; ++sub) {
+                        const int k = 2 * P + sub;
+                        if (k >= kb && k < ke && k != i && slot_hit(k)) {
+                            if (nn < kNearCap) qh[nn * kTileThreads] = static_cast<uint16_t>(k);
+                            ++nn;
+                        }
+                    }
+                }
+            } else {  // more pairs than records (rare on these grids): count the hits exactly
+#pragma unroll 1
+                for (int row9 = 0; row9 < 9; ++row9) {
+                    const int c = hc + (row9 % 3 - 1) * kHX + (row9 / 3 - 1) * kHX * kHY;
+                    const int kb = hoff[c - 1], ke = hoff[c + 2];
+                    for (int k = kb; k < ke; ++k)
+                        if (k != i && slot_hit(k)) ++nn;
+                }
+                // (more than kPairCap pairs always hold more than kNearCap hits: only the
+                //  particle's own pair is recorded without one -- the slots next to a range
+                //  end sit two cells away along x; the overflow branch copes either way)
+                if (nn <= kNearCap) nn = kNearCap + 1;
+            }
+            ql = qh;  // the resolution below reads hit slots
+        }
+#endif
         // resolve: sorted indices, and shape.hpp:70 self-exclusion by id
         int32_t e[kNearCap];
         int m = 0;
+#if NT_FUSED
+        // the first trial T1 (a pure function of slot, round and iteration) becomes the
+        // tentative record of the new state
+        const double4 me64 = S.rec[qi];
+        double t1[3];
+        {
+            const double xi[3] = {me64.x, me64.y, me64.z};
+            propose<3>(box, xi, rp.c_m, rp.key, static_cast<uint32_t>(S.slot[qi]), 0u, t1);
+        }
+        rec_new[qi] = make_double4(t1[0], t1[1], t1[2], me64.w);
+        if (nn > kNearCap) dflag[qi] = kUndecided;
         if (nn <= kNearCap) {
+            const int32_t idi = S.id[qi];
+            const int mycls = hcls[hc];
+            unsigned pmask = 0;  // bit t: entry t precedes this particle in (class, cell, slot)
+#pragma unroll
+            for (int t = 0; t < kNearCap; ++t) {
+                if (t < nn) {
+                    const int tk = ql[t * kTileThreads];
+                    const int k = tk & 0xfff, r9 = tk >> 12;
+                    const int c = hc + (r9 % 3 - 1) * kHX + (r9 / 3 - 1) * kHX * kHY;
+                    const int hcj = c - 1 + (k >= hoff[c] ? 1 : 0) + (k >= hoff[c + 1] ? 1 : 0);
+                    const int32_t j = pj[k];
+                    if (S.id[j] != idi) {
+                        const bool pre = hcls[hcj] < mycls || (hcj == hc && k < i);
+#pragma unroll
+                        for (int u = 0; u < kNearCap; ++u)
+                            if (u == m) e[u] = j;
+                        pmask |= (pre ? 1u : 0u) << m;
+                        ++m;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kNearCap; ++u)
+                if (u >= m) e[u] = 0;
+            bool decided = false;
+            if (pmask == 0) {  // every near neighbour is visited later: it sits at its round-start record
+                decided = true;
+#pragma unroll
+                for (int u = 0; u < kNearCap; ++u) {
+                    if (u < m) {
+                        const double4 v = S.rec[e[u]];
+                        const double xl[3] = {v.x, v.y, v.z};
+                        if (sphere_overlap<3>(box, t1, me64.w, xl, v.w)) decided = false;
+                    }
+                }
+            }
+            dflag[qi] = decided ? static_cast<uint8_t>(0) : kUndecided;
+            if (decided) {
+                if (rp.write_acc) acc[qi] = 0;
+                continue;
+            }
+            int4* rowp = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
+            rowp[0] = make_int4(m | static_cast<int>(pmask << 8) | kRowMask, e[0], e[1], e[2]);
+            rowp[1] = make_int4(e[3], e[4], e[5], e[6]);
+            continue;
+        }
+        if (false) {  // (longer lists: the overflow branch below)
+#else
+        if (nn <= kNearCap) {
+#endif
             const int32_t idi = S.id[qi];
 #pragma unroll
             for (int t = 0; t < kNearCap; ++t) {
@@ -355,7 +533,14 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                         if (d2 <= l2 && k != i) {
                             const int32_t j = pj[k];
                             if (S.id[j] != idi) {
+#if NT_FUSED
+                                // (bit 31: the entry precedes this particle in the sweep order)
+                                const int hcj = c - 1 + (k >= hoff[c] ? 1 : 0) + (k >= hoff[c + 1] ? 1 : 0);
+                                const bool pre = hcls[hcj] < hcls[hc] || (hcj == hc && k < i);
+                                if (m < nn) dst[m] = pre ? (j | static_cast<int32_t>(0x80000000u)) : j;
+#else
                                 if (m < nn) dst[m] = j;  // never past the entries reserved above
+#endif
                                 ++m;
                             }
                         }
@@ -366,13 +551,20 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                 row[0] = make_int4(m, -1, 0, 0);
                 row[1] = make_int4(0, 0, 0, 0);
             } else if (m > kNearCap) {
-                row[0] = make_int4(m, static_cast<int32_t>(off), 0, 0);
+                row[0] = make_int4(m | (NT_FUSED ? kRowPool : 0), static_cast<int32_t>(off), 0, 0);
                 row[1] = make_int4(0, 0, 0, 0);
             } else {  // same-id images removed: the list fits the row after all
                 int32_t e2[kNearCap];
+                unsigned pm = 0;
 #pragma unroll
-                for (int t = 0; t < kNearCap; ++t) e2[t] = t < m ? dst[t] : 0;
-                row[0] = make_int4(m, e2[0], e2[1], e2[2]);
+                for (int t = 0; t < kNearCap; ++t) {
+                    e2[t] = t < m ? dst[t] : 0;
+                    if (NT_FUSED && e2[t] < 0) {
+                        pm |= 1u << t;
+                        e2[t] &= 0x7fffffff;
+                    }
+                }
+                row[0] = make_int4(m | (NT_FUSED ? static_cast<int>(pm << 8) | kRowMask : 0), e2[0], e2[1], e2[2]);
                 row[1] = make_int4(e2[3], e2[4], e2[5], e2[6]);
             }
             continue;

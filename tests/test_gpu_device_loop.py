@@ -12,7 +12,7 @@ import paper_2605_18254_b200 as srm
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["", "lane", "trials", "wave"])
+@pytest.fixture(autouse=True, params=["", "lane", "trials", "wave", "resolve"])
 def sweep_kernel(request, monkeypatch):
     """Every test once per sweep kernel (SRM_B200_SWEEP: "" = chosen by the grid, lane =
     k_sweep_warpq, trials = k_sweep_trials, team = k_sweep_team, wave = the one-launch wavefront

@@ -14,7 +14,7 @@ from paper_2605_18254_b200 import _native
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["", "lane", "trials", "team", "wave"])
+@pytest.fixture(autouse=True, params=["", "lane", "trials", "team", "wave", "resolve"])
 def sweep_kernel(request, monkeypatch):
     """Every test once per sweep kernel (SRM_B200_SWEEP: "" = chosen by the grid, lane =
     k_sweep_warpq, trials = k_sweep_trials, team = k_sweep_team, wave = the one-launch wavefront

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="particles (box scaled to keep the density)")
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--timing", action="store_true")
+    ap.add_argument("--n_l", type=int, default=0, help="attempts per particle (default: the configuration's)")
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
     n = args.n or cfg["n"]
@@ -37,7 +38,7 @@ def main():
     ctx.sync()
     rt.cudaProfilerStart()  # ncu --profile-from-start off captures only the timed rounds
     ctx.stopwatch_start()
-    st = ctx.rounds(cs, c_m, cfg.get("n_l", bench.N_L), 77, 0, 1, args.rounds)
+    st = ctx.rounds(cs, c_m, args.n_l or cfg.get("n_l", bench.N_L), 77, 0, 1, args.rounds)
     ms = ctx.stopwatch_stop()
     rt.cudaProfilerStop()
     print(f"{args.rounds} rounds: {ms:.3f} ms ({ms / args.rounds:.3f} ms/round), overlaps {st.overlap_pairs}, "
