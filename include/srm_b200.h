@@ -224,13 +224,26 @@ const char* srm_b200_io_error(void);
 /* descriptors.hpp:96-115 nearest_neighbor_distances of the context's state (exact: the
  * minimum over all other centres, as the reference's ring search) and, when counts_out is
  * given, descriptors.hpp:254-277 histogram(nnd, bins, lo, hi) (counts[bins], total,
- * in_range).  nnd_out (nullable): n distances in download order.  Spheres/disks. */
+ * in_range).  nnd_out (nullable): n distances in download order.  Any shape (platelets:
+ * centre distances). */
 int srm_b200_nnd_histogram(srm_b200_ctx* ctx, int bins, double lo, double hi, int64_t* counts_out,
                            int64_t* total_out, int64_t* in_range_out, double* nnd_out);
 /* Unordered centre-pair distances (min image) binned on edges[0..bins] with
  * numpy.histogram's rule (last bin closed): the RDF counts of the parity tests
  * (tests/stats_util.py rdf_counts; the reference has no RDF). */
 int srm_b200_pair_counts(srm_b200_ctx* ctx, const double* edges, int bins, int64_t* counts_out);
+/* Platelet statistics on the device (platelet contexts; every output nullable, per-platelet
+ * outputs in download order):
+ *   value_out / count_out  descriptors.hpp:182-209 local_nematic_order(snapshot, cutoff):
+ *                          mean |n_i . n_j| over the platelets whose centre lies within
+ *                          cutoff (NaN when none) and their number; skipped when cutoff <= 0
+ *                          and both are null, ValidationError's code when asked with cutoff <= 0
+ *   nnd_out / nn_align_out centre nearest-neighbour distance and |n . n'| of that neighbour
+ *   q_out[6]               sum over platelets of n (x) n: xx, yy, zz, xy, xz, yz (the Q tensor
+ *                          of the nematic order parameter S2 = largest eigenvalue of
+ *                          (3 q / n - 1) / 2), summed in a fixed order */
+int srm_b200_platelet_order(srm_b200_ctx* ctx, double cutoff, double* value_out, int32_t* count_out, double* nnd_out,
+                            double* nn_align_out, double* q_out);
 
 /* ---- initial states (rsa.hpp:21-69) ------------------------------------------------ */
 /* rsa_place with Rng(seed) (std::mt19937_64): bit-identical to the reference for the

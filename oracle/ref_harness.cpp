@@ -406,6 +406,26 @@ int ref_generate_platelets(const double* L, int64_t n, double* pos, double* nrm,
     }
 }
 
+// descriptors.hpp:182-209 local_nematic_order; 0 ok, 2 invalid cutoff
+int ref_local_nematic_order(const double* L, int64_t n, const double* pos, const double* nrm, const double* D,
+                            const double* t, double cutoff, double* value, int32_t* count) {
+    PlateletSnapshot snap;
+    snap.box = make_box<3>(L);
+    snap.particles.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i)
+        snap.particles[i] = make_pl(pos + 3 * i, nrm + 3 * i, D[i], t[i], static_cast<int32_t>(i));
+    try {
+        const auto o = local_nematic_order(snap, cutoff);
+        for (int64_t i = 0; i < n; ++i) {
+            value[i] = o.value[i];
+            count[i] = o.neighbor_count[i];
+        }
+        return 0;
+    } catch (const ValidationError&) {
+        return 2;
+    }
+}
+
 // CPU baseline for platelets: `threads` replicas x `rounds` SRM rounds at fixed size
 // (build_shape_grid -> migrate -> shape_any_collision with SpherodiskShape).  Wall s.
 double ref_pl_bench_rounds(const double* L, int64_t n, const double* pos, const double* nrm, const double* D,

@@ -466,6 +466,26 @@ class Context:
         self._c(_native.lib().srm_b200_pair_counts(self._h, L, bins, _ptr(counts)))
         return counts
 
+    def local_nematic_order(self, cutoff: float):
+        """descriptors.hpp:182-209 on the device: (value, neighbor_count) per platelet
+        (download order; value is NaN where no centre lies within the cutoff)."""
+        value = np.empty(max(self.n, 1))
+        count = np.zeros(max(self.n, 1), np.int32)
+        self._c(_native.lib().srm_b200_platelet_order(self._h, float(cutoff), _ptr(value), _ptr(count), None, None, None))
+        return value[:self.n], count[:self.n]
+
+    def platelet_summary(self):
+        """Platelet parity summaries on the device: centre nearest-neighbour distances, the
+        |n . n'| of each platelet with its nearest neighbour, and the nematic order
+        parameter S2 (largest eigenvalue of <(3 n n - 1) / 2>)."""
+        nnd = np.empty(max(self.n, 1))
+        align = np.empty(max(self.n, 1))
+        q = np.zeros(6)
+        self._c(_native.lib().srm_b200_platelet_order(self._h, 0.0, None, None, _ptr(nnd), _ptr(align), _ptr(q)))
+        Q = np.array([[q[0], q[3], q[4]], [q[3], q[1], q[5]], [q[4], q[5], q[2]]])
+        s2 = float(np.linalg.eigvalsh((3.0 * Q / self.n - np.eye(3)) / 2.0)[-1])
+        return nnd[:self.n], align[:self.n], s2
+
     def set_generate_mode(self, device_loop: bool) -> None:
         """generate(): one device-resident CUDA graph (True, default) or the host-driven loop"""
         self._c(_native.lib().srm_b200_set_generate_mode(self._h, 1 if device_loop else 0))

@@ -118,6 +118,8 @@ _SIGS = {
     "srm_b200_nnd_histogram": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_void_p, c_int64_p, c_int64_p,
                                          C.c_void_p]),
     "srm_b200_pair_counts": (C.c_int, [C.c_void_p, c_double_p, C.c_int, C.c_void_p]),
+    "srm_b200_platelet_order": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]),
     "srm_b200_rsa_clustered": (C.c_int, [C.c_int, c_double_p, C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_int64,
                                          C.c_uint64, C.c_void_p, C.c_void_p, c_int64_p]),
     "srm_b200_rsa_platelets": (C.c_int, [C.c_int64, C.c_double, C.c_double, c_double_p, C.c_int64, C.c_uint64, C.c_void_p,

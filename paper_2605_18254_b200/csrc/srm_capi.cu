@@ -1322,7 +1322,6 @@ int srm_b200_nnd_histogram(srm_b200_ctx* c, int bins, double lo, double hi, int6
         if (n < 2) throw Invalid{"nearest_neighbor_distances: need at least 2 particles"};
         if (counts_out && bins < 1) throw Invalid{"histogram: bin_count must be >= 1"};
         if (counts_out && !(hi > lo)) throw Invalid{"histogram: need hi > lo"};
-        if (c->platelets()) throw Invalid{"nnd: spheres and disks only"};
         const double mr = c->max_radius(c->P);
         // any grid gives the exact answer; about one particle per cell, as descriptor_grid
         double vol = 1.0;
@@ -1493,11 +1492,66 @@ int srm_b200_rsa_platelets_device(srm_b200_ctx* c, int64_t n, double diameter, d
     });
 }
 
+int srm_b200_platelet_order(srm_b200_ctx* c, double cutoff, double* value_out, int32_t* count_out, double* nnd_out,
+                            double* nn_align_out, double* q_out) {
+    return guarded(c, [&]() -> int {
+        const int64_t n = c->n;
+        if (!c->platelets()) throw Invalid{"platelet_order: a platelet context is required"};
+        if ((value_out || count_out) && !(cutoff > 0.0))
+            throw Invalid{"local_nematic_order: cutoff must be positive"};  // descriptors.hpp:183
+        const double mr = c->max_radius(c->P);
+        const int nb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 16));
+        if (value_out || count_out) {
+            c->set_grid(c->make_grid(cutoff, mr, 0.0));  // cells >= cutoff: a one-cell stencil
+            c->grid_build(c->P);
+            const GridParams& g = c->hg;
+            int32_t sw[3];
+            for (int a = 0; a < 3; ++a) sw[a] = g.dims[a] <= 3 ? -1 : 1;
+            DevBuf<int32_t> dsw(3), cnt(n);
+            DevBuf<double> val(n);
+            SRM_CUDA(cudaMemcpyAsync(dsw.p, sw, sizeof(sw), cudaMemcpyHostToDevice, c->stream));
+            k_local_nematic<<<nb, 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, dsw.p, cutoff, val.p,
+                                                       cnt.p);
+            c->launched();
+            if (value_out) SRM_CUDA(cudaMemcpyAsync(value_out, val.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+            if (count_out) SRM_CUDA(cudaMemcpyAsync(count_out, cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        if (nnd_out || nn_align_out) {
+            if (n < 2) throw Invalid{"nearest_neighbor_distances: need at least 2 particles"};
+            double cell = std::pow(c->box_measure() / static_cast<double>(n), 1.0 / 3.0);
+            cell = std::max(cell, 1e-3 * mr);
+            c->set_grid(c->make_grid(cell, mr, 0.0));
+            c->grid_build(c->P);
+            DevBuf<double> d(n), al(n);
+            k_nnd<3><<<nb, 256, 0, c->stream>>>(n, c->S, c->box, c->gp, c->cell_start, c->skey, d.p, al.p);
+            c->launched();
+            if (nnd_out) SRM_CUDA(cudaMemcpyAsync(nnd_out, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+            if (nn_align_out) SRM_CUDA(cudaMemcpyAsync(nn_align_out, al.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        if (q_out) {
+            constexpr int kQBlocks = 296;
+            DevBuf<double> part(kQBlocks * 6);
+            k_q_tensor<<<kQBlocks, 256, 0, c->stream>>>(n, c->P.aux, part.p);
+            c->launched();
+            std::vector<double> hp(kQBlocks * 6);
+            SRM_CUDA(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, c->stream));
+            SRM_CUDA(cudaStreamSynchronize(c->stream));
+            for (int k = 0; k < 6; ++k) {
+                double s = 0.0;
+                for (int b = 0; b < kQBlocks; ++b) s += hp[b * 6 + k];
+                q_out[k] = s;
+            }
+        }
+        return SRM_B200_OK;
+    });
+}
+
 int srm_b200_pair_counts(srm_b200_ctx* c, const double* edges, int bins, int64_t* counts_out) {
     return guarded(c, [&]() -> int {
         const int64_t n = c->n;
         if (bins < 1 || !(edges[bins] > edges[0]) || !(edges[0] >= 0.0)) throw Invalid{"pair_counts: bad edges"};
-        if (c->platelets()) throw Invalid{"pair_counts: spheres and disks only"};
         std::vector<unsigned long long> hh(static_cast<size_t>(bins), 0ull);
         if (n >= 2) {
             const double hi = edges[bins];

@@ -53,10 +53,13 @@ __device__ __forceinline__ void for_ring_ranges(const GridParams& g, const cell_
 // r = 0, 1, ... until the best squared distance is below (r edge_min)^2 (every unvisited
 // cell is at least r cells away along some axis: descriptors.hpp:68-73); a grid too small
 // for the next ring falls back to all particles.
+// nn_align (platelets, optional): |n_q . n_j| of the nearest neighbour j found (the first
+// at the minimum distance in scan order), by slot -- the nearest-neighbour alignment of
+// the platelet parity summaries.
 template <int D>
 __global__ void __launch_bounds__(256) k_nnd(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
                                              const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
-                                             double* __restrict__ out) {
+                                             double* __restrict__ out, double* __restrict__ nn_align = nullptr) {
     const GridParams& g = *gp;
     double emin = g.edge[0];
     for (int a = 1; a < D; ++a) emin = g.edge[a] < emin ? g.edge[a] : emin;
@@ -68,13 +71,17 @@ __global__ void __launch_bounds__(256) k_nnd(int64_t n, State S, Box box, const 
         int c[3];
         decode_key<D>(g, skey[q], c);
         double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+        int64_t arg = -1;
         auto scan = [&](int64_t b, int64_t e) {
             for (int64_t j = b; j < e; ++j) {
                 if (j == q) continue;
                 double y[D];
                 rec_pos<D>(S.rec[j], y);
                 const double d2 = dist2<D>(box, x, y);
-                best = d2 < best ? d2 : best;
+                if (d2 < best) {
+                    best = d2;
+                    arg = j;
+                }
             }
         };
         bool done = false;
@@ -89,7 +96,76 @@ __global__ void __launch_bounds__(256) k_nnd(int64_t n, State S, Box box, const 
             done = best < bound * bound;
         }
         out[S.slot[q]] = sqrt(best);
+        if (nn_align) {
+            double a = __longlong_as_double(0x7ff8000000000000LL);  // NaN: no neighbour
+            if (arg >= 0) {
+                const double4 u = S.aux[q], w = S.aux[arg];
+                a = fabs(u.x * w.x + u.y * w.y + u.z * w.z);
+            }
+            nn_align[S.slot[q]] = a;
+        }
     }
+}
+
+// descriptors.hpp:182-209 local_nematic_order: per platelet the mean |n_i . n_j| over the
+// platelets whose centre lies within `cutoff` (NaN when none) and their number, by slot.
+// The grid's cells are at least `cutoff` wide, so the one-cell stencil `s` holds them all.
+__global__ void __launch_bounds__(256) k_local_nematic(int64_t n, State S, Box box, const GridParams* __restrict__ gp,
+                                                       const cell_t* __restrict__ cs,
+                                                       const uint32_t* __restrict__ skey, const int32_t* s,
+                                                       double cutoff, double* __restrict__ value,
+                                                       int32_t* __restrict__ count) {
+    const GridParams& g = *gp;
+    const double cut2 = cutoff * cutoff;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        double x[3];
+        rec_pos<3>(S.rec[q], x);
+        const double4 u = S.aux[q];
+        double acc = 0.0;
+        int cnt = 0;
+        for_near_ranges<3>(g, cs, skey[q], s, [&](int64_t b0, int64_t e0) {
+            for (int64_t j = b0; j < e0; ++j) {
+                if (j == q) continue;
+                double y[3];
+                rec_pos<3>(S.rec[j], y);
+                if (dist2<3>(box, x, y) <= cut2) {
+                    const double4 w = S.aux[j];
+                    acc += fabs(u.x * w.x + u.y * w.y + u.z * w.z);
+                    ++cnt;
+                }
+            }
+        });
+        const int32_t sl = S.slot[q];
+        count[sl] = cnt;
+        value[sl] = cnt > 0 ? acc / cnt : __longlong_as_double(0x7ff8000000000000LL);
+    }
+}
+
+// Sum of n (x) n over the platelets (xx, yy, zz, xy, xz, yz) in a fixed order: per-block
+// partials, finished on the host -- the Q tensor of the nematic order parameter S2.
+__global__ void __launch_bounds__(256) k_q_tensor(int64_t n, const double4* __restrict__ aux,
+                                                  double* __restrict__ part) {
+    __shared__ double ss[6][256];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = blockIdx.x * chunk, b1 = b0 + chunk < n ? b0 + chunk : n;
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += 256) {
+        const double4 u = aux[i];
+        a[0] += u.x * u.x;
+        a[1] += u.y * u.y;
+        a[2] += u.z * u.z;
+        a[3] += u.x * u.y;
+        a[4] += u.x * u.z;
+        a[5] += u.y * u.z;
+    }
+    for (int k = 0; k < 6; ++k) ss[k][threadIdx.x] = a[k];
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (static_cast<int>(threadIdx.x) < w)
+            for (int k = 0; k < 6; ++k) ss[k][threadIdx.x] += ss[k][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 6) part[blockIdx.x * 6 + threadIdx.x] = ss[threadIdx.x][0];
 }
 
 // descriptors.hpp:254-277 histogram over [lo, hi] (top edge inclusive, non-finite values

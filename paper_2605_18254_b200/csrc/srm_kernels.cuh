@@ -49,6 +49,7 @@ __host__ __device__ inline FastDiv make_fastdiv(uint32_t d) {
 struct GridParams {
     int32_t dims[3];
     double edge[3];
+    double inv_edge[3];  // 1 / edge (cell_of's quotient estimate)
     int64_t ncells;
     int32_t near_s[3];  // near-search half width per axis; -1 = every cell on the axis
     double extra;       // near cutoff: (ri + rj + extra) * (1 + 1e-9) + 1e-300
@@ -132,6 +133,7 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
         if (a >= dim) {
             g.dims[a] = 1;
             g.edge[a] = 1.0;
+            g.inv_edge[a] = 1.0;
             g.near_s[a] = -1;
             continue;
         }
@@ -142,6 +144,7 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
         if (nn < 3) nn = 3;
         g.dims[a] = nn;
         g.edge[a] = L / nn;
+        g.inv_edge[a] = 1.0 / g.edge[a];
         g.ncells *= nn;
         if (g.ncells > 4294967295LL) return 2;
     }
@@ -292,9 +295,19 @@ __device__ __forceinline__ uint32_t cell_of(const GridParams& g, const double* p
     uint64_t idx = 0;
 #pragma unroll
     for (int a = D - 1; a >= 0; --a) {
-        int i = static_cast<int>(floor(__ddiv_rn(p[a], g.edge[a])));
-        i %= g.dims[a];
-        if (i < 0) i += g.dims[a];
+        // floor(p / edge) of the correctly rounded quotient, as the reference computes it.
+        // The product with 1 / edge is within 3e-16 (relative) of that quotient, so when it
+        // is farther than 1e-9 (1 + |t|) from an integer the two floors agree and the
+        // division (some 40 instructions) is skipped; otherwise the quotient proper.
+        const double t = __dmul_rn(p[a], g.inv_edge[a]);
+        const double fl = floor(t), fr = t - fl, eps = 1e-9 * (1.0 + fabs(t));
+        int i;
+        if (fr > eps && 1.0 - fr > eps && fabs(t) < 1e9) i = static_cast<int>(fl);
+        else i = static_cast<int>(floor(__ddiv_rn(p[a], g.edge[a])));
+        if (i < 0 || i >= g.dims[a]) {  // (wrapped positions: only i == dims, by rounding)
+            i %= g.dims[a];
+            if (i < 0) i += g.dims[a];
+        }
         idx = idx * static_cast<uint64_t>(g.dims[a]) + static_cast<uint64_t>(i);
     }
     return static_cast<uint32_t>(idx);

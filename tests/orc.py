@@ -125,6 +125,8 @@ def ref():
         L.ref_generate_platelets.restype = C.c_int
         L.ref_generate_platelets.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, d, d, d, C.c_int, C.c_int, d,
                                              C.c_int64, C.c_uint64, C.c_int, vp, vp]
+        L.ref_local_nematic_order.restype = C.c_int
+        L.ref_local_nematic_order.argtypes = [vp, C.c_int64, vp, vp, vp, vp, d, vp, vp]
         L.ref_pl_any_collision.restype = C.c_int
         L.ref_pl_any_collision.argtypes = [vp, d, C.c_int64, vp, vp, vp, vp, vp]
         _ref = L
@@ -381,6 +383,18 @@ def r_rsa_platelets(n, diameter, aspect, L, max_attempts, seed):
     ids = np.zeros(n, np.int32)
     st = ref().ref_rsa_platelets(n, diameter, aspect, P(arr(L)), max_attempts, seed, P(pos), P(nrm), P(ids))
     return st, pos, nrm, ids
+
+
+def r_local_nematic_order(L, pos, nrm, D, t, cutoff):
+    """the reference's local_nematic_order (descriptors.hpp:182-209): (value, neighbor_count)"""
+    n = len(D)
+    value = np.zeros(n)
+    count = np.zeros(n, np.int32)
+    rc = ref().ref_local_nematic_order(P(arr(L)), n, P(arr(pos)), P(arr(nrm)), P(arr(D)), P(arr(t)), float(cutoff),
+                                       P(value), P(count))
+    if rc != 0:
+        raise ValueError("local_nematic_order: cutoff must be positive")
+    return value, count
 
 
 def o_rsa_rounds(dim, L, radii, seed, max_rounds):

@@ -50,3 +50,40 @@ def test_pair_counts_match_numpy(dim, n, f, seed, poly, hi_rel):
         ctx.upload(pos, r, ids)
         c = ctx.pair_counts(np.linspace(lo, hi, bins + 1))
     assert np.array_equal(c, stats_util.rdf_counts(pos, L, lo, hi, bins))
+
+
+# ---- platelets (the platelet parity statistics on the device) -----------------
+@pytest.mark.parametrize("n,aspect,rho,seed,cut_rel", [(3000, 20.0, 2.0, 11, 1.5), (800, 100.0, 3.0, 12, 1.0),
+                                                        (200, 10.0, 1.0, 13, 4.0)])
+def test_platelet_order_vs_reference(n, aspect, rho, seed, cut_rel):
+    """local_nematic_order (descriptors.hpp:182-209): neighbour counts exact, values within
+    1e-12 (the sum over neighbours runs in another cell order); centre NND bit for bit; the
+    nearest-neighbour alignment and S2 against numpy."""
+    box = 10.0
+    L = [box] * 3
+    D0 = (rho * box ** 3 / n) ** (1.0 / 3.0)
+    st, pos, nrm, ids = orc.r_rsa_platelets(n, D0, aspect, L, 100000, seed)
+    assert st == 0
+    D, t = np.full(n, D0), np.full(n, D0 / aspect)
+    cutoff = cut_rel * D0
+    with srm.Context(L, n, shape="platelet") as ctx:
+        ctx.upload_platelets(pos, nrm, D, t, ids)
+        value, count = ctx.local_nematic_order(cutoff)
+        nnd, align, s2 = ctx.platelet_summary()
+        with pytest.raises(srm.ValidationError):
+            ctx.local_nematic_order(0.0)
+    v_ref, c_ref = orc.r_local_nematic_order(L, pos, nrm, D, t, cutoff)
+    assert np.array_equal(count, c_ref)
+    assert np.array_equal(np.isnan(value), np.isnan(v_ref))
+    ok = ~np.isnan(v_ref)
+    assert np.allclose(value[ok], v_ref[ok], rtol=1e-12, atol=0.0)
+    assert np.array_equal(nnd, orc.r_nnd(3, L, pos))
+    # nearest neighbour by brute force (ties have probability zero for random centres)
+    d = pos[:, None, :] - pos[None, :, :]
+    d -= box * np.round(d / box)
+    d2 = (d * d).sum(-1)
+    np.fill_diagonal(d2, np.inf)
+    j = d2.argmin(1)
+    assert np.allclose(align, np.abs((nrm * nrm[j]).sum(1)), rtol=0, atol=1e-14)
+    Q = (3.0 * np.einsum("ni,nj->ij", nrm, nrm) / n - np.eye(3)) / 2.0
+    assert abs(s2 - float(np.linalg.eigvalsh(Q)[-1])) < 1e-12

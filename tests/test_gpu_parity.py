@@ -100,6 +100,35 @@ def test_grid_build_bit_exact(dim, n, cs, L):
     assert np.array_equal(remap[order], np.arange(n))
 
 
+@pytest.mark.parametrize("dim,cs,L", [(3, 0.0123, [1.0, 1.0, 1.0]), (2, 0.0371, [2.0, 1.0]), (3, 0.05, [1.0, 1.3, 0.7])])
+def test_keys_on_cell_boundaries_bit_exact(dim, cs, L):
+    """cell_of takes floor(p / edge) from a reciprocal product unless that product is within
+    1e-9 of an integer; coordinates on, and a few ulps around, every cell boundary must give
+    the reference's keys (floor of the correctly rounded quotient, cell_grid.hpp:62-79)."""
+    dims, edge = orc.o_grid(dim, L, cs)
+    rows = []
+    rng = np.random.default_rng(5)
+    for a in range(dim):
+        b = np.arange(dims[a] + 1) * edge[a]           # the boundaries as the grid computes them
+        b = np.concatenate([b, np.arange(dims[a] + 1) * (L[a] / dims[a]), np.linspace(0.0, L[a], dims[a] + 1)])
+        for k in range(-3, 4):
+            x = b.copy()
+            for _ in range(abs(k)):
+                x = np.nextafter(x, np.inf if k > 0 else -np.inf)
+            x = x[(x >= 0.0) & (x < L[a])]
+            p = rng.uniform(0.0, 1.0, (len(x), dim)) * np.array(L)
+            p[:, a] = x
+            rows.append(p)
+    pos = np.concatenate(rows)
+    r = np.full(len(pos), 0.001)
+    with _ctx(L, pos, r) as ctx:
+        keys, _, _ = ctx.grid_build(cs)
+    k_o, _, _ = orc.o_keys(dim, L, cs, pos)
+    assert np.array_equal(keys, k_o)
+    k_r, _ = orc.r_keys(dim, L, cs, pos)
+    assert np.array_equal(keys.astype(np.uint64), k_r)
+
+
 def test_reorder_by_locality_matches_reference():
     L = [1.0, 1.0, 1.0]
     pos, r = orc.random_particles(4000, 3, 0.001, 0.002, L, 5)
