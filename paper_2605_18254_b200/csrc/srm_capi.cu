@@ -118,7 +118,7 @@ struct srm_b200_ctx {
     int32_t* list_a = nullptr;   // resolve: pending lists (ping-pong)
     int32_t* list_b = nullptr;
     int32_t* seg_cnt = nullptr;  // resolve: entries per CTA segment of the pending lists (ping-pong)
-    static constexpr int resolve_ctas = 148 * SRM_RESOLVE_MINB;
+    static constexpr int resolve_ctas = kResolveMaxCtas;
     // opt-in (SRM_B200_WAVE=1 or SRM_B200_SWEEP=wave): measured no faster than the class
     // launches at cfg 4, so the class launches stay the default
     bool wave_default = [] {

@@ -33,6 +33,7 @@ constexpr int kResolveThreads = 256;
 #ifndef SRM_RESOLVE_MINB
 #define SRM_RESOLVE_MINB 4  // CTAs per SM of k_resolve_pass (64 registers)
 #endif
+constexpr int kResolveMaxCtas = 148 * SRM_RESOLVE_MINB;  // CTAs (list segments) of a pass: all resident
 constexpr int kResolveSoloItems = 512;         // a list this short is finished by one CTA
 constexpr int32_t kRowMask = 1 << 30;          // row[0] bit: bits 8-14 hold the precedence mask
 constexpr int32_t kRowPool = 1 << 29;          // row[0] bit: the list is in the pool, precedence in bit 31 of each entry
@@ -402,16 +403,22 @@ __global__ void __launch_bounds__(kResolveThreads, SRM_RESOLVE_MINB) k_resolve_p
     __shared__ int64_t s_m;
     __shared__ int s_w[kResolveThreads / 32];
     int32_t* cur = out;
-    if (threadIdx.x == 0) s_m = 0;
+    __shared__ int s_off[kResolveMaxCtas + 1];  // first position of a segment's entries in the gathered list
+    if (threadIdx.x == 0) {
+        int at = 0;
+        for (int b = 0; b < G; ++b) {
+            s_off[b] = at;
+            at += cnt_in[b];
+        }
+        s_off[G] = at;
+        s_m = at;
+    }
     __syncthreads();
     for (int b = 0; b < G; ++b) {
-        const int c = cnt_in[b];
-        const int64_t at = s_m;
-        for (int k = threadIdx.x; k < c; k += kResolveThreads) cur[at + k] = in[static_cast<int64_t>(b) * span + k];
-        __syncthreads();
-        if (threadIdx.x == 0) s_m = at + c;
-        __syncthreads();
+        const int c = s_off[b + 1] - s_off[b];
+        for (int k = threadIdx.x; k < c; k += kResolveThreads) cur[s_off[b] + k] = in[static_cast<int64_t>(b) * span + k];
     }
+    __syncthreads();
     int64_t m = s_m;
     while (m > 0) {
         __syncthreads();
