@@ -754,9 +754,6 @@ struct RowMap {
 #ifndef SRM_CNEAR_SCREEN
 #define SRM_CNEAR_SCREEN 0  // the crowded bricks (most lists overflow: they need the hit count)
 #endif
-#ifndef SRM_NEAR_EXP
-#define SRM_NEAR_EXP 0  // 1 / 2 / 3: timing experiments (no id loads / no screen / 5 of 9 rows); results are WRONG
-#endif
 #ifndef SRM_NEAR_ROWUNROLL
 #define SRM_NEAR_ROWUNROLL 9
 #endif

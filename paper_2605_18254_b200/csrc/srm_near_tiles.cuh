@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         };
 #endif
 #pragma unroll kNearRowUnroll
-        for (int row9 = 0; row9 < (SRM_NEAR_EXP == 2 ? 0 : (SRM_NEAR_EXP == 3 ? 5 : 9)); ++row9) {  // (EXP: timing experiments)
+        for (int row9 = 0; row9 < 9; ++row9) {
             const int ddy = row9 % 3 - 1, ddz = row9 / 3 - 1;
             const int c = hc + ddy * kHX + ddz * kHX * kHY;
             const int kb = hoff[c - 1], ke = hoff[c + 2];
@@ -486,22 +486,14 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
 #else
         if (nn <= kNearCap) {
 #endif
-#if SRM_NEAR_EXP == 1  // (timing experiment: no id loads)
-            const int32_t idi = -1;
-#else
             const int32_t idi = S.id[qi];
-#endif
 #pragma unroll
             for (int t = 0; t < kNearCap; ++t) {
                 e[t] = 0;
                 if (t < nn) {
                     const int32_t j = pj[ql[t * kTileThreads]];
-#if SRM_NEAR_EXP == 1
-                    e[t] = j;
-#else
                     if (S.id[j] != idi) e[t] = j;
                     else e[t] = -1;
-#endif
                 }
             }
 #pragma unroll
