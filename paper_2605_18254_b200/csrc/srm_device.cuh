@@ -7,6 +7,24 @@
 
 #include <cstdint>
 
+// Checked build (-DSRM_B200_CHECKED, tools/build_variant.sh): index bounds of the hot
+// kernels, a message and a trap on the first violation.  compute-sanitizer is closed on
+// the GPU pool this was developed on (profiles/r11_sanitizer_refused.log); the GPU parity
+// tests run once under this build instead (profiles/r16_checked_build.log).
+#ifdef SRM_B200_CHECKED
+#include <cstdio>
+#define SRM_CHK(cond, code)                                                                           \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("SRM_CHK %d failed at %s:%d (block %d thread %d)\n", code, __FILE__, __LINE__,     \
+                   static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                      \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define SRM_CHK(cond, code) ((void)0)
+#endif
+
 namespace srmb {
 
 constexpr uint8_t kNotAccepted = 255;

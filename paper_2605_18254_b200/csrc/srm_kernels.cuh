@@ -50,6 +50,7 @@ struct GridParams {
     int32_t dims[3];
     double edge[3];
     double inv_edge[3];  // 1 / edge (cell_of's quotient estimate)
+    int64_t n_state;     // particles of the state the grid indexes (checked builds: index bounds)
     int64_t ncells;
     int32_t near_s[3];  // near-search half width per axis; -1 = every cell on the axis
     double extra;       // near cutoff: (ri + rj + extra) * (1 + 1e-9) + 1e-300
@@ -150,6 +151,7 @@ __host__ __device__ inline int grid_params(double cell_size, double max_r_state,
     }
     g.extra = extra;
     g.rmax = max_r_state;
+    g.n_state = n;
     const double cut = ((max_r_state + max_r_state + extra) * (1.0 + 1e-9) + 1e-300) * (1.0 + 1e-9);
     for (int a = 0; a < dim; ++a) {
         int64_t s = 1;
@@ -322,6 +324,7 @@ __global__ void k_keys(int64_t n, State T, const GridParams* __restrict__ gp,
         double p[D];
         rec_pos<D>(T.rec[i], p);
         const uint32_t k = cell_of<D>(g, p);
+        SRM_CHK(static_cast<int64_t>(k) < g.ncells, 401);
         key[i] = k;
         atomicAdd(&count[k], 1u);
     }
@@ -446,6 +449,7 @@ __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const int
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = key[i];
         const uint32_t r = atomicSub(&count[k], 1u) - 1u;
+        SRM_CHK(cell_start[k] + static_cast<int64_t>(r) >= 0 && cell_start[k] + static_cast<int64_t>(r) < n, 403);
         perm[cell_start[k] + r] = (static_cast<unsigned long long>(static_cast<uint32_t>(slot[i])) << 32) |
                                   static_cast<uint32_t>(i);
     }
@@ -499,6 +503,7 @@ __global__ void k_gather(int64_t n, const unsigned long long* __restrict__ perm,
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
          q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t src = static_cast<int32_t>(perm[q] & 0xffffffffull);
+        SRM_CHK(src >= 0 && src < n, 402);
         const double4 v = T.rec[src];
         S.rec[q] = v;
         double rb = v.w;
@@ -888,6 +893,9 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     const int32_t* row = nbr + q * kNearRow;
     const int4 h0 = *reinterpret_cast<const int4*>(row);  // (n, e0, e1, e2)
     const int nn = h0.x;
+    SRM_CHK(q >= 0 && q < g.n_state && nn >= 0, 201);
+    SRM_CHK(nn > kNearCap || ((nn < 1 || (h0.y >= 0 && h0.y < g.n_state)) && (nn < 2 || (h0.z >= 0 && h0.z < g.n_state)) &&
+                              (nn < 3 || (h0.w >= 0 && h0.w < g.n_state))), 202);
     double4 v[SRM_PREFETCH];
     if (nn <= kNearCap) {
         if (nn > 0) v[0] = ld_rec<kLive>(S.rec + h0.y);
@@ -904,6 +912,7 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
             }
         }
         for (int t = SRM_PREFETCH; t < nn; ++t) {  // the rest of the row (rare at the bench window)
+            SRM_CHK(row[1 + t] >= 0 && row[1 + t] < g.n_state, 203);
             const double4 w = ld_rec<kLive>(S.rec + row[1 + t]);
             const double xl[3] = {w.x, w.y, w.z};
             if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;
@@ -913,6 +922,7 @@ __device__ __forceinline__ bool trial_clear(int64_t q, int32_t sl, int l, const 
     if (h0.y >= 0) {  // the list is in the overflow pool
         const int32_t* e = pool + h0.y;
         for (int t = 0; t < nn; ++t) {
+            SRM_CHK(e[t] >= 0 && e[t] < g.n_state, 204);
             const double4 w = ld_rec<kLive>(S.rec + e[t]);
             const double xl[3] = {w.x, w.y, w.z};
             if (sphere_overlap<D>(box, p, ri, xl, w.w)) return false;

@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                     if (r + step < kHRows && hoff[(r + step) * kHX] <= k) r += step;
                 const RowMap& m = rmap[r];
                 src[u] = static_cast<int32_t>(k + (k < m.ka ? m.sa : (k < m.kc ? m.sb : m.sc)));
+                SRM_CHK(src[u] >= 0 && src[u] < g.n_state, 101);
                 sxf[u] = k < m.ka ? -g.L_f[0] : (k < m.kc ? 0.f : g.L_f[0]);
                 syf[u] = m.sy;
                 szf[u] = m.sz;
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         for (int step = 8; step > 0; step >>= 1)
             if (hx + step <= wx && hoff[rb + hx + step] <= i) hx += step;
         const int hc = rb + hx;
+        SRM_CHK(i >= 0 && i < total && hc > kHX * kHY && hc < kHCells - kHX * kHY, 102);
         const float mx = reinterpret_cast<const float*>(pxy + (i >> 1))[i & 1];
         const float my = reinterpret_cast<const float*>(pxy + (i >> 1))[2 + (i & 1)];
         const float mz = reinterpret_cast<const float*>(pzw + (i >> 1))[i & 1];
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
             const int ddy = row9 % 3 - 1, ddz = row9 / 3 - 1;
             const int c = hc + ddy * kHX + ddz * kHX * kHY;
             const int kb = hoff[c - 1], ke = hoff[c + 2];
+            SRM_CHK(c >= 1 && c + 2 <= kHCells && kb >= 0 && kb <= ke && ke <= total, 103);
 #if NT_SCREEN == 0
             // slots [kb, ke) two at a time (pairs 2p, 2p + 1; the ends masked)
             for (int p = kb >> 1; 2 * p < ke; ++p) {
@@ -444,6 +447,7 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                 if (t < nn) {
                     const int tk = ql[t * kTileThreads];
                     const int k = tk & 0xfff, r9 = tk >> 12;
+                    SRM_CHK(k < total && r9 < 9, 106);
                     const int c = hc + (r9 % 3 - 1) * kHX + (r9 / 3 - 1) * kHX * kHY;
                     const int hcj = c - 1 + (k >= hoff[c] ? 1 : 0) + (k >= hoff[c + 1] ? 1 : 0);
                     const int32_t j = pj[k];
@@ -491,7 +495,9 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
             for (int t = 0; t < kNearCap; ++t) {
                 e[t] = 0;
                 if (t < nn) {
+                    SRM_CHK(ql[t * kTileThreads] < total, 104);
                     const int32_t j = pj[ql[t * kTileThreads]];
+                    SRM_CHK(j >= 0 && j < g.n_state, 105);
                     if (S.id[j] != idi) e[t] = j;
                     else e[t] = -1;
                 }

@@ -177,6 +177,7 @@ __device__ __forceinline__ int resolve_try(int32_t q, int pass, const State& S, 
                                            const uint32_t* __restrict__ skey, const int32_t* __restrict__ nbr,
                                            const int32_t* __restrict__ pool, uint8_t* __restrict__ acc,
                                            int32_t* __restrict__ active, StatsDev* stats) {
+    SRM_CHK(q >= 0 && q < g.n_state, 301);
     const int4* row = reinterpret_cast<const int4*>(nbr + static_cast<int64_t>(q) * kNearRow);
     const int4 h0 = row[0];
     if (h0.x & kRowPool) {  // a longer list in the pool; bit 31 of an entry: it precedes q
@@ -198,6 +199,7 @@ __device__ __forceinline__ int resolve_try(int32_t q, int pass, const State& S, 
                 fl[u] = 0;
                 if (t0 + u < nn) {
                     const int32_t j = e[u] & 0x7fffffff;
+                    SRM_CHK(j < g.n_state, 302);
                     if (e[u] < 0) fl[u] = __ldcg(dflag + j);
                     v[u] = e[u] < 0 ? ldcg_rec(rec_new + j) : S.rec[j];
                 }
@@ -223,6 +225,9 @@ __device__ __forceinline__ int resolve_try(int32_t q, int pass, const State& S, 
     const int nn = h0.x & 0xff;
     const unsigned mask = (static_cast<unsigned>(h0.x) >> 8) & 0x7fu;
     const int32_t e[kNearCap] = {h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+    for (int t = 0; t < kNearCap; ++t) SRM_CHK(t >= nn || (e[t] >= 0 && e[t] < g.n_state), 303);
+    SRM_CHK(nn <= kNearCap, 304);
     auto live = [&](int t, int32_t j) {  // final record of a preceding neighbour, round-start record of a following one
         return ((mask >> t) & 1u) ? ldcg_rec(rec_new + j) : S.rec[j];
     };
@@ -372,6 +377,7 @@ __global__ void __launch_bounds__(kResolveThreads, SRM_RESOLVE_MINB) k_resolve_p
             }
             __syncthreads();
             if (s_flush) {
+                SRM_CHK(kept + static_cast<int>(threadIdx.x) < span, 305);
                 mine[kept + threadIdx.x] = s_keep[s_nkeep + threadIdx.x];
                 kept += kResolveThreads;
             }
@@ -384,6 +390,7 @@ __global__ void __launch_bounds__(kResolveThreads, SRM_RESOLVE_MINB) k_resolve_p
         }
         // what is left in the buffers
         const int nk = s_nkeep, nr = s_nretry;
+        SRM_CHK(kept + nk <= span && nk <= 2 * kResolveThreads && nr <= 2 * kResolveThreads, 306);
         if (static_cast<int>(threadIdx.x) < nk) mine[kept + threadIdx.x] = s_keep[threadIdx.x];
         if (threadIdx.x == 0) {
             cnt_out[blockIdx.x] = kept + nk;
