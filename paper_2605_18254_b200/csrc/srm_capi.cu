@@ -118,6 +118,9 @@ struct srm_b200_ctx {
     int32_t* list_a = nullptr;   // resolve: pending lists (ping-pong)
     int32_t* list_b = nullptr;
     int32_t* seg_cnt = nullptr;  // resolve: entries per CTA segment of the pending lists (ping-pong)
+    int2* rev = nullptr;         // half-stencil bricks: reverse entries (j, i) of a round
+    int64_t rev_cap = 0;
+    int32_t* ovf = nullptr;      // ... rows to rebuild from the full stencil
     static constexpr int resolve_ctas = kResolveMaxCtas;
     // opt-in (SRM_B200_WAVE=1 or SRM_B200_SWEEP=wave): measured no faster than the class
     // launches at cfg 4, so the class launches stay the default
@@ -327,6 +330,11 @@ struct srm_b200_ctx {
             queue_ctas = std::max(1, per_sm) * std::max(1, sms);
         }
         S.xf = dalloc<float4>(cap);
+        if (dim == 3) {  // (expected: 0.35 reverse entries per particle at cfg 4's window, 0.9 at cfg 2's)
+            rev_cap = 2 * cap + 1024;
+            rev = dalloc<int2>(rev_cap);
+            ovf = dalloc<int32_t>(cap + 1024);
+        }
         if (!platelets() && dim == 3) {
             rec2 = dalloc<double4>(cap);
             dflag = dalloc<uint8_t>(cap);
@@ -359,7 +367,7 @@ struct srm_b200_ctx {
         cudaFree(gp); cudaFree(rp); cudaFree(active); cudaFree(stats); cudaFree(red_part_sum);
         cudaFree(nbr); cudaFree(pool.e); cudaFree(S.xf); cudaFree(wave_ctl); cudaFree(wave_order); cudaFree(wave_done);
         cudaFree(red_part_max); cudaFree(red_out); cudaFree(rec_stage);
-        cudaFree(rec2); cudaFree(dflag); cudaFree(list_a); cudaFree(list_b); cudaFree(seg_cnt);
+        cudaFree(rec2); cudaFree(dflag); cudaFree(list_a); cudaFree(list_b); cudaFree(seg_cnt); cudaFree(rev); cudaFree(ovf);
         if (h_stats) cudaFreeHost(h_stats);
         if (h_red) cudaFreeHost(h_red);
         for (auto e : ev_pool) cudaEventDestroy(e);
@@ -474,6 +482,23 @@ struct srm_b200_ctx {
         launched();
     }
 
+    // near lists of a sparse 3D grid: the shared-memory bricks (half stencil: each pair once)
+    // and the merge of their reverse entries (every kernel tests the grid: GridParams::near_kind)
+    void sparse_bricks(int ntiles) {
+#if SRM_NEAR_HALF
+        tiles::k_near_tiles<<<ntiles, tiles::kTileThreads, tiles::kTileSmem, stream>>>(S, gp, cell_start, skey, nbr, pool,
+                                                                                       stats, rev, rev_cap, ovf);
+        const int mb = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 148 * 8));
+        k_near_merge<<<mb, 256, 0, stream>>>(gp, rev, rev_cap, nbr, ovf, stats);
+        k_near_rebuild<<<148, 128, 0, stream>>>(S, gp, cell_start, skey, nbr, pool, ovf, stats);
+        launched(3);
+#else
+        tiles::k_near_tiles<<<ntiles, tiles::kTileThreads, tiles::kTileSmem, stream>>>(S, gp, cell_start, skey, nbr, pool,
+                                                                                       stats);
+        launched(1);
+#endif
+    }
+
     // passes 1 .. of the dependency resolution (srm_resolve.cuh); the last one finishes
     // whatever is left
     void resolve_passes_launch(const GridParams& g) {
@@ -514,9 +539,7 @@ struct srm_b200_ctx {
             FamScope fs(this, 2);  // near lists
             const int nb = blocks_for(n, 256);
             if (hg.near_kind == 0) {  // shared-memory bricks
-                tiles::k_near_tiles<<<hg.ntiles, tiles::kTileThreads, tiles::kTileSmem, stream>>>(S, gp, cell_start, skey,
-                                                                                                 nbr, pool, stats);
-                launched(1);
+                sparse_bricks(hg.ntiles);
             } else if (hg.near_kind == 3) {  // crowded: small bricks, large staging
                 ctiles::k_near_tiles<<<hg.ntiles, ctiles::kTileThreads, ctiles::kTileSmem, stream>>>(
                     S, gp, cell_start, skey, nbr, pool, stats);
@@ -776,6 +799,7 @@ struct srm_b200_ctx {
         key.resolve_np = resolve_passes(g0);
         const void* bufs[18] = {P.rec, Q.rec, S.rec, P.aux, Q.aux, S.aux, count, cell_start, perm64, nbr, pool.e, S.xf,
                                 wave_order, wave_done, rec2, dflag, list_a, list_b};
+        (void)rev;  // (allocated with S.xf: the same lifetime)
         (void)seg_cnt;  // (allocated with list_a: the same lifetime)
         std::memcpy(key.bufs, bufs, sizeof bufs);
         if (gexec && key == gkey) {
@@ -810,8 +834,7 @@ struct srm_b200_ctx {
                     });
                     // one round on Q
                     grid_build(Q, nc_max);
-                    tiles::k_near_tiles<<<ntiles_max, tiles::kTileThreads, tiles::kTileSmem, stream>>>(
-                        S, gp, cell_start, skey, nbr, pool, stats);
+                    sparse_bricks(ntiles_max);
                     ctiles::k_near_tiles<<<ctiles_max, ctiles::kTileThreads, ctiles::kTileSmem, stream>>>(
                         S, gp, cell_start, skey, nbr, pool, stats);
                     if (dim == 2) k_near_lists<2><<<nb, 256, 0, stream>>>(n, S, gp, cell_start, skey, nbr, pool, stats);

@@ -275,6 +275,8 @@ struct StatsDev {
     unsigned long long wave_polls;    // k_sweep_wave: polls of unfinished dependency rows (diagnostic)
     unsigned long long pair_tests;    // platelets: ordered pair tests (spherodisk_overlap) of the sweep + reduction
     unsigned long long pend[48];      // dependency resolution: pend[p] = particles still pending after pass p
+    unsigned long long rev_count;     // half-stencil bricks: reverse entries (j, i) of the round
+    unsigned long long ovf_count;     // ... and rows that outgrew their 7 entries (rebuilt from the full stencil)
 };
 
 // Overflow pool of the near lists: a row whose list does not fit (n > kNearCap) keeps
@@ -756,6 +758,15 @@ struct RowMap {
 #ifndef SRM_NEAR_SCREEN
 #define SRM_NEAR_SCREEN 0  // the sparse bricks (2: a record per pair of slots -- fewer instructions, measured slower)
 #endif
+#ifndef SRM_NEAR_HALF
+#define SRM_NEAR_HALF 0  // 1: the sparse bricks screen half the stencil (each pair once) and a merge kernel
+                         // completes the rows -- bit-exact, measured slower (0.91 + 0.11 + 0.02 ms against 0.72 ms
+                         // at cfg 4: the branchy row loop and 3.5e6 row atomics cost more than the 37% fewer
+                         // candidates save; profiles/r15_near_analysis.md)
+#endif
+#if SRM_NEAR_HALF && SRM_NEAR_SCREEN != 0
+#error "the half stencil records hits with the store-per-candidate screen"
+#endif
 #ifndef SRM_CNEAR_SCREEN
 #define SRM_CNEAR_SCREEN 0  // the crowded bricks (most lists overflow: they need the hit count)
 #endif
@@ -773,6 +784,7 @@ constexpr int kNearRowUnroll = SRM_NEAR_ROWUNROLL;
 static_assert(kResolveMaxPasses + 2 <= 48, "StatsDev::pend");
 #define NT_FUSED 0
 #define NT_SCREEN SRM_NEAR_SCREEN
+#define NT_HALF SRM_NEAR_HALF
 namespace tiles {  // sparse grids (~1-2 particles per cell): 16 x 8 x 4 bricks
 #define NT_X SRM_TILE_X
 #define NT_Y SRM_TILE_Y
@@ -790,6 +802,8 @@ namespace tiles {  // sparse grids (~1-2 particles per cell): 16 x 8 x 4 bricks
 #undef NT_MINB
 #undef NT_KIND
 }  // namespace tiles
+#undef NT_HALF
+#define NT_HALF 0
 #undef NT_SCREEN
 #define NT_SCREEN SRM_CNEAR_SCREEN
 namespace ctiles {  // crowded grids: 4 x 4 x 4 bricks, 4096 staged particles
@@ -832,6 +846,37 @@ namespace rtiles {  // the sparse bricks fused with pass 0 of the dependency res
 }  // namespace rtiles
 #undef NT_FUSED
 #undef NT_SCREEN
+#undef NT_HALF
+
+// Half-stencil bricks: the reverse entries (j, i) -- "i, found from i's side, is a near
+// neighbour of j" -- appended to j's row.  Rows in the pool (n > kNearCap) hold their full
+// stencil already; a row that outgrows its entries goes to the overflow list once and is
+// rebuilt from the full stencil by k_near_rebuild.  (The order of a row's entries is free:
+// every entry is tested, the decisions are ANDs.)
+__global__ void __launch_bounds__(256) k_near_merge(const GridParams* __restrict__ gp, const int2* __restrict__ rev,
+                                                    int64_t rev_cap, int32_t* __restrict__ nbr,
+                                                    int32_t* __restrict__ ovf, StatsDev* stats) {
+    if (gp->near_kind != 0 || gp->resolve) return;
+    const int64_t m = min(static_cast<int64_t>(stats->rev_count), rev_cap);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const int2 e = rev[t];
+        int32_t* row = nbr + static_cast<int64_t>(e.x) * kNearRow;
+        if (*reinterpret_cast<volatile int32_t*>(row) > kNearCap) continue;
+        const int pos = atomicAdd(row, 1);
+        if (pos < kNearCap) row[1 + pos] = e.y;
+        else if (pos == kNearCap) ovf[atomicAdd(&stats->ovf_count, 1ull)] = e.x;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_near_rebuild(State S, const GridParams* __restrict__ gp,
+                                                      const cell_t* __restrict__ cs, const uint32_t* __restrict__ skey,
+                                                      int32_t* __restrict__ nbr, NearPool pool,
+                                                      const int32_t* __restrict__ ovf, StatsDev* stats) {
+    if (gp->near_kind != 0 || gp->resolve) return;
+    const int64_t m = static_cast<int64_t>(stats->ovf_count);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+        near_full_particle<3>(ovf[t], S, *gp, cs, skey, nbr, pool, stats);
+}
 
 #ifndef SRM_SWEEP_THREADS
 #define SRM_SWEEP_THREADS 64

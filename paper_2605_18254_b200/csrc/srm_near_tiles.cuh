@@ -43,6 +43,10 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
                                                              const uint32_t* __restrict__ skey,
                                                              int32_t* __restrict__ nbr, NearPool pool,
                                                              StatsDev* stats
+#if NT_HALF
+                                                             , int2* __restrict__ rev, int64_t rev_cap,
+                                                             int32_t* __restrict__ ovf
+#endif
 #if NT_FUSED
                                                              , Box box, const RoundParams* __restrict__ rpp,
                                                              double4* __restrict__ rec_new,
@@ -59,6 +63,17 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
     int32_t* hsrc = hoff + kHCells + 1;                             // [kHCells] first sorted index of a cell
     uint16_t* lst = reinterpret_cast<uint16_t*>(hsrc);              // [kNearCap + 1][kTileThreads] hit slots
                                                                     // (aliases hsrc: used after the staging)
+#if NT_HALF
+    // half stencil: an interior particle screens the cells AFTER its own in
+    // (z, y, x) order, the later slots of its cell, and whatever part of the stencil lies in
+    // the brick's halo; a hit on another interior particle j is j's hit on i as well and goes
+    // to the reverse list (j, i), merged into j's row by k_near_merge
+    constexpr int kRevCap = 320;
+    __shared__ int2 s_rev[kRevCap];
+    __shared__ int s_nrev;
+    __shared__ unsigned long long s_revbase;
+    if (threadIdx.x == 0) s_nrev = 0;
+#endif
     __shared__ int wsum[kTileThreads / 32];
     __shared__ int rowoff[kTY * kTZ + 1];
     __shared__ RowMap rmap[kHRows];
@@ -270,6 +285,150 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
             if (nn < kNearCap) ql[nn * kTileThreads] = static_cast<uint16_t>(k);
             ++nn;
         };
+#endif
+#if NT_HALF
+        {
+            const int hy = 1 + r % wy, hz = 1 + r / wy;
+            // slots [kb, ke) two at a time; hits carry the stencil row beside the slot
+            auto scan = [&](int kb, int ke, int tag) {
+                const int kbt = kb + tag, ket = ke + tag, it = i + tag;
+                int kt = (kb & ~1) + tag;
+                for (int p = kb >> 1; 2 * p < ke; ++p, kt += 2) {
+                    const float4 A = pxy[p], B = pzw[p];
+                    const float2 ex = __fadd2_rn(make_float2(A.x, A.y), nmx);
+                    const float2 ey = __fadd2_rn(make_float2(A.z, A.w), nmy);
+                    const float2 ez = __fadd2_rn(make_float2(B.x, B.y), nmz);
+                    const float2 d2 = __ffma2_rn(ex, ex, __ffma2_rn(ey, ey, __fmul2_rn(ez, ez)));
+                    const float2 lim = __fadd2_rn(make_float2(B.z, B.w), base2);
+                    const float2 l2 = __fmul2_rn(__fmul2_rn(lim, lim), fac2);
+                    ql[at * kTileThreads] = static_cast<uint16_t>(kt);
+                    nn += (d2.x <= l2.x && kt >= kbt && kt != it) ? 1 : 0;
+                    at = min(nn, kNearCap);
+                    ql[at * kTileThreads] = static_cast<uint16_t>(kt + 1);
+                    nn += (d2.y <= l2.y && kt + 1 < ket && kt + 1 != it) ? 1 : 0;
+                    at = min(nn, kNearCap);
+                }
+            };
+#pragma unroll 1
+            for (int row9 = 0; row9 < 9; ++row9) {
+                const int ddy = row9 % 3 - 1, ddz = row9 / 3 - 1;
+                const int c = hc + ddy * kHX + ddz * kHX * kHY;
+                const int tag = row9 << 12;
+                SRM_CHK(c >= 1 && c + 2 <= kHCells, 103);
+                if (row9 > 4) {  // a row after this one: all three cells
+                    scan(hoff[c - 1], hoff[c + 2], tag);
+                } else if (row9 == 4) {  // the particle's row: the later slots of its cell and
+                                         // the next cell; the previous cell when it is halo
+                    scan(i + 1, hoff[c + 2], tag);
+                    if (hx == 1) scan(hoff[c - 1], hoff[c], tag);
+                } else if (hy + ddy < 1 || hy + ddy > wy || hz + ddz < 1) {  // a halo row before this one
+                    scan(hoff[c - 1], hoff[c + 2], tag);
+                } else {  // an interior row before this one: its halo cells only
+                    if (hx == 1) scan(hoff[c - 1], hoff[c], tag);
+                    if (hx == wx) scan(hoff[c + 1], hoff[c + 2], tag);
+                }
+            }
+            const int32_t idi = S.id[qi];
+            // a hit (slot k of stencil row r9) -> sorted index, or -1 for the same id; an
+            // interior particle after this one in scan order learns of the pair from here
+            auto push_rev = [&](int32_t j) {
+                const int at_ = atomicAdd(&s_nrev, 1);
+                if (at_ < kRevCap) {
+                    s_rev[at_] = make_int2(j, qi);
+                } else {  // (buffer full: straight to the global list)
+                    const unsigned long long gpos = atomicAdd(&stats->rev_count, 1ull);
+                    if (static_cast<int64_t>(gpos) < rev_cap) rev[gpos] = make_int2(j, qi);
+                    else ovf[atomicAdd(&stats->ovf_count, 1ull)] = j;  // (list full: j's row is rebuilt)
+                }
+            };
+            auto symmetric = [&](int k, int r9) {
+                const int ddy = r9 % 3 - 1, ddz = r9 / 3 - 1;
+                const int c = hc + ddy * kHX + ddz * kHX * kHY;
+                const int hxj = hx - 1 + (k >= hoff[c] ? 1 : 0) + (k >= hoff[c + 1] ? 1 : 0);
+                const bool after = r9 > 4 || (r9 == 4 && k > i);
+                return after && hxj >= 1 && hxj <= wx && hy + ddy >= 1 && hy + ddy <= wy && hz + ddz >= 1 &&
+                       hz + ddz <= wz;
+            };
+            if (nn <= kNearCap) {
+                int32_t e[kNearCap];
+                int m = 0;
+#pragma unroll
+                for (int t = 0; t < kNearCap; ++t) {
+                    if (t < nn) {
+                        const int tk = ql[t * kTileThreads];
+                        const int k = tk & 0xfff, r9 = tk >> 12;
+                        SRM_CHK(k < total && r9 < 9, 106);
+                        const int32_t j = pj[k];
+                        if (S.id[j] != idi) {
+#pragma unroll
+                            for (int u = 0; u < kNearCap; ++u)
+                                if (u == m) e[u] = j;
+                            ++m;
+                            if (symmetric(k, r9)) push_rev(j);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kNearCap; ++u)
+                    if (u >= m) e[u] = 0;
+                int4* rowp = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
+                rowp[0] = make_int4(m, e[0], e[1], e[2]);
+                rowp[1] = make_int4(e[3], e[4], e[5], e[6]);
+                continue;
+            }
+            // more hits than the row holds already: the full stencil into the overflow pool
+            // (as the full-stencil kernel does: count, reserve, fill -- the same predicate
+            // both times), and the reverse entries of the pairs this particle owns
+            int cnt = 0;
+            int32_t* dst = nullptr;
+            int64_t off = 0;
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+                int m = 0;
+#pragma unroll 1
+                for (int r9 = 0; r9 < 9; ++r9) {
+                    const int c = hc + (r9 % 3 - 1) * kHX + (r9 / 3 - 1) * kHX * kHY;
+                    const int kb = hoff[c - 1], ke = hoff[c + 2];
+                    for (int k = kb; k < ke; ++k) {
+                        const float* a = reinterpret_cast<const float*>(pxy + (k >> 1)) + (k & 1);
+                        const float* b = reinterpret_cast<const float*>(pzw + (k >> 1)) + (k & 1);
+                        const float ex = __fadd_rn(a[0], -mx), ey = __fadd_rn(a[2], -my), ez = __fadd_rn(b[0], -mz);
+                        const float d2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, __fmul_rn(ez, ez)));
+                        const float lim = __fadd_rn(b[2], base);
+                        if (d2 <= __fmul_rn(__fmul_rn(lim, lim), 1.00001f) && k != i) {
+                            const int32_t j = pj[k];
+                            if (S.id[j] != idi) {
+                                if (pass == 1) {
+                                    if (dst && m < cnt) dst[m] = j;
+                                    if (symmetric(k, r9)) push_rev(j);
+                                }
+                                ++m;
+                            }
+                        }
+                    }
+                }
+                if (pass == 0) {
+                    cnt = m;
+                    off = static_cast<int64_t>(atomicAdd(&stats->pool_top, static_cast<unsigned long long>(cnt)));
+                    dst = off + cnt <= pool.cap ? pool.e + off : nullptr;
+                }
+            }
+            int4* rowp = reinterpret_cast<int4*>(nbr + static_cast<int64_t>(qi) * kNearRow);
+            if (!dst) {  // pool full: the sweep rescans the stencil
+                rowp[0] = make_int4(cnt, -1, 0, 0);
+                rowp[1] = make_int4(0, 0, 0, 0);
+            } else if (cnt > kNearCap) {
+                rowp[0] = make_int4(cnt, static_cast<int32_t>(off), 0, 0);
+                rowp[1] = make_int4(0, 0, 0, 0);
+            } else {  // same-id images removed: the list fits the row after all
+                int32_t e2[kNearCap];
+#pragma unroll
+                for (int t = 0; t < kNearCap; ++t) e2[t] = t < cnt ? dst[t] : 0;
+                rowp[0] = make_int4(cnt, e2[0], e2[1], e2[2]);
+                rowp[1] = make_int4(e2[3], e2[4], e2[5], e2[6]);
+            }
+            continue;
+        }
 #endif
 #pragma unroll kNearRowUnroll
         for (int row9 = 0; row9 < 9; ++row9) {
@@ -579,5 +738,17 @@ __global__ void __launch_bounds__(kTileThreads, NT_MINB) k_near_tiles(State S, c
         row[0] = make_int4(m, e[0], e[1], e[2]);
         row[1] = make_int4(e[3], e[4], e[5], e[6]);
     }
+#if NT_HALF
+    // the brick's reverse entries leave with one atomic
+    __syncthreads();
+    const int nrev = min(s_nrev, kRevCap);
+    if (threadIdx.x == 0 && nrev) s_revbase = atomicAdd(&stats->rev_count, static_cast<unsigned long long>(nrev));
+    __syncthreads();
+    for (int t = threadIdx.x; t < nrev; t += blockDim.x) {
+        const int64_t gpos = static_cast<int64_t>(s_revbase) + t;
+        if (gpos < rev_cap) rev[gpos] = s_rev[t];
+        else ovf[atomicAdd(&stats->ovf_count, 1ull)] = s_rev[t].x;
+    }
+#endif
 }
 
