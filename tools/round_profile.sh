@@ -15,5 +15,5 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --profile-from-start off --csv python tools/profile_round.py --rounds 2 > $O/launches_$T.csv 2> $O/launches_$T.err
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-  -k regex:"k_gather|k_near_tiles|k_sweep_warpq" -c 3 -o $O/full_$T python tools/profile_round.py --rounds 1 > $O/full_$T.log 2>&1
+  -k regex:"k_gather|k_near_tiles|k_sweep_warpq|k_keys" -c 4 -o $O/full_$T python tools/profile_round.py --rounds 1 > $O/full_$T.log 2>&1
 for c in cfg1 cfg2 cfg3 cfg5; do timeout 500 python bench.py --config $c --steps 10 > $O/bench_${T}_$c.log 2>&1; done
