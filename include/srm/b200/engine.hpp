@@ -14,6 +14,7 @@
 //   rsa_place           rsa.hpp:21-61       (seeded form; bit-identical to Rng(seed))
 //   rsa_platelets       recipes.cpp:107-148 (seeded form; bit-identical to Rng(seed))
 //   nearest_neighbor_distances  descriptors.hpp:96-115 (exact, on the device)
+//   local_nematic_order         descriptors.hpp:182-209 (platelets; counts exact, values to 1e-12)
 //
 // Differences the caller can observe:
 //   * migrate is the coloured Gauss-Seidel sweep: the reference's
@@ -26,6 +27,7 @@
 #pragma once
 
 #include <algorithm>
+#include <limits>
 #include <cstddef>
 #include <cstdint>
 #include <exception>
@@ -409,6 +411,26 @@ std::vector<double> nearest_neighbor_distances(const Snapshot<S>& snap) {
     dev.upload(snap.particles);
     std::vector<double> out(snap.particles.size());
     detail::check(srm_b200_nnd_histogram(dev.get(), 0, 0.0, 0.0, nullptr, nullptr, nullptr, out.data()), dev.get());
+    return out;
+}
+
+// descriptors.hpp:182-209 on the device: per platelet the mean |n_i . n_j| over the
+// platelets whose centre lies within `cutoff` (NaN when none) and their number.  The
+// counts are the reference's; the values agree to rounding (the sum over neighbours runs
+// in another cell order).
+inline NematicOrder local_nematic_order(const Snapshot<SpherodiskShape>& snap, double cutoff) {
+    if (!(cutoff > 0.0)) throw ValidationError("local_nematic_order: cutoff must be positive");
+    NematicOrder out;
+    const std::size_t n = snap.particles.size();
+    out.value.assign(n, std::numeric_limits<double>::quiet_NaN());
+    out.neighbor_count.assign(n, 0);
+    if (n == 0) return out;
+    detail::Device<SpherodiskShape> dev(snap.box, n);
+    dev.upload(snap.particles);
+    std::vector<int32_t> cnt(n);
+    detail::check(srm_b200_platelet_order(dev.get(), cutoff, out.value.data(), cnt.data(), nullptr, nullptr, nullptr),
+                  dev.get());
+    for (std::size_t i = 0; i < n; ++i) out.neighbor_count[i] = cnt[i];
     return out;
 }
 

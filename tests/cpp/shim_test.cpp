@@ -171,6 +171,30 @@ int main() {
         for (std::size_t i = 0; same && i < ref.size(); ++i) same = mine[i] == ref[i];
         CHECK(same);
     }
+    // local_nematic_order on the device: the reference's neighbour counts, values to rounding
+    {
+        const PeriodicBox3 box = PeriodicBox3::cube(8.0);
+        Rng rng(17);
+        const auto snap = srm::rsa_platelets(600, 1.0, 20.0, box, 100000, rng);
+        const auto ref = srm::local_nematic_order(snap, 1.5);
+        const auto mine = srm::b200::local_nematic_order(snap, 1.5);
+        bool same = ref.value.size() == mine.value.size();
+        for (std::size_t i = 0; same && i < ref.value.size(); ++i) {
+            same = ref.neighbor_count[i] == mine.neighbor_count[i];
+            if (ref.neighbor_count[i] > 0)
+                same = same && std::fabs(ref.value[i] - mine.value[i]) <= 1e-12 * std::fabs(ref.value[i]);
+            else
+                same = same && std::isnan(mine.value[i]);
+        }
+        CHECK(same);
+        bool threw = false;
+        try {
+            srm::b200::local_nematic_order(snap, 0.0);
+        } catch (const ValidationError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     // platelets (SpherodiskShape): rsa_platelets bit-identical to the reference's for
     // Rng(seed); srm_generate to a target fraction, no overlap by the reference's own test
     {
