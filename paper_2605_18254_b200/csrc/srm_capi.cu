@@ -330,12 +330,14 @@ struct srm_b200_ctx {
             queue_ctas = std::max(1, per_sm) * std::max(1, sms);
         }
         S.xf = dalloc<float4>(cap);
+#if SRM_NEAR_HALF
         if (dim == 3) {  // (expected: 0.35 reverse entries per particle at cfg 4's window, 0.9 at cfg 2's)
             rev_cap = 2 * cap + 1024;
             rev = dalloc<int2>(rev_cap);
             ovf = dalloc<int32_t>(cap + 1024);
         }
-        if (!platelets() && dim == 3) {
+#endif
+        if (!platelets() && dim == 3 && (wave_mode & 2)) {  // (the opt-in dependency resolution's buffers)
             rec2 = dalloc<double4>(cap);
             dflag = dalloc<uint8_t>(cap);
             // (a CTA's segment is its index range rounded up to whole chunks)
