@@ -50,9 +50,15 @@ tests/cpp/shim_test: tests/cpp/shim_test.cpp include/srm/b200/engine.hpp include
 	    -L$(PKG) -lsrm_b200 -Loracle/_ref -lsrm_ref \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle/_ref'
 
+# memory-system ceiling of the migrate step's access patterns
+microbench: tools/random_access_bench
+
+tools/random_access_bench: tools/random_access_bench.cu
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -o $@ $<
+
 clean:
 	rm -f $(CSRC)/*.o $(LIB) $(CSRC)/ptxas.log tests/cpp/shim_test
 	$(MAKE) -f oracle/Makefile clean
 
-.PHONY: all lib oracle shimtest clean
+.PHONY: all lib oracle shimtest microbench clean
 
