@@ -18,7 +18,7 @@ CXXFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off
 # snapshot header -- the copy vendored in the image's cudnn_frontend package
 JSON_INC ?= $(firstword $(wildcard /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty))
 
-all: lib oracle
+all: lib oracle microbench
 	@if [ -d "$(REF)/core/include" ]; then $(MAKE) shimtest; else echo "shimtest: $(REF) absent, keeping prebuilt binary (if any)"; fi
 
 lib: $(LIB)
