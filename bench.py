@@ -493,6 +493,46 @@ def run_b200(args, cfg, world, rank, local, pg):
     e2e_ms = max_over_ranks(pg, ctx.stopwatch_stop()) / e2e_steps
     e2e_value = world * n * n_k / (e2e_ms * 1e-3)
 
+    # the same step with two contexts in flight on two host threads (independent states, the
+    # reference's `srmgen --ensemble` pattern, srmgen.cpp:119-143): one context's copies run
+    # under the other's rounds.  Reported beside e2e, not instead of it; wall clock between
+    # device synchronisations (two streams).
+    piped = None
+    if kind != "platelet" and world == 1 and not args.no_pipelined:
+        import threading
+        ctx2 = srm.Context(ctx.box, n, local)
+        bufs2 = tuple(pinned(b.shape, torch.from_numpy(b).dtype) for b in bufs)
+        for dst, src in zip(bufs2, bufs):
+            dst[...] = src
+        ctx2.upload(*bufs2)
+        ctx2.rounds(cs, c_m, n_l, key, 5000, 1, n_k)  # (warm-up: its grid, its lists)
+        ctx2.download(*bufs2)
+
+        def worker(c, b, base):
+            for s in range(e2e_steps):
+                c.upload(*b)
+                c.rounds(cs, c_m, n_l, key, base + s * n_k, 1, n_k)
+                c.download(*b)
+
+        ctx.sync()
+        ctx2.sync()
+        th = [threading.Thread(target=worker, args=(ctx, bufs, 6000)),
+              threading.Thread(target=worker, args=(ctx2, bufs2, 7000))]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        ctx.sync()
+        ctx2.sync()
+        wall = time.perf_counter() - t0
+        ctx2.close()
+        piped = {"value": 2 * n * n_k * e2e_steps / wall, "unit": UNIT, "contexts": 2,
+                 "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io, "rounds_per_step": n_k,
+                 "timing": "wall clock between device synchronisations",
+                 "api": "two contexts on two host threads, each: srm_b200_upload + srm_b200_rounds(n_k) + "
+                        "srm_b200_download (the ensemble pattern)"}
+
     tb, tsrc = step_traffic() if args.config == "cfg4" else (None, None)  # profiled on cfg4 only
     traffic = tb * n if tb else None  # DRAM bytes (read + write) of one step (one round), ncu
 
@@ -534,6 +574,8 @@ def run_b200(args, cfg, world, rank, local, pg):
             line["pair_tests"] = {"per_round": pair_tests, "per_s": pair_tests / t_pl if t_pl > 0 else None,
                                   "what": "ordered spherodisk_overlap tests (sweep trials + overlap reduction) per "
                                           "round / (sweep + reduction device time)"}
+        if piped is not None:
+            line["e2e_pipelined"] = piped
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -567,6 +609,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipelined", action="store_true", help="skip the two-context e2e measurement")
     ap.add_argument("--device-rsa", action="store_true",
                     help="the start from the device RSA (rsa_place / rsa_platelets in rounds: statistically equal, "
                          "not bit-identical, to the reference's)")
